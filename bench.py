@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of one DS-PHD/MIB filter cycle (the north-star hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfgT]
+
+One "step" = one full cycle (predict, sort/assign, cell update, births, moments, resampling) over one
+synthetic measurement grid of BASELINE configuration cfg T (2048x2048 cells, 8M persistent + 800k
+birth particles; SURVEY.md 8(d) "north-star 1-GPU target").  Inputs are resident in HBM before the
+timed region; L2 is flushed (256 MiB write) between timed cycles, outside the per-cycle events.
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the tier's reference arm)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per filter cycle and particles/s at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "particles/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# algorithmic bytes per launch of each stage
+def stage_bytes(stage: str, cfg, n_in: int) -> float:
+    nu, nb, C = cfg.nu, cfg.nu_b, cfg.C
+    table = {
+        "predict": 36.0 * nu,
+        "sort_pass0": 12.0 * nu,
+        "sort_pass1": 16.0 * nu,
+        "sort_pass2": 16.0 * nu,
+        "sort_pass3": 16.0 * nu,
+        "scan_counts": 8.0 * C,
+        "cells": 68.0 * C,
+        "scan_joint": 28.0 * C,
+        "moments": 16.0 * n_in,
+        "moments_fixup": 0.0,
+        "births": 16.0 * nb,
+        "resample": 36.0 * nu,
+    }
+    return table.get(stage, 0.0)
+
+
+def a_alg(cfg) -> float:
+    """Method-level algorithmic bytes per cycle: 64 nu + 32 nu_b + 56 C."""
+    return 64.0 * cfg.nu + 32.0 * cfg.nu_b + 56.0 * cfg.C
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0])); mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+# ------------------------------------------------------------------------------------------ oracle timing
+def oracle_sample_cfg(cfg, rows: int):
+    """A bounded sample of the workload: a band of `rows` grid rows through the sensor, with the
+    particle budgets scaled by the band's share of the grid."""
+    from paper_1605_02406_b200 import inputs as I
+    frac = rows / cfg.height
+    return I.config(cfg.name, height=rows, nu=int(cfg.nu * frac), nu_b=int(cfg.nu_b * frac)), frac
+
+
+def run_oracle_steps(cfg, scene, frame_fn, steps, warmup, state=None):
+    import oracle
+    oracle.build()
+    o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b,
+                                    cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params()))
+    if state is not None:
+        o.set_state(state["x"], state["y"], state["vx"], state["vy"], state["w_bar"], state["m_free"], state["k"])
+    k0 = state["k"] if state is not None else 0
+    for k in range(warmup):
+        o.step(frame_fn(k0 + k), cfg.dt)
+    ts = []
+    for k in range(steps):
+        meas = frame_fn(k0 + warmup + k)
+        t0 = time.perf_counter()
+        o.step(meas, cfg.dt)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def bench_reference(args, cfg):
+    """The tier's reference arm: the CPU oracle as it stands, single-threaded, on a band of the
+    workload (each step = one full oracle cycle on that band)."""
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_1605_02406_b200 import inputs as I
+    band, frac = oracle_sample_cfg(cfg, args.ref_rows)
+    sc = I.scene(cfg)
+    r0 = cfg.height // 2 - args.ref_rows // 2
+
+    def frame(k):
+        return sc.frame(k).numpy()[r0:r0 + args.ref_rows].copy()
+
+    ts = run_oracle_steps(band, sc, frame, args.steps, args.warmup)
+    t = sum(ts) / len(ts)
+    value = band.nu / t
+    sample = (f"{args.ref_rows}-row band of {cfg.name} through the sensor ({band.width}x{band.height} cells, "
+              f"{band.nu} + {band.nu_b} particles), {args.steps} timed oracle cycles after {args.warmup} warm-up")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu, "nu_b": cfg.nu_b,
+                   "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ GPU bench
+def bench_ours(args, cfg):
+    import numpy as np
+    import torch
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1605_02406_b200 import dog
+    from paper_1605_02406_b200 import inputs as I
+
+    # replicas: each rank runs the full workload with its own filter seed (multi-GPU)
+    cfg_r = I.config(cfg.name, seed=cfg.seed + 7919 * rank) if world > 1 else cfg
+    sc = I.scene(cfg_r)
+    settle, W, K = args.settle, args.warmup, args.steps
+    nframes = settle + W + K
+    frames = [sc.frame(k, device=dev).contiguous() for k in range(nframes)]
+    f = dog.Filter.from_config(cfg_r)
+    stream = torch.cuda.current_stream()
+    for k in range(settle + W):
+        f.step(frames[k], cfg.dt, stream)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    clocks = ClockSampler(local_rank)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    f.profile_begin(K)
+    for i in range(K):
+        flush.zero_()
+        ev0[i].record(stream)
+        f.step(frames[settle + W + i], cfg.dt, stream)
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    stages, nprof = f.profile_end()
+    clk = clocks.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    step_ms = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(K))
+    ms_mean = float(np.mean(step_ms))
+    ms_all = torch.tensor([ms_mean], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(ms_all, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(ms_all.item())
+
+    # end-to-end through the public host entry point: pinned host meas in, host occupancy out
+    e2e = None
+    if args.e2e_steps > 0:
+        host_frames = [frames[settle + W + (i % K)].cpu().pin_memory() for i in range(min(args.e2e_steps, K))]
+        occ_host = torch.empty(cfg.C, dtype=torch.float32).pin_memory()
+        f.step_host(host_frames[0], cfg.dt, occ_host, stream)   # warm the staging buffer
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for i in range(args.e2e_steps):
+            f.step_host(host_frames[i % len(host_frames)], cfg.dt, occ_host, stream)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = s0.elapsed_time(s1) / args.e2e_steps
+        e2e_t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
+        e2e = {"value": world * cfg.nu / (float(e2e_t.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 4 * cfg.C,
+               "ms_per_step": float(e2e_t.item()), "steps": args.e2e_steps,
+               "entry": "dog_step_host (pinned host meas -> device, cycle, occupancy -> pinned host)"}
+
+    # per-stage times and roofline of the dominant kernel
+    st_avg = {k: v / max(nprof, 1) for k, v in stages.items()}
+    kern = {k: v for k, v in st_avg.items() if k != "memset"}
+    dom = max(kern, key=kern.get)
+    hbm, peak_src = peaks()
+    sc_dev = dog_scalars(f)
+    bytes_dom = stage_bytes(dom, cfg, sc_dev["n_in"])
+    achieved = bytes_dom / (kern[dom] * 1e-3) / 1e9
+    traffic = ncu_traffic(dom)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": bytes_dom, "avg_launch_ms": kern[dom]}
+    step_roof = {"A_alg_bytes": a_alg(cfg), "achieved": a_alg(cfg) / (ms_mean * 1e-3) / 1e9,
+                 "frac": a_alg(cfg) / (ms_mean * 1e-3) / 1e9 / hbm, "unit": "GB/s",
+                 "formula": "64 nu + 32 nu_b + 56 C (SURVEY.md 8(d))"}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and args.cpu_baseline_steps > 0:
+        st = f.get_state()
+        ts = run_oracle_steps(cfg, sc, lambda k: sc.frame(k).numpy(), args.cpu_baseline_steps, 0, state=st)
+        t = sum(ts) / len(ts)
+        cpu = {"value": cfg.nu / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{len(ts)} full {cfg.name} cycles ({cfg.width}x{cfg.height}, {cfg.nu} + {cfg.nu_b}) from "
+                         f"the GPU's warmed state, single-threaded C oracle", "ms_per_step": t * 1e3}
+    value = world * cfg.nu / (ms_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded ray-cast urban scene, inputs.py)",
+        "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} grid, {cfg.nu} persistent + {cfg.nu_b} birth "
+                               f"particles, urban ray-cast scene", "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu,
+                   "nu_b": cfg.nu_b, "dt_s": cfg.dt, "settle_cycles": settle,
+                   "l2": "flushed between timed cycles (256 MiB write outside the cycle events)",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "p10_p90_ms": [step_ms[int(0.1 * (K - 1))], step_ms[int(0.9 * (K - 1))]]},
+        "roofline": roof, "step_roofline": step_roof,
+        "stages_ms": {k: round(v, 5) for k, v in st_avg.items()},
+        "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": f.launches_per_step() * K, "clocks": clk,
+        "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
+        "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def dog_scalars(f):
+    import numpy as np
+    from paper_1605_02406_b200 import dog
+    a = np.zeros(8, np.uint64)
+    rc = dog.dog_get_debug(f.handle, dog.DEBUG_IDS["SCALARS"], a.ctypes.data, a.nbytes)
+    if rc < 0:
+        return {"n_in": 0, "W": 0}
+    return {"n_in": int(a[7]), "W": int(a[0])}
+
+
+def ncu_traffic(kernel_stage: str):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel_stage)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfgT")
+    ap.add_argument("--settle", type=int, default=30, help="untimed cycles from the empty state before warm-up")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-baseline-steps", type=int, default=2)
+    ap.add_argument("--ref-rows", type=int, default=256)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    from paper_1605_02406_b200 import inputs as I
+    cfg = I.CONFIGS[args.config]
+    if args.impl == "reference":
+        bench_reference(args, cfg)
+    else:
+        bench_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

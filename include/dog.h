@@ -1,0 +1,153 @@
+/*
+ * dog.h -- C ABI of the B200-native DS-PHD/MIB dynamic occupancy grid filter (libdog.so).
+ *
+ * One call of dog_step runs one full filter cycle k -> k+1 of the particle-based DS-PHD/MIB filter
+ * of Nuss et al., arXiv 1605.02406 (section VI; parallel pipeline section VII,
+ * P:1249-1520) on the GPU, with a measurement grid of occupied/free masses only (spatial likelihood
+ * g = 1, association probability p_A = 0, Abar birth set only; A-27):
+ *   1 predict      CV model x' = F(T) x + xi (Eq. 14), w = p_S w (Eq. 39)
+ *   2 assign       stable sort of particles by cell key, per-cell offsets (Alg. 2)
+ *   3 cells        m_p = min(sum w, occ_max) (Eqs. 17/61), m_Fp = min(alpha m_F, 1 - m_p) (Eq. 62),
+ *                  (m_O, m_F) = Dempster(m_p, meas) (Eq. 63), birth split rho_b/rho_p (Eqs. 67-68)
+ *   4 persistent   w = rho_p / m_p * w_pred (Eq. 71 with p_A = 0, Eq. 73)
+ *   5 births       nu_b new particles in proportion to rho_b (Alg. 5)
+ *   6 moments      per-cell velocity mean / covariance of persistent particles (Eqs. 81-84)
+ *   7 resample     systematic resampling to nu particles of equal weight (Alg. 7, Eq. 57)
+ *
+ * Conventions:
+ *   - grid: width x height cells, x = column (fastest), y = row; cell key c = row*width + col.
+ *     Particle positions are in CELL UNITS relative to the grid origin (x_cell = x_m / cell_size);
+ *     velocities in m/s.  Integral coordinates belong to the upper cell (A-4).
+ *   - all floating-point state and outputs are IEEE binary32 (f32).
+ *   - random draws: Philox4x32-10 keyed by the 64-bit seed, counter (index, k, stage, k>>32) (A-20),
+ *     so the CPU oracle reproduces every draw bit for bit.
+ *
+ * Status codes: every function returns int, DOG_OK (0) on success, < 0 on error.  No C++ types or
+ * exceptions cross this boundary.  A context is not thread-safe; distinct contexts are independent.
+ */
+#ifndef DOG_H
+#define DOG_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DOG_OK        0
+#define DOG_E_INVAL  (-1) /* invalid argument: sizes <= 0, C >= 2^31-1, probabilities out of range,
+                             non-positive dt, NaN parameters, null pointers                        */
+#define DOG_E_NOMEM  (-2) /* device or pinned-host allocation failed                             */
+#define DOG_E_CUDA   (-3) /* a CUDA call failed; the context is poisoned (only dog_destroy)     */
+#define DOG_E_NCCL   (-4) /* an NCCL call failed; the context is poisoned                        */
+#define DOG_E_MEAS   (-5) /* a measurement cell was invalid (m_zO < 0, m_zF < 0, m_zO + m_zF >
+                             1 + 2^-20, or NaN); such cells were treated as vacuous (0, 0).  Sticky
+                             device flag, reported by the next synchronous call (dog_read_cells,
+                             dog_get_state, dog_get_debug, dog_sync) and then cleared.           */
+#define DOG_E_STATE  (-6) /* call-order misuse (e.g. sharded call on an unsharded context)      */
+
+typedef struct dog_ctx dog_ctx;   /* opaque; created and owned by the library */
+
+typedef struct {
+    int32_t width, height;        /* cells; C = width*height, 1 <= C < 2^31 - 1                */
+    float   cell_size;            /* metres per cell, > 0 (Table I: 0.1 m)             */
+} dog_grid;
+
+typedef struct {
+    float p_s;             /* persistence probability in (0,1]         (Eq. 39; Table I 0.99)   */
+    float p_b;             /* birth probability in [0,1)               (Eq. 67; 0.005..0.1)     */
+    float sigma_pos;       /* m per (T/s); applied SD sigma_pos*T     (Table I 0.02; A-1)      */
+    float sigma_vel;       /* (m/s) per (T/s); applied SD sigma_vel*T (Table I 0.8; A-1)       */
+    float sigma_birth_vel; /* m/s, SD of new-born velocity            (Table I 4 m/s)          */
+    float free_tau;        /* s, > 0: alpha(T) = exp(-T/free_tau); +INF gives alpha = 1 (A-9)  */
+    float occ_max;         /* cap on predicted occupied mass, (0,1]; default 1 (Eq. 17; A-7)  */
+    float v_max;           /* clamp of new-born |vx|,|vy| in m/s; <= 0 disables (A-16)         */
+} dog_params;
+
+/* dog_create -- allocate a filter on the current CUDA device in the empty initial state (A-19):
+ * all nu particles at the sentinel position (-2^30 cells) with weight 0, m_F = 0, k = 0.
+ *   grid, params : validated copies are kept (DOG_E_INVAL on violation).
+ *   n_particles  : nu >= 1, persistent particles per cycle (< 2^31).
+ *   n_birth      : nu_b >= 0, new-born particles per cycle ("remains constant").
+ *   seed         : Philox key (low 32 bits, high 32 bits).
+ *   flags        : DOG_FLAG_DEBUG keeps per-stage device arrays for dog_get_debug (parity tests);
+ *                  0 for production (no extra traffic).
+ *   out          : receives the context; the context owns every device allocation it makes. */
+#define DOG_FLAG_DEBUG 1u
+int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+               uint64_t seed, uint32_t flags, dog_ctx** out);
+
+/* dog_step -- run one filter cycle.
+ *   meas   : DEVICE pointer (same device as the context), float[height][width][2] =
+ *            (m_zO, m_zF) per cell, row-major.  Read stream-ordered on `stream`; it must stay valid
+ *            until the stream passes this step.  The library does not retain it.
+ *   dt     : T in seconds, > 0 (A-29: all T-dependent scalars are recomputed per step).
+ *   stream : cudaStream_t (0 = legacy default stream).  Asynchronous: returns after enqueueing. */
+int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream);
+
+/* dog_step_host -- the same cycle fed from HOST memory: copies meas (host, float[C][2]) to the
+ * device, runs dog_step, and, if occ_host != NULL, copies the occupancy readout (float[C]) back;
+ * synchronous on `stream`.  This is the end-to-end entry point (host buffers in, host result out). */
+int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream);
+
+/* dog_read_cells -- copy the readouts of the last completed cycle (posterior, before resampling,
+ * P:1444) into caller DEVICE buffers (any may be NULL):
+ *   occ[C] = m_O, free_mass[C] = m_F (Eq. 63); vel_mean[C][2] = (mean_vx, mean_vy) (Eq. 81);
+ *   vel_cov[C][3] = (var_x, var_y, cov_xy) (Eqs. 83-84).  Cells without persistent particles or with
+ *   rho_p <= 0 report mean = cov = 0.  Synchronises `stream`; returns DOG_E_MEAS if the sticky
+ *   measurement flag was raised since the last report. */
+int dog_read_cells(dog_ctx* ctx, float* occ, float* free_mass, float* vel_mean, float* vel_cov,
+                   void* stream);
+
+/* dog_sync -- synchronise the context's work on `stream` and report deferred errors. */
+int dog_sync(dog_ctx* ctx, void* stream);
+
+int dog_destroy(dog_ctx* ctx);
+const char* dog_error_string(int status);
+
+/* ---- state I/O (checkpoint/resume and parity injection; synchronous, HOST buffers) ----
+ * The canonical state S_k is: nu particles (x, y in cell units; vx, vy in m/s) in canonical order,
+ * ONE weight w_bar shared by all particles (Eq. 57 makes resampled weights equal), m_free[C], k.
+ * Because draws are counter-based, set_state(get_state()) resumes bit-exactly. */
+int dog_get_state(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float* w_bar,
+                  float* m_free, int64_t* k);
+int dog_set_state(dog_ctx* ctx, const float* x, const float* y, const float* vx, const float* vy,
+                  float w_bar, const float* m_free, int64_t k);
+
+/* ---- per-stage debug dumps of the last cycle (requires DOG_FLAG_DEBUG; synchronous) ----
+ * `what` selects the array; host_dst receives `bytes` (must be >= the array size).  Returns the
+ * number of bytes written (>= 0) or an error. */
+enum {
+    DOG_DBG_PRED_X = 1, DOG_DBG_PRED_Y, DOG_DBG_PRED_VX, DOG_DBG_PRED_VY, /* f32 [nu], input order */
+    DOG_DBG_KEY,        /* u32 [nu] cell key, C = outside the grid                      */
+    DOG_DBG_PERM,       /* u32 [nu] input index of each cell-sorted slot                */
+    DOG_DBG_OFFSETS,    /* u32 [C+1] first sorted slot of each cell                      */
+    DOG_DBG_RHO_P,      /* f32 [C]                                                       */
+    DOG_DBG_RHO_B,      /* f32 [C]                                                       */
+    DOG_DBG_RP,         /* u64 [C] fixed-point persistent mass floor(rho_p 2^40) (A-23)  */
+    DOG_DBG_RB,         /* u64 [C] fixed-point born mass, 0 unless m_zO > 0 (A-13)       */
+    DOG_DBG_NB,         /* u32 [C] birth slots per cell (A-15)                           */
+    DOG_DBG_BIRTH_X, DOG_DBG_BIRTH_Y, DOG_DBG_BIRTH_VX, DOG_DBG_BIRTH_VY, /* f32 [nu_b]     */
+    DOG_DBG_JOINT_IDX,  /* u32 [nu] joint index selected by each resampled particle      */
+    DOG_DBG_SCALARS     /* u64 [8]: W, U, A, meas_bad_count, w_pred bits, w_bar bits, k, n_in */
+};
+int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes);
+
+/* ---- stage profiling (bench evidence) ----
+ * dog_profile_begin enables per-stage CUDA events (recorded on the step's stream, no host sync) for up
+ * to max_steps subsequent dog_step calls; dog_profile_end synchronises and returns, per stage, the
+ * summed device time in ms (stage_ms[DOG_MAX_STAGES]) and the number of profiled steps.
+ * dog_profile_stage_name(i) names stage i ("predict", "sort0", ... "resample"). */
+#define DOG_MAX_STAGES 16
+int dog_profile_begin(dog_ctx* ctx, int max_steps);
+int dog_profile_end(dog_ctx* ctx, float* stage_ms, int* n_stages, int* n_steps);
+const char* dog_profile_stage_name(dog_ctx* ctx, int i);
+
+/* ---- library introspection ---- */
+int dog_version(void);                 /* ABI version, currently 1 */
+int dog_launches_per_step(dog_ctx* ctx); /* kernels one dog_step launches (bench evidence) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOG_H */

@@ -1,0 +1,584 @@
+// dog.cu -- host orchestration and C ABI (include/dog.h) of the B200-native DS-PHD/MIB filter.
+//
+// One context = one filter on one device.  All state lives in HBM; a cycle is a fixed sequence of
+// stream-ordered kernel launches (dog_kernels.cuh) with no host synchronisation: every scalar the
+// next stage needs (w_bar, w_pred, W, A, U, n_in) is device-resident (DevScalars).
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/dog.h"
+#include "dog_kernels.cuh"
+
+using namespace dog;
+
+namespace {
+
+inline size_t round_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+inline uint32_t cdiv(uint64_t a, uint64_t b) { return (uint32_t)((a + b - 1) / b); }
+
+}  // namespace
+
+struct dog_ctx {
+    int device = 0;
+    dog_grid grid{};
+    dog_params params{};
+    uint64_t seed = 0;
+    uint32_t flags = 0;
+    int64_t nu = 0, nu_b = 0;
+    uint32_t C = 0;
+    int npass = 0;
+    int64_t k = 0;
+    bool poisoned = false;
+    size_t nu_cap = 0;          // particle arrays padded to the sort tile
+    uint32_t sort_tiles = 0, cell_tiles = 0, joint_tiles = 0, mom_ranges = 0;
+
+    // state S_k and predicted state (SoA, f32)
+    float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
+    float *px = nullptr, *py = nullptr, *pvx = nullptr, *pvy = nullptr;
+    // sort
+    uint32_t *keyA = nullptr, *keyB = nullptr, *valA = nullptr, *valB = nullptr, *key_dbg = nullptr;
+    uint32_t *skeys = nullptr, *perm = nullptr;   // results (alias keyX/valX)
+    // cells
+    uint32_t* offsets = nullptr;
+    float *m_free = nullptr, *occ = nullptr, *fre = nullptr, *rho_p = nullptr, *rho_b = nullptr;
+    float2* mean = nullptr;
+    float* cov = nullptr;
+    uint64_t *Rp = nullptr, *Rb = nullptr, *P = nullptr;
+    uint32_t* sb = nullptr;
+    uint64_t *aggA = nullptr, *incA = nullptr, *aggJ = nullptr, *incJ = nullptr;
+    // births, resampling
+    float *bx = nullptr, *by = nullptr, *bvx = nullptr, *bvy = nullptr;
+    uint32_t* jidx = nullptr;
+    // moments partials
+    MomPartial *head = nullptr, *tail = nullptr;
+    uint32_t* tail_cell = nullptr;
+    uint8_t* head_ends = nullptr;
+    DevScalars* sc = nullptr;
+    // zeroed once per cycle (one memset): counts, radix histograms, tile counters, look-back status
+    uint8_t* zero = nullptr;
+    size_t zero_bytes = 0;
+    uint32_t *counts = nullptr, *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr,
+             *st_counts = nullptr, *flagA = nullptr, *flagJ = nullptr;
+    // end-to-end staging
+    float* meas_dev = nullptr;
+    // profiling: events[step][stage boundary]
+    std::vector<cudaEvent_t> pev;
+    int prof_max = 0, prof_steps = 0, prof_nst = 0;
+    const char* stage_names[DOG_MAX_STAGES] = {};
+
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+int fail(dog_ctx* c, cudaError_t e, const char* what)
+{
+    if (c) c->poisoned = true;
+    fprintf(stderr, "libdog: %s failed: %s\n", what, cudaGetErrorString(e));
+    return DOG_E_CUDA;
+}
+
+#define CK(call)                                              \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return fail(ctx, _e, #call);   \
+    } while (0)
+
+template <typename T>
+int dalloc(dog_ctx* ctx, T** p, size_t n)
+{
+    void* q = nullptr;
+    if (cudaMalloc(&q, n * sizeof(T) > 0 ? n * sizeof(T) : 16) != cudaSuccess) {
+        cudaGetLastError();
+        return DOG_E_NOMEM;
+    }
+    ctx->allocs.push_back(q);
+    *p = (T*)q;
+    return DOG_OK;
+}
+
+void free_all(dog_ctx* ctx)
+{
+    for (void* p : ctx->allocs) cudaFree(p);
+    ctx->allocs.clear();
+}
+
+bool finite(float v) { return std::isfinite(v); }
+
+StepArgs step_args(const dog_ctx* ctx, float dt)
+{
+    // fp64 once, rounded to f32; same expression order as the oracle
+    const double T = (double)dt;
+    StepArgs a;
+    a.Tc = (float)(T / (double)ctx->grid.cell_size);
+    a.s_p = (float)(((double)ctx->params.sigma_pos * T) / (double)ctx->grid.cell_size);
+    a.s_v = (float)((double)ctx->params.sigma_vel * T);
+    a.alpha = (float)std::exp(-(T / (double)ctx->params.free_tau));
+    a.k = ctx->k;
+    return a;
+}
+
+FilterConst filter_const(const dog_ctx* ctx)
+{
+    FilterConst f;
+    f.W = ctx->grid.width;
+    f.H = ctx->grid.height;
+    f.C = ctx->C;
+    f.nu = (uint32_t)ctx->nu;
+    f.nu_b = (uint32_t)ctx->nu_b;
+    f.p_s = ctx->params.p_s;
+    f.p_b = ctx->params.p_b;
+    f.sigma_b = ctx->params.sigma_birth_vel;
+    f.occ_max = ctx->params.occ_max;
+    f.v_max = ctx->params.v_max;
+    f.seed = ctx->seed;
+    return f;
+}
+
+int set_device(dog_ctx* ctx)
+{
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != ctx->device) CK(cudaSetDevice(ctx->device));
+    return DOG_OK;
+}
+
+int report_meas(dog_ctx* ctx)
+{
+    uint32_t bad = 0;
+    CK(cudaMemcpy(&bad, &ctx->sc->meas_bad, 4, cudaMemcpyDeviceToHost));
+    if (bad) {
+        CK(cudaMemset(&ctx->sc->meas_bad, 0, 4));
+        return DOG_E_MEAS;
+    }
+    return DOG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dog_version(void) { return 1; }
+
+const char* dog_error_string(int s)
+{
+    switch (s) {
+    case DOG_OK: return "ok";
+    case DOG_E_INVAL: return "invalid argument";
+    case DOG_E_NOMEM: return "out of memory";
+    case DOG_E_CUDA: return "CUDA error (context poisoned)";
+    case DOG_E_NCCL: return "NCCL error (context poisoned)";
+    case DOG_E_MEAS: return "invalid measurement cells were treated as vacuous";
+    case DOG_E_STATE: return "call-order misuse";
+    default: return "unknown status";
+    }
+}
+
+int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+               uint64_t seed, uint32_t flags, dog_ctx** out)
+{
+    if (!grid || !params || !out) return DOG_E_INVAL;
+    *out = nullptr;
+    const dog_params& p = *params;
+    const int64_t C = (int64_t)grid->width * grid->height;
+    if (grid->width <= 0 || grid->height <= 0 || C >= (1ll << 24) || !(grid->cell_size > 0.0f) ||
+        !finite(grid->cell_size))
+        return DOG_E_INVAL;   // C < 2^24 keeps every fixed-point total below 2^64 (A-23)
+    if (n_particles < 1 || n_particles >= (1ll << 30) || n_birth < 0 || n_birth >= (1ll << 30))
+        return DOG_E_INVAL;
+    if (!(p.p_s > 0.0f && p.p_s <= 1.0f) || !(p.p_b >= 0.0f && p.p_b < 1.0f) ||
+        !(p.sigma_pos >= 0.0f) || !finite(p.sigma_pos) || !(p.sigma_vel >= 0.0f) || !finite(p.sigma_vel) ||
+        !(p.sigma_birth_vel >= 0.0f) || !finite(p.sigma_birth_vel) || !(p.free_tau > 0.0f) ||
+        !(p.occ_max > 0.0f && p.occ_max <= 1.0f) || std::isnan(p.v_max))
+        return DOG_E_INVAL;
+
+    dog_ctx* ctx = new (std::nothrow) dog_ctx();
+    if (!ctx) return DOG_E_NOMEM;
+    cudaGetDevice(&ctx->device);
+    ctx->grid = *grid;
+    ctx->params = p;
+    ctx->seed = seed;
+    ctx->flags = flags;
+    ctx->nu = n_particles;
+    ctx->nu_b = n_birth;
+    ctx->C = (uint32_t)C;
+    int bits = 1;
+    while ((1ull << bits) <= (uint64_t)C) ++bits;   // keys 0..C
+    ctx->npass = (bits + 7) / 8;
+    ctx->nu_cap = round_up((size_t)n_particles, kRsTile);
+    ctx->sort_tiles = cdiv(n_particles, kRsTile);
+    ctx->cell_tiles = cdiv(C, kScTile);
+    ctx->joint_tiles = cdiv(C, kJTile);
+    ctx->mom_ranges = cdiv(n_particles, kMomRange);
+    const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
+
+    int rc = DOG_OK;
+#define AL(ptr, n) \
+    if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
+    AL(ctx->x, N); AL(ctx->y, N); AL(ctx->vx, N); AL(ctx->vy, N);
+    AL(ctx->px, N); AL(ctx->py, N); AL(ctx->pvx, N); AL(ctx->pvy, N);
+    AL(ctx->keyA, N); AL(ctx->keyB, N); AL(ctx->valA, N); AL(ctx->valB, N);
+    if (flags & DOG_FLAG_DEBUG) { AL(ctx->key_dbg, N); AL(ctx->rho_b, Cs); AL(ctx->jidx, N); }
+    AL(ctx->offsets, Cs + 1);
+    AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs); AL(ctx->rho_p, Cs);
+    AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
+    AL(ctx->Rp, Cs); AL(ctx->Rb, Cs); AL(ctx->P, Cs + 1); AL(ctx->sb, Cs + 1);
+    AL(ctx->aggA, ctx->joint_tiles); AL(ctx->incA, ctx->joint_tiles);
+    AL(ctx->aggJ, ctx->joint_tiles); AL(ctx->incJ, ctx->joint_tiles);
+    AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
+    AL(ctx->head, ctx->mom_ranges); AL(ctx->tail, ctx->mom_ranges);
+    AL(ctx->tail_cell, ctx->mom_ranges); AL(ctx->head_ends, ctx->mom_ranges);
+    AL(ctx->sc, 1);
+    // zero region layout (u32 words)
+    const size_t w_counts = Cs + 1, w_rhist = kMaxPasses * 256, w_ctrs = 16,
+                 w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256, w_cnt = ctx->cell_tiles,
+                 w_fA = ctx->joint_tiles, w_fJ = ctx->joint_tiles;
+    ctx->zero_bytes = 4 * (w_counts + w_rhist + w_ctrs + w_sort + w_cnt + w_fA + w_fJ);
+    AL(ctx->zero, ctx->zero_bytes);
+#undef AL
+    if (rc != DOG_OK) {
+        free_all(ctx);
+        delete ctx;
+        return rc;
+    }
+    uint32_t* z = (uint32_t*)ctx->zero;
+    ctx->counts = z; z += w_counts;
+    ctx->rhist = z; z += w_rhist;
+    ctx->ctrs = z; z += w_ctrs;
+    ctx->st_sort = z; z += w_sort;
+    ctx->st_counts = z; z += w_cnt;
+    ctx->flagA = z; z += w_fA;
+    ctx->flagJ = z; z += w_fJ;
+
+    // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
+    std::vector<float> sent(N, kSentinelPos);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->x, sent.data(), N * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->y, sent.data(), N * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(ctx->vx, 0, N * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->vy, 0, N * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->m_free, 0, Cs * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->occ, 0, Cs * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->fre, 0, Cs * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->mean, 0, Cs * 8);
+    if (e == cudaSuccess) e = cudaMemset(ctx->cov, 0, Cs * 12);
+    if (e == cudaSuccess) e = cudaMemset(ctx->sc, 0, sizeof(DevScalars));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "libdog: dog_create init failed: %s\n", cudaGetErrorString(e));
+        free_all(ctx);
+        delete ctx;
+        return DOG_E_CUDA;
+    }
+    *out = ctx;
+    return DOG_OK;
+}
+
+int dog_destroy(dog_ctx* ctx)
+{
+    if (!ctx) return DOG_E_INVAL;
+    set_device(ctx);
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : ctx->pev) cudaEventDestroy(e);
+    free_all(ctx);
+    delete ctx;
+    return DOG_OK;
+}
+
+int dog_launches_per_step(dog_ctx* ctx)
+{
+    if (!ctx) return DOG_E_INVAL;
+    return 7 + ctx->npass + (ctx->nu_b > 0 ? 1 : 0);   // kernels (the memset is not a kernel)
+}
+
+int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
+{
+    if (!ctx || !meas) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const StepArgs a = step_args(ctx, dt);
+    const FilterConst fc = filter_const(ctx);
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    const uint32_t nu = (uint32_t)ctx->nu;
+
+    const bool prof = ctx->prof_steps < ctx->prof_max;
+    int mark_i = 0;
+    auto mark = [&](const char* name) -> cudaError_t {
+        if (!prof) return cudaSuccess;
+        if (mark_i > 0) ctx->stage_names[mark_i - 1] = name;
+        return cudaEventRecord(ctx->pev[(size_t)ctx->prof_steps * (DOG_MAX_STAGES + 1) + mark_i++], st);
+    };
+    CK(mark(nullptr));
+    CK(cudaMemsetAsync(ctx->zero, 0, ctx->zero_bytes, st));
+    CK(cudaMemsetAsync(&ctx->sc->A, 0, sizeof(uint64_t), st));
+    CK(mark("memset"));
+
+    // 1. predict (+ counts, radix histograms)
+    const uint32_t n4 = cdiv(nu, 4);
+    k_predict<<<cdiv(n4, kPredThreads), kPredThreads, 0, st>>>(
+        (const float4*)ctx->x, (const float4*)ctx->y, (const float4*)ctx->vx, (const float4*)ctx->vy,
+        (float4*)ctx->px, (float4*)ctx->py, (float4*)ctx->pvx, (float4*)ctx->pvy, (uint4*)ctx->keyA,
+        dbg ? ctx->key_dbg : nullptr, ctx->counts, ctx->rhist, ctx->npass, ctx->sc, fc, a);
+    CK(cudaGetLastError());
+    CK(mark("predict"));
+
+    // 2. stable radix sort of (key, index) + offsets
+    uint32_t *kin = ctx->keyA, *vin = nullptr, *kout = ctx->keyB, *vout = ctx->valB;
+    for (int p = 0; p < ctx->npass; ++p) {
+        uint32_t* stp = ctx->st_sort + (size_t)p * ctx->sort_tiles * 256;
+        if (p == 0)
+            k_onesweep<true><<<ctx->sort_tiles, kRsThreads, 0, st>>>(kin, vin, kout, vout, nu, 8 * p,
+                                                                      ctx->rhist + 256 * p, ctx->ctrs + p, stp);
+        else
+            k_onesweep<false><<<ctx->sort_tiles, kRsThreads, 0, st>>>(kin, vin, kout, vout, nu, 8 * p,
+                                                                       ctx->rhist + 256 * p, ctx->ctrs + p, stp);
+        CK(cudaGetLastError());
+        static const char* sort_names[kMaxPasses] = {"sort_pass0", "sort_pass1", "sort_pass2", "sort_pass3"};
+        CK(mark(sort_names[p]));
+        uint32_t* nk = (kout == ctx->keyB) ? ctx->keyA : ctx->keyB;
+        uint32_t* nv = (vout == ctx->valB) ? ctx->valA : ctx->valB;
+        kin = kout; vin = vout; kout = nk; vout = nv;
+    }
+    ctx->skeys = kin;
+    ctx->perm = vin;
+    k_scan_counts<<<ctx->cell_tiles, kScThreads, 0, st>>>(ctx->counts, ctx->offsets, ctx->C, ctx->ctrs + 8,
+                                                          ctx->st_counts, ctx->sc);
+    CK(cudaGetLastError());
+    CK(mark("scan_counts"));
+
+    // 3. cells: DS predict/update, birth split, fixed point
+    const uint32_t cgrid = std::min<uint32_t>(cdiv(ctx->C, 256), 148u * 16u);
+    k_cells<<<cgrid, 256, 0, st>>>(ctx->offsets, ctx->m_free, (const float2*)meas, ctx->occ, ctx->fre,
+                                   ctx->rho_p, dbg ? ctx->rho_b : nullptr, ctx->Rp, ctx->Rb, ctx->mean,
+                                   ctx->cov, ctx->sc, fc, a.alpha);
+    CK(cudaGetLastError());
+    CK(mark("cells"));
+
+    // 5a. birth slots + joint CDF
+    k_scan_joint<<<ctx->joint_tiles, kJThreads, 0, st>>>(ctx->Rp, ctx->Rb, ctx->sb, ctx->P, ctx->C,
+                                                          ctx->ctrs + 9, ctx->flagA, ctx->aggA, ctx->incA,
+                                                          ctx->flagJ, ctx->aggJ, ctx->incJ, ctx->sc, fc, a.k);
+    CK(cudaGetLastError());
+    CK(mark("scan_joint"));
+
+    // 6. moments
+    k_moments<<<cdiv(ctx->mom_ranges, 8), 256, 0, st>>>(ctx->skeys, ctx->perm, ctx->pvx, ctx->pvy,
+                                                         ctx->offsets, ctx->rho_p, ctx->mean, ctx->cov,
+                                                         ctx->head, ctx->tail, ctx->tail_cell,
+                                                         ctx->head_ends, ctx->sc, ctx->mom_ranges);
+    CK(cudaGetLastError());
+    CK(mark("moments"));
+    k_moments_fixup<<<cdiv(ctx->mom_ranges, 256), 256, 0, st>>>(ctx->head, ctx->tail, ctx->tail_cell,
+                                                                 ctx->head_ends, ctx->offsets, ctx->rho_p,
+                                                                 ctx->mean, ctx->cov, ctx->sc, ctx->mom_ranges);
+    CK(cudaGetLastError());
+    CK(mark("moments_fixup"));
+
+    // 5b. births
+    if (ctx->nu_b > 0) {
+        k_births<<<cdiv(ctx->nu_b, 256), 256, 0, st>>>(ctx->sb, ctx->bx, ctx->by, ctx->bvx, ctx->bvy, ctx->sc,
+                                                        fc, a.k);
+        CK(cudaGetLastError());
+    }
+    CK(mark("births"));
+
+    // 7. resampling -> next state
+    k_resample<<<cdiv(nu, 256), 256, 0, st>>>(ctx->P, ctx->sb, ctx->offsets, ctx->Rp, ctx->Rb, ctx->perm,
+                                              ctx->px, ctx->py, ctx->pvx, ctx->pvy, ctx->bx, ctx->by,
+                                              ctx->bvx, ctx->bvy, ctx->x, ctx->y, ctx->vx, ctx->vy,
+                                              dbg ? ctx->jidx : nullptr, ctx->sc, fc);
+    CK(cudaGetLastError());
+    CK(mark("resample"));
+    if (prof) {
+        ctx->prof_nst = mark_i - 1;
+        ctx->prof_steps += 1;
+    }
+    ctx->k += 1;
+    return DOG_OK;
+}
+
+int dog_profile_begin(dog_ctx* ctx, int max_steps)
+{
+    if (!ctx || max_steps < 0) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    for (cudaEvent_t e : ctx->pev) cudaEventDestroy(e);
+    ctx->pev.assign((size_t)max_steps * (DOG_MAX_STAGES + 1), nullptr);
+    for (auto& e : ctx->pev) CK(cudaEventCreate(&e));
+    ctx->prof_max = max_steps;
+    ctx->prof_steps = 0;
+    return DOG_OK;
+}
+
+int dog_profile_end(dog_ctx* ctx, float* stage_ms, int* n_stages, int* n_steps)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    if (stage_ms)
+        for (int i = 0; i < DOG_MAX_STAGES; ++i) stage_ms[i] = 0.0f;
+    for (int s = 0; s < ctx->prof_steps; ++s) {
+        cudaEvent_t* ev = &ctx->pev[(size_t)s * (DOG_MAX_STAGES + 1)];
+        CK(cudaEventSynchronize(ev[ctx->prof_nst]));
+        for (int i = 0; i < ctx->prof_nst; ++i) {
+            float ms = 0.0f;
+            CK(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            if (stage_ms) stage_ms[i] += ms;
+        }
+    }
+    if (n_stages) *n_stages = ctx->prof_nst;
+    if (n_steps) *n_steps = ctx->prof_steps;
+    for (cudaEvent_t e : ctx->pev) cudaEventDestroy(e);
+    ctx->pev.clear();
+    ctx->prof_max = 0;
+    ctx->prof_steps = 0;
+    return DOG_OK;
+}
+
+const char* dog_profile_stage_name(dog_ctx* ctx, int i)
+{
+    if (!ctx || i < 0 || i >= DOG_MAX_STAGES || !ctx->stage_names[i]) return "";
+    return ctx->stage_names[i];
+}
+
+int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream)
+{
+    if (!ctx || !meas_host) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!ctx->meas_dev) {
+        int rc = dalloc(ctx, &ctx->meas_dev, 2 * (size_t)ctx->C);
+        if (rc) return rc;
+    }
+    CK(cudaMemcpyAsync(ctx->meas_dev, meas_host, 8 * (size_t)ctx->C, cudaMemcpyHostToDevice, st));
+    int rc = dog_step(ctx, ctx->meas_dev, dt, stream);
+    if (rc) return rc;
+    if (occ_host) CK(cudaMemcpyAsync(occ_host, ctx->occ, 4 * (size_t)ctx->C, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DOG_OK;
+}
+
+int dog_sync(dog_ctx* ctx, void* stream)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return report_meas(ctx);
+}
+
+int dog_read_cells(dog_ctx* ctx, float* occ, float* free_mass, float* vel_mean, float* vel_cov, void* stream)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t C = ctx->C;
+    if (occ) CK(cudaMemcpyAsync(occ, ctx->occ, 4 * C, cudaMemcpyDeviceToDevice, st));
+    if (free_mass) CK(cudaMemcpyAsync(free_mass, ctx->fre, 4 * C, cudaMemcpyDeviceToDevice, st));
+    if (vel_mean) CK(cudaMemcpyAsync(vel_mean, ctx->mean, 8 * C, cudaMemcpyDeviceToDevice, st));
+    if (vel_cov) CK(cudaMemcpyAsync(vel_cov, ctx->cov, 12 * C, cudaMemcpyDeviceToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return report_meas(ctx);
+}
+
+int dog_get_state(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float* w_bar, float* m_free,
+                  int64_t* k)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaDeviceSynchronize());
+    const size_t n = (size_t)ctx->nu * 4;
+    if (x) CK(cudaMemcpy(x, ctx->x, n, cudaMemcpyDeviceToHost));
+    if (y) CK(cudaMemcpy(y, ctx->y, n, cudaMemcpyDeviceToHost));
+    if (vx) CK(cudaMemcpy(vx, ctx->vx, n, cudaMemcpyDeviceToHost));
+    if (vy) CK(cudaMemcpy(vy, ctx->vy, n, cudaMemcpyDeviceToHost));
+    if (m_free) CK(cudaMemcpy(m_free, ctx->m_free, (size_t)ctx->C * 4, cudaMemcpyDeviceToHost));
+    if (w_bar) CK(cudaMemcpy(w_bar, &ctx->sc->w_bar, 4, cudaMemcpyDeviceToHost));
+    if (k) *k = ctx->k;
+    return report_meas(ctx);
+}
+
+int dog_set_state(dog_ctx* ctx, const float* x, const float* y, const float* vx, const float* vy, float w_bar,
+                  const float* m_free, int64_t k)
+{
+    if (!ctx || !x || !y || !vx || !vy || !m_free || !(w_bar >= 0.0f) || !finite(w_bar) || k < 0)
+        return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaDeviceSynchronize());
+    const size_t n = (size_t)ctx->nu * 4;
+    CK(cudaMemcpy(ctx->x, x, n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->y, y, n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->vx, vx, n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->vy, vy, n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->m_free, m_free, (size_t)ctx->C * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(&ctx->sc->w_bar, &w_bar, 4, cudaMemcpyHostToDevice));
+    ctx->k = k;
+    return DOG_OK;
+}
+
+int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
+{
+    if (!ctx || !host_dst) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaDeviceSynchronize());
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    const size_t nu = (size_t)ctx->nu, C = ctx->C, nb = (size_t)ctx->nu_b;
+    const void* src = nullptr;
+    size_t n = 0;
+    switch (what) {
+    case DOG_DBG_PRED_X: src = ctx->px; n = nu * 4; break;
+    case DOG_DBG_PRED_Y: src = ctx->py; n = nu * 4; break;
+    case DOG_DBG_PRED_VX: src = ctx->pvx; n = nu * 4; break;
+    case DOG_DBG_PRED_VY: src = ctx->pvy; n = nu * 4; break;
+    case DOG_DBG_KEY: if (!dbg) return DOG_E_STATE; src = ctx->key_dbg; n = nu * 4; break;
+    case DOG_DBG_PERM: src = ctx->perm; n = nu * 4; break;
+    case DOG_DBG_OFFSETS: src = ctx->offsets; n = (C + 1) * 4; break;
+    case DOG_DBG_RHO_P: src = ctx->rho_p; n = C * 4; break;
+    case DOG_DBG_RHO_B: if (!dbg) return DOG_E_STATE; src = ctx->rho_b; n = C * 4; break;
+    case DOG_DBG_RP: src = ctx->Rp; n = C * 8; break;
+    case DOG_DBG_RB: src = ctx->Rb; n = C * 8; break;
+    case DOG_DBG_BIRTH_X: src = ctx->bx; n = nb * 4; break;
+    case DOG_DBG_BIRTH_Y: src = ctx->by; n = nb * 4; break;
+    case DOG_DBG_BIRTH_VX: src = ctx->bvx; n = nb * 4; break;
+    case DOG_DBG_BIRTH_VY: src = ctx->bvy; n = nb * 4; break;
+    case DOG_DBG_JOINT_IDX: if (!dbg) return DOG_E_STATE; src = ctx->jidx; n = nu * 4; break;
+    case DOG_DBG_NB: {
+        n = C * 4;
+        if (bytes < n) return DOG_E_INVAL;
+        std::vector<uint32_t> s(C + 1);
+        CK(cudaMemcpy(s.data(), ctx->sb, (C + 1) * 4, cudaMemcpyDeviceToHost));
+        uint32_t* d = (uint32_t*)host_dst;
+        for (size_t c = 0; c < C; ++c) d[c] = s[c + 1] - s[c];
+        return (int64_t)n;
+    }
+    case DOG_DBG_SCALARS: {
+        n = 8 * 8;
+        if (bytes < n) return DOG_E_INVAL;
+        DevScalars s;
+        CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+        uint64_t* d = (uint64_t*)host_dst;
+        uint32_t wp, wb;
+        memcpy(&wp, &s.w_pred, 4);
+        memcpy(&wb, &s.w_bar, 4);
+        d[0] = s.W; d[1] = s.U; d[2] = s.A; d[3] = s.meas_bad; d[4] = wp; d[5] = wb;
+        d[6] = (uint64_t)(ctx->k - 1); d[7] = s.n_in;
+        return (int64_t)n;
+    }
+    default: return DOG_E_INVAL;
+    }
+    if (bytes < n) return DOG_E_INVAL;
+    if (n) CK(cudaMemcpy(host_dst, src, n, cudaMemcpyDeviceToHost));
+    return (int64_t)n;
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+"""Thin Python binding of libdog.so (include/dog.h) -- argument marshalling only.
+
+Every stage of the filter cycle runs in the CUDA kernels of ``csrc/``; this module only converts
+arguments (torch tensors -> device pointers, streams -> cudaStream_t) and status codes -> exceptions.
+There is no CPU fallback: if the library is missing or cannot load, import fails loudly.
+
+The C functions are re-exported under their C names (``dog_create``, ``dog_step``, ...); the
+``Filter`` class is a convenience wrapper over them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdog.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libdog.so not found at {LIB_PATH}: build it with `python -m paper_1605_02406_b200.build` "
+        "(or __graft_entry__.build()); there is no fallback implementation")
+_lib = C.CDLL(LIB_PATH)
+
+DOG_OK, DOG_E_INVAL, DOG_E_NOMEM, DOG_E_CUDA, DOG_E_NCCL, DOG_E_MEAS, DOG_E_STATE = 0, -1, -2, -3, -4, -5, -6
+DOG_FLAG_DEBUG = 1
+
+DEBUG_IDS = {n: i + 1 for i, n in enumerate([
+    "PRED_X", "PRED_Y", "PRED_VX", "PRED_VY", "KEY", "PERM", "OFFSETS", "RHO_P", "RHO_B", "RP", "RB",
+    "NB", "BIRTH_X", "BIRTH_Y", "BIRTH_VX", "BIRTH_VY", "JOINT_IDX", "SCALARS"])}
+
+
+class dog_grid(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("cell_size", C.c_float)]
+
+
+class dog_params(C.Structure):
+    _fields_ = [("p_s", C.c_float), ("p_b", C.c_float), ("sigma_pos", C.c_float), ("sigma_vel", C.c_float),
+                ("sigma_birth_vel", C.c_float), ("free_tau", C.c_float), ("occ_max", C.c_float),
+                ("v_max", C.c_float)]
+
+
+_vp, _f32p = C.c_void_p, C.POINTER(C.c_float)
+_SIGS = {
+    "dog_version": ([], C.c_int),
+    "dog_error_string": ([C.c_int], C.c_char_p),
+    "dog_create": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
+                    C.POINTER(_vp)], C.c_int),
+    "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
+    "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
+    "dog_read_cells": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "dog_sync": ([_vp, _vp], C.c_int),
+    "dog_destroy": ([_vp], C.c_int),
+    "dog_get_state": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_int64)], C.c_int),
+    "dog_set_state": ([_vp, _vp, _vp, _vp, _vp, C.c_float, _vp, C.c_int64], C.c_int),
+    "dog_get_debug": ([_vp, C.c_int, _vp, C.c_size_t], C.c_int64),
+    "dog_launches_per_step": ([_vp], C.c_int),
+    "dog_profile_begin": ([_vp, C.c_int], C.c_int),
+    "dog_profile_end": ([_vp, _vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
+}
+DOG_MAX_STAGES = 16
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+    globals()[_name] = _f
+
+
+class DogError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(f"{what}: {dog_error_string(status).decode()} ({status})")
+
+
+def _check(rc: int, what: str) -> int:
+    if rc < 0:
+        raise DogError(rc, what)
+    return rc
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def _np_ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Filter:
+    """One DS-PHD/MIB filter (a dog_ctx) on the current CUDA device."""
+
+    def __init__(self, width: int, height: int, nu: int, nu_b: int, *, cell_size: float = 0.1,
+                 p_s: float = 0.99, p_b: float = 0.02, sigma_pos: float = 0.02, sigma_vel: float = 0.8,
+                 sigma_birth_vel: float = 4.0, free_tau: float = 2.0, occ_max: float = 1.0,
+                 v_max: float = 0.0, seed: int = 2406, debug: bool = False):
+        self.width, self.height, self.nu, self.nu_b = width, height, nu, nu_b
+        self.C = width * height
+        g = dog_grid(width, height, cell_size)
+        p = dog_params(p_s, p_b, sigma_pos, sigma_vel, sigma_birth_vel, free_tau, occ_max, v_max)
+        h = _vp()
+        _check(dog_create(C.byref(g), nu, nu_b, C.byref(p), seed, DOG_FLAG_DEBUG if debug else 0, C.byref(h)),
+               "dog_create")
+        self._h = h
+
+    @classmethod
+    def from_config(cls, cfg, debug: bool = False, **over) -> "Filter":
+        kw = dict(cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params())
+        kw.update(over)
+        return cls(cfg.width, cfg.height, cfg.nu, cfg.nu_b, debug=debug, **kw)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            dog_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def handle(self):
+        return self._h
+
+    def launches_per_step(self) -> int:
+        return _check(dog_launches_per_step(self._h), "dog_launches_per_step")
+
+    def profile_begin(self, max_steps: int):
+        _check(dog_profile_begin(self._h, max_steps), "dog_profile_begin")
+
+    def profile_end(self) -> tuple[dict, int]:
+        """Summed device ms per stage over the profiled steps, and the number of steps."""
+        ms = np.zeros(DOG_MAX_STAGES, np.float32)
+        ns, nst = C.c_int(), C.c_int()
+        _check(dog_profile_end(self._h, _np_ptr(ms), C.byref(ns), C.byref(nst)), "dog_profile_end")
+        names = [dog_profile_stage_name(self._h, i).decode() for i in range(ns.value)]
+        return {n: float(ms[i]) for i, n in enumerate(names)}, nst.value
+
+    def step(self, meas: torch.Tensor, dt: float, stream=None):
+        assert meas.is_cuda and meas.dtype == torch.float32 and meas.is_contiguous()
+        assert meas.numel() == 2 * self.C
+        _check(dog_step(self._h, meas.data_ptr(), dt, _stream_ptr(stream)), "dog_step")
+
+    def step_host(self, meas_host: torch.Tensor, dt: float, occ_host: torch.Tensor | None = None, stream=None):
+        assert not meas_host.is_cuda and meas_host.dtype == torch.float32 and meas_host.is_contiguous()
+        occ_ptr = occ_host.data_ptr() if occ_host is not None else None
+        _check(dog_step_host(self._h, meas_host.data_ptr(), dt, occ_ptr, _stream_ptr(stream)), "dog_step_host")
+
+    def sync(self, stream=None) -> int:
+        return dog_sync(self._h, _stream_ptr(stream))
+
+    def read_cells(self, stream=None, check: bool = True) -> dict:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        out = dict(occ=torch.empty(self.C, device=dev), free=torch.empty(self.C, device=dev),
+                   mean=torch.empty(self.C, 2, device=dev), cov=torch.empty(self.C, 3, device=dev))
+        rc = dog_read_cells(self._h, out["occ"].data_ptr(), out["free"].data_ptr(), out["mean"].data_ptr(),
+                            out["cov"].data_ptr(), _stream_ptr(stream))
+        if check:
+            _check(rc, "dog_read_cells")
+        out["status"] = rc
+        return out
+
+    def get_state(self) -> dict:
+        nu = self.nu
+        x, y, vx, vy = (np.zeros(nu, np.float32) for _ in range(4))
+        mf = np.zeros(self.C, np.float32)
+        wb = np.zeros(1, np.float32)
+        k = C.c_int64()
+        _check(dog_get_state(self._h, _np_ptr(x), _np_ptr(y), _np_ptr(vx), _np_ptr(vy), _np_ptr(wb), _np_ptr(mf),
+                             C.byref(k)), "dog_get_state")
+        return dict(x=x, y=y, vx=vx, vy=vy, w_bar=wb[0], m_free=mf, k=k.value)
+
+    def set_state(self, x, y, vx, vy, w_bar: float, m_free, k: int):
+        arrs = [np.ascontiguousarray(a, dtype=np.float32) for a in (x, y, vx, vy, m_free)]
+        assert all(a.size == self.nu for a in arrs[:4]) and arrs[4].size == self.C
+        _check(dog_set_state(self._h, *[_np_ptr(a) for a in arrs[:4]], float(w_bar), _np_ptr(arrs[4]), int(k)),
+               "dog_set_state")
+
+    _DT = {"KEY": np.uint32, "PERM": np.uint32, "OFFSETS": np.uint32, "RP": np.uint64, "RB": np.uint64,
+           "NB": np.uint32, "JOINT_IDX": np.uint32, "SCALARS": np.uint64}
+
+    def debug(self, name: str) -> np.ndarray:
+        n = {"OFFSETS": self.C + 1, "SCALARS": 8}.get(name)
+        if n is None:
+            if name.startswith("PRED") or name in ("KEY", "PERM", "JOINT_IDX"):
+                n = self.nu
+            elif name.startswith("BIRTH"):
+                n = self.nu_b
+            else:
+                n = self.C
+        a = np.zeros(n, self._DT.get(name, np.float32))
+        _check(dog_get_debug(self._h, DEBUG_IDS[name], _np_ptr(a), a.nbytes), f"dog_get_debug({name})")
+        return a
+
+    def scalars(self) -> dict:
+        s = self.debug("SCALARS")
+        return dict(W=int(s[0]), U=int(s[1]), A=int(s[2]), meas_bad=int(s[3]),
+                    w_pred=np.uint32(s[4]).view(np.float32), w_bar=np.uint32(s[5]).view(np.float32),
+                    k=int(s[6]), n_in=int(s[7]))

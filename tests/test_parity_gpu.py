@@ -1,0 +1,229 @@
+"""GPU parity: libdog.so (through its C ABI) vs the CPU oracle, element by element, on the same seeded
+inputs and the same injected states.  Bit-exact on every integer / index / f32-state output; masses are
+expected (and checked) bit-identical; velocity moments within the north-star 1e-4 relative tolerance
+(DESIGN.md section 4).  Requires a CUDA device: run with `-m gpu`."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1605_02406_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test selected but no CUDA device is visible")
+    oracle.build()
+    torch.cuda.set_device(0)
+
+
+def pair(cfg, **over):
+    from paper_1605_02406_b200 import dog
+    kw = dict(cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params())
+    kw.update(over)
+    g = dog.Filter(cfg.width, cfg.height, cfg.nu, cfg.nu_b, debug=True, **kw)
+    o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b, **kw))
+    return o, g
+
+
+def inject(o, g, st):
+    o.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+    g.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+
+
+def assert_bits(a, b, what):
+    a = np.ascontiguousarray(a); b = np.ascontiguousarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    if a.dtype == np.float32:
+        a, b = a.view(np.uint32), b.view(np.uint32)
+    bad = np.nonzero(a != b)[0]
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[:5]}: {a[bad[:5]]} vs {b[bad[:5]]}"
+
+
+def rel_close(a, b, rel, abs_, what):
+    a = a.astype(np.float64); b = b.astype(np.float64)
+    tol = rel * np.maximum(np.abs(a), np.abs(b)) + abs_
+    bad = np.nonzero(np.abs(a - b) > tol)[0]
+    assert bad.size == 0, f"{what}: {bad.size} beyond tolerance, first {bad[:5]}: {a[bad[:5]]} vs {b[bad[:5]]}"
+
+
+def compare_cycle(o, g, rc_gpu=None):
+    """Stage-by-stage comparison of the last cycle."""
+    for n in ("PRED_X", "PRED_Y", "PRED_VX", "PRED_VY", "KEY", "PERM", "OFFSETS", "RHO_P", "RHO_B", "RP",
+              "RB", "NB", "JOINT_IDX"):
+        assert_bits(o.dump(n), g.debug(n), n)
+    so, sg = o.scalars(), g.scalars()
+    for k in ("W", "U", "A", "n_in", "k"):
+        assert so[k] == sg[k], (k, so[k], sg[k])
+    for k in ("w_pred", "w_bar"):
+        assert np.float32(so[k]).view(np.uint32) == np.float32(sg[k]).view(np.uint32), k
+    nslots = g.nu_b if so["A"] > 0 else 0
+    for n in ("BIRTH_X", "BIRTH_Y", "BIRTH_VX", "BIRTH_VY"):
+        assert_bits(o.dump(n)[:nslots], g.debug(n)[:nslots], n)
+    co = o.read_cells()
+    cg = {k: v.cpu().numpy() for k, v in g.read_cells(check=False).items() if k != "status"}
+    assert_bits(co["occ"], cg["occ"], "occ")
+    assert_bits(co["free"], cg["free"], "free")
+    mo, mg = co["mean"].reshape(-1), cg["mean"].reshape(-1)
+    rel_close(mo, mg, 1e-4, 1e-6, "vel_mean")
+    vo, vg = co["cov"].reshape(-1, 3), cg["cov"].reshape(-1, 3)
+    rel_close(vo[:, :2].reshape(-1), vg[:, :2].reshape(-1), 1e-4, 1e-8, "vel_var")
+    scale = np.sqrt(np.abs(vo[:, 0] * vo[:, 1])).astype(np.float64)
+    assert np.all(np.abs(vo[:, 2].astype(np.float64) - vg[:, 2]) <= 1e-4 * scale + 1e-8), "vel_cov"
+    sto, stg = o.get_state(), g.get_state()
+    for k in ("x", "y", "vx", "vy", "m_free"):
+        assert_bits(sto[k], stg[k], "state." + k)
+    assert sto["k"] == stg["k"]
+
+
+def run_lockstep(cfg, steps, st=None, frames=None, **over):
+    o, g = pair(cfg, **over)
+    if st is not None:
+        inject(o, g, st)
+    sc = I.scene(cfg) if frames is None else None
+    for k in range(steps):
+        meas = frames[k] if frames is not None else sc.frame(k).numpy()
+        o.step(meas, cfg.dt)
+        g.step(torch.from_numpy(np.ascontiguousarray(meas, np.float32)).cuda(), cfg.dt)
+        compare_cycle(o, g)
+    return o, g
+
+
+def test_cfg1_lockstep_10_cycles():
+    """BASELINE configs[0]: 32x32, 10k + 1k particles, moving box, 10 cycles from the empty state."""
+    run_lockstep(I.CONFIGS["cfg1"], 10)
+
+
+def test_ragged_sizes():
+    """nu not a multiple of 4 / of the 4096-element sort tile, odd nu_b, non-square grid."""
+    cfg = I.config("cfg1", width=37, height=23, nu=10_007, nu_b=999)
+    run_lockstep(cfg, 6)
+
+
+def test_no_births():
+    """nu_b = 0 with an injected population: no birth kernel, pure persistence."""
+    cfg = I.config("cfg1", nu=20_000, nu_b=0)
+    rng = np.random.default_rng(3)
+    st = I.cells_state(cfg, rng.integers(0, 30, cfg.C) * (rng.random(cfg.C) < 0.5), 0.01, rng=rng,
+                       vel=(1.0, -0.5), vel_sd=2.0)
+    run_lockstep(cfg, 4, st=st)
+
+
+def test_multitile_scene():
+    """A 256x256 ray-cast scene with 300k particles (74 sort tiles, 16 cell tiles) for 5 cycles."""
+    cfg = I.config("cfg2", width=256, height=256, nu=300_000, nu_b=30_000, beams=600, movers=4, peds=3,
+                   boxes=15)
+    run_lockstep(cfg, 5)
+
+
+def test_single_cell_holds_everything():
+    """One cell holds every particle (one segment spanning every moments range and sort tile)."""
+    cfg = I.config("cfg1", width=16, height=16, nu=50_000, nu_b=5_000, sigma_pos=0.0, sigma_vel=0.0)
+    counts = np.zeros(cfg.C, np.int64); counts[77] = cfg.nu
+    st = I.cells_state(cfg, counts, 1.0 / cfg.nu, vel=(0.0, 0.0), vel_sd=3.0)
+    meas = np.zeros((3, cfg.C, 2), np.float32); meas[:, 77, 0] = 0.9; meas[:, :77, 1] = 0.5
+    run_lockstep(cfg, 3, st=st, frames=meas)
+
+
+def test_all_particles_leave_the_grid():
+    """Every particle predicted outside (sentinel key C): no persistent mass, births only."""
+    cfg = I.config("cfg1", nu=5_000, nu_b=500, sigma_pos=0.0, sigma_vel=0.0)
+    st = I.cells_state(cfg, np.r_[np.zeros(cfg.C - 1, int), [cfg.nu]], 1.0 / cfg.nu, vel=(50.0, 0.0))
+    meas = np.zeros((2, cfg.C, 2), np.float32); meas[:, 5, 0] = 0.8
+    run_lockstep(cfg, 2, st=st, frames=meas)
+
+
+def test_empty_world_stays_empty():
+    cfg = I.CONFIGS["cfg1"]
+    meas = np.zeros((3, cfg.C, 2), np.float32); meas[..., 1] = 0.4
+    o, g = run_lockstep(cfg, 3, frames=meas)
+    assert g.scalars()["W"] == 0
+
+
+def test_bayesian_injection():
+    """The P-BBF setup (p_S = 1, alpha = 1, sigma = 0, p_B = 0) with Bayesian measurements."""
+    cfg = I.config("cfg1", nu=1024 * 50, nu_b=0, p_s=1.0, p_b=0.0, sigma_pos=0.0, sigma_vel=0.0,
+                   free_tau=float("inf"))
+    rng = np.random.default_rng(5)
+    st = I.cells_state(cfg, rng.integers(5, 50, cfg.C), 1.0 / 50, rng=rng)
+    st["m_free"] = np.clip(1 - st["w_bar"] * np.bincount(
+        (st["y"][st["x"] >= 0].astype(int) * 32 + st["x"][st["x"] >= 0].astype(int)), minlength=cfg.C),
+        0, 1).astype(np.float32)
+    z = rng.uniform(0.05, 0.95, (4, cfg.C)).astype(np.float32)
+    frames = np.stack([z, 1 - z], -1).astype(np.float32)
+    run_lockstep(cfg, 4, st=st, frames=frames)
+
+
+def test_invalid_measurement_cells():
+    """A-27: NaN / negative / over-unity cells are treated as vacuous on both sides and reported
+    as DOG_E_MEAS by the next synchronous call."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    sc = I.scene(cfg)
+    frames = [sc.frame(k).numpy().reshape(-1, 2).copy() for k in range(3)]
+    frames[1][3] = [np.nan, 0.1]; frames[1][4] = [-0.1, 0.2]; frames[1][5] = [0.7, 0.6]
+    o, g = pair(cfg)
+    for k in range(3):
+        o.step(frames[k], cfg.dt)
+        g.step(torch.from_numpy(frames[k]).cuda(), cfg.dt)
+        rc = g.read_cells(check=False)["status"]
+        assert rc == (dog.DOG_E_MEAS if k == 1 else dog.DOG_OK)
+        compare_cycle(o, g)
+
+
+def test_resume_bit_exact_and_host_entry():
+    """dog_get_state / dog_set_state resume exactly (counter-based RNG), and dog_step_host (host
+    buffers, the end-to-end entry) computes the same cycle as dog_step."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    sc = I.scene(cfg)
+    a = dog.Filter.from_config(cfg)
+    for k in range(4):
+        a.step(sc.frame(k).cuda(), cfg.dt)
+    st = a.get_state()
+    b = dog.Filter.from_config(cfg)
+    b.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+    occ_host = torch.empty(cfg.C).pin_memory()
+    for k in range(4, 7):
+        a.step(sc.frame(k).cuda(), cfg.dt)
+        b.step_host(sc.frame(k).contiguous().pin_memory(), cfg.dt, occ_host)
+        assert torch.equal(a.read_cells()["occ"].cpu(), occ_host)
+    sa, sb = a.get_state(), b.get_state()
+    for k in ("x", "y", "vx", "vy", "m_free"):
+        assert_bits(sa[k], sb[k], k)
+
+
+def test_profile_stages():
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    f = dog.Filter.from_config(cfg)
+    f.profile_begin(3)
+    meas = I.scene(cfg).frame(0).cuda()
+    for _ in range(3):
+        f.step(meas, cfg.dt)
+    stages, n = f.profile_end()
+    assert n == 3 and "predict" in stages and "resample" in stages and all(v >= 0 for v in stages.values())
+
+
+@pytest.mark.slow
+def test_full_size_cfgT_one_cycle():
+    """The bench configuration (cfg T: 2048x2048, 8M + 800k) in the bench's launch configuration: warm
+    the GPU filter for 6 cycles, inject its state into the oracle, run one more cycle on both and
+    compare every stage element by element."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfgT"]
+    sc = I.scene(cfg)
+    g = dog.Filter.from_config(cfg, debug=True)
+    for k in range(6):
+        g.step(sc.frame(k, device="cuda"), cfg.dt)
+    st = g.get_state()
+    o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b,
+                                    cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params()))
+    o.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+    meas = sc.frame(6).numpy()
+    o.step(meas, cfg.dt)
+    g.step(torch.from_numpy(meas).cuda(), cfg.dt)
+    compare_cycle(o, g)
