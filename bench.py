@@ -40,18 +40,15 @@ def peaks():
 def stage_bytes(stage: str, cfg, n_in: int) -> float:
     nu, nb, C = cfg.nu, cfg.nu_b, cfg.C
     table = {
-        "predict": 36.0 * nu,
-        "sort_pass0": 12.0 * nu,
+        "predict": 36.0 * nu,                       # state in 16, predicted state out 16, key 4
+        "sort_pass0": 12.0 * nu,                    # key in 4, (key, index) out 8
         "sort_pass1": 16.0 * nu,
         "sort_pass2": 16.0 * nu,
         "sort_pass3": 16.0 * nu,
-        "scan_counts": 8.0 * C,
-        "cells": 68.0 * C,
-        "scan_joint": 28.0 * C,
-        "moments": 16.0 * n_in,
+        "cells": 28.0 * C,                          # counts 4, m_F 4, meas 8 in; occ 4, free 4, m_F 4 out
+        "list_scan": 0.0,
+        "resample": 40.0 * n_in + 16.0 * nb,        # sorted key 4, perm 4, gathered state 16, next state 16
         "moments_fixup": 0.0,
-        "births": 16.0 * nb,
-        "resample": 36.0 * nu,
     }
     return table.get(stage, 0.0)
 

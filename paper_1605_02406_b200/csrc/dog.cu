@@ -13,6 +13,8 @@
 
 #include "../../include/dog.h"
 #include "dog_kernels.cuh"
+#include "dog_cells.cuh"
+#include "dog_resample.cuh"
 
 using namespace dog;
 
@@ -35,7 +37,7 @@ struct dog_ctx {
     int64_t k = 0;
     bool poisoned = false;
     size_t nu_cap = 0;          // particle arrays padded to the sort tile
-    uint32_t sort_tiles = 0, cell_tiles = 0, joint_tiles = 0, mom_ranges = 0;
+    uint32_t sort_tiles = 0, cell_tiles = 0, list_tiles = 0, mom_ranges = 0, pers_blocks = 0;
 
     // state S_k and predicted state (SoA, f32)
     float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
@@ -43,27 +45,28 @@ struct dog_ctx {
     // sort
     uint32_t *keyA = nullptr, *keyB = nullptr, *valA = nullptr, *valB = nullptr, *key_dbg = nullptr;
     uint32_t *skeys = nullptr, *perm = nullptr;   // results (alias keyX/valX)
+    uint32_t* counts = nullptr;                   // n_c, zeroed by k_cells after use
     // cells
-    uint32_t* offsets = nullptr;
-    float *m_free = nullptr, *occ = nullptr, *fre = nullptr, *rho_p = nullptr, *rho_b = nullptr;
+    float *m_free = nullptr, *occ = nullptr, *fre = nullptr;
     float2* mean = nullptr;
     float* cov = nullptr;
-    uint64_t *Rp = nullptr, *Rb = nullptr, *P = nullptr;
-    uint32_t* sb = nullptr;
-    uint64_t *aggA = nullptr, *incA = nullptr, *aggJ = nullptr, *incJ = nullptr;
-    // births, resampling
+    uint32_t* mvalid = nullptr;                   // moments-reported bitmask
+    CellList list{};
+    uint32_t* cell2list = nullptr;
+    ulonglong2 *agg1 = nullptr, *inc1 = nullptr, *agg2 = nullptr, *inc2 = nullptr;
+    // debug-only arrays
+    float *dbg_rho_p = nullptr, *dbg_rho_b = nullptr;
+    uint64_t *dbg_Rp = nullptr, *dbg_Rb = nullptr;
     float *bx = nullptr, *by = nullptr, *bvx = nullptr, *bvy = nullptr;
     uint32_t* jidx = nullptr;
     // moments partials
-    MomPartial *head = nullptr, *tail = nullptr;
-    uint32_t* tail_cell = nullptr;
-    uint8_t* head_ends = nullptr;
+    MomScratch ms{};
     DevScalars* sc = nullptr;
-    // zeroed once per cycle (one memset): counts, radix histograms, tile counters, look-back status
+    // zeroed once per cycle (one memset): radix histograms, tile counters, look-back status
     uint8_t* zero = nullptr;
     size_t zero_bytes = 0;
-    uint32_t *counts = nullptr, *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr,
-             *st_counts = nullptr, *flagA = nullptr, *flagJ = nullptr;
+    uint32_t *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr, *st_cells = nullptr, *flag1 = nullptr,
+             *flag2 = nullptr;
     // end-to-end staging
     float* meas_dev = nullptr;
     // profiling: events[step][stage boundary]
@@ -212,10 +215,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->npass = (bits + 7) / 8;
     ctx->nu_cap = round_up((size_t)n_particles, kRsTile);
     ctx->sort_tiles = cdiv(n_particles, kRsTile);
-    ctx->cell_tiles = cdiv(C, kScTile);
-    ctx->joint_tiles = cdiv(C, kJTile);
+    ctx->cell_tiles = cdiv(C, kCellTile);
+    ctx->list_tiles = cdiv(C, kLsTile);
     ctx->mom_ranges = cdiv(n_particles, kMomRange);
+    ctx->pers_blocks = cdiv(ctx->mom_ranges, 8);
     const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
+    const bool dbg = (flags & DOG_FLAG_DEBUG) != 0;
 
     int rc = DOG_OK;
 #define AL(ptr, n) \
@@ -223,22 +228,29 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->x, N); AL(ctx->y, N); AL(ctx->vx, N); AL(ctx->vy, N);
     AL(ctx->px, N); AL(ctx->py, N); AL(ctx->pvx, N); AL(ctx->pvy, N);
     AL(ctx->keyA, N); AL(ctx->keyB, N); AL(ctx->valA, N); AL(ctx->valB, N);
-    if (flags & DOG_FLAG_DEBUG) { AL(ctx->key_dbg, N); AL(ctx->rho_b, Cs); AL(ctx->jidx, N); }
-    AL(ctx->offsets, Cs + 1);
-    AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs); AL(ctx->rho_p, Cs);
+    AL(ctx->counts, Cs + 1);
+    if (dbg) {
+        AL(ctx->key_dbg, N); AL(ctx->jidx, N);
+        AL(ctx->dbg_rho_p, Cs); AL(ctx->dbg_rho_b, Cs); AL(ctx->dbg_Rp, Cs); AL(ctx->dbg_Rb, Cs);
+        AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
+    }
+    AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs);
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
-    AL(ctx->Rp, Cs); AL(ctx->Rb, Cs); AL(ctx->P, Cs + 1); AL(ctx->sb, Cs + 1);
-    AL(ctx->aggA, ctx->joint_tiles); AL(ctx->incA, ctx->joint_tiles);
-    AL(ctx->aggJ, ctx->joint_tiles); AL(ctx->incJ, ctx->joint_tiles);
-    AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
-    AL(ctx->head, ctx->mom_ranges); AL(ctx->tail, ctx->mom_ranges);
-    AL(ctx->tail_cell, ctx->mom_ranges); AL(ctx->head_ends, ctx->mom_ranges);
+    AL(ctx->mvalid, Cs / 32 + 1);
+    AL(ctx->list.c, Cs); AL(ctx->list.n, Cs); AL(ctx->list.Rp, Cs); AL(ctx->list.Rb, Cs);
+    AL(ctx->list.rho_p, Cs); AL(ctx->list.start, Cs); AL(ctx->list.sb, Cs); AL(ctx->list.nb, Cs);
+    AL(ctx->list.P, Cs); AL(ctx->list.bp, Cs); AL(ctx->list.rp, Cs); AL(ctx->list.bb, Cs);
+    AL(ctx->list.rb, Cs);
+    AL(ctx->cell2list, Cs);
+    AL(ctx->agg1, ctx->list_tiles); AL(ctx->inc1, ctx->list_tiles);
+    AL(ctx->agg2, ctx->list_tiles); AL(ctx->inc2, ctx->list_tiles);
+    AL(ctx->ms.head, ctx->mom_ranges); AL(ctx->ms.tail, ctx->mom_ranges);
+    AL(ctx->ms.tail_cell, ctx->mom_ranges); AL(ctx->ms.head_ends, ctx->mom_ranges);
     AL(ctx->sc, 1);
     // zero region layout (u32 words)
-    const size_t w_counts = Cs + 1, w_rhist = kMaxPasses * 256, w_ctrs = 16,
-                 w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256, w_cnt = ctx->cell_tiles,
-                 w_fA = ctx->joint_tiles, w_fJ = ctx->joint_tiles;
-    ctx->zero_bytes = 4 * (w_counts + w_rhist + w_ctrs + w_sort + w_cnt + w_fA + w_fJ);
+    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16, w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256,
+                 w_cells = ctx->cell_tiles, w_f1 = ctx->list_tiles, w_f2 = ctx->list_tiles;
+    ctx->zero_bytes = 4 * (w_rhist + w_ctrs + w_sort + w_cells + w_f1 + w_f2);
     AL(ctx->zero, ctx->zero_bytes);
 #undef AL
     if (rc != DOG_OK) {
@@ -247,13 +259,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         return rc;
     }
     uint32_t* z = (uint32_t*)ctx->zero;
-    ctx->counts = z; z += w_counts;
     ctx->rhist = z; z += w_rhist;
     ctx->ctrs = z; z += w_ctrs;
     ctx->st_sort = z; z += w_sort;
-    ctx->st_counts = z; z += w_cnt;
-    ctx->flagA = z; z += w_fA;
-    ctx->flagJ = z; z += w_fJ;
+    ctx->st_cells = z; z += w_cells;
+    ctx->flag1 = z; z += w_f1;
+    ctx->flag2 = z; z += w_f2;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
     std::vector<float> sent(N, kSentinelPos);
@@ -268,6 +279,8 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     if (e == cudaSuccess) e = cudaMemset(ctx->mean, 0, Cs * 8);
     if (e == cudaSuccess) e = cudaMemset(ctx->cov, 0, Cs * 12);
     if (e == cudaSuccess) e = cudaMemset(ctx->sc, 0, sizeof(DevScalars));
+    if (e == cudaSuccess) e = cudaMemset(ctx->counts, 0, (Cs + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         fprintf(stderr, "libdog: dog_create init failed: %s\n", cudaGetErrorString(e));
@@ -293,7 +306,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 7 + ctx->npass + (ctx->nu_b > 0 ? 1 : 0);   // kernels (the memset is not a kernel)
+    return 5 + ctx->npass;   // predict, sort passes, cells, list scan, resample, moments fixup
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -348,54 +361,37 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     }
     ctx->skeys = kin;
     ctx->perm = vin;
-    k_scan_counts<<<ctx->cell_tiles, kScThreads, 0, st>>>(ctx->counts, ctx->offsets, ctx->C, ctx->ctrs + 8,
-                                                          ctx->st_counts, ctx->sc);
-    CK(cudaGetLastError());
-    CK(mark("scan_counts"));
 
-    // 3. cells: DS predict/update, birth split, fixed point
-    const uint32_t cgrid = std::min<uint32_t>(cdiv(ctx->C, 256), 148u * 16u);
-    k_cells<<<cgrid, 256, 0, st>>>(ctx->offsets, ctx->m_free, (const float2*)meas, ctx->occ, ctx->fre,
-                                   ctx->rho_p, dbg ? ctx->rho_b : nullptr, ctx->Rp, ctx->Rb, ctx->mean,
-                                   ctx->cov, ctx->sc, fc, a.alpha);
+    // 3. cells: DS predict/update, birth split, fixed point, active-cell list
+    CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
+    k_cells<<<ctx->cell_tiles, kCellThreads, 0, st>>>(ctx->counts, ctx->m_free, (const float2*)meas, ctx->occ,
+                                                      ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->list,
+                                                      ctx->cell2list, ctx->ctrs + 8, ctx->st_cells, ctx->sc, fc,
+                                                      a.alpha);
     CK(cudaGetLastError());
     CK(mark("cells"));
 
-    // 5a. birth slots + joint CDF
-    k_scan_joint<<<ctx->joint_tiles, kJThreads, 0, st>>>(ctx->Rp, ctx->Rb, ctx->sb, ctx->P, ctx->C,
-                                                          ctx->ctrs + 9, ctx->flagA, ctx->aggA, ctx->incA,
-                                                          ctx->flagJ, ctx->aggJ, ctx->incJ, ctx->sc, fc, a.k);
+    // 5a/7a. birth slots + joint CDF over the active list
+    LookbackPair lb1{ctx->flag1, ctx->agg1, ctx->inc1}, lb2{ctx->flag2, ctx->agg2, ctx->inc2};
+    k_list_scan<<<ctx->list_tiles, kLsThreads, 0, st>>>(ctx->list, ctx->ctrs + 9, lb1, lb2, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
-    CK(mark("scan_joint"));
+    CK(mark("list_scan"));
 
-    // 6. moments
-    k_moments<<<cdiv(ctx->mom_ranges, 8), 256, 0, st>>>(ctx->skeys, ctx->perm, ctx->pvx, ctx->pvy,
-                                                         ctx->offsets, ctx->rho_p, ctx->mean, ctx->cov,
-                                                         ctx->head, ctx->tail, ctx->tail_cell,
-                                                         ctx->head_ends, ctx->sc, ctx->mom_ranges);
-    CK(cudaGetLastError());
-    CK(mark("moments"));
-    k_moments_fixup<<<cdiv(ctx->mom_ranges, 256), 256, 0, st>>>(ctx->head, ctx->tail, ctx->tail_cell,
-                                                                 ctx->head_ends, ctx->offsets, ctx->rho_p,
-                                                                 ctx->mean, ctx->cov, ctx->sc, ctx->mom_ranges);
-    CK(cudaGetLastError());
-    CK(mark("moments_fixup"));
-
-    // 5b. births
-    if (ctx->nu_b > 0) {
-        k_births<<<cdiv(ctx->nu_b, 256), 256, 0, st>>>(ctx->sb, ctx->bx, ctx->by, ctx->bvx, ctx->bvy, ctx->sc,
-                                                        fc, a.k);
-        CK(cudaGetLastError());
-    }
-    CK(mark("births"));
-
-    // 7. resampling -> next state
-    k_resample<<<cdiv(nu, 256), 256, 0, st>>>(ctx->P, ctx->sb, ctx->offsets, ctx->Rp, ctx->Rb, ctx->perm,
-                                              ctx->px, ctx->py, ctx->pvx, ctx->pvy, ctx->bx, ctx->by,
-                                              ctx->bvx, ctx->bvy, ctx->x, ctx->y, ctx->vx, ctx->vy,
-                                              dbg ? ctx->jidx : nullptr, ctx->sc, fc);
+    // 5b/6/7b. births, moments and resampling in one pass over the joint set
+    Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
+    NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
+    BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
+    const uint32_t birth_blocks = cdiv(ctx->nu_b, 256);
+    k_resample<<<ctx->pers_blocks + birth_blocks, 256, 0, st>>>(ctx->skeys, ctx->perm, pr, ctx->list,
+                                                                ctx->cell2list, ns, bd, ctx->mean, ctx->cov,
+                                                                ctx->ms, ctx->sc, fc, a.k, ctx->pers_blocks,
+                                                                ctx->mom_ranges);
     CK(cudaGetLastError());
     CK(mark("resample"));
+    k_moments_fixup<<<cdiv(ctx->mom_ranges, 256), 256, 0, st>>>(ctx->ms, ctx->list, ctx->cell2list, ctx->mean,
+                                                                 ctx->cov, ctx->sc, ctx->mom_ranges);
+    CK(cudaGetLastError());
+    CK(mark("moments_fixup"));
     if (prof) {
         ctx->prof_nst = mark_i - 1;
         ctx->prof_steps += 1;
@@ -535,6 +531,22 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     const size_t nu = (size_t)ctx->nu, C = ctx->C, nb = (size_t)ctx->nu_b;
     const void* src = nullptr;
     size_t n = 0;
+    // the active-cell list (for OFFSETS / NB reconstruction)
+    auto read_list = [&](std::vector<uint32_t>& lc, std::vector<uint32_t>& ln, std::vector<uint32_t>& lst,
+                         std::vector<uint32_t>& lnb, uint32_t& Ln, uint64_t& n_in) -> int {
+        DevScalars s;
+        CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+        Ln = s.L;
+        n_in = s.n_in;
+        lc.resize(Ln); ln.resize(Ln); lst.resize(Ln); lnb.resize(Ln);
+        if (Ln) {
+            CK(cudaMemcpy(lc.data(), ctx->list.c, Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ln.data(), ctx->list.n, Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lst.data(), ctx->list.start, Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lnb.data(), ctx->list.nb, Ln * 4, cudaMemcpyDeviceToHost));
+        }
+        return DOG_OK;
+    };
     switch (what) {
     case DOG_DBG_PRED_X: src = ctx->px; n = nu * 4; break;
     case DOG_DBG_PRED_Y: src = ctx->py; n = nu * 4; break;
@@ -542,23 +554,41 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     case DOG_DBG_PRED_VY: src = ctx->pvy; n = nu * 4; break;
     case DOG_DBG_KEY: if (!dbg) return DOG_E_STATE; src = ctx->key_dbg; n = nu * 4; break;
     case DOG_DBG_PERM: src = ctx->perm; n = nu * 4; break;
-    case DOG_DBG_OFFSETS: src = ctx->offsets; n = (C + 1) * 4; break;
-    case DOG_DBG_RHO_P: src = ctx->rho_p; n = C * 4; break;
-    case DOG_DBG_RHO_B: if (!dbg) return DOG_E_STATE; src = ctx->rho_b; n = C * 4; break;
-    case DOG_DBG_RP: src = ctx->Rp; n = C * 8; break;
-    case DOG_DBG_RB: src = ctx->Rb; n = C * 8; break;
-    case DOG_DBG_BIRTH_X: src = ctx->bx; n = nb * 4; break;
-    case DOG_DBG_BIRTH_Y: src = ctx->by; n = nb * 4; break;
-    case DOG_DBG_BIRTH_VX: src = ctx->bvx; n = nb * 4; break;
-    case DOG_DBG_BIRTH_VY: src = ctx->bvy; n = nb * 4; break;
+    case DOG_DBG_RHO_P: if (!dbg) return DOG_E_STATE; src = ctx->dbg_rho_p; n = C * 4; break;
+    case DOG_DBG_RHO_B: if (!dbg) return DOG_E_STATE; src = ctx->dbg_rho_b; n = C * 4; break;
+    case DOG_DBG_RP: if (!dbg) return DOG_E_STATE; src = ctx->dbg_Rp; n = C * 8; break;
+    case DOG_DBG_RB: if (!dbg) return DOG_E_STATE; src = ctx->dbg_Rb; n = C * 8; break;
+    case DOG_DBG_BIRTH_X: if (!dbg) return DOG_E_STATE; src = ctx->bx; n = nb * 4; break;
+    case DOG_DBG_BIRTH_Y: if (!dbg) return DOG_E_STATE; src = ctx->by; n = nb * 4; break;
+    case DOG_DBG_BIRTH_VX: if (!dbg) return DOG_E_STATE; src = ctx->bvx; n = nb * 4; break;
+    case DOG_DBG_BIRTH_VY: if (!dbg) return DOG_E_STATE; src = ctx->bvy; n = nb * 4; break;
     case DOG_DBG_JOINT_IDX: if (!dbg) return DOG_E_STATE; src = ctx->jidx; n = nu * 4; break;
+    case DOG_DBG_OFFSETS: {
+        n = (C + 1) * 4;
+        if (bytes < n) return DOG_E_INVAL;
+        std::vector<uint32_t> lc, ln, lst, lnb;
+        uint32_t Ln; uint64_t n_in;
+        if (int r = read_list(lc, ln, lst, lnb, Ln, n_in)) return r;
+        uint32_t* d = (uint32_t*)host_dst;
+        uint32_t next = (uint32_t)n_in;   // first sorted slot of the next cell holding particles
+        int64_t li = (int64_t)Ln - 1;
+        d[C] = (uint32_t)n_in;
+        for (int64_t c = (int64_t)C - 1; c >= 0; --c) {
+            while (li >= 0 && lc[li] > (uint32_t)c) --li;
+            if (li >= 0 && lc[li] == (uint32_t)c && ln[li] > 0) next = lst[li];
+            d[c] = next;
+        }
+        return (int64_t)n;
+    }
     case DOG_DBG_NB: {
         n = C * 4;
         if (bytes < n) return DOG_E_INVAL;
-        std::vector<uint32_t> s(C + 1);
-        CK(cudaMemcpy(s.data(), ctx->sb, (C + 1) * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> lc, ln, lst, lnb;
+        uint32_t Ln; uint64_t n_in;
+        if (int r = read_list(lc, ln, lst, lnb, Ln, n_in)) return r;
         uint32_t* d = (uint32_t*)host_dst;
-        for (size_t c = 0; c < C; ++c) d[c] = s[c + 1] - s[c];
+        for (size_t c = 0; c < C; ++c) d[c] = 0;
+        for (uint32_t i = 0; i < Ln; ++i) d[lc[i]] = lnb[i];
         return (int64_t)n;
     }
     case DOG_DBG_SCALARS: {

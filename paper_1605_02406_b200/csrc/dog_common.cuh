@@ -14,9 +14,15 @@ struct DevScalars {
     uint32_t meas_bad;   // invalid measurement cells seen (sticky until reported)
     uint64_t W;          // total fixed-point joint weight (A-23)
     uint64_t A;          // total fixed-point born mass
-    uint64_t n_in;       // particles inside the grid after predict (= offsets[C])
+    uint64_t n_in;       // particles inside the grid after predict
     uint64_t s_total;    // birth slots allocated (nu_b or 0)
+    uint32_t L;          // active cells (n_c > 0 or R_b > 0) of the cycle
+    uint32_t pad;
 };
+
+constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
+constexpr float kMeasSumMax = 0x1.00001p+0f;    // 1 + 2^-20 (= 1.0f + 1e-6f rounded), A-27
+constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStMask = (1u << 30) - 1u;
 
 // Per-step scalars computed on the host in fp64 and rounded once to f32.
 struct StepArgs {
@@ -60,6 +66,86 @@ __device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p)
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+__device__ __forceinline__ ulonglong2 ld_relaxed128(const ulonglong2* p)
+{
+    ulonglong2 v;
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+}
+
+// Decoupled look-back (Merrill & Garland), warp-parallel: the calling WARP inspects 32 predecessor
+// tiles per step.  Packed variant: a tile aggregate < 2^30 shares one u32 with a 2-bit status.
+// Returns the exclusive prefix of `tile`; publishes the tile's inclusive prefix.  Call with all 32
+// lanes of one warp; every lane gets the result.
+__device__ __forceinline__ uint32_t lookback_u30(uint32_t* status, uint32_t tile, uint32_t total)
+{
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_relaxed(status, kStInc | total);
+        return 0;
+    }
+    if (lane == 0) st_relaxed(status + tile, kStAgg | total);
+    uint32_t excl = 0;
+    int j = (int)tile - 1;
+    while (true) {
+        const int p = j - lane;
+        const uint32_t s = p >= 0 ? ld_relaxed(status + p) : kStInc;
+        const uint32_t incm = __ballot_sync(0xffffffffu, (s & kStInc) != 0);
+        const int first = incm ? __ffs(incm) - 1 : 31;
+        const uint32_t zm = __ballot_sync(0xffffffffu, (s & ~kStMask) == 0);
+        if (zm & ((2u << first) - 1u)) continue;       // a needed predecessor has not published yet
+        excl += warp_sum(lane <= first ? (s & kStMask) : 0u);
+        if (incm) break;
+        j -= 32;
+    }
+    if (lane == 0) st_relaxed(status + tile, kStInc | (excl + total));
+    return excl;
+}
+
+// Pair-of-u64 variant: status flag (1 = aggregate, 2 = inclusive) + 16-byte value slots written
+// before the flag with release semantics.
+struct LookbackPair {
+    uint32_t* flag;
+    ulonglong2* agg;
+    ulonglong2* inc;
+};
+
+__device__ __forceinline__ ulonglong2 lookback_pair(LookbackPair s, uint32_t tile, ulonglong2 total)
+{
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) { s.inc[0] = total; st_release(s.flag, 2u); }
+        return make_ulonglong2(0ull, 0ull);
+    }
+    if (lane == 0) { s.agg[tile] = total; st_release(s.flag + tile, 1u); }
+    unsigned long long ex = 0, ey = 0;
+    int j = (int)tile - 1;
+    while (true) {
+        const int p = j - lane;
+        const uint32_t f = p >= 0 ? ld_acquire(s.flag + p) : 2u;
+        const uint32_t incm = __ballot_sync(0xffffffffu, f == 2u);
+        const int first = incm ? __ffs(incm) - 1 : 31;
+        const uint32_t zm = __ballot_sync(0xffffffffu, f == 0u);
+        if (zm & ((2u << first) - 1u)) continue;
+        ulonglong2 v = make_ulonglong2(0ull, 0ull);
+        if (lane <= first && p >= 0) v = ld_relaxed128(f == 2u ? s.inc + p : s.agg + p);
+        ex += warp_sum(v.x);
+        ey += warp_sum(v.y);
+        if (incm) break;
+        j -= 32;
+    }
+    if (lane == 0) { s.inc[tile] = make_ulonglong2(ex + total.x, ey + total.y); st_release(s.flag + tile, 2u); }
+    return make_ulonglong2(ex, ey);
 }
 
 // Warp inclusive scan (add) of T via shuffles.
