@@ -373,7 +373,8 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
 
     // 5a/7a. birth slots + joint CDF over the active list
     LookbackPair lb1{ctx->flag1, ctx->agg1, ctx->inc1}, lb2{ctx->flag2, ctx->agg2, ctx->inc2};
-    k_list_scan<<<ctx->list_tiles, kLsThreads, 0, st>>>(ctx->list, ctx->ctrs + 9, lb1, lb2, ctx->sc, fc, a.k);
+    k_list_scan<<<std::min<uint32_t>(ctx->list_tiles, 2u * 148u), kLsThreads, 0, st>>>(ctx->list, ctx->ctrs + 9, lb1,
+                                                                                      lb2, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
     CK(mark("list_scan"));
 

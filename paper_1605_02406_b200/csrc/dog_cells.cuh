@@ -75,12 +75,13 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     return o;
 }
 
-constexpr int kCellThreads = 256, kCellItems = 16, kCellTile = kCellThreads * kCellItems;
+constexpr int kCellThreads = 256, kCellItems = 4, kCellTile = kCellThreads * kCellItems;
 
 struct CellDebug { float* rho_p; float* rho_b; uint64_t* Rp; uint64_t* Rb; };
 
-// Striped tile: item i of thread t is cell tile*4096 + i*256 + t, so each warp touches 32
-// consecutive cells per item (coalesced) and one 32-bit word of the moments-valid bitmask.
+// Striped tile: item i of thread t is cell tile*1024 + i*256 + t, so each warp touches 32
+// consecutive cells per item (coalesced) and one 32-bit word of the moments-valid bitmask.  All loads
+// of a tile are issued before any dependent work; results stay in registers across the look-back.
 __global__ __launch_bounds__(kCellThreads) void k_cells(
     uint32_t* __restrict__ counts, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
@@ -100,58 +101,58 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
     const float w_pred = sc->w_pred;
     const uint32_t lt = (1u << lane) - 1u;
 
-    // pass A: readouts, moment bitmask, active flags
-    uint32_t actmask = 0;
-    uint64_t A_loc = 0;
-    uint32_t bad_loc = 0;
-#pragma unroll 4
+    uint32_t n[kCellItems], prev[kCellItems];
+    float mf[kCellItems];
+    float2 z[kCellItems];
+#pragma unroll
     for (int i = 0; i < kCellItems; ++i) {
         const uint32_t c = base + i * kCellThreads + tid;
         const bool valid = c < fc.C;
-        CellOut o{};
-        if (valid) o = cell_math(counts[c], m_free[c], meas[c], w_pred, alpha, fc);
-        const bool vnow = valid && o.n > 0 && o.rp > 0.0f && o.S > 0.0f;
-        const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
+        n[i] = valid ? counts[c] : 0u;
+        mf[i] = valid ? m_free[c] : 0.0f;
+        z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
         const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
-        const bool wvalid = (word << 5) < fc.C;
-        uint32_t prev = 0;
-        if (lane == 0 && wvalid) prev = mvalid[word];
-        prev = __shfl_sync(0xffffffffu, prev, 0);
+        prev[i] = (lane == 0 && (word << 5) < fc.C) ? mvalid[word] : 0u;
+    }
+    CellOut o[kCellItems];
+    uint32_t abal[kCellItems];
+    uint64_t A_loc = 0;
+    uint32_t bad_loc = 0;
+#pragma unroll
+    for (int i = 0; i < kCellItems; ++i) {
+        const uint32_t c = base + i * kCellThreads + tid;
+        const bool valid = c < fc.C;
+        o[i] = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
+        const bool vnow = valid && o[i].n > 0 && o[i].rp > 0.0f && o[i].S > 0.0f;
+        const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
+        const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
+        const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
         if (valid) {
-            occ[c] = o.mO;
-            free_out[c] = o.mF;
-            if (!vnow && ((prev >> lane) & 1u)) {   // moments were reported last cycle: clear (A-18)
+            occ[c] = o[i].mO;
+            free_out[c] = o[i].mF;
+            m_free[c] = o[i].mF;                    // Alg. 3 store_values
+            if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_predict
+            if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
                 mean[c] = make_float2(0.0f, 0.0f);
                 cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
             }
-            if (dbg.rho_p) { dbg.rho_p[c] = o.rp; dbg.rho_b[c] = o.rb; dbg.Rp[c] = o.Rp; dbg.Rb[c] = o.Rb; }
-            A_loc += o.Rb;
-            bad_loc += o.bad ? 1u : 0u;
+            if (dbg.rho_p) {
+                dbg.rho_p[c] = o[i].rp; dbg.rho_b[c] = o[i].rb; dbg.Rp[c] = o[i].Rp; dbg.Rb[c] = o[i].Rb;
+            }
+            A_loc += o[i].Rb;
+            bad_loc += o[i].bad ? 1u : 0u;
         }
-        if (lane == 0 && wvalid && bal != prev) mvalid[word] = bal;
-        const bool act = valid && (o.n > 0 || o.Rb > 0);
-        const uint32_t abal = __ballot_sync(0xffffffffu, act);
-        if (lane == 0) s_cnt[i][warp] = __popc(abal);
-        actmask |= (act ? 1u : 0u) << i;
+        if (lane == 0 && (word << 5) < fc.C && bal != pw) mvalid[word] = bal;
+        const bool act = valid && (o[i].n > 0 || o[i].Rb > 0);
+        abal[i] = __ballot_sync(0xffffffffu, act);
+        if (lane == 0) s_cnt[i][warp] = __popc(abal[i]);
     }
     __syncthreads();
-    // tile-local exclusive offsets in cell order (item-major, then warp) and the tile total
+    // tile-local exclusive offsets in cell order (item-major, then warp), tile total, look-back
     if (warp == 0) {
-        uint32_t v[4], sum = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {   // lane handles entries 4*lane .. 4*lane+3 of the 128
-            const int e = 4 * lane + q;
-            v[q] = s_cnt[e >> 3][e & 7];
-            sum += v[q];
-        }
-        const uint32_t incl = warp_incl_scan(sum, lane);
-        uint32_t run = incl - sum;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = 4 * lane + q;
-            s_cnt[e >> 3][e & 7] = run;
-            run += v[q];
-        }
+        const uint32_t v = lane < kCellItems * 8 ? s_cnt[lane >> 3][lane & 7] : 0u;
+        const uint32_t incl = warp_incl_scan(v, lane);
+        if (lane < kCellItems * 8) s_cnt[lane >> 3][lane & 7] = incl - v;
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t excl = lookback_u30(status, tile, total);
         if (lane == 0) {
@@ -161,22 +162,13 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
     }
     __syncthreads();
     const uint32_t texcl = s_excl;
-    // pass B: recompute (inputs are L1/L2-resident), commit m_F, reset counts, append active cells
-#pragma unroll 4
+#pragma unroll
     for (int i = 0; i < kCellItems; ++i) {
-        const uint32_t c = base + i * kCellThreads + tid;
-        const bool act = (actmask >> i) & 1u;
-        const uint32_t abal = __ballot_sync(0xffffffffu, act);
-        if (c < fc.C) {
-            const uint32_t n = counts[c];
-            const CellOut o = cell_math(n, m_free[c], meas[c], w_pred, alpha, fc);
-            m_free[c] = o.mF;                       // Alg. 3 store_values
-            if (n) counts[c] = 0u;                  // ready for the next cycle's k_predict
-            if (act) {
-                const uint32_t pos = texcl + s_cnt[i][warp] + __popc(abal & lt);
-                L.c[pos] = c; L.n[pos] = n; L.Rp[pos] = o.Rp; L.Rb[pos] = o.Rb; L.rho_p[pos] = o.rp;
-                cell2list[c] = pos;
-            }
+        if ((abal[i] >> lane) & 1u) {
+            const uint32_t c = base + i * kCellThreads + tid;
+            const uint32_t pos = texcl + s_cnt[i][warp] + __popc(abal[i] & lt);
+            L.c[pos] = c; L.n[pos] = o[i].n; L.Rp[pos] = o[i].Rp; L.Rb[pos] = o[i].Rb; L.rho_p[pos] = o[i].rp;
+            cell2list[c] = pos;
         }
     }
     // device totals (integers: order-independent)
@@ -208,6 +200,8 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_
 
 constexpr int kLsThreads = 256, kLsItems = 8, kLsTile = kLsThreads * kLsItems;
 
+// Persistent CTAs take list tiles in order from an atomic counter until the list is exhausted (the
+// list is short: ~1 % of the grid), so no launch depends on the device-resident list length.
 __global__ __launch_bounds__(kLsThreads) void k_list_scan(
     CellList L, uint32_t* __restrict__ tile_ctr, LookbackPair lb1, LookbackPair lb2,
     DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
@@ -216,86 +210,88 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(
     __shared__ uint32_t s_tile;
     __shared__ ulonglong2 s_ex;
     const int tid = threadIdx.x, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
     const uint32_t Ln = sc->L;
-    const uint32_t b0 = tile * kLsTile;
-    if (b0 >= Ln && tile > 0) return;           // beyond the list (no later tile waits on it)
     const uint64_t A = sc->A;
     const uint64_t nu_b = fc.nu_b;
-    const uint32_t b = b0 + tid * kLsItems;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        const uint32_t b0 = tile * kLsTile;
+        if (b0 >= Ln && tile > 0) return;       // tiles are taken in order: the rest lie beyond too
+        const uint32_t b = b0 + tid * kLsItems;
 
-    uint32_t n[kLsItems];
-    uint64_t Rb[kLsItems];
-    uint64_t ns = 0, rbs = 0;
+        uint32_t n[kLsItems];
+        uint64_t Rb[kLsItems], Rp[kLsItems];
+        uint64_t ns = 0, rbs = 0;
 #pragma unroll
-    for (int i = 0; i < kLsItems; ++i) {
-        const bool ok = b + i < Ln;
-        n[i] = ok ? L.n[b + i] : 0u;
-        Rb[i] = ok ? L.Rb[b + i] : 0ull;
-        ns += n[i];
-        rbs += Rb[i];
-    }
-    uint64_t tn, trb;
-    const uint64_t xn = block_excl_scan<uint64_t, kLsThreads / 32>(ns, s_a, tn);
-    const uint64_t xrb = block_excl_scan<uint64_t, kLsThreads / 32>(rbs, s_b, trb);
-    if (warp == 0) {
-        const ulonglong2 e = lookback_pair(lb1, tile, make_ulonglong2(tn, trb));
-        if (tid == 0) s_ex = e;
-    }
-    __syncthreads();
-    uint64_t start = s_ex.x + xn;
-    uint64_t Ax = s_ex.y + xrb;                 // A_{c-1}
-    uint64_t s_prev = slot_of(Ax, A, nu_b);
-    uint64_t J[kLsItems];
-    uint32_t nbv[kLsItems];
-    uint64_t js = 0;
-#pragma unroll
-    for (int i = 0; i < kLsItems; ++i) {
-        Ax += Rb[i];
-        const uint64_t s = Rb[i] ? slot_of(Ax, A, nu_b) : s_prev;
-        nbv[i] = (uint32_t)(s - s_prev);
-        if (b + i < Ln) {
-            const uint64_t rp = L.Rp[b + i];
-            L.start[b + i] = (uint32_t)start;
-            L.sb[b + i] = (uint32_t)s_prev;
-            L.nb[b + i] = nbv[i];
-            L.bp[b + i] = n[i] ? rp / n[i] : 0ull;
-            L.rp[b + i] = n[i] ? (uint32_t)(rp % n[i]) : 0u;
-            L.bb[b + i] = nbv[i] ? Rb[i] / nbv[i] : 0ull;
-            L.rb[b + i] = nbv[i] ? (uint32_t)(Rb[i] % nbv[i]) : 0u;
-            J[i] = rp + (nbv[i] ? Rb[i] : 0ull);
-        } else {
-            J[i] = 0;
+        for (int i = 0; i < kLsItems; ++i) {
+            const bool ok = b + i < Ln;
+            n[i] = ok ? L.n[b + i] : 0u;
+            Rb[i] = ok ? L.Rb[b + i] : 0ull;
+            Rp[i] = ok ? L.Rp[b + i] : 0ull;
+            ns += n[i];
+            rbs += Rb[i];
         }
-        start += n[i];
-        js += J[i];
-        s_prev = s;
-    }
-    uint64_t tj, dummy;
-    const uint64_t xj = block_excl_scan<uint64_t, kLsThreads / 32>(js, s_a, tj);
-    (void)dummy;
-    if (warp == 0) {
-        const ulonglong2 e = lookback_pair(lb2, tile, make_ulonglong2(tj, 0ull));
-        if (tid == 0) s_ex = e;
-    }
-    __syncthreads();
-    uint64_t run = s_ex.x + xj;
+        uint64_t tn, trb;
+        const uint64_t xn = block_excl_scan<uint64_t, kLsThreads / 32>(ns, s_a, tn);
+        const uint64_t xrb = block_excl_scan<uint64_t, kLsThreads / 32>(rbs, s_b, trb);
+        if (warp == 0) {
+            const ulonglong2 e = lookback_pair(lb1, tile, make_ulonglong2(tn, trb));
+            if (tid == 0) s_ex = e;
+        }
+        __syncthreads();
+        uint64_t start = s_ex.x + xn;
+        uint64_t Ax = s_ex.y + xrb;             // A_{c-1}
+        uint64_t s_prev = slot_of(Ax, A, nu_b);
+        uint64_t J[kLsItems];
+        uint64_t js = 0;
 #pragma unroll
-    for (int i = 0; i < kLsItems; ++i) {
-        if (b + i < Ln) L.P[b + i] = run;
-        run += J[i];
-    }
-    // the thread holding the list's last entry (or tile 0 of an empty list) publishes the totals
-    const bool last = Ln == 0 ? (tile == 0 && tid == 0) : (b <= Ln - 1 && Ln - 1 < b + kLsItems);
-    if (last) {
-        const uint64_t W = run;
-        sc->W = W;
-        sc->s_total = s_prev;
-        sc->n_in = start;
-        sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
-        sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
+        for (int i = 0; i < kLsItems; ++i) {
+            Ax += Rb[i];
+            const uint64_t s = Rb[i] ? slot_of(Ax, A, nu_b) : s_prev;
+            const uint32_t nbv = (uint32_t)(s - s_prev);
+            if (b + i < Ln) {
+                L.start[b + i] = (uint32_t)start;
+                L.sb[b + i] = (uint32_t)s_prev;
+                L.nb[b + i] = nbv;
+                L.bp[b + i] = n[i] ? Rp[i] / n[i] : 0ull;
+                L.rp[b + i] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
+                L.bb[b + i] = nbv ? Rb[i] / nbv : 0ull;
+                L.rb[b + i] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
+                J[i] = Rp[i] + (nbv ? Rb[i] : 0ull);
+            } else {
+                J[i] = 0;
+            }
+            start += n[i];
+            js += J[i];
+            s_prev = s;
+        }
+        uint64_t tj;
+        const uint64_t xj = block_excl_scan<uint64_t, kLsThreads / 32>(js, s_a, tj);
+        if (warp == 0) {
+            const ulonglong2 e = lookback_pair(lb2, tile, make_ulonglong2(tj, 0ull));
+            if (tid == 0) s_ex = e;
+        }
+        __syncthreads();
+        uint64_t run = s_ex.x + xj;
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            if (b + i < Ln) L.P[b + i] = run;
+            run += J[i];
+        }
+        // the thread holding the list's last entry (or tile 0 of an empty list) publishes the totals
+        const bool last = Ln == 0 ? (tile == 0 && tid == 0) : (b <= Ln - 1 && Ln - 1 < b + kLsItems);
+        if (last) {
+            const uint64_t W = run;
+            sc->W = W;
+            sc->s_total = s_prev;
+            sc->n_in = start;
+            sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
+            sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
+        }
+        __syncthreads();
     }
 }
 

@@ -23,14 +23,10 @@ struct MomPartial { double s[5]; };
 struct RsConst {
     uint64_t W;
     uint32_t U, nu;
-    double invE;     // 1 / (W 2^32)
-    u128 UW;         // U * W
+    double nu_over_W;  // nu / W  (fp64)
+    double U_frac;     // U 2^-32  (exact)
+    u128 UW;           // U * W
 };
-
-__device__ __forceinline__ double u128_to_double(u128 v)
-{
-    return __fma_rn((double)(uint64_t)(v >> 64), 0x1p64, (double)(uint64_t)v);
-}
 
 __device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t nu)
 {
@@ -38,22 +34,31 @@ __device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t n
     r.W = sc->W;
     r.U = sc->U;
     r.nu = nu;
-    r.invE = r.W ? 1.0 / ((double)r.W * 4294967296.0) : 0.0;
+    r.nu_over_W = r.W ? (double)nu / (double)r.W : 0.0;
+    r.U_frac = (double)r.U * 0x1p-32;
     r.UW = (u128)r.U * (u128)r.W;
     return r;
 }
 
-// F(X) = number of systematic targets t_i below X.
+// F(X) = number of systematic targets t_i below X = clamp(ceil(y), 0, nu) with
+// y = (X nu 2^32 - U W) / (W 2^32) = X nu / W - U 2^-32.  The fp64 estimate of y is within 2^-20
+// of y (|y| < 2^31, relative error < 2^-51); when it is further than 2^-16 from an integer its
+// ceiling is exact, otherwise the ceiling is settled with exact 128-bit products.
 __device__ __forceinline__ uint32_t fcount(uint64_t X, const RsConst& r)
 {
+    const double y = __fma_rn((double)X, r.nu_over_W, -r.U_frac);
+    if (y <= -0.5) return 0u;
+    if (y >= (double)r.nu) return r.nu;
+    const double cy = ceil(y);
+    const double d = cy - y;                       // in [0, 1)
+    if (d > 0x1p-16 && d < 1.0 - 0x1p-16) return (uint32_t)cy;
+    // exact: smallest q >= 0 with q W 2^32 >= X nu 2^32 - U W
     const u128 num0 = ((u128)X * (u128)r.nu) << 32;
     if (num0 <= r.UW) return 0u;
     const u128 num = num0 - r.UW;
     const u128 E = ((u128)r.W) << 32;
-    const double est = u128_to_double(num) * r.invE;
-    if (est >= (double)r.nu + 2.0) return r.nu;
-    uint64_t q = (uint64_t)est;
-    while ((u128)q * E < num) ++q;                     // smallest q with q E >= num
+    uint64_t q = (uint64_t)fmax(cy - 1.0, 0.0);
+    while ((u128)q * E < num) ++q;
     while (q > 0 && (u128)(q - 1) * E >= num) --q;
     return (uint32_t)(q < r.nu ? q : r.nu);
 }
