@@ -37,7 +37,7 @@ struct dog_ctx {
     int64_t k = 0;
     bool poisoned = false;
     size_t nu_cap = 0;          // particle arrays padded to the sort tile
-    uint32_t sort_tiles = 0, cell_tiles = 0, list_tiles = 0, mom_ranges = 0, pers_blocks = 0;
+    uint32_t sort_tiles = 0, cell_blocks = 0, cell_chunk = 0, mom_ranges = 0, pers_blocks = 0;
 
     // state S_k and predicted state (SoA, f32)
     float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
@@ -52,8 +52,8 @@ struct dog_ctx {
     float* cov = nullptr;
     uint32_t* mvalid = nullptr;                   // moments-reported bitmask
     CellList list{};
+    BlockTotals bt{};
     uint32_t* cell2list = nullptr;
-    ulonglong2 *agg1 = nullptr, *inc1 = nullptr, *agg2 = nullptr, *inc2 = nullptr;
     // debug-only arrays
     float *dbg_rho_p = nullptr, *dbg_rho_b = nullptr;
     uint64_t *dbg_Rp = nullptr, *dbg_Rb = nullptr;
@@ -65,8 +65,7 @@ struct dog_ctx {
     // zeroed once per cycle (one memset): radix histograms, tile counters, look-back status
     uint8_t* zero = nullptr;
     size_t zero_bytes = 0;
-    uint32_t *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr, *st_cells = nullptr, *flag1 = nullptr,
-             *flag2 = nullptr;
+    uint32_t *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr;
     // end-to-end staging
     float* meas_dev = nullptr;
     // profiling: events[step][stage boundary]
@@ -215,8 +214,13 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->npass = (bits + 7) / 8;
     ctx->nu_cap = round_up((size_t)n_particles, kRsTile);
     ctx->sort_tiles = cdiv(n_particles, kRsTile);
-    ctx->cell_tiles = cdiv(C, kCellTile);
-    ctx->list_tiles = cdiv(C, kLsTile);
+    {   // cell chunks: ~4 blocks per SM, each a multiple of one 1024-cell iteration
+        uint32_t chunk = cdiv(cdiv(C, 4u * 148u), kCellIter) * kCellIter;
+        uint32_t nblk = cdiv(C, chunk);
+        while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(C, chunk); }
+        ctx->cell_chunk = chunk;
+        ctx->cell_blocks = nblk;
+    }
     ctx->mom_ranges = cdiv(n_particles, kMomRange);
     ctx->pers_blocks = cdiv(ctx->mom_ranges, 8);
     const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
@@ -237,20 +241,20 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs);
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
     AL(ctx->mvalid, Cs / 32 + 1);
-    AL(ctx->list.c, Cs); AL(ctx->list.n, Cs); AL(ctx->list.Rp, Cs); AL(ctx->list.Rb, Cs);
-    AL(ctx->list.rho_p, Cs); AL(ctx->list.start, Cs); AL(ctx->list.sb, Cs); AL(ctx->list.nb, Cs);
-    AL(ctx->list.P, Cs); AL(ctx->list.bp, Cs); AL(ctx->list.rp, Cs); AL(ctx->list.bb, Cs);
-    AL(ctx->list.rb, Cs);
+    const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
+    AL(ctx->list.c, LC); AL(ctx->list.n, LC); AL(ctx->list.Rp, LC); AL(ctx->list.Rb, LC);
+    AL(ctx->list.rho_p, LC); AL(ctx->list.start, LC); AL(ctx->list.sb, LC); AL(ctx->list.nb, LC);
+    AL(ctx->list.Pl, LC); AL(ctx->list.bp, LC); AL(ctx->list.rp, LC); AL(ctx->list.bb, LC);
+    AL(ctx->list.rb, LC);
     AL(ctx->cell2list, Cs);
-    AL(ctx->agg1, ctx->list_tiles); AL(ctx->inc1, ctx->list_tiles);
-    AL(ctx->agg2, ctx->list_tiles); AL(ctx->inc2, ctx->list_tiles);
+    AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n, ctx->cell_blocks); AL(ctx->bt.rb, ctx->cell_blocks);
+    AL(ctx->bt.J, ctx->cell_blocks); AL(ctx->bt.s0, ctx->cell_blocks); AL(ctx->bt.P0, ctx->cell_blocks);
     AL(ctx->ms.head, ctx->mom_ranges); AL(ctx->ms.tail, ctx->mom_ranges);
     AL(ctx->ms.tail_cell, ctx->mom_ranges); AL(ctx->ms.head_ends, ctx->mom_ranges);
     AL(ctx->sc, 1);
     // zero region layout (u32 words)
-    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16, w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256,
-                 w_cells = ctx->cell_tiles, w_f1 = ctx->list_tiles, w_f2 = ctx->list_tiles;
-    ctx->zero_bytes = 4 * (w_rhist + w_ctrs + w_sort + w_cells + w_f1 + w_f2);
+    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16, w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256;
+    ctx->zero_bytes = 4 * (w_rhist + w_ctrs + w_sort);
     AL(ctx->zero, ctx->zero_bytes);
 #undef AL
     if (rc != DOG_OK) {
@@ -262,9 +266,6 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->rhist = z; z += w_rhist;
     ctx->ctrs = z; z += w_ctrs;
     ctx->st_sort = z; z += w_sort;
-    ctx->st_cells = z; z += w_cells;
-    ctx->flag1 = z; z += w_f1;
-    ctx->flag2 = z; z += w_f2;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
     std::vector<float> sent(N, kSentinelPos);
@@ -306,7 +307,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 5 + ctx->npass;   // predict, sort passes, cells, list scan, resample, moments fixup
+    return 6 + ctx->npass;   // predict, sort passes, cells, list scan + finish, resample, moments fixup
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -364,17 +365,18 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
 
     // 3. cells: DS predict/update, birth split, fixed point, active-cell list
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
-    k_cells<<<ctx->cell_tiles, kCellThreads, 0, st>>>(ctx->counts, ctx->m_free, (const float2*)meas, ctx->occ,
-                                                      ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->list,
-                                                      ctx->cell2list, ctx->ctrs + 8, ctx->st_cells, ctx->sc, fc,
-                                                      a.alpha);
+    k_cells<<<ctx->cell_blocks, kCellThreads, 0, st>>>(ctx->counts, ctx->m_free, (const float2*)meas, ctx->occ,
+                                                       ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->list,
+                                                       ctx->cell2list, ctx->bt, ctx->cell_chunk, ctx->sc, fc,
+                                                       a.alpha);
     CK(cudaGetLastError());
     CK(mark("cells"));
 
     // 5a/7a. birth slots + joint CDF over the active list
-    LookbackPair lb1{ctx->flag1, ctx->agg1, ctx->inc1}, lb2{ctx->flag2, ctx->agg2, ctx->inc2};
-    k_list_scan<<<std::min<uint32_t>(ctx->list_tiles, 2u * 148u), kLsThreads, 0, st>>>(ctx->list, ctx->ctrs + 9, lb1,
-                                                                                      lb2, ctx->sc, fc, a.k);
+    k_list_scan<<<ctx->cell_blocks, kLsThreads, 0, st>>>(ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
+                                                        ctx->sc, fc);
+    CK(cudaGetLastError());
+    k_list_finish<<<1, 1024, 0, st>>>(ctx->bt, ctx->cell_blocks, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
     CK(mark("list_scan"));
 
@@ -383,10 +385,9 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
     BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
     const uint32_t birth_blocks = cdiv(ctx->nu_b, 256);
-    k_resample<<<ctx->pers_blocks + birth_blocks, 256, 0, st>>>(ctx->skeys, ctx->perm, pr, ctx->list,
-                                                                ctx->cell2list, ns, bd, ctx->mean, ctx->cov,
-                                                                ctx->ms, ctx->sc, fc, a.k, ctx->pers_blocks,
-                                                                ctx->mom_ranges);
+    k_resample<<<ctx->pers_blocks + birth_blocks, 256, 0, st>>>(
+        ctx->skeys, ctx->perm, pr, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, ns, bd,
+        ctx->mean, ctx->cov, ctx->ms, ctx->sc, fc, a.k, ctx->pers_blocks, ctx->mom_ranges);
     CK(cudaGetLastError());
     CK(mark("resample"));
     k_moments_fixup<<<cdiv(ctx->mom_ranges, 256), 256, 0, st>>>(ctx->ms, ctx->list, ctx->cell2list, ctx->mean,
@@ -533,19 +534,25 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     const void* src = nullptr;
     size_t n = 0;
     // the active-cell list (for OFFSETS / NB reconstruction)
+    // the active-cell list, chunk by chunk (for OFFSETS / NB reconstruction)
     auto read_list = [&](std::vector<uint32_t>& lc, std::vector<uint32_t>& ln, std::vector<uint32_t>& lst,
                          std::vector<uint32_t>& lnb, uint32_t& Ln, uint64_t& n_in) -> int {
         DevScalars s;
         CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
-        Ln = s.L;
         n_in = s.n_in;
-        lc.resize(Ln); ln.resize(Ln); lst.resize(Ln); lnb.resize(Ln);
-        if (Ln) {
-            CK(cudaMemcpy(lc.data(), ctx->list.c, Ln * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(ln.data(), ctx->list.n, Ln * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(lst.data(), ctx->list.start, Ln * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(lnb.data(), ctx->list.nb, Ln * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> cnt(ctx->cell_blocks);
+        CK(cudaMemcpy(cnt.data(), ctx->bt.cnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
+        lc.clear(); ln.clear(); lst.clear(); lnb.clear();
+        for (uint32_t b = 0; b < ctx->cell_blocks; ++b) {
+            const size_t m = cnt[b], o = (size_t)b * ctx->cell_chunk, at = lc.size();
+            if (!m) continue;
+            lc.resize(at + m); ln.resize(at + m); lst.resize(at + m); lnb.resize(at + m);
+            CK(cudaMemcpy(lc.data() + at, ctx->list.c + o, m * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ln.data() + at, ctx->list.n + o, m * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lst.data() + at, ctx->list.start + o, m * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lnb.data() + at, ctx->list.nb + o, m * 4, cudaMemcpyDeviceToHost));
         }
+        Ln = (uint32_t)lc.size();
         return DOG_OK;
     };
     switch (what) {

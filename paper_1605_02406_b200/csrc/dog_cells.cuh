@@ -4,13 +4,15 @@
 // (Eq. 61, exact), m_p = min(S_c, occ_max) (Eq. 17), m_Fp = min(alpha m_F, 1 - m_p) (Eq. 62),
 // Dempster update (Eq. 63), birth split (Eqs. 67-68), fixed-point masses (A-23) and the readouts.
 // Cells holding particles or receiving born mass ("active" cells, typically ~1 % of the grid) are
-// appended, in cell order, to a compact list through a decoupled look-back; every later stage works
-// on that list instead of the whole grid.
+// staged, in cell order, in their block's segment of a list; every later stage works on that list.
+// Each block owns a contiguous chunk of cells, so the list is ordered by (block, position) and block
+// prefixes are a scan over a few hundred block totals -- no grid-wide look-back chain.
 //
-// k_list_scan: one pass over the active list: prefix of n_c (first sorted slot of each cell), prefix
-// of R_b (born-mass CDF) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A)) (A-15), the
-// gated joint mass J_c = R_p + [n_b > 0] R_b and its exclusive prefix P_c (the joint CDF in
-// cell-interleaved order, A-25), the per-cell even-split parameters, W, w_bar (Eq. 57) and U.
+// k_list_scan (one block per cell chunk): prefix of n_c (first sorted slot of each cell), prefix of
+// R_b (born-mass CDF) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A)) (A-15), the gated
+// joint mass J_c = R_p + [n_b > 0] R_b and its block-local exclusive prefix, the even-split
+// parameters of each cell; k_list_finish scans the block totals of J -> joint CDF offsets, W, w_bar
+// (Eq. 57) and U.  The joint CDF is in cell-interleaved order (A-25).
 #pragma once
 #include <cstdint>
 #include "dog_common.cuh"
@@ -18,20 +20,29 @@
 
 namespace dog {
 
-struct CellList {           // SoA, capacity C
+struct CellList {           // SoA staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
     uint32_t* c;            // cell index
     uint32_t* n;            // persistent particles n_c
     uint64_t* Rp;           // floor(rho_p 2^40) (0 if n_c = 0)
     uint64_t* Rb;           // floor(rho_b 2^40) if m_zO > 0 else 0
     float* rho_p;           // f32 rho_p (moments denominator)
     uint32_t* start;        // first cell-sorted slot of the cell          (k_list_scan)
-    uint32_t* sb;           // first birth slot of the cell                 (k_list_scan)
+    uint32_t* sb;           // first birth slot of the cell (global)        (k_list_scan)
     uint32_t* nb;           // birth slots of the cell                      (k_list_scan)
-    uint64_t* P;            // exclusive joint prefix P_c                   (k_list_scan)
+    uint64_t* Pl;           // block-local exclusive joint prefix           (k_list_scan)
     uint64_t* bp;           // R_p / n_c        (even split of R_p)         (k_list_scan)
     uint32_t* rp;           // R_p mod n_c
     uint64_t* bb;           // R_b / n_b
     uint32_t* rb;           // R_b mod n_b
+};
+
+struct BlockTotals {        // one entry per cell chunk
+    uint32_t* cnt;          // active cells staged by the block                (k_cells)
+    uint64_t* n;            // sum of n_c over them                             (k_cells)
+    uint64_t* rb;           // sum of R_b over them                             (k_cells)
+    uint64_t* J;            // sum of J over them                               (k_list_scan)
+    uint32_t* s0;           // first birth slot of the block (global)           (k_list_scan)
+    uint64_t* P0;           // exclusive joint prefix of the block              (k_list_finish)
 };
 
 __device__ __forceinline__ uint64_t fx40(float m)
@@ -75,110 +86,122 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     return o;
 }
 
-constexpr int kCellThreads = 256, kCellItems = 4, kCellTile = kCellThreads * kCellItems;
+constexpr int kCellThreads = 256, kCellItems = 4, kCellIter = kCellThreads * kCellItems;   // 1024 cells
 
 struct CellDebug { float* rho_p; float* rho_b; uint64_t* Rp; uint64_t* Rb; };
 
-// Striped tile: item i of thread t is cell tile*1024 + i*256 + t, so each warp touches 32
-// consecutive cells per item (coalesced) and one 32-bit word of the moments-valid bitmask.  All loads
-// of a tile are issued before any dependent work; results stay in registers across the look-back.
+// Block b owns cells [b chunk, (b+1) chunk), processed 1024 at a time; item i of thread t in an
+// iteration is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid
+// bitmask).  The next iteration's inputs are loaded before the current one is processed.
 __global__ __launch_bounds__(kCellThreads) void k_cells(
     uint32_t* __restrict__ counts, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, CellList L, uint32_t* __restrict__ cell2list,
-    uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ status, DevScalars* __restrict__ sc,
-    FilterConst fc, float alpha)
+    BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
 {
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
-    __shared__ uint32_t s_tile, s_excl;
-    __shared__ uint64_t s_A[8];
+    __shared__ uint32_t s_run;
+    __shared__ uint64_t s_A[8], s_N[8];
     __shared__ uint32_t s_bad[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint32_t base = tile * kCellTile;
-    const float w_pred = sc->w_pred;
     const uint32_t lt = (1u << lane) - 1u;
+    const float w_pred = sc->w_pred;
+    const uint32_t c0 = blockIdx.x * chunk;
+    const uint32_t c1 = min(c0 + chunk, fc.C);
+    const uint32_t lbase = blockIdx.x * chunk;
+    if (tid == 0) s_run = 0;
 
     uint32_t n[kCellItems], prev[kCellItems];
     float mf[kCellItems];
     float2 z[kCellItems];
+    auto load = [&](uint32_t base) {
 #pragma unroll
-    for (int i = 0; i < kCellItems; ++i) {
-        const uint32_t c = base + i * kCellThreads + tid;
-        const bool valid = c < fc.C;
-        n[i] = valid ? counts[c] : 0u;
-        mf[i] = valid ? m_free[c] : 0.0f;
-        z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
-        const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
-        prev[i] = (lane == 0 && (word << 5) < fc.C) ? mvalid[word] : 0u;
-    }
-    CellOut o[kCellItems];
-    uint32_t abal[kCellItems];
-    uint64_t A_loc = 0;
-    uint32_t bad_loc = 0;
-#pragma unroll
-    for (int i = 0; i < kCellItems; ++i) {
-        const uint32_t c = base + i * kCellThreads + tid;
-        const bool valid = c < fc.C;
-        o[i] = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
-        const bool vnow = valid && o[i].n > 0 && o[i].rp > 0.0f && o[i].S > 0.0f;
-        const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
-        const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
-        const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
-        if (valid) {
-            occ[c] = o[i].mO;
-            free_out[c] = o[i].mF;
-            m_free[c] = o[i].mF;                    // Alg. 3 store_values
-            if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_predict
-            if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
-                mean[c] = make_float2(0.0f, 0.0f);
-                cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
-            }
-            if (dbg.rho_p) {
-                dbg.rho_p[c] = o[i].rp; dbg.rho_b[c] = o[i].rb; dbg.Rp[c] = o[i].Rp; dbg.Rb[c] = o[i].Rb;
-            }
-            A_loc += o[i].Rb;
-            bad_loc += o[i].bad ? 1u : 0u;
-        }
-        if (lane == 0 && (word << 5) < fc.C && bal != pw) mvalid[word] = bal;
-        const bool act = valid && (o[i].n > 0 || o[i].Rb > 0);
-        abal[i] = __ballot_sync(0xffffffffu, act);
-        if (lane == 0) s_cnt[i][warp] = __popc(abal[i]);
-    }
-    __syncthreads();
-    // tile-local exclusive offsets in cell order (item-major, then warp), tile total, look-back
-    if (warp == 0) {
-        const uint32_t v = lane < kCellItems * 8 ? s_cnt[lane >> 3][lane & 7] : 0u;
-        const uint32_t incl = warp_incl_scan(v, lane);
-        if (lane < kCellItems * 8) s_cnt[lane >> 3][lane & 7] = incl - v;
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t excl = lookback_u30(status, tile, total);
-        if (lane == 0) {
-            s_excl = excl;
-            if (tile == gridDim.x - 1) sc->L = excl + total;
-        }
-    }
-    __syncthreads();
-    const uint32_t texcl = s_excl;
-#pragma unroll
-    for (int i = 0; i < kCellItems; ++i) {
-        if ((abal[i] >> lane) & 1u) {
+        for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
-            const uint32_t pos = texcl + s_cnt[i][warp] + __popc(abal[i] & lt);
-            L.c[pos] = c; L.n[pos] = o[i].n; L.Rp[pos] = o[i].Rp; L.Rb[pos] = o[i].Rb; L.rho_p[pos] = o[i].rp;
-            cell2list[c] = pos;
+            const bool valid = c < c1;
+            n[i] = valid ? counts[c] : 0u;
+            mf[i] = valid ? m_free[c] : 0.0f;
+            z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
+            const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
+            prev[i] = (lane == 0 && (word << 5) < c1) ? mvalid[word] : 0u;
         }
+    };
+    uint64_t A_loc = 0, N_loc = 0;
+    uint32_t bad_loc = 0;
+    if (c0 < c1) load(c0);
+    for (uint32_t base = c0; base < c1; base += kCellIter) {
+        uint32_t cn[kCellItems], cp[kCellItems];
+        float cmf[kCellItems];
+        float2 cz[kCellItems];
+#pragma unroll
+        for (int i = 0; i < kCellItems; ++i) { cn[i] = n[i]; cp[i] = prev[i]; cmf[i] = mf[i]; cz[i] = z[i]; }
+        if (base + kCellIter < c1) load(base + kCellIter);     // prefetch the next iteration
+
+        CellOut o[kCellItems];
+        uint32_t abal[kCellItems];
+#pragma unroll
+        for (int i = 0; i < kCellItems; ++i) {
+            const uint32_t c = base + i * kCellThreads + tid;
+            const bool valid = c < c1;
+            o[i] = cell_math(cn[i], cmf[i], cz[i], w_pred, alpha, fc);
+            const bool vnow = valid && o[i].n > 0 && o[i].rp > 0.0f && o[i].S > 0.0f;
+            const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
+            const uint32_t pw = __shfl_sync(0xffffffffu, cp[i], 0);
+            const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
+            if (valid) {
+                occ[c] = o[i].mO;
+                free_out[c] = o[i].mF;
+                m_free[c] = o[i].mF;                    // Alg. 3 store_values
+                if (cn[i]) counts[c] = 0u;              // ready for the next cycle's k_predict
+                if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
+                    mean[c] = make_float2(0.0f, 0.0f);
+                    cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
+                }
+                if (dbg.rho_p) {
+                    dbg.rho_p[c] = o[i].rp; dbg.rho_b[c] = o[i].rb; dbg.Rp[c] = o[i].Rp; dbg.Rb[c] = o[i].Rb;
+                }
+                bad_loc += o[i].bad ? 1u : 0u;
+            }
+            if (lane == 0 && (word << 5) < c1 && bal != pw) mvalid[word] = bal;
+            const bool act = valid && (o[i].n > 0 || o[i].Rb > 0);
+            abal[i] = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) s_cnt[i][warp] = __popc(abal[i]);
+        }
+        __syncthreads();
+        if (warp == 0) {   // exclusive offsets in cell order (item-major, then warp) + running total
+            const uint32_t v = lane < kCellItems * 8 ? s_cnt[lane >> 3][lane & 7] : 0u;
+            const uint32_t incl = warp_incl_scan(v, lane);
+            const uint32_t run = s_run;
+            if (lane < kCellItems * 8) s_cnt[lane >> 3][lane & 7] = run + incl - v;
+            __syncwarp();
+            if (lane == 31) s_run = run + incl;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kCellItems; ++i) {
+            if ((abal[i] >> lane) & 1u) {
+                const uint32_t c = base + i * kCellThreads + tid;
+                const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
+                L.c[li] = c; L.n[li] = o[i].n; L.Rp[li] = o[i].Rp; L.Rb[li] = o[i].Rb; L.rho_p[li] = o[i].rp;
+                cell2list[c] = li;
+                A_loc += o[i].Rb;
+                N_loc += o[i].n;
+            }
+        }
+        __syncthreads();
     }
-    // device totals (integers: order-independent)
+    // block totals (integers: order-independent)
     A_loc = warp_sum(A_loc);
+    N_loc = warp_sum(N_loc);
     bad_loc = warp_sum(bad_loc);
-    if (lane == 0) { s_A[warp] = A_loc; s_bad[warp] = bad_loc; }
+    if (lane == 0) { s_A[warp] = A_loc; s_N[warp] = N_loc; s_bad[warp] = bad_loc; }
     __syncthreads();
     if (tid == 0) {
-        uint64_t A = 0; uint32_t b = 0;
-        for (int w = 0; w < kCellThreads / 32; ++w) { A += s_A[w]; b += s_bad[w]; }
+        uint64_t A = 0, N = 0; uint32_t b = 0;
+        for (int w = 0; w < kCellThreads / 32; ++w) { A += s_A[w]; N += s_N[w]; b += s_bad[w]; }
+        bt.cnt[blockIdx.x] = s_run;
+        bt.n[blockIdx.x] = N;
+        bt.rb[blockIdx.x] = A;
         if (A) atomicAdd((unsigned long long*)&sc->A, (unsigned long long)A);
         if (b) atomicAdd(&sc->meas_bad, b);
     }
@@ -199,51 +222,59 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_
 }
 
 constexpr int kLsThreads = 256, kLsItems = 8, kLsTile = kLsThreads * kLsItems;
+constexpr int kMaxCellBlocks = 2048;
 
-// Persistent CTAs take list tiles in order from an atomic counter until the list is exhausted (the
-// list is short: ~1 % of the grid), so no launch depends on the device-resident list length.
-__global__ __launch_bounds__(kLsThreads) void k_list_scan(
-    CellList L, uint32_t* __restrict__ tile_ctr, LookbackPair lb1, LookbackPair lb2,
-    DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+// Exclusive prefix of the first `b` block totals, computed redundantly by every block (nblk is a few
+// hundred).  Returns the sums over blocks [0, b) of (n, rb) and the grand total of rb.
+__device__ __forceinline__ void block_prefix(const BlockTotals& bt, uint32_t nblk, uint32_t b, uint64_t& n0,
+                                             uint64_t& rb0)
+{
+    __shared__ uint64_t s_n[kLsThreads / 32], s_r[kLsThreads / 32];
+    uint64_t pn = 0, pr = 0;
+    for (uint32_t i = threadIdx.x; i < b; i += blockDim.x) { pn += bt.n[i]; pr += bt.rb[i]; }
+    pn = warp_sum(pn);
+    pr = warp_sum(pr);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) { s_n[warp] = pn; s_r[warp] = pr; }
+    __syncthreads();
+    n0 = 0; rb0 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { n0 += s_n[w]; rb0 += s_r[w]; }
+    __syncthreads();
+}
+
+__global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
+                                                          DevScalars* __restrict__ sc, FilterConst fc)
 {
     __shared__ uint64_t s_a[kLsThreads / 32 + 1], s_b[kLsThreads / 32 + 1];
-    __shared__ uint32_t s_tile;
-    __shared__ ulonglong2 s_ex;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t Ln = sc->L;
+    const int tid = threadIdx.x;
+    const uint32_t blk = blockIdx.x;
     const uint64_t A = sc->A;
     const uint64_t nu_b = fc.nu_b;
-    while (true) {
-        if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        __syncthreads();
-        const uint32_t b0 = tile * kLsTile;
-        if (b0 >= Ln && tile > 0) return;       // tiles are taken in order: the rest lie beyond too
-        const uint32_t b = b0 + tid * kLsItems;
-
+    uint64_t start0, A0;
+    block_prefix(bt, nblk, blk, start0, A0);
+    const uint32_t cnt = bt.cnt[blk];
+    const uint32_t lbase = blk * chunk;
+    if (tid == 0) bt.s0[blk] = (uint32_t)slot_of(A0, A, nu_b);
+    uint64_t J0 = 0;                          // block-local joint prefix
+    for (uint32_t t0 = 0; t0 < cnt; t0 += kLsTile) {
+        const uint32_t b = t0 + tid * kLsItems;
         uint32_t n[kLsItems];
         uint64_t Rb[kLsItems], Rp[kLsItems];
         uint64_t ns = 0, rbs = 0;
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
-            const bool ok = b + i < Ln;
-            n[i] = ok ? L.n[b + i] : 0u;
-            Rb[i] = ok ? L.Rb[b + i] : 0ull;
-            Rp[i] = ok ? L.Rp[b + i] : 0ull;
+            const bool ok = b + i < cnt;
+            n[i] = ok ? L.n[lbase + b + i] : 0u;
+            Rb[i] = ok ? L.Rb[lbase + b + i] : 0ull;
+            Rp[i] = ok ? L.Rp[lbase + b + i] : 0ull;
             ns += n[i];
             rbs += Rb[i];
         }
         uint64_t tn, trb;
         const uint64_t xn = block_excl_scan<uint64_t, kLsThreads / 32>(ns, s_a, tn);
         const uint64_t xrb = block_excl_scan<uint64_t, kLsThreads / 32>(rbs, s_b, trb);
-        if (warp == 0) {
-            const ulonglong2 e = lookback_pair(lb1, tile, make_ulonglong2(tn, trb));
-            if (tid == 0) s_ex = e;
-        }
-        __syncthreads();
-        uint64_t start = s_ex.x + xn;
-        uint64_t Ax = s_ex.y + xrb;             // A_{c-1}
+        uint64_t start = start0 + xn;
+        uint64_t Ax = A0 + xrb;               // A_{c-1}
         uint64_t s_prev = slot_of(Ax, A, nu_b);
         uint64_t J[kLsItems];
         uint64_t js = 0;
@@ -252,14 +283,15 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(
             Ax += Rb[i];
             const uint64_t s = Rb[i] ? slot_of(Ax, A, nu_b) : s_prev;
             const uint32_t nbv = (uint32_t)(s - s_prev);
-            if (b + i < Ln) {
-                L.start[b + i] = (uint32_t)start;
-                L.sb[b + i] = (uint32_t)s_prev;
-                L.nb[b + i] = nbv;
-                L.bp[b + i] = n[i] ? Rp[i] / n[i] : 0ull;
-                L.rp[b + i] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
-                L.bb[b + i] = nbv ? Rb[i] / nbv : 0ull;
-                L.rb[b + i] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
+            if (b + i < cnt) {
+                const uint32_t li = lbase + b + i;
+                L.start[li] = (uint32_t)start;
+                L.sb[li] = (uint32_t)s_prev;
+                L.nb[li] = nbv;
+                L.bp[li] = n[i] ? Rp[i] / n[i] : 0ull;
+                L.rp[li] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
+                L.bb[li] = nbv ? Rb[i] / nbv : 0ull;
+                L.rb[li] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
                 J[i] = Rp[i] + (nbv ? Rb[i] : 0ull);
             } else {
                 J[i] = 0;
@@ -270,28 +302,45 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(
         }
         uint64_t tj;
         const uint64_t xj = block_excl_scan<uint64_t, kLsThreads / 32>(js, s_a, tj);
-        if (warp == 0) {
-            const ulonglong2 e = lookback_pair(lb2, tile, make_ulonglong2(tj, 0ull));
-            if (tid == 0) s_ex = e;
-        }
-        __syncthreads();
-        uint64_t run = s_ex.x + xj;
+        uint64_t run = J0 + xj;
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
-            if (b + i < Ln) L.P[b + i] = run;
+            if (b + i < cnt) L.Pl[lbase + b + i] = run;
             run += J[i];
         }
-        // the thread holding the list's last entry (or tile 0 of an empty list) publishes the totals
-        const bool last = Ln == 0 ? (tile == 0 && tid == 0) : (b <= Ln - 1 && Ln - 1 < b + kLsItems);
-        if (last) {
-            const uint64_t W = run;
-            sc->W = W;
-            sc->s_total = s_prev;
-            sc->n_in = start;
-            sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
-            sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
-        }
-        __syncthreads();
+        start0 += tn;
+        A0 += trb;
+        J0 += tj;
+    }
+    if (tid == 0) bt.J[blk] = J0;
+}
+
+// One block: joint-CDF offsets of the cell chunks, totals W and n_in, w_bar (Eq. 57), U (A-24).
+__global__ __launch_bounds__(1024) void k_list_finish(BlockTotals bt, uint32_t nblk, DevScalars* __restrict__ sc,
+                                                      FilterConst fc, int64_t k)
+{
+    __shared__ uint64_t s_w[33];
+    const int tid = threadIdx.x;
+    uint64_t carry = 0, ncarry = 0;
+    for (uint32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
+        const uint32_t b = b0 + tid;
+        const uint64_t v = b < nblk ? bt.J[b] : 0ull;
+        const uint64_t nv = b < nblk ? bt.n[b] : 0ull;
+        uint64_t tot;
+        const uint64_t x = block_excl_scan<uint64_t, 32>(v, s_w, tot);
+        if (b < nblk) bt.P0[b] = carry + x;
+        carry += tot;
+        uint64_t ntot;
+        block_excl_scan<uint64_t, 32>(nv, s_w, ntot);
+        ncarry += ntot;
+    }
+    if (tid == 0) {
+        const uint64_t W = carry;
+        sc->W = W;
+        sc->n_in = ncarry;
+        sc->s_total = sc->A ? (uint64_t)fc.nu_b : 0ull;
+        sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
+        sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
     }
 }
 

@@ -84,10 +84,10 @@ struct BirthDebug { float *x, *y, *vx, *vy; };
 struct MomScratch { MomPartial* head; MomPartial* tail; uint32_t* tail_cell; uint8_t* head_ends; };
 
 __global__ __launch_bounds__(256) void k_resample(
-    const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ perm, Pred pr, CellList L,
-    const uint32_t* __restrict__ cell2list, NextState out, BirthDebug bdbg, float2* __restrict__ mean,
-    float* __restrict__ cov, MomScratch ms, const DevScalars* __restrict__ sc, FilterConst fc, int64_t k,
-    uint32_t pers_blocks, uint32_t nranges)
+    const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ perm, Pred pr, CellList L, BlockTotals bt,
+    uint32_t nblk, uint32_t chunk, const uint32_t* __restrict__ cell2list, NextState out, BirthDebug bdbg,
+    float2* __restrict__ mean, float* __restrict__ cov, MomScratch ms, const DevScalars* __restrict__ sc,
+    FilterConst fc, int64_t k, uint32_t pers_blocks, uint32_t nranges)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu);
@@ -102,7 +102,12 @@ __global__ __launch_bounds__(256) void k_resample(
         // ---------------- birth slots (Alg. 5): state from the slot's Philox draw, then copies
         const uint32_t s = (blockIdx.x - pers_blocks) * blockDim.x + tid;
         if ((uint64_t)s >= sc->s_total) return;
-        uint32_t lo = 0, hi = sc->L;               // last entry with sb <= s
+        uint32_t blo = 0, bhi = nblk;              // last cell chunk with first slot <= s
+        while (bhi - blo > 1) {
+            const uint32_t mid = (blo + bhi) >> 1;
+            if (bt.s0[mid] <= s) blo = mid; else bhi = mid;
+        }
+        uint32_t lo = blo * chunk, hi = lo + bt.cnt[blo];   // last entry of the chunk with sb <= s
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) >> 1;
             if (L.sb[mid] <= s) lo = mid; else hi = mid;
@@ -129,7 +134,7 @@ __global__ __launch_bounds__(256) void k_resample(
         if (rc.W == 0) return;
         const uint64_t bb = L.bb[li];
         const uint32_t rbm = L.rb[li];
-        const uint64_t Q0 = L.P[li] + L.Rp[li] + (uint64_t)r * bb + min(r, rbm);
+        const uint64_t Q0 = bt.P0[li / chunk] + L.Pl[li] + L.Rp[li] + (uint64_t)r * bb + min(r, rbm);
         const uint64_t Q1 = Q0 + bb + (r < rbm ? 1u : 0u);
         const uint32_t o0 = fcount(Q0, rc), o1 = fcount(Q1, rc);
         const uint32_t joint = L.start[li] + L.sb[li] + L.n[li] + r;
@@ -178,7 +183,7 @@ __global__ __launch_bounds__(256) void k_resample(
                 const uint32_t r = j - cst;
                 const uint64_t bp = L.bp[li];
                 const uint32_t rpm = L.rp[li];
-                const uint64_t Q0 = L.P[li] + (uint64_t)r * bp + min(r, rpm);
+                const uint64_t Q0 = bt.P0[li / chunk] + L.Pl[li] + (uint64_t)r * bp + min(r, rpm);
                 const uint64_t Q1 = Q0 + bp + (r < rpm ? 1u : 0u);
                 const uint32_t o0 = fcount(Q0, rc), o1 = fcount(Q1, rc);
                 const uint32_t joint = cst + L.sb[li] + r;
