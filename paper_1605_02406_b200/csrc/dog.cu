@@ -37,7 +37,7 @@ struct dog_ctx {
     int64_t k = 0;
     bool poisoned = false;
     size_t nu_cap = 0;          // particle arrays padded to the sort tile
-    uint32_t sort_tiles = 0, cell_blocks = 0, cell_chunk = 0, mom_ranges = 0, pers_blocks = 0;
+    uint32_t sort_tiles = 0, cell_blocks = 0, cell_chunk = 0, rs_blocks = 0;
 
     // state S_k and predicted state (SoA, f32)
     float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
@@ -59,8 +59,8 @@ struct dog_ctx {
     uint64_t *dbg_Rp = nullptr, *dbg_Rb = nullptr;
     float *bx = nullptr, *by = nullptr, *bvx = nullptr, *bvy = nullptr;
     uint32_t* jidx = nullptr;
-    // moments partials
-    MomScratch ms{};
+    // moments partials of cells split over several work items
+    MomPartial* partial = nullptr;
     DevScalars* sc = nullptr;
     // zeroed once per cycle (one memset): radix histograms, tile counters, look-back status
     uint8_t* zero = nullptr;
@@ -215,14 +215,18 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->nu_cap = round_up((size_t)n_particles, kRsTile);
     ctx->sort_tiles = cdiv(n_particles, kRsTile);
     {   // cell chunks: ~4 blocks per SM, each a multiple of one 1024-cell iteration
-        uint32_t chunk = cdiv(cdiv(C, 4u * 148u), kCellIter) * kCellIter;
+        uint32_t chunk = 2u * kCellIter;
         uint32_t nblk = cdiv(C, chunk);
         while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(C, chunk); }
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
-    ctx->mom_ranges = cdiv(n_particles, kMomRange);
-    ctx->pers_blocks = cdiv(ctx->mom_ranges, 8);
+    {   // k_resample: persistent grid, as many blocks as fit on the GPU at once
+        int per_sm = 0, sms = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resample, 256, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        ctx->rs_blocks = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
+    }
     const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
     const bool dbg = (flags & DOG_FLAG_DEBUG) != 0;
 
@@ -244,16 +248,19 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
     AL(ctx->list.c, LC); AL(ctx->list.n, LC); AL(ctx->list.Rp, LC); AL(ctx->list.Rb, LC);
     AL(ctx->list.rho_p, LC); AL(ctx->list.start, LC); AL(ctx->list.sb, LC); AL(ctx->list.nb, LC);
-    AL(ctx->list.Pl, LC); AL(ctx->list.bp, LC); AL(ctx->list.rp, LC); AL(ctx->list.bb, LC);
-    AL(ctx->list.rb, LC);
+    AL(ctx->list.Pl, LC); AL(ctx->list.it, LC); AL(ctx->list.bp, LC); AL(ctx->list.rp, LC);
+    AL(ctx->list.bb, LC); AL(ctx->list.rb, LC); AL(ctx->list.done, LC);
     AL(ctx->cell2list, Cs);
-    AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n, ctx->cell_blocks); AL(ctx->bt.rb, ctx->cell_blocks);
-    AL(ctx->bt.J, ctx->cell_blocks); AL(ctx->bt.s0, ctx->cell_blocks); AL(ctx->bt.P0, ctx->cell_blocks);
-    AL(ctx->ms.head, ctx->mom_ranges); AL(ctx->ms.tail, ctx->mom_ranges);
-    AL(ctx->ms.tail_cell, ctx->mom_ranges); AL(ctx->ms.head_ends, ctx->mom_ranges);
+    AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
+    AL(ctx->bt.P0, ctx->cell_blocks); AL(ctx->bt.item0, ctx->cell_blocks); AL(ctx->bt.s0, ctx->cell_blocks);
+    {   // work items: (nu + nu_b) / 256 full items plus at most two partial items per active cell
+        const size_t members = (size_t)n_particles + (size_t)n_birth;
+        AL(ctx->partial, members / kItem + 2 * std::min<size_t>(Cs, members) + 16);
+    }
     AL(ctx->sc, 1);
     // zero region layout (u32 words)
     const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16, w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256;
+    // ctrs[0..3]: radix tile counters; ctrs[8..9]: finished-block counters of k_cells / k_list_scan
     ctx->zero_bytes = 4 * (w_rhist + w_ctrs + w_sort);
     AL(ctx->zero, ctx->zero_bytes);
 #undef AL
@@ -265,6 +272,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     uint32_t* z = (uint32_t*)ctx->zero;
     ctx->rhist = z; z += w_rhist;
     ctx->ctrs = z; z += w_ctrs;
+    ctx->bt.done = ctx->ctrs + 8;
     ctx->st_sort = z; z += w_sort;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
@@ -307,7 +315,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 6 + ctx->npass;   // predict, sort passes, cells, list scan + finish, resample, moments fixup
+    return 4 + ctx->npass;   // predict, sort passes, cells, list scan, resample
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -373,10 +381,7 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     CK(mark("cells"));
 
     // 5a/7a. birth slots + joint CDF over the active list
-    k_list_scan<<<ctx->cell_blocks, kLsThreads, 0, st>>>(ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
-                                                        ctx->sc, fc);
-    CK(cudaGetLastError());
-    k_list_finish<<<1, 1024, 0, st>>>(ctx->bt, ctx->cell_blocks, ctx->sc, fc, a.k);
+    k_list_scan<<<ctx->cell_blocks, kLsThreads, 0, st>>>(ctx->list, ctx->bt, ctx->cell_chunk, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
     CK(mark("list_scan"));
 
@@ -384,16 +389,10 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
     NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
     BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-    const uint32_t birth_blocks = cdiv(ctx->nu_b, 256);
-    k_resample<<<ctx->pers_blocks + birth_blocks, 256, 0, st>>>(
-        ctx->skeys, ctx->perm, pr, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, ns, bd,
-        ctx->mean, ctx->cov, ctx->ms, ctx->sc, fc, a.k, ctx->pers_blocks, ctx->mom_ranges);
+    k_resample<<<ctx->rs_blocks, 256, 0, st>>>(ctx->perm, pr, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
+                                               ns, bd, ctx->mean, ctx->cov, ctx->partial, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
     CK(mark("resample"));
-    k_moments_fixup<<<cdiv(ctx->mom_ranges, 256), 256, 0, st>>>(ctx->ms, ctx->list, ctx->cell2list, ctx->mean,
-                                                                 ctx->cov, ctx->sc, ctx->mom_ranges);
-    CK(cudaGetLastError());
-    CK(mark("moments_fixup"));
     if (prof) {
         ctx->prof_nst = mark_i - 1;
         ctx->prof_steps += 1;

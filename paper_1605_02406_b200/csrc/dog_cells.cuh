@@ -5,20 +5,22 @@
 // Dempster update (Eq. 63), birth split (Eqs. 67-68), fixed-point masses (A-23) and the readouts.
 // Cells holding particles or receiving born mass ("active" cells, typically ~1 % of the grid) are
 // staged, in cell order, in their block's segment of a list; every later stage works on that list.
-// Each block owns a contiguous chunk of cells, so the list is ordered by (block, position) and block
-// prefixes are a scan over a few hundred block totals -- no grid-wide look-back chain.
+// Each block owns a contiguous chunk of cells, so the list is ordered by (block, position); the last
+// block to finish scans the few thousand block totals (no grid-wide look-back chain).
 //
-// k_list_scan (one block per cell chunk): prefix of n_c (first sorted slot of each cell), prefix of
-// R_b (born-mass CDF) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A)) (A-15), the gated
-// joint mass J_c = R_p + [n_b > 0] R_b and its block-local exclusive prefix, the even-split
-// parameters of each cell; k_list_finish scans the block totals of J -> joint CDF offsets, W, w_bar
-// (Eq. 57) and U.  The joint CDF is in cell-interleaved order (A-25).
+// k_list_scan (one block per cell chunk): first sorted slot of each cell (prefix of n_c), born-mass
+// CDF A_c (prefix of R_b) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A)) (A-15), the
+// gated joint mass J_c = R_p + [n_b > 0] R_b and its prefix (the joint CDF in cell-interleaved order,
+// A-25), the even-split parameters, and the work items of k_resample (<= 256 members of one cell).
+// Its last block scans the block totals -> joint-CDF offsets, W, w_bar (Eq. 57), U (A-24).
 #pragma once
 #include <cstdint>
 #include "dog_common.cuh"
 #include "dog_rng.cuh"
 
 namespace dog {
+
+constexpr uint32_t kItem = 256;   // members per k_resample work item
 
 struct CellList {           // SoA staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
     uint32_t* c;            // cell index
@@ -30,19 +32,22 @@ struct CellList {           // SoA staging, capacity nblk * chunk (>= C); entry 
     uint32_t* sb;           // first birth slot of the cell (global)        (k_list_scan)
     uint32_t* nb;           // birth slots of the cell                      (k_list_scan)
     uint64_t* Pl;           // block-local exclusive joint prefix           (k_list_scan)
+    uint32_t* it;           // block-local exclusive work-item prefix       (k_list_scan)
     uint64_t* bp;           // R_p / n_c        (even split of R_p)         (k_list_scan)
     uint32_t* rp;           // R_p mod n_c
     uint64_t* bb;           // R_b / n_b
     uint32_t* rb;           // R_b mod n_b
+    uint32_t* done;         // finished persistent work items (moments combine)
 };
 
 struct BlockTotals {        // one entry per cell chunk
     uint32_t* cnt;          // active cells staged by the block                (k_cells)
-    uint64_t* n;            // sum of n_c over them                             (k_cells)
-    uint64_t* rb;           // sum of R_b over them                             (k_cells)
-    uint64_t* J;            // sum of J over them                               (k_list_scan)
+    uint64_t* n0;           // sum of n_c over them -> exclusive prefix        (k_cells, last block)
+    uint64_t* rb0;          // sum of R_b over them -> exclusive prefix        (k_cells, last block)
+    uint64_t* P0;           // sum of J -> exclusive joint prefix of the block  (k_list_scan, last block)
+    uint32_t* item0;        // work items -> exclusive prefix of the block      (k_list_scan, last block)
     uint32_t* s0;           // first birth slot of the block (global)           (k_list_scan)
-    uint64_t* P0;           // exclusive joint prefix of the block              (k_list_finish)
+    uint32_t* done;         // [2] finished-block counters of k_cells / k_list_scan (zeroed per cycle)
 };
 
 __device__ __forceinline__ uint64_t fx40(float m)
@@ -58,6 +63,7 @@ struct CellOut {
 };
 
 // Alg. 3 for one cell, canonical operation order of DESIGN.md 3.2 (bit-identical to the oracle).
+// Divisions by exactly 1 and of exactly 0 are skipped: IEEE gives the same result without them.
 __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z, float w_pred, float alpha,
                                              const FilterConst& fc)
 {
@@ -74,12 +80,15 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     const float oneK = __fsub_rn(1.0f, K);
     if (oneK <= 0.0f) { o.mO = bO; o.mF = bF; }                            // A-10
     else {
-        o.mO = __fdiv_rn(__fadd_rn(__fmul_rn(aO, bO), __fadd_rn(__fmul_rn(aO, bW), __fmul_rn(aW, bO))), oneK);
-        o.mF = __fdiv_rn(__fadd_rn(__fmul_rn(aF, bF), __fadd_rn(__fmul_rn(aF, bW), __fmul_rn(aW, bF))), oneK);
+        const float nO = __fadd_rn(__fmul_rn(aO, bO), __fadd_rn(__fmul_rn(aO, bW), __fmul_rn(aW, bO)));
+        const float nF = __fadd_rn(__fmul_rn(aF, bF), __fadd_rn(__fmul_rn(aF, bW), __fmul_rn(aW, bF)));
+        if (oneK == 1.0f) { o.mO = nO; o.mF = nF; }
+        else { o.mO = __fdiv_rn(nO, oneK); o.mF = __fdiv_rn(nF, oneK); }
     }
     const float q = __fmul_rn(fc.p_b, __fsub_rn(1.0f, m_p));               // Eqs. 67-68 (A-11)
     const float den = __fadd_rn(m_p, q);
-    o.rb = den > 0.0f ? __fdiv_rn(__fmul_rn(o.mO, q), den) : 0.0f;
+    const float mq = __fmul_rn(o.mO, q);
+    o.rb = den > 0.0f ? (mq == 0.0f ? mq : __fdiv_rn(mq, den)) : 0.0f;     // (+-0)/den = +-0
     o.rp = __fsub_rn(o.mO, o.rb);
     o.Rp = n > 0 ? fx40(o.rp) : 0ull;                                      // A-23
     o.Rb = z.x > 0.0f ? fx40(o.rb) : 0ull;                                 // P:1197 gate (A-13)
@@ -87,12 +96,31 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
 }
 
 constexpr int kCellThreads = 256, kCellItems = 4, kCellIter = kCellThreads * kCellItems;   // 1024 cells
+constexpr int kMaxCellBlocks = 4096;
 
 struct CellDebug { float* rho_p; float* rho_b; uint64_t* Rp; uint64_t* Rb; };
 
-// Block b owns cells [b chunk, (b+1) chunk), processed 1024 at a time; item i of thread t in an
-// iteration is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid
-// bitmask).  The next iteration's inputs are loaded before the current one is processed.
+// Exclusive prefix of v[0..m) in place (one block, 256 threads), returns the total.
+template <typename T>
+__device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
+{
+    T carry = 0;
+    for (uint32_t b0 = 0; b0 < m; b0 += blockDim.x * 8) {
+        T x[8], sum = 0;
+        const uint32_t b = b0 + threadIdx.x * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { x[i] = b + i < m ? __ldcg(v + b + i) : T(0); sum += x[i]; }
+        T tot;
+        T run = carry + block_excl_scan<T, 8>(sum, s_scan, tot);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { if (b + i < m) v[b + i] = run; run += x[i]; }
+        carry += tot;
+    }
+    return carry;
+}
+
+// Block b owns cells [b chunk, (b+1) chunk), 1024 per iteration; item i of thread t in an iteration
+// is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid bitmask).
 __global__ __launch_bounds__(kCellThreads) void k_cells(
     uint32_t* __restrict__ counts, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
@@ -101,8 +129,9 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
 {
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
     __shared__ uint32_t s_run;
-    __shared__ uint64_t s_A[8], s_N[8];
+    __shared__ uint64_t s_A[9], s_N[9];
     __shared__ uint32_t s_bad[8];
+    __shared__ bool s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const float w_pred = sc->w_pred;
@@ -111,10 +140,12 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
     const uint32_t lbase = blockIdx.x * chunk;
     if (tid == 0) s_run = 0;
 
-    uint32_t n[kCellItems], prev[kCellItems];
-    float mf[kCellItems];
-    float2 z[kCellItems];
-    auto load = [&](uint32_t base) {
+    uint64_t A_loc = 0, N_loc = 0;
+    uint32_t bad_loc = 0;
+    for (uint32_t base = c0; base < c1; base += kCellIter) {
+        uint32_t n[kCellItems], prev[kCellItems];
+        float mf[kCellItems];
+        float2 z[kCellItems];
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
@@ -125,34 +156,22 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
             prev[i] = (lane == 0 && (word << 5) < c1) ? mvalid[word] : 0u;
         }
-    };
-    uint64_t A_loc = 0, N_loc = 0;
-    uint32_t bad_loc = 0;
-    if (c0 < c1) load(c0);
-    for (uint32_t base = c0; base < c1; base += kCellIter) {
-        uint32_t cn[kCellItems], cp[kCellItems];
-        float cmf[kCellItems];
-        float2 cz[kCellItems];
-#pragma unroll
-        for (int i = 0; i < kCellItems; ++i) { cn[i] = n[i]; cp[i] = prev[i]; cmf[i] = mf[i]; cz[i] = z[i]; }
-        if (base + kCellIter < c1) load(base + kCellIter);     // prefetch the next iteration
-
         CellOut o[kCellItems];
         uint32_t abal[kCellItems];
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
-            o[i] = cell_math(cn[i], cmf[i], cz[i], w_pred, alpha, fc);
+            o[i] = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
             const bool vnow = valid && o[i].n > 0 && o[i].rp > 0.0f && o[i].S > 0.0f;
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
-            const uint32_t pw = __shfl_sync(0xffffffffu, cp[i], 0);
+            const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
             if (valid) {
                 occ[c] = o[i].mO;
                 free_out[c] = o[i].mF;
                 m_free[c] = o[i].mF;                    // Alg. 3 store_values
-                if (cn[i]) counts[c] = 0u;              // ready for the next cycle's k_predict
+                if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_predict
                 if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
                     mean[c] = make_float2(0.0f, 0.0f);
                     cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
@@ -200,11 +219,19 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
         uint64_t A = 0, N = 0; uint32_t b = 0;
         for (int w = 0; w < kCellThreads / 32; ++w) { A += s_A[w]; N += s_N[w]; b += s_bad[w]; }
         bt.cnt[blockIdx.x] = s_run;
-        bt.n[blockIdx.x] = N;
-        bt.rb[blockIdx.x] = A;
-        if (A) atomicAdd((unsigned long long*)&sc->A, (unsigned long long)A);
+        bt.n0[blockIdx.x] = N;
+        bt.rb0[blockIdx.x] = A;
         if (b) atomicAdd(&sc->meas_bad, b);
+        __threadfence();
+        s_last = atomicAdd(&bt.done[0], 1u) == gridDim.x - 1;
     }
+    __syncthreads();
+    if (!s_last) return;
+    // the last block: exclusive prefixes of the block totals, grand totals
+    __threadfence();
+    const uint64_t N = block_prefix_inplace<uint64_t>(bt.n0, gridDim.x, s_N);
+    const uint64_t A = block_prefix_inplace<uint64_t>(bt.rb0, gridDim.x, s_A);
+    if (tid == 0) { sc->n_in = N; sc->A = A; }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -222,40 +249,23 @@ __device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_
 }
 
 constexpr int kLsThreads = 256, kLsItems = 8, kLsTile = kLsThreads * kLsItems;
-constexpr int kMaxCellBlocks = 2048;
 
-// Exclusive prefix of the first `b` block totals, computed redundantly by every block (nblk is a few
-// hundred).  Returns the sums over blocks [0, b) of (n, rb) and the grand total of rb.
-__device__ __forceinline__ void block_prefix(const BlockTotals& bt, uint32_t nblk, uint32_t b, uint64_t& n0,
-                                             uint64_t& rb0)
-{
-    __shared__ uint64_t s_n[kLsThreads / 32], s_r[kLsThreads / 32];
-    uint64_t pn = 0, pr = 0;
-    for (uint32_t i = threadIdx.x; i < b; i += blockDim.x) { pn += bt.n[i]; pr += bt.rb[i]; }
-    pn = warp_sum(pn);
-    pr = warp_sum(pr);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) { s_n[warp] = pn; s_r[warp] = pr; }
-    __syncthreads();
-    n0 = 0; rb0 = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { n0 += s_n[w]; rb0 += s_r[w]; }
-    __syncthreads();
-}
-
-__global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
-                                                          DevScalars* __restrict__ sc, FilterConst fc)
+__global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotals bt, uint32_t chunk,
+                                                          DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
     __shared__ uint64_t s_a[kLsThreads / 32 + 1], s_b[kLsThreads / 32 + 1];
+    __shared__ uint32_t s_c[kLsThreads / 32 + 1];
+    __shared__ bool s_last;
     const int tid = threadIdx.x;
     const uint32_t blk = blockIdx.x;
     const uint64_t A = sc->A;
     const uint64_t nu_b = fc.nu_b;
-    uint64_t start0, A0;
-    block_prefix(bt, nblk, blk, start0, A0);
+    uint64_t start0 = bt.n0[blk], A0 = bt.rb0[blk];
     const uint32_t cnt = bt.cnt[blk];
     const uint32_t lbase = blk * chunk;
     if (tid == 0) bt.s0[blk] = (uint32_t)slot_of(A0, A, nu_b);
     uint64_t J0 = 0;                          // block-local joint prefix
+    uint32_t I0 = 0;                          // block-local work-item prefix
     for (uint32_t t0 = 0; t0 < cnt; t0 += kLsTile) {
         const uint32_t b = t0 + tid * kLsItems;
         uint32_t n[kLsItems];
@@ -277,7 +287,9 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
         uint64_t Ax = A0 + xrb;               // A_{c-1}
         uint64_t s_prev = slot_of(Ax, A, nu_b);
         uint64_t J[kLsItems];
+        uint32_t its[kLsItems];
         uint64_t js = 0;
+        uint32_t is = 0;
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
             Ax += Rb[i];
@@ -292,53 +304,51 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
                 L.rp[li] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
                 L.bb[li] = nbv ? Rb[i] / nbv : 0ull;
                 L.rb[li] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
+                L.done[li] = 0u;
                 J[i] = Rp[i] + (nbv ? Rb[i] : 0ull);
+                its[i] = (n[i] + kItem - 1) / kItem + (nbv + kItem - 1) / kItem;
             } else {
                 J[i] = 0;
+                its[i] = 0;
             }
             start += n[i];
             js += J[i];
+            is += its[i];
             s_prev = s;
         }
         uint64_t tj;
+        uint32_t ti;
         const uint64_t xj = block_excl_scan<uint64_t, kLsThreads / 32>(js, s_a, tj);
+        const uint32_t xi = block_excl_scan<uint32_t, kLsThreads / 32>(is, s_c, ti);
         uint64_t run = J0 + xj;
+        uint32_t irun = I0 + xi;
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
-            if (b + i < cnt) L.Pl[lbase + b + i] = run;
+            if (b + i < cnt) { L.Pl[lbase + b + i] = run; L.it[lbase + b + i] = irun; }
             run += J[i];
+            irun += its[i];
         }
         start0 += tn;
         A0 += trb;
         J0 += tj;
-    }
-    if (tid == 0) bt.J[blk] = J0;
-}
-
-// One block: joint-CDF offsets of the cell chunks, totals W and n_in, w_bar (Eq. 57), U (A-24).
-__global__ __launch_bounds__(1024) void k_list_finish(BlockTotals bt, uint32_t nblk, DevScalars* __restrict__ sc,
-                                                      FilterConst fc, int64_t k)
-{
-    __shared__ uint64_t s_w[33];
-    const int tid = threadIdx.x;
-    uint64_t carry = 0, ncarry = 0;
-    for (uint32_t b0 = 0; b0 < nblk; b0 += blockDim.x) {
-        const uint32_t b = b0 + tid;
-        const uint64_t v = b < nblk ? bt.J[b] : 0ull;
-        const uint64_t nv = b < nblk ? bt.n[b] : 0ull;
-        uint64_t tot;
-        const uint64_t x = block_excl_scan<uint64_t, 32>(v, s_w, tot);
-        if (b < nblk) bt.P0[b] = carry + x;
-        carry += tot;
-        uint64_t ntot;
-        block_excl_scan<uint64_t, 32>(nv, s_w, ntot);
-        ncarry += ntot;
+        I0 += ti;
     }
     if (tid == 0) {
-        const uint64_t W = carry;
+        bt.P0[blk] = J0;
+        bt.item0[blk] = I0;
+        __threadfence();
+        s_last = atomicAdd(&bt.done[1], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // the last block: joint-CDF and work-item offsets of the chunks, totals (Eq. 57, A-24, A-26)
+    __threadfence();
+    const uint64_t W = block_prefix_inplace<uint64_t>(bt.P0, gridDim.x, s_a);
+    const uint32_t items = block_prefix_inplace<uint32_t>(bt.item0, gridDim.x, s_c);
+    if (tid == 0) {
         sc->W = W;
-        sc->n_in = ncarry;
-        sc->s_total = sc->A ? (uint64_t)fc.nu_b : 0ull;
+        sc->n_items = items;
+        sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
         sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
         sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
     }

@@ -16,7 +16,7 @@ struct DevScalars {
     uint64_t A;          // total fixed-point born mass
     uint64_t n_in;       // particles inside the grid after predict
     uint64_t s_total;    // birth slots allocated (nu_b or 0)
-    uint32_t L;          // active cells (n_c > 0 or R_b > 0) of the cycle
+    uint32_t n_items;    // k_resample work items of the cycle
     uint32_t pad;
 };
 

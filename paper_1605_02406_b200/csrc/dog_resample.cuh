@@ -2,13 +2,16 @@
 // Eqs. 81-84), new-born particle initialisation (Alg. 5) and systematic resampling (Alg. 7,
 // Eq. 57) to the next state.
 //
-// Resampling is member-driven: every member of the joint list (the cell-sorted persistent particles
-// and the birth slots, cell-interleaved, A-25) knows its cumulative fixed-point weight range
-// [Q, Q') from its cell's joint prefix P_c and the even split of the cell's mass (A-23), and writes
-// its copies to the outputs i with Q <= t_i < Q', t_i = floor((i 2^32 + U) W / (nu 2^32)) (A-24):
-// i in [F(Q), F(Q')) with F(X) = #{i : t_i < X} = clamp(ceil((X nu 2^32 - U W) / (W 2^32)), 0, nu).
-// This selects exactly what the oracle's binary search over the particle-level CDF selects; F is
-// evaluated with an fp64 estimate corrected by exact 128-bit products (no 128-bit division).
+// Work items: up to 256 members of ONE cell -- either persistent particles (cell-sorted slots) or
+// birth slots -- so a warp loads its cell's parameters once, reduces the velocity sums with a plain
+// warp reduction, and cells split over several items are combined by the last item to finish, in
+// item order (deterministic).  Each warp takes a contiguous range of items.
+//
+// Resampling is member-driven: member r of a cell owns the fixed-point weight range [Q_r, Q_{r+1})
+// of the joint CDF (cell prefix P_c plus the even split of the cell's mass, A-23) and writes its
+// copies to the outputs i with Q_r <= t_i < Q_{r+1}, t_i = floor((i 2^32 + U) W / (nu 2^32))
+// (A-24): i in [F(Q_r), F(Q_{r+1})), F(X) = #{i : t_i < X} = clamp(ceil((X nu 2^32 - U W) / (W 2^32)),
+// 0, nu).  This selects exactly what the oracle's binary search over the particle-level CDF selects.
 #pragma once
 #include <cstdint>
 #include "dog_cells.cuh"
@@ -17,7 +20,6 @@
 
 namespace dog {
 
-constexpr int kMomRange = 256;   // sorted slots per warp in the persistent part
 struct MomPartial { double s[5]; };
 
 struct RsConst {
@@ -52,13 +54,12 @@ __device__ __forceinline__ uint32_t fcount(uint64_t X, const RsConst& r)
     const double cy = ceil(y);
     const double d = cy - y;                       // in [0, 1)
     if (d > 0x1p-16 && d < 1.0 - 0x1p-16) return (uint32_t)cy;
-    // exact: smallest q >= 0 with q W 2^32 >= X nu 2^32 - U W
     const u128 num0 = ((u128)X * (u128)r.nu) << 32;
     if (num0 <= r.UW) return 0u;
     const u128 num = num0 - r.UW;
     const u128 E = ((u128)r.W) << 32;
     uint64_t q = (uint64_t)fmax(cy - 1.0, 0.0);
-    while ((u128)q * E < num) ++q;
+    while ((u128)q * E < num) ++q;                 // smallest q with q W 2^32 >= X nu 2^32 - U W
     while (q > 0 && (u128)(q - 1) * E >= num) --q;
     return (uint32_t)(q < r.nu ? q : r.nu);
 }
@@ -81,13 +82,30 @@ __device__ __forceinline__ void finalize_cell(uint32_t c, const double* s, uint3
 struct NextState { float *x, *y, *vx, *vy; uint32_t* jidx; };
 struct Pred { const float *x, *y, *vx, *vy; };
 struct BirthDebug { float *x, *y, *vx, *vy; };
-struct MomScratch { MomPartial* head; MomPartial* tail; uint32_t* tail_cell; uint8_t* head_ends; };
+
+// Last index in [lo, hi) whose value v(idx) <= key, warp-cooperative 32-ary search; assumes
+// v(lo) <= key.  Every lane returns the result.
+template <typename F>
+__device__ __forceinline__ uint32_t warp_last_le(uint32_t lo, uint32_t hi, uint32_t key, F v)
+{
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 1) {
+        const uint32_t span = hi - lo;
+        const uint32_t step = (span + 31) / 32;
+        const uint32_t p = lo + (uint32_t)lane * step;     // probe lane's position
+        const bool ok = p < hi && v(p) <= key;
+        const uint32_t m = __ballot_sync(0xffffffffu, ok);   // a prefix of lanes (monotone values)
+        const int last = 31 - __clz(m);                      // lane 0 always ok
+        lo = lo + (uint32_t)last * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
 
 __global__ __launch_bounds__(256) void k_resample(
-    const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ perm, Pred pr, CellList L, BlockTotals bt,
-    uint32_t nblk, uint32_t chunk, const uint32_t* __restrict__ cell2list, NextState out, BirthDebug bdbg,
-    float2* __restrict__ mean, float* __restrict__ cov, MomScratch ms, const DevScalars* __restrict__ sc,
-    FilterConst fc, int64_t k, uint32_t pers_blocks, uint32_t nranges)
+    const uint32_t* __restrict__ perm, Pred pr, CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
+    NextState out, BirthDebug bdbg, float2* __restrict__ mean, float* __restrict__ cov,
+    MomPartial* __restrict__ partial, const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu);
@@ -97,175 +115,140 @@ __global__ __launch_bounds__(256) void k_resample(
             if (out.jidx) out.jidx[i] = 0xFFFFFFFFu;
         }
     }
-
-    if (blockIdx.x >= pers_blocks) {
-        // ---------------- birth slots (Alg. 5): state from the slot's Philox draw, then copies
-        const uint32_t s = (blockIdx.x - pers_blocks) * blockDim.x + tid;
-        if ((uint64_t)s >= sc->s_total) return;
-        uint32_t blo = 0, bhi = nblk;              // last cell chunk with first slot <= s
-        while (bhi - blo > 1) {
-            const uint32_t mid = (blo + bhi) >> 1;
-            if (bt.s0[mid] <= s) blo = mid; else bhi = mid;
-        }
-        uint32_t lo = blo * chunk, hi = lo + bt.cnt[blo];   // last entry of the chunk with sb <= s
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (L.sb[mid] <= s) lo = mid; else hi = mid;
-        }
-        const uint32_t li = lo;
-        const uint32_t r = s - L.sb[li];
-        const uint32_t c = L.c[li];
-        const uint32_t col = c % (uint32_t)fc.W, row = c / (uint32_t)fc.W;
-        const Philox4 d = draw(fc.seed, s, k, STAGE_BIRTH);
-        const float colf = (float)col, rowf = (float)row;
-        float bx = __fadd_rn(colf, unit24(d.r0));
-        float by = __fadd_rn(rowf, unit24(d.r1));
-        const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
-        if (bx >= cx1) bx = __int_as_float(__float_as_int(cx1) - 1);    // nextafter(col+1, 0) (A-16)
-        if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
-        float n0, n1;
-        box_muller(d.r2, d.r3, n0, n1);
-        float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
-        if (fc.v_max > 0.0f) {
-            bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
-            bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
-        }
-        if (bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
-        if (rc.W == 0) return;
-        const uint64_t bb = L.bb[li];
-        const uint32_t rbm = L.rb[li];
-        const uint64_t Q0 = bt.P0[li / chunk] + L.Pl[li] + L.Rp[li] + (uint64_t)r * bb + min(r, rbm);
-        const uint64_t Q1 = Q0 + bb + (r < rbm ? 1u : 0u);
-        const uint32_t o0 = fcount(Q0, rc), o1 = fcount(Q1, rc);
-        const uint32_t joint = L.start[li] + L.sb[li] + L.n[li] + r;
-        for (uint32_t o = o0; o < o1; ++o) {
-            out.x[o] = bx; out.y[o] = by; out.vx[o] = bvx; out.vy[o] = bvy;
-            if (out.jidx) out.jidx[o] = joint;
-        }
-        return;
-    }
-
-    // ---------------- persistent members: one warp per range of 256 cell-sorted slots
-    const uint32_t wr = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
-    if (wr >= nranges) return;
-    const uint32_t n_in = (uint32_t)sc->n_in;
+    const uint32_t n_items = sc->n_items;
     const float w_pred = sc->w_pred;
-    const uint32_t start = wr * kMomRange;
-    if (start >= n_in) {
-        if (lane == 0) { ms.tail_cell[wr] = 0xFFFFFFFFu; ms.head_ends[wr] = 1; }
-        return;
-    }
-    const uint32_t end = min(start + (uint32_t)kMomRange, n_in);
-    const uint32_t first_cell = skeys[start];
-    const bool cont_before = start > 0 && skeys[start - 1] == first_cell;
-    bool have_carry = false;
-    uint32_t carry_cell = 0xFFFFFFFFu;
-    double carry[5] = {0, 0, 0, 0, 0};
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+    const uint32_t per = (n_items + nwarps - 1) / nwarps;
+    uint32_t q = gw * per;
+    const uint32_t q_end = min(q + per, n_items);
+    if (q >= q_end) return;
 
-    for (uint32_t j0 = start; j0 < end; j0 += 32) {
-        const uint32_t j = j0 + lane;
-        const bool valid = j < end;
-        const uint32_t cell = valid ? skeys[j] : 0xFFFFFFFEu;
-        const uint32_t cell_next = (j + 1 < n_in) ? skeys[j + 1] : 0xFFFFFFFFu;
-        uint32_t li = 0, cst = 0, cn = 0;
-        float crho = 0.0f;
-        double v[5] = {0, 0, 0, 0, 0};
-        if (valid) {
-            li = cell2list[cell];
-            cst = L.start[li];
-            cn = L.n[li];
-            crho = L.rho_p[li];
-            const uint32_t src = perm[j];
-            const float X = pr.x[src], Y = pr.y[src], VX = pr.vx[src], VY = pr.vy[src];
-            const double a = (double)VX, bq = (double)VY;
-            v[0] = a; v[1] = bq; v[2] = a * a; v[3] = bq * bq; v[4] = a * bq;
-            if (rc.W) {
-                const uint32_t r = j - cst;
-                const uint64_t bp = L.bp[li];
-                const uint32_t rpm = L.rp[li];
-                const uint64_t Q0 = bt.P0[li / chunk] + L.Pl[li] + (uint64_t)r * bp + min(r, rpm);
-                const uint64_t Q1 = Q0 + bp + (r < rpm ? 1u : 0u);
-                const uint32_t o0 = fcount(Q0, rc), o1 = fcount(Q1, rc);
-                const uint32_t joint = cst + L.sb[li] + r;
-                for (uint32_t o = o0; o < o1; ++o) {
-                    out.x[o] = X; out.y[o] = Y; out.vx[o] = VX; out.vy[o] = VY;
-                    if (out.jidx) out.jidx[o] = joint;
+    // locate the first item: chunk b, then entry li within the chunk
+    uint32_t b = warp_last_le(0u, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
+    uint32_t lbase = b * chunk;
+    uint32_t li = warp_last_le(lbase, lbase + bt.cnt[b], q - bt.item0[b],
+                               [&](uint32_t i) { return L.it[i]; });
+    uint32_t sub = q - bt.item0[b] - L.it[li];
+
+    while (true) {
+        // cell parameters (uniform across the warp)
+        const uint32_t c = L.c[li], n = L.n[li], start = L.start[li], nb = L.nb[li];
+        const uint32_t np = (n + kItem - 1) / kItem;
+        const uint64_t P = bt.P0[b] + L.Pl[li];
+        if (sub < np) {
+            // ---------------- persistent members [r0, r0 + m) of cell c
+            const uint32_t r0 = sub * kItem, m = min(kItem, n - r0);
+            const uint64_t bp = L.bp[li];
+            const uint32_t rpm = L.rp[li];
+            const uint32_t jbase = start + L.sb[li];
+            double acc[5] = {0, 0, 0, 0, 0};
+            for (uint32_t t = 0; t < m; t += 32) {
+                const bool valid = t + lane < m;
+                const uint32_t r = r0 + t + lane;
+                float X = 0.f, Y = 0.f, VX = 0.f, VY = 0.f;
+                if (valid) {
+                    const uint32_t src = perm[start + r];
+                    X = pr.x[src]; Y = pr.y[src]; VX = pr.vx[src]; VY = pr.vy[src];
+                    const double a = (double)VX, bq = (double)VY;
+                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                }
+                if (rc.W) {
+                    const uint64_t Q0 = P + (uint64_t)r * bp + min(r, rpm);
+                    const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
+                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                    if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bp + (r < rpm ? 1u : 0u), rc);
+                    if (valid) {
+                        for (uint32_t o = F0; o < F1; ++o) {
+                            out.x[o] = X; out.y[o] = Y; out.vx[o] = VX; out.vy[o] = VY;
+                            if (out.jidx) out.jidx[o] = jbase + r;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
+            if (np == 1) {
+                if (lane == 0) finalize_cell(c, acc, n, L.rho_p[li], w_pred, mean, cov);
+            } else {
+                // several items: publish this item's sums; the last one to finish combines in order
+                const uint32_t q0 = bt.item0[b] + L.it[li];   // the cell's first item
+                uint32_t old = 0;
+                if (lane == 0) {
+                    MomPartial p;
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) p.s[i] = acc[i];
+                    partial[q0 + sub] = p;
+                    __threadfence();
+                    old = atomicAdd(&L.done[li], 1u);
+                }
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == np - 1) {
+                    __threadfence();
+                    double s[5] = {0, 0, 0, 0, 0};
+                    if (lane == 0) {
+                        for (uint32_t j = 0; j < np; ++j) {
+                            const double* ps = (const double*)&partial[q0 + j];
+#pragma unroll
+                            for (int i = 0; i < 5; ++i) s[i] += __ldcg(ps + i);
+                        }
+                        finalize_cell(c, s, n, L.rho_p[li], w_pred, mean, cov);
+                    }
+                }
+            }
+        } else {
+            // ---------------- birth slots [r0, r0 + m) of cell c (Alg. 5): state from the slot's draw
+            const uint32_t r0 = (sub - np) * kItem, m = min(kItem, nb - r0);
+            const uint64_t bb = L.bb[li];
+            const uint32_t rbm = L.rb[li], sb = L.sb[li];
+            const uint64_t PB = P + L.Rp[li];
+            const uint32_t jbase = start + sb + n;
+            const uint32_t col = c % (uint32_t)fc.W, row = c / (uint32_t)fc.W;
+            const float colf = (float)col, rowf = (float)row;
+            const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
+            for (uint32_t t = 0; t < m; t += 32) {
+                const bool valid = t + lane < m;
+                const uint32_t r = r0 + t + lane;
+                const uint32_t s = sb + r;
+                const Philox4 d = draw(fc.seed, s, k, STAGE_BIRTH);
+                float bx = __fadd_rn(colf, unit24(d.r0));
+                float by = __fadd_rn(rowf, unit24(d.r1));
+                if (bx >= cx1) bx = __int_as_float(__float_as_int(cx1) - 1);    // nextafter(col+1, 0) (A-16)
+                if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
+                float n0, n1;
+                box_muller(d.r2, d.r3, n0, n1);
+                float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
+                if (fc.v_max > 0.0f) {
+                    bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
+                    bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
+                }
+                if (valid && bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
+                if (rc.W) {
+                    const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
+                    const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
+                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                    if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bb + (r < rbm ? 1u : 0u), rc);
+                    if (valid) {
+                        for (uint32_t o = F0; o < F1; ++o) {
+                            out.x[o] = bx; out.y[o] = by; out.vx[o] = bvx; out.vy[o] = bvy;
+                            if (out.jidx) out.jidx[o] = jbase + r;
+                        }
+                    }
                 }
             }
         }
-        // segmented inclusive scan of the velocity sums within the 32-slot chunk
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t oc = __shfl_up_sync(0xffffffffu, cell, off);
-#pragma unroll
-            for (int q = 0; q < 5; ++q) {
-                const double o = __shfl_up_sync(0xffffffffu, v[q], off);
-                if (lane >= off && oc == cell) v[q] += o;
-            }
-        }
-        if (have_carry && cell == carry_cell) {
-#pragma unroll
-            for (int q = 0; q < 5; ++q) v[q] += carry[q];
-        }
-        const bool seg_end = valid && cell_next != cell;
-        if (seg_end) {
-            if (cell == first_cell && cont_before) {
-                MomPartial hp;
-#pragma unroll
-                for (int q = 0; q < 5; ++q) hp.s[q] = v[q];
-                ms.head[wr] = hp;
-                ms.head_ends[wr] = 1;
-            } else {
-                finalize_cell(cell, v, cn, crho, w_pred, mean, cov);
-            }
-        }
-        const int last = (int)min(31u, end - 1 - j0);
-        const uint32_t lc = __shfl_sync(0xffffffffu, cell, last);
-        const bool lend = __shfl_sync(0xffffffffu, (int)seg_end, last) != 0;
-#pragma unroll
-        for (int q = 0; q < 5; ++q) carry[q] = __shfl_sync(0xffffffffu, v[q], last);
-        have_carry = !lend;
-        carry_cell = lc;
+        // next item
+        if (++q >= q_end) break;
+        const uint32_t nitems_cell = np + (nb + kItem - 1) / kItem;
+        if (++sub < nitems_cell) continue;
+        const uint32_t chunk_end = b + 1 < nblk ? bt.item0[b + 1] : n_items;
+        if (q >= chunk_end)                    // past this chunk's items: find the chunk holding q
+            b = warp_last_le(b, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
+        const uint32_t lo = q >= chunk_end ? b * chunk : li + 1;
+        lbase = b * chunk;
+        li = warp_last_le(lo, lbase + bt.cnt[b], q - bt.item0[b], [&](uint32_t i) { return L.it[i]; });
+        sub = q - bt.item0[b] - L.it[li];
     }
-    if (lane == 0) {
-        if (have_carry) {
-            MomPartial p;
-#pragma unroll
-            for (int q = 0; q < 5; ++q) p.s[q] = carry[q];
-            if (carry_cell == first_cell && cont_before) {   // the range lies inside one segment
-                ms.head[wr] = p;
-                ms.head_ends[wr] = 0;
-                ms.tail_cell[wr] = 0xFFFFFFFFu;
-            } else {
-                ms.tail[wr] = p;
-                ms.tail_cell[wr] = carry_cell;
-                if (!cont_before) ms.head_ends[wr] = 1;
-            }
-        } else {
-            ms.tail_cell[wr] = 0xFFFFFFFFu;
-            if (!cont_before) ms.head_ends[wr] = 1;
-        }
-    }
-}
-
-// Segments spanning several warp ranges: tail partial of the range where the segment starts plus the
-// head partials of the following ranges, in a fixed order (deterministic).
-__global__ void k_moments_fixup(MomScratch ms, CellList L, const uint32_t* __restrict__ cell2list,
-                                float2* __restrict__ mean, float* __restrict__ cov,
-                                const DevScalars* __restrict__ sc, uint32_t nranges)
-{
-    const uint32_t wr = blockIdx.x * blockDim.x + threadIdx.x;
-    if (wr >= nranges) return;
-    const uint32_t c = ms.tail_cell[wr];
-    if (c == 0xFFFFFFFFu) return;
-    double s[5];
-    for (int q = 0; q < 5; ++q) s[q] = ms.tail[wr].s[q];
-    for (uint32_t r = wr + 1; r < nranges; ++r) {
-        for (int q = 0; q < 5; ++q) s[q] += ms.head[r].s[q];
-        if (ms.head_ends[r]) break;
-    }
-    const uint32_t li = cell2list[c];
-    finalize_cell(c, s, L.n[li], L.rho_p[li], sc->w_pred, mean, cov);
 }
 
 }  // namespace dog
