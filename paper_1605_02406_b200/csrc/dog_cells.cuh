@@ -69,6 +69,13 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
 {
     CellOut o;
     o.n = n;
+    if (n == 0 && z.x == 0.0f && z.y == 0.0f && __float_as_uint(z.x) == 0u) {
+        // empty cell under a vacuous measurement: the general path below yields exactly these values
+        // (S = +0, K = 0, 1-K = 1, m_O = +0, m_F = m_Fp, rho_b = rho_p = +0, R = 0)
+        o.S = 0.0f; o.mO = 0.0f; o.rp = 0.0f; o.rb = 0.0f; o.Rp = 0ull; o.Rb = 0ull; o.bad = false;
+        o.mF = fminf(__fmul_rn(alpha, m_free), 1.0f);
+        return o;
+    }
     o.S = __double2float_rn(__dmul_rn((double)n, (double)w_pred));        // Eq. 61, exact
     const float m_p = fminf(o.S, fc.occ_max);                              // Eq. 17 cap (A-7)
     const float m_fp = fminf(__fmul_rn(alpha, m_free), __fsub_rn(1.0f, m_p));   // Eq. 62

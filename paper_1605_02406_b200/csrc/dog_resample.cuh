@@ -143,25 +143,42 @@ __global__ __launch_bounds__(256) void k_resample(
             const uint32_t rpm = L.rp[li];
             const uint32_t jbase = start + L.sb[li];
             double acc[5] = {0, 0, 0, 0, 0};
-            for (uint32_t t = 0; t < m; t += 32) {
-                const bool valid = t + lane < m;
-                const uint32_t r = r0 + t + lane;
-                float X = 0.f, Y = 0.f, VX = 0.f, VY = 0.f;
-                if (valid) {
-                    const uint32_t src = perm[start + r];
-                    X = pr.x[src]; Y = pr.y[src]; VX = pr.vx[src]; VY = pr.vy[src];
-                    const double a = (double)VX, bq = (double)VY;
-                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+            for (uint32_t t0 = 0; t0 < m; t0 += 4 * 32) {
+                // batch: 4 perm loads, then 16 gathers in flight per lane, then compute
+                uint32_t src[4];
+                float X[4], Y[4], VX[4], VY[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t t = t0 + 32 * u + lane;
+                    src[u] = t < m ? perm[start + r0 + t] : 0u;
                 }
-                if (rc.W) {
-                    const uint64_t Q0 = P + (uint64_t)r * bp + min(r, rpm);
-                    const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
-                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                    if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bp + (r < rpm ? 1u : 0u), rc);
-                    if (valid) {
-                        for (uint32_t o = F0; o < F1; ++o) {
-                            out.x[o] = X; out.y[o] = Y; out.vx[o] = VX; out.vy[o] = VY;
-                            if (out.jidx) out.jidx[o] = jbase + r;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool valid = t0 + 32 * u + lane < m;
+                    X[u] = valid ? pr.x[src[u]] : 0.f;
+                    Y[u] = valid ? pr.y[src[u]] : 0.f;
+                    VX[u] = valid ? pr.vx[src[u]] : 0.f;
+                    VY[u] = valid ? pr.vy[src[u]] : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t t = t0 + 32 * u;
+                    if (t >= m) break;                              // warp-uniform
+                    const bool valid = t + lane < m;
+                    const uint32_t r = r0 + t + lane;
+                    const double a = (double)VX[u], bq = (double)VY[u];
+                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                    if (rc.W) {
+                        const uint64_t Q0 = P + (uint64_t)r * bp + min(r, rpm);
+                        const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
+                        uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                        if (valid && (lane == 31 || t + lane + 1 == m))
+                            F1 = fcount(Q0 + bp + (r < rpm ? 1u : 0u), rc);
+                        if (valid) {
+                            for (uint32_t o = F0; o < F1; ++o) {
+                                out.x[o] = X[u]; out.y[o] = Y[u]; out.vx[o] = VX[u]; out.vy[o] = VY[u];
+                                if (out.jidx) out.jidx[o] = jbase + r;
+                            }
                         }
                     }
                 }
