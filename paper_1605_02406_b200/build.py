@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdog.so")
 SOURCES = ["dog.cu"]
-HEADERS = ["dog_common.cuh", "dog_rng.cuh", "dog_kernels.cuh", "dog_cells.cuh", "dog_resample.cuh"]
+HEADERS = ["dog_common.cuh", "dog_rng.cuh", "dog_kernels.cuh", "dog_cells.cuh", "dog_resample.cuh", "dog_sort.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -13,6 +13,7 @@
 
 #include "../../include/dog.h"
 #include "dog_kernels.cuh"
+#include "dog_sort.cuh"
 #include "dog_cells.cuh"
 #include "dog_resample.cuh"
 
@@ -65,7 +66,8 @@ struct dog_ctx {
     // zeroed once per cycle (one memset): radix histograms, tile counters, look-back status
     uint8_t* zero = nullptr;
     size_t zero_bytes = 0;
-    uint32_t *rhist = nullptr, *ctrs = nullptr, *st_sort = nullptr;
+    uint32_t *rhist = nullptr, *ctrs = nullptr;
+    uint32_t* histT = nullptr;                    // [npass][256][sort_tiles] tile digit counts -> offsets
     // end-to-end staging
     float* meas_dev = nullptr;
     // profiling: events[step][stage boundary]
@@ -212,8 +214,8 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     int bits = 1;
     while ((1ull << bits) <= (uint64_t)C) ++bits;   // keys 0..C
     ctx->npass = (bits + 7) / 8;
-    ctx->nu_cap = round_up((size_t)n_particles, kRsTile);
-    ctx->sort_tiles = cdiv(n_particles, kRsTile);
+    ctx->nu_cap = round_up((size_t)n_particles, kSortTile);
+    ctx->sort_tiles = cdiv(n_particles, kSortTile);
     {   // cell chunks: ~4 blocks per SM, each a multiple of one 1024-cell iteration
         uint32_t chunk = 2u * kCellIter;
         uint32_t nblk = cdiv(C, chunk);
@@ -259,9 +261,10 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     }
     AL(ctx->sc, 1);
     // zero region layout (u32 words)
-    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16, w_sort = (size_t)ctx->npass * ctx->sort_tiles * 256;
-    // ctrs[0..3]: radix tile counters; ctrs[8..9]: finished-block counters of k_cells / k_list_scan
-    ctx->zero_bytes = 4 * (w_rhist + w_ctrs + w_sort);
+    AL(ctx->histT, (size_t)ctx->npass * 256 * ctx->sort_tiles);
+    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16;
+    // ctrs[8..9]: finished-block counters of k_cells / k_list_scan
+    ctx->zero_bytes = 4 * (w_rhist + w_ctrs);
     AL(ctx->zero, ctx->zero_bytes);
 #undef AL
     if (rc != DOG_OK) {
@@ -273,7 +276,6 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->rhist = z; z += w_rhist;
     ctx->ctrs = z; z += w_ctrs;
     ctx->bt.done = ctx->ctrs + 8;
-    ctx->st_sort = z; z += w_sort;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
     std::vector<float> sent(N, kSentinelPos);
@@ -315,7 +317,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 4 + ctx->npass;   // predict, sort passes, cells, list scan, resample
+    return 4 + 3 * ctx->npass - 1;   // predict, per pass (up,) scan, down, cells, list scan, resample
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -342,25 +344,31 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     CK(cudaMemsetAsync(&ctx->sc->A, 0, sizeof(uint64_t), st));
     CK(mark("memset"));
 
-    // 1. predict (+ counts, radix histograms)
-    const uint32_t n4 = cdiv(nu, 4);
-    k_predict<<<cdiv(n4, kPredThreads), kPredThreads, 0, st>>>(
+    // 1. predict (+ counts, radix histograms, pass-0 tile histograms)
+    const uint32_t T = ctx->sort_tiles;
+    k_predict<<<T, kPredThreads, 0, st>>>(
         (const float4*)ctx->x, (const float4*)ctx->y, (const float4*)ctx->vx, (const float4*)ctx->vy,
         (float4*)ctx->px, (float4*)ctx->py, (float4*)ctx->pvx, (float4*)ctx->pvy, (uint4*)ctx->keyA,
-        dbg ? ctx->key_dbg : nullptr, ctx->counts, ctx->rhist, ctx->npass, ctx->sc, fc, a);
+        dbg ? ctx->key_dbg : nullptr, ctx->counts, ctx->rhist, ctx->histT, T, ctx->npass, ctx->sc, fc, a);
     CK(cudaGetLastError());
     CK(mark("predict"));
 
-    // 2. stable radix sort of (key, index) + offsets
+    // 2. stable LSD radix sort of (key, index), reduce-then-scan per 8-bit digit
     uint32_t *kin = ctx->keyA, *vin = nullptr, *kout = ctx->keyB, *vout = ctx->valB;
     for (int p = 0; p < ctx->npass; ++p) {
-        uint32_t* stp = ctx->st_sort + (size_t)p * ctx->sort_tiles * 256;
-        if (p == 0)
-            k_onesweep<true><<<ctx->sort_tiles, kRsThreads, 0, st>>>(kin, vin, kout, vout, nu, 8 * p,
-                                                                      ctx->rhist + 256 * p, ctx->ctrs + p, stp);
-        else
-            k_onesweep<false><<<ctx->sort_tiles, kRsThreads, 0, st>>>(kin, vin, kout, vout, nu, 8 * p,
-                                                                       ctx->rhist + 256 * p, ctx->ctrs + p, stp);
+        uint32_t* h = ctx->histT + (size_t)p * 256 * T;
+        const bool last = p == ctx->npass - 1;
+        if (p > 0) {
+            k_rs_up<<<T, kRsThreads, 0, st>>>(kin, nu, 8 * p, h, T);
+            CK(cudaGetLastError());
+        }
+        k_rs_scan<<<256, 256, 0, st>>>(h, ctx->rhist + 256 * p, T);
+        CK(cudaGetLastError());
+        uint32_t* ko = last ? nullptr : kout;
+        if (p == 0 && last) k_rs_down<true, true><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
+        else if (p == 0) k_rs_down<true, false><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
+        else if (last) k_rs_down<false, true><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
+        else k_rs_down<false, false><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
         CK(cudaGetLastError());
         static const char* sort_names[kMaxPasses] = {"sort_pass0", "sort_pass1", "sort_pass2", "sort_pass3"};
         CK(mark(sort_names[p]));
@@ -368,7 +376,6 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         uint32_t* nv = (vout == ctx->valB) ? ctx->valA : ctx->valB;
         kin = kout; vin = vout; kout = nk; vout = nv;
     }
-    ctx->skeys = kin;
     ctx->perm = vin;
 
     // 3. cells: DS predict/update, birth split, fixed point, active-cell list

@@ -2,7 +2,7 @@
 //
 // Stage map (paper -> kernel):
 //   Alg. 1 predict              -> k_predict      (+ cell counts, radix histograms)
-//   Alg. 2 sort + assign        -> k_onesweep x P (stable LSD radix sort of (key, idx))
+//   Alg. 2 sort + assign        -> dog_sort.cuh   (stable LSD radix sort of (key, idx))
 //   Alg. 3 occupancy predict/update           -> k_cells        (dog_cells.cuh)
 //   Alg. 4 persistent update    -> implicit: weights are uniform per cell (A-8, A-23)
 //   Alg. 5 slots + Alg. 7 joint CDF           -> k_list_scan    (dog_cells.cuh)
@@ -19,18 +19,21 @@ namespace dog {
 
 
 // ------------------------------------------------------------------------------------------------
-// Alg. 1 -- particle prediction.  Each thread advances 4 consecutive particles (16-byte SoA I/O).
-// Also: warp-aggregated per-cell counts n_c (for offsets) and the radix-sort digit histograms.
+// Alg. 1 -- particle prediction.  One block advances one 4096-particle sort tile (each thread 4
+// consecutive particles per step, 16-byte SoA I/O).  Also: warp-aggregated per-cell counts n_c,
+// the global radix digit histograms of every pass, and the tile's pass-0 digit histogram.
 // ------------------------------------------------------------------------------------------------
 constexpr int kPredThreads = 256;
 constexpr int kMaxPasses = 4;
+constexpr int kSortTile = 4096;     // particles per sort tile (= one k_predict block)
 
 __global__ __launch_bounds__(kPredThreads) void k_predict(
     const float4* __restrict__ x, const float4* __restrict__ y, const float4* __restrict__ vx,
     const float4* __restrict__ vy, float4* __restrict__ px, float4* __restrict__ py,
     float4* __restrict__ pvx, float4* __restrict__ pvy, uint4* __restrict__ keys,
     uint32_t* __restrict__ key_dbg, uint32_t* __restrict__ counts, uint32_t* __restrict__ rhist,
-    int npass, DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
+    uint32_t* __restrict__ hist0, uint32_t ntiles, int npass, DevScalars* __restrict__ sc, FilterConst fc,
+    StepArgs a)
 {
     __shared__ uint32_t s_hist[kMaxPasses * 256];
     for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) s_hist[i] = 0;
@@ -42,9 +45,11 @@ __global__ __launch_bounds__(kPredThreads) void k_predict(
     const float Wf = (float)fc.W, Hf = (float)fc.H;
     const uint32_t n4 = (fc.nu + 3u) >> 2;
     const int lane = threadIdx.x & 31;
+    const uint32_t g0 = blockIdx.x * (kSortTile / 4);
 
-    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g - lane < n4;
-         g += gridDim.x * blockDim.x) {
+#pragma unroll 1
+    for (int it = 0; it < kSortTile / 4 / kPredThreads; ++it) {
+        const uint32_t g = g0 + it * kPredThreads + threadIdx.x;
         const bool gv = g < n4;
         float4 X = make_float4(0, 0, 0, 0), Y = X, VX = X, VY = X;
         if (gv) { X = x[g]; Y = y[g]; VX = vx[g]; VY = vy[g]; }
@@ -88,111 +93,8 @@ __global__ __launch_bounds__(kPredThreads) void k_predict(
     __syncthreads();
     for (int i = threadIdx.x; i < npass * 256; i += blockDim.x)
         if (s_hist[i]) atomicAdd(&rhist[i], s_hist[i]);
-}
-
-// ------------------------------------------------------------------------------------------------
-// Alg. 2 -- stable LSD radix sort of (cell key, input index), one kernel per 8-bit digit
-// ("onesweep": global digit histograms from k_predict + decoupled look-back across tiles).
-// Stability: within a tile, warps own consecutive 512-element slices and rank in order
-// (match_any + running per-warp digit counters), so equal digits keep input order (A-6).
-// ------------------------------------------------------------------------------------------------
-constexpr int kRsThreads = 256, kRsItems = 16, kRsTile = kRsThreads * kRsItems, kRsWarps = 8;
-
-template <bool FIRST>
-__global__ __launch_bounds__(kRsThreads) void k_onesweep(
-    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-    uint32_t* __restrict__ vout, uint32_t n, int shift, const uint32_t* __restrict__ hist,
-    uint32_t* __restrict__ tile_ctr, uint32_t* __restrict__ status)
-{
-    __shared__ uint32_t s_keys[kRsTile];
-    __shared__ uint32_t s_vals[kRsTile];
-    __shared__ uint32_t s_whist[kRsWarps][256];
-    __shared__ uint32_t s_gofs[256];
-    __shared__ uint32_t s_lstart[256];
-    __shared__ uint32_t s_scan[kRsWarps + 1];
-    __shared__ uint32_t s_tile;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
-    for (int i = tid; i < kRsWarps * 256; i += kRsThreads) (&s_whist[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint32_t base = tile * kRsTile + warp * (kRsItems * 32);
-    const uint32_t lt = (1u << lane) - 1u;
-
-    uint32_t k[kRsItems], v[kRsItems], rk[kRsItems];
-#pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        const bool ok = idx < n;
-        k[i] = ok ? kin[idx] : 0u;
-        v[i] = FIRST ? idx : (ok ? vin[idx] : 0u);
-    }
-#pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        const bool ok = idx < n;
-        const uint32_t dig = ok ? ((k[i] >> shift) & 255u) : 0x100u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
-        const uint32_t r = __popc(peers & lt);
-        uint32_t prev = 0;
-        if (ok) prev = s_whist[warp][dig];
-        __syncwarp();
-        if (ok && r == 0) s_whist[warp][dig] = prev + __popc(peers);
-        __syncwarp();
-        rk[i] = prev + r;
-    }
-    __syncthreads();
-    // per digit (thread = digit): exclusive prefix over warps, tile count
-    uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) {
-        const uint32_t c = s_whist[w][tid];
-        s_whist[w][tid] = run;
-        run += c;
-    }
-    const uint32_t tcount = run;
-    // decoupled look-back per digit
-    uint32_t* st = status + (size_t)tile * 256 + tid;
-    uint32_t excl = 0;
-    if (tile == 0) {
-        st_relaxed(st, kStInc | tcount);
-    } else {
-        st_relaxed(st, kStAgg | tcount);
-        int j = (int)tile - 1;
-        while (true) {
-            const uint32_t s = ld_relaxed(status + (size_t)j * 256 + tid);
-            if ((s & ~kStMask) == 0) continue;
-            excl += s & kStMask;
-            if (s & kStInc) break;
-            --j;
-        }
-        st_relaxed(st, kStInc | (excl + tcount));
-    }
-    uint32_t tot;
-    const uint32_t dbase = block_excl_scan<uint32_t, kRsWarps>(hist[tid], s_scan, tot);
-    const uint32_t lstart = block_excl_scan<uint32_t, kRsWarps>(tcount, s_scan, tot);
-    s_lstart[tid] = lstart;
-    s_gofs[tid] = dbase + excl - lstart;
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        if (idx < n) {
-            const uint32_t dig = (k[i] >> shift) & 255u;
-            const uint32_t pos = s_lstart[dig] + s_whist[warp][dig] + rk[i];
-            s_keys[pos] = k[i];
-            s_vals[pos] = v[i];
-        }
-    }
-    __syncthreads();
-    const uint32_t tile0 = tile * kRsTile;
-    const uint32_t nvalid = n > tile0 ? min((uint32_t)kRsTile, n - tile0) : 0u;
-    for (uint32_t p = tid; p < nvalid; p += kRsThreads) {
-        const uint32_t key = s_keys[p];
-        const uint32_t o = s_gofs[(key >> shift) & 255u] + p;
-        kout[o] = key;
-        vout[o] = s_vals[p];
-    }
+    // this tile's pass-0 digit counts, digit-major (hist0[d * ntiles + tile])
+    hist0[(size_t)threadIdx.x * ntiles + blockIdx.x] = s_hist[threadIdx.x];
 }
 
 }  // namespace dog
