@@ -34,19 +34,20 @@ struct dog_ctx {
     uint32_t flags = 0;
     int64_t nu = 0, nu_b = 0;
     uint32_t C = 0;
-    int npass = 0;
     int64_t k = 0;
     bool poisoned = false;
     size_t nu_cap = 0;          // particle arrays padded to the sort tile
-    uint32_t sort_tiles = 0, cell_blocks = 0, cell_chunk = 0, rs_blocks = 0;
+    uint32_t tiles = 0, cell_blocks = 0, cell_chunk = 0, birth_blocks = 0;
 
     // state S_k and predicted state (SoA, f32)
     float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
     float *px = nullptr, *py = nullptr, *pvx = nullptr, *pvy = nullptr;
-    // sort
-    uint32_t *keyA = nullptr, *keyB = nullptr, *valA = nullptr, *valB = nullptr, *key_dbg = nullptr;
-    uint32_t *skeys = nullptr, *perm = nullptr;   // results (alias keyX/valX)
-    uint32_t* counts = nullptr;                   // n_c, zeroed by k_cells after use
+    // assignment (dog_sort.cuh)
+    uint32_t* keys = nullptr;                     // cell key per predicted particle
+    uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
+    TilePairs tp{};                               // runs of equal keys per tile
+    uint32_t *plist = nullptr, *ptmp = nullptr;   // per-cell run lists
+    uint32_t *counts = nullptr, *npairs = nullptr;   // n_c and runs per cell, zeroed by k_cells
     // cells
     float *m_free = nullptr, *occ = nullptr, *fre = nullptr;
     float2* mean = nullptr;
@@ -55,19 +56,15 @@ struct dog_ctx {
     CellList list{};
     BlockTotals bt{};
     uint32_t* cell2list = nullptr;
+    MomPartial* ppart = nullptr;                  // velocity sums per run
     // debug-only arrays
+    uint32_t* perm = nullptr;
     float *dbg_rho_p = nullptr, *dbg_rho_b = nullptr;
     uint64_t *dbg_Rp = nullptr, *dbg_Rb = nullptr;
     float *bx = nullptr, *by = nullptr, *bvx = nullptr, *bvy = nullptr;
     uint32_t* jidx = nullptr;
-    // moments partials of cells split over several work items
-    MomPartial* partial = nullptr;
     DevScalars* sc = nullptr;
-    // zeroed once per cycle (one memset): radix histograms, tile counters, look-back status
-    uint8_t* zero = nullptr;
-    size_t zero_bytes = 0;
-    uint32_t *rhist = nullptr, *ctrs = nullptr;
-    uint32_t* histT = nullptr;                    // [npass][256][sort_tiles] tile digit counts -> offsets
+    uint32_t* ctrs = nullptr;                     // zeroed once per cycle: finished-block counters
     // end-to-end staging
     float* meas_dev = nullptr;
     // profiling: events[step][stage boundary]
@@ -211,23 +208,20 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->nu = n_particles;
     ctx->nu_b = n_birth;
     ctx->C = (uint32_t)C;
-    int bits = 1;
-    while ((1ull << bits) <= (uint64_t)C) ++bits;   // keys 0..C
-    ctx->npass = (bits + 7) / 8;
     ctx->nu_cap = round_up((size_t)n_particles, kSortTile);
-    ctx->sort_tiles = cdiv(n_particles, kSortTile);
-    {   // cell chunks: ~4 blocks per SM, each a multiple of one 1024-cell iteration
+    ctx->tiles = cdiv(n_particles, kSortTile);
+    {   // cell chunks of 2048 cells (at most kMaxCellBlocks chunks)
         uint32_t chunk = 2u * kCellIter;
         uint32_t nblk = cdiv(C, chunk);
         while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(C, chunk); }
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
-    {   // k_resample: persistent grid, as many blocks as fit on the GPU at once
+    {   // k_births: persistent grid, as many blocks as fit on the GPU at once
         int per_sm = 0, sms = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_resample, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_births, 256, 0);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-        ctx->rs_blocks = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
+        ctx->birth_blocks = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
     }
     const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
     const bool dbg = (flags & DOG_FLAG_DEBUG) != 0;
@@ -237,10 +231,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
     AL(ctx->x, N); AL(ctx->y, N); AL(ctx->vx, N); AL(ctx->vy, N);
     AL(ctx->px, N); AL(ctx->py, N); AL(ctx->pvx, N); AL(ctx->pvy, N);
-    AL(ctx->keyA, N); AL(ctx->keyB, N); AL(ctx->valA, N); AL(ctx->valB, N);
-    AL(ctx->counts, Cs + 1);
+    AL(ctx->keys, N); AL(ctx->lperm, N);
+    AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.pre, N); AL(ctx->tp.nd, ctx->tiles);
+    AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
+    AL(ctx->counts, Cs + 1); AL(ctx->npairs, Cs + 1);
     if (dbg) {
-        AL(ctx->key_dbg, N); AL(ctx->jidx, N);
+        AL(ctx->perm, N); AL(ctx->jidx, N);
         AL(ctx->dbg_rho_p, Cs); AL(ctx->dbg_rho_b, Cs); AL(ctx->dbg_Rp, Cs); AL(ctx->dbg_Rb, Cs);
         AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
     }
@@ -251,31 +247,21 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->list.c, LC); AL(ctx->list.n, LC); AL(ctx->list.Rp, LC); AL(ctx->list.Rb, LC);
     AL(ctx->list.rho_p, LC); AL(ctx->list.start, LC); AL(ctx->list.sb, LC); AL(ctx->list.nb, LC);
     AL(ctx->list.Pl, LC); AL(ctx->list.it, LC); AL(ctx->list.bp, LC); AL(ctx->list.rp, LC);
-    AL(ctx->list.bb, LC); AL(ctx->list.rb, LC); AL(ctx->list.done, LC);
+    AL(ctx->list.bb, LC); AL(ctx->list.rb, LC);
+    AL(ctx->list.np, LC); AL(ctx->list.ps, LC); AL(ctx->list.pfill, LC); AL(ctx->list.pdone, LC);
     AL(ctx->cell2list, Cs);
     AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
-    AL(ctx->bt.P0, ctx->cell_blocks); AL(ctx->bt.item0, ctx->cell_blocks); AL(ctx->bt.s0, ctx->cell_blocks);
-    {   // work items: (nu + nu_b) / 256 full items plus at most two partial items per active cell
-        const size_t members = (size_t)n_particles + (size_t)n_birth;
-        AL(ctx->partial, members / kItem + 2 * std::min<size_t>(Cs, members) + 16);
-    }
+    AL(ctx->bt.P0, ctx->cell_blocks); AL(ctx->bt.item0, ctx->cell_blocks); AL(ctx->bt.ps0, ctx->cell_blocks);
+    AL(ctx->bt.s0, ctx->cell_blocks);
     AL(ctx->sc, 1);
-    // zero region layout (u32 words)
-    AL(ctx->histT, (size_t)ctx->npass * 256 * ctx->sort_tiles);
-    const size_t w_rhist = kMaxPasses * 256, w_ctrs = 16;
-    // ctrs[8..9]: finished-block counters of k_cells / k_list_scan
-    ctx->zero_bytes = 4 * (w_rhist + w_ctrs);
-    AL(ctx->zero, ctx->zero_bytes);
+    AL(ctx->ctrs, 16);
 #undef AL
     if (rc != DOG_OK) {
         free_all(ctx);
         delete ctx;
         return rc;
     }
-    uint32_t* z = (uint32_t*)ctx->zero;
-    ctx->rhist = z; z += w_rhist;
-    ctx->ctrs = z; z += w_ctrs;
-    ctx->bt.done = ctx->ctrs + 8;
+    ctx->bt.done = ctx->ctrs;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
     std::vector<float> sent(N, kSentinelPos);
@@ -291,6 +277,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     if (e == cudaSuccess) e = cudaMemset(ctx->cov, 0, Cs * 12);
     if (e == cudaSuccess) e = cudaMemset(ctx->sc, 0, sizeof(DevScalars));
     if (e == cudaSuccess) e = cudaMemset(ctx->counts, 0, (Cs + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->npairs, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -317,7 +304,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 4 + 3 * ctx->npass - 1;   // predict, per pass (up,) scan, down, cells, list scan, resample
+    return 8;   // predict, tilesort, cells, list_scan, pair_fill, pair_sort, resample_tiles, births
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -340,66 +327,57 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         return cudaEventRecord(ctx->pev[(size_t)ctx->prof_steps * (DOG_MAX_STAGES + 1) + mark_i++], st);
     };
     CK(mark(nullptr));
-    CK(cudaMemsetAsync(ctx->zero, 0, ctx->zero_bytes, st));
-    CK(cudaMemsetAsync(&ctx->sc->A, 0, sizeof(uint64_t), st));
-    CK(mark("memset"));
+    CK(cudaMemsetAsync(ctx->ctrs, 0, 16 * sizeof(uint32_t), st));
+    const uint32_t T = ctx->tiles;
 
-    // 1. predict (+ counts, radix histograms, pass-0 tile histograms)
-    const uint32_t T = ctx->sort_tiles;
+    // 1. predict (Alg. 1)
     k_predict<<<T, kPredThreads, 0, st>>>(
         (const float4*)ctx->x, (const float4*)ctx->y, (const float4*)ctx->vx, (const float4*)ctx->vy,
-        (float4*)ctx->px, (float4*)ctx->py, (float4*)ctx->pvx, (float4*)ctx->pvy, (uint4*)ctx->keyA,
-        dbg ? ctx->key_dbg : nullptr, ctx->counts, ctx->rhist, ctx->histT, T, ctx->npass, ctx->sc, fc, a);
+        (float4*)ctx->px, (float4*)ctx->py, (float4*)ctx->pvx, (float4*)ctx->pvy, (uint4*)ctx->keys, ctx->sc, fc, a);
     CK(cudaGetLastError());
     CK(mark("predict"));
 
-    // 2. stable LSD radix sort of (key, index), reduce-then-scan per 8-bit digit
-    uint32_t *kin = ctx->keyA, *vin = nullptr, *kout = ctx->keyB, *vout = ctx->valB;
-    for (int p = 0; p < ctx->npass; ++p) {
-        uint32_t* h = ctx->histT + (size_t)p * 256 * T;
-        const bool last = p == ctx->npass - 1;
-        if (p > 0) {
-            k_rs_up<<<T, kRsThreads, 0, st>>>(kin, nu, 8 * p, h, T);
-            CK(cudaGetLastError());
-        }
-        k_rs_scan<<<256, 256, 0, st>>>(h, ctx->rhist + 256 * p, T);
-        CK(cudaGetLastError());
-        uint32_t* ko = last ? nullptr : kout;
-        if (p == 0 && last) k_rs_down<true, true><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
-        else if (p == 0) k_rs_down<true, false><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
-        else if (last) k_rs_down<false, true><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
-        else k_rs_down<false, false><<<T, kRsThreads, 0, st>>>(kin, vin, ko, vout, nu, 8 * p, h, T);
-        CK(cudaGetLastError());
-        static const char* sort_names[kMaxPasses] = {"sort_pass0", "sort_pass1", "sort_pass2", "sort_pass3"};
-        CK(mark(sort_names[p]));
-        uint32_t* nk = (kout == ctx->keyB) ? ctx->keyA : ctx->keyB;
-        uint32_t* nv = (vout == ctx->valB) ? ctx->valA : ctx->valB;
-        kin = kout; vin = vout; kout = nk; vout = nv;
-    }
-    ctx->perm = vin;
+    // 2. assignment (Alg. 2): tile-local stable sort, runs, per-cell counts
+    k_tilesort<<<T, kTsThreads, 0, st>>>(ctx->keys, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, nu, ctx->C);
+    CK(cudaGetLastError());
+    CK(mark("tilesort"));
 
-    // 3. cells: DS predict/update, birth split, fixed point, active-cell list
+    // 3. cells: DS predict/update, birth split, fixed point, active-cell list (Alg. 3)
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
-    k_cells<<<ctx->cell_blocks, kCellThreads, 0, st>>>(ctx->counts, ctx->m_free, (const float2*)meas, ctx->occ,
-                                                       ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->list,
-                                                       ctx->cell2list, ctx->bt, ctx->cell_chunk, ctx->sc, fc,
-                                                       a.alpha);
+    k_cells<<<ctx->cell_blocks, kCellThreads, 0, st>>>(ctx->counts, ctx->npairs, ctx->m_free, (const float2*)meas,
+                                                       ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg,
+                                                       ctx->list, ctx->cell2list, ctx->bt, ctx->cell_chunk, ctx->sc,
+                                                       fc, a.alpha);
     CK(cudaGetLastError());
     CK(mark("cells"));
 
-    // 5a/7a. birth slots + joint CDF over the active list
+    // 4. slots, joint CDF, run-list offsets over the active list (Alg. 5 / Alg. 7 prefix sums)
     k_list_scan<<<ctx->cell_blocks, kLsThreads, 0, st>>>(ctx->list, ctx->bt, ctx->cell_chunk, ctx->sc, fc, a.k);
     CK(cudaGetLastError());
     CK(mark("list_scan"));
 
-    // 5b/6/7b. births, moments and resampling in one pass over the joint set
+    // 5. each cell's runs in tile order -> stable within-cell ranks
+    k_pair_fill<<<T, 256, 0, st>>>(ctx->tp, ctx->list, ctx->bt, ctx->cell_chunk, ctx->cell2list, ctx->plist, ctx->C);
+    CK(cudaGetLastError());
+    k_pair_sort<<<ctx->cell_blocks, 256, 0, st>>>(ctx->tp, ctx->list, ctx->bt, ctx->cell_chunk, ctx->plist, ctx->ptmp);
+    CK(cudaGetLastError());
+    CK(mark("pairs"));
+
+    // 6. persistent particles: moments + resampling copies; births
     Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
     NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
-    BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-    k_resample<<<ctx->rs_blocks, 256, 0, st>>>(ctx->perm, pr, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
-                                               ns, bd, ctx->mean, ctx->cov, ctx->partial, ctx->sc, fc, a.k);
+    k_resample_tiles<<<T, kRtThreads, 0, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ctx->bt, ctx->cell_chunk,
+                                               ctx->cell2list, ctx->plist, ns, dbg ? ctx->perm : nullptr, ctx->mean,
+                                               ctx->cov, ctx->ppart, ctx->sc, fc);
     CK(cudaGetLastError());
     CK(mark("resample"));
+    if (ctx->nu_b > 0) {
+        BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
+        k_births<<<ctx->birth_blocks, 256, 0, st>>>(ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk, ns, bd,
+                                                    ctx->sc, fc, a.k);
+        CK(cudaGetLastError());
+    }
+    CK(mark("births"));
     if (prof) {
         ctx->prof_nst = mark_i - 1;
         ctx->prof_steps += 1;
@@ -566,8 +544,22 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     case DOG_DBG_PRED_Y: src = ctx->py; n = nu * 4; break;
     case DOG_DBG_PRED_VX: src = ctx->pvx; n = nu * 4; break;
     case DOG_DBG_PRED_VY: src = ctx->pvy; n = nu * 4; break;
-    case DOG_DBG_KEY: if (!dbg) return DOG_E_STATE; src = ctx->key_dbg; n = nu * 4; break;
-    case DOG_DBG_PERM: src = ctx->perm; n = nu * 4; break;
+    case DOG_DBG_KEY: src = ctx->keys; n = nu * 4; break;
+    case DOG_DBG_PERM: {   // cell-sorted slots [0, n_in) from the resample kernel; sentinels follow in input order
+        if (!dbg) return DOG_E_STATE;
+        n = nu * 4;
+        if (bytes < n) return DOG_E_INVAL;
+        DevScalars s;
+        CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+        uint32_t* dst = (uint32_t*)host_dst;
+        if (s.n_in) CK(cudaMemcpy(dst, ctx->perm, s.n_in * 4, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> kk(nu);
+        CK(cudaMemcpy(kk.data(), ctx->keys, nu * 4, cudaMemcpyDeviceToHost));
+        size_t o = s.n_in;
+        for (size_t i = 0; i < nu; ++i)
+            if (kk[i] >= ctx->C) dst[o++] = (uint32_t)i;
+        return (int64_t)n;
+    }
     case DOG_DBG_RHO_P: if (!dbg) return DOG_E_STATE; src = ctx->dbg_rho_p; n = C * 4; break;
     case DOG_DBG_RHO_B: if (!dbg) return DOG_E_STATE; src = ctx->dbg_rho_b; n = C * 4; break;
     case DOG_DBG_RP: if (!dbg) return DOG_E_STATE; src = ctx->dbg_Rp; n = C * 8; break;

@@ -32,12 +32,15 @@ struct CellList {           // SoA staging, capacity nblk * chunk (>= C); entry 
     uint32_t* sb;           // first birth slot of the cell (global)        (k_list_scan)
     uint32_t* nb;           // birth slots of the cell                      (k_list_scan)
     uint64_t* Pl;           // block-local exclusive joint prefix           (k_list_scan)
-    uint32_t* it;           // block-local exclusive work-item prefix       (k_list_scan)
+    uint32_t* it;           // block-local exclusive birth work-item prefix (k_list_scan)
     uint64_t* bp;           // R_p / n_c        (even split of R_p)         (k_list_scan)
     uint32_t* rp;           // R_p mod n_c
     uint64_t* bb;           // R_b / n_b
     uint32_t* rb;           // R_b mod n_b
-    uint32_t* done;         // finished persistent work items (moments combine)
+    uint32_t* np;           // runs ("pairs") of the cell over the sort tiles   (k_cells)
+    uint32_t* ps;           // block-local exclusive prefix of np               (k_list_scan)
+    uint32_t* pfill;        // pair-list fill counter                           (k_list_scan resets)
+    uint32_t* pdone;        // finished pairs (moments combine)                 (k_list_scan resets)
 };
 
 struct BlockTotals {        // one entry per cell chunk
@@ -45,7 +48,8 @@ struct BlockTotals {        // one entry per cell chunk
     uint64_t* n0;           // sum of n_c over them -> exclusive prefix        (k_cells, last block)
     uint64_t* rb0;          // sum of R_b over them -> exclusive prefix        (k_cells, last block)
     uint64_t* P0;           // sum of J -> exclusive joint prefix of the block  (k_list_scan, last block)
-    uint32_t* item0;        // work items -> exclusive prefix of the block      (k_list_scan, last block)
+    uint32_t* item0;        // birth work items -> exclusive prefix             (k_list_scan, last block)
+    uint32_t* ps0;          // pairs -> exclusive prefix of the block           (k_list_scan, last block)
     uint32_t* s0;           // first birth slot of the block (global)           (k_list_scan)
     uint32_t* done;         // [2] finished-block counters of k_cells / k_list_scan (zeroed per cycle)
 };
@@ -129,7 +133,7 @@ __device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
 // Block b owns cells [b chunk, (b+1) chunk), 1024 per iteration; item i of thread t in an iteration
 // is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid bitmask).
 __global__ __launch_bounds__(kCellThreads) void k_cells(
-    uint32_t* __restrict__ counts, float* __restrict__ m_free, const float2* __restrict__ meas,
+    uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, CellList L, uint32_t* __restrict__ cell2list,
     BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
@@ -178,7 +182,7 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
                 occ[c] = o[i].mO;
                 free_out[c] = o[i].mF;
                 m_free[c] = o[i].mF;                    // Alg. 3 store_values
-                if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_predict
+                if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_tilesort
                 if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
                     mean[c] = make_float2(0.0f, 0.0f);
                     cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
@@ -209,6 +213,9 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
                 const uint32_t c = base + i * kCellThreads + tid;
                 const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
                 L.c[li] = c; L.n[li] = o[i].n; L.Rp[li] = o[i].Rp; L.Rb[li] = o[i].Rb; L.rho_p[li] = o[i].rp;
+                uint32_t npc = 0;
+                if (o[i].n) { npc = npairs[c]; npairs[c] = 0u; }
+                L.np[li] = npc;
                 cell2list[c] = li;
                 A_loc += o[i].Rb;
                 N_loc += o[i].n;
@@ -272,21 +279,33 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
     const uint32_t lbase = blk * chunk;
     if (tid == 0) bt.s0[blk] = (uint32_t)slot_of(A0, A, nu_b);
     uint64_t J0 = 0;                          // block-local joint prefix
-    uint32_t I0 = 0;                          // block-local work-item prefix
+    uint32_t I0 = 0;                          // block-local birth work-item prefix
+    uint32_t PS0 = 0;                         // block-local pair prefix
     for (uint32_t t0 = 0; t0 < cnt; t0 += kLsTile) {
         const uint32_t b = t0 + tid * kLsItems;
-        uint32_t n[kLsItems];
+        uint32_t n[kLsItems], npv[kLsItems];
         uint64_t Rb[kLsItems], Rp[kLsItems];
         uint64_t ns = 0, rbs = 0;
+        uint32_t pss = 0;
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
             const bool ok = b + i < cnt;
             n[i] = ok ? L.n[lbase + b + i] : 0u;
+            npv[i] = ok ? L.np[lbase + b + i] : 0u;
             Rb[i] = ok ? L.Rb[lbase + b + i] : 0ull;
             Rp[i] = ok ? L.Rp[lbase + b + i] : 0ull;
             ns += n[i];
             rbs += Rb[i];
+            pss += npv[i];
         }
+        uint32_t tps;
+        uint32_t xps = PS0 + block_excl_scan<uint32_t, kLsThreads / 32>(pss, s_c, tps);
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            if (b + i < cnt) L.ps[lbase + b + i] = xps;
+            xps += npv[i];
+        }
+        PS0 += tps;
         uint64_t tn, trb;
         const uint64_t xn = block_excl_scan<uint64_t, kLsThreads / 32>(ns, s_a, tn);
         const uint64_t xrb = block_excl_scan<uint64_t, kLsThreads / 32>(rbs, s_b, trb);
@@ -311,9 +330,10 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
                 L.rp[li] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
                 L.bb[li] = nbv ? Rb[i] / nbv : 0ull;
                 L.rb[li] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
-                L.done[li] = 0u;
+                L.pfill[li] = 0u;
+                L.pdone[li] = 0u;
                 J[i] = Rp[i] + (nbv ? Rb[i] : 0ull);
-                its[i] = (n[i] + kItem - 1) / kItem + (nbv + kItem - 1) / kItem;
+                its[i] = (nbv + kItem - 1) / kItem;
             } else {
                 J[i] = 0;
                 its[i] = 0;
@@ -343,6 +363,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
     if (tid == 0) {
         bt.P0[blk] = J0;
         bt.item0[blk] = I0;
+        bt.ps0[blk] = PS0;
         __threadfence();
         s_last = atomicAdd(&bt.done[1], 1u) == gridDim.x - 1;
     }
@@ -352,6 +373,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotal
     __threadfence();
     const uint64_t W = block_prefix_inplace<uint64_t>(bt.P0, gridDim.x, s_a);
     const uint32_t items = block_prefix_inplace<uint32_t>(bt.item0, gridDim.x, s_c);
+    block_prefix_inplace<uint32_t>(bt.ps0, gridDim.x, s_c);
     if (tid == 0) {
         sc->W = W;
         sc->n_items = items;

@@ -2,11 +2,11 @@
 //
 // Stage map (paper -> kernel):
 //   Alg. 1 predict              -> k_predict      (+ cell counts, radix histograms)
-//   Alg. 2 sort + assign        -> dog_sort.cuh   (stable LSD radix sort of (key, idx))
+//   Alg. 2 sort + assign        -> dog_sort.cuh   (tile-local stable sort + per-cell run lists)
 //   Alg. 3 occupancy predict/update           -> k_cells        (dog_cells.cuh)
 //   Alg. 4 persistent update    -> implicit: weights are uniform per cell (A-8, A-23)
 //   Alg. 5 slots + Alg. 7 joint CDF           -> k_list_scan    (dog_cells.cuh)
-//   Alg. 5 births, Alg. 6 moments, Alg. 7     -> k_resample     (dog_resample.cuh, one fused pass)
+//   Alg. 5 births, Alg. 6 moments, Alg. 7     -> k_resample_tiles + k_births (dog_resample.cuh)
 //
 // Every floating-point expression on the parity path uses explicit round-to-nearest intrinsics in
 // the operation order of DESIGN.md section 3 so the CPU oracle reproduces it bit for bit (A-21).
@@ -20,8 +20,7 @@ namespace dog {
 
 // ------------------------------------------------------------------------------------------------
 // Alg. 1 -- particle prediction.  One block advances one 4096-particle sort tile (each thread 4
-// consecutive particles per step, 16-byte SoA I/O).  Also: warp-aggregated per-cell counts n_c,
-// the global radix digit histograms of every pass, and the tile's pass-0 digit histogram.
+// consecutive particles per step, 16-byte SoA I/O) and writes the new cell keys.
 // ------------------------------------------------------------------------------------------------
 constexpr int kPredThreads = 256;
 constexpr int kMaxPasses = 4;
@@ -31,28 +30,20 @@ __global__ __launch_bounds__(kPredThreads) void k_predict(
     const float4* __restrict__ x, const float4* __restrict__ y, const float4* __restrict__ vx,
     const float4* __restrict__ vy, float4* __restrict__ px, float4* __restrict__ py,
     float4* __restrict__ pvx, float4* __restrict__ pvy, uint4* __restrict__ keys,
-    uint32_t* __restrict__ key_dbg, uint32_t* __restrict__ counts, uint32_t* __restrict__ rhist,
-    uint32_t* __restrict__ hist0, uint32_t ntiles, int npass, DevScalars* __restrict__ sc, FilterConst fc,
-    StepArgs a)
+    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
 {
-    __shared__ uint32_t s_hist[kMaxPasses * 256];
-    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) s_hist[i] = 0;
-    __syncthreads();
-
     const float w_bar = sc->w_bar;
     const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->w_pred = w_pred;
     const float Wf = (float)fc.W, Hf = (float)fc.H;
     const uint32_t n4 = (fc.nu + 3u) >> 2;
-    const int lane = threadIdx.x & 31;
     const uint32_t g0 = blockIdx.x * (kSortTile / 4);
 
 #pragma unroll 1
     for (int it = 0; it < kSortTile / 4 / kPredThreads; ++it) {
         const uint32_t g = g0 + it * kPredThreads + threadIdx.x;
-        const bool gv = g < n4;
-        float4 X = make_float4(0, 0, 0, 0), Y = X, VX = X, VY = X;
-        if (gv) { X = x[g]; Y = y[g]; VX = vx[g]; VY = vy[g]; }
+        if (g >= n4) break;
+        const float4 X = x[g], Y = y[g], VX = vx[g], VY = vy[g];
         float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w};
         float vxs[4] = {VX.x, VX.y, VX.z, VX.w}, vys[4] = {VY.x, VY.y, VY.z, VY.w};
         uint32_t ks[4];
@@ -70,31 +61,15 @@ __global__ __launch_bounds__(kPredThreads) void k_predict(
             vys[e] = __fmaf_rn(a.s_v, n3, vys[e]);
             xs[e] = xn; ys[e] = yn;
             const bool inside = (xn >= 0.0f) && (xn < Wf) && (yn >= 0.0f) && (yn < Hf);
-            const bool valid = gv && i < fc.nu;
             ks[e] = inside ? (uint32_t)__float2int_rz(yn) * (uint32_t)fc.W + (uint32_t)__float2int_rz(xn)
                            : fc.C;                                  // A-4, A-5
-            // per-cell counts (sentinel excluded), warp-aggregated
-            const uint32_t ck = (valid && inside) ? ks[e] : 0xFFFFFFFFu;
-            const uint32_t peers = __match_any_sync(0xffffffffu, ck);
-            if (ck != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&counts[ck], __popc(peers));
-            if (valid) {
-                for (int p = 0; p < npass; ++p) atomicAdd(&s_hist[p * 256 + ((ks[e] >> (8 * p)) & 255u)], 1u);
-                if (key_dbg) key_dbg[i] = ks[e];
-            }
         }
-        if (gv) {
-            px[g] = make_float4(xs[0], xs[1], xs[2], xs[3]);
-            py[g] = make_float4(ys[0], ys[1], ys[2], ys[3]);
-            pvx[g] = make_float4(vxs[0], vxs[1], vxs[2], vxs[3]);
-            pvy[g] = make_float4(vys[0], vys[1], vys[2], vys[3]);
-            keys[g] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
-        }
+        px[g] = make_float4(xs[0], xs[1], xs[2], xs[3]);
+        py[g] = make_float4(ys[0], ys[1], ys[2], ys[3]);
+        pvx[g] = make_float4(vxs[0], vxs[1], vxs[2], vxs[3]);
+        pvy[g] = make_float4(vys[0], vys[1], vys[2], vys[3]);
+        keys[g] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x)
-        if (s_hist[i]) atomicAdd(&rhist[i], s_hist[i]);
-    // this tile's pass-0 digit counts, digit-major (hist0[d * ntiles + tile])
-    hist0[(size_t)threadIdx.x * ntiles + blockIdx.x] = s_hist[threadIdx.x];
 }
 
 }  // namespace dog

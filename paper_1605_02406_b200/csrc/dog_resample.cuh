@@ -2,10 +2,9 @@
 // Eqs. 81-84), new-born particle initialisation (Alg. 5) and systematic resampling (Alg. 7,
 // Eq. 57) to the next state.
 //
-// Work items: up to 256 members of ONE cell -- either persistent particles (cell-sorted slots) or
-// birth slots -- so a warp loads its cell's parameters once, reduces the velocity sums with a plain
-// warp reduction, and cells split over several items are combined by the last item to finish, in
-// item order (deterministic).  Each warp takes a contiguous range of items.
+// Persistent particles are processed tile by tile (k_resample_tiles): the predicted state is read in
+// the tile's local sorted order (dog_sort.cuh), so no global permutation pass is needed; births by
+// per-cell work items (k_births).
 //
 // Resampling is member-driven: member r of a cell owns the fixed-point weight range [Q_r, Q_{r+1})
 // of the joint CDF (cell prefix P_c plus the even split of the cell's mass, A-23) and writes its
@@ -17,6 +16,7 @@
 #include "dog_cells.cuh"
 #include "dog_common.cuh"
 #include "dog_rng.cuh"
+#include "dog_sort.cuh"
 
 namespace dog {
 
@@ -102,12 +102,27 @@ __device__ __forceinline__ uint32_t warp_last_le(uint32_t lo, uint32_t hi, uint3
     return lo;
 }
 
-__global__ __launch_bounds__(256) void k_resample(
-    const uint32_t* __restrict__ perm, Pred pr, CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
-    NextState out, BirthDebug bdbg, float2* __restrict__ mean, float* __restrict__ cov,
-    MomPartial* __restrict__ partial, const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+constexpr int kRtThreads = 256;
+constexpr int kMaxBigUnits = 48;   // units of runs longer than one unit, per tile (<= 4096/256 + 16)
+
+// Persistent particles, one block per sort tile.  Work units: <= 256 consecutive particles of one run
+// (one cell) in the tile's local sorted order; a warp loads the run's cell parameters once.  Member
+// rank r = pre(run) + position within the run; the particle's copies go to [F(Q_r), F(Q_{r+1})).
+// Velocity sums per run are combined over a cell's runs in tile order by the last run to finish.
+__global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
+    const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
+    const uint32_t* __restrict__ cell2list, const uint32_t* __restrict__ plist, NextState out,
+    uint32_t* __restrict__ perm_dbg, float2* __restrict__ mean, float* __restrict__ cov,
+    MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
-    const int tid = threadIdx.x, lane = tid & 31;
+    __shared__ uint16_t s_lp[kSortTile];
+    __shared__ uint32_t s_unit[kSortTile + 32];        // (run << 5) | unit-within-run
+    __shared__ uint32_t s_scan[9];
+    __shared__ uint32_t s_nu;
+    __shared__ MomPartial s_big[kMaxBigUnits];
+    __shared__ uint16_t s_bigslot[kSortTile];           // first big-unit slot of a run (runs with > 1 unit)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x) {
@@ -115,152 +130,197 @@ __global__ __launch_bounds__(256) void k_resample(
             if (out.jidx) out.jidx[i] = 0xFFFFFFFFu;
         }
     }
-    const uint32_t n_items = sc->n_items;
+    const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
+    if (n == 0) return;
+    const uint32_t nd = tp.nd[t];
     const float w_pred = sc->w_pred;
+    for (uint32_t p = tid; p < n; p += kRtThreads) s_lp[p] = lperm[base + p];
+
+    // work units: runs inside the grid, split into 256-particle units
+    {
+        uint32_t cnt_units = 0, cnt_big = 0;
+        uint32_t u_of[16], b_of[16];
+        const uint32_t r0 = tid * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t r = r0 + i;
+            uint32_t u = 0;
+            if (r < nd && tp.key[base + r] < fc.C) u = ((uint32_t)tp.cnt[base + r] + 1u + kItem - 1) / kItem;
+            u_of[i] = u;
+            b_of[i] = u > 1 ? u : 0u;
+            cnt_units += u;
+            cnt_big += b_of[i];
+        }
+        uint32_t tot_u, tot_b;
+        uint32_t uo = block_excl_scan<uint32_t, 8>(cnt_units, s_scan, tot_u);
+        uint32_t bo = block_excl_scan<uint32_t, 8>(cnt_big, s_scan, tot_b);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t r = r0 + i;
+            for (uint32_t k = 0; k < u_of[i]; ++k) s_unit[uo + k] = (r << 5) | k;
+            if (b_of[i]) s_bigslot[r] = (uint16_t)bo;
+            uo += u_of[i];
+            bo += b_of[i];
+        }
+        if (tid == 0) s_nu = tot_u;
+    }
+    __syncthreads();
+    const uint32_t nunits = s_nu;
+
+    for (uint32_t u = warp; u < nunits; u += kRtThreads / 32) {
+        const uint32_t code = s_unit[u];
+        const uint32_t r = code >> 5, k = code & 31u;
+        const uint32_t key = tp.key[base + r];
+        const uint32_t first = tp.first[base + r], cnt = (uint32_t)tp.cnt[base + r] + 1u;
+        const uint32_t pre = tp.pre[base + r];
+        const uint32_t li = cell2list[key];
+        const uint32_t cn = L.n[li], start = L.start[li];
+        const uint64_t P = bt.P0[li / chunk] + L.Pl[li];
+        const uint64_t bp = L.bp[li];
+        const uint32_t rpm = L.rp[li];
+        const uint32_t jbase = start + L.sb[li];
+        const uint32_t o0 = k * kItem, m = min(kItem, cnt - o0);
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (uint32_t q0 = 0; q0 < m; q0 += 32) {
+            const bool valid = q0 + lane < m;
+            const uint32_t p = first + o0 + q0 + lane;          // local sorted position
+            const uint32_t mr = pre + o0 + q0 + lane;           // member rank within the cell
+            float X = 0.f, Y = 0.f, VX = 0.f, VY = 0.f;
+            uint32_t src = 0;
+            if (valid) {
+                src = base + s_lp[p];
+                X = pr.x[src]; Y = pr.y[src]; VX = pr.vx[src]; VY = pr.vy[src];
+                const double a = (double)VX, bq = (double)VY;
+                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                if (perm_dbg) perm_dbg[start + mr] = src;
+            }
+            if (rc.W) {
+                const uint64_t Q0 = P + (uint64_t)mr * bp + min(mr, rpm);
+                const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
+                uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                if (valid && (lane == 31 || q0 + lane + 1 == m)) F1 = fcount(Q0 + bp + (mr < rpm ? 1u : 0u), rc);
+                if (valid) {
+                    for (uint32_t o = F0; o < F1; ++o) {
+                        out.x[o] = X; out.y[o] = Y; out.vx[o] = VX; out.vy[o] = VY;
+                        if (out.jidx) out.jidx[o] = jbase + mr;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
+        if (lane == 0) {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] = acc[i];
+            if (cnt <= kItem) ppart[base + r] = mp;         // single-unit run
+            else s_big[s_bigslot[r] + k] = mp;
+        }
+        (void)cn;
+    }
+    __syncthreads();
+    // runs spanning several units: sum their units in order
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        const uint32_t cnt = (uint32_t)tp.cnt[base + r] + 1u;
+        if (cnt > kItem && tp.key[base + r] < fc.C) {
+            const uint32_t nu_r = (cnt + kItem - 1) / kItem, s0 = s_bigslot[r];
+            MomPartial mp = s_big[s0];
+            for (uint32_t k = 1; k < nu_r; ++k)
+#pragma unroll
+                for (int i = 0; i < 5; ++i) mp.s[i] += s_big[s0 + k].s[i];
+            ppart[base + r] = mp;
+        }
+    }
+    __syncthreads();
+    // cell completion: the last of a cell's runs to finish combines them in tile order (deterministic)
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        const uint32_t key = tp.key[base + r];
+        if (key >= fc.C) continue;
+        const uint32_t li = cell2list[key];
+        const uint32_t m = L.np[li];
+        if (m == 1) {
+            finalize_cell(key, ppart[base + r].s, L.n[li], L.rho_p[li], w_pred, mean, cov);
+            continue;
+        }
+        __threadfence();
+        if (atomicAdd(&L.pdone[li], 1u) != m - 1) continue;
+        __threadfence();
+        const uint32_t* pl = plist + bt.ps0[li / chunk] + L.ps[li];
+        double s[5] = {0, 0, 0, 0, 0};
+        for (uint32_t q = 0; q < m; ++q) {
+            const double* ps = ppart[pl[q]].s;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s[i] += __ldcg(ps + i);
+        }
+        finalize_cell(key, s, L.n[li], L.rho_p[li], w_pred, mean, cov);
+    }
+}
+
+// New-born particles (Alg. 5): work items of <= 256 birth slots of one cell; each warp takes a
+// contiguous range of items.  State from the slot's Philox draw; copies as for persistent members.
+__global__ __launch_bounds__(256) void k_births(CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
+                                                NextState out, BirthDebug bdbg, const DevScalars* __restrict__ sc,
+                                                FilterConst fc, int64_t k)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    const RsConst rc = make_rsconst(sc, fc.nu);
+    const uint32_t n_items = sc->n_items;
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
     const uint32_t per = (n_items + nwarps - 1) / nwarps;
     uint32_t q = gw * per;
     const uint32_t q_end = min(q + per, n_items);
     if (q >= q_end) return;
-
-    // locate the first item: chunk b, then entry li within the chunk
     uint32_t b = warp_last_le(0u, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
     uint32_t lbase = b * chunk;
-    uint32_t li = warp_last_le(lbase, lbase + bt.cnt[b], q - bt.item0[b],
-                               [&](uint32_t i) { return L.it[i]; });
+    uint32_t li = warp_last_le(lbase, lbase + bt.cnt[b], q - bt.item0[b], [&](uint32_t i) { return L.it[i]; });
     uint32_t sub = q - bt.item0[b] - L.it[li];
-
     while (true) {
-        // cell parameters (uniform across the warp)
         const uint32_t c = L.c[li], n = L.n[li], start = L.start[li], nb = L.nb[li];
-        const uint32_t np = (n + kItem - 1) / kItem;
         const uint64_t P = bt.P0[b] + L.Pl[li];
-        if (sub < np) {
-            // ---------------- persistent members [r0, r0 + m) of cell c
-            const uint32_t r0 = sub * kItem, m = min(kItem, n - r0);
-            const uint64_t bp = L.bp[li];
-            const uint32_t rpm = L.rp[li];
-            const uint32_t jbase = start + L.sb[li];
-            double acc[5] = {0, 0, 0, 0, 0};
-            for (uint32_t t0 = 0; t0 < m; t0 += 4 * 32) {
-                // batch: 4 perm loads, then 16 gathers in flight per lane, then compute
-                uint32_t src[4];
-                float X[4], Y[4], VX[4], VY[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t t = t0 + 32 * u + lane;
-                    src[u] = t < m ? perm[start + r0 + t] : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const bool valid = t0 + 32 * u + lane < m;
-                    X[u] = valid ? pr.x[src[u]] : 0.f;
-                    Y[u] = valid ? pr.y[src[u]] : 0.f;
-                    VX[u] = valid ? pr.vx[src[u]] : 0.f;
-                    VY[u] = valid ? pr.vy[src[u]] : 0.f;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const uint32_t t = t0 + 32 * u;
-                    if (t >= m) break;                              // warp-uniform
-                    const bool valid = t + lane < m;
-                    const uint32_t r = r0 + t + lane;
-                    const double a = (double)VX[u], bq = (double)VY[u];
-                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                    if (rc.W) {
-                        const uint64_t Q0 = P + (uint64_t)r * bp + min(r, rpm);
-                        const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
-                        uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                        if (valid && (lane == 31 || t + lane + 1 == m))
-                            F1 = fcount(Q0 + bp + (r < rpm ? 1u : 0u), rc);
-                        if (valid) {
-                            for (uint32_t o = F0; o < F1; ++o) {
-                                out.x[o] = X[u]; out.y[o] = Y[u]; out.vx[o] = VX[u]; out.vy[o] = VY[u];
-                                if (out.jidx) out.jidx[o] = jbase + r;
-                            }
-                        }
-                    }
-                }
+        const uint32_t r0 = sub * kItem, m = min(kItem, nb - r0);
+        const uint64_t bb = L.bb[li];
+        const uint32_t rbm = L.rb[li], sb = L.sb[li];
+        const uint64_t PB = P + L.Rp[li];
+        const uint32_t jbase = start + sb + n;
+        const uint32_t col = c % (uint32_t)fc.W, row = c / (uint32_t)fc.W;
+        const float colf = (float)col, rowf = (float)row;
+        const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
+        for (uint32_t t = 0; t < m; t += 32) {
+            const bool valid = t + lane < m;
+            const uint32_t r = r0 + t + lane;
+            const uint32_t s = sb + r;
+            const Philox4 d = draw(fc.seed, s, k, STAGE_BIRTH);
+            float bx = __fadd_rn(colf, unit24(d.r0));
+            float by = __fadd_rn(rowf, unit24(d.r1));
+            if (bx >= cx1) bx = __int_as_float(__float_as_int(cx1) - 1);    // nextafter(col+1, 0) (A-16)
+            if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
+            float n0, n1;
+            box_muller(d.r2, d.r3, n0, n1);
+            float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
+            if (fc.v_max > 0.0f) {
+                bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
+                bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
             }
-#pragma unroll
-            for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
-            if (np == 1) {
-                if (lane == 0) finalize_cell(c, acc, n, L.rho_p[li], w_pred, mean, cov);
-            } else {
-                // several items: publish this item's sums; the last one to finish combines in order
-                const uint32_t q0 = bt.item0[b] + L.it[li];   // the cell's first item
-                uint32_t old = 0;
-                if (lane == 0) {
-                    MomPartial p;
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) p.s[i] = acc[i];
-                    partial[q0 + sub] = p;
-                    __threadfence();
-                    old = atomicAdd(&L.done[li], 1u);
-                }
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == np - 1) {
-                    __threadfence();
-                    double s[5] = {0, 0, 0, 0, 0};
-                    if (lane == 0) {
-                        for (uint32_t j = 0; j < np; ++j) {
-                            const double* ps = (const double*)&partial[q0 + j];
-#pragma unroll
-                            for (int i = 0; i < 5; ++i) s[i] += __ldcg(ps + i);
-                        }
-                        finalize_cell(c, s, n, L.rho_p[li], w_pred, mean, cov);
-                    }
-                }
-            }
-        } else {
-            // ---------------- birth slots [r0, r0 + m) of cell c (Alg. 5): state from the slot's draw
-            const uint32_t r0 = (sub - np) * kItem, m = min(kItem, nb - r0);
-            const uint64_t bb = L.bb[li];
-            const uint32_t rbm = L.rb[li], sb = L.sb[li];
-            const uint64_t PB = P + L.Rp[li];
-            const uint32_t jbase = start + sb + n;
-            const uint32_t col = c % (uint32_t)fc.W, row = c / (uint32_t)fc.W;
-            const float colf = (float)col, rowf = (float)row;
-            const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
-            for (uint32_t t = 0; t < m; t += 32) {
-                const bool valid = t + lane < m;
-                const uint32_t r = r0 + t + lane;
-                const uint32_t s = sb + r;
-                const Philox4 d = draw(fc.seed, s, k, STAGE_BIRTH);
-                float bx = __fadd_rn(colf, unit24(d.r0));
-                float by = __fadd_rn(rowf, unit24(d.r1));
-                if (bx >= cx1) bx = __int_as_float(__float_as_int(cx1) - 1);    // nextafter(col+1, 0) (A-16)
-                if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
-                float n0, n1;
-                box_muller(d.r2, d.r3, n0, n1);
-                float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
-                if (fc.v_max > 0.0f) {
-                    bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
-                    bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
-                }
-                if (valid && bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
-                if (rc.W) {
-                    const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
-                    const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
-                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                    if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bb + (r < rbm ? 1u : 0u), rc);
-                    if (valid) {
-                        for (uint32_t o = F0; o < F1; ++o) {
-                            out.x[o] = bx; out.y[o] = by; out.vx[o] = bvx; out.vy[o] = bvy;
-                            if (out.jidx) out.jidx[o] = jbase + r;
-                        }
+            if (valid && bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
+            if (rc.W) {
+                const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
+                const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
+                uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bb + (r < rbm ? 1u : 0u), rc);
+                if (valid) {
+                    for (uint32_t o = F0; o < F1; ++o) {
+                        out.x[o] = bx; out.y[o] = by; out.vx[o] = bvx; out.vy[o] = bvy;
+                        if (out.jidx) out.jidx[o] = jbase + r;
                     }
                 }
             }
         }
-        // next item
         if (++q >= q_end) break;
-        const uint32_t nitems_cell = np + (nb + kItem - 1) / kItem;
-        if (++sub < nitems_cell) continue;
+        if (++sub < (nb + kItem - 1) / kItem) continue;
+        sub = 0;
         const uint32_t chunk_end = b + 1 < nblk ? bt.item0[b + 1] : n_items;
-        if (q >= chunk_end)                    // past this chunk's items: find the chunk holding q
-            b = warp_last_le(b, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
+        if (q >= chunk_end) b = warp_last_le(b, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
         const uint32_t lo = q >= chunk_end ? b * chunk : li + 1;
         lbase = b * chunk;
         li = warp_last_le(lo, lbase + bt.cnt[b], q - bt.item0[b], [&](uint32_t i) { return L.it[i]; });

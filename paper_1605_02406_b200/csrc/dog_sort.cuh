@@ -1,117 +1,60 @@
-// dog_sort.cuh -- Alg. 2: stable sort of the predicted particles by cell key.
+// dog_sort.cuh -- Alg. 2: particle-to-cell assignment by a stable key sort, B200 style.
 //
-// LSD radix sort of (key, input index) with 8-bit digits, reduce-then-scan per pass (no look-back):
-//   up   : per 4096-element tile, the digit histogram of the pass (pass 0: fused into k_predict)
-//   scan : per digit, exclusive prefix over tiles + the digit's global base -> each tile's offsets
-//   down : per tile, stable local ranking (warps own consecutive 512-element slices and rank in
-//          order with match_any + running per-warp digit counters, A-6), then scatter.
-// Sorting (key, index) pairs with a stable LSD sort orders ties by input index, exactly the
-// oracle's stable sort.  The last pass writes only the permutation (cell-sorted slot -> index).
+// The paper sorts the whole particle array by cell index (Thrust) and takes first/last indices per
+// cell.  What the rest of the cycle needs from that sort is, for every particle, its cell and its
+// stable rank among the particles of that cell (A-6: ties by input index).  Because the input is the
+// previous resampling output -- already ordered by source cell -- and particles move a few cells per
+// step, every 4096-particle tile holds few distinct cells.  So:
+//   k_tilesort  : per tile, a stable LSD radix sort of the tile's keys in shared memory (only the
+//                 digits the tile's key range needs), runs of equal keys -> "pairs" (tile, cell, count,
+//                 first local position), the local permutation, and per-cell counts n_c / pair counts.
+//   k_pair_fill : each pair appends itself to its cell's pair list (position by atomic, unordered).
+//   k_pair_sort : per active cell, its pair list sorted by tile (keys are unique: one run per tile per
+//                 cell) and the exclusive prefix of the counts = the rank of each run's first particle
+//                 among the cell's particles in input order.
+// The global order (cell, input index) of the paper's sort is thereby fully determined without moving
+// any particle: a particle's cell-sorted slot is start_c + pre(tile, run) + (position within the run).
 #pragma once
 #include <cstdint>
+#include "dog_cells.cuh"
 #include "dog_common.cuh"
 #include "dog_kernels.cuh"
 
 namespace dog {
 
-constexpr int kRsThreads = 256, kRsItems = 16, kRsWarps = 8;
-static_assert(kRsThreads * kRsItems == kSortTile, "sort tile");
+constexpr int kTsThreads = 256, kTsItems = 16, kTsWarps = 8;
+static_assert(kTsThreads * kTsItems == kSortTile, "sort tile");
 
-// Digit histogram of pass `shift` for every tile of the (already permuted) key array.
-__global__ __launch_bounds__(kRsThreads) void k_rs_up(const uint32_t* __restrict__ kin, uint32_t n, int shift,
-                                                      uint32_t* __restrict__ hist, uint32_t ntiles)
-{
-    __shared__ uint32_t s_h[kRsWarps][256];
-    const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < kRsWarps * 256; i += kRsThreads) (&s_h[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t base = blockIdx.x * kSortTile;
-#pragma unroll
-    for (int i = 0; i < kRsItems / 4; ++i) {
-        const uint32_t idx = base + (i * kRsThreads + tid) * 4;
-        if (idx + 3 < n) {
-            const uint4 k4 = *reinterpret_cast<const uint4*>(kin + idx);
-            atomicAdd(&s_h[warp][(k4.x >> shift) & 255u], 1u);
-            atomicAdd(&s_h[warp][(k4.y >> shift) & 255u], 1u);
-            atomicAdd(&s_h[warp][(k4.z >> shift) & 255u], 1u);
-            atomicAdd(&s_h[warp][(k4.w >> shift) & 255u], 1u);
-        } else {
-            for (uint32_t e = idx; e < n && e < idx + 4; ++e) atomicAdd(&s_h[warp][(kin[e] >> shift) & 255u], 1u);
-        }
-    }
-    __syncthreads();
-    uint32_t t = 0;
-#pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) t += s_h[w][tid];
-    hist[(size_t)tid * ntiles + blockIdx.x] = t;
-}
+struct TilePairs {          // per tile t: entries [t*4096, t*4096 + nd[t])
+    uint32_t* key;          // cell key of the run (C = outside the grid)
+    uint16_t* first;        // first local sorted position of the run
+    uint16_t* cnt;          // particles in the run (1..4096, stored as cnt-1)
+    uint32_t* pre;          // rank of the run's first particle within its cell        (k_pair_sort)
+    uint32_t* nd;           // [tiles] runs of the tile
+};
 
-// One block per digit d: hist[d][*] (counts per tile) -> global output offset of each tile's first
-// element with digit d = (elements with smaller digits) + (digit-d elements of earlier tiles).
-__global__ __launch_bounds__(256) void k_rs_scan(uint32_t* __restrict__ hist, const uint32_t* __restrict__ dhist,
-                                                 uint32_t ntiles)
+// Stable LSD radix pass over the tile in shared memory: warps own consecutive 512-element slices of
+// the current order and rank by 8-bit digit with match_any + running per-warp counters.
+__device__ __forceinline__ void tile_radix_pass(uint32_t* s_k, uint16_t* s_i, uint32_t (*s_whist)[256],
+                                                uint32_t* s_scan, uint32_t kmin, int shift, uint32_t n)
 {
-    __shared__ uint32_t s_scan[9];
-    __shared__ uint32_t s_base;
-    const int d = blockIdx.x, tid = threadIdx.x;
-    uint32_t part = 0;
-    for (int i = tid; i < d; i += 256) part += dhist[i];
-    part = warp_sum(part);
-    if ((tid & 31) == 0) s_scan[tid >> 5] = part;
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t b = 0;
-        for (int w = 0; w < 8; ++w) b += s_scan[w];
-        s_base = b;
-    }
-    __syncthreads();
-    uint32_t carry = s_base;
-    uint32_t* row = hist + (size_t)d * ntiles;
-    for (uint32_t t0 = 0; t0 < ntiles; t0 += 256 * 8) {
-        uint32_t v[8], sum = 0;
-        const uint32_t b = t0 + tid * 8;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { v[i] = b + i < ntiles ? row[b + i] : 0u; sum += v[i]; }
-        uint32_t tot;
-        uint32_t run = carry + block_excl_scan<uint32_t, 8>(sum, s_scan, tot);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) { if (b + i < ntiles) row[b + i] = run; run += v[i]; }
-        carry += tot;
-    }
-}
-
-template <bool FIRST, bool LAST>
-__global__ __launch_bounds__(kRsThreads) void k_rs_down(
-    const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
-    uint32_t* __restrict__ vout, uint32_t n, int shift, const uint32_t* __restrict__ offs, uint32_t ntiles)
-{
-    __shared__ uint32_t s_keys[kSortTile];
-    __shared__ uint32_t s_vals[kSortTile];
-    __shared__ uint32_t s_whist[kRsWarps][256];
-    __shared__ uint32_t s_gofs[256];
-    __shared__ uint32_t s_lstart[256];
-    __shared__ uint32_t s_scan[kRsWarps + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < kRsWarps * 256; i += kRsThreads) (&s_whist[0][0])[i] = 0;
-    const uint32_t tile = blockIdx.x;
-    const uint32_t base = tile * kSortTile + warp * (kRsItems * 32);
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t goff = offs[(size_t)tid * ntiles + tile];      // this tile's offset for digit tid
-    __syncthreads();
-
-    uint32_t k[kRsItems], v[kRsItems], rk[kRsItems];
+    for (int i = tid; i < kTsWarps * 256; i += kTsThreads) (&s_whist[0][0])[i] = 0;
+    uint32_t k[kTsItems], rk[kTsItems];
+    uint16_t v[kTsItems];
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        const bool ok = idx < n;
-        k[i] = ok ? kin[idx] : 0u;
-        v[i] = FIRST ? idx : (ok ? vin[idx] : 0u);
+    for (int i = 0; i < kTsItems; ++i) {
+        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
+        k[i] = s_k[p];
+        v[i] = s_i[p];
     }
+    __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        const bool ok = idx < n;
-        const uint32_t dig = ok ? ((k[i] >> shift) & 255u) : 0x100u;
+    for (int i = 0; i < kTsItems; ++i) {
+        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
+        const bool ok = p < n;
+        const uint32_t dig = ok ? (((k[i] - kmin) >> shift) & 255u) : 0x100u;
         const uint32_t peers = __match_any_sync(0xffffffffu, dig);
         const uint32_t r = __popc(peers & lt);
         uint32_t prev = 0;
@@ -124,34 +67,166 @@ __global__ __launch_bounds__(kRsThreads) void k_rs_down(
     __syncthreads();
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < kRsWarps; ++w) {
+    for (int w = 0; w < kTsWarps; ++w) {
         const uint32_t c = s_whist[w][tid];
         s_whist[w][tid] = run;
         run += c;
     }
     uint32_t tot;
-    const uint32_t lstart = block_excl_scan<uint32_t, kRsWarps>(run, s_scan, tot);
-    s_lstart[tid] = lstart;
-    s_gofs[tid] = goff - lstart;
+    const uint32_t lstart = block_excl_scan<uint32_t, kTsWarps>(run, s_scan, tot);
+#pragma unroll
+    for (int w = 0; w < kTsWarps; ++w) s_whist[w][tid] += lstart;
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
-        const uint32_t idx = base + i * 32 + lane;
-        if (idx < n) {
-            const uint32_t dig = (k[i] >> shift) & 255u;
-            const uint32_t pos = s_lstart[dig] + s_whist[warp][dig] + rk[i];
-            s_keys[pos] = k[i];
-            s_vals[pos] = v[i];
+    for (int i = 0; i < kTsItems; ++i) {
+        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
+        if (p < n) {
+            const uint32_t dig = ((k[i] - kmin) >> shift) & 255u;
+            const uint32_t pos = s_whist[warp][dig] + rk[i];
+            s_k[pos] = k[i];
+            s_i[pos] = v[i];
         }
     }
     __syncthreads();
-    const uint32_t tile0 = tile * kSortTile;
-    const uint32_t nvalid = n > tile0 ? min((uint32_t)kSortTile, n - tile0) : 0u;
-    for (uint32_t p = tid; p < nvalid; p += kRsThreads) {
-        const uint32_t key = s_keys[p];
-        const uint32_t o = s_gofs[(key >> shift) & 255u] + p;
-        if (!LAST || kout) kout[o] = key;
-        vout[o] = s_vals[p];
+}
+
+__global__ __launch_bounds__(kTsThreads) void k_tilesort(const uint32_t* __restrict__ keys, uint16_t* __restrict__ lperm,
+                                                         TilePairs tp, uint32_t* __restrict__ counts,
+                                                         uint32_t* __restrict__ npairs, uint32_t nu, uint32_t C)
+{
+    __shared__ uint32_t s_k[kSortTile];
+    __shared__ uint16_t s_i[kSortTile];
+    __shared__ uint32_t s_whist[kTsWarps][256];
+    __shared__ uint16_t s_start[kSortTile + 1];
+    __shared__ uint32_t s_scan[kTsWarps + 1];
+    __shared__ uint32_t s_min[kTsWarps], s_max[kTsWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t base = blockIdx.x * kSortTile;
+    const uint32_t n = nu > base ? min((uint32_t)kSortTile, nu - base) : 0u;
+
+    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll
+    for (int i = 0; i < kTsItems / 4; ++i) {
+        const uint32_t l = (i * kTsThreads + tid) * 4;
+        uint4 k4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (l + 3 < n) k4 = *reinterpret_cast<const uint4*>(keys + base + l);
+        else {
+            if (l < n) k4.x = keys[base + l];
+            if (l + 1 < n) k4.y = keys[base + l + 1];
+            if (l + 2 < n) k4.z = keys[base + l + 2];
+        }
+        const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            s_k[l + e] = kk[e];
+            s_i[l + e] = (uint16_t)(l + e);
+            if (l + e < n) { kmin = min(kmin, kk[e]); kmax = max(kmax, kk[e]); }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
+        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+    }
+    if (lane == 0) { s_min[warp] = kmin; s_max[warp] = kmax; }
+    __syncthreads();
+    kmin = s_min[0]; kmax = s_max[0];
+#pragma unroll
+    for (int w = 1; w < kTsWarps; ++w) { kmin = min(kmin, s_min[w]); kmax = max(kmax, s_max[w]); }
+    const uint32_t range = n ? kmax - kmin : 0u;
+    const int bits = range ? 32 - __clz(range) : 0;
+    for (int shift = 0; shift < bits; shift += 8) tile_radix_pass(s_k, s_i, s_whist, s_scan, kmin, shift, n);
+
+    // runs of equal keys in sorted order -> pairs
+    const uint32_t p0 = tid * kTsItems;
+    uint32_t flags = 0, nrun = 0;
+#pragma unroll
+    for (int i = 0; i < kTsItems; ++i) {
+        const uint32_t p = p0 + i;
+        const bool head = p < n && (p == 0 || s_k[p] != s_k[p - 1]);
+        flags |= (head ? 1u : 0u) << i;
+        nrun += head ? 1u : 0u;
+    }
+    uint32_t nd;
+    uint32_t j = block_excl_scan<uint32_t, kTsWarps>(nrun, s_scan, nd);
+#pragma unroll
+    for (int i = 0; i < kTsItems; ++i)
+        if ((flags >> i) & 1u) s_start[j++] = (uint16_t)(p0 + i);
+    if (tid == 0) { s_start[nd] = (uint16_t)n; tp.nd[blockIdx.x] = nd; }
+    __syncthreads();
+    for (uint32_t r = tid; r < nd; r += kTsThreads) {
+        const uint32_t f = s_start[r], c = (uint32_t)s_start[r + 1] - f;
+        const uint32_t key = s_k[f];
+        tp.key[base + r] = key;
+        tp.first[base + r] = (uint16_t)f;
+        tp.cnt[base + r] = (uint16_t)(c - 1);
+        if (key < C) {
+            atomicAdd(&counts[key], c);
+            atomicAdd(&npairs[key], 1u);
+        }
+    }
+    for (uint32_t p = tid; p < n; p += kTsThreads) lperm[base + p] = s_i[p];
+}
+
+// Each pair appends itself (tile << 12 | run) to its cell's list (unordered; k_pair_sort orders it).
+__global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, BlockTotals bt, uint32_t chunk,
+                                                   const uint32_t* __restrict__ cell2list, uint32_t* __restrict__ plist,
+                                                   uint32_t C)
+{
+    const uint32_t t = blockIdx.x, base = t * kSortTile;
+    const uint32_t nd = tp.nd[t];
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
+        const uint32_t key = tp.key[base + r];
+        if (key >= C) continue;
+        const uint32_t li = cell2list[key];
+        const uint32_t slot = atomicAdd(&L.pfill[li], 1u);
+        plist[bt.ps0[li / chunk] + L.ps[li] + slot] = (t << 12) | r;
+    }
+}
+
+// Per active cell: sort its pair list by tile (warp-cooperative rank-by-count for any length; lists
+// are short), then the exclusive prefix of the run counts in that order -> pre of every run.
+__global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, BlockTotals bt, uint32_t chunk,
+                                                   uint32_t* __restrict__ plist, uint32_t* __restrict__ ptmp)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.x;
+    const uint32_t cnt = bt.cnt[b], lbase = b * chunk;
+    for (uint32_t e = warp; e < cnt; e += blockDim.x >> 5) {
+        const uint32_t li = lbase + e;
+        const uint32_t m = L.np[li];
+        if (m == 0) continue;
+        uint32_t* pl = plist + bt.ps0[b] + L.ps[li];
+        if (m == 1) {                                // (tile << 12 | run) is the run's slot index
+            if (lane == 0) tp.pre[pl[0]] = 0u;
+            continue;
+        }
+        uint32_t* tmp = ptmp + bt.ps0[b] + L.ps[li];
+        // rank of each entry = number of smaller entries (entries are distinct)
+        for (uint32_t a = lane; a < m; a += 32) {
+            const uint32_t va = pl[a];
+            uint32_t rank = 0;
+            for (uint32_t q = 0; q < m; ++q) rank += pl[q] < va ? 1u : 0u;
+            tmp[rank] = va;
+        }
+        __syncwarp();
+        // exclusive prefix of counts in tile order
+        uint32_t carry = 0;
+        for (uint32_t a0 = 0; a0 < m; a0 += 32) {
+            const uint32_t a = a0 + lane;
+            uint32_t v = 0, c = 0;
+            if (a < m) {
+                v = tmp[a];
+                c = (uint32_t)tp.cnt[v] + 1u;
+            }
+            const uint32_t incl = warp_incl_scan(c, lane);
+            if (a < m) {
+                tp.pre[v] = carry + incl - c;
+                pl[a] = v;                   // the cell's list, now in tile order
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        __syncwarp();
     }
 }
 
