@@ -102,13 +102,40 @@ __device__ __forceinline__ uint32_t warp_last_le(uint32_t lo, uint32_t hi, uint3
     return lo;
 }
 
-constexpr int kRtThreads = 256;
-constexpr int kMaxBigUnits = 48;   // units of runs longer than one unit, per tile (<= 4096/256 + 16)
+constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
 
-// Persistent particles, one block per sort tile.  Work units: <= 256 consecutive particles of one run
-// (one cell) in the tile's local sorted order; a warp loads the run's cell parameters once.  Member
-// rank r = pre(run) + position within the run; the particle's copies go to [F(Q_r), F(Q_{r+1})).
-// Velocity sums per run are combined over a cell's runs in tile order by the last run to finish.
+struct RunParams {
+    uint32_t j, first, end, pre, key, li, jbase, rpm;
+    uint64_t P, bp;
+    bool in_grid;
+};
+
+__device__ __forceinline__ RunParams load_run(uint32_t j, uint32_t base, const uint16_t* s_first, TilePairs tp,
+                                              CellList L, BlockTotals bt, uint32_t chunk,
+                                              const uint32_t* __restrict__ cell2list, uint32_t C)
+{
+    RunParams q;
+    q.j = j;
+    q.first = s_first[j];
+    q.end = s_first[j + 1];
+    q.key = tp.key[base + j];
+    q.in_grid = q.key < C;
+    if (q.in_grid) {
+        q.pre = tp.pre[base + j];
+        q.li = cell2list[q.key];
+        q.P = bt.P0[q.li / chunk] + L.Pl[q.li];
+        q.bp = L.bp[q.li];
+        q.rpm = L.rp[q.li];
+        q.jbase = L.start[q.li] + L.sb[q.li];
+    }
+    return q;
+}
+
+// Persistent particles, one block per sort tile; thread t owns the tile's local sorted positions
+// [16t, 16t+16).  Position p of run j (cell c) is member r = pre(j) + (p - first(j)) of cell c: its
+// copies go to [F(Q_r), F(Q_{r+1})).  Velocity sums are accumulated per run segment; segments that
+// span threads are combined in thread order, and a cell's runs over the tiles in tile order by the
+// last run to finish (deterministic).
 __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
     const uint32_t* __restrict__ cell2list, const uint32_t* __restrict__ plist, NextState out,
@@ -116,12 +143,9 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
     __shared__ uint16_t s_lp[kSortTile];
-    __shared__ uint32_t s_unit[kSortTile + 32];        // (run << 5) | unit-within-run
-    __shared__ uint32_t s_scan[9];
-    __shared__ uint32_t s_nu;
-    __shared__ MomPartial s_big[kMaxBigUnits];
-    __shared__ uint16_t s_bigslot[kSortTile];           // first big-unit slot of a run (runs with > 1 unit)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ uint16_t s_first[kSortTile + 1];
+    __shared__ MomPartial s_pa[kRtThreads], s_pb[kRtThreads];
+    const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
@@ -135,101 +159,79 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint32_t nd = tp.nd[t];
     const float w_pred = sc->w_pred;
     for (uint32_t p = tid; p < n; p += kRtThreads) s_lp[p] = lperm[base + p];
-
-    // work units: runs inside the grid, split into 256-particle units
-    {
-        uint32_t cnt_units = 0, cnt_big = 0;
-        uint32_t u_of[16], b_of[16];
-        const uint32_t r0 = tid * 16;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t r = r0 + i;
-            uint32_t u = 0;
-            if (r < nd && tp.key[base + r] < fc.C) u = ((uint32_t)tp.cnt[base + r] + 1u + kItem - 1) / kItem;
-            u_of[i] = u;
-            b_of[i] = u > 1 ? u : 0u;
-            cnt_units += u;
-            cnt_big += b_of[i];
-        }
-        uint32_t tot_u, tot_b;
-        uint32_t uo = block_excl_scan<uint32_t, 8>(cnt_units, s_scan, tot_u);
-        uint32_t bo = block_excl_scan<uint32_t, 8>(cnt_big, s_scan, tot_b);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t r = r0 + i;
-            for (uint32_t k = 0; k < u_of[i]; ++k) s_unit[uo + k] = (r << 5) | k;
-            if (b_of[i]) s_bigslot[r] = (uint16_t)bo;
-            uo += u_of[i];
-            bo += b_of[i];
-        }
-        if (tid == 0) s_nu = tot_u;
-    }
+    for (uint32_t r = tid; r < nd; r += kRtThreads) s_first[r] = tp.first[base + r];
+    if (tid == 0) s_first[nd] = (uint16_t)n;
     __syncthreads();
-    const uint32_t nunits = s_nu;
 
-    for (uint32_t u = warp; u < nunits; u += kRtThreads / 32) {
-        const uint32_t code = s_unit[u];
-        const uint32_t r = code >> 5, k = code & 31u;
-        const uint32_t key = tp.key[base + r];
-        const uint32_t first = tp.first[base + r], cnt = (uint32_t)tp.cnt[base + r] + 1u;
-        const uint32_t pre = tp.pre[base + r];
-        const uint32_t li = cell2list[key];
-        const uint32_t cn = L.n[li], start = L.start[li];
-        const uint64_t P = bt.P0[li / chunk] + L.Pl[li];
-        const uint64_t bp = L.bp[li];
-        const uint32_t rpm = L.rp[li];
-        const uint32_t jbase = start + L.sb[li];
-        const uint32_t o0 = k * kItem, m = min(kItem, cnt - o0);
+    const uint32_t p0 = tid * kRtItems;
+    if (p0 < n) {
+        uint32_t lo = 0, hi = nd;                           // run containing p0
+        while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (s_first[m] <= p0) lo = m; else hi = m; }
+        RunParams q = load_run(lo, base, s_first, tp, L, bt, chunk, cell2list, fc.C);
         double acc[5] = {0, 0, 0, 0, 0};
-        for (uint32_t q0 = 0; q0 < m; q0 += 32) {
-            const bool valid = q0 + lane < m;
-            const uint32_t p = first + o0 + q0 + lane;          // local sorted position
-            const uint32_t mr = pre + o0 + q0 + lane;           // member rank within the cell
-            float X = 0.f, Y = 0.f, VX = 0.f, VY = 0.f;
-            uint32_t src = 0;
-            if (valid) {
-                src = base + s_lp[p];
-                X = pr.x[src]; Y = pr.y[src]; VX = pr.vx[src]; VY = pr.vy[src];
-                const double a = (double)VX, bq = (double)VY;
-                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                if (perm_dbg) perm_dbg[start + mr] = src;
+        bool first_seg = true;
+        uint32_t F_next = 0xFFFFFFFFu;                      // F(Q_{r+1}) of the previous position, same run
+        const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
+        auto flush = [&]() {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
+            if (q.in_grid) {
+                if (q.first >= p0 && q.end <= pend) ppart[base + q.j] = mp;    // run inside this thread
+                else if (first_seg) s_pa[tid] = mp;
+                else s_pb[tid] = mp;
             }
-            if (rc.W) {
-                const uint64_t Q0 = P + (uint64_t)mr * bp + min(mr, rpm);
-                const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
-                uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                if (valid && (lane == 31 || q0 + lane + 1 == m)) F1 = fcount(Q0 + bp + (mr < rpm ? 1u : 0u), rc);
-                if (valid) {
+            first_seg = false;
+        };
+#pragma unroll 1
+        for (uint32_t b0 = p0; b0 < pend; b0 += 8) {
+            // batch: 8 local indices, then 32 gathers in flight
+            float X[8], Y[8], VX[8], VY[8];
+            uint32_t src[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) src[u] = base + s_lp[min(b0 + u, pend - 1)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { X[u] = pr.x[src[u]]; Y[u] = pr.y[src[u]]; VX[u] = pr.vx[src[u]]; VY[u] = pr.vy[src[u]]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t p = b0 + u;
+                if (p >= pend) break;
+                if (p >= q.end) {                           // next run
+                    flush();
+                    q = load_run(q.j + 1, base, s_first, tp, L, bt, chunk, cell2list, fc.C);
+                    F_next = 0xFFFFFFFFu;
+                }
+                if (!q.in_grid) continue;
+                const double a = (double)VX[u], bq = (double)VY[u];
+                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                const uint32_t mr = q.pre + (p - q.first);   // member rank within the cell
+                if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
+                if (rc.W) {
+                    const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+                    const uint32_t F0 = F_next != 0xFFFFFFFFu ? F_next : fcount(Q0, rc);
+                    const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                    F_next = F1;
                     for (uint32_t o = F0; o < F1; ++o) {
-                        out.x[o] = X; out.y[o] = Y; out.vx[o] = VX; out.vy[o] = VY;
-                        if (out.jidx) out.jidx[o] = jbase + mr;
+                        out.x[o] = X[u]; out.y[o] = Y[u]; out.vx[o] = VX[u]; out.vy[o] = VY[u];
+                        if (out.jidx) out.jidx[o] = q.jbase + mr;
                     }
                 }
             }
         }
-#pragma unroll
-        for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
-        if (lane == 0) {
-            MomPartial mp;
-#pragma unroll
-            for (int i = 0; i < 5; ++i) mp.s[i] = acc[i];
-            if (cnt <= kItem) ppart[base + r] = mp;         // single-unit run
-            else s_big[s_bigslot[r] + k] = mp;
-        }
-        (void)cn;
+        flush();
     }
     __syncthreads();
-    // runs spanning several units: sum their units in order
+    // runs spanning several threads: combine the segments in thread order
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
-        const uint32_t cnt = (uint32_t)tp.cnt[base + r] + 1u;
-        if (cnt > kItem && tp.key[base + r] < fc.C) {
-            const uint32_t nu_r = (cnt + kItem - 1) / kItem, s0 = s_bigslot[r];
-            MomPartial mp = s_big[s0];
-            for (uint32_t k = 1; k < nu_r; ++k)
+        const uint32_t f = s_first[r], e = s_first[r + 1];
+        if (tp.key[base + r] >= fc.C) continue;
+        const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
+        if (tf == tl) continue;                             // written directly
+        MomPartial mp = (f > tf * kRtItems) ? s_pb[tf] : s_pa[tf];
+        for (uint32_t u = tf + 1; u <= tl; ++u)
 #pragma unroll
-                for (int i = 0; i < 5; ++i) mp.s[i] += s_big[s0 + k].s[i];
-            ppart[base + r] = mp;
-        }
+            for (int i = 0; i < 5; ++i) mp.s[i] += s_pa[u].s[i];
+        ppart[base + r] = mp;
     }
     __syncthreads();
     // cell completion: the last of a cell's runs to finish combines them in tile order (deterministic)
@@ -246,13 +248,13 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         if (atomicAdd(&L.pdone[li], 1u) != m - 1) continue;
         __threadfence();
         const uint32_t* pl = plist + bt.ps0[li / chunk] + L.ps[li];
-        double s[5] = {0, 0, 0, 0, 0};
-        for (uint32_t q = 0; q < m; ++q) {
-            const double* ps = ppart[pl[q]].s;
+        double sum[5] = {0, 0, 0, 0, 0};
+        for (uint32_t qq = 0; qq < m; ++qq) {
+            const double* ps = ppart[pl[qq]].s;
 #pragma unroll
-            for (int i = 0; i < 5; ++i) s[i] += __ldcg(ps + i);
+            for (int i = 0; i < 5; ++i) sum[i] += __ldcg(ps + i);
         }
-        finalize_cell(key, s, L.n[li], L.rho_p[li], w_pred, mean, cov);
+        finalize_cell(key, sum, L.n[li], L.rho_p[li], w_pred, mean, cov);
     }
 }
 
