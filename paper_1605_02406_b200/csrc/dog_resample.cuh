@@ -103,30 +103,25 @@ __device__ __forceinline__ uint32_t warp_last_le(uint32_t lo, uint32_t hi, uint3
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
+constexpr int kRtRunCache = 352;                                      // runs whose parameters sit in smem
 
 struct RunParams {
-    uint32_t j, first, end, pre, key, li, jbase, rpm;
     uint64_t P, bp;
-    bool in_grid;
+    uint32_t pre, rpm, jbase, key;
 };
 
-__device__ __forceinline__ RunParams load_run(uint32_t j, uint32_t base, const uint16_t* s_first, TilePairs tp,
-                                              CellList L, BlockTotals bt, uint32_t chunk,
-                                              const uint32_t* __restrict__ cell2list, uint32_t C)
+__device__ __forceinline__ RunParams fetch_run(uint32_t base, uint32_t j, TilePairs tp, CellList L, BlockTotals bt,
+                                               uint32_t chunk, const uint32_t* __restrict__ cell2list, uint32_t C)
 {
-    RunParams q;
-    q.j = j;
-    q.first = s_first[j];
-    q.end = s_first[j + 1];
+    RunParams q{};
     q.key = tp.key[base + j];
-    q.in_grid = q.key < C;
-    if (q.in_grid) {
+    if (q.key < C) {
         q.pre = tp.pre[base + j];
-        q.li = cell2list[q.key];
-        q.P = bt.P0[q.li / chunk] + L.Pl[q.li];
-        q.bp = L.bp[q.li];
-        q.rpm = L.rp[q.li];
-        q.jbase = L.start[q.li] + L.sb[q.li];
+        const uint32_t li = cell2list[q.key];
+        q.P = bt.P0[li / chunk] + L.Pl[li];
+        q.bp = L.bp[li];
+        q.rpm = L.rp[li];
+        q.jbase = L.start[li] + L.sb[li];
     }
     return q;
 }
@@ -136,15 +131,16 @@ __device__ __forceinline__ RunParams load_run(uint32_t j, uint32_t base, const u
 // copies go to [F(Q_r), F(Q_{r+1})).  Velocity sums are accumulated per run segment; segments that
 // span threads are combined in thread order, and a cell's runs over the tiles in tile order by the
 // last run to finish (deterministic).
-__global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
+__global__ __launch_bounds__(kRtThreads, 4) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
     const uint32_t* __restrict__ cell2list, const uint32_t* __restrict__ plist, NextState out,
     uint32_t* __restrict__ perm_dbg, float2* __restrict__ mean, float* __restrict__ cov,
     MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
-    __shared__ uint16_t s_lp[kSortTile];
-    __shared__ uint16_t s_first[kSortTile + 1];
+    __shared__ __align__(16) uint16_t s_lp[kSortTile];
+    __shared__ __align__(16) uint16_t s_first[kSortTile + 8];
     __shared__ MomPartial s_pa[kRtThreads], s_pb[kRtThreads];
+    __shared__ RunParams s_run[kRtRunCache];
     const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
@@ -158,16 +154,27 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const float w_pred = sc->w_pred;
-    for (uint32_t p = tid; p < n; p += kRtThreads) s_lp[p] = lperm[base + p];
-    for (uint32_t r = tid; r < nd; r += kRtThreads) s_first[r] = tp.first[base + r];
+    const uint32_t p0 = tid * kRtItems;
+    {   // one round trip: 16 local indices and 16 run starts per thread (32-byte vector loads)
+        const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0);
+        const uint4* fi4 = reinterpret_cast<const uint4*>(tp.first + base + p0);
+        uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
+        if (p0 < n) { a = lp4[0]; b = lp4[1]; }
+        if (p0 < nd) { c = fi4[0]; d = fi4[1]; }
+        if (p0 < n) { reinterpret_cast<uint4*>(s_lp + p0)[0] = a; reinterpret_cast<uint4*>(s_lp + p0)[1] = b; }
+        if (p0 < nd) { reinterpret_cast<uint4*>(s_first + p0)[0] = c; reinterpret_cast<uint4*>(s_first + p0)[1] = d; }
+    }
+    for (uint32_t r = tid; r < nd && r < (uint32_t)kRtRunCache; r += kRtThreads)
+        s_run[r] = fetch_run(base, r, tp, L, bt, chunk, cell2list, fc.C);
+    __syncthreads();
     if (tid == 0) s_first[nd] = (uint16_t)n;
     __syncthreads();
 
-    const uint32_t p0 = tid * kRtItems;
     if (p0 < n) {
         uint32_t lo = 0, hi = nd;                           // run containing p0
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (s_first[m] <= p0) lo = m; else hi = m; }
-        RunParams q = load_run(lo, base, s_first, tp, L, bt, chunk, cell2list, fc.C);
+        uint32_t j = lo, first = s_first[j], end = s_first[j + 1];
+        RunParams q = j < (uint32_t)kRtRunCache ? s_run[j] : fetch_run(base, j, tp, L, bt, chunk, cell2list, fc.C);
         double acc[5] = {0, 0, 0, 0, 0};
         bool first_seg = true;
         uint32_t F_next = 0xFFFFFFFFu;                      // F(Q_{r+1}) of the previous position, same run
@@ -176,8 +183,8 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
-            if (q.in_grid) {
-                if (q.first >= p0 && q.end <= pend) ppart[base + q.j] = mp;    // run inside this thread
+            if (q.key < fc.C) {
+                if (first >= p0 && end <= pend) ppart[base + j] = mp;    // run inside this thread
                 else if (first_seg) s_pa[tid] = mp;
                 else s_pb[tid] = mp;
             }
@@ -185,7 +192,6 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         };
 #pragma unroll 1
         for (uint32_t b0 = p0; b0 < pend; b0 += 8) {
-            // batch: 8 local indices, then 32 gathers in flight
             float X[8], Y[8], VX[8], VY[8];
             uint32_t src[8];
 #pragma unroll
@@ -196,16 +202,17 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
             for (int u = 0; u < 8; ++u) {
                 const uint32_t p = b0 + u;
                 if (p >= pend) break;
-                if (p >= q.end) {                           // next run
+                if (p >= end) {                             // next run
                     flush();
-                    q = load_run(q.j + 1, base, s_first, tp, L, bt, chunk, cell2list, fc.C);
+                    ++j; first = end; end = s_first[j + 1];
+                    q = j < (uint32_t)kRtRunCache ? s_run[j] : fetch_run(base, j, tp, L, bt, chunk, cell2list, fc.C);
                     F_next = 0xFFFFFFFFu;
                 }
-                if (!q.in_grid) continue;
+                if (q.key >= fc.C) continue;
                 const double a = (double)VX[u], bq = (double)VY[u];
                 acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                const uint32_t mr = q.pre + (p - q.first);   // member rank within the cell
-                if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
+                const uint32_t mr = q.pre + (p - first);    // member rank within the cell
+                if (perm_dbg) perm_dbg[q.jbase - L.sb[cell2list[q.key]] + mr] = src[u];
                 if (rc.W) {
                     const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
                     const uint32_t F0 = F_next != 0xFFFFFFFFu ? F_next : fcount(Q0, rc);
