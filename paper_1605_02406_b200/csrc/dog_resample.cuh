@@ -102,46 +102,60 @@ __device__ __forceinline__ uint32_t warp_last_le(uint32_t lo, uint32_t hi, uint3
     return lo;
 }
 
-constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
-constexpr int kRtRunCache = 352;                                      // runs whose parameters sit in smem
-
-struct RunParams {
-    uint64_t P, bp;
-    uint32_t pre, rpm, jbase, key;
-};
-
-__device__ __forceinline__ RunParams fetch_run(uint32_t base, uint32_t j, TilePairs tp, CellList L, BlockTotals bt,
-                                               uint32_t chunk, const uint32_t* __restrict__ cell2list, uint32_t C)
+// Warp-cooperative write of the copies of 32 consecutive members (lanes): member l owns outputs
+// [F0_l, F1_l), consecutive members own consecutive ranges, so the warp's outputs are one contiguous
+// range [F0_0, F1_last) written 32 at a time; the owner of output o is found by a 5-step shuffle
+// search.  Balanced and coalesced whatever the copy counts (a member can own hundreds of outputs).
+__device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F1, float X, float Y, float VX,
+                                             float VY, uint32_t J, NextState& out)
 {
-    RunParams q{};
-    q.key = tp.key[base + j];
-    if (q.key < C) {
-        q.pre = tp.pre[base + j];
-        const uint32_t li = cell2list[q.key];
-        q.P = bt.P0[li / chunk] + L.Pl[li];
-        q.bp = L.bp[li];
-        q.rpm = L.rp[li];
-        q.jbase = L.start[li] + L.sb[li];
+    const int lane = threadIdx.x & 31;
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (!vm) return;
+    const int lastv = 31 - __clz(vm);
+    const uint32_t lo = __shfl_sync(0xffffffffu, F0, __ffs(vm) - 1);
+    const uint32_t hi = __shfl_sync(0xffffffffu, F1, lastv);
+    const uint32_t f0 = valid ? F0 : hi;                    // invalid lanes own nothing
+    for (uint32_t o0 = lo; o0 < hi; o0 += 32) {
+        const uint32_t o = o0 + lane;
+        int own = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const int cand = own + step;
+            const uint32_t f = __shfl_sync(0xffffffffu, f0, cand);
+            if (f <= o) own = cand;
+        }
+        const float x = __shfl_sync(0xffffffffu, X, own), y = __shfl_sync(0xffffffffu, Y, own);
+        const float vx = __shfl_sync(0xffffffffu, VX, own), vy = __shfl_sync(0xffffffffu, VY, own);
+        const uint32_t jj = __shfl_sync(0xffffffffu, J, own);
+        if (o < hi) {
+            out.x[o] = x; out.y[o] = y; out.vx[o] = vx; out.vy[o] = vy;
+            if (out.jidx) out.jidx[o] = jj;
+        }
     }
-    return q;
 }
 
-// Persistent particles, one block per sort tile; thread t owns the tile's local sorted positions
-// [16t, 16t+16).  Position p of run j (cell c) is member r = pre(j) + (p - first(j)) of cell c: its
-// copies go to [F(Q_r), F(Q_{r+1})).  Velocity sums are accumulated per run segment; segments that
-// span threads are combined in thread order, and a cell's runs over the tiles in tile order by the
-// last run to finish (deterministic).
-__global__ __launch_bounds__(kRtThreads, 4) void k_resample_tiles(
+constexpr int kRtThreads = 256;
+constexpr int kMaxBigUnits = 48;   // units of runs longer than one unit, per tile (<= 4096/256 + 16)
+
+// Persistent particles, one block per sort tile.  Work units: <= 256 consecutive particles of one run
+// (one cell) in the tile's local sorted order; a warp loads the run's cell parameters once, its lanes
+// take 32 consecutive members at a time.  Member rank r = pre(run) + position within the run; the
+// member's copies go to [F(Q_r), F(Q_{r+1})).  Velocity sums per run are combined over a cell's runs
+// in tile order by the last run to finish (deterministic).
+__global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
     const uint32_t* __restrict__ cell2list, const uint32_t* __restrict__ plist, NextState out,
     uint32_t* __restrict__ perm_dbg, float2* __restrict__ mean, float* __restrict__ cov,
     MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
     __shared__ __align__(16) uint16_t s_lp[kSortTile];
-    __shared__ __align__(16) uint16_t s_first[kSortTile + 8];
-    __shared__ MomPartial s_pa[kRtThreads], s_pb[kRtThreads];
-    __shared__ RunParams s_run[kRtRunCache];
-    const int tid = threadIdx.x;
+    __shared__ uint32_t s_unit[kSortTile + 32];        // (run << 5) | unit-within-run
+    __shared__ uint32_t s_scan[9];
+    __shared__ uint32_t s_nu;
+    __shared__ MomPartial s_big[kMaxBigUnits];
+    __shared__ uint16_t s_bigslot[kSortTile];           // first big-unit slot of a run (runs with > 1 unit)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
@@ -154,91 +168,112 @@ __global__ __launch_bounds__(kRtThreads, 4) void k_resample_tiles(
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const float w_pred = sc->w_pred;
-    const uint32_t p0 = tid * kRtItems;
-    {   // one round trip: 16 local indices and 16 run starts per thread (32-byte vector loads)
-        const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0);
-        const uint4* fi4 = reinterpret_cast<const uint4*>(tp.first + base + p0);
-        uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
-        if (p0 < n) { a = lp4[0]; b = lp4[1]; }
-        if (p0 < nd) { c = fi4[0]; d = fi4[1]; }
-        if (p0 < n) { reinterpret_cast<uint4*>(s_lp + p0)[0] = a; reinterpret_cast<uint4*>(s_lp + p0)[1] = b; }
-        if (p0 < nd) { reinterpret_cast<uint4*>(s_first + p0)[0] = c; reinterpret_cast<uint4*>(s_first + p0)[1] = d; }
+    {   // the tile's local permutation in one round trip (32-byte vector loads)
+        const uint32_t p0 = tid * 16;
+        if (p0 < n) {
+            const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0);
+            const uint4 a = lp4[0], b = lp4[1];
+            reinterpret_cast<uint4*>(s_lp + p0)[0] = a;
+            reinterpret_cast<uint4*>(s_lp + p0)[1] = b;
+        }
     }
-    for (uint32_t r = tid; r < nd && r < (uint32_t)kRtRunCache; r += kRtThreads)
-        s_run[r] = fetch_run(base, r, tp, L, bt, chunk, cell2list, fc.C);
+    {   // work units: runs inside the grid, split into 256-particle units
+        uint32_t cnt_units = 0, cnt_big = 0;
+        uint32_t u_of[16];
+        const uint32_t r0 = tid * 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t r = r0 + i;
+            uint32_t u = 0;
+            if (r < nd && tp.key[base + r] < fc.C) u = ((uint32_t)tp.cnt[base + r] + 1u + kItem - 1) / kItem;
+            u_of[i] = u;
+            cnt_units += u;
+            cnt_big += u > 1 ? u : 0u;
+        }
+        uint32_t tot_u, tot_b;
+        uint32_t uo = block_excl_scan<uint32_t, 8>(cnt_units, s_scan, tot_u);
+        uint32_t bo = block_excl_scan<uint32_t, 8>(cnt_big, s_scan, tot_b);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t r = r0 + i;
+            for (uint32_t k = 0; k < u_of[i]; ++k) s_unit[uo + k] = (r << 5) | k;
+            if (u_of[i] > 1) { s_bigslot[r] = (uint16_t)bo; bo += u_of[i]; }
+            uo += u_of[i];
+        }
+        if (tid == 0) s_nu = tot_u;
+    }
     __syncthreads();
-    if (tid == 0) s_first[nd] = (uint16_t)n;
-    __syncthreads();
+    const uint32_t nunits = s_nu;
 
-    if (p0 < n) {
-        uint32_t lo = 0, hi = nd;                           // run containing p0
-        while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (s_first[m] <= p0) lo = m; else hi = m; }
-        uint32_t j = lo, first = s_first[j], end = s_first[j + 1];
-        RunParams q = j < (uint32_t)kRtRunCache ? s_run[j] : fetch_run(base, j, tp, L, bt, chunk, cell2list, fc.C);
+    for (uint32_t u = warp; u < nunits; u += kRtThreads / 32) {
+        const uint32_t code = s_unit[u];
+        const uint32_t r = code >> 5, k = code & 31u;
+        const uint32_t key = tp.key[base + r];
+        const uint32_t first = tp.first[base + r], cnt = (uint32_t)tp.cnt[base + r] + 1u;
+        const uint32_t pre = tp.pre[base + r];
+        const uint32_t li = cell2list[key];
+        const uint32_t start = L.start[li];
+        const uint64_t P = bt.P0[li / chunk] + L.Pl[li];
+        const uint64_t bp = L.bp[li];
+        const uint32_t rpm = L.rp[li];
+        const uint32_t jbase = start + L.sb[li];
+        const uint32_t o0 = k * kItem, m = min(kItem, cnt - o0);
         double acc[5] = {0, 0, 0, 0, 0};
-        bool first_seg = true;
-        uint32_t F_next = 0xFFFFFFFFu;                      // F(Q_{r+1}) of the previous position, same run
-        const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
-        auto flush = [&]() {
-            MomPartial mp;
+        for (uint32_t q0 = 0; q0 < m; q0 += 64) {
+            // two 32-member chunks per round: 8 gathers in flight per lane
+            float X[2], Y[2], VX[2], VY[2];
+            uint32_t src[2];
+            bool valid[2];
 #pragma unroll
-            for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
-            if (q.key < fc.C) {
-                if (first >= p0 && end <= pend) ppart[base + j] = mp;    // run inside this thread
-                else if (first_seg) s_pa[tid] = mp;
-                else s_pb[tid] = mp;
+            for (int h = 0; h < 2; ++h) {
+                valid[h] = q0 + 32 * h + lane < m;
+                src[h] = base + s_lp[first + o0 + min(q0 + 32 * h + lane, m - 1)];
             }
-            first_seg = false;
-        };
-#pragma unroll 1
-        for (uint32_t b0 = p0; b0 < pend; b0 += 8) {
-            float X[8], Y[8], VX[8], VY[8];
-            uint32_t src[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) src[u] = base + s_lp[min(b0 + u, pend - 1)];
+            for (int h = 0; h < 2; ++h) {
+                X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]];
+            }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) { X[u] = pr.x[src[u]]; Y[u] = pr.y[src[u]]; VX[u] = pr.vx[src[u]]; VY[u] = pr.vy[src[u]]; }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t p = b0 + u;
-                if (p >= pend) break;
-                if (p >= end) {                             // next run
-                    flush();
-                    ++j; first = end; end = s_first[j + 1];
-                    q = j < (uint32_t)kRtRunCache ? s_run[j] : fetch_run(base, j, tp, L, bt, chunk, cell2list, fc.C);
-                    F_next = 0xFFFFFFFFu;
+            for (int h = 0; h < 2; ++h) {
+                if (q0 + 32 * h >= m) break;                    // warp-uniform
+                const uint32_t mr = pre + o0 + q0 + 32 * h + lane;   // member rank within the cell
+                if (valid[h]) {
+                    const double a = (double)VX[h], bq = (double)VY[h];
+                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                    if (perm_dbg) perm_dbg[start + mr] = src[h];
                 }
-                if (q.key >= fc.C) continue;
-                const double a = (double)VX[u], bq = (double)VY[u];
-                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                const uint32_t mr = q.pre + (p - first);    // member rank within the cell
-                if (perm_dbg) perm_dbg[q.jbase - L.sb[cell2list[q.key]] + mr] = src[u];
                 if (rc.W) {
-                    const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-                    const uint32_t F0 = F_next != 0xFFFFFFFFu ? F_next : fcount(Q0, rc);
-                    const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
-                    F_next = F1;
-                    for (uint32_t o = F0; o < F1; ++o) {
-                        out.x[o] = X[u]; out.y[o] = Y[u]; out.vx[o] = VX[u]; out.vy[o] = VY[u];
-                        if (out.jidx) out.jidx[o] = q.jbase + mr;
-                    }
+                    const uint64_t Q0 = P + (uint64_t)mr * bp + min(mr, rpm);
+                    const uint32_t F0 = valid[h] ? fcount(Q0, rc) : 0u;
+                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
+                    if (valid[h] && (lane == 31 || q0 + 32 * h + lane + 1 == m))
+                        F1 = fcount(Q0 + bp + (mr < rpm ? 1u : 0u), rc);
+                    write_copies(valid[h], F0, F1, X[h], Y[h], VX[h], VY[h], jbase + mr, out);
                 }
             }
         }
-        flush();
+#pragma unroll
+        for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
+        if (lane == 0) {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] = acc[i];
+            if (cnt <= kItem) ppart[base + r] = mp;         // single-unit run
+            else s_big[s_bigslot[r] + k] = mp;
+        }
     }
     __syncthreads();
-    // runs spanning several threads: combine the segments in thread order
+    // runs spanning several units: sum their units in order
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
-        const uint32_t f = s_first[r], e = s_first[r + 1];
-        if (tp.key[base + r] >= fc.C) continue;
-        const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
-        if (tf == tl) continue;                             // written directly
-        MomPartial mp = (f > tf * kRtItems) ? s_pb[tf] : s_pa[tf];
-        for (uint32_t u = tf + 1; u <= tl; ++u)
+        const uint32_t cnt = (uint32_t)tp.cnt[base + r] + 1u;
+        if (cnt > kItem && tp.key[base + r] < fc.C) {
+            const uint32_t nu_r = (cnt + kItem - 1) / kItem, s0 = s_bigslot[r];
+            MomPartial mp = s_big[s0];
+            for (uint32_t k = 1; k < nu_r; ++k)
 #pragma unroll
-            for (int i = 0; i < 5; ++i) mp.s[i] += s_pa[u].s[i];
-        ppart[base + r] = mp;
+                for (int i = 0; i < 5; ++i) mp.s[i] += s_big[s0 + k].s[i];
+            ppart[base + r] = mp;
+        }
     }
     __syncthreads();
     // cell completion: the last of a cell's runs to finish combines them in tile order (deterministic)
@@ -317,12 +352,7 @@ __global__ __launch_bounds__(256) void k_births(CellList L, BlockTotals bt, uint
                 const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
                 uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
                 if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bb + (r < rbm ? 1u : 0u), rc);
-                if (valid) {
-                    for (uint32_t o = F0; o < F1; ++o) {
-                        out.x[o] = bx; out.y[o] = by; out.vx[o] = bvx; out.vy[o] = bvy;
-                        if (out.jidx) out.jidx[o] = jbase + r;
-                    }
-                }
+                write_copies(valid, F0, F1, bx, by, bvx, bvy, jbase + r, out);
             }
         }
         if (++q >= q_end) break;
