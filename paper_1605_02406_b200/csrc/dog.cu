@@ -217,6 +217,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
+    cudaFuncSetAttribute(k_resample_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     {   // k_births: persistent grid, as many blocks as fit on the GPU at once
         int per_sm = 0, sms = 148;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_births, 256, 0);
@@ -232,7 +233,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->x, N); AL(ctx->y, N); AL(ctx->vx, N); AL(ctx->vy, N);
     AL(ctx->px, N); AL(ctx->py, N); AL(ctx->pvx, N); AL(ctx->pvy, N);
     AL(ctx->keys, N); AL(ctx->lperm, N);
-    AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.pre, N); AL(ctx->tp.nd, ctx->tiles);
+    AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
     AL(ctx->counts, Cs + 1); AL(ctx->npairs, Cs + 1);
     if (dbg) {
@@ -366,9 +367,9 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     // 6. persistent particles: moments + resampling copies; births
     Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
     NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
-    k_resample_tiles<<<T, kRtThreads, 0, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ctx->bt, ctx->cell_chunk,
-                                               ctx->cell2list, ctx->plist, ns, dbg ? ctx->perm : nullptr, ctx->mean,
-                                               ctx->cov, ctx->ppart, ctx->sc, fc);
+    k_resample_tiles<<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ctx->bt, ctx->cell_chunk,
+                                                          ctx->plist, ns, dbg ? ctx->perm : nullptr, ctx->mean,
+                                                          ctx->cov, ctx->ppart, ctx->sc, fc);
     CK(cudaGetLastError());
     CK(mark("resample"));
     if (ctx->nu_b > 0) {

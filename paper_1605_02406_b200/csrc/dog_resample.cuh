@@ -135,27 +135,37 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
     }
 }
 
-constexpr int kRtThreads = 256;
-constexpr int kMaxBigUnits = 48;   // units of runs longer than one unit, per tile (<= 4096/256 + 16)
+constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
+constexpr int kRtRunCache = 256;                                      // runs whose RunInfo sits in smem
 
-// Persistent particles, one block per sort tile.  Work units: <= 256 consecutive particles of one run
-// (one cell) in the tile's local sorted order; a warp loads the run's cell parameters once, its lanes
-// take 32 consecutive members at a time.  Member rank r = pre(run) + position within the run; the
-// member's copies go to [F(Q_r), F(Q_{r+1})).  Velocity sums per run are combined over a cell's runs
-// in tile order by the last run to finish (deterministic).
-__global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
+struct RtSmem {   // dynamic shared memory of k_resample_tiles
+    uint16_t lp[kSortTile];            // local sorted position -> local index
+    uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
+    uint32_t F[kSortTile];             // F(Q_r) of the member at each position (its first output)
+    uint32_t os[kSortTile + 8];        // tile-local output slot of each run's first output
+    RunInfo run[kRtRunCache];
+    MomPartial pa[kRtThreads], pb[kRtThreads];
+    uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
+};
+constexpr size_t kRtSmemBytes = sizeof(RtSmem);
+
+// Persistent particles, one block per sort tile.  Phase B: thread t owns the tile's local sorted
+// positions [16t, 16t+16) -- batched gathers of the predicted state, velocity sums per run segment,
+// and F(Q_r) for every member (member r = pre(run) + position within the run).  Phase C: the tile's
+// outputs are written by all threads together: output slot s -> run (search over the runs' output
+// offsets) -> owner member (search over F) -> coalesced stores, whatever the copy counts.  Phase D:
+// run segments spanning threads are combined in thread order, a cell's runs over the tiles in tile
+// order by the last run to finish (deterministic).
+__global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
-    const uint32_t* __restrict__ cell2list, const uint32_t* __restrict__ plist, NextState out,
-    uint32_t* __restrict__ perm_dbg, float2* __restrict__ mean, float* __restrict__ cov,
-    MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
+    const uint32_t* __restrict__ plist, NextState out, uint32_t* __restrict__ perm_dbg,
+    float2* __restrict__ mean, float* __restrict__ cov, MomPartial* __restrict__ ppart,
+    const DevScalars* __restrict__ sc, FilterConst fc)
 {
-    __shared__ __align__(16) uint16_t s_lp[kSortTile];
-    __shared__ uint32_t s_unit[kSortTile + 32];        // (run << 5) | unit-within-run
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
     __shared__ uint32_t s_scan[9];
-    __shared__ uint32_t s_nu;
-    __shared__ MomPartial s_big[kMaxBigUnits];
-    __shared__ uint16_t s_bigslot[kSortTile];           // first big-unit slot of a run (runs with > 1 unit)
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
@@ -168,119 +178,146 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const float w_pred = sc->w_pred;
-    {   // the tile's local permutation in one round trip (32-byte vector loads)
-        const uint32_t p0 = tid * 16;
-        if (p0 < n) {
-            const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0);
-            const uint4 a = lp4[0], b = lp4[1];
-            reinterpret_cast<uint4*>(s_lp + p0)[0] = a;
-            reinterpret_cast<uint4*>(s_lp + p0)[1] = b;
-        }
-    }
-    {   // work units: runs inside the grid, split into 256-particle units
-        uint32_t cnt_units = 0, cnt_big = 0;
-        uint32_t u_of[16];
-        const uint32_t r0 = tid * 16;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t r = r0 + i;
-            uint32_t u = 0;
-            if (r < nd && tp.key[base + r] < fc.C) u = ((uint32_t)tp.cnt[base + r] + 1u + kItem - 1) / kItem;
-            u_of[i] = u;
-            cnt_units += u;
-            cnt_big += u > 1 ? u : 0u;
-        }
-        uint32_t tot_u, tot_b;
-        uint32_t uo = block_excl_scan<uint32_t, 8>(cnt_units, s_scan, tot_u);
-        uint32_t bo = block_excl_scan<uint32_t, 8>(cnt_big, s_scan, tot_b);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t r = r0 + i;
-            for (uint32_t k = 0; k < u_of[i]; ++k) s_unit[uo + k] = (r << 5) | k;
-            if (u_of[i] > 1) { s_bigslot[r] = (uint16_t)bo; bo += u_of[i]; }
-            uo += u_of[i];
-        }
-        if (tid == 0) s_nu = tot_u;
+    const uint32_t p0 = tid * kRtItems;
+    // ---- phase A: local permutation, run starts, run parameters (one round trip)
+    {
+        uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
+        if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }
+        if (p0 < nd) { const uint4* f4 = reinterpret_cast<const uint4*>(tp.first + base + p0); c = f4[0]; d = f4[1]; }
+        if (p0 < n) { reinterpret_cast<uint4*>(S.lp + p0)[0] = a; reinterpret_cast<uint4*>(S.lp + p0)[1] = b; }
+        if (p0 < nd) { reinterpret_cast<uint4*>(S.first + p0)[0] = c; reinterpret_cast<uint4*>(S.first + p0)[1] = d; }
+        if ((uint32_t)tid < nd && tid < kRtRunCache) S.run[tid] = tp.run[base + tid];
+        if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
     __syncthreads();
-    const uint32_t nunits = s_nu;
+    if (tid == 0) S.first[nd] = (uint16_t)n;
+    __syncthreads();
+    const uint32_t srun = S.sentinel_run;
+    auto run_info = [&](uint32_t j) -> RunInfo { return j < (uint32_t)kRtRunCache ? S.run[j] : tp.run[base + j]; };
 
-    for (uint32_t u = warp; u < nunits; u += kRtThreads / 32) {
-        const uint32_t code = s_unit[u];
-        const uint32_t r = code >> 5, k = code & 31u;
-        const uint32_t key = tp.key[base + r];
-        const uint32_t first = tp.first[base + r], cnt = (uint32_t)tp.cnt[base + r] + 1u;
-        const uint32_t pre = tp.pre[base + r];
-        const uint32_t li = cell2list[key];
-        const uint32_t start = L.start[li];
-        const uint64_t P = bt.P0[li / chunk] + L.Pl[li];
-        const uint64_t bp = L.bp[li];
-        const uint32_t rpm = L.rp[li];
-        const uint32_t jbase = start + L.sb[li];
-        const uint32_t o0 = k * kItem, m = min(kItem, cnt - o0);
+    // ---- phase B: gathers, velocity sums, F per member
+    if (p0 < n) {
+        uint32_t lo = 0, hi = nd;                           // run containing p0
+        while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= p0) lo = m; else hi = m; }
+        uint32_t j = lo, first = S.first[j], end = S.first[j + 1];
+        RunInfo q = run_info(j);
         double acc[5] = {0, 0, 0, 0, 0};
-        for (uint32_t q0 = 0; q0 < m; q0 += 64) {
-            // two 32-member chunks per round: 8 gathers in flight per lane
-            float X[2], Y[2], VX[2], VY[2];
-            uint32_t src[2];
-            bool valid[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                valid[h] = q0 + 32 * h + lane < m;
-                src[h] = base + s_lp[first + o0 + min(q0 + 32 * h + lane, m - 1)];
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]];
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (q0 + 32 * h >= m) break;                    // warp-uniform
-                const uint32_t mr = pre + o0 + q0 + 32 * h + lane;   // member rank within the cell
-                if (valid[h]) {
-                    const double a = (double)VX[h], bq = (double)VY[h];
-                    acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                    if (perm_dbg) perm_dbg[start + mr] = src[h];
-                }
-                if (rc.W) {
-                    const uint64_t Q0 = P + (uint64_t)mr * bp + min(mr, rpm);
-                    const uint32_t F0 = valid[h] ? fcount(Q0, rc) : 0u;
-                    uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                    if (valid[h] && (lane == 31 || q0 + 32 * h + lane + 1 == m))
-                        F1 = fcount(Q0 + bp + (mr < rpm ? 1u : 0u), rc);
-                    write_copies(valid[h], F0, F1, X[h], Y[h], VX[h], VY[h], jbase + mr, out);
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 5; ++i) acc[i] = warp_sum(acc[i]);
-        if (lane == 0) {
+        bool first_seg = true;
+        const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
+        auto flush = [&]() {
             MomPartial mp;
 #pragma unroll
-            for (int i = 0; i < 5; ++i) mp.s[i] = acc[i];
-            if (cnt <= kItem) ppart[base + r] = mp;         // single-unit run
-            else s_big[s_bigslot[r] + k] = mp;
-        }
-    }
-    __syncthreads();
-    // runs spanning several units: sum their units in order
-    for (uint32_t r = tid; r < nd; r += kRtThreads) {
-        const uint32_t cnt = (uint32_t)tp.cnt[base + r] + 1u;
-        if (cnt > kItem && tp.key[base + r] < fc.C) {
-            const uint32_t nu_r = (cnt + kItem - 1) / kItem, s0 = s_bigslot[r];
-            MomPartial mp = s_big[s0];
-            for (uint32_t k = 1; k < nu_r; ++k)
+            for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
+            if (j != srun) {
+                if (first >= p0 && end <= pend) ppart[base + j] = mp;    // run inside this thread
+                else if (first_seg) S.pa[tid] = mp;
+                else S.pb[tid] = mp;
+            }
+            first_seg = false;
+        };
+#pragma unroll 1
+        for (uint32_t b0 = p0; b0 < pend; b0 += 8) {
+            float VX[8], VY[8];
+            uint32_t src[8];
 #pragma unroll
-                for (int i = 0; i < 5; ++i) mp.s[i] += s_big[s0 + k].s[i];
-            ppart[base + r] = mp;
+            for (int u = 0; u < 8; ++u) src[u] = base + S.lp[min(b0 + u, pend - 1)];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { VX[u] = pr.vx[src[u]]; VY[u] = pr.vy[src[u]]; }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t p = b0 + u;
+                if (p >= pend) break;
+                if (p >= end) {                             // next run
+                    flush();
+                    ++j; first = end; end = S.first[j + 1];
+                    q = run_info(j);
+                }
+                if (j == srun) continue;
+                const double a = (double)VX[u], bq = (double)VY[u];
+                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                const uint32_t mr = q.pre + (p - first);    // member rank within the cell
+                if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
+                if (rc.W) S.F[p] = fcount(q.P + (uint64_t)mr * q.bp + min(mr, q.rpm), rc);
+            }
         }
+        flush();
     }
     __syncthreads();
-    // cell completion: the last of a cell's runs to finish combines them in tile order (deterministic)
+    // ---- phase C: output slots of the runs, then cooperative coalesced writes
+    {
+        uint32_t cnt_out[kRtItems], sum = 0;
+        const uint32_t r0 = tid * kRtItems;
+#pragma unroll
+        for (int i = 0; i < kRtItems; ++i) {
+            const uint32_t r = r0 + i;
+            uint32_t co = 0;
+            if (rc.W && r < nd && r != srun) {
+                const RunInfo q = run_info(r);
+                const uint32_t f = S.first[r], e = S.first[r + 1];
+                const uint32_t me = q.pre + (e - f);        // rank one past the run's last member
+                const uint32_t Fe = fcount(q.P + (uint64_t)me * q.bp + min(me, q.rpm), rc);
+                co = Fe - S.F[f];
+            }
+            cnt_out[i] = co;
+            sum += co;
+        }
+        uint32_t tot;
+        uint32_t run = block_excl_scan<uint32_t, 8>(sum, s_scan, tot);
+#pragma unroll
+        for (int i = 0; i < kRtItems; ++i) {
+            if (r0 + i <= nd) S.os[r0 + i] = run;
+            run += cnt_out[i];
+        }
+        if (tid == 0 && nd == kSortTile) S.os[nd] = tot;
+    }
+    __syncthreads();
+    const uint32_t O = S.os[nd];
+    for (uint32_t s0 = 0; s0 < O; s0 += kRtThreads * 4) {
+        uint32_t o[4], src[4], jj[4];
+        bool ok[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const uint32_t s = s0 + h * kRtThreads + tid;
+            ok[h] = s < O;
+            const uint32_t ss = ok[h] ? s : 0u;
+            uint32_t lo = 0, hi = nd;                       // run holding output slot ss
+            while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.os[m] <= ss) lo = m; else hi = m; }
+            const uint32_t f = S.first[lo], e = S.first[lo + 1];
+            o[h] = S.F[f] + (ss - S.os[lo]);
+            uint32_t a = f, b = e;                          // owner: last member with F <= o
+            while (b - a > 1) { const uint32_t m = (a + b) >> 1; if (S.F[m] <= o[h]) a = m; else b = m; }
+            src[h] = base + S.lp[a];
+            jj[h] = out.jidx ? run_info(lo).jbase + run_info(lo).pre + (a - f) : 0u;
+        }
+        float X[4], Y[4], VX[4], VY[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]];
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            if (!ok[h]) continue;
+            out.x[o[h]] = X[h]; out.y[o[h]] = Y[h]; out.vx[o[h]] = VX[h]; out.vy[o[h]] = VY[h];
+            if (out.jidx) out.jidx[o[h]] = jj[h];
+        }
+    }
+    // ---- phase D: run segments spanning threads, then cell completion
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        if (r == srun) continue;
+        const uint32_t f = S.first[r], e = S.first[r + 1];
+        const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
+        if (tf == tl) continue;                             // written directly in phase B
+        MomPartial mp = (f > tf * kRtItems) ? S.pb[tf] : S.pa[tf];
+        for (uint32_t u = tf + 1; u <= tl; ++u)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] += S.pa[u].s[i];
+        ppart[base + r] = mp;
+    }
+    __syncthreads();
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        if (r == srun) continue;
         const uint32_t key = tp.key[base + r];
-        if (key >= fc.C) continue;
-        const uint32_t li = cell2list[key];
+        const uint32_t li = run_info(r).li;
         const uint32_t m = L.np[li];
         if (m == 1) {
             finalize_cell(key, ppart[base + r].s, L.n[li], L.rho_p[li], w_pred, mean, cov);

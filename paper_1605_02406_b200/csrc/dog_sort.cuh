@@ -25,11 +25,21 @@ namespace dog {
 constexpr int kTsThreads = 256, kTsItems = 16, kTsWarps = 8;
 static_assert(kTsThreads * kTsItems == kSortTile, "sort tile");
 
+// What k_resample_tiles needs of a run (written by k_pair_sort, one coalesced 32-byte load per run).
+struct RunInfo {
+    uint64_t P;             // joint-CDF prefix of the run's cell (A-25)
+    uint64_t bp;            // R_p / n_c of the cell (even split, A-23)
+    uint32_t rpm;           // R_p mod n_c
+    uint32_t pre;           // rank of the run's first particle among the cell's particles
+    uint32_t jbase;         // joint index of the cell's first member (debug)
+    uint32_t li;            // the cell's active-list entry
+};
+
 struct TilePairs {          // per tile t: entries [t*4096, t*4096 + nd[t])
     uint32_t* key;          // cell key of the run (C = outside the grid)
     uint16_t* first;        // first local sorted position of the run
     uint16_t* cnt;          // particles in the run (1..4096, stored as cnt-1)
-    uint32_t* pre;          // rank of the run's first particle within its cell        (k_pair_sort)
+    RunInfo* run;           // per-run resampling parameters                           (k_pair_sort)
     uint32_t* nd;           // [tiles] runs of the tile
 };
 
@@ -197,8 +207,14 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, Blo
         const uint32_t m = L.np[li];
         if (m == 0) continue;
         uint32_t* pl = plist + bt.ps0[b] + L.ps[li];
+        RunInfo ri;
+        ri.P = bt.P0[b] + L.Pl[li];
+        ri.bp = L.bp[li];
+        ri.rpm = L.rp[li];
+        ri.jbase = L.start[li] + L.sb[li];
+        ri.li = li;
         if (m == 1) {                                // (tile << 12 | run) is the run's slot index
-            if (lane == 0) tp.pre[pl[0]] = 0u;
+            if (lane == 0) { ri.pre = 0u; tp.run[pl[0]] = ri; }
             continue;
         }
         uint32_t* tmp = ptmp + bt.ps0[b] + L.ps[li];
@@ -221,7 +237,9 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, Blo
             }
             const uint32_t incl = warp_incl_scan(c, lane);
             if (a < m) {
-                tp.pre[v] = carry + incl - c;
+                RunInfo r2 = ri;
+                r2.pre = carry + incl - c;
+                tp.run[v] = r2;
                 pl[a] = v;                   // the cell's list, now in tile order
             }
             carry += __shfl_sync(0xffffffffu, incl, 31);
