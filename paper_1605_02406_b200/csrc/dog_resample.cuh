@@ -137,25 +137,69 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
 constexpr int kRtRunCache = 256;                                      // runs whose RunInfo sits in smem
+constexpr uint32_t kNoF = 0xFFFFFFFFu;                                // position outside the grid
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
-    uint32_t F[kSortTile];             // F(Q_r) of the member at each position (its first output)
-    uint32_t os[kSortTile + 8];        // tile-local output slot of each run's first output
+    uint32_t F0[kSortTile];            // F(Q_r): first output of the member at each position
+    uint32_t F1[kSortTile];            // F(Q_{r+1}): one past its last output
     RunInfo run[kRtRunCache];
     MomPartial pa[kRtThreads], pb[kRtThreads];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
 
+// Warp-cooperative write of the copies of the lanes' members: lanes whose output ranges are adjacent
+// (F1 of a lane == F0 of the next) form a segment whose outputs are one contiguous range, written 32 at
+// a time; the owner of an output is found by a 5-step shuffle search.  Coalesced and balanced whatever
+// the copy counts (one member can own hundreds of outputs).
+__device__ __forceinline__ void write_segments(bool valid, uint32_t F0, uint32_t F1, float X, float Y, float VX,
+                                               float VY, uint32_t J, NextState& out)
+{
+    const int lane = threadIdx.x & 31;
+    const uint32_t pF1 = __shfl_up_sync(0xffffffffu, F1, 1);
+    const bool pvalid = __shfl_up_sync(0xffffffffu, valid, 1);
+    const bool head = valid && (lane == 0 || !pvalid || pF1 != F0);
+    uint32_t heads = __ballot_sync(0xffffffffu, head);
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    while (heads) {
+        const int a = __ffs(heads) - 1;
+        heads &= heads - 1;
+        const int nxt_head = heads ? __ffs(heads) - 1 : 32;
+        // segment = valid lanes [a, b]: stops before the next head or the first invalid lane after a
+        const uint32_t inval_after = ~vmask & (0xffffffffu << a);
+        const int nxt_inval = inval_after ? __ffs(inval_after) - 1 : 32;
+        const int b = min(nxt_head, nxt_inval) - 1;
+        const uint32_t lo = __shfl_sync(0xffffffffu, F0, a);
+        const uint32_t hi = __shfl_sync(0xffffffffu, F1, b);
+        const uint32_t f0 = lane < a ? 0u : (lane > b ? hi : F0);
+        for (uint32_t o0 = lo; o0 < hi; o0 += 32) {
+            const uint32_t o = o0 + lane;
+            int own = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+                const int cand = own + step;
+                const uint32_t f = __shfl_sync(0xffffffffu, f0, cand);
+                if (f <= o) own = cand;
+            }
+            const float x = __shfl_sync(0xffffffffu, X, own), y = __shfl_sync(0xffffffffu, Y, own);
+            const float vx = __shfl_sync(0xffffffffu, VX, own), vy = __shfl_sync(0xffffffffu, VY, own);
+            const uint32_t jj = __shfl_sync(0xffffffffu, J, own);
+            if (o < hi) {
+                out.x[o] = x; out.y[o] = y; out.vx[o] = vx; out.vy[o] = vy;
+                if (out.jidx) out.jidx[o] = jj;
+            }
+        }
+    }
+}
+
 // Persistent particles, one block per sort tile.  Phase B: thread t owns the tile's local sorted
-// positions [16t, 16t+16) -- batched gathers of the predicted state, velocity sums per run segment,
-// and F(Q_r) for every member (member r = pre(run) + position within the run).  Phase C: the tile's
-// outputs are written by all threads together: output slot s -> run (search over the runs' output
-// offsets) -> owner member (search over F) -> coalesced stores, whatever the copy counts.  Phase D:
-// run segments spanning threads are combined in thread order, a cell's runs over the tiles in tile
-// order by the last run to finish (deterministic).
+// positions [16t, 16t+16) -- batched gathers of the predicted velocities, velocity sums per run
+// segment, and the output range [F(Q_r), F(Q_{r+1})) of every member (member r = pre(run) + position
+// within the run).  Phase C: warps take 32 consecutive positions at a time, gather the full state and
+// write the copies cooperatively (write_segments).  Phase D: run segments spanning threads are combined
+// in thread order, a cell's runs over the tiles in tile order by the last run to finish (deterministic).
 __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
     const uint32_t* __restrict__ plist, NextState out, uint32_t* __restrict__ perm_dbg,
@@ -164,8 +208,7 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
-    __shared__ uint32_t s_scan[9];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
@@ -195,7 +238,7 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
     const uint32_t srun = S.sentinel_run;
     auto run_info = [&](uint32_t j) -> RunInfo { return j < (uint32_t)kRtRunCache ? S.run[j] : tp.run[base + j]; };
 
-    // ---- phase B: gathers, velocity sums, F per member
+    // ---- phase B: velocity gathers, velocity sums, output ranges per member
     if (p0 < n) {
         uint32_t lo = 0, hi = nd;                           // run containing p0
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= p0) lo = m; else hi = m; }
@@ -203,6 +246,7 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
         RunInfo q = run_info(j);
         double acc[5] = {0, 0, 0, 0, 0};
         bool first_seg = true;
+        uint32_t Fcarry = kNoF;                             // F(Q_r) of the next member, same run
         const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
         auto flush = [&]() {
             MomPartial mp;
@@ -231,74 +275,54 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
                     flush();
                     ++j; first = end; end = S.first[j + 1];
                     q = run_info(j);
+                    Fcarry = kNoF;
                 }
-                if (j == srun) continue;
+                if (j == srun) { S.F0[p] = kNoF; S.F1[p] = kNoF; continue; }
                 const double a = (double)VX[u], bq = (double)VY[u];
                 acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
                 const uint32_t mr = q.pre + (p - first);    // member rank within the cell
                 if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
-                if (rc.W) S.F[p] = fcount(q.P + (uint64_t)mr * q.bp + min(mr, q.rpm), rc);
+                if (rc.W) {
+                    const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+                    const uint32_t F0 = Fcarry != kNoF ? Fcarry : fcount(Q0, rc);
+                    const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                    S.F0[p] = F0; S.F1[p] = F1;
+                    Fcarry = F1;
+                }
             }
         }
         flush();
     }
     __syncthreads();
-    // ---- phase C: output slots of the runs, then cooperative coalesced writes
-    {
-        uint32_t cnt_out[kRtItems], sum = 0;
-        const uint32_t r0 = tid * kRtItems;
+    // ---- phase C: warp-strided positions, full-state gathers, cooperative coalesced copy writes
+    if (rc.W) {
+#pragma unroll 1
+        for (int it = 0; it < kRtItems; it += 4) {
+            uint32_t pp[4], src[4], F0[4], F1[4];
+            bool ok[4];
 #pragma unroll
-        for (int i = 0; i < kRtItems; ++i) {
-            const uint32_t r = r0 + i;
-            uint32_t co = 0;
-            if (rc.W && r < nd && r != srun) {
-                const RunInfo q = run_info(r);
-                const uint32_t f = S.first[r], e = S.first[r + 1];
-                const uint32_t me = q.pre + (e - f);        // rank one past the run's last member
-                const uint32_t Fe = fcount(q.P + (uint64_t)me * q.bp + min(me, q.rpm), rc);
-                co = Fe - S.F[f];
+            for (int h = 0; h < 4; ++h) {
+                pp[h] = (uint32_t)(warp * kRtItems + it + h) * 32 + lane;
+                ok[h] = pp[h] < n;
+                const uint32_t pc = ok[h] ? pp[h] : 0u;
+                F0[h] = S.F0[pc]; F1[h] = S.F1[pc];
+                ok[h] = ok[h] && F0[h] != kNoF;
+                src[h] = base + S.lp[pc];
             }
-            cnt_out[i] = co;
-            sum += co;
-        }
-        uint32_t tot;
-        uint32_t run = block_excl_scan<uint32_t, 8>(sum, s_scan, tot);
+            float X[4], Y[4], VX[4], VY[4];
 #pragma unroll
-        for (int i = 0; i < kRtItems; ++i) {
-            if (r0 + i <= nd) S.os[r0 + i] = run;
-            run += cnt_out[i];
-        }
-        if (tid == 0 && nd == kSortTile) S.os[nd] = tot;
-    }
-    __syncthreads();
-    const uint32_t O = S.os[nd];
-    for (uint32_t s0 = 0; s0 < O; s0 += kRtThreads * 4) {
-        uint32_t o[4], src[4], jj[4];
-        bool ok[4];
+            for (int h = 0; h < 4; ++h) { X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]]; }
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const uint32_t s = s0 + h * kRtThreads + tid;
-            ok[h] = s < O;
-            const uint32_t ss = ok[h] ? s : 0u;
-            uint32_t lo = 0, hi = nd;                       // run holding output slot ss
-            while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.os[m] <= ss) lo = m; else hi = m; }
-            const uint32_t f = S.first[lo], e = S.first[lo + 1];
-            o[h] = S.F[f] + (ss - S.os[lo]);
-            uint32_t a = f, b = e;                          // owner: last member with F <= o
-            while (b - a > 1) { const uint32_t m = (a + b) >> 1; if (S.F[m] <= o[h]) a = m; else b = m; }
-            src[h] = base + S.lp[a];
-            jj[h] = out.jidx ? run_info(lo).jbase + run_info(lo).pre + (a - f) : 0u;
-        }
-        float X[4], Y[4], VX[4], VY[4];
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]];
-        }
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            if (!ok[h]) continue;
-            out.x[o[h]] = X[h]; out.y[o[h]] = Y[h]; out.vx[o[h]] = VX[h]; out.vy[o[h]] = VY[h];
-            if (out.jidx) out.jidx[o[h]] = jj[h];
+            for (int h = 0; h < 4; ++h) {
+                uint32_t J = 0;
+                if (out.jidx && ok[h]) {                    // debug: joint index of the member
+                    uint32_t lo = 0, hi = nd;
+                    while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= pp[h]) lo = m; else hi = m; }
+                    const RunInfo q = run_info(lo);
+                    J = q.jbase + q.pre + (pp[h] - S.first[lo]);
+                }
+                write_segments(ok[h], F0[h], F1[h], X[h], Y[h], VX[h], VY[h], J, out);
+            }
         }
     }
     // ---- phase D: run segments spanning threads, then cell completion
