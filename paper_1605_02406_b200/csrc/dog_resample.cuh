@@ -325,17 +325,28 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
             }
         }
     }
-    // ---- phase D: run segments spanning threads, then cell completion
-    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+    // ---- phase D: run segments spanning threads (one warp per run, fixed summation order), then
+    //      cell completion
+    __syncthreads();
+    for (uint32_t r = warp; r < nd; r += kRtThreads / 32) {
         if (r == srun) continue;
         const uint32_t f = S.first[r], e = S.first[r + 1];
         const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
         if (tf == tl) continue;                             // written directly in phase B
-        MomPartial mp = (f > tf * kRtItems) ? S.pb[tf] : S.pa[tf];
-        for (uint32_t u = tf + 1; u <= tl; ++u)
+        double s5[5] = {0, 0, 0, 0, 0};
+        for (uint32_t u = tf + lane; u <= tl; u += 32) {
+            const MomPartial& mp = (u == tf) ? ((f > tf * kRtItems) ? S.pb[tf] : S.pa[tf]) : S.pa[u];
 #pragma unroll
-            for (int i = 0; i < 5; ++i) mp.s[i] += S.pa[u].s[i];
-        ppart[base + r] = mp;
+            for (int i = 0; i < 5; ++i) s5[i] += mp.s[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) s5[i] = warp_sum(s5[i]);
+        if (lane == 0) {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+            ppart[base + r] = mp;
+        }
     }
     __syncthreads();
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
