@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -53,8 +54,10 @@ struct dog_ctx {
     float2* mean = nullptr;
     float* cov = nullptr;
     uint32_t* mvalid = nullptr;                   // moments-reported bitmask
-    CellList list{};
+    StageList stage{};                            // k_cells staging (per cell chunk)
+    CellList list{};                              // flat active-cell list
     BlockTotals bt{};
+    uint32_t ls_cluster = 0, flat_blocks = 0;     // k_list_scan cluster size; lane-per-cell grids
     uint32_t* cell2list = nullptr;
     MomPartial* ppart = nullptr;                  // velocity sums per run
     // debug-only arrays
@@ -218,11 +221,32 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         ctx->cell_blocks = nblk;
     }
     cudaFuncSetAttribute(k_resample_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
-    {   // k_births: persistent grid, as many blocks as fit on the GPU at once
+    {   // persistent grids: as many blocks as fit on the GPU at once
         int per_sm = 0, sms = 148;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_births, 256, 0);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_births, 256, 0);
         ctx->birth_blocks = (uint32_t)std::max(1, per_sm) * (uint32_t)sms;
+        ctx->flat_blocks = 4u * (uint32_t)sms;   // lane-per-cell kernels over the active list
+        // k_list_scan: one cluster, 16 CTAs where the GPU allows it (non-portable size), else 8
+        cudaFuncSetAttribute(k_list_scan, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (uint32_t ncl : {(uint32_t)kLsClusterMax, 8u}) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = ncl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(ncl); cfg.blockDim = dim3(kLsThreads); cfg.attrs = at; cfg.numAttrs = 1;
+            int ncls = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncls, k_list_scan, &cfg) == cudaSuccess && ncls > 0) {
+                ctx->ls_cluster = ncl;
+                break;
+            }
+            cudaGetLastError();
+        }
+        if (!ctx->ls_cluster) {
+            fprintf(stderr, "libdog: no thread-block cluster configuration fits k_list_scan\n");
+            delete ctx;
+            return DOG_E_CUDA;
+        }
     }
     const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
     const bool dbg = (flags & DOG_FLAG_DEBUG) != 0;
@@ -245,15 +269,15 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
     AL(ctx->mvalid, Cs / 32 + 1);
     const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
-    AL(ctx->list.c, LC); AL(ctx->list.n, LC); AL(ctx->list.Rp, LC); AL(ctx->list.Rb, LC);
-    AL(ctx->list.rho_p, LC); AL(ctx->list.start, LC); AL(ctx->list.sb, LC); AL(ctx->list.nb, LC);
-    AL(ctx->list.Pl, LC); AL(ctx->list.it, LC); AL(ctx->list.bp, LC); AL(ctx->list.rp, LC);
-    AL(ctx->list.bb, LC); AL(ctx->list.rb, LC);
-    AL(ctx->list.np, LC); AL(ctx->list.ps, LC); AL(ctx->list.pfill, LC); AL(ctx->list.pdone, LC);
+    AL(ctx->stage.c, LC); AL(ctx->stage.n, LC); AL(ctx->stage.Rp, LC); AL(ctx->stage.Rb, LC);
+    AL(ctx->stage.rho_p, LC); AL(ctx->stage.np, LC);
+    AL(ctx->list.c, Cs); AL(ctx->list.n, Cs); AL(ctx->list.Rp, Cs); AL(ctx->list.rho_p, Cs);
+    AL(ctx->list.start, Cs); AL(ctx->list.sb, Cs); AL(ctx->list.nb, Cs); AL(ctx->list.P, Cs);
+    AL(ctx->list.it, Cs); AL(ctx->list.bp, Cs); AL(ctx->list.rp, Cs); AL(ctx->list.bb, Cs);
+    AL(ctx->list.rb, Cs); AL(ctx->list.np, Cs); AL(ctx->list.ps, Cs); AL(ctx->list.pfill, Cs);
     AL(ctx->cell2list, Cs);
     AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
-    AL(ctx->bt.P0, ctx->cell_blocks); AL(ctx->bt.item0, ctx->cell_blocks); AL(ctx->bt.ps0, ctx->cell_blocks);
-    AL(ctx->bt.s0, ctx->cell_blocks);
+
     AL(ctx->sc, 1);
     AL(ctx->ctrs, 16);
 #undef AL
@@ -280,6 +304,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     if (e == cudaSuccess) e = cudaMemset(ctx->counts, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->npairs, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
+
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         fprintf(stderr, "libdog: dog_create init failed: %s\n", cudaGetErrorString(e));
@@ -305,7 +330,8 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    return 8;   // predict, tilesort, cells, list_scan, pair_fill, pair_sort, resample_tiles, births
+    // predict, tilesort, cells, list_scan, pair_fill, pair_sort, resample_tiles, moments, births
+    return ctx->nu_b > 0 ? 9 : 8;
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -347,35 +373,43 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
     k_cells<<<ctx->cell_blocks, kCellThreads, 0, st>>>(ctx->counts, ctx->npairs, ctx->m_free, (const float2*)meas,
                                                        ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg,
-                                                       ctx->list, ctx->cell2list, ctx->bt, ctx->cell_chunk, ctx->sc,
-                                                       fc, a.alpha);
+                                                       ctx->stage, ctx->bt, ctx->cell_chunk, ctx->sc, fc, a.alpha);
     CK(cudaGetLastError());
     CK(mark("cells"));
 
     // 4. slots, joint CDF, run-list offsets over the active list (Alg. 5 / Alg. 7 prefix sums)
-    k_list_scan<<<ctx->cell_blocks, kLsThreads, 0, st>>>(ctx->list, ctx->bt, ctx->cell_chunk, ctx->sc, fc, a.k);
+    {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ctx->ls_cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(ctx->ls_cluster); cfg.blockDim = dim3(kLsThreads); cfg.stream = st;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, k_list_scan, ctx->stage, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
+                              ctx->cell2list, ctx->sc, fc, (int64_t)a.k));
+    }
     CK(cudaGetLastError());
     CK(mark("list_scan"));
 
     // 5. each cell's runs in tile order -> stable within-cell ranks
-    k_pair_fill<<<T, 256, 0, st>>>(ctx->tp, ctx->list, ctx->bt, ctx->cell_chunk, ctx->cell2list, ctx->plist, ctx->C);
+    k_pair_fill<<<T, 256, 0, st>>>(ctx->tp, ctx->list, ctx->cell2list, ctx->plist, ctx->C);
     CK(cudaGetLastError());
-    k_pair_sort<<<ctx->cell_blocks, 256, 0, st>>>(ctx->tp, ctx->list, ctx->bt, ctx->cell_chunk, ctx->plist, ctx->ptmp);
+    k_pair_sort<<<ctx->flat_blocks, 256, 0, st>>>(ctx->tp, ctx->list, ctx->plist, ctx->ptmp, ctx->sc);
     CK(cudaGetLastError());
     CK(mark("pairs"));
 
     // 6. persistent particles: moments + resampling copies; births
     Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
     NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
-    k_resample_tiles<<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ctx->bt, ctx->cell_chunk,
-                                                          ctx->plist, ns, dbg ? ctx->perm : nullptr, ctx->mean,
-                                                          ctx->cov, ctx->ppart, ctx->sc, fc);
+    k_resample_tiles<<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ns,
+                                                          dbg ? ctx->perm : nullptr, ctx->ppart, ctx->sc, fc);
+    CK(cudaGetLastError());
+    k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
     CK(cudaGetLastError());
     CK(mark("resample"));
     if (ctx->nu_b > 0) {
         BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-        k_births<<<ctx->birth_blocks, 256, 0, st>>>(ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk, ns, bd,
-                                                    ctx->sc, fc, a.k);
+        k_births<<<ctx->birth_blocks, 256, 0, st>>>(ctx->list, ns, bd, ctx->sc, fc, a.k);
         CK(cudaGetLastError());
     }
     CK(mark("births"));
@@ -518,26 +552,20 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     const size_t nu = (size_t)ctx->nu, C = ctx->C, nb = (size_t)ctx->nu_b;
     const void* src = nullptr;
     size_t n = 0;
-    // the active-cell list (for OFFSETS / NB reconstruction)
-    // the active-cell list, chunk by chunk (for OFFSETS / NB reconstruction)
+    // the flat active-cell list (for OFFSETS / NB reconstruction)
     auto read_list = [&](std::vector<uint32_t>& lc, std::vector<uint32_t>& ln, std::vector<uint32_t>& lst,
                          std::vector<uint32_t>& lnb, uint32_t& Ln, uint64_t& n_in) -> int {
         DevScalars s;
         CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
         n_in = s.n_in;
-        std::vector<uint32_t> cnt(ctx->cell_blocks);
-        CK(cudaMemcpy(cnt.data(), ctx->bt.cnt, cnt.size() * 4, cudaMemcpyDeviceToHost));
-        lc.clear(); ln.clear(); lst.clear(); lnb.clear();
-        for (uint32_t b = 0; b < ctx->cell_blocks; ++b) {
-            const size_t m = cnt[b], o = (size_t)b * ctx->cell_chunk, at = lc.size();
-            if (!m) continue;
-            lc.resize(at + m); ln.resize(at + m); lst.resize(at + m); lnb.resize(at + m);
-            CK(cudaMemcpy(lc.data() + at, ctx->list.c + o, m * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(ln.data() + at, ctx->list.n + o, m * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(lst.data() + at, ctx->list.start + o, m * 4, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy(lnb.data() + at, ctx->list.nb + o, m * 4, cudaMemcpyDeviceToHost));
+        Ln = s.Lc;
+        lc.resize(Ln); ln.resize(Ln); lst.resize(Ln); lnb.resize(Ln);
+        if (Ln) {
+            CK(cudaMemcpy(lc.data(), ctx->list.c, (size_t)Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(ln.data(), ctx->list.n, (size_t)Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lst.data(), ctx->list.start, (size_t)Ln * 4, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(lnb.data(), ctx->list.nb, (size_t)Ln * 4, cudaMemcpyDeviceToHost));
         }
-        Ln = (uint32_t)lc.size();
         return DOG_OK;
     };
     switch (what) {

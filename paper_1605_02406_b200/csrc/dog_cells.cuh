@@ -1,19 +1,21 @@
 // dog_cells.cuh -- per-cell stages of the cycle (Alg. 3, Alg. 5 slot allocation, Alg. 7 joint CDF).
 //
-// k_cells: one pass over the grid.  For every cell: n_c (from k_predict's counts), S_c = n_c w_pred
+// k_cells: one pass over the grid.  For every cell: n_c (from k_tilesort's counts), S_c = n_c w_pred
 // (Eq. 61, exact), m_p = min(S_c, occ_max) (Eq. 17), m_Fp = min(alpha m_F, 1 - m_p) (Eq. 62),
 // Dempster update (Eq. 63), birth split (Eqs. 67-68), fixed-point masses (A-23) and the readouts.
 // Cells holding particles or receiving born mass ("active" cells, typically ~1 % of the grid) are
-// staged, in cell order, in their block's segment of a list; every later stage works on that list.
-// Each block owns a contiguous chunk of cells, so the list is ordered by (block, position); the last
-// block to finish scans the few thousand block totals (no grid-wide look-back chain).
+// staged, in cell order, in their block's segment of a staging list (each block owns a contiguous chunk
+// of cells, so no grid-wide scan is needed); the last block to finish turns the per-block counts into
+// offsets, so (block, position) maps to a position in one flat, cell-ordered active list.
 //
-// k_list_scan (one block per cell chunk): first sorted slot of each cell (prefix of n_c), born-mass
-// CDF A_c (prefix of R_b) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A)) (A-15), the
-// gated joint mass J_c = R_p + [n_b > 0] R_b and its prefix (the joint CDF in cell-interleaved order,
-// A-25), the even-split parameters, and the work items of k_resample (<= 256 members of one cell).
-// Its last block scans the block totals -> joint-CDF offsets, W, w_bar (Eq. 57), U (A-24).
+// k_list_scan (persistent blocks over 2048-entry tiles of the flat active list, decoupled look-back):
+// gathers the staged entries into the flat list, first sorted slot of each cell (prefix of n_c),
+// born-mass CDF A_c (prefix of R_b) -> exact slot allocation s_c = floor((2 nu_b A_c + A) / (2A))
+// (A-15), the gated joint mass J_c = R_p + [n_b > 0] R_b and its prefix (the joint CDF in
+// cell-interleaved order, A-25), the even-split parameters, the birth work items (<= 256 slots of one
+// cell) and the run-list offsets.  The tile holding the last entry publishes W, w_bar (Eq. 57), U (A-24).
 #pragma once
+#include <cooperative_groups.h>
 #include <cstdint>
 #include "dog_common.cuh"
 #include "dog_rng.cuh"
@@ -22,36 +24,39 @@ namespace dog {
 
 constexpr uint32_t kItem = 256;   // members per k_resample work item
 
-struct CellList {           // SoA staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
+struct StageList {          // k_cells staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
     uint32_t* c;            // cell index
     uint32_t* n;            // persistent particles n_c
     uint64_t* Rp;           // floor(rho_p 2^40) (0 if n_c = 0)
     uint64_t* Rb;           // floor(rho_b 2^40) if m_zO > 0 else 0
     float* rho_p;           // f32 rho_p (moments denominator)
-    uint32_t* start;        // first cell-sorted slot of the cell          (k_list_scan)
-    uint32_t* sb;           // first birth slot of the cell (global)        (k_list_scan)
-    uint32_t* nb;           // birth slots of the cell                      (k_list_scan)
-    uint64_t* Pl;           // block-local exclusive joint prefix           (k_list_scan)
-    uint32_t* it;           // block-local exclusive birth work-item prefix (k_list_scan)
-    uint64_t* bp;           // R_p / n_c        (even split of R_p)         (k_list_scan)
+    uint32_t* np;           // runs ("pairs") of the cell over the sort tiles
+};
+
+struct CellList {           // the flat active list in cell order (SoA, capacity C)   (k_list_scan)
+    uint32_t* c;            // cell index
+    uint32_t* n;            // persistent particles n_c
+    uint64_t* Rp;           // floor(rho_p 2^40)
+    float* rho_p;           // f32 rho_p
+    uint32_t* start;        // first cell-sorted slot of the cell
+    uint32_t* sb;           // first birth slot of the cell (global)
+    uint32_t* nb;           // birth slots of the cell
+    uint64_t* P;            // exclusive joint-CDF prefix (A-25)
+    uint32_t* it;           // exclusive birth work-item prefix
+    uint64_t* bp;           // R_p / n_c        (even split of R_p)
     uint32_t* rp;           // R_p mod n_c
     uint64_t* bb;           // R_b / n_b
     uint32_t* rb;           // R_b mod n_b
-    uint32_t* np;           // runs ("pairs") of the cell over the sort tiles   (k_cells)
-    uint32_t* ps;           // block-local exclusive prefix of np               (k_list_scan)
-    uint32_t* pfill;        // pair-list fill counter                           (k_list_scan resets)
-    uint32_t* pdone;        // finished pairs (moments combine)                 (k_list_scan resets)
+    uint32_t* np;           // runs of the cell
+    uint32_t* ps;           // exclusive prefix of np (offset of the cell's run list)
+    uint32_t* pfill;        // run-list fill counter (reset here, k_pair_fill)
 };
 
 struct BlockTotals {        // one entry per cell chunk
-    uint32_t* cnt;          // active cells staged by the block                (k_cells)
-    uint64_t* n0;           // sum of n_c over them -> exclusive prefix        (k_cells, last block)
-    uint64_t* rb0;          // sum of R_b over them -> exclusive prefix        (k_cells, last block)
-    uint64_t* P0;           // sum of J -> exclusive joint prefix of the block  (k_list_scan, last block)
-    uint32_t* item0;        // birth work items -> exclusive prefix             (k_list_scan, last block)
-    uint32_t* ps0;          // pairs -> exclusive prefix of the block           (k_list_scan, last block)
-    uint32_t* s0;           // first birth slot of the block (global)           (k_list_scan)
-    uint32_t* done;         // [2] finished-block counters of k_cells / k_list_scan (zeroed per cycle)
+    uint32_t* cnt;          // active cells staged by the block -> exclusive prefix (k_cells, last block)
+    uint64_t* n0;           // sum of n_c over them (grand total by the last block)
+    uint64_t* rb0;          // sum of R_b over them (grand total by the last block)
+    uint32_t* done;         // finished-block counter of k_cells (zeroed per cycle)
 };
 
 __device__ __forceinline__ uint64_t fx40(float m)
@@ -132,16 +137,16 @@ __device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
 
 // Block b owns cells [b chunk, (b+1) chunk), 1024 per iteration; item i of thread t in an iteration
 // is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid bitmask).
-__global__ __launch_bounds__(kCellThreads) void k_cells(
+__global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
-    uint32_t* __restrict__ mvalid, CellDebug dbg, CellList L, uint32_t* __restrict__ cell2list,
-    BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
+    uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
 {
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
     __shared__ uint32_t s_run;
     __shared__ uint64_t s_A[9], s_N[9];
     __shared__ uint32_t s_bad[8];
+    __shared__ uint32_t s_C[9];
     __shared__ bool s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
@@ -216,7 +221,6 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
                 uint32_t npc = 0;
                 if (o[i].n) { npc = npairs[c]; npairs[c] = 0u; }
                 L.np[li] = npc;
-                cell2list[c] = li;
                 A_loc += o[i].Rb;
                 N_loc += o[i].n;
             }
@@ -245,142 +249,205 @@ __global__ __launch_bounds__(kCellThreads) void k_cells(
     __threadfence();
     const uint64_t N = block_prefix_inplace<uint64_t>(bt.n0, gridDim.x, s_N);
     const uint64_t A = block_prefix_inplace<uint64_t>(bt.rb0, gridDim.x, s_A);
-    if (tid == 0) { sc->n_in = N; sc->A = A; }
+    const uint32_t Lc = block_prefix_inplace<uint32_t>(bt.cnt, gridDim.x, s_C);
+    if (tid == 0) { sc->n_in = N; sc->A = A; sc->Lc = Lc; }
 }
 
 // ------------------------------------------------------------------------------------------------
-// exact floor((2 nu_b X + A) / (2A)) for X <= A < 2^64 without a 128-bit division: fp64 estimate,
-// then exact integer correction (the quotient is <= nu_b < 2^30).
-__device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_b)
+// exact floor((2 nu_b X + A) / (2A)) for X <= A < 2^64 without a 128-bit division: fp64 estimate
+// (rcpA = 1/A rounded, shared by all cells), then exact integer correction (the quotient is
+// <= nu_b < 2^30; the estimate is within one of it).
+__device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_b, double rcpA)
 {
     if (A == 0) return 0;
     const u128 num = (u128)2 * (u128)nu_b * (u128)X + (u128)A;
     const u128 den = (u128)2 * (u128)A;
-    uint64_t q = (uint64_t)floor(fma((double)X / (double)A, (double)nu_b, 0.5));
-    while ((u128)q * den > num) --q;
+    uint64_t q = (uint64_t)floor(fma((double)X * rcpA, (double)nu_b, 0.5));
+    while (q > 0 && (u128)q * den > num) --q;
     while ((u128)(q + 1) * den <= num) ++q;
     return q;
 }
-
-constexpr int kLsThreads = 256, kLsItems = 8, kLsTile = kLsThreads * kLsItems;
-
-__global__ __launch_bounds__(kLsThreads) void k_list_scan(CellList L, BlockTotals bt, uint32_t chunk,
-                                                          DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+__device__ __forceinline__ uint64_t slot_of(uint64_t X, uint64_t A, uint64_t nu_b)
 {
-    __shared__ uint64_t s_a[kLsThreads / 32 + 1], s_b[kLsThreads / 32 + 1];
-    __shared__ uint32_t s_c[kLsThreads / 32 + 1];
-    __shared__ bool s_last;
-    const int tid = threadIdx.x;
-    const uint32_t blk = blockIdx.x;
-    const uint64_t A = sc->A;
-    const uint64_t nu_b = fc.nu_b;
-    uint64_t start0 = bt.n0[blk], A0 = bt.rb0[blk];
-    const uint32_t cnt = bt.cnt[blk];
-    const uint32_t lbase = blk * chunk;
-    if (tid == 0) bt.s0[blk] = (uint32_t)slot_of(A0, A, nu_b);
-    uint64_t J0 = 0;                          // block-local joint prefix
-    uint32_t I0 = 0;                          // block-local birth work-item prefix
-    uint32_t PS0 = 0;                         // block-local pair prefix
-    for (uint32_t t0 = 0; t0 < cnt; t0 += kLsTile) {
-        const uint32_t b = t0 + tid * kLsItems;
-        uint32_t n[kLsItems], npv[kLsItems];
-        uint64_t Rb[kLsItems], Rp[kLsItems];
-        uint64_t ns = 0, rbs = 0;
-        uint32_t pss = 0;
+    return slot_of(X, A, nu_b, A ? 1.0 / (double)A : 0.0);
+}
+
+// floor(a / d) and a mod d for a < 2^53, 0 < d < 2^32 (fixed-point masses are <= 2^40): the fp64
+// estimate a * (1/d) is within one of the exact quotient; one integer correction settles it.
+__device__ __forceinline__ uint64_t divmod53(uint64_t a, uint32_t d, uint32_t& r)
+{
+    const double est = __dmul_rn((double)a, __drcp_rn((double)d));
+    uint64_t q = est > 0.0 ? (uint64_t)est : 0ull;
+    int64_t rem = (int64_t)(a - q * (uint64_t)d);
+    if (rem < 0) { --q; rem += d; }
+    else if (rem >= (int64_t)d) { ++q; rem -= d; }
+    r = (uint32_t)rem;
+    return q;
+}
+
+// k_list_scan runs as ONE thread-block cluster (kLsCluster CTAs of 1024 threads on as many SMs): the two
+// dependent prefix sums over the active list -- (n_c, runs, R_b) and then (J_c, birth work items) --
+// are exchanged between the CTAs through distributed shared memory with cluster barriers, so no
+// global-memory look-back chain is needed.  The list is processed in rounds of kLsCluster*1024*kLsItems
+// entries (one round for typical scenes).
+constexpr int kLsThreads = 1024, kLsWarps = kLsThreads / 32, kLsItems = 2;
+constexpr int kLsClusterMax = 16;
+
+// Exclusive prefix over a warp's 32*I entries laid out entry = i*32 + lane (so loads and stores of
+// consecutive entries coalesce); returns the warp total.
+template <int I>
+__device__ __forceinline__ uint64_t warp_excl_items(const uint64_t (&v)[I], uint64_t (&ex)[I])
+{
+    const int lane = threadIdx.x & 31;
+    uint64_t carry = 0;
 #pragma unroll
-        for (int i = 0; i < kLsItems; ++i) {
-            const bool ok = b + i < cnt;
-            n[i] = ok ? L.n[lbase + b + i] : 0u;
-            npv[i] = ok ? L.np[lbase + b + i] : 0u;
-            Rb[i] = ok ? L.Rb[lbase + b + i] : 0ull;
-            Rp[i] = ok ? L.Rp[lbase + b + i] : 0ull;
-            ns += n[i];
-            rbs += Rb[i];
-            pss += npv[i];
-        }
-        uint32_t tps;
-        uint32_t xps = PS0 + block_excl_scan<uint32_t, kLsThreads / 32>(pss, s_c, tps);
-#pragma unroll
-        for (int i = 0; i < kLsItems; ++i) {
-            if (b + i < cnt) L.ps[lbase + b + i] = xps;
-            xps += npv[i];
-        }
-        PS0 += tps;
-        uint64_t tn, trb;
-        const uint64_t xn = block_excl_scan<uint64_t, kLsThreads / 32>(ns, s_a, tn);
-        const uint64_t xrb = block_excl_scan<uint64_t, kLsThreads / 32>(rbs, s_b, trb);
-        uint64_t start = start0 + xn;
-        uint64_t Ax = A0 + xrb;               // A_{c-1}
-        uint64_t s_prev = slot_of(Ax, A, nu_b);
-        uint64_t J[kLsItems];
-        uint32_t its[kLsItems];
-        uint64_t js = 0;
-        uint32_t is = 0;
-#pragma unroll
-        for (int i = 0; i < kLsItems; ++i) {
-            Ax += Rb[i];
-            const uint64_t s = Rb[i] ? slot_of(Ax, A, nu_b) : s_prev;
-            const uint32_t nbv = (uint32_t)(s - s_prev);
-            if (b + i < cnt) {
-                const uint32_t li = lbase + b + i;
-                L.start[li] = (uint32_t)start;
-                L.sb[li] = (uint32_t)s_prev;
-                L.nb[li] = nbv;
-                L.bp[li] = n[i] ? Rp[i] / n[i] : 0ull;
-                L.rp[li] = n[i] ? (uint32_t)(Rp[i] % n[i]) : 0u;
-                L.bb[li] = nbv ? Rb[i] / nbv : 0ull;
-                L.rb[li] = nbv ? (uint32_t)(Rb[i] % nbv) : 0u;
-                L.pfill[li] = 0u;
-                L.pdone[li] = 0u;
-                J[i] = Rp[i] + (nbv ? Rb[i] : 0ull);
-                its[i] = (nbv + kItem - 1) / kItem;
-            } else {
-                J[i] = 0;
-                its[i] = 0;
-            }
-            start += n[i];
-            js += J[i];
-            is += its[i];
-            s_prev = s;
-        }
-        uint64_t tj;
-        uint32_t ti;
-        const uint64_t xj = block_excl_scan<uint64_t, kLsThreads / 32>(js, s_a, tj);
-        const uint32_t xi = block_excl_scan<uint32_t, kLsThreads / 32>(is, s_c, ti);
-        uint64_t run = J0 + xj;
-        uint32_t irun = I0 + xi;
-#pragma unroll
-        for (int i = 0; i < kLsItems; ++i) {
-            if (b + i < cnt) { L.Pl[lbase + b + i] = run; L.it[lbase + b + i] = irun; }
-            run += J[i];
-            irun += its[i];
-        }
-        start0 += tn;
-        A0 += trb;
-        J0 += tj;
-        I0 += ti;
+    for (int i = 0; i < I; ++i) {
+        const uint64_t inc = warp_incl_scan(v[i], lane);
+        ex[i] = carry + inc - v[i];
+        carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    if (tid == 0) {
-        bt.P0[blk] = J0;
-        bt.item0[blk] = I0;
-        bt.ps0[blk] = PS0;
-        __threadfence();
-        s_last = atomicAdd(&bt.done[1], 1u) == gridDim.x - 1;
+    return carry;
+}
+
+// Two-value exclusive prefix over the CTA's warps (warp totals t) and over the cluster's CTAs.
+// Returns the offset of the calling warp within the cluster round; *round_total = the round's total.
+__device__ __forceinline__ ulonglong2 cluster_offsets(ulonglong2 t, ulonglong2* s_w, ulonglong2* s_tot,
+                                                      ulonglong2* s_base, ulonglong2& round_total)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_w[warp] = t;
+    __syncthreads();
+    if (warp == 0) {
+        const ulonglong2 v = s_w[lane];
+        const uint64_t ix = warp_incl_scan(v.x, lane), iy = warp_incl_scan(v.y, lane);
+        s_w[lane] = make_ulonglong2(ix - v.x, iy - v.y);
+        if (lane == 31) *s_tot = make_ulonglong2(ix, iy);
+    }
+    cluster.sync();                                  // every CTA's total is visible cluster-wide
+    if (warp == 0) {
+        const unsigned rank = cluster.block_rank(), nc = cluster.num_blocks();
+        ulonglong2 v = make_ulonglong2(0ull, 0ull);
+        if ((unsigned)lane < nc) v = *cluster.map_shared_rank(s_tot, lane);
+        const uint64_t px = warp_sum((unsigned)lane < rank ? v.x : 0ull);
+        const uint64_t py = warp_sum((unsigned)lane < rank ? v.y : 0ull);
+        const uint64_t tx = warp_sum(v.x), ty = warp_sum(v.y);
+        if (lane == 0) { s_base[0] = make_ulonglong2(px, py); s_base[1] = make_ulonglong2(tx, ty); }
     }
     __syncthreads();
-    if (!s_last) return;
-    // the last block: joint-CDF and work-item offsets of the chunks, totals (Eq. 57, A-24, A-26)
-    __threadfence();
-    const uint64_t W = block_prefix_inplace<uint64_t>(bt.P0, gridDim.x, s_a);
-    const uint32_t items = block_prefix_inplace<uint32_t>(bt.item0, gridDim.x, s_c);
-    block_prefix_inplace<uint32_t>(bt.ps0, gridDim.x, s_c);
-    if (tid == 0) {
-        sc->W = W;
-        sc->n_items = items;
-        sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
-        sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
+    const ulonglong2 w = s_w[warp], cb = s_base[0];
+    round_total = s_base[1];
+    __syncthreads();
+    return make_ulonglong2(cb.x + w.x, cb.y + w.y);
+}
+
+__global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList L, BlockTotals bt, uint32_t nblk,
+                                                          uint32_t chunk, uint32_t* __restrict__ cell2list,
+                                                          DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+{
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ uint32_t s_cnt0[kMaxCellBlocks + 1];
+    __shared__ ulonglong2 s_w[kLsWarps];
+    __shared__ ulonglong2 s_tot[2];
+    __shared__ ulonglong2 s_base[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t rank = cluster.block_rank(), nc = cluster.num_blocks();
+    const uint32_t Lc = sc->Lc;
+    const uint64_t A = sc->A;
+    const uint64_t nu_b = fc.nu_b;
+    const double rcpA = A ? 1.0 / (double)A : 0.0;
+    for (uint32_t b = tid; b < nblk; b += kLsThreads) s_cnt0[b] = bt.cnt[b];
+    if (tid == 0) s_cnt0[nblk] = Lc;
+    __syncthreads();
+    const uint32_t cap = nc * kLsThreads * kLsItems;
+    ulonglong2 carry1 = make_ulonglong2(0ull, 0ull), carry2 = carry1;
+    for (uint32_t r0 = 0; r0 < Lc; r0 += cap) {
+        const uint32_t gw = r0 + rank * (kLsThreads * kLsItems) + warp * (32 * kLsItems) + lane;   // + 32 i
+        uint32_t c[kLsItems], n[kLsItems], npv[kLsItems];
+        uint64_t Rb[kLsItems], Rp[kLsItems], X[kLsItems];
+        float rho[kLsItems];
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            const uint32_t g = gw + 32 * i;
+            c[i] = 0; n[i] = 0; npv[i] = 0; Rb[i] = 0; Rp[i] = 0; rho[i] = 0.0f;
+            if (g < Lc) {   // staged position: chunk b = last with cnt0[b] <= g
+                uint32_t lo = 0, hi = nblk;
+                while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (s_cnt0[m] <= g) lo = m; else hi = m; }
+                const uint32_t si = lo * chunk + (g - s_cnt0[lo]);
+                c[i] = Ls.c[si]; n[i] = Ls.n[si]; npv[i] = Ls.np[si];
+                Rb[i] = Ls.Rb[si]; Rp[i] = Ls.Rp[si]; rho[i] = Ls.rho_p[si];
+            }
+            X[i] = (uint64_t)n[i] | ((uint64_t)npv[i] << 32);
+        }
+        uint64_t exX[kLsItems], exB[kLsItems];
+        const uint64_t wX = warp_excl_items<kLsItems>(X, exX);
+        const uint64_t wB = warp_excl_items<kLsItems>(Rb, exB);
+        ulonglong2 tot1;
+        const ulonglong2 off1 = cluster_offsets(make_ulonglong2(wX, wB), s_w, &s_tot[0], s_base, tot1);
+        const ulonglong2 base1 = make_ulonglong2(carry1.x + off1.x, carry1.y + off1.y);
+        uint64_t J[kLsItems], its[kLsItems], sp[kLsItems];
+        uint32_t nbv[kLsItems];
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            const bool ok = gw + 32 * i < Lc;
+            const uint64_t Ax = base1.y + exB[i];   // A_{c-1}
+            sp[i] = ok ? slot_of(Ax, A, nu_b, rcpA) : 0ull;
+            const uint64_t s_next = Rb[i] ? slot_of(Ax + Rb[i], A, nu_b, rcpA) : sp[i];
+            nbv[i] = (uint32_t)(s_next - sp[i]);
+            J[i] = ok ? Rp[i] + (nbv[i] ? Rb[i] : 0ull) : 0ull;
+            its[i] = (nbv[i] + kItem - 1) / kItem;
+        }
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            const uint32_t g = gw + 32 * i;
+            if (g >= Lc) continue;
+            const uint64_t x0 = base1.x + exX[i];
+            L.c[g] = c[i]; L.n[g] = n[i]; L.Rp[g] = Rp[i]; L.rho_p[g] = rho[i];
+            L.np[g] = npv[i]; L.ps[g] = (uint32_t)(x0 >> 32); L.pfill[g] = 0u;
+            L.start[g] = (uint32_t)x0;
+            L.sb[g] = (uint32_t)sp[i];
+            L.nb[g] = nbv[i];
+            uint32_t rem = 0;
+            L.bp[g] = n[i] ? divmod53(Rp[i], n[i], rem) : 0ull;
+            L.rp[g] = rem;
+            rem = 0;
+            L.bb[g] = nbv[i] ? divmod53(Rb[i], nbv[i], rem) : 0ull;
+            L.rb[g] = rem;
+            cell2list[c[i]] = g;
+        }
+        uint64_t exJ[kLsItems], exI[kLsItems];
+        const uint64_t wJ = warp_excl_items<kLsItems>(J, exJ);
+        const uint64_t wI = warp_excl_items<kLsItems>(its, exI);
+        ulonglong2 tot2;
+        const ulonglong2 off2 = cluster_offsets(make_ulonglong2(wJ, wI), s_w, &s_tot[1], s_base, tot2);
+        const ulonglong2 base2 = make_ulonglong2(carry2.x + off2.x, carry2.y + off2.y);
+#pragma unroll
+        for (int i = 0; i < kLsItems; ++i) {
+            const uint32_t g = gw + 32 * i;
+            if (g >= Lc) continue;
+            const uint64_t P = base2.x + exJ[i];
+            const uint32_t it0 = (uint32_t)(base2.y + exI[i]);
+            L.P[g] = P;
+            L.it[g] = it0;
+            if (g == Lc - 1) {   // the list's last entry publishes the totals
+                const uint64_t W = P + J[i];
+                sc->W = W;
+                sc->n_items = it0 + (uint32_t)its[i];
+                sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
+                sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
+                sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
+            }
+        }
+        carry1.x += tot1.x; carry1.y += tot1.y;
+        carry2.x += tot2.x; carry2.y += tot2.y;
+    }
+    if (Lc == 0 && rank == 0 && tid == 0) {   // empty list (A-26)
+        sc->W = 0; sc->n_items = 0; sc->s_total = 0; sc->w_bar = 0.0f;
         sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
     }
+    cluster.sync();   // no CTA leaves while another may still read its shared memory
 }
 
 }  // namespace dog

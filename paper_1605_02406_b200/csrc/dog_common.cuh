@@ -16,8 +16,8 @@ struct DevScalars {
     uint64_t A;          // total fixed-point born mass
     uint64_t n_in;       // particles inside the grid after predict
     uint64_t s_total;    // birth slots allocated (nu_b or 0)
-    uint32_t n_items;    // k_resample work items of the cycle
-    uint32_t pad;
+    uint32_t n_items;    // birth work items of the cycle
+    uint32_t Lc;         // entries of the active-cell list
 };
 
 constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
@@ -112,39 +112,41 @@ __device__ __forceinline__ uint32_t lookback_u30(uint32_t* status, uint32_t tile
     return excl;
 }
 
-// Pair-of-u64 variant: status flag (1 = aggregate, 2 = inclusive) + 16-byte value slots written
-// before the flag with release semantics.
+// Pair-of-u64 variant: status flag + 16-byte value slots written before the flag with release
+// semantics.  Flags carry the cycle's epoch (flag = epoch << 2 | 1 aggregate / 2 inclusive), so they
+// never need resetting between cycles.
 struct LookbackPair {
     uint32_t* flag;
     ulonglong2* agg;
     ulonglong2* inc;
 };
 
-__device__ __forceinline__ ulonglong2 lookback_pair(LookbackPair s, uint32_t tile, ulonglong2 total)
+__device__ __forceinline__ ulonglong2 lookback_pair(LookbackPair s, uint32_t tile, ulonglong2 total, uint32_t epoch)
 {
     const int lane = threadIdx.x & 31;
+    const uint32_t fa = (epoch << 2) | 1u, fi = (epoch << 2) | 2u;
     if (tile == 0) {
-        if (lane == 0) { s.inc[0] = total; st_release(s.flag, 2u); }
+        if (lane == 0) { s.inc[0] = total; st_release(s.flag, fi); }
         return make_ulonglong2(0ull, 0ull);
     }
-    if (lane == 0) { s.agg[tile] = total; st_release(s.flag + tile, 1u); }
+    if (lane == 0) { s.agg[tile] = total; st_release(s.flag + tile, fa); }
     unsigned long long ex = 0, ey = 0;
     int j = (int)tile - 1;
     while (true) {
         const int p = j - lane;
-        const uint32_t f = p >= 0 ? ld_acquire(s.flag + p) : 2u;
-        const uint32_t incm = __ballot_sync(0xffffffffu, f == 2u);
+        const uint32_t f = p >= 0 ? ld_acquire(s.flag + p) : fi;
+        const uint32_t incm = __ballot_sync(0xffffffffu, f == fi);
         const int first = incm ? __ffs(incm) - 1 : 31;
-        const uint32_t zm = __ballot_sync(0xffffffffu, f == 0u);
+        const uint32_t zm = __ballot_sync(0xffffffffu, f != fi && f != fa);
         if (zm & ((2u << first) - 1u)) continue;
         ulonglong2 v = make_ulonglong2(0ull, 0ull);
-        if (lane <= first && p >= 0) v = ld_relaxed128(f == 2u ? s.inc + p : s.agg + p);
+        if (lane <= first && p >= 0) v = ld_relaxed128(f == fi ? s.inc + p : s.agg + p);
         ex += warp_sum(v.x);
         ey += warp_sum(v.y);
         if (incm) break;
         j -= 32;
     }
-    if (lane == 0) { s.inc[tile] = make_ulonglong2(ex + total.x, ey + total.y); st_release(s.flag + tile, 2u); }
+    if (lane == 0) { s.inc[tile] = make_ulonglong2(ex + total.x, ey + total.y); st_release(s.flag + tile, fi); }
     return make_ulonglong2(ex, ey);
 }
 

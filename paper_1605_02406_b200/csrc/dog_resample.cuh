@@ -12,6 +12,7 @@
 // (A-24): i in [F(Q_r), F(Q_{r+1})), F(X) = #{i : t_i < X} = clamp(ceil((X nu 2^32 - U W) / (W 2^32)),
 // 0, nu).  This selects exactly what the oracle's binary search over the particle-level CDF selects.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include "dog_cells.cuh"
 #include "dog_common.cuh"
@@ -65,18 +66,19 @@ __device__ __forceinline__ uint32_t fcount(uint64_t X, const RsConst& r)
 }
 
 // Moments of cell c from its velocity sums (Eqs. 81-84 with the uniform weight w' = rho_p / S w_pred).
-__device__ __forceinline__ void finalize_cell(uint32_t c, const double* s, uint32_t n, float rp, float w_pred,
-                                              float2* __restrict__ mean, float* __restrict__ cov)
+__device__ __forceinline__ void finalize_cell(uint32_t c, double s0, double s1, double s2, double s3, double s4,
+                                              uint32_t n, float rp, float w_pred, float2* __restrict__ mean,
+                                              float* __restrict__ cov)
 {
     const float S = __double2float_rn(__dmul_rn((double)n, (double)w_pred));
     if (!(rp > 0.0f) || !(S > 0.0f)) return;
     const float w = __fmul_rn(__fdiv_rn(rp, S), w_pred);       // Eq. 71 with p_A = 0, Eq. 73
     const double wd = (double)w, rd = (double)rp;
-    const double mx = wd * s[0] / rd, my = wd * s[1] / rd;
+    const double mx = wd * s0 / rd, my = wd * s1 / rd;
     mean[c] = make_float2((float)mx, (float)my);
-    cov[3 * (size_t)c] = (float)(wd * s[2] / rd - mx * mx);
-    cov[3 * (size_t)c + 1] = (float)(wd * s[3] / rd - my * my);
-    cov[3 * (size_t)c + 2] = (float)(wd * s[4] / rd - mx * my);
+    cov[3 * (size_t)c] = (float)(wd * s2 / rd - mx * mx);
+    cov[3 * (size_t)c + 1] = (float)(wd * s3 / rd - my * my);
+    cov[3 * (size_t)c + 2] = (float)(wd * s4 / rd - mx * my);
 }
 
 struct NextState { float *x, *y, *vx, *vy; uint32_t* jidx; };
@@ -136,75 +138,56 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
-constexpr int kRtRunCache = 256;                                      // runs whose RunInfo sits in smem
+constexpr int kRtRunCache = 128;                                      // runs whose RunInfo sits in smem
 constexpr uint32_t kNoF = 0xFFFFFFFFu;                                // position outside the grid
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
     uint32_t F0[kSortTile];            // F(Q_r): first output of the member at each position
-    uint32_t F1[kSortTile];            // F(Q_{r+1}): one past its last output
-    RunInfo run[kRtRunCache];
-    MomPartial pa[kRtThreads], pb[kRtThreads];
+    uint32_t rO[kSortTile + 4];        // run -> F(Q_end) (phase B), then its offset in the tile's compact
+                                       // output space (exclusive prefix of the runs' output counts)
+    alignas(16) RunInfo run[kRtRunCache];
+    union alignas(16) {
+        struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phases B, D
+        uint32_t osrc[kSortTile];      // phase C: compact output -> (run << 12 | position) + 1
+    } u;
+    uint32_t scan[kRtThreads / 32 + 1];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
+static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, F0) % 16 == 0, "vector smem access");
 
-// Warp-cooperative write of the copies of the lanes' members: lanes whose output ranges are adjacent
-// (F1 of a lane == F0 of the next) form a segment whose outputs are one contiguous range, written 32 at
-// a time; the owner of an output is found by a 5-step shuffle search.  Coalesced and balanced whatever
-// the copy counts (one member can own hundreds of outputs).
-__device__ __forceinline__ void write_segments(bool valid, uint32_t F0, uint32_t F1, float X, float Y, float VX,
-                                               float VY, uint32_t J, NextState& out)
+// Block-wide exclusive max-scan of one value per thread (values >= 0).
+__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
 {
-    const int lane = threadIdx.x & 31;
-    const uint32_t pF1 = __shfl_up_sync(0xffffffffu, F1, 1);
-    const bool pvalid = __shfl_up_sync(0xffffffffu, valid, 1);
-    const bool head = valid && (lane == 0 || !pvalid || pF1 != F0);
-    uint32_t heads = __ballot_sync(0xffffffffu, head);
-    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-    while (heads) {
-        const int a = __ffs(heads) - 1;
-        heads &= heads - 1;
-        const int nxt_head = heads ? __ffs(heads) - 1 : 32;
-        // segment = valid lanes [a, b]: stops before the next head or the first invalid lane after a
-        const uint32_t inval_after = ~vmask & (0xffffffffu << a);
-        const int nxt_inval = inval_after ? __ffs(inval_after) - 1 : 32;
-        const int b = min(nxt_head, nxt_inval) - 1;
-        const uint32_t lo = __shfl_sync(0xffffffffu, F0, a);
-        const uint32_t hi = __shfl_sync(0xffffffffu, F1, b);
-        const uint32_t f0 = lane < a ? 0u : (lane > b ? hi : F0);
-        for (uint32_t o0 = lo; o0 < hi; o0 += 32) {
-            const uint32_t o = o0 + lane;
-            int own = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
 #pragma unroll
-            for (int step = 16; step; step >>= 1) {
-                const int cand = own + step;
-                const uint32_t f = __shfl_sync(0xffffffffu, f0, cand);
-                if (f <= o) own = cand;
-            }
-            const float x = __shfl_sync(0xffffffffu, X, own), y = __shfl_sync(0xffffffffu, Y, own);
-            const float vx = __shfl_sync(0xffffffffu, VX, own), vy = __shfl_sync(0xffffffffu, VY, own);
-            const uint32_t jj = __shfl_sync(0xffffffffu, J, own);
-            if (o < hi) {
-                out.x[o] = x; out.y[o] = y; out.vx[o] = vx; out.vy[o] = vy;
-                if (out.jidx) out.jidx[o] = jj;
-            }
-        }
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc = max(inc, o);
     }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < warp; ++w) pre = max(pre, s_warp[w]);
+    const uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    __syncthreads();
+    return max(pre, lane ? ex : 0u);
 }
 
-// Persistent particles, one block per sort tile.  Phase B: thread t owns the tile's local sorted
-// positions [16t, 16t+16) -- batched gathers of the predicted velocities, velocity sums per run
-// segment, and the output range [F(Q_r), F(Q_{r+1})) of every member (member r = pre(run) + position
-// within the run).  Phase C: warps take 32 consecutive positions at a time, gather the full state and
-// write the copies cooperatively (write_segments).  Phase D: run segments spanning threads are combined
-// in thread order, a cell's runs over the tiles in tile order by the last run to finish (deterministic).
-__global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
-    const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, BlockTotals bt, uint32_t chunk,
-    const uint32_t* __restrict__ plist, NextState out, uint32_t* __restrict__ perm_dbg,
-    float2* __restrict__ mean, float* __restrict__ cov, MomPartial* __restrict__ ppart,
-    const DevScalars* __restrict__ sc, FilterConst fc)
+// Persistent particles, one block per sort tile (4096 particles in input order; lperm gives their
+// stable cell order).  Phase B: thread t owns the sorted positions [16t, 16t+16) -- batched gathers of
+// the predicted velocities, velocity sums per run segment, and F(Q_r) of every member (member r =
+// pre(run) + position within the run).  Phase D: run segments spanning threads are combined in thread
+// order (deterministic) -> per-run velocity sums.  Phase C: the members' output ranges, concatenated
+// over the tile's runs, form a compact output space; in windows of 4096 outputs each member with
+// copies marks its first output, a block max-scan spreads the owner over its outputs, and threads then
+// write consecutive outputs (coalesced, balanced whatever the copy counts).
+__global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
+    const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, NextState out,
+    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
@@ -220,7 +203,6 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
     const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
-    const float w_pred = sc->w_pred;
     const uint32_t p0 = tid * kRtItems;
     // ---- phase A: local permutation, run starts, run parameters (one round trip)
     {
@@ -238,24 +220,26 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
     const uint32_t srun = S.sentinel_run;
     auto run_info = [&](uint32_t j) -> RunInfo { return j < (uint32_t)kRtRunCache ? S.run[j] : tp.run[base + j]; };
 
-    // ---- phase B: velocity gathers, velocity sums, output ranges per member
+    // ---- phase B: velocity gathers, velocity sums, F(Q_r) per member
+    const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
+    uint32_t j0 = 0;                                        // run containing p0
     if (p0 < n) {
-        uint32_t lo = 0, hi = nd;                           // run containing p0
+        uint32_t lo = 0, hi = nd;
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= p0) lo = m; else hi = m; }
+        j0 = lo;
         uint32_t j = lo, first = S.first[j], end = S.first[j + 1];
         RunInfo q = run_info(j);
         double acc[5] = {0, 0, 0, 0, 0};
         bool first_seg = true;
         uint32_t Fcarry = kNoF;                             // F(Q_r) of the next member, same run
-        const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
         auto flush = [&]() {
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
             if (j != srun) {
                 if (first >= p0 && end <= pend) ppart[base + j] = mp;    // run inside this thread
-                else if (first_seg) S.pa[tid] = mp;
-                else S.pb[tid] = mp;
+                else if (first_seg) S.u.m.pa[tid] = mp;
+                else S.u.m.pb[tid] = mp;
             }
             first_seg = false;
         };
@@ -277,57 +261,23 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
                     q = run_info(j);
                     Fcarry = kNoF;
                 }
-                if (j == srun) { S.F0[p] = kNoF; S.F1[p] = kNoF; continue; }
+                if (j == srun) { S.F0[p] = kNoF; continue; }
                 const double a = (double)VX[u], bq = (double)VY[u];
                 acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
                 const uint32_t mr = q.pre + (p - first);    // member rank within the cell
                 if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
-                if (rc.W) {
-                    const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-                    const uint32_t F0 = Fcarry != kNoF ? Fcarry : fcount(Q0, rc);
-                    const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
-                    S.F0[p] = F0; S.F1[p] = F1;
-                    Fcarry = F1;
-                }
+                const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+                const uint32_t F0 = Fcarry != kNoF ? Fcarry : fcount(Q0, rc);
+                const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                S.F0[p] = F0;
+                if (p + 1 == end) S.rO[j] = F1;            // F(Q_end) of the run
+                Fcarry = F1;
             }
         }
         flush();
     }
     __syncthreads();
-    // ---- phase C: warp-strided positions, full-state gathers, cooperative coalesced copy writes
-    if (rc.W) {
-#pragma unroll 1
-        for (int it = 0; it < kRtItems; it += 4) {
-            uint32_t pp[4], src[4], F0[4], F1[4];
-            bool ok[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                pp[h] = (uint32_t)(warp * kRtItems + it + h) * 32 + lane;
-                ok[h] = pp[h] < n;
-                const uint32_t pc = ok[h] ? pp[h] : 0u;
-                F0[h] = S.F0[pc]; F1[h] = S.F1[pc];
-                ok[h] = ok[h] && F0[h] != kNoF;
-                src[h] = base + S.lp[pc];
-            }
-            float X[4], Y[4], VX[4], VY[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) { X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]]; }
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                uint32_t J = 0;
-                if (out.jidx && ok[h]) {                    // debug: joint index of the member
-                    uint32_t lo = 0, hi = nd;
-                    while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= pp[h]) lo = m; else hi = m; }
-                    const RunInfo q = run_info(lo);
-                    J = q.jbase + q.pre + (pp[h] - S.first[lo]);
-                }
-                write_segments(ok[h], F0[h], F1[h], X[h], Y[h], VX[h], VY[h], J, out);
-            }
-        }
-    }
-    // ---- phase D: run segments spanning threads (one warp per run, fixed summation order), then
-    //      cell completion
-    __syncthreads();
+    // ---- phase D: run segments spanning threads (one warp per run, fixed summation order)
     for (uint32_t r = warp; r < nd; r += kRtThreads / 32) {
         if (r == srun) continue;
         const uint32_t f = S.first[r], e = S.first[r + 1];
@@ -335,7 +285,7 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
         if (tf == tl) continue;                             // written directly in phase B
         double s5[5] = {0, 0, 0, 0, 0};
         for (uint32_t u = tf + lane; u <= tl; u += 32) {
-            const MomPartial& mp = (u == tf) ? ((f > tf * kRtItems) ? S.pb[tf] : S.pa[tf]) : S.pa[u];
+            const MomPartial& mp = (u == tf) ? ((f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf]) : S.u.m.pa[u];
 #pragma unroll
             for (int i = 0; i < 5; ++i) s5[i] += mp.s[i];
         }
@@ -348,52 +298,138 @@ __global__ __launch_bounds__(kRtThreads, 2) void k_resample_tiles(
             ppart[base + r] = mp;
         }
     }
+    if (rc.W == 0) return;
+    // ---- compact output space: exclusive prefix over runs of F(Q_end) - F(Q_first)
+    uint32_t carry = 0;
+    for (uint32_t r0 = 0; r0 < nd; r0 += kRtThreads) {
+        const uint32_t r = r0 + tid;
+        const uint32_t c = (r < nd && r != srun) ? S.rO[r] - S.F0[S.first[r]] : 0u;
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
+        if (r < nd) S.rO[r] = carry + ex;
+        carry += tot;
+    }
+    if (tid == 0) S.rO[nd] = carry;
     __syncthreads();
-    for (uint32_t r = tid; r < nd; r += kRtThreads) {
-        if (r == srun) continue;
-        const uint32_t key = tp.key[base + r];
-        const uint32_t li = run_info(r).li;
-        const uint32_t m = L.np[li];
-        if (m == 1) {
-            finalize_cell(key, ppart[base + r].s, L.n[li], L.rho_p[li], w_pred, mean, cov);
-            continue;
+    const uint32_t Ot = carry;
+    // ---- phase C: windows of the compact output space
+    for (uint32_t w0 = 0; w0 < Ot; w0 += kSortTile) {
+        uint32_t* os = S.u.osrc;
+        reinterpret_cast<uint4*>(os + p0)[0] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(os + p0)[1] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(os + p0)[2] = make_uint4(0, 0, 0, 0);
+        reinterpret_cast<uint4*>(os + p0)[3] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        if (p0 < n) {   // members with copies mark the first of their outputs inside the window
+            uint32_t j = j0, first = S.first[j], end = S.first[j + 1];
+            uint32_t D = j == srun ? 0u : S.F0[first] - S.rO[j];
+            for (uint32_t p = p0; p < pend; ++p) {
+                if (p >= end) { ++j; first = end; end = S.first[j + 1]; D = j == srun ? 0u : S.F0[first] - S.rO[j]; }
+                if (j == srun) break;                       // the sentinel run is the tile's last
+                const uint32_t C0 = S.F0[p] - D;
+                const uint32_t C1 = p + 1 < end ? S.F0[p + 1] - D : S.rO[j + 1];
+                if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = ((j << 12) | p) + 1u;
+            }
         }
-        __threadfence();
-        if (atomicAdd(&L.pdone[li], 1u) != m - 1) continue;
-        __threadfence();
-        const uint32_t* pl = plist + bt.ps0[li / chunk] + L.ps[li];
-        double sum[5] = {0, 0, 0, 0, 0};
-        for (uint32_t qq = 0; qq < m; ++qq) {
-            const double* ps = ppart[pl[qq]].s;
+        __syncthreads();
+        {   // inclusive max-scan over the window: thread-contiguous 16 entries
+            uint32_t v[kRtItems];
 #pragma unroll
-            for (int i = 0; i < 5; ++i) sum[i] += __ldcg(ps + i);
+            for (int i = 0; i < kRtItems / 4; ++i) {
+                const uint4 x = reinterpret_cast<const uint4*>(os + p0)[i];
+                v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
+            }
+#pragma unroll
+            for (int i = 1; i < kRtItems; ++i) v[i] = max(v[i], v[i - 1]);
+            const uint32_t pre = block_excl_max(v[kRtItems - 1], S.scan);
+#pragma unroll
+            for (int i = 0; i < kRtItems / 4; ++i)
+                reinterpret_cast<uint4*>(os + p0)[i] =
+                    make_uint4(max(v[4 * i], pre), max(v[4 * i + 1], pre), max(v[4 * i + 2], pre), max(v[4 * i + 3], pre));
         }
-        finalize_cell(key, sum, L.n[li], L.rho_p[li], w_pred, mean, cov);
+        __syncthreads();
+        const uint32_t wn = min((uint32_t)kSortTile, Ot - w0);
+#pragma unroll 1
+        for (uint32_t i0 = 0; i0 < wn; i0 += 4 * kRtThreads) {
+            uint32_t o[4], src[4], J[4];
+            bool ok[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const uint32_t i = i0 + h * kRtThreads + tid;
+                ok[h] = i < wn;
+                const uint32_t v = os[ok[h] ? i : 0u] - 1u;
+                const uint32_t j = v >> 12, p = v & 4095u;
+                o[h] = w0 + i + S.F0[S.first[j]] - S.rO[j];
+                src[h] = base + S.lp[p];
+                J[h] = 0;
+                if (out.jidx) { const RunInfo q = run_info(j); J[h] = q.jbase + q.pre + (p - S.first[j]); }
+            }
+            float X[4], Y[4], VX[4], VY[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) { X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]]; }
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if (!ok[h]) continue;
+                out.x[o[h]] = X[h]; out.y[o[h]] = Y[h]; out.vx[o[h]] = VX[h]; out.vy[o[h]] = VY[h];
+                if (out.jidx) out.jidx[o[h]] = J[h];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Velocity moments per cell (Eqs. 81-84): the cell's run sums combined in tile order (k_pair_sort left
+// the run list in that order) in a fixed summation order.  Groups of 8 lanes take one cell each.
+constexpr int kMoGroup = 8;
+
+__global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
+                                                 const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
+                                                 float* __restrict__ cov, const DevScalars* __restrict__ sc)
+{
+    const int lane = threadIdx.x & 31, gl = lane & (kMoGroup - 1);
+    const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
+    const uint32_t Lc = sc->Lc;
+    const float w_pred = sc->w_pred;
+    const uint32_t ng = (gridDim.x * blockDim.x) / kMoGroup;
+    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) / kMoGroup; li < Lc; li += ng) {
+        const uint32_t m = L.np[li];
+        if (m == 0) continue;
+        const uint32_t* pl = plist + L.ps[li];
+        double s5[5] = {0, 0, 0, 0, 0};
+        for (uint32_t q = gl; q < m; q += kMoGroup) {
+            const double* ps = ppart[pl[q]].s;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += ps[i];
+        }
+        if (m > 1) {
+#pragma unroll
+            for (int d = kMoGroup / 2; d; d >>= 1)
+#pragma unroll
+                for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(gmask, s5[i], d, kMoGroup);
+        }
+        if (gl == 0) finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
     }
 }
 
 // New-born particles (Alg. 5): work items of <= 256 birth slots of one cell; each warp takes a
 // contiguous range of items.  State from the slot's Philox draw; copies as for persistent members.
-__global__ __launch_bounds__(256) void k_births(CellList L, BlockTotals bt, uint32_t nblk, uint32_t chunk,
-                                                NextState out, BirthDebug bdbg, const DevScalars* __restrict__ sc,
-                                                FilterConst fc, int64_t k)
+__global__ __launch_bounds__(256) void k_births(CellList L, NextState out, BirthDebug bdbg,
+                                                const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu);
-    const uint32_t n_items = sc->n_items;
+    const uint32_t n_items = sc->n_items, Lc = sc->Lc;
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
     const uint32_t per = (n_items + nwarps - 1) / nwarps;
     uint32_t q = gw * per;
     const uint32_t q_end = min(q + per, n_items);
     if (q >= q_end) return;
-    uint32_t b = warp_last_le(0u, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
-    uint32_t lbase = b * chunk;
-    uint32_t li = warp_last_le(lbase, lbase + bt.cnt[b], q - bt.item0[b], [&](uint32_t i) { return L.it[i]; });
-    uint32_t sub = q - bt.item0[b] - L.it[li];
+    uint32_t li = warp_last_le(0u, Lc, q, [&](uint32_t i) { return L.it[i]; });
+    uint32_t sub = q - L.it[li];
     while (true) {
         const uint32_t c = L.c[li], n = L.n[li], start = L.start[li], nb = L.nb[li];
-        const uint64_t P = bt.P0[b] + L.Pl[li];
+        const uint64_t P = L.P[li];
         const uint32_t r0 = sub * kItem, m = min(kItem, nb - r0);
         const uint64_t bb = L.bb[li];
         const uint32_t rbm = L.rb[li], sb = L.sb[li];
@@ -430,12 +466,8 @@ __global__ __launch_bounds__(256) void k_births(CellList L, BlockTotals bt, uint
         if (++q >= q_end) break;
         if (++sub < (nb + kItem - 1) / kItem) continue;
         sub = 0;
-        const uint32_t chunk_end = b + 1 < nblk ? bt.item0[b + 1] : n_items;
-        if (q >= chunk_end) b = warp_last_le(b, nblk, q, [&](uint32_t i) { return bt.item0[i]; });
-        const uint32_t lo = q >= chunk_end ? b * chunk : li + 1;
-        lbase = b * chunk;
-        li = warp_last_le(lo, lbase + bt.cnt[b], q - bt.item0[b], [&](uint32_t i) { return L.it[i]; });
-        sub = q - bt.item0[b] - L.it[li];
+        li = warp_last_le(li + 1, Lc, q, [&](uint32_t i) { return L.it[i]; });
+        sub = q - L.it[li];
     }
 }
 

@@ -179,9 +179,8 @@ __global__ __launch_bounds__(kTsThreads) void k_tilesort(const uint32_t* __restr
 }
 
 // Each pair appends itself (tile << 12 | run) to its cell's list (unordered; k_pair_sort orders it).
-__global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, BlockTotals bt, uint32_t chunk,
-                                                   const uint32_t* __restrict__ cell2list, uint32_t* __restrict__ plist,
-                                                   uint32_t C)
+__global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, const uint32_t* __restrict__ cell2list,
+                                                   uint32_t* __restrict__ plist, uint32_t C)
 {
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const uint32_t nd = tp.nd[t];
@@ -190,61 +189,78 @@ __global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, Blo
         if (key >= C) continue;
         const uint32_t li = cell2list[key];
         const uint32_t slot = atomicAdd(&L.pfill[li], 1u);
-        plist[bt.ps0[li / chunk] + L.ps[li] + slot] = (t << 12) | r;
+        plist[L.ps[li] + slot] = (t << 12) | r;
     }
 }
 
-// Per active cell: sort its pair list by tile (warp-cooperative rank-by-count for any length; lists
-// are short), then the exclusive prefix of the run counts in that order -> pre of every run.
-__global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, BlockTotals bt, uint32_t chunk,
-                                                   uint32_t* __restrict__ plist, uint32_t* __restrict__ ptmp)
+// Per active cell: its pair list sorted by tile, then the exclusive prefix of the run counts in that
+// order -> pre of every run, and the run's resampling parameters (RunInfo).  Groups of 8 lanes take one
+// cell each (4 cells per warp, so neighbouring cells with long lists proceed in parallel); lists are
+// staged in shared memory and sorted by rank-by-count (entries are distinct, lists are short).
+constexpr int kPsGroup = 8, kPsBuf = 128;
+
+__global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
+                                                   uint32_t* __restrict__ ptmp, const DevScalars* __restrict__ sc)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t b = blockIdx.x;
-    const uint32_t cnt = bt.cnt[b], lbase = b * chunk;
-    for (uint32_t e = warp; e < cnt; e += blockDim.x >> 5) {
-        const uint32_t li = lbase + e;
+    __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
+    const int lane = threadIdx.x & 31, gl = lane & (kPsGroup - 1), grp = threadIdx.x / kPsGroup;
+    const uint32_t gmask = 0xFFu << (lane & ~(kPsGroup - 1));
+    const uint32_t Lc = sc->Lc;
+    const uint32_t ng = (gridDim.x * blockDim.x) / kPsGroup;
+    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) / kPsGroup; li < Lc; li += ng) {
         const uint32_t m = L.np[li];
         if (m == 0) continue;
-        uint32_t* pl = plist + bt.ps0[b] + L.ps[li];
         RunInfo ri;
-        ri.P = bt.P0[b] + L.Pl[li];
+        ri.P = L.P[li];
         ri.bp = L.bp[li];
         ri.rpm = L.rp[li];
+        ri.pre = 0u;
         ri.jbase = L.start[li] + L.sb[li];
         ri.li = li;
-        if (m == 1) {                                // (tile << 12 | run) is the run's slot index
-            if (lane == 0) { ri.pre = 0u; tp.run[pl[0]] = ri; }
+        uint32_t* pl = plist + L.ps[li];
+        if (m == 1) {                                 // (tile << 12 | run) is the run's slot index
+            if (gl == 0) tp.run[pl[0]] = ri;
             continue;
         }
-        uint32_t* tmp = ptmp + bt.ps0[b] + L.ps[li];
+        const bool sm = m <= (uint32_t)kPsBuf;
+        uint32_t* src = sm ? s_buf[grp][0] : pl;
+        uint32_t* tmp = sm ? s_buf[grp][1] : ptmp + L.ps[li];
+        const uint32_t mr = (m + kPsGroup - 1) / kPsGroup * kPsGroup;   // group-uniform trip counts
+        if (sm)
+            for (uint32_t a = gl; a < m; a += kPsGroup) src[a] = pl[a];
+        __syncwarp(gmask);
         // rank of each entry = number of smaller entries (entries are distinct)
-        for (uint32_t a = lane; a < m; a += 32) {
-            const uint32_t va = pl[a];
+        for (uint32_t a = gl; a < m; a += kPsGroup) {
+            const uint32_t va = src[a];
             uint32_t rank = 0;
-            for (uint32_t q = 0; q < m; ++q) rank += pl[q] < va ? 1u : 0u;
+            for (uint32_t q = 0; q < m; ++q) rank += src[q] < va ? 1u : 0u;
             tmp[rank] = va;
         }
-        __syncwarp();
+        __syncwarp(gmask);
         // exclusive prefix of counts in tile order
         uint32_t carry = 0;
-        for (uint32_t a0 = 0; a0 < m; a0 += 32) {
-            const uint32_t a = a0 + lane;
+        for (uint32_t a0 = 0; a0 < mr; a0 += kPsGroup) {
+            const uint32_t a = a0 + gl;
             uint32_t v = 0, c = 0;
             if (a < m) {
                 v = tmp[a];
                 c = (uint32_t)tp.cnt[v] + 1u;
             }
-            const uint32_t incl = warp_incl_scan(c, lane);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < kPsGroup; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(gmask, incl, d, kPsGroup);
+                if (gl >= d) incl += o;
+            }
             if (a < m) {
                 RunInfo r2 = ri;
                 r2.pre = carry + incl - c;
                 tp.run[v] = r2;
                 pl[a] = v;                   // the cell's list, now in tile order
             }
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+            carry += __shfl_sync(gmask, incl, kPsGroup - 1, kPsGroup);
         }
-        __syncwarp();
+        __syncwarp(gmask);
     }
 }
 

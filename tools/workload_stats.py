@@ -28,3 +28,7 @@ print(f"runs per 4096-tile: mean={runs.mean():.1f} median={np.median(runs):.0f} 
 print(f"total runs={runs.sum()} mean run length={cfg.nu / runs.sum():.1f}")
 s = f.scalars()
 print("W mass", s["W"] * 2.0 ** -40, "A", s["A"] * 2.0 ** -40)
+nb = f.debug("NB")
+Rb = f.debug("RB")
+print(f"cells with nb>0: {int(np.count_nonzero(nb))}  cells with Rb>0: {int(np.count_nonzero(Rb))}  "
+      f"active (n>0 or Rb>0): {int(np.count_nonzero((n > 0) | (Rb > 0)))}")
