@@ -41,8 +41,9 @@ struct dog_ctx {
     uint32_t tiles = 0, cell_blocks = 0, cell_chunk = 0, birth_blocks = 0;
 
     // state S_k and predicted state (SoA, f32)
-    float *x = nullptr, *y = nullptr, *vx = nullptr, *vy = nullptr;
-    float *px = nullptr, *py = nullptr, *pvx = nullptr, *pvy = nullptr;
+    float4* st = nullptr;                         // (x, y, vx, vy) per particle
+    float4* pst = nullptr;                        // predicted state, same layout
+    uint32_t* rD = nullptr;                       // k_resample_tiles per-run offsets beyond its smem
     // assignment (dog_sort.cuh)
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
@@ -220,7 +221,8 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
-    cudaFuncSetAttribute(k_resample_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
+    cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
+    cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     {   // persistent grids: as many blocks as fit on the GPU at once
         int per_sm = 0, sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -254,8 +256,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->x, N); AL(ctx->y, N); AL(ctx->vx, N); AL(ctx->vy, N);
-    AL(ctx->px, N); AL(ctx->py, N); AL(ctx->pvx, N); AL(ctx->pvy, N);
+    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rD, N);
     AL(ctx->keys, N); AL(ctx->lperm, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
@@ -289,12 +290,9 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->bt.done = ctx->ctrs;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
-    std::vector<float> sent(N, kSentinelPos);
+    std::vector<float4> sent(N, make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f));
     cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->x, sent.data(), N * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->y, sent.data(), N * 4, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(ctx->vx, 0, N * 4);
-    if (e == cudaSuccess) e = cudaMemset(ctx->vy, 0, N * 4);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->st, sent.data(), N * 16, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(ctx->m_free, 0, Cs * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->occ, 0, Cs * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->fre, 0, Cs * 4);
@@ -358,9 +356,7 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     const uint32_t T = ctx->tiles;
 
     // 1. predict (Alg. 1)
-    k_predict<<<T, kPredThreads, 0, st>>>(
-        (const float4*)ctx->x, (const float4*)ctx->y, (const float4*)ctx->vx, (const float4*)ctx->vy,
-        (float4*)ctx->px, (float4*)ctx->py, (float4*)ctx->pvx, (float4*)ctx->pvy, (uint4*)ctx->keys, ctx->sc, fc, a);
+    k_predict<<<T, kPredThreads, 0, st>>>(ctx->st, ctx->pst, ctx->keys, ctx->sc, fc, a);
     CK(cudaGetLastError());
     CK(mark("predict"));
 
@@ -399,10 +395,13 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     CK(mark("pairs"));
 
     // 6. persistent particles: moments + resampling copies; births
-    Pred pr{ctx->px, ctx->py, ctx->pvx, ctx->pvy};
-    NextState ns{ctx->x, ctx->y, ctx->vx, ctx->vy, dbg ? ctx->jidx : nullptr};
-    k_resample_tiles<<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, pr, ctx->list, ns,
-                                                          dbg ? ctx->perm : nullptr, ctx->ppart, ctx->sc, fc);
+    NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
+    if (dbg)
+        k_resample_tiles<true><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
+                                                                    ctx->perm, ctx->ppart, ctx->rD, ctx->sc, fc);
+    else
+        k_resample_tiles<false><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
+                                                                     nullptr, ctx->ppart, ctx->rD, ctx->sc, fc);
     CK(cudaGetLastError());
     k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
     CK(cudaGetLastError());
@@ -512,11 +511,9 @@ int dog_get_state(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float*
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaDeviceSynchronize());
-    const size_t n = (size_t)ctx->nu * 4;
-    if (x) CK(cudaMemcpy(x, ctx->x, n, cudaMemcpyDeviceToHost));
-    if (y) CK(cudaMemcpy(y, ctx->y, n, cudaMemcpyDeviceToHost));
-    if (vx) CK(cudaMemcpy(vx, ctx->vx, n, cudaMemcpyDeviceToHost));
-    if (vy) CK(cudaMemcpy(vy, ctx->vy, n, cudaMemcpyDeviceToHost));
+    float* comp[4] = {x, y, vx, vy};
+    for (int c = 0; c < 4; ++c)   // one component of the (x, y, vx, vy) records: strided copy
+        if (comp[c]) CK(cudaMemcpy2D(comp[c], 4, (const float*)ctx->st + c, 16, 4, (size_t)ctx->nu, cudaMemcpyDeviceToHost));
     if (m_free) CK(cudaMemcpy(m_free, ctx->m_free, (size_t)ctx->C * 4, cudaMemcpyDeviceToHost));
     if (w_bar) CK(cudaMemcpy(w_bar, &ctx->sc->w_bar, 4, cudaMemcpyDeviceToHost));
     if (k) *k = ctx->k;
@@ -531,11 +528,9 @@ int dog_set_state(dog_ctx* ctx, const float* x, const float* y, const float* vx,
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaDeviceSynchronize());
-    const size_t n = (size_t)ctx->nu * 4;
-    CK(cudaMemcpy(ctx->x, x, n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->y, y, n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->vx, vx, n, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->vy, vy, n, cudaMemcpyHostToDevice));
+    const float* comp[4] = {x, y, vx, vy};
+    for (int c = 0; c < 4; ++c)
+        CK(cudaMemcpy2D((float*)ctx->st + c, 16, comp[c], 4, 4, (size_t)ctx->nu, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->m_free, m_free, (size_t)ctx->C * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(&ctx->sc->w_bar, &w_bar, 4, cudaMemcpyHostToDevice));
     ctx->k = k;
@@ -569,10 +564,13 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
         return DOG_OK;
     };
     switch (what) {
-    case DOG_DBG_PRED_X: src = ctx->px; n = nu * 4; break;
-    case DOG_DBG_PRED_Y: src = ctx->py; n = nu * 4; break;
-    case DOG_DBG_PRED_VX: src = ctx->pvx; n = nu * 4; break;
-    case DOG_DBG_PRED_VY: src = ctx->pvy; n = nu * 4; break;
+    case DOG_DBG_PRED_X: case DOG_DBG_PRED_Y: case DOG_DBG_PRED_VX: case DOG_DBG_PRED_VY: {
+        n = nu * 4;
+        if (bytes < n) return DOG_E_INVAL;
+        const int c = what - DOG_DBG_PRED_X;
+        CK(cudaMemcpy2D(host_dst, 4, (const float*)ctx->pst + c, 16, 4, nu, cudaMemcpyDeviceToHost));
+        return (int64_t)n;
+    }
     case DOG_DBG_KEY: src = ctx->keys; n = nu * 4; break;
     case DOG_DBG_PERM: {   // cell-sorted slots [0, n_in) from the resample kernel; sentinels follow in input order
         if (!dbg) return DOG_E_STATE;

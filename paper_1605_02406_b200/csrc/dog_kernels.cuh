@@ -19,56 +19,41 @@ namespace dog {
 
 
 // ------------------------------------------------------------------------------------------------
-// Alg. 1 -- particle prediction.  One block advances one 4096-particle sort tile (each thread 4
-// consecutive particles per step, 16-byte SoA I/O) and writes the new cell keys.
+// Alg. 1 -- particle prediction.  One block advances one 4096-particle sort tile (state and predicted
+// state are (x, y, vx, vy) float4 per particle: one 16-byte load and store each) and writes the new
+// cell keys.
 // ------------------------------------------------------------------------------------------------
 constexpr int kPredThreads = 256;
-constexpr int kMaxPasses = 4;
 constexpr int kSortTile = 4096;     // particles per sort tile (= one k_predict block)
 
-__global__ __launch_bounds__(kPredThreads) void k_predict(
-    const float4* __restrict__ x, const float4* __restrict__ y, const float4* __restrict__ vx,
-    const float4* __restrict__ vy, float4* __restrict__ px, float4* __restrict__ py,
-    float4* __restrict__ pvx, float4* __restrict__ pvy, uint4* __restrict__ keys,
-    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
+__global__ __launch_bounds__(kPredThreads) void k_predict(const float4* __restrict__ st, float4* __restrict__ pst,
+                                                          uint32_t* __restrict__ keys, DevScalars* __restrict__ sc,
+                                                          FilterConst fc, StepArgs a)
 {
     const float w_bar = sc->w_bar;
     const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->w_pred = w_pred;
     const float Wf = (float)fc.W, Hf = (float)fc.H;
-    const uint32_t n4 = (fc.nu + 3u) >> 2;
-    const uint32_t g0 = blockIdx.x * (kSortTile / 4);
+    const uint32_t i0 = blockIdx.x * kSortTile;
 
-#pragma unroll 1
-    for (int it = 0; it < kSortTile / 4 / kPredThreads; ++it) {
-        const uint32_t g = g0 + it * kPredThreads + threadIdx.x;
-        if (g >= n4) break;
-        const float4 X = x[g], Y = y[g], VX = vx[g], VY = vy[g];
-        float xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w};
-        float vxs[4] = {VX.x, VX.y, VX.z, VX.w}, vys[4] = {VY.x, VY.y, VY.z, VY.w};
-        uint32_t ks[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint32_t i = g * 4u + e;
-            const Philox4 r = draw(fc.seed, i, a.k, STAGE_PREDICT);
-            float n0, n1, n2, n3;
-            box_muller(r.r0, r.r1, n0, n1);
-            box_muller(r.r2, r.r3, n2, n3);
-            // p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v
-            const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(vxs[e], a.Tc, xs[e]));
-            const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(vys[e], a.Tc, ys[e]));
-            vxs[e] = __fmaf_rn(a.s_v, n2, vxs[e]);
-            vys[e] = __fmaf_rn(a.s_v, n3, vys[e]);
-            xs[e] = xn; ys[e] = yn;
-            const bool inside = (xn >= 0.0f) && (xn < Wf) && (yn >= 0.0f) && (yn < Hf);
-            ks[e] = inside ? (uint32_t)__float2int_rz(yn) * (uint32_t)fc.W + (uint32_t)__float2int_rz(xn)
-                           : fc.C;                                  // A-4, A-5
-        }
-        px[g] = make_float4(xs[0], xs[1], xs[2], xs[3]);
-        py[g] = make_float4(ys[0], ys[1], ys[2], ys[3]);
-        pvx[g] = make_float4(vxs[0], vxs[1], vxs[2], vxs[3]);
-        pvy[g] = make_float4(vys[0], vys[1], vys[2], vys[3]);
-        keys[g] = make_uint4(ks[0], ks[1], ks[2], ks[3]);
+#pragma unroll 2
+    for (int it = 0; it < kSortTile / kPredThreads; ++it) {
+        const uint32_t i = i0 + it * kPredThreads + threadIdx.x;
+        if (i >= fc.nu) break;
+        const float4 S = st[i];
+        const Philox4 r = draw(fc.seed, i, a.k, STAGE_PREDICT);
+        float n0, n1, n2, n3;
+        box_muller(r.r0, r.r1, n0, n1);
+        box_muller(r.r2, r.r3, n2, n3);
+        // p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v
+        const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(S.z, a.Tc, S.x));
+        const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(S.w, a.Tc, S.y));
+        const float vxn = __fmaf_rn(a.s_v, n2, S.z);
+        const float vyn = __fmaf_rn(a.s_v, n3, S.w);
+        const bool inside = (xn >= 0.0f) && (xn < Wf) && (yn >= 0.0f) && (yn < Hf);
+        keys[i] = inside ? (uint32_t)__float2int_rz(yn) * (uint32_t)fc.W + (uint32_t)__float2int_rz(xn)
+                         : fc.C;                                    // A-4, A-5
+        pst[i] = make_float4(xn, yn, vxn, vyn);
     }
 }
 

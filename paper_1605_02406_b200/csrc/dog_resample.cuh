@@ -81,8 +81,7 @@ __device__ __forceinline__ void finalize_cell(uint32_t c, double s0, double s1, 
     cov[3 * (size_t)c + 2] = (float)(wd * s4 / rd - mx * my);
 }
 
-struct NextState { float *x, *y, *vx, *vy; uint32_t* jidx; };
-struct Pred { const float *x, *y, *vx, *vy; };
+struct NextState { float4* s; uint32_t* jidx; };   // (x, y, vx, vy) per particle; joint index (debug)
 struct BirthDebug { float *x, *y, *vx, *vy; };
 
 // Last index in [lo, hi) whose value v(idx) <= key, warp-cooperative 32-ary search; assumes
@@ -131,32 +130,34 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
         const float vx = __shfl_sync(0xffffffffu, VX, own), vy = __shfl_sync(0xffffffffu, VY, own);
         const uint32_t jj = __shfl_sync(0xffffffffu, J, own);
         if (o < hi) {
-            out.x[o] = x; out.y[o] = y; out.vx[o] = vx; out.vy[o] = vy;
+            out.s[o] = make_float4(x, y, vx, vy);
             if (out.jidx) out.jidx[o] = jj;
         }
     }
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
-constexpr int kRtRunCache = 128;                                      // runs whose RunInfo sits in smem
+constexpr int kRtRunCache = 64;                                       // runs whose RunInfo sits in smem
+constexpr int kRtRunSm = 2048;                                        // runs whose offset D sits in smem
 constexpr uint32_t kNoF = 0xFFFFFFFFu;                                // position outside the grid
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
+    uint16_t runof[kSortTile];         // sorted position -> run
     uint32_t F0[kSortTile];            // F(Q_r): first output of the member at each position
-    uint32_t rO[kSortTile + 4];        // run -> F(Q_end) (phase B), then its offset in the tile's compact
-                                       // output space (exclusive prefix of the runs' output counts)
+    uint32_t rD[kRtRunSm];             // per run: F(Q_end) (phase B), then F0(first) - compact offset
     alignas(16) RunInfo run[kRtRunCache];
     union alignas(16) {
         struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phases B, D
-        uint32_t osrc[kSortTile];      // phase C: compact output -> (run << 12 | position) + 1
+        uint32_t osrc[kSortTile];      // phase C: compact output -> owner position + 1
     } u;
     uint32_t scan[kRtThreads / 32 + 1];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
-static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, F0) % 16 == 0, "vector smem access");
+static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, F0) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0,
+              "vector smem access");
 
 // Block-wide exclusive max-scan of one value per thread (values >= 0).
 __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
@@ -178,16 +179,20 @@ __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
 }
 
 // Persistent particles, one block per sort tile (4096 particles in input order; lperm gives their
-// stable cell order).  Phase B: thread t owns the sorted positions [16t, 16t+16) -- batched gathers of
-// the predicted velocities, velocity sums per run segment, and F(Q_r) of every member (member r =
-// pre(run) + position within the run).  Phase D: run segments spanning threads are combined in thread
-// order (deterministic) -> per-run velocity sums.  Phase C: the members' output ranges, concatenated
-// over the tile's runs, form a compact output space; in windows of 4096 outputs each member with
-// copies marks its first output, a block max-scan spreads the owner over its outputs, and threads then
-// write consecutive outputs (coalesced, balanced whatever the copy counts).
+// stable cell order).
+//   phase B (thread t owns sorted positions [16t, 16t+16)): run of every position, batched gathers of
+//     the predicted velocities, velocity sums per run segment (runs inside a thread -> ppart directly).
+//   phase F (lanes = positions): F(Q_r) of every member (member r = pre(run) + position in the run).
+//   phase D: run segments spanning threads combined in thread order (deterministic) -> ppart.
+//   phase C: the members' output ranges, concatenated over the tile's runs, form a compact output
+//     space; in windows of 4096 outputs each member with copies marks its first output, a block
+//     max-scan spreads the owner over its outputs, and threads write consecutive outputs (coalesced,
+//     balanced whatever the copy counts).
+template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
-    const uint16_t* __restrict__ lperm, TilePairs tp, Pred pr, CellList L, NextState out,
-    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
+    const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
+    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, uint32_t* __restrict__ rD_g,
+    const DevScalars* __restrict__ sc, FilterConst fc)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
@@ -196,8 +201,8 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x) {
-            out.x[i] = kSentinelPos; out.y[i] = kSentinelPos; out.vx[i] = 0.0f; out.vy[i] = 0.0f;
-            if (out.jidx) out.jidx[i] = 0xFFFFFFFFu;
+            out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
+            if (kDbg) out.jidx[i] = 0xFFFFFFFFu;
         }
     }
     const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
@@ -219,64 +224,79 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     __syncthreads();
     const uint32_t srun = S.sentinel_run;
     auto run_info = [&](uint32_t j) -> RunInfo { return j < (uint32_t)kRtRunCache ? S.run[j] : tp.run[base + j]; };
+    auto rD_ld = [&](uint32_t j) -> uint32_t { return j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j]; };
+    auto rD_st = [&](uint32_t j, uint32_t v) { if (j < (uint32_t)kRtRunSm) S.rD[j] = v; else rD_g[base + j] = v; };
+    const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
 
-    // ---- phase B: velocity gathers, velocity sums, F(Q_r) per member
-    const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
-    uint32_t j0 = 0;                                        // run containing p0
+    // ---- phase B: run of every position, velocity sums per run segment
     if (p0 < n) {
-        uint32_t lo = 0, hi = nd;
+        uint32_t lo = 0, hi = nd;                           // run containing p0
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= p0) lo = m; else hi = m; }
-        j0 = lo;
         uint32_t j = lo, first = S.first[j], end = S.first[j + 1];
-        RunInfo q = run_info(j);
         double acc[5] = {0, 0, 0, 0, 0};
         bool first_seg = true;
-        uint32_t Fcarry = kNoF;                             // F(Q_r) of the next member, same run
         auto flush = [&]() {
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
             if (j != srun) {
-                if (first >= p0 && end <= pend) ppart[base + j] = mp;    // run inside this thread
+                if (first >= p0 && end <= p0 + kRtItems) ppart[base + j] = mp;    // run inside this thread
                 else if (first_seg) S.u.m.pa[tid] = mp;
                 else S.u.m.pb[tid] = mp;
             }
             first_seg = false;
         };
 #pragma unroll 1
-        for (uint32_t b0 = p0; b0 < pend; b0 += 8) {
-            float VX[8], VY[8];
-            uint32_t src[8];
+        for (int h = 0; h < 2; ++h) {                       // two batches of 8 positions
+            uint32_t src[8], rpk[4];
+            {
+                const uint4 a = reinterpret_cast<const uint4*>(S.lp + p0)[h];
+                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-            for (int u = 0; u < 8; ++u) src[u] = base + S.lp[min(b0 + u, pend - 1)];
+                for (int u = 0; u < 4; ++u) { src[2 * u] = base + (w[u] & 0xFFFFu); src[2 * u + 1] = base + (w[u] >> 16); }
+            }
+            float2 V[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) { VX[u] = pr.vx[src[u]]; VY[u] = pr.vy[src[u]]; }
+            for (int u = 0; u < 8; ++u)
+                V[u] = (p0 + 8 * h + u < n) ? pv[2 * (size_t)src[u] + 1] : make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const uint32_t p = b0 + u;
-                if (p >= pend) break;
-                if (p >= end) {                             // next run
-                    flush();
-                    ++j; first = end; end = S.first[j + 1];
-                    q = run_info(j);
-                    Fcarry = kNoF;
+                const uint32_t p = p0 + 8 * h + u;
+                if (p < n) {
+                    if (p >= end) {                         // next run
+                        flush();
+                        ++j; first = end; end = S.first[j + 1];
+                    }
+                    if (j != srun) {
+                        const double a = (double)V[u].x, bq = (double)V[u].y;
+                        acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
+                        if (kDbg) {
+                            const RunInfo q = run_info(j);
+                            perm_dbg[q.jbase - L.sb[q.li] + q.pre + (p - first)] = src[u];
+                        }
+                    }
                 }
-                if (j == srun) { S.F0[p] = kNoF; continue; }
-                const double a = (double)VX[u], bq = (double)VY[u];
-                acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                const uint32_t mr = q.pre + (p - first);    // member rank within the cell
-                if (perm_dbg) perm_dbg[q.jbase - L.sb[q.li] + mr] = src[u];
-                const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-                const uint32_t F0 = Fcarry != kNoF ? Fcarry : fcount(Q0, rc);
-                const uint32_t F1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
-                S.F0[p] = F0;
-                if (p + 1 == end) S.rO[j] = F1;            // F(Q_end) of the run
-                Fcarry = F1;
+                if (u & 1) rpk[u >> 1] |= j << 16; else rpk[u >> 1] = j;
             }
+            reinterpret_cast<uint4*>(S.runof + p0)[h] = make_uint4(rpk[0], rpk[1], rpk[2], rpk[3]);
         }
         flush();
     }
     __syncthreads();
+    // ---- phase F: F(Q_r) per member (lanes = consecutive positions); F(Q_end) per run
+#pragma unroll 4
+    for (int it = 0; it < kRtItems; ++it) {
+        const uint32_t p = it * kRtThreads + tid;
+        if (p >= n) break;
+        const uint32_t j = S.runof[p];
+        if (j == srun) { S.F0[p] = kNoF; continue; }
+        const RunInfo q = run_info(j);
+        const uint32_t f = S.first[j], e = S.first[j + 1];
+        const uint32_t mr = q.pre + (p - f);
+        const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+        S.F0[p] = rc.W ? fcount(Q0, rc) : 0u;
+        if (p + 1 == e) rD_st(j, rc.W ? fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc) : 0u);
+    }
     // ---- phase D: run segments spanning threads (one warp per run, fixed summation order)
     for (uint32_t r = warp; r < nd; r += kRtThreads / 32) {
         if (r == srun) continue;
@@ -298,38 +318,43 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
             ppart[base + r] = mp;
         }
     }
+    __syncthreads();
     if (rc.W == 0) return;
-    // ---- compact output space: exclusive prefix over runs of F(Q_end) - F(Q_first)
+    // ---- compact output space: D(j) = F0(first_j) - exclusive prefix over runs of F(Q_end) - F(Q_first)
     uint32_t carry = 0;
     for (uint32_t r0 = 0; r0 < nd; r0 += kRtThreads) {
         const uint32_t r = r0 + tid;
-        const uint32_t c = (r < nd && r != srun) ? S.rO[r] - S.F0[S.first[r]] : 0u;
+        const bool live = r < nd && r != srun;
+        const uint32_t fF = live ? S.F0[S.first[r]] : 0u;
+        const uint32_t c = live ? rD_ld(r) - fF : 0u;
         uint32_t tot;
         const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
-        if (r < nd) S.rO[r] = carry + ex;
+        if (live) rD_st(r, fF - (carry + ex));
         carry += tot;
     }
-    if (tid == 0) S.rO[nd] = carry;
     __syncthreads();
     const uint32_t Ot = carry;
+    // compact end of run j = compact start of run j+1 (or the total)
+    auto cend = [&](uint32_t j) -> uint32_t {
+        const uint32_t k2 = j + 1;
+        return (k2 < nd && k2 != srun) ? S.F0[S.first[k2]] - rD_ld(k2) : Ot;
+    };
     // ---- phase C: windows of the compact output space
     for (uint32_t w0 = 0; w0 < Ot; w0 += kSortTile) {
         uint32_t* os = S.u.osrc;
-        reinterpret_cast<uint4*>(os + p0)[0] = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4*>(os + p0)[1] = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4*>(os + p0)[2] = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4*>(os + p0)[3] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int i = 0; i < kRtItems / 4; ++i) reinterpret_cast<uint4*>(os + p0)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
-        if (p0 < n) {   // members with copies mark the first of their outputs inside the window
-            uint32_t j = j0, first = S.first[j], end = S.first[j + 1];
-            uint32_t D = j == srun ? 0u : S.F0[first] - S.rO[j];
-            for (uint32_t p = p0; p < pend; ++p) {
-                if (p >= end) { ++j; first = end; end = S.first[j + 1]; D = j == srun ? 0u : S.F0[first] - S.rO[j]; }
-                if (j == srun) break;                       // the sentinel run is the tile's last
-                const uint32_t C0 = S.F0[p] - D;
-                const uint32_t C1 = p + 1 < end ? S.F0[p + 1] - D : S.rO[j + 1];
-                if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = ((j << 12) | p) + 1u;
-            }
+#pragma unroll 4
+        for (int it = 0; it < kRtItems; ++it) {   // members with copies mark their first output in the window
+            const uint32_t p = it * kRtThreads + tid;
+            if (p >= n) break;
+            const uint32_t j = S.runof[p];
+            if (j == srun) continue;
+            const uint32_t D = rD_ld(j);
+            const uint32_t C0 = S.F0[p] - D;
+            const uint32_t C1 = p + 1 < S.first[j + 1] ? S.F0[p + 1] - D : cend(j);
+            if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = p + 1u;
         }
         __syncthreads();
         {   // inclusive max-scan over the window: thread-contiguous 16 entries
@@ -357,21 +382,21 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
             for (int h = 0; h < 4; ++h) {
                 const uint32_t i = i0 + h * kRtThreads + tid;
                 ok[h] = i < wn;
-                const uint32_t v = os[ok[h] ? i : 0u] - 1u;
-                const uint32_t j = v >> 12, p = v & 4095u;
-                o[h] = w0 + i + S.F0[S.first[j]] - S.rO[j];
+                const uint32_t p = os[ok[h] ? i : 0u] - 1u;
+                const uint32_t j = S.runof[p];
+                o[h] = w0 + i + rD_ld(j);
                 src[h] = base + S.lp[p];
                 J[h] = 0;
-                if (out.jidx) { const RunInfo q = run_info(j); J[h] = q.jbase + q.pre + (p - S.first[j]); }
+                if (kDbg) { const RunInfo q = run_info(j); J[h] = q.jbase + q.pre + (p - S.first[j]); }
             }
-            float X[4], Y[4], VX[4], VY[4];
+            float4 X[4];
 #pragma unroll
-            for (int h = 0; h < 4; ++h) { X[h] = pr.x[src[h]]; Y[h] = pr.y[src[h]]; VX[h] = pr.vx[src[h]]; VY[h] = pr.vy[src[h]]; }
+            for (int h = 0; h < 4; ++h) X[h] = pred[src[h]];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
                 if (!ok[h]) continue;
-                out.x[o[h]] = X[h]; out.y[o[h]] = Y[h]; out.vx[o[h]] = VX[h]; out.vy[o[h]] = VY[h];
-                if (out.jidx) out.jidx[o[h]] = J[h];
+                out.s[o[h]] = X[h];
+                if (kDbg) out.jidx[o[h]] = J[h];
             }
         }
         __syncthreads();

@@ -17,7 +17,7 @@ def main(path, kernel, top=25):
             hdr = r
             continue
         if len(r) == 2:
-            fname = r[1].split('/')[-1]
+            fname = r[1].split('/')[-1][:24]
             continue
         if hdr is None or len(r) < 5 or not r[0].isdigit():
             continue
