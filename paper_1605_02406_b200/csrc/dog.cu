@@ -43,7 +43,6 @@ struct dog_ctx {
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
     float4* pst = nullptr;                        // predicted state, same layout
-    uint32_t* rD = nullptr;                       // k_resample_tiles per-run offsets beyond its smem
     // assignment (dog_sort.cuh)
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
@@ -256,7 +255,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rD, N);
+    AL(ctx->st, N); AL(ctx->pst, N);
     AL(ctx->keys, N); AL(ctx->lperm, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
@@ -398,10 +397,10 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     if (dbg)
         k_resample_tiles<true><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                    ctx->perm, ctx->ppart, ctx->rD, ctx->sc, fc);
+                                                                    ctx->perm, ctx->ppart, ctx->sc, fc);
     else
         k_resample_tiles<false><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                     nullptr, ctx->ppart, ctx->rD, ctx->sc, fc);
+                                                                     nullptr, ctx->ppart, ctx->sc, fc);
     CK(cudaGetLastError());
     k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
     CK(cudaGetLastError());

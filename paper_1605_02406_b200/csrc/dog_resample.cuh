@@ -137,27 +137,21 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
-constexpr int kRtRunCache = 64;                                       // runs whose RunInfo sits in smem
-constexpr int kRtRunSm = 2048;                                        // runs whose offset D sits in smem
-constexpr uint32_t kNoF = 0xFFFFFFFFu;                                // position outside the grid
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
     uint16_t runof[kSortTile];         // sorted position -> run
-    uint32_t F0[kSortTile];            // F(Q_r): first output of the member at each position
-    uint32_t rD[kRtRunSm];             // per run: F(Q_end) (phase B), then F0(first) - compact offset
-    alignas(16) RunInfo run[kRtRunCache];
+    uint32_t rD[kSortTile];            // per run: F(Q_first) - offset of the run in the compact output space
     union alignas(16) {
-        struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phases B, D
+        struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phase B -> phase R
         uint32_t osrc[kSortTile];      // phase C: compact output -> owner position + 1
     } u;
     uint32_t scan[kRtThreads / 32 + 1];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
-static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, F0) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0,
-              "vector smem access");
+static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0, "vector smem access");
 
 // Block-wide exclusive max-scan of one value per thread (values >= 0).
 __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
@@ -178,25 +172,31 @@ __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
     return max(pre, lane ? ex : 0u);
 }
 
+// Q of member mr of a run's cell: P + mr bp + min(mr, rpm) (even split of the cell's R_p, A-23).
+__device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
+{
+    return q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+}
+
 // Persistent particles, one block per sort tile (4096 particles in input order; lperm gives their
 // stable cell order).
 //   phase B (thread t owns sorted positions [16t, 16t+16)): run of every position, batched gathers of
 //     the predicted velocities, velocity sums per run segment (runs inside a thread -> ppart directly).
-//   phase F (lanes = positions): F(Q_r) of every member (member r = pre(run) + position in the run).
-//   phase D: run segments spanning threads combined in thread order (deterministic) -> ppart.
-//   phase C: the members' output ranges, concatenated over the tile's runs, form a compact output
-//     space; in windows of 4096 outputs each member with copies marks its first output, a block
-//     max-scan spreads the owner over its outputs, and threads write consecutive outputs (coalesced,
+//   phase R (thread per run): run segments spanning threads combined in thread order (deterministic)
+//     -> ppart; the run's output range [F(Q_first), F(Q_end)) and its offset in the tile's compact
+//     output space (the runs' ranges concatenated).
+//   phase C, per window of 4096 compact outputs: lanes take consecutive positions, compute F(Q_r) of
+//     their member (the next member's from the neighbour lane) and mark the member's first output; a
+//     block max-scan spreads the owner over its outputs; threads write consecutive outputs (coalesced,
 //     balanced whatever the copy counts).
 template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
-    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, uint32_t* __restrict__ rD_g,
-    const DevScalars* __restrict__ sc, FilterConst fc)
+    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu);
     if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
@@ -209,23 +209,20 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const uint32_t p0 = tid * kRtItems;
-    // ---- phase A: local permutation, run starts, run parameters (one round trip)
+    const RunInfo* __restrict__ runs = tp.run + base;
+    // ---- phase A: local permutation, run starts (one round trip)
     {
         uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
         if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }
         if (p0 < nd) { const uint4* f4 = reinterpret_cast<const uint4*>(tp.first + base + p0); c = f4[0]; d = f4[1]; }
         if (p0 < n) { reinterpret_cast<uint4*>(S.lp + p0)[0] = a; reinterpret_cast<uint4*>(S.lp + p0)[1] = b; }
         if (p0 < nd) { reinterpret_cast<uint4*>(S.first + p0)[0] = c; reinterpret_cast<uint4*>(S.first + p0)[1] = d; }
-        if ((uint32_t)tid < nd && tid < kRtRunCache) S.run[tid] = tp.run[base + tid];
         if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
     __syncthreads();
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
     const uint32_t srun = S.sentinel_run;
-    auto run_info = [&](uint32_t j) -> RunInfo { return j < (uint32_t)kRtRunCache ? S.run[j] : tp.run[base + j]; };
-    auto rD_ld = [&](uint32_t j) -> uint32_t { return j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j]; };
-    auto rD_st = [&](uint32_t j, uint32_t v) { if (j < (uint32_t)kRtRunSm) S.rD[j] = v; else rD_g[base + j] = v; };
     const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
 
     // ---- phase B: run of every position, velocity sums per run segment
@@ -271,7 +268,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                         const double a = (double)V[u].x, bq = (double)V[u].y;
                         acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
                         if (kDbg) {
-                            const RunInfo q = run_info(j);
+                            const RunInfo q = runs[j];
                             perm_dbg[q.jbase - L.sb[q.li] + q.pre + (p - first)] = src[u];
                         }
                     }
@@ -283,78 +280,70 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
         flush();
     }
     __syncthreads();
-    // ---- phase F: F(Q_r) per member (lanes = consecutive positions); F(Q_end) per run
-#pragma unroll 4
-    for (int it = 0; it < kRtItems; ++it) {
-        const uint32_t p = it * kRtThreads + tid;
-        if (p >= n) break;
-        const uint32_t j = S.runof[p];
-        if (j == srun) { S.F0[p] = kNoF; continue; }
-        const RunInfo q = run_info(j);
-        const uint32_t f = S.first[j], e = S.first[j + 1];
-        const uint32_t mr = q.pre + (p - f);
-        const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-        S.F0[p] = rc.W ? fcount(Q0, rc) : 0u;
-        if (p + 1 == e) rD_st(j, rc.W ? fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc) : 0u);
-    }
-    // ---- phase D: run segments spanning threads (one warp per run, fixed summation order)
-    for (uint32_t r = warp; r < nd; r += kRtThreads / 32) {
-        if (r == srun) continue;
-        const uint32_t f = S.first[r], e = S.first[r + 1];
-        const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
-        if (tf == tl) continue;                             // written directly in phase B
-        double s5[5] = {0, 0, 0, 0, 0};
-        for (uint32_t u = tf + lane; u <= tl; u += 32) {
-            const MomPartial& mp = (u == tf) ? ((f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf]) : S.u.m.pa[u];
-#pragma unroll
-            for (int i = 0; i < 5; ++i) s5[i] += mp.s[i];
-        }
-#pragma unroll
-        for (int i = 0; i < 5; ++i) s5[i] = warp_sum(s5[i]);
-        if (lane == 0) {
-            MomPartial mp;
-#pragma unroll
-            for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
-            ppart[base + r] = mp;
-        }
-    }
-    __syncthreads();
-    if (rc.W == 0) return;
-    // ---- compact output space: D(j) = F0(first_j) - exclusive prefix over runs of F(Q_end) - F(Q_first)
+    // ---- phase R: spanning run segments -> ppart; output range and compact offset of every run
     uint32_t carry = 0;
     for (uint32_t r0 = 0; r0 < nd; r0 += kRtThreads) {
         const uint32_t r = r0 + tid;
         const bool live = r < nd && r != srun;
-        const uint32_t fF = live ? S.F0[S.first[r]] : 0u;
-        const uint32_t c = live ? rD_ld(r) - fF : 0u;
+        uint32_t Flo = 0, c = 0;
+        if (live) {
+            const uint32_t f = S.first[r], e = S.first[r + 1];
+            const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
+            if (tf != tl) {                                 // segments over threads tf..tl, in thread order
+                const MomPartial& m0 = (f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf];
+                double s5[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) s5[i] = m0.s[i];
+                for (uint32_t u = tf + 1; u <= tl; ++u)
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) s5[i] += S.u.m.pa[u].s[i];
+                MomPartial mp;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+                ppart[base + r] = mp;
+            }
+            if (rc.W) {
+                const RunInfo q = runs[r];
+                Flo = fcount(member_Q(q, q.pre), rc);
+                c = fcount(member_Q(q, q.pre + (e - f)), rc) - Flo;
+            }
+        }
         uint32_t tot;
         const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
-        if (live) rD_st(r, fF - (carry + ex));
+        if (r < nd) S.rD[r] = Flo - (carry + ex);
         carry += tot;
     }
     __syncthreads();
     const uint32_t Ot = carry;
-    // compact end of run j = compact start of run j+1 (or the total)
-    auto cend = [&](uint32_t j) -> uint32_t {
-        const uint32_t k2 = j + 1;
-        return (k2 < nd && k2 != srun) ? S.F0[S.first[k2]] - rD_ld(k2) : Ot;
-    };
     // ---- phase C: windows of the compact output space
     for (uint32_t w0 = 0; w0 < Ot; w0 += kSortTile) {
         uint32_t* os = S.u.osrc;
 #pragma unroll
         for (int i = 0; i < kRtItems / 4; ++i) reinterpret_cast<uint4*>(os + p0)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
         for (int it = 0; it < kRtItems; ++it) {   // members with copies mark their first output in the window
             const uint32_t p = it * kRtThreads + tid;
-            if (p >= n) break;
-            const uint32_t j = S.runof[p];
-            if (j == srun) continue;
-            const uint32_t D = rD_ld(j);
-            const uint32_t C0 = S.F0[p] - D;
-            const uint32_t C1 = p + 1 < S.first[j + 1] ? S.F0[p + 1] - D : cend(j);
-            if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = p + 1u;
+            const bool inb = p < n;
+            const uint32_t j = inb ? S.runof[p] : srun;
+            const bool live = inb && j != srun;
+            uint32_t F0 = 0, e = 0;
+            uint64_t Q1 = 0;
+            if (live) {
+                const RunInfo q = runs[j];
+                e = S.first[j + 1];
+                const uint32_t mr = q.pre + (p - S.first[j]);
+                const uint64_t Q0 = member_Q(q, mr);
+                Q1 = Q0 + q.bp + (mr < q.rpm ? 1u : 0u);
+                F0 = fcount(Q0, rc);
+            }
+            const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);   // the next position's F(Q)
+            if (live) {
+                const uint32_t F1 = (lane < 31 && p + 1 < e) ? Fn : fcount(Q1, rc);
+                const uint32_t D = S.rD[j];
+                const uint32_t C0 = F0 - D, C1 = F1 - D;
+                if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = p + 1u;
+            }
         }
         __syncthreads();
         {   // inclusive max-scan over the window: thread-contiguous 16 entries
@@ -384,10 +373,10 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 ok[h] = i < wn;
                 const uint32_t p = os[ok[h] ? i : 0u] - 1u;
                 const uint32_t j = S.runof[p];
-                o[h] = w0 + i + rD_ld(j);
+                o[h] = w0 + i + S.rD[j];
                 src[h] = base + S.lp[p];
                 J[h] = 0;
-                if (kDbg) { const RunInfo q = run_info(j); J[h] = q.jbase + q.pre + (p - S.first[j]); }
+                if (kDbg) { const RunInfo q = runs[j]; J[h] = q.jbase + q.pre + (p - S.first[j]); }
             }
             float4 X[4];
 #pragma unroll
