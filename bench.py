@@ -36,19 +36,20 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# algorithmic bytes per launch of each stage
+# Algorithmic bytes per launch of each stage: the kernel's share of SURVEY.md 8(d)'s
+# A_alg = 64 nu + 32 nu_b + 56 C.  Transient arrays of this design (keys, local
+# permutations, run lists) are not algorithmic and count zero.
 def stage_bytes(stage: str, cfg, n_in: int) -> float:
     nu, nb, C = cfg.nu, cfg.nu_b, cfg.C
     table = {
-        "predict": 36.0 * nu,                       # state in 16, predicted state out 16, key 4
-        "sort_pass0": 12.0 * nu,                    # key in 4, (key, index) out 8
-        "sort_pass1": 16.0 * nu,
-        "sort_pass2": 16.0 * nu,
-        "sort_pass3": 16.0 * nu,
-        "cells": 28.0 * C,                          # counts 4, m_F 4, meas 8 in; occ 4, free 4, m_F 4 out
+        "predict": 32.0 * nu,        # read the state (16) + write the predicted state (16)
+        "tilesort": 0.0,             # keys / local permutation: transient
+        "cells": 28.0 * C,           # meas 8 + m_F read/write 8 + occ/free 8 + counts 4
         "list_scan": 0.0,
-        "resample": 40.0 * n_in + 16.0 * nb,        # sorted key 4, perm 4, gathered state 16, next state 16
-        "moments_fixup": 0.0,
+        "pairs": 0.0,
+        "resample": 32.0 * n_in,     # read the cell-ordered predicted state (16) + write the resampled state (16)
+        "moments": 0.0,              # 20 B per active cell (~1 % of C): negligible
+        "births": 16.0 * nb,         # write the new-born states
     }
     return table.get(stage, 0.0)
 

@@ -402,9 +402,10 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         k_resample_tiles<false><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
                                                                      nullptr, ctx->ppart, ctx->sc, fc);
     CK(cudaGetLastError());
+    CK(mark("resample"));
     k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
     CK(cudaGetLastError());
-    CK(mark("resample"));
+    CK(mark("moments"));
     if (ctx->nu_b > 0) {
         BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
         k_births<<<ctx->birth_blocks, 256, 0, st>>>(ctx->list, ns, bd, ctx->sc, fc, a.k);
