@@ -42,8 +42,7 @@ def peaks():
 def stage_bytes(stage: str, cfg, n_in: int) -> float:
     nu, nb, C = cfg.nu, cfg.nu_b, cfg.C
     table = {
-        "predict": 32.0 * nu,        # read the state (16) + write the predicted state (16)
-        "tilesort": 0.0,             # keys / local permutation: transient
+        "predict_sort": 32.0 * nu,   # read the state (16) + write the predicted state (16); keys stay on chip
         "cells": 28.0 * C,           # meas 8 + m_F read/write 8 + occ/free 8 + counts 4
         "list_scan": 0.0,
         "pairs": 0.0,

@@ -220,6 +220,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
+    cudaFuncSetAttribute(k_predict_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     {   // persistent grids: as many blocks as fit on the GPU at once
@@ -256,12 +257,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
     AL(ctx->st, N); AL(ctx->pst, N);
-    AL(ctx->keys, N); AL(ctx->lperm, N);
+    AL(ctx->lperm, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
     AL(ctx->counts, Cs + 1); AL(ctx->npairs, Cs + 1);
     if (dbg) {
-        AL(ctx->perm, N); AL(ctx->jidx, N);
+        AL(ctx->keys, N); AL(ctx->perm, N); AL(ctx->jidx, N);
         AL(ctx->dbg_rho_p, Cs); AL(ctx->dbg_rho_b, Cs); AL(ctx->dbg_Rp, Cs); AL(ctx->dbg_Rb, Cs);
         AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
     }
@@ -327,8 +328,8 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
-    // predict, tilesort, cells, list_scan, pair_fill, pair_sort, resample_tiles, moments, births
-    return ctx->nu_b > 0 ? 9 : 8;
+    // predict_sort, cells, list_scan, pair_fill, pair_sort, resample_tiles, moments, births
+    return ctx->nu_b > 0 ? 8 : 7;
 }
 
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
@@ -341,7 +342,6 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     const StepArgs a = step_args(ctx, dt);
     const FilterConst fc = filter_const(ctx);
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
-    const uint32_t nu = (uint32_t)ctx->nu;
 
     const bool prof = ctx->prof_steps < ctx->prof_max;
     int mark_i = 0;
@@ -354,15 +354,11 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     CK(cudaMemsetAsync(ctx->ctrs, 0, 16 * sizeof(uint32_t), st));
     const uint32_t T = ctx->tiles;
 
-    // 1. predict (Alg. 1)
-    k_predict<<<T, kPredThreads, 0, st>>>(ctx->st, ctx->pst, ctx->keys, ctx->sc, fc, a);
+    // 1-2. predict (Alg. 1) fused with the tile-local stable sort (Alg. 2): runs, per-cell counts
+    k_predict_sort<<<T, kPsThreads, kPsSmemBytes, st>>>(ctx->st, ctx->pst, dbg ? ctx->keys : nullptr, ctx->lperm,
+                                                        ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a);
     CK(cudaGetLastError());
-    CK(mark("predict"));
-
-    // 2. assignment (Alg. 2): tile-local stable sort, runs, per-cell counts
-    k_tilesort<<<T, kTsThreads, 0, st>>>(ctx->keys, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, nu, ctx->C);
-    CK(cudaGetLastError());
-    CK(mark("tilesort"));
+    CK(mark("predict_sort"));
 
     // 3. cells: DS predict/update, birth split, fixed point, active-cell list (Alg. 3)
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
@@ -571,7 +567,7 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
         CK(cudaMemcpy2D(host_dst, 4, (const float*)ctx->pst + c, 16, 4, nu, cudaMemcpyDeviceToHost));
         return (int64_t)n;
     }
-    case DOG_DBG_KEY: src = ctx->keys; n = nu * 4; break;
+    case DOG_DBG_KEY: if (!dbg) return DOG_E_STATE; src = ctx->keys; n = nu * 4; break;
     case DOG_DBG_PERM: {   // cell-sorted slots [0, n_in) from the resample kernel; sentinels follow in input order
         if (!dbg) return DOG_E_STATE;
         n = nu * 4;

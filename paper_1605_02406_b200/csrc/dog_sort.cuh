@@ -19,11 +19,9 @@
 #include "dog_cells.cuh"
 #include "dog_common.cuh"
 #include "dog_kernels.cuh"
+#include "dog_rng.cuh"
 
 namespace dog {
-
-constexpr int kTsThreads = 256, kTsItems = 16, kTsWarps = 8;
-static_assert(kTsThreads * kTsItems == kSortTile, "sort tile");
 
 // What k_resample_tiles needs of a run (written by k_pair_sort, one coalesced 32-byte load per run).
 struct RunInfo {
@@ -43,139 +41,168 @@ struct TilePairs {          // per tile t: entries [t*4096, t*4096 + nd[t])
     uint32_t* nd;           // [tiles] runs of the tile
 };
 
-// Stable LSD radix pass over the tile in shared memory: warps own consecutive 512-element slices of
-// the current order and rank by 8-bit digit with match_any + running per-warp counters.
-__device__ __forceinline__ void tile_radix_pass(uint32_t* s_k, uint16_t* s_i, uint32_t (*s_whist)[256],
-                                                uint32_t* s_scan, uint32_t kmin, int shift, uint32_t n)
+// ------------------------------------------------------------------------------------------------
+// Alg. 1 + the tile-local part of Alg. 2, fused: one block per 4096-particle tile predicts its particles
+// (one Philox4x32-10 draw and two Box-Muller pairs each, A-1/A-2/A-20), keeps their cell keys in
+// shared memory, sorts them stably (LSD radix over the bits of key - kmin the tile needs; 8-bit
+// digits; ranks from match_any + per-warp running counters, so equal keys keep input order), and
+// emits the runs of equal keys, the local permutation and per-cell counts.  Keys never touch HBM
+// (debug builds write them for the KEY dump).
+// ------------------------------------------------------------------------------------------------
+constexpr int kPsThreads = 256, kPsWarps = kPsThreads / 32, kPsRows = kSortTile / kPsThreads;   // 16
+
+struct PsSmem {
+    uint32_t k[2][kSortTile];          // keys, ping-pong
+    uint16_t v[2][kSortTile];          // local input index, ping-pong
+    uint16_t rank[kSortTile];          // rank of each element among its warp's equal digits
+    uint32_t hist[kPsWarps][256];      // per-warp digit counters -> scatter offsets
+    uint32_t scan[kPsWarps + 1];
+    uint32_t mn[kPsWarps], mx[kPsWarps];
+};
+constexpr size_t kPsSmemBytes = sizeof(PsSmem);
+
+// Warp w owns positions [512 w, 512 w + 512) as 16 rows of 32 lanes (position = 512 w + 32 i + lane).
+__global__ __launch_bounds__(kPsThreads) void k_predict_sort(
+    const float4* __restrict__ st, float4* __restrict__ pst, uint32_t* __restrict__ keys_dbg,
+    uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs,
+    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
 {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    PsSmem& S = *reinterpret_cast<PsSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    for (int i = tid; i < kTsWarps * 256; i += kTsThreads) (&s_whist[0][0])[i] = 0;
-    uint32_t k[kTsItems], rk[kTsItems];
-    uint16_t v[kTsItems];
-#pragma unroll
-    for (int i = 0; i < kTsItems; ++i) {
-        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
-        k[i] = s_k[p];
-        v[i] = s_i[p];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kTsItems; ++i) {
-        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
-        const bool ok = p < n;
-        const uint32_t dig = ok ? (((k[i] - kmin) >> shift) & 255u) : 0x100u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dig);
-        const uint32_t r = __popc(peers & lt);
-        uint32_t prev = 0;
-        if (ok) prev = s_whist[warp][dig];
-        __syncwarp();
-        if (ok && r == 0) s_whist[warp][dig] = prev + __popc(peers);
-        __syncwarp();
-        rk[i] = prev + r;
-    }
-    __syncthreads();
-    uint32_t run = 0;
-#pragma unroll
-    for (int w = 0; w < kTsWarps; ++w) {
-        const uint32_t c = s_whist[w][tid];
-        s_whist[w][tid] = run;
-        run += c;
-    }
-    uint32_t tot;
-    const uint32_t lstart = block_excl_scan<uint32_t, kTsWarps>(run, s_scan, tot);
-#pragma unroll
-    for (int w = 0; w < kTsWarps; ++w) s_whist[w][tid] += lstart;
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kTsItems; ++i) {
-        const uint32_t p = warp * (kTsItems * 32) + i * 32 + lane;
-        if (p < n) {
-            const uint32_t dig = ((k[i] - kmin) >> shift) & 255u;
-            const uint32_t pos = s_whist[warp][dig] + rk[i];
-            s_k[pos] = k[i];
-            s_i[pos] = v[i];
-        }
-    }
-    __syncthreads();
-}
-
-__global__ __launch_bounds__(kTsThreads) void k_tilesort(const uint32_t* __restrict__ keys, uint16_t* __restrict__ lperm,
-                                                         TilePairs tp, uint32_t* __restrict__ counts,
-                                                         uint32_t* __restrict__ npairs, uint32_t nu, uint32_t C)
-{
-    __shared__ uint32_t s_k[kSortTile];
-    __shared__ uint16_t s_i[kSortTile];
-    __shared__ uint32_t s_whist[kTsWarps][256];
-    __shared__ uint16_t s_start[kSortTile + 1];
-    __shared__ uint32_t s_scan[kTsWarps + 1];
-    __shared__ uint32_t s_min[kTsWarps], s_max[kTsWarps];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t base = blockIdx.x * kSortTile;
-    const uint32_t n = nu > base ? min((uint32_t)kSortTile, nu - base) : 0u;
+    const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
+    const float w_bar = sc->w_bar;
+    const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
+    if (blockIdx.x == 0 && tid == 0) sc->w_pred = w_pred;
+    const float Wf = (float)fc.W, Hf = (float)fc.H;
 
+    // ---- predict (Alg. 1): position p = local index (input order)
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
-#pragma unroll
-    for (int i = 0; i < kTsItems / 4; ++i) {
-        const uint32_t l = (i * kTsThreads + tid) * 4;
-        uint4 k4 = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (l + 3 < n) k4 = *reinterpret_cast<const uint4*>(keys + base + l);
-        else {
-            if (l < n) k4.x = keys[base + l];
-            if (l + 1 < n) k4.y = keys[base + l + 1];
-            if (l + 2 < n) k4.z = keys[base + l + 2];
+#pragma unroll 2
+    for (int i = 0; i < kPsRows; ++i) {
+        const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+        uint32_t key = 0xFFFFFFFFu;
+        if (p < n) {
+            const uint32_t g = base + p;
+            const float4 X = st[g];
+            const Philox4 r = draw(fc.seed, g, a.k, STAGE_PREDICT);
+            float n0, n1, n2, n3;
+            box_muller(r.r0, r.r1, n0, n1);
+            box_muller(r.r2, r.r3, n2, n3);
+            // p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v
+            const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(X.z, a.Tc, X.x));
+            const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(X.w, a.Tc, X.y));
+            const float vxn = __fmaf_rn(a.s_v, n2, X.z);
+            const float vyn = __fmaf_rn(a.s_v, n3, X.w);
+            const bool inside = (xn >= 0.0f) && (xn < Wf) && (yn >= 0.0f) && (yn < Hf);
+            key = inside ? (uint32_t)__float2int_rz(yn) * (uint32_t)fc.W + (uint32_t)__float2int_rz(xn) : fc.C;  // A-4, A-5
+            pst[g] = make_float4(xn, yn, vxn, vyn);
+            if (keys_dbg) keys_dbg[g] = key;
+            kmin = min(kmin, key);
+            kmax = max(kmax, key);
         }
-        const uint32_t kk[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            s_k[l + e] = kk[e];
-            s_i[l + e] = (uint16_t)(l + e);
-            if (l + e < n) { kmin = min(kmin, kk[e]); kmax = max(kmax, kk[e]); }
-        }
+        S.k[0][p] = key;
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
     }
-    if (lane == 0) { s_min[warp] = kmin; s_max[warp] = kmax; }
+    if (lane == 0) { S.mn[warp] = kmin; S.mx[warp] = kmax; }
     __syncthreads();
-    kmin = s_min[0]; kmax = s_max[0];
+    kmin = S.mn[0]; kmax = S.mx[0];
 #pragma unroll
-    for (int w = 1; w < kTsWarps; ++w) { kmin = min(kmin, s_min[w]); kmax = max(kmax, s_max[w]); }
-    const uint32_t range = n ? kmax - kmin : 0u;
+    for (int w = 1; w < kPsWarps; ++w) { kmin = min(kmin, S.mn[w]); kmax = max(kmax, S.mx[w]); }
+    if (n == 0) return;
+    const uint32_t range = kmax - kmin;
     const int bits = range ? 32 - __clz(range) : 0;
-    for (int shift = 0; shift < bits; shift += 8) tile_radix_pass(s_k, s_i, s_whist, s_scan, kmin, shift, n);
 
-    // runs of equal keys in sorted order -> pairs
-    const uint32_t p0 = tid * kTsItems;
-    uint32_t flags = 0, nrun = 0;
+    // ---- stable LSD radix passes (positions >= n carry key 0xFFFFFFFF and stay at the end)
+    int cur = 0;
+    for (int shift = 0; shift < bits; shift += 8, cur ^= 1) {
+        for (int i = tid; i < kPsWarps * 256; i += kPsThreads) (&S.hist[0][0])[i] = 0;
+        __syncthreads();
+#pragma unroll 4
+        for (int i = 0; i < kPsRows; ++i) {                  // count + per-warp ranks
+            const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+            const uint32_t key = S.k[cur][p];
+            const uint32_t dig = p < n ? ((key - kmin) >> shift) & 255u : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+            uint32_t prev = 0;
+            if (dig < 256u) prev = S.hist[warp][dig];
+            __syncwarp();
+            if (dig < 256u && (peers & lt) == 0) S.hist[warp][dig] = prev + __popc(peers);
+            __syncwarp();
+            S.rank[p] = (uint16_t)(prev + __popc(peers & lt));
+        }
+        __syncthreads();
+        {   // digit d = tid: offsets over (digit, warp) in that order
+            uint32_t run = 0;
 #pragma unroll
-    for (int i = 0; i < kTsItems; ++i) {
-        const uint32_t p = p0 + i;
-        const bool head = p < n && (p == 0 || s_k[p] != s_k[p - 1]);
-        flags |= (head ? 1u : 0u) << i;
-        nrun += head ? 1u : 0u;
+            for (int w = 0; w < kPsWarps; ++w) { const uint32_t c = S.hist[w][tid]; S.hist[w][tid] = run; run += c; }
+            uint32_t tot;
+            const uint32_t ds = block_excl_scan<uint32_t, kPsWarps>(run, S.scan, tot);
+#pragma unroll
+            for (int w = 0; w < kPsWarps; ++w) S.hist[w][tid] += ds;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int i = 0; i < kPsRows; ++i) {                  // scatter
+            const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+            if (p >= n) continue;
+            const uint32_t key = S.k[cur][p];
+            const uint32_t dig = ((key - kmin) >> shift) & 255u;
+            const uint32_t pos = S.hist[warp][dig] + S.rank[p];
+            S.k[cur ^ 1][pos] = key;
+            S.v[cur ^ 1][pos] = shift == 0 ? (uint16_t)p : S.v[cur][p];
+        }
+        __syncthreads();
+    }
+    const uint32_t* sk = S.k[cur];
+    const uint16_t* sv = S.v[cur];
+    const bool identity = bits == 0;                        // one key: input order is sorted order
+
+    // ---- runs of equal keys (warp rows -> heads in position order)
+    uint32_t hb[kPsRows];
+    uint32_t wc = 0;
+#pragma unroll
+    for (int i = 0; i < kPsRows; ++i) {
+        const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+        const bool head = p < n && (p == 0 || sk[p] != sk[p - 1]);
+        hb[i] = __ballot_sync(0xffffffffu, head);
+        wc += __popc(hb[i]);
     }
     uint32_t nd;
-    uint32_t j = block_excl_scan<uint32_t, kTsWarps>(nrun, s_scan, nd);
+    uint32_t j = block_excl_scan<uint32_t, kPsWarps>(lane == 0 ? wc : 0u, S.scan, nd);
+    j = __shfl_sync(0xffffffffu, j, 0);
+    uint16_t* s_start = S.rank;                             // reuse: run starts (nd <= n)
 #pragma unroll
-    for (int i = 0; i < kTsItems; ++i)
-        if ((flags >> i) & 1u) s_start[j++] = (uint16_t)(p0 + i);
-    if (tid == 0) { s_start[nd] = (uint16_t)n; tp.nd[blockIdx.x] = nd; }
+    for (int i = 0; i < kPsRows; ++i) {
+        const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+        if ((hb[i] >> lane) & 1u) s_start[j + __popc(hb[i] & lt)] = (uint16_t)p;
+        j += __popc(hb[i]);
+    }
     __syncthreads();
-    for (uint32_t r = tid; r < nd; r += kTsThreads) {
-        const uint32_t f = s_start[r], c = (uint32_t)s_start[r + 1] - f;
-        const uint32_t key = s_k[f];
+    for (uint32_t r = tid; r < nd; r += kPsThreads) {
+        const uint32_t f = s_start[r], e = r + 1 < nd ? (uint32_t)s_start[r + 1] : n, c = e - f;
+        const uint32_t key = sk[f];
         tp.key[base + r] = key;
         tp.first[base + r] = (uint16_t)f;
         tp.cnt[base + r] = (uint16_t)(c - 1);
-        if (key < C) {
+        if (key < fc.C) {
             atomicAdd(&counts[key], c);
             atomicAdd(&npairs[key], 1u);
         }
     }
-    for (uint32_t p = tid; p < n; p += kTsThreads) lperm[base + p] = s_i[p];
+    if (tid == 0) tp.nd[blockIdx.x] = nd;
+    // ---- local permutation (sorted position -> local input index), two per thread-step
+    for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
+        const uint32_t p = 2 * q;
+        const uint32_t v0 = identity ? p : sv[p], v1 = identity ? p + 1 : sv[p + 1];
+        reinterpret_cast<uint32_t*>(lperm + base)[q] = v0 | (v1 << 16);
+    }
 }
 
 // Each pair appends itself (tile << 12 | run) to its cell's list (unordered; k_pair_sort orders it).

@@ -205,7 +205,7 @@ def test_profile_stages():
     for _ in range(3):
         f.step(meas, cfg.dt)
     stages, n = f.profile_end()
-    assert n == 3 and "predict" in stages and "resample" in stages and all(v >= 0 for v in stages.values())
+    assert n == 3 and "predict_sort" in stages and "resample" in stages and all(v >= 0 for v in stages.values())
 
 
 @pytest.mark.slow

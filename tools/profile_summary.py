@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE_OF = {"k_predict": "predict", "k_tilesort": "tilesort", "k_cells": "cells", "k_list_scan": "list_scan",
+STAGE_OF = {"k_predict_sort": "predict_sort", "k_predict": "predict", "k_tilesort": "tilesort", "k_cells": "cells", "k_list_scan": "list_scan",
             "k_pair_fill": "pairs", "k_pair_sort": "pairs", "k_resample_tiles": "resample", "k_moments": "moments",
             "k_births": "births"}
 
