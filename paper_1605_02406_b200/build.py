@@ -6,8 +6,8 @@ import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libdog.so")
+CSRC = os.environ.get("DOG_CSRC") or os.path.join(PKG, "csrc")   # DOG_CSRC: alternative sources (A/B)
+LIB = os.environ.get("DOG_LIB") or os.path.join(PKG, "libdog.so")
 SOURCES = ["dog.cu"]
 HEADERS = ["dog_common.cuh", "dog_rng.cuh", "dog_kernels.cuh", "dog_cells.cuh", "dog_resample.cuh", "dog_sort.cuh"]
 

@@ -43,6 +43,7 @@ struct dog_ctx {
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
     float4* pst = nullptr;                        // predicted state, same layout
+    uint32_t* rD = nullptr;                       // k_resample_tiles per-run offsets beyond its smem
     // assignment (dog_sort.cuh)
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
@@ -223,6 +224,10 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     cudaFuncSetAttribute(k_predict_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
+    if (const char* cv = getenv("DOG_RS_CARVEOUT")) {   // experiments: shared-memory share of the L1/smem array
+        cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+        cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+    }
     {   // persistent grids: as many blocks as fit on the GPU at once
         int per_sm = 0, sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -256,7 +261,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->st, N); AL(ctx->pst, N);
+    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rD, N);
     AL(ctx->lperm, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
@@ -393,10 +398,10 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     if (dbg)
         k_resample_tiles<true><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                    ctx->perm, ctx->ppart, ctx->sc, fc);
+                                                                    ctx->perm, ctx->ppart, ctx->rD, ctx->sc, fc);
     else
         k_resample_tiles<false><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                     nullptr, ctx->ppart, ctx->sc, fc);
+                                                                     nullptr, ctx->ppart, ctx->rD, ctx->sc, fc);
     CK(cudaGetLastError());
     CK(mark("resample"));
     k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
@@ -639,5 +644,17 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     if (n) CK(cudaMemcpy(host_dst, src, n, cudaMemcpyDeviceToHost));
     return (int64_t)n;
 }
+
+#ifdef DOG_TIMING
+int dog_timing_dump(unsigned long long* host, int n, int reset)
+{
+    if (cudaMemcpyFromSymbol(host, g_phase_ns, (size_t)n * 8) != cudaSuccess) return -1;
+    if (reset) {
+        static unsigned long long z[64] = {};
+        cudaMemcpyToSymbol(g_phase_ns, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
 
 }  // extern "C"

@@ -75,6 +75,24 @@ __device__ __forceinline__ ulonglong2 ld_relaxed128(const ulonglong2* p)
     return v;
 }
 
+// Diagnostics build only (DOG_NVCC_EXTRA=-DDOG_TIMING, tools/phase_timing.py): per-phase block time,
+// accumulated by thread 0 of every block into g_phase_ns[slot].
+#ifdef DOG_TIMING
+__device__ unsigned long long g_phase_ns[64];
+__device__ __forceinline__ unsigned long long gtimer_ns()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define PHASE_BEGIN() unsigned long long _pt = threadIdx.x == 0 ? gtimer_ns() : 0ull
+#define PHASE_MARK(slot) do { if (threadIdx.x == 0) { const unsigned long long _n = gtimer_ns(); \
+    atomicAdd(&g_phase_ns[slot], _n - _pt); _pt = _n; } } while (0)
+#else
+#define PHASE_BEGIN() do { } while (0)
+#define PHASE_MARK(slot) do { } while (0)
+#endif
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v)
 {

@@ -137,12 +137,15 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
+constexpr int kRtRunSm = 2048;                                        // runs whose offset sits in smem (rest: global)
+constexpr int kRtRunCache = 64;                                       // runs whose parameters sit in smem
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
     uint16_t runof[kSortTile];         // sorted position -> run
-    uint32_t rD[kSortTile];            // per run: F(Q_first) - offset of the run in the compact output space
+    uint32_t rD[kRtRunSm];             // per run: F(Q_first) - offset of the run in the compact output space
+    struct RunS { uint64_t P, bp; uint32_t rpm, pre; } rs[kRtRunCache];   // resampling parameters of the first runs
     union alignas(16) {
         struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phase B -> phase R
         uint32_t osrc[kSortTile];      // phase C: compact output -> owner position + 1
@@ -192,7 +195,8 @@ __device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
 template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
-    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, const DevScalars* __restrict__ sc, FilterConst fc)
+    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, uint32_t* __restrict__ rD_g,
+    const DevScalars* __restrict__ sc, FilterConst fc)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
@@ -210,21 +214,35 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint32_t nd = tp.nd[t];
     const uint32_t p0 = tid * kRtItems;
     const RunInfo* __restrict__ runs = tp.run + base;
-    // ---- phase A: local permutation, run starts (one round trip)
+    PHASE_BEGIN();
+    // ---- phase A: local permutation, run starts, run parameters, and this thread's velocity gathers
+    //      (its 16 sorted positions are the 16 local-permutation entries it loads)
+    const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
     {
         uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
         if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }
         if (p0 < nd) { const uint4* f4 = reinterpret_cast<const uint4*>(tp.first + base + p0); c = f4[0]; d = f4[1]; }
         if (p0 < n) { reinterpret_cast<uint4*>(S.lp + p0)[0] = a; reinterpret_cast<uint4*>(S.lp + p0)[1] = b; }
         if (p0 < nd) { reinterpret_cast<uint4*>(S.first + p0)[0] = c; reinterpret_cast<uint4*>(S.first + p0)[1] = d; }
+        if ((uint32_t)tid < nd && tid < kRtRunCache) {
+            const RunInfo q = runs[tid];
+            S.rs[tid] = RtSmem::RunS{q.P, q.bp, q.rpm, q.pre};
+        }
         if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
     __syncthreads();
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
     const uint32_t srun = S.sentinel_run;
-    const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
+    auto rinfo = [&](uint32_t j) -> RtSmem::RunS {
+#ifndef RT_NO_RUNCACHE
+        if (j < (uint32_t)kRtRunCache) return S.rs[j];
+#endif
+        const RunInfo q = runs[j];
+        return RtSmem::RunS{q.P, q.bp, q.rpm, q.pre};
+    };
 
+    PHASE_MARK(0);
     // ---- phase B: run of every position, velocity sums per run segment
     if (p0 < n) {
         uint32_t lo = 0, hi = nd;                           // run containing p0
@@ -280,6 +298,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
         flush();
     }
     __syncthreads();
+    PHASE_MARK(1);
     // ---- phase R: spanning run segments -> ppart; output range and compact offset of every run
     uint32_t carry = 0;
     for (uint32_t r0 = 0; r0 < nd; r0 += kRtThreads) {
@@ -303,18 +322,20 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 ppart[base + r] = mp;
             }
             if (rc.W) {
-                const RunInfo q = runs[r];
-                Flo = fcount(member_Q(q, q.pre), rc);
-                c = fcount(member_Q(q, q.pre + (e - f)), rc) - Flo;
+                const RtSmem::RunS q = rinfo(r);
+                Flo = fcount(q.P + (uint64_t)q.pre * q.bp + min(q.pre, q.rpm), rc);
+                const uint32_t me = q.pre + (e - f);
+                c = fcount(q.P + (uint64_t)me * q.bp + min(me, q.rpm), rc) - Flo;
             }
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
-        if (r < nd) S.rD[r] = Flo - (carry + ex);
+        if (r < nd) { if (r < (uint32_t)kRtRunSm) S.rD[r] = Flo - (carry + ex); else rD_g[base + r] = Flo - (carry + ex); }
         carry += tot;
     }
     __syncthreads();
     const uint32_t Ot = carry;
+    PHASE_MARK(2);
     // ---- phase C: windows of the compact output space
     for (uint32_t w0 = 0; w0 < Ot; w0 += kSortTile) {
         uint32_t* os = S.u.osrc;
@@ -330,22 +351,23 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
             uint32_t F0 = 0, e = 0;
             uint64_t Q1 = 0;
             if (live) {
-                const RunInfo q = runs[j];
+                const RtSmem::RunS q = rinfo(j);
                 e = S.first[j + 1];
                 const uint32_t mr = q.pre + (p - S.first[j]);
-                const uint64_t Q0 = member_Q(q, mr);
+                const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
                 Q1 = Q0 + q.bp + (mr < q.rpm ? 1u : 0u);
                 F0 = fcount(Q0, rc);
             }
             const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);   // the next position's F(Q)
             if (live) {
                 const uint32_t F1 = (lane < 31 && p + 1 < e) ? Fn : fcount(Q1, rc);
-                const uint32_t D = S.rD[j];
+                const uint32_t D = j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j];
                 const uint32_t C0 = F0 - D, C1 = F1 - D;
                 if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = p + 1u;
             }
         }
         __syncthreads();
+        PHASE_MARK(3);
         {   // inclusive max-scan over the window: thread-contiguous 16 entries
             uint32_t v[kRtItems];
 #pragma unroll
@@ -362,6 +384,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                     make_uint4(max(v[4 * i], pre), max(v[4 * i + 1], pre), max(v[4 * i + 2], pre), max(v[4 * i + 3], pre));
         }
         __syncthreads();
+        PHASE_MARK(4);
         const uint32_t wn = min((uint32_t)kSortTile, Ot - w0);
 #pragma unroll 1
         for (uint32_t i0 = 0; i0 < wn; i0 += 4 * kRtThreads) {
@@ -373,7 +396,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 ok[h] = i < wn;
                 const uint32_t p = os[ok[h] ? i : 0u] - 1u;
                 const uint32_t j = S.runof[p];
-                o[h] = w0 + i + S.rD[j];
+                o[h] = w0 + i + (j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j]);
                 src[h] = base + S.lp[p];
                 J[h] = 0;
                 if (kDbg) { const RunInfo q = runs[j]; J[h] = q.jbase + q.pre + (p - S.first[j]); }
@@ -389,6 +412,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
             }
         }
         __syncthreads();
+        PHASE_MARK(5);
     }
 }
 

@@ -78,6 +78,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     if (blockIdx.x == 0 && tid == 0) sc->w_pred = w_pred;
     const float Wf = (float)fc.W, Hf = (float)fc.H;
 
+    PHASE_BEGIN();
     // ---- predict (Alg. 1): position p = local index (input order)
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
 #pragma unroll 2
@@ -116,6 +117,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
 #pragma unroll
     for (int w = 1; w < kPsWarps; ++w) { kmin = min(kmin, S.mn[w]); kmax = max(kmax, S.mx[w]); }
     if (n == 0) return;
+    PHASE_MARK(8);
     const uint32_t range = kmax - kmin;
     const int bits = range ? 32 - __clz(range) : 0;
 
@@ -160,6 +162,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
         }
         __syncthreads();
     }
+    PHASE_MARK(9);
     const uint32_t* sk = S.k[cur];
     const uint16_t* sv = S.v[cur];
     const bool identity = bits == 0;                        // one key: input order is sorted order
@@ -197,12 +200,14 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
         }
     }
     if (tid == 0) tp.nd[blockIdx.x] = nd;
+    PHASE_MARK(10);
     // ---- local permutation (sorted position -> local input index), two per thread-step
     for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
         const uint32_t p = 2 * q;
         const uint32_t v0 = identity ? p : sv[p], v1 = identity ? p + 1 : sv[p + 1];
         reinterpret_cast<uint32_t*>(lperm + base)[q] = v0 | (v1 << 16);
     }
+    PHASE_MARK(11);
 }
 
 // Each pair appends itself (tile << 12 | run) to its cell's list (unordered; k_pair_sort orders it).

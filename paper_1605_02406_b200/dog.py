@@ -16,7 +16,8 @@ import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdog.so")
+# DOG_LIB selects another in-tree build of the same library (A/B experiments, tools/ab.sh)
+LIB_PATH = os.environ.get("DOG_LIB") or os.path.join(_PKG, "libdog.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

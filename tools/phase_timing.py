@@ -1,0 +1,32 @@
+"""Per-phase block times of the instrumented kernels (diagnostics build: DOG_NVCC_EXTRA=-DDOG_TIMING).
+
+Runs the cfgT filter for 30 settle cycles, then 10 cycles with the phase counters reset; prints the
+average per-block microseconds of each phase slot."""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1605_02406_b200 import dog, inputs as I
+
+NAMES = {0: "rs A (loads)", 1: "rs B (moments, runof)", 2: "rs R (spanning, prefix)", 3: "rs C scatter (F)",
+         4: "rs C max-scan", 5: "rs C outputs", 8: "ps predict", 9: "ps radix passes", 10: "ps runs", 11: "ps lperm"}
+cfg = I.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfgT"]
+sc = I.scene(cfg)
+f = dog.Filter.from_config(cfg)
+frames = [sc.frame(k, device="cuda") for k in range(40)]
+for k in range(30):
+    f.step(frames[k], cfg.dt)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 64)()
+dog._lib.dog_timing_dump(buf, 64, 1)
+for k in range(30, 40):
+    f.step(frames[k], cfg.dt)
+torch.cuda.synchronize()
+dog._lib.dog_timing_dump(buf, 64, 0)
+t = np.frombuffer(buf, dtype=np.uint64).astype(np.float64)
+blocks = (cfg.nu + 4095) // 4096 * 10
+for i, nm in NAMES.items():
+    print(f"{nm:28s} {t[i] / blocks / 1000:8.2f} us per block")
