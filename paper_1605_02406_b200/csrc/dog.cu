@@ -68,7 +68,6 @@ struct dog_ctx {
     float *bx = nullptr, *by = nullptr, *bvx = nullptr, *bvy = nullptr;
     uint32_t* jidx = nullptr;
     DevScalars* sc = nullptr;
-    uint32_t* ctrs = nullptr;                     // zeroed once per cycle: finished-block counters
     // end-to-end staging
     float* meas_dev = nullptr;
     // profiling: events[step][stage boundary]
@@ -285,14 +284,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
 
     AL(ctx->sc, 1);
-    AL(ctx->ctrs, 16);
 #undef AL
     if (rc != DOG_OK) {
         free_all(ctx);
         delete ctx;
         return rc;
     }
-    ctx->bt.done = ctx->ctrs;
 
     // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
     std::vector<float4> sent(N, make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f));
@@ -356,7 +353,6 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         return cudaEventRecord(ctx->pev[(size_t)ctx->prof_steps * (DOG_MAX_STAGES + 1) + mark_i++], st);
     };
     CK(mark(nullptr));
-    CK(cudaMemsetAsync(ctx->ctrs, 0, 16 * sizeof(uint32_t), st));
     const uint32_t T = ctx->tiles;
 
     // 1-2. predict (Alg. 1) fused with the tile-local stable sort (Alg. 2): runs, per-cell counts

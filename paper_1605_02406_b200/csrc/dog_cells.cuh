@@ -52,11 +52,10 @@ struct CellList {           // the flat active list in cell order (SoA, capacity
     uint32_t* pfill;        // run-list fill counter (reset here, k_pair_fill)
 };
 
-struct BlockTotals {        // one entry per cell chunk
-    uint32_t* cnt;          // active cells staged by the block -> exclusive prefix (k_cells, last block)
-    uint64_t* n0;           // sum of n_c over them (grand total by the last block)
-    uint64_t* rb0;          // sum of R_b over them (grand total by the last block)
-    uint32_t* done;         // finished-block counter of k_cells (zeroed per cycle)
+struct BlockTotals {        // one entry per cell chunk (k_cells); prefixes / totals are formed in k_list_scan
+    uint32_t* cnt;          // active cells staged by the block
+    uint64_t* n0;           // sum of n_c over them
+    uint64_t* rb0;          // sum of R_b over them
 };
 
 __device__ __forceinline__ uint64_t fx40(float m)
@@ -111,7 +110,7 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     return o;
 }
 
-constexpr int kCellThreads = 256, kCellItems = 4, kCellIter = kCellThreads * kCellItems;   // 1024 cells
+constexpr int kCellThreads = 256, kCellItems = 8, kCellIter = kCellThreads * kCellItems;   // 2048 cells
 constexpr int kMaxCellBlocks = 4096;
 
 struct CellDebug { float* rho_p; float* rho_b; uint64_t* Rp; uint64_t* Rb; };
@@ -135,8 +134,11 @@ __device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
     return carry;
 }
 
-// Block b owns cells [b chunk, (b+1) chunk), 1024 per iteration; item i of thread t in an iteration
-// is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid bitmask).
+// Block b owns cells [b chunk, (b+1) chunk), 2048 per iteration; item i of thread t in an iteration
+// is cell base + i*256 + t (coalesced; one warp = one 32-bit word of the moments-valid bitmask).  All
+// loads of an iteration are issued up front.  Active cells (~1 %) keep their inputs (n_c, m_F) untouched
+// in the first pass; after the block's staging offsets are known they are recomputed from them
+// (identical arithmetic) and staged, and only then is m_F updated and n_c cleared.
 __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
@@ -146,8 +148,6 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     __shared__ uint32_t s_run;
     __shared__ uint64_t s_A[9], s_N[9];
     __shared__ uint32_t s_bad[8];
-    __shared__ uint32_t s_C[9];
-    __shared__ bool s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const float w_pred = sc->w_pred;
@@ -172,57 +172,60 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
             prev[i] = (lane == 0 && (word << 5) < c1) ? mvalid[word] : 0u;
         }
-        CellOut o[kCellItems];
         uint32_t abal[kCellItems];
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
-            o[i] = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
-            const bool vnow = valid && o[i].n > 0 && o[i].rp > 0.0f && o[i].S > 0.0f;
+            const CellOut o = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
+            const bool vnow = valid && o.n > 0 && o.rp > 0.0f && o.S > 0.0f;
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
             const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
+            const bool act = valid && (o.n > 0 || o.Rb > 0);
             if (valid) {
-                occ[c] = o[i].mO;
-                free_out[c] = o[i].mF;
-                m_free[c] = o[i].mF;                    // Alg. 3 store_values
-                if (n[i]) counts[c] = 0u;               // ready for the next cycle's k_tilesort
+                occ[c] = o.mO;
+                free_out[c] = o.mF;
+                if (!act) m_free[c] = o.mF;             // Alg. 3 store_values (active cells: below)
                 if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
                     mean[c] = make_float2(0.0f, 0.0f);
                     cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
                 }
                 if (dbg.rho_p) {
-                    dbg.rho_p[c] = o[i].rp; dbg.rho_b[c] = o[i].rb; dbg.Rp[c] = o[i].Rp; dbg.Rb[c] = o[i].Rb;
+                    dbg.rho_p[c] = o.rp; dbg.rho_b[c] = o.rb; dbg.Rp[c] = o.Rp; dbg.Rb[c] = o.Rb;
                 }
-                bad_loc += o[i].bad ? 1u : 0u;
+                bad_loc += o.bad ? 1u : 0u;
             }
             if (lane == 0 && (word << 5) < c1 && bal != pw) mvalid[word] = bal;
-            const bool act = valid && (o[i].n > 0 || o[i].Rb > 0);
             abal[i] = __ballot_sync(0xffffffffu, act);
             if (lane == 0) s_cnt[i][warp] = __popc(abal[i]);
         }
         __syncthreads();
         if (warp == 0) {   // exclusive offsets in cell order (item-major, then warp) + running total
-            const uint32_t v = lane < kCellItems * 8 ? s_cnt[lane >> 3][lane & 7] : 0u;
-            const uint32_t incl = warp_incl_scan(v, lane);
+            const uint32_t v0 = s_cnt[lane >> 3][lane & 7], v1 = s_cnt[4 + (lane >> 3)][lane & 7];
+            const uint32_t i0 = warp_incl_scan(v0, lane), i1 = warp_incl_scan(v1, lane);
+            const uint32_t t0 = __shfl_sync(0xffffffffu, i0, 31);
             const uint32_t run = s_run;
-            if (lane < kCellItems * 8) s_cnt[lane >> 3][lane & 7] = run + incl - v;
+            s_cnt[lane >> 3][lane & 7] = run + i0 - v0;
+            s_cnt[4 + (lane >> 3)][lane & 7] = run + t0 + i1 - v1;
             __syncwarp();
-            if (lane == 31) s_run = run + incl;
+            if (lane == 31) s_run = run + t0 + i1;
         }
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
-            if ((abal[i] >> lane) & 1u) {
+            if ((abal[i] >> lane) & 1u) {               // active cell: same inputs (untouched), same arithmetic
                 const uint32_t c = base + i * kCellThreads + tid;
+                const CellOut o = cell_math(__ldcg(counts + c), __ldcg(m_free + c), meas[c], w_pred, alpha, fc);
+                m_free[c] = o.mF;
+                if (o.n) counts[c] = 0u;                // ready for the next cycle's k_predict_sort
                 const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
-                L.c[li] = c; L.n[li] = o[i].n; L.Rp[li] = o[i].Rp; L.Rb[li] = o[i].Rb; L.rho_p[li] = o[i].rp;
+                L.c[li] = c; L.n[li] = o.n; L.Rp[li] = o.Rp; L.Rb[li] = o.Rb; L.rho_p[li] = o.rp;
                 uint32_t npc = 0;
-                if (o[i].n) { npc = npairs[c]; npairs[c] = 0u; }
+                if (o.n) { npc = npairs[c]; npairs[c] = 0u; }
                 L.np[li] = npc;
-                A_loc += o[i].Rb;
-                N_loc += o[i].n;
+                A_loc += o.Rb;
+                N_loc += o.n;
             }
         }
         __syncthreads();
@@ -240,17 +243,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         bt.n0[blockIdx.x] = N;
         bt.rb0[blockIdx.x] = A;
         if (b) atomicAdd(&sc->meas_bad, b);
-        __threadfence();
-        s_last = atomicAdd(&bt.done[0], 1u) == gridDim.x - 1;
     }
-    __syncthreads();
-    if (!s_last) return;
-    // the last block: exclusive prefixes of the block totals, grand totals
-    __threadfence();
-    const uint64_t N = block_prefix_inplace<uint64_t>(bt.n0, gridDim.x, s_N);
-    const uint64_t A = block_prefix_inplace<uint64_t>(bt.rb0, gridDim.x, s_A);
-    const uint32_t Lc = block_prefix_inplace<uint32_t>(bt.cnt, gridDim.x, s_C);
-    if (tid == 0) { sc->n_in = N; sc->A = A; sc->Lc = Lc; }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -309,6 +302,24 @@ __device__ __forceinline__ uint64_t warp_excl_items(const uint64_t (&v)[I], uint
     return carry;
 }
 
+// Block-level exclusive scan of one ulonglong2 per thread (this CTA only); returns the CTA total.
+__device__ __forceinline__ ulonglong2 cta_excl_scan2(ulonglong2 v, ulonglong2* s_w, ulonglong2& off)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t ix = warp_incl_scan(v.x, lane), iy = warp_incl_scan(v.y, lane);
+    if (lane == 31) s_w[warp] = make_ulonglong2(ix, iy);
+    __syncthreads();
+    uint64_t ox = 0, oy = 0, tx = 0, ty = 0;
+    for (int w = 0; w < kLsWarps; ++w) {
+        const ulonglong2 x = s_w[w];
+        if (w < warp) { ox += x.x; oy += x.y; }
+        tx += x.x; ty += x.y;
+    }
+    __syncthreads();
+    off = make_ulonglong2(ox + ix - v.x, oy + iy - v.y);
+    return make_ulonglong2(tx, ty);
+}
+
 // Two-value exclusive prefix over the CTA's warps (warp totals t) and over the cluster's CTAs.
 // Returns the offset of the calling warp within the cluster round; *round_total = the round's total.
 __device__ __forceinline__ ulonglong2 cluster_offsets(ulonglong2 t, ulonglong2* s_w, ulonglong2* s_tot,
@@ -354,12 +365,42 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
     __shared__ ulonglong2 s_base[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t rank = cluster.block_rank(), nc = cluster.num_blocks();
-    const uint32_t Lc = sc->Lc;
-    const uint64_t A = sc->A;
+    // chunk offsets (exclusive prefix of the staged counts) and the grand totals n_in, A -- every CTA
+    // forms them itself from k_cells' per-chunk totals (nblk <= 4096: four per thread)
+    uint32_t Lc;
+    uint64_t A, N;
+    {
+        constexpr int kI = (kMaxCellBlocks + kLsThreads - 1) / kLsThreads;
+        uint32_t cv[kI];
+        uint32_t cs = 0;
+        uint64_t as = 0, ns = 0;
+#pragma unroll
+        for (int i = 0; i < kI; ++i) {
+            const uint32_t b = tid * kI + i;
+            cv[i] = b < nblk ? bt.cnt[b] : 0u;
+            cs += cv[i];
+            if (b < nblk) { as += bt.rb0[b]; ns += bt.n0[b]; }
+        }
+        ulonglong2 off;
+        ulonglong2 tot = cta_excl_scan2(make_ulonglong2(cs, 0ull), s_w, off);
+        uint32_t run = (uint32_t)off.x;
+#pragma unroll
+        for (int i = 0; i < kI; ++i) {
+            const uint32_t b = tid * kI + i;
+            if (b < nblk) s_cnt0[b] = run;
+            run += cv[i];
+        }
+        Lc = (uint32_t)tot.x;
+        const ulonglong2 t2 = cta_excl_scan2(make_ulonglong2(as, ns), s_w, off);
+        A = t2.x;
+        N = t2.y;
+        if (tid == 0) {
+            s_cnt0[nblk] = Lc;
+            if (rank == 0) { sc->Lc = Lc; sc->A = A; sc->n_in = N; }
+        }
+    }
     const uint64_t nu_b = fc.nu_b;
     const double rcpA = A ? 1.0 / (double)A : 0.0;
-    for (uint32_t b = tid; b < nblk; b += kLsThreads) s_cnt0[b] = bt.cnt[b];
-    if (tid == 0) s_cnt0[nblk] = Lc;
     __syncthreads();
     const uint32_t cap = nc * kLsThreads * kLsItems;
     ulonglong2 carry1 = make_ulonglong2(0ull, 0ull), carry2 = carry1;
