@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstring>
 #include <new>
+#include <utility>
 #include <vector>
 
 #include "../../include/dog.h"
@@ -113,6 +114,32 @@ void free_all(dog_ctx* ctx)
 }
 
 bool finite(float v) { return std::isfinite(v); }
+
+// Every kernel of a cycle is launched with programmatic stream serialization (PDL, dog_common.cuh):
+// its CTAs may start while the previous kernel drains and wait in griddepcontrol.wait for its results.
+bool g_pdl = getenv("DOG_NO_PDL") == nullptr;
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, uint32_t cluster,
+                   Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (g_pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster; at[na].val.clusterDim.y = 1; at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
+    cfg.attrs = at; cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 StepArgs step_args(const dog_ctx* ctx, float dt)
 {
@@ -356,57 +383,45 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     const uint32_t T = ctx->tiles;
 
     // 1-2. predict (Alg. 1) fused with the tile-local stable sort (Alg. 2): runs, per-cell counts
-    k_predict_sort<<<T, kPsThreads, kPsSmemBytes, st>>>(ctx->st, ctx->pst, dbg ? ctx->keys : nullptr, ctx->lperm,
-                                                        ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a);
-    CK(cudaGetLastError());
+    CK(launch(k_predict_sort, T, kPsThreads, kPsSmemBytes, st, 0, ctx->st, ctx->pst, dbg ? ctx->keys : nullptr,
+              ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
     CK(mark("predict_sort"));
 
-    // 3. cells: DS predict/update, birth split, fixed point, active-cell list (Alg. 3)
+    // 3. cells: DS predict/update, birth split, fixed point, active-cell staging (Alg. 3)
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
-    k_cells<<<ctx->cell_blocks, kCellThreads, 0, st>>>(ctx->counts, ctx->npairs, ctx->m_free, (const float2*)meas,
-                                                       ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg,
-                                                       ctx->stage, ctx->bt, ctx->cell_chunk, ctx->sc, fc, a.alpha);
-    CK(cudaGetLastError());
+    CK(launch(k_cells, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
+              (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
+              ctx->cell_chunk, ctx->sc, fc, a.alpha));
     CK(mark("cells"));
 
-    // 4. slots, joint CDF, run-list offsets over the active list (Alg. 5 / Alg. 7 prefix sums)
-    {
-        cudaLaunchConfig_t cfg = {};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = ctx->ls_cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(ctx->ls_cluster); cfg.blockDim = dim3(kLsThreads); cfg.stream = st;
-        cfg.attrs = at; cfg.numAttrs = 1;
-        CK(cudaLaunchKernelEx(&cfg, k_list_scan, ctx->stage, ctx->list, ctx->bt, ctx->cell_blocks, ctx->cell_chunk,
-                              ctx->cell2list, ctx->sc, fc, (int64_t)a.k));
-    }
-    CK(cudaGetLastError());
+    // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
+    CK(launch(k_list_scan, ctx->ls_cluster, kLsThreads, 0, st, ctx->ls_cluster, ctx->stage, ctx->list, ctx->bt,
+              ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, ctx->sc, fc, (int64_t)a.k));
     CK(mark("list_scan"));
 
     // 5. each cell's runs in tile order -> stable within-cell ranks
-    k_pair_fill<<<T, 256, 0, st>>>(ctx->tp, ctx->list, ctx->cell2list, ctx->plist, ctx->C);
-    CK(cudaGetLastError());
-    k_pair_sort<<<ctx->flat_blocks, 256, 0, st>>>(ctx->tp, ctx->list, ctx->plist, ctx->ptmp, ctx->sc);
-    CK(cudaGetLastError());
+    CK(launch(k_pair_fill, T, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist, ctx->C));
+    CK(launch(k_pair_sort, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp,
+              (const DevScalars*)ctx->sc));
     CK(mark("pairs"));
 
     // 6. persistent particles: moments + resampling copies; births
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     if (dbg)
-        k_resample_tiles<true><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                    ctx->perm, ctx->ppart, ctx->rD, ctx->sc, fc);
+        CK(launch(k_resample_tiles<true>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+                  (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rD, (const DevScalars*)ctx->sc, fc));
     else
-        k_resample_tiles<false><<<T, kRtThreads, kRtSmemBytes, st>>>(ctx->lperm, ctx->tp, ctx->pst, ctx->list, ns,
-                                                                     nullptr, ctx->ppart, ctx->rD, ctx->sc, fc);
-    CK(cudaGetLastError());
+        CK(launch(k_resample_tiles<false>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+                  (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rD,
+                  (const DevScalars*)ctx->sc, fc));
     CK(mark("resample"));
-    k_moments<<<ctx->flat_blocks, 256, 0, st>>>(ctx->list, ctx->plist, ctx->ppart, ctx->mean, ctx->cov, ctx->sc);
-    CK(cudaGetLastError());
+    CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
+              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc));
     CK(mark("moments"));
     if (ctx->nu_b > 0) {
         BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-        k_births<<<ctx->birth_blocks, 256, 0, st>>>(ctx->list, ns, bd, ctx->sc, fc, a.k);
-        CK(cudaGetLastError());
+        CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
+                  (int64_t)a.k));
     }
     CK(mark("births"));
     if (prof) {

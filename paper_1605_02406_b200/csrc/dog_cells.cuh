@@ -144,6 +144,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
 {
+    PDL_ENTER();
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
     __shared__ uint32_t s_run;
     __shared__ uint64_t s_A[9], s_N[9];
@@ -357,6 +358,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
                                                           uint32_t chunk, uint32_t* __restrict__ cell2list,
                                                           DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
+    PDL_ENTER();
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ uint32_t s_cnt0[kMaxCellBlocks + 1];

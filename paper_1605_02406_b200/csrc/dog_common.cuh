@@ -93,6 +93,13 @@ __device__ __forceinline__ unsigned long long gtimer_ns()
 #define PHASE_MARK(slot) do { } while (0)
 #endif
 
+// Programmatic dependent launch (every kernel of a cycle is launched with the PDL attribute): a kernel
+// lets the next one launch as soon as all its CTAs are running, and waits for its predecessor's results
+// (full completion and memory flush) before touching them.  Hides the launch gap between kernels.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+#define PDL_ENTER() do { pdl_trigger(); pdl_wait(); } while (0)
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v)
 {

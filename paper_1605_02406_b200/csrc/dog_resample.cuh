@@ -198,6 +198,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, uint32_t* __restrict__ rD_g,
     const DevScalars* __restrict__ sc, FilterConst fc)
 {
+    PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -424,6 +425,7 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
                                                  const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
                                                  float* __restrict__ cov, const DevScalars* __restrict__ sc)
 {
+    PDL_ENTER();
     const int lane = threadIdx.x & 31, gl = lane & (kMoGroup - 1);
     const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
     const uint32_t Lc = sc->Lc;
@@ -454,6 +456,7 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
 __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, BirthDebug bdbg,
                                                 const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
+    PDL_ENTER();
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu);
     const uint32_t n_items = sc->n_items, Lc = sc->Lc;

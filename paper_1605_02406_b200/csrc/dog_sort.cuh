@@ -67,6 +67,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs,
     DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
 {
+    PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     PsSmem& S = *reinterpret_cast<PsSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -214,6 +215,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
 __global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, const uint32_t* __restrict__ cell2list,
                                                    uint32_t* __restrict__ plist, uint32_t C)
 {
+    PDL_ENTER();
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const uint32_t nd = tp.nd[t];
     for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
@@ -234,6 +236,7 @@ constexpr int kPsGroup = 8, kPsBuf = 128;
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
                                                    uint32_t* __restrict__ ptmp, const DevScalars* __restrict__ sc)
 {
+    PDL_ENTER();
     __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
     const int lane = threadIdx.x & 31, gl = lane & (kPsGroup - 1), grp = threadIdx.x / kPsGroup;
     const uint32_t gmask = 0xFFu << (lane & ~(kPsGroup - 1));
