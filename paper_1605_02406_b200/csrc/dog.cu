@@ -44,7 +44,7 @@ struct dog_ctx {
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
     float4* pst = nullptr;                        // predicted state, same layout
-    uint32_t* rD = nullptr;                       // k_resample_tiles per-run offsets beyond its smem
+    RunF* rfg = nullptr;                          // k_resample_tiles per-run parameters beyond its smem
     // assignment (dog_sort.cuh)
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
@@ -287,7 +287,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rD, N);
+    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rfg, N);
     AL(ctx->lperm, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
@@ -409,10 +409,10 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     if (dbg)
         CK(launch(k_resample_tiles<true>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                  (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rD, (const DevScalars*)ctx->sc, fc));
+                  (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg, (const DevScalars*)ctx->sc, fc));
     else
         CK(launch(k_resample_tiles<false>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                  (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rD,
+                  (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
                   (const DevScalars*)ctx->sc, fc));
     CK(mark("resample"));
     CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,

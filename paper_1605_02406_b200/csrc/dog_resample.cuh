@@ -137,24 +137,47 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 }
 
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
-constexpr int kRtRunSm = 2048;                                        // runs whose offset sits in smem (rest: global)
-constexpr int kRtRunCache = 64;                                       // runs whose parameters sit in smem
+constexpr int kRtRunCache = 64;                                       // runs whose RunF sits in smem (rest: global)
+constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
+constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 window entries per thread
 
-struct RtSmem {   // dynamic shared memory of k_resample_tiles
+// Per run, everything the owner marks need: F(Q_r) of member r = pre + k (k = position - first) is
+// ceil(y) with y = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
+// pieces, steps bp + 1 and bp); D = F(Q_pre) - the run's offset in the tile's compact output space.
+struct RunF {
+    double y0, d1, yR, d2;
+    uint32_t pre, rpm;
+    uint16_t first, end;
+    uint32_t D;
+};
+
+struct RtSmem {   // dynamic shared memory of k_resample_tiles (~47 KB: three blocks per SM with a large L1)
     uint16_t lp[kSortTile];            // local sorted position -> local index
     uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
     uint16_t runof[kSortTile];         // sorted position -> run
-    uint32_t rD[kRtRunSm];             // per run: F(Q_first) - offset of the run in the compact output space
-    struct RunS { uint64_t P, bp; uint32_t rpm, pre; } rs[kRtRunCache];   // resampling parameters of the first runs
+    alignas(16) RunF rf[kRtRunCache];
     union alignas(16) {
         struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phase B -> phase R
-        uint32_t osrc[kSortTile];      // phase C: compact output -> owner position + 1
+        uint16_t osrc[kRtWin];         // phase C: compact output -> owner position + 1
     } u;
     uint32_t scan[kRtThreads / 32 + 1];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
+    uint32_t slow;                     // an estimate was too close to an integer: exact marks needed
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
 static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0, "vector smem access");
+
+// ceil(y) clamped to [0, nu] when y is provably within 2^-27 of the exact value and further than 2^-22
+// from an integer; otherwise *amb is set (the caller redoes the work with exact products).
+__device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, bool& amb)
+{
+    if (y <= -0.5) return 0u;
+    if (y >= (double)nu) return nu;
+    const double cy = ceil(y);
+    const double d = cy - y;
+    amb |= !(d > 0x1p-22 && d < 1.0 - 0x1p-22);
+    return (uint32_t)cy;
+}
 
 // Block-wide exclusive max-scan of one value per thread (values >= 0).
 __device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
@@ -195,7 +218,7 @@ __device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
 template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
-    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, uint32_t* __restrict__ rD_g,
+    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
     const DevScalars* __restrict__ sc, FilterConst fc)
 {
     PDL_ENTER();
@@ -225,23 +248,14 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
         if (p0 < nd) { const uint4* f4 = reinterpret_cast<const uint4*>(tp.first + base + p0); c = f4[0]; d = f4[1]; }
         if (p0 < n) { reinterpret_cast<uint4*>(S.lp + p0)[0] = a; reinterpret_cast<uint4*>(S.lp + p0)[1] = b; }
         if (p0 < nd) { reinterpret_cast<uint4*>(S.first + p0)[0] = c; reinterpret_cast<uint4*>(S.first + p0)[1] = d; }
-        if ((uint32_t)tid < nd && tid < kRtRunCache) {
-            const RunInfo q = runs[tid];
-            S.rs[tid] = RtSmem::RunS{q.P, q.bp, q.rpm, q.pre};
-        }
+        if (tid == 0) S.slow = 0u;
         if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
     __syncthreads();
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
     const uint32_t srun = S.sentinel_run;
-    auto rinfo = [&](uint32_t j) -> RtSmem::RunS {
-#ifndef RT_NO_RUNCACHE
-        if (j < (uint32_t)kRtRunCache) return S.rs[j];
-#endif
-        const RunInfo q = runs[j];
-        return RtSmem::RunS{q.P, q.bp, q.rpm, q.pre};
-    };
+    auto runf = [&](uint32_t j) -> const RunF& { return j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j]; };
 
     PHASE_MARK(0);
     // ---- phase B: run of every position, velocity sums per run segment
@@ -323,70 +337,112 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 ppart[base + r] = mp;
             }
             if (rc.W) {
-                const RtSmem::RunS q = rinfo(r);
-                Flo = fcount(q.P + (uint64_t)q.pre * q.bp + min(q.pre, q.rpm), rc);
-                const uint32_t me = q.pre + (e - f);
-                c = fcount(q.P + (uint64_t)me * q.bp + min(me, q.rpm), rc) - Flo;
+                const RunInfo q = runs[r];
+                Flo = fcount(member_Q(q, q.pre), rc);
+                c = fcount(member_Q(q, q.pre + (e - f)), rc) - Flo;
             }
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
-        if (r < nd) { if (r < (uint32_t)kRtRunSm) S.rD[r] = Flo - (carry + ex); else rD_g[base + r] = Flo - (carry + ex); }
+        if (live && rc.W) {
+            const RunInfo q = runs[r];
+            RunF x;
+            x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
+            x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
+            x.yR = __fma_rn((double)(q.P + (uint64_t)q.rpm * (q.bp + 1u)), rc.nu_over_W, -rc.U_frac);
+            x.d2 = __dmul_rn((double)q.bp, rc.nu_over_W);
+            x.pre = q.pre; x.rpm = q.rpm;
+            x.first = S.first[r]; x.end = S.first[r + 1];
+            x.D = Flo - (carry + ex);
+            if (r < (uint32_t)kRtRunCache) S.rf[r] = x; else rf_g[base + r] = x;
+        }
         carry += tot;
     }
     __syncthreads();
     const uint32_t Ot = carry;
     PHASE_MARK(2);
     // ---- phase C: windows of the compact output space
-    for (uint32_t w0 = 0; w0 < Ot; w0 += kSortTile) {
-        uint32_t* os = S.u.osrc;
+    uint16_t* os = S.u.osrc;
+    const uint32_t q0 = tid * kRtWinItems;                  // this thread's window entries in the max-scan
+    for (uint32_t w0 = 0; w0 < Ot; w0 += kRtWin) {
 #pragma unroll
-        for (int i = 0; i < kRtItems / 4; ++i) reinterpret_cast<uint4*>(os + p0)[i] = make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < kRtWinItems / 8; ++i) reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
+        bool amb = false;
 #pragma unroll 2
         for (int it = 0; it < kRtItems; ++it) {   // members with copies mark their first output in the window
             const uint32_t p = it * kRtThreads + tid;
             const bool inb = p < n;
             const uint32_t j = inb ? S.runof[p] : srun;
             const bool live = inb && j != srun;
-            uint32_t F0 = 0, e = 0;
-            uint64_t Q1 = 0;
+            uint32_t F0 = 0, F1 = 0, D = 0, e = 0;
+            double y1 = 0.0;
             if (live) {
-                const RtSmem::RunS q = rinfo(j);
-                e = S.first[j + 1];
-                const uint32_t mr = q.pre + (p - S.first[j]);
-                const uint64_t Q0 = q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-                Q1 = Q0 + q.bp + (mr < q.rpm ? 1u : 0u);
-                F0 = fcount(Q0, rc);
+                const RunF& x = runf(j);
+                const uint32_t mr = x.pre + (p - x.first);
+                const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), x.d2, x.yR);
+                y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), x.d2, x.yR);
+                F0 = fast_ceil(y, rc.nu, amb);
+                D = x.D;
+                e = x.end;
             }
             const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);   // the next position's F(Q)
             if (live) {
-                const uint32_t F1 = (lane < 31 && p + 1 < e) ? Fn : fcount(Q1, rc);
-                const uint32_t D = j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j];
+                F1 = (lane < 31 && p + 1 < e) ? Fn : fast_ceil(y1, rc.nu, amb);
                 const uint32_t C0 = F0 - D, C1 = F1 - D;
-                if (C1 > C0 && C1 > w0 && C0 < w0 + kSortTile) os[max(C0, w0) - w0] = p + 1u;
+                if (C1 > C0 && C1 > w0 && C0 < w0 + kRtWin) os[max(C0, w0) - w0] = (uint16_t)(p + 1u);
             }
         }
+        if (amb) S.slow = 1u;
         __syncthreads();
-        PHASE_MARK(3);
-        {   // inclusive max-scan over the window: thread-contiguous 16 entries
-            uint32_t v[kRtItems];
+#ifdef DOG_TIMING
+        if (S.slow && tid == 0) atomicAdd(&g_phase_ns[20], 1ull);
+        if (tid == 0) atomicAdd(&g_phase_ns[21], 1ull);
+#endif
+        if (S.slow) {   // rare: some estimate was ambiguous -- redo the marks with exact products
 #pragma unroll
-            for (int i = 0; i < kRtItems / 4; ++i) {
-                const uint4 x = reinterpret_cast<const uint4*>(os + p0)[i];
+            for (int i = 0; i < kRtWinItems / 8; ++i) reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            for (int it = 0; it < kRtItems; ++it) {
+                const uint32_t p = it * kRtThreads + tid;
+                if (p >= n) break;
+                const uint32_t j = S.runof[p];
+                if (j == srun) continue;
+                const RunInfo q = runs[j];
+                const RunF& x = runf(j);
+                const uint32_t mr = q.pre + (p - x.first);
+                const uint64_t Q0 = member_Q(q, mr);
+                const uint32_t C0 = fcount(Q0, rc) - x.D;
+                const uint32_t C1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc) - x.D;
+                if (C1 > C0 && C1 > w0 && C0 < w0 + kRtWin) os[max(C0, w0) - w0] = (uint16_t)(p + 1u);
+            }
+            __syncthreads();
+        }
+        PHASE_MARK(3);
+        {   // inclusive max-scan over the window: thread-contiguous 32 entries (u16 pairs)
+            uint32_t v[kRtWinItems / 2];
+#pragma unroll
+            for (int i = 0; i < kRtWinItems / 8; ++i) {
+                const uint4 x = reinterpret_cast<const uint4*>(os + q0)[i];
                 v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
             }
+            uint32_t run = 0;
 #pragma unroll
-            for (int i = 1; i < kRtItems; ++i) v[i] = max(v[i], v[i - 1]);
-            const uint32_t pre = block_excl_max(v[kRtItems - 1], S.scan);
+            for (int i = 0; i < kRtWinItems / 2; ++i) {
+                const uint32_t lo = max(v[i] & 0xFFFFu, run), hi = max(v[i] >> 16, lo);
+                v[i] = lo | (hi << 16);
+                run = hi;
+            }
+            const uint32_t pre = block_excl_max(run, S.scan);
+            const uint32_t pre2 = pre | (pre << 16);
 #pragma unroll
-            for (int i = 0; i < kRtItems / 4; ++i)
-                reinterpret_cast<uint4*>(os + p0)[i] =
-                    make_uint4(max(v[4 * i], pre), max(v[4 * i + 1], pre), max(v[4 * i + 2], pre), max(v[4 * i + 3], pre));
+            for (int i = 0; i < kRtWinItems / 8; ++i)
+                reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(__vmaxu2(v[4 * i], pre2), __vmaxu2(v[4 * i + 1], pre2),
+                                                                  __vmaxu2(v[4 * i + 2], pre2), __vmaxu2(v[4 * i + 3], pre2));
         }
         __syncthreads();
         PHASE_MARK(4);
-        const uint32_t wn = min((uint32_t)kSortTile, Ot - w0);
+        const uint32_t wn = min((uint32_t)kRtWin, Ot - w0);
 #pragma unroll 1
         for (uint32_t i0 = 0; i0 < wn; i0 += 4 * kRtThreads) {
             uint32_t o[4], src[4], J[4];
@@ -395,9 +451,9 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
             for (int h = 0; h < 4; ++h) {
                 const uint32_t i = i0 + h * kRtThreads + tid;
                 ok[h] = i < wn;
-                const uint32_t p = os[ok[h] ? i : 0u] - 1u;
+                const uint32_t p = (uint32_t)os[ok[h] ? i : 0u] - 1u;
                 const uint32_t j = S.runof[p];
-                o[h] = w0 + i + (j < (uint32_t)kRtRunSm ? S.rD[j] : rD_g[base + j]);
+                o[h] = w0 + i + runf(j).D;
                 src[h] = base + S.lp[p];
                 J[h] = 0;
                 if (kDbg) { const RunInfo q = runs[j]; J[h] = q.jbase + q.pre + (p - S.first[j]); }
