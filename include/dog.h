@@ -90,6 +90,52 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream);
  * synchronous on `stream`.  This is the end-to-end entry point (host buffers in, host result out). */
 int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream);
 
+/* ---- row-band contexts (multi-GPU) ----
+ * The grid is split into horizontal bands of rows, one context (and one GPU) per band.  A band context
+ * owns its cells (m_F, readouts; the caller passes the band's measurement rows) and the particles whose
+ * cell lies in the band.  The coupling between bands is exactly (i) particles that move into the band
+ * above or below during predict, (ii) the born-mass prefix of the bands below for the slot
+ * allocation (Alg. 5, A-15) and (iii) the joint-weight prefix for systematic resampling (Alg. 7, A-24).
+ * The cycle is therefore split into phases; between them the CALLER moves data between the contexts
+ * (NCCL send/recv and all-gathers in paper_1605_02406_b200/shard.py).  Philox counters use global
+ * particle / slot indices, so the union of the bands reproduces the whole-grid filter bit for bit.
+ *   dog_band.row0/row1      : rows [row0, row1) of this band; rank/world: band index and count (bands
+ *                             ordered bottom-up; rank 0 starts at row 0, the last ends at height).
+ *   dog_band.lo_row0/hi_row1: first row of the band below / end row of the band above (one-hop reach;
+ *                             particles predicted beyond it are counted in n_far and dropped).
+ *   dog_band.migrant_cap    : capacity, in particles, for migrants per direction per cycle.
+ * Call order per cycle: predict -> sizes -> buffers (+ caller's send/recv of the migrant records,
+ * 16 bytes (x, y, vx, vy) each, in the order given) -> assign -> (caller all-gathers *mass_dev over the
+ * bands into mass_all[world], device) -> joint -> (all-gather *weight_dev into weight_all[world]) ->
+ * resample.  Out-of-order calls return DOG_E_STATE.  Band contexts have no debug dumps (flags must be
+ * 0) and do not accept dog_step / dog_get_state particle arrays; m_F and readouts work as usual on
+ * the band's cells. */
+typedef struct {
+    int32_t row0, row1, rank, world, lo_row0, hi_row1;
+    uint32_t migrant_cap;
+} dog_band;
+int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+                    uint64_t seed, uint32_t flags, const dog_band* band, dog_ctx** out);
+/* phase 1: Alg. 1 for the own particles; migrants packed (device) for the neighbours. */
+int dog_band_predict(dog_ctx* ctx, float dt, void* stream);
+/* synchronises `stream`; migrant counts down/up, own particles of this cycle, far migrants so far.
+ * DOG_E_NOMEM if a direction overflowed migrant_cap (the cycle cannot be completed exactly). */
+int dog_band_sizes(dog_ctx* ctx, uint32_t* n_down, uint32_t* n_up, uint32_t* n_own, uint32_t* n_far, void* stream);
+/* device buffers: packed migrants to send down / up (float4 records, counts from dog_band_sizes) and
+ * where the n_lo / n_hi records received from the band below / above must be written (before assign). */
+int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** send_down, const float** send_up,
+                     float** recv_lo, float** recv_hi, void* stream);
+/* phase 2: tile sort of [from below | own | from above], Alg. 3 on the band; *mass_dev = this band's
+ * fixed-point born mass (device u64) to all-gather. */
+int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_dev, void* stream);
+/* phase 3: slots on the global born-mass CDF, joint CDF of the band; *weight_dev = its joint weight. */
+int dog_band_joint(dog_ctx* ctx, const uint64_t* mass_all_dev, const uint64_t** weight_dev, void* stream);
+/* phase 4: moments, resampling of the band's share [F(P'), F(P' + W_band)) of the global outputs, births. */
+int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream);
+/* synchronous: own particles of the current state (float4 records, host) and the global index of the
+ * first one; xyvv_host may be NULL to query the count. */
+int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n_own, uint64_t* global_first);
+
 /* dog_read_cells -- copy the readouts of the last completed cycle (posterior, before resampling,
  * P:1444) into caller DEVICE buffers (any may be NULL):
  *   occ[C] = m_O, free_mass[C] = m_F (Eq. 63); vel_mean[C][2] = (mean_vx, mean_vy) (Eq. 81);

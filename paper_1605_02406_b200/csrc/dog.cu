@@ -35,11 +35,20 @@ struct dog_ctx {
     uint64_t seed = 0;
     uint32_t flags = 0;
     int64_t nu = 0, nu_b = 0;
-    uint32_t C = 0;
+    uint32_t C = 0;             // cells of this context (its band)
+    uint32_t Cg = 0;            // cells of the whole grid
     int64_t k = 0;
     bool poisoned = false;
-    size_t nu_cap = 0;          // particle arrays padded to the sort tile
-    uint32_t tiles = 0, cell_blocks = 0, cell_chunk = 0, birth_blocks = 0;
+    // row band (a whole-grid context is the band [0, H) of a world of one)
+    int32_t row0 = 0, row1 = 0, rank = 0, world = 1;
+    uint32_t c_lo = 0, c_hi = 0;    // global cells of the neighbour bands
+    uint32_t lo_cap = 0, hi_cap = 0, own_cap = 0;   // particle slots: [lo | own | hi]
+    size_t nu_cap = 0;          // total particle slots (multiple of the sort tile)
+    uint32_t tiles = 0, own_tiles = 0, cell_blocks = 0, cell_chunk = 0, birth_blocks = 0;
+    Migrants mg{};              // band contexts: migrants packed for the neighbours
+    int phase = 0;              // band cycle: 0 idle, 1 predicted, 2 sizes read, 3 assigned, 4 joint
+    float band_dt = 0.0f;
+    uint32_t n_own_host = 0;
 
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
@@ -160,6 +169,14 @@ FilterConst filter_const(const dog_ctx* ctx)
     f.W = ctx->grid.width;
     f.H = ctx->grid.height;
     f.C = ctx->C;
+    f.Cg = ctx->Cg;
+    f.c_off = (uint32_t)ctx->row0 * (uint32_t)ctx->grid.width;
+    f.row0 = (uint32_t)ctx->row0;
+    f.lo_cap = ctx->lo_cap;
+    f.rank = (uint32_t)ctx->rank;
+    f.world = (uint32_t)ctx->world;
+    f.c_lo = ctx->c_lo;
+    f.c_hi = ctx->c_hi;
     f.nu = (uint32_t)ctx->nu;
     f.nu_b = (uint32_t)ctx->nu_b;
     f.p_s = ctx->params.p_s;
@@ -210,8 +227,8 @@ const char* dog_error_string(int s)
     }
 }
 
-int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
-               uint64_t seed, uint32_t flags, dog_ctx** out)
+static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+                       uint64_t seed, uint32_t flags, const dog_band* band, dog_ctx** out)
 {
     if (!grid || !params || !out) return DOG_E_INVAL;
     *out = nullptr;
@@ -227,6 +244,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         !(p.sigma_birth_vel >= 0.0f) || !finite(p.sigma_birth_vel) || !(p.free_tau > 0.0f) ||
         !(p.occ_max > 0.0f && p.occ_max <= 1.0f) || std::isnan(p.v_max))
         return DOG_E_INVAL;
+    if (band && (band->world < 1 || band->rank < 0 || band->rank >= band->world || band->row0 < 0 ||
+                 band->row1 <= band->row0 || band->row1 > grid->height || band->lo_row0 > band->row0 ||
+                 band->lo_row0 < 0 || band->hi_row1 < band->row1 || band->hi_row1 > grid->height ||
+                 (band->rank == 0) != (band->row0 == 0) || (band->rank == band->world - 1) != (band->row1 == grid->height) ||
+                 band->migrant_cap == 0 || band->migrant_cap >= (1u << 26)))
+        return DOG_E_INVAL;
 
     dog_ctx* ctx = new (std::nothrow) dog_ctx();
     if (!ctx) return DOG_E_NOMEM;
@@ -237,17 +260,30 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     ctx->flags = flags;
     ctx->nu = n_particles;
     ctx->nu_b = n_birth;
-    ctx->C = (uint32_t)C;
-    ctx->nu_cap = round_up((size_t)n_particles, kSortTile);
-    ctx->tiles = cdiv(n_particles, kSortTile);
+    ctx->Cg = (uint32_t)C;
+    if (band && band->world > 1) {
+        ctx->row0 = band->row0; ctx->row1 = band->row1; ctx->rank = band->rank; ctx->world = band->world;
+        ctx->lo_cap = ctx->hi_cap = (uint32_t)round_up(band->migrant_cap, kSortTile);
+        ctx->c_lo = (uint32_t)band->lo_row0 * (uint32_t)grid->width;
+        ctx->c_hi = (uint32_t)band->hi_row1 * (uint32_t)grid->width;
+    } else {
+        ctx->row0 = 0; ctx->row1 = grid->height; ctx->rank = 0; ctx->world = 1;
+        ctx->c_lo = 0; ctx->c_hi = (uint32_t)C;
+    }
+    ctx->C = (uint32_t)(ctx->row1 - ctx->row0) * (uint32_t)grid->width;
+    ctx->own_cap = (uint32_t)round_up((size_t)n_particles, kSortTile);
+    ctx->nu_cap = (size_t)ctx->lo_cap + ctx->own_cap + ctx->hi_cap;
+    ctx->tiles = (uint32_t)(ctx->nu_cap / kSortTile);
+    ctx->own_tiles = ctx->own_cap / kSortTile;
     {   // cell chunks of 2048 cells (at most kMaxCellBlocks chunks)
         uint32_t chunk = 2u * kCellIter;
-        uint32_t nblk = cdiv(C, chunk);
-        while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(C, chunk); }
+        uint32_t nblk = cdiv(ctx->C, chunk);
+        while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(ctx->C, chunk); }
         ctx->cell_chunk = chunk;
         ctx->cell_blocks = nblk;
     }
-    cudaFuncSetAttribute(k_predict_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
+    cudaFuncSetAttribute(k_predict_sort<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
+    cudaFuncSetAttribute(k_predict_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     if (const char* cv = getenv("DOG_RS_CARVEOUT")) {   // experiments: shared-memory share of the L1/smem array
@@ -281,7 +317,7 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
             return DOG_E_CUDA;
         }
     }
-    const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)C;
+    const size_t N = ctx->nu_cap, NB = (size_t)(n_birth > 0 ? n_birth : 1), Cs = (size_t)ctx->C;
     const bool dbg = (flags & DOG_FLAG_DEBUG) != 0;
 
     int rc = DOG_OK;
@@ -310,6 +346,12 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     AL(ctx->cell2list, Cs);
     AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
 
+    if (ctx->world > 1) {
+        for (int d = 0; d < 2; ++d) {
+            AL(ctx->mg.scr[d], ctx->own_cap); AL(ctx->mg.cnt[d], ctx->own_tiles); AL(ctx->mg.send[d], ctx->lo_cap);
+        }
+        ctx->mg.cap = ctx->lo_cap;
+    }
     AL(ctx->sc, 1);
 #undef AL
     if (rc != DOG_OK) {
@@ -318,7 +360,8 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
         return rc;
     }
 
-    // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0
+    // empty initial state (A-19): sentinel particles of weight 0, m_F = 0, k = 0 (a band context starts
+    // with no own particles: the sentinels contribute nothing to any band)
     std::vector<float4> sent(N, make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f));
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = cudaMemcpy(ctx->st, sent.data(), N * 16, cudaMemcpyHostToDevice);
@@ -328,6 +371,10 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     if (e == cudaSuccess) e = cudaMemset(ctx->mean, 0, Cs * 8);
     if (e == cudaSuccess) e = cudaMemset(ctx->cov, 0, Cs * 12);
     if (e == cudaSuccess) e = cudaMemset(ctx->sc, 0, sizeof(DevScalars));
+    if (e == cudaSuccess) {
+        const uint32_t own0[2] = {ctx->world > 1 ? 0u : (uint32_t)n_particles, ctx->world > 1 ? 0u : (uint32_t)n_particles};
+        e = cudaMemcpy(ctx->sc->n_own, own0, sizeof(own0), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaMemset(ctx->counts, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->npairs, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
@@ -341,6 +388,20 @@ int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const
     }
     *out = ctx;
     return DOG_OK;
+}
+
+int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+               uint64_t seed, uint32_t flags, dog_ctx** out)
+{
+    return create_impl(grid, n_particles, n_birth, params, seed, flags, nullptr, out);
+}
+
+int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+                    uint64_t seed, uint32_t flags, const dog_band* band, dog_ctx** out)
+{
+    if (!band) return DOG_E_INVAL;
+    if (flags & DOG_FLAG_DEBUG) return DOG_E_INVAL;   // stage dumps are whole-grid only
+    return create_impl(grid, n_particles, n_birth, params, seed, flags, band, out);
 }
 
 int dog_destroy(dog_ctx* ctx)
@@ -361,16 +422,89 @@ int dog_launches_per_step(dog_ctx* ctx)
     return ctx->nu_b > 0 ? 8 : 7;
 }
 
+// ---- the kernels of one cycle (shared by the whole-grid step and the band phases)
+static int L_predict_sort(dog_ctx* ctx, bool fused, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    if (fused)
+        CK(launch(k_predict_sort<true>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
+                  dbg ? ctx->keys : nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
+    else
+        CK(launch(k_predict_sort<false>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
+                  (uint32_t*)nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
+    return DOG_OK;
+}
+
+static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
+    CK(launch(k_cells, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
+              (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
+              ctx->cell_chunk, ctx->sc, fc, a.alpha));
+    return DOG_OK;
+}
+
+static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    CK(launch(k_list_scan, ctx->ls_cluster, kLsThreads, 0, st, ctx->ls_cluster, ctx->stage, ctx->list, ctx->bt,
+              ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, A_all, ctx->sc, fc, (int64_t)a.k));
+    return DOG_OK;
+}
+
+static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist,
+              ctx->C));
+    CK(launch(k_pair_sort, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all, ctx->sc,
+              fc, (int)(a.k & 1)));
+    return DOG_OK;
+}
+
+static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
+    const int par = (int)(a.k & 1);
+    if (dbg)
+        CK(launch(k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
+                  ctx->tp, (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
+                  (const DevScalars*)ctx->sc, fc, par));
+    else
+        CK(launch(k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
+                  ctx->tp, (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
+                  (const DevScalars*)ctx->sc, fc, par));
+    return DOG_OK;
+}
+
+static int L_moments(dog_ctx* ctx, cudaStream_t st)
+{
+    CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
+              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc));
+    return DOG_OK;
+}
+
+static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+{
+    if (ctx->nu_b == 0) return DOG_OK;
+    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
+    NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
+    BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
+    CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
+              (int64_t)a.k));
+    return DOG_OK;
+}
+
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
 {
     if (!ctx || !meas) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1) return DOG_E_STATE;                 // band contexts run the dog_band_* phases
     if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
     if (int r = set_device(ctx)) return r;
     cudaStream_t st = (cudaStream_t)stream;
     const StepArgs a = step_args(ctx, dt);
     const FilterConst fc = filter_const(ctx);
-    const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
 
     const bool prof = ctx->prof_steps < ctx->prof_max;
     int mark_i = 0;
@@ -380,49 +514,24 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         return cudaEventRecord(ctx->pev[(size_t)ctx->prof_steps * (DOG_MAX_STAGES + 1) + mark_i++], st);
     };
     CK(mark(nullptr));
-    const uint32_t T = ctx->tiles;
-
     // 1-2. predict (Alg. 1) fused with the tile-local stable sort (Alg. 2): runs, per-cell counts
-    CK(launch(k_predict_sort, T, kPsThreads, kPsSmemBytes, st, 0, ctx->st, ctx->pst, dbg ? ctx->keys : nullptr,
-              ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
+    if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
     CK(mark("predict_sort"));
-
     // 3. cells: DS predict/update, birth split, fixed point, active-cell staging (Alg. 3)
-    CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
-    CK(launch(k_cells, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
-              (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-              ctx->cell_chunk, ctx->sc, fc, a.alpha));
+    if (int r = L_cells(ctx, meas, a, fc, st)) return r;
     CK(mark("cells"));
-
     // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
-    CK(launch(k_list_scan, ctx->ls_cluster, kLsThreads, 0, st, ctx->ls_cluster, ctx->stage, ctx->list, ctx->bt,
-              ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, ctx->sc, fc, (int64_t)a.k));
+    if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
     CK(mark("list_scan"));
-
-    // 5. each cell's runs in tile order -> stable within-cell ranks
-    CK(launch(k_pair_fill, T, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist, ctx->C));
-    CK(launch(k_pair_sort, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp,
-              (const DevScalars*)ctx->sc));
+    // 5. each cell's runs in tile order -> stable within-cell ranks; global totals (w_bar)
+    if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
     CK(mark("pairs"));
-
     // 6. persistent particles: moments + resampling copies; births
-    NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
-    if (dbg)
-        CK(launch(k_resample_tiles<true>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                  (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg, (const DevScalars*)ctx->sc, fc));
-    else
-        CK(launch(k_resample_tiles<false>, T, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                  (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
-                  (const DevScalars*)ctx->sc, fc));
+    if (int r = L_resample(ctx, a, fc, st)) return r;
     CK(mark("resample"));
-    CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
-              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc));
+    if (int r = L_moments(ctx, st)) return r;
     CK(mark("moments"));
-    if (ctx->nu_b > 0) {
-        BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-        CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
-                  (int64_t)a.k));
-    }
+    if (int r = L_births(ctx, a, fc, st)) return r;
     CK(mark("births"));
     if (prof) {
         ctx->prof_nst = mark_i - 1;
@@ -430,6 +539,129 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     }
     ctx->k += 1;
     return DOG_OK;
+}
+
+// ---- row-band contexts: the cycle in four phases with the caller's exchanges in between
+int dog_band_predict(dog_ctx* ctx, float dt, void* stream)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world < 2 || ctx->phase != 0) return DOG_E_STATE;
+    if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    ctx->band_dt = dt;
+    const StepArgs a = step_args(ctx, dt);
+    const FilterConst fc = filter_const(ctx);
+    CK(launch(k_predict_band, ctx->own_tiles, kPsThreads, 0, st, 0, (const float4*)ctx->st, ctx->pst, ctx->mg,
+              ctx->sc, fc, a));
+    CK(launch(k_pack_migrants, 1, 1024, 0, st, 0, ctx->mg, ctx->own_tiles, ctx->sc));
+    ctx->phase = 1;
+    return DOG_OK;
+}
+
+int dog_band_sizes(dog_ctx* ctx, uint32_t* n_down, uint32_t* n_up, uint32_t* n_own, uint32_t* n_far, void* stream)
+{
+    if (!ctx || !n_down || !n_up || !n_own) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 1) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    DevScalars s;
+    CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+    *n_down = s.mig_cnt[0];
+    *n_up = s.mig_cnt[1];
+    *n_own = s.n_own[ctx->k & 1];
+    if (n_far) *n_far = s.far;
+    ctx->n_own_host = *n_own;
+    ctx->phase = 2;
+    if (s.mig_cnt[0] > ctx->mg.cap || s.mig_cnt[1] > ctx->mg.cap) return DOG_E_NOMEM;   // migrant capacity
+    return DOG_OK;
+}
+
+int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** send_down, const float** send_up,
+                     float** recv_lo, float** recv_hi, void* stream)
+{
+    if (!ctx || !send_down || !send_up || !recv_lo || !recv_hi) return DOG_E_INVAL;
+    if (ctx->phase != 2) return DOG_E_STATE;
+    if (n_lo > ctx->lo_cap || n_hi > ctx->hi_cap || (ctx->rank == 0 && n_lo) || (ctx->rank == ctx->world - 1 && n_hi))
+        return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    const uint32_t nn[2] = {n_lo, n_hi};
+    CK(cudaMemcpyAsync(&ctx->sc->n_lo, nn, sizeof(nn), cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));   // nn lives on this stack frame
+    *send_down = (const float*)ctx->mg.send[0];
+    *send_up = (const float*)ctx->mg.send[1];
+    *recv_lo = (float*)(ctx->pst + ctx->lo_cap - n_lo);
+    *recv_hi = (float*)(ctx->pst + ctx->lo_cap + ctx->n_own_host);
+    return DOG_OK;
+}
+
+int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_dev, void* stream)
+{
+    if (!ctx || !meas_band || !mass_dev) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 2) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const StepArgs a = step_args(ctx, ctx->band_dt);
+    const FilterConst fc = filter_const(ctx);
+    if (int r = L_predict_sort(ctx, false, a, fc, st)) return r;
+    if (int r = L_cells(ctx, meas_band, a, fc, st)) return r;
+    *mass_dev = &ctx->sc->A_acc;
+    ctx->phase = 3;
+    return DOG_OK;
+}
+
+int dog_band_joint(dog_ctx* ctx, const uint64_t* mass_all_dev, const uint64_t** weight_dev, void* stream)
+{
+    if (!ctx || !mass_all_dev || !weight_dev) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 3) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const StepArgs a = step_args(ctx, ctx->band_dt);
+    const FilterConst fc = filter_const(ctx);
+    if (int r = L_list_scan(ctx, mass_all_dev, a, fc, st)) return r;
+    *weight_dev = &ctx->sc->W;
+    ctx->phase = 4;
+    return DOG_OK;
+}
+
+int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream)
+{
+    if (!ctx || !weight_all_dev) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 4) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const StepArgs a = step_args(ctx, ctx->band_dt);
+    const FilterConst fc = filter_const(ctx);
+    if (int r = L_pairs(ctx, weight_all_dev, a, fc, st)) return r;
+    if (int r = L_resample(ctx, a, fc, st)) return r;
+    if (int r = L_moments(ctx, st)) return r;
+    if (int r = L_births(ctx, a, fc, st)) return r;
+    ctx->phase = 0;
+    ctx->k += 1;
+    return DOG_OK;
+}
+
+int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n_own, uint64_t* global_first)
+{
+    if (!ctx || !n_own) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaDeviceSynchronize());
+    DevScalars s;
+    CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+    const int par = (int)(ctx->k & 1);
+    *n_own = s.n_own[par];
+    if (global_first) *global_first = s.o_base[par];
+    if (xyvv_host) {
+        if (cap < *n_own) return DOG_E_INVAL;
+        if (*n_own) CK(cudaMemcpy(xyvv_host, ctx->st + ctx->lo_cap, (size_t)*n_own * 16, cudaMemcpyDeviceToHost));
+    }
+    return report_meas(ctx);
 }
 
 int dog_profile_begin(dog_ctx* ctx, int max_steps)
@@ -520,6 +752,7 @@ int dog_get_state(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float*
                   int64_t* k)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (ctx->world > 1 && (x || y || vx || vy)) return DOG_E_STATE;   // band particles: dog_band_particles
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaDeviceSynchronize());
@@ -537,6 +770,7 @@ int dog_set_state(dog_ctx* ctx, const float* x, const float* y, const float* vx,
 {
     if (!ctx || !x || !y || !vx || !vy || !m_free || !(w_bar >= 0.0f) || !finite(w_bar) || k < 0)
         return DOG_E_INVAL;
+    if (ctx->world > 1) return DOG_E_STATE;
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaDeviceSynchronize());
@@ -553,6 +787,7 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
 {
     if (!ctx || !host_dst) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1 && what != DOG_DBG_SCALARS) return DOG_E_STATE;
     if (int r = set_device(ctx)) return r;
     CK(cudaDeviceSynchronize());
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;

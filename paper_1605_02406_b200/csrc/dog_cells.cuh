@@ -244,6 +244,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         bt.n0[blockIdx.x] = N;
         bt.rb0[blockIdx.x] = A;
         if (b) atomicAdd(&sc->meas_bad, b);
+        if (A) atomicAdd((unsigned long long*)&sc->A_acc, (unsigned long long)A);   // integer: order-free
     }
 }
 
@@ -354,8 +355,11 @@ __device__ __forceinline__ ulonglong2 cluster_offsets(ulonglong2 t, ulonglong2* 
     return make_ulonglong2(cb.x + w.x, cb.y + w.y);
 }
 
+// A_all: born mass of every shard (band contexts, gathered after k_cells), or nullptr (whole grid): the
+// slots of the band's cells are allocated on the GLOBAL born-mass CDF (prefix of the shards below).
 __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList L, BlockTotals bt, uint32_t nblk,
                                                           uint32_t chunk, uint32_t* __restrict__ cell2list,
+                                                          const uint64_t* __restrict__ A_all,
                                                           DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
 {
     PDL_ENTER();
@@ -370,7 +374,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
     // chunk offsets (exclusive prefix of the staged counts) and the grand totals n_in, A -- every CTA
     // forms them itself from k_cells' per-chunk totals (nblk <= 4096: four per thread)
     uint32_t Lc;
-    uint64_t A, N;
+    uint64_t A, N, Apre = 0;
     {
         constexpr int kI = (kMaxCellBlocks + kLsThreads - 1) / kLsThreads;
         uint32_t cv[kI];
@@ -396,6 +400,12 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
         const ulonglong2 t2 = cta_excl_scan2(make_ulonglong2(as, ns), s_w, off);
         A = t2.x;
         N = t2.y;
+        if (A_all) {                                        // global born-mass CDF over the shards
+            uint64_t pre = 0, tot_all = 0;
+            for (uint32_t r = 0; r < fc.world; ++r) { if (r < fc.rank) pre += A_all[r]; tot_all += A_all[r]; }
+            Apre = pre;
+            A = tot_all;
+        }
         if (tid == 0) {
             s_cnt0[nblk] = Lc;
             if (rank == 0) { sc->Lc = Lc; sc->A = A; sc->n_in = N; }
@@ -405,7 +415,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
     const double rcpA = A ? 1.0 / (double)A : 0.0;
     __syncthreads();
     const uint32_t cap = nc * kLsThreads * kLsItems;
-    ulonglong2 carry1 = make_ulonglong2(0ull, 0ull), carry2 = carry1;
+    ulonglong2 carry1 = make_ulonglong2(0ull, Apre), carry2 = make_ulonglong2(0ull, 0ull);
     for (uint32_t r0 = 0; r0 < Lc; r0 += cap) {
         const uint32_t gw = r0 + rank * (kLsThreads * kLsItems) + warp * (32 * kLsItems) + lane;   // + 32 i
         uint32_t c[kLsItems], n[kLsItems], npv[kLsItems];
@@ -474,12 +484,10 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
             const uint32_t it0 = (uint32_t)(base2.y + exI[i]);
             L.P[g] = P;
             L.it[g] = it0;
-            if (g == Lc - 1) {   // the list's last entry publishes the totals
-                const uint64_t W = P + J[i];
-                sc->W = W;
+            if (g == Lc - 1) {   // the list's last entry publishes the totals (this context's W)
+                sc->W = P + J[i];
                 sc->n_items = it0 + (uint32_t)its[i];
                 sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
-                sc->w_bar = W ? __double2float_rn(__ddiv_rn(__dmul_rn((double)W, 0x1p-40), (double)fc.nu)) : 0.0f;
                 sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
             }
         }
@@ -487,7 +495,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
         carry2.x += tot2.x; carry2.y += tot2.y;
     }
     if (Lc == 0 && rank == 0 && tid == 0) {   // empty list (A-26)
-        sc->W = 0; sc->n_items = 0; sc->s_total = 0; sc->w_bar = 0.0f;
+        sc->W = 0; sc->n_items = 0; sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
         sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
     }
     cluster.sync();   // no CTA leaves while another may still read its shared memory

@@ -18,6 +18,16 @@ struct DevScalars {
     uint64_t s_total;    // birth slots allocated (nu_b or 0)
     uint32_t n_items;    // birth work items of the cycle
     uint32_t Lc;         // entries of the active-cell list
+    // Local particle array = [migrants from the shard below | own particles | migrants from above]
+    // (row-band contexts; a whole-grid context has only own particles).
+    uint32_t n_lo, n_hi;         // migrants received this cycle
+    uint32_t n_own[2];           // own particles, indexed by cycle parity
+    uint64_t o_base[2];          // global index of the first own particle (Philox counter base), by parity
+    uint64_t A_acc;              // this context's born mass (k_cells atomics; shared over shards)
+    uint64_t Wtot, Ppre;         // joint weight over all shards, joint prefix of the shards below
+    uint32_t mig_cnt[2];         // migrants leaving down / up this cycle
+    uint32_t far;                // migrants that would need more than one hop (dropped, counted)
+    uint32_t pad2;
 };
 
 constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
@@ -35,7 +45,13 @@ struct StepArgs {
 
 struct FilterConst {
     int32_t W, H;
-    uint32_t C;
+    uint32_t C;          // cells of this context (the band; the whole grid for a whole-grid context)
+    uint32_t Cg;         // cells of the whole grid (key of a particle outside the grid)
+    uint32_t c_off;      // global index of the context's first cell (row0 * W)
+    uint32_t row0;       // first grid row of the context
+    uint32_t lo_cap;     // particle slots reserved before the own region (migrants from below)
+    uint32_t rank, world;
+    uint32_t c_lo, c_hi; // global cells of the neighbour bands [c_lo, c_hi) (one-hop migration reach)
     uint32_t nu, nu_b;
     float p_s, p_b, sigma_b, occ_max, v_max;
     uint64_t seed;

@@ -23,48 +23,6 @@ namespace dog {
 
 struct MomPartial { double s[5]; };
 
-struct RsConst {
-    uint64_t W;
-    uint32_t U, nu;
-    double nu_over_W;  // nu / W  (fp64)
-    double U_frac;     // U 2^-32  (exact)
-    u128 UW;           // U * W
-};
-
-__device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t nu)
-{
-    RsConst r;
-    r.W = sc->W;
-    r.U = sc->U;
-    r.nu = nu;
-    r.nu_over_W = r.W ? (double)nu / (double)r.W : 0.0;
-    r.U_frac = (double)r.U * 0x1p-32;
-    r.UW = (u128)r.U * (u128)r.W;
-    return r;
-}
-
-// F(X) = number of systematic targets t_i below X = clamp(ceil(y), 0, nu) with
-// y = (X nu 2^32 - U W) / (W 2^32) = X nu / W - U 2^-32.  The fp64 estimate of y is within 2^-20
-// of y (|y| < 2^31, relative error < 2^-51); when it is further than 2^-16 from an integer its
-// ceiling is exact, otherwise the ceiling is settled with exact 128-bit products.
-__device__ __forceinline__ uint32_t fcount(uint64_t X, const RsConst& r)
-{
-    const double y = __fma_rn((double)X, r.nu_over_W, -r.U_frac);
-    if (y <= -0.5) return 0u;
-    if (y >= (double)r.nu) return r.nu;
-    const double cy = ceil(y);
-    const double d = cy - y;                       // in [0, 1)
-    if (d > 0x1p-16 && d < 1.0 - 0x1p-16) return (uint32_t)cy;
-    const u128 num0 = ((u128)X * (u128)r.nu) << 32;
-    if (num0 <= r.UW) return 0u;
-    const u128 num = num0 - r.UW;
-    const u128 E = ((u128)r.W) << 32;
-    uint64_t q = (uint64_t)fmax(cy - 1.0, 0.0);
-    while ((u128)q * E < num) ++q;                 // smallest q with q W 2^32 >= X nu 2^32 - U W
-    while (q > 0 && (u128)(q - 1) * E >= num) --q;
-    return (uint32_t)(q < r.nu ? q : r.nu);
-}
-
 // Moments of cell c from its velocity sums (Eqs. 81-84 with the uniform weight w' = rho_p / S w_pred).
 __device__ __forceinline__ void finalize_cell(uint32_t c, double s0, double s1, double s2, double s3, double s4,
                                               uint32_t n, float rp, float w_pred, float2* __restrict__ mean,
@@ -219,21 +177,25 @@ template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
     uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
-    const DevScalars* __restrict__ sc, FilterConst fc)
+    const DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31;
-    const uint32_t t = blockIdx.x, base = t * kSortTile;
+    const uint32_t t = blockIdx.x, base = t * kSortTile;     // this tile's slot in the per-tile arrays
     const RsConst rc = make_rsconst(sc, fc.nu);
-    if (rc.W == 0) {   // empty world (A-26): every next particle goes to the sentinel
+    const uint32_t n_lo = sc->n_lo, n_loc = n_lo + sc->n_own[par] + sc->n_hi;
+    const uint32_t pbase = fc.lo_cap - n_lo + base;                // its first particle
+    // next-cycle own particles start at lo_cap: global output o -> slot lo_cap + o - F(P'_shard)
+    out.s += fc.lo_cap - sc->o_base[par ^ 1];
+    if (rc.W == 0 && fc.world == 1) {   // empty world (A-26): every next particle goes to the sentinel
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x) {
             out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
             if (kDbg) out.jidx[i] = 0xFFFFFFFFu;
         }
     }
-    const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
+    const uint32_t n = n_loc > base ? min((uint32_t)kSortTile, n_loc - base) : 0u;
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const uint32_t p0 = tid * kRtItems;
@@ -283,7 +245,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 const uint4 a = reinterpret_cast<const uint4*>(S.lp + p0)[h];
                 const uint32_t w[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u) { src[2 * u] = base + (w[u] & 0xFFFFu); src[2 * u + 1] = base + (w[u] >> 16); }
+                for (int u = 0; u < 4; ++u) { src[2 * u] = pbase + (w[u] & 0xFFFFu); src[2 * u + 1] = pbase + (w[u] >> 16); }
             }
             float2 V[8];
 #pragma unroll
@@ -454,7 +416,7 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
                 const uint32_t p = (uint32_t)os[ok[h] ? i : 0u] - 1u;
                 const uint32_t j = S.runof[p];
                 o[h] = w0 + i + runf(j).D;
-                src[h] = base + S.lp[p];
+                src[h] = pbase + S.lp[p];
                 J[h] = 0;
                 if (kDbg) { const RunInfo q = runs[j]; J[h] = q.jbase + q.pre + (p - S.first[j]); }
             }
@@ -515,6 +477,9 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
     PDL_ENTER();
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu);
+    const int par = (int)(k & 1);
+    out.s += fc.lo_cap - sc->o_base[par ^ 1];                     // global output -> local slot
+    const uint64_t Ppre = sc->Ppre;                                // joint prefix of the shards below
     const uint32_t n_items = sc->n_items, Lc = sc->Lc;
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
@@ -526,13 +491,14 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
     uint32_t sub = q - L.it[li];
     while (true) {
         const uint32_t c = L.c[li], n = L.n[li], start = L.start[li], nb = L.nb[li];
-        const uint64_t P = L.P[li];
+        const uint64_t P = Ppre + L.P[li];
         const uint32_t r0 = sub * kItem, m = min(kItem, nb - r0);
         const uint64_t bb = L.bb[li];
         const uint32_t rbm = L.rb[li], sb = L.sb[li];
         const uint64_t PB = P + L.Rp[li];
         const uint32_t jbase = start + sb + n;
-        const uint32_t col = c % (uint32_t)fc.W, row = c / (uint32_t)fc.W;
+        const uint32_t cg = c + fc.c_off;                             // global cell
+        const uint32_t col = cg % (uint32_t)fc.W, row = cg / (uint32_t)fc.W;
         const float colf = (float)col, rowf = (float)row;
         const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
         for (uint32_t t = 0; t < m; t += 32) {

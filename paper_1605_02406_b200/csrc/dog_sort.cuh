@@ -18,6 +18,7 @@
 #include <cstdint>
 #include "dog_cells.cuh"
 #include "dog_common.cuh"
+#include "dog_fcount.cuh"
 #include "dog_kernels.cuh"
 #include "dog_rng.cuh"
 
@@ -61,7 +62,38 @@ struct PsSmem {
 };
 constexpr size_t kPsSmemBytes = sizeof(PsSmem);
 
+// One particle of Alg. 1: p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v.  The
+// four normals come from one Philox4x32-10 draw keyed by the particle's GLOBAL index (A-20), so a band
+// context predicts exactly what a whole-grid context predicts for the same particle.
+__device__ __forceinline__ float4 predict_one(float4 X, uint64_t gidx, const FilterConst& fc, const StepArgs& a)
+{
+    const Philox4 r = draw(fc.seed, (uint32_t)gidx, a.k, STAGE_PREDICT);
+    float n0, n1, n2, n3;
+    box_muller(r.r0, r.r1, n0, n1);
+    box_muller(r.r2, r.r3, n2, n3);
+    const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(X.z, a.Tc, X.x));
+    const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(X.w, a.Tc, X.y));
+    return make_float4(xn, yn, __fmaf_rn(a.s_v, n2, X.z), __fmaf_rn(a.s_v, n3, X.w));
+}
+
+// Global cell key of a predicted particle: row * W + col inside the grid, Cg outside (A-4, A-5).
+__device__ __forceinline__ uint32_t global_key(float4 P, const FilterConst& fc)
+{
+    const bool inside = (P.x >= 0.0f) && (P.x < (float)fc.W) && (P.y >= 0.0f) && (P.y < (float)fc.H);
+    return inside ? (uint32_t)__float2int_rz(P.y) * (uint32_t)fc.W + (uint32_t)__float2int_rz(P.x) : fc.Cg;
+}
+
+// Context-local key: the cell within this context's band, C for anything outside it.
+__device__ __forceinline__ uint32_t local_key(uint32_t kg, const FilterConst& fc)
+{
+    return (kg >= fc.c_off && kg - fc.c_off < fc.C) ? kg - fc.c_off : fc.C;
+}
+
+// Tiles cover the local particle array [s0, s0 + n_loc), s0 = lo_cap - n_lo (DevScalars).  kPredict:
+// whole-grid context, predict + sort fused (own particles only).  !kPredict: band context, the tile's
+// particles were predicted by k_predict_band (own) or by the neighbour shard (migrants): keys only.
 // Warp w owns positions [512 w, 512 w + 512) as 16 rows of 32 lanes (position = 512 w + 32 i + lane).
+template <bool kPredict>
 __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     const float4* __restrict__ st, float4* __restrict__ pst, uint32_t* __restrict__ keys_dbg,
     uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs,
@@ -72,15 +104,21 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     PsSmem& S = *reinterpret_cast<PsSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    const uint32_t base = blockIdx.x * kSortTile;
-    const uint32_t n = fc.nu > base ? min((uint32_t)kSortTile, fc.nu - base) : 0u;
-    const float w_bar = sc->w_bar;
-    const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
-    if (blockIdx.x == 0 && tid == 0) sc->w_pred = w_pred;
-    const float Wf = (float)fc.W, Hf = (float)fc.H;
+    const int par = (int)(a.k & 1);
+    const uint32_t n_lo = sc->n_lo, n_own = sc->n_own[par], n_loc = n_lo + n_own + sc->n_hi;
+    const uint64_t o_base = sc->o_base[par];
+    const uint32_t s0 = fc.lo_cap - n_lo;
+    const uint32_t tb = blockIdx.x * kSortTile;                // this tile's slot in the per-tile arrays
+    const uint32_t base = s0 + tb;                             // its first particle
+    const uint32_t n = n_loc > tb ? min((uint32_t)kSortTile, n_loc - tb) : 0u;
+    if (kPredict) {
+        const float w_bar = sc->w_bar;
+        const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
+        if (blockIdx.x == 0 && tid == 0) { sc->w_pred = w_pred; sc->A_acc = 0ull; }
+    }
 
     PHASE_BEGIN();
-    // ---- predict (Alg. 1): position p = local index (input order)
+    // ---- predict (Alg. 1) or load: position p = local index (input order)
     uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
 #pragma unroll 2
     for (int i = 0; i < kPsRows; ++i) {
@@ -88,20 +126,16 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
         uint32_t key = 0xFFFFFFFFu;
         if (p < n) {
             const uint32_t g = base + p;
-            const float4 X = st[g];
-            const Philox4 r = draw(fc.seed, g, a.k, STAGE_PREDICT);
-            float n0, n1, n2, n3;
-            box_muller(r.r0, r.r1, n0, n1);
-            box_muller(r.r2, r.r3, n2, n3);
-            // p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v
-            const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(X.z, a.Tc, X.x));
-            const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(X.w, a.Tc, X.y));
-            const float vxn = __fmaf_rn(a.s_v, n2, X.z);
-            const float vyn = __fmaf_rn(a.s_v, n3, X.w);
-            const bool inside = (xn >= 0.0f) && (xn < Wf) && (yn >= 0.0f) && (yn < Hf);
-            key = inside ? (uint32_t)__float2int_rz(yn) * (uint32_t)fc.W + (uint32_t)__float2int_rz(xn) : fc.C;  // A-4, A-5
-            pst[g] = make_float4(xn, yn, vxn, vyn);
-            if (keys_dbg) keys_dbg[g] = key;
+            float4 P;
+            if (kPredict) {
+                P = predict_one(st[g], o_base + (g - fc.lo_cap), fc, a);
+                pst[g] = P;
+            } else {
+                P = pst[g];
+            }
+            const uint32_t kg = global_key(P, fc);
+            if (keys_dbg) keys_dbg[g] = kg;
+            key = local_key(kg, fc);
             kmin = min(kmin, key);
             kmax = max(kmax, key);
         }
@@ -117,7 +151,10 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     kmin = S.mn[0]; kmax = S.mx[0];
 #pragma unroll
     for (int w = 1; w < kPsWarps; ++w) { kmin = min(kmin, S.mn[w]); kmax = max(kmax, S.mx[w]); }
-    if (n == 0) return;
+    if (n == 0) {                                           // beyond the particles of this cycle
+        if (tid == 0) tp.nd[blockIdx.x] = 0u;
+        return;
+    }
     PHASE_MARK(8);
     const uint32_t range = kmax - kmin;
     const int bits = range ? 32 - __clz(range) : 0;
@@ -192,9 +229,9 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     for (uint32_t r = tid; r < nd; r += kPsThreads) {
         const uint32_t f = s_start[r], e = r + 1 < nd ? (uint32_t)s_start[r + 1] : n, c = e - f;
         const uint32_t key = sk[f];
-        tp.key[base + r] = key;
-        tp.first[base + r] = (uint16_t)f;
-        tp.cnt[base + r] = (uint16_t)(c - 1);
+        tp.key[tb + r] = key;
+        tp.first[tb + r] = (uint16_t)f;
+        tp.cnt[tb + r] = (uint16_t)(c - 1);
         if (key < fc.C) {
             atomicAdd(&counts[key], c);
             atomicAdd(&npairs[key], 1u);
@@ -206,9 +243,112 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
         const uint32_t p = 2 * q;
         const uint32_t v0 = identity ? p : sv[p], v1 = identity ? p + 1 : sv[p + 1];
-        reinterpret_cast<uint32_t*>(lperm + base)[q] = v0 | (v1 << 16);
+        reinterpret_cast<uint32_t*>(lperm + tb)[q] = v0 | (v1 << 16);
     }
     PHASE_MARK(11);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Row-band contexts: Alg. 1 for the own particles, then the particles whose
+// new cell lies in the band below / above are packed, in input (= global index) order, for the
+// neighbour shards.  Their slots in the local array keep them with a key outside the band, so the
+// local sort leaves them out (like particles outside the grid).
+// ------------------------------------------------------------------------------------------------
+struct Migrants {
+    float4* scr[2];        // per tile, compacted: [tile * 4096 + k]
+    uint32_t* cnt[2];      // per tile
+    float4* send[2];       // packed for the neighbours (capacity cap)
+    uint32_t cap;
+};
+
+__global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __restrict__ st, float4* __restrict__ pst,
+                                                             Migrants mg, DevScalars* __restrict__ sc, FilterConst fc,
+                                                             StepArgs a)
+{
+    PDL_ENTER();
+    __shared__ uint32_t s_w[2][kPsWarps + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int par = (int)(a.k & 1);
+    const uint32_t n_own = sc->n_own[par];
+    const uint64_t o_base = sc->o_base[par];
+    const uint32_t tb = blockIdx.x * kSortTile;
+    const uint32_t n = n_own > tb ? min((uint32_t)kSortTile, n_own - tb) : 0u;
+    if (blockIdx.x == 0 && tid == 0) {
+        sc->w_pred = __fmul_rn(fc.p_s, sc->w_bar);         // Eq. 39 (A-3)
+        sc->A_acc = 0ull;
+    }
+    float4 P[kPsRows];
+    uint32_t dir[kPsRows];                                  // 0 down, 1 up, 2 stays
+    uint32_t wc[2] = {0, 0};
+#pragma unroll
+    for (int i = 0; i < kPsRows; ++i) {
+        const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+        dir[i] = 2u;
+        if (p < n) {
+            const uint32_t q = fc.lo_cap + tb + p;
+            P[i] = predict_one(st[q], o_base + tb + p, fc, a);
+            pst[q] = P[i];
+            const uint32_t kg = global_key(P[i], fc);
+            if (kg < fc.Cg && kg < fc.c_off) dir[i] = 0u;
+            else if (kg < fc.Cg && kg - fc.c_off >= fc.C) dir[i] = 1u;
+            if (dir[i] < 2u && (kg < fc.c_lo || kg >= fc.c_hi)) atomicAdd(&sc->far, 1u);   // beyond the neighbour
+        }
+#pragma unroll
+        for (int d = 0; d < 2; ++d) wc[d] += __popc(__ballot_sync(0xffffffffu, dir[i] == (uint32_t)d));
+    }
+    if (lane == 0) { s_w[0][warp] = wc[0]; s_w[1][warp] = wc[1]; }
+    __syncthreads();
+    uint32_t off[2] = {0, 0}, tot[2] = {0, 0};
+#pragma unroll
+    for (int w = 0; w < kPsWarps; ++w)
+#pragma unroll
+        for (int d = 0; d < 2; ++d) { if (w < warp) off[d] += s_w[d][w]; tot[d] += s_w[d][w]; }
+#pragma unroll
+    for (int i = 0; i < kPsRows; ++i) {
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+            const uint32_t b = __ballot_sync(0xffffffffu, dir[i] == (uint32_t)d);
+            if (dir[i] == (uint32_t)d) mg.scr[d][tb + off[d] + __popc(b & lt)] = P[i];
+            off[d] += __popc(b);
+        }
+    }
+    if (tid < 2) mg.cnt[tid][blockIdx.x] = tot[tid];
+}
+
+// One block: exclusive prefix of the per-tile migrant counts, then the packed send buffers (input
+// order); counts go to DevScalars (read by the host to size the exchange).
+__global__ __launch_bounds__(1024) void k_pack_migrants(Migrants mg, uint32_t tiles, DevScalars* __restrict__ sc)
+{
+    PDL_ENTER();
+    __shared__ uint32_t s_run[2];
+    __shared__ uint32_t s_w[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int d = 0; d < 2; ++d) {
+        if (tid == 0) s_run[d] = 0u;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < tiles; t0 += 1024) {
+            const uint32_t t = t0 + tid;
+            const uint32_t c = t < tiles ? mg.cnt[d][t] : 0u;
+            const uint32_t inc = warp_incl_scan(c, lane);
+            if (lane == 31) s_w[warp] = inc;
+            __syncthreads();
+            if (warp == 0) {
+                const uint32_t v = s_w[lane];
+                const uint32_t vi = warp_incl_scan(v, lane);
+                s_w[lane] = vi - v;
+                if (lane == 31) s_w[32] = vi;
+            }
+            __syncthreads();
+            const uint32_t dst0 = s_run[d] + s_w[warp] + inc - c;
+            for (uint32_t k = 0; k < c; ++k)               // migrants are ~1 %: a short serial copy per tile
+                if (dst0 + k < mg.cap) mg.send[d][dst0 + k] = mg.scr[d][t * kSortTile + k];
+            __syncthreads();
+            if (tid == 0) s_run[d] += s_w[32];
+            __syncthreads();
+        }
+        if (tid == 0) sc->mig_cnt[d] = s_run[d];
+    }
 }
 
 // Each pair appends itself (tile << 12 | run) to its cell's list (unordered; k_pair_sort orders it).
@@ -233,8 +373,13 @@ __global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, con
 // staged in shared memory and sorted by rank-by-count (entries are distinct, lists are short).
 constexpr int kPsGroup = 8, kPsBuf = 128;
 
+// W_all: joint weight of every shard (band contexts, gathered after k_list_scan) or nullptr (whole grid).
+// Block 0 also publishes the cycle's global totals: W over all shards, the joint prefix of the shards
+// below, w_bar = W 2^-40 / nu (Eq. 57), and -- band contexts -- the next cycle's own particles: the
+// global outputs [F(P'), F(P' + W_local)) (A-24).
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
-                                                   uint32_t* __restrict__ ptmp, const DevScalars* __restrict__ sc)
+                                                   uint32_t* __restrict__ ptmp, const uint64_t* __restrict__ W_all,
+                                                   DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
@@ -242,11 +387,32 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     const uint32_t gmask = 0xFFu << (lane & ~(kPsGroup - 1));
     const uint32_t Lc = sc->Lc;
     const uint32_t ng = (gridDim.x * blockDim.x) / kPsGroup;
+    uint64_t Ppre = 0, Wtot = sc->W;
+    if (W_all) {
+        Wtot = 0;
+        for (uint32_t r = 0; r < fc.world; ++r) { if (r < fc.rank) Ppre += W_all[r]; Wtot += W_all[r]; }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->Wtot = Wtot;
+        sc->Ppre = Ppre;
+        sc->w_bar = Wtot ? __double2float_rn(__ddiv_rn(__dmul_rn((double)Wtot, 0x1p-40), (double)fc.nu)) : 0.0f;
+        if (W_all) {
+            RsConst r;
+            r.W = Wtot; r.U = sc->U; r.nu = fc.nu;
+            r.nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
+            r.U_frac = (double)r.U * 0x1p-32;
+            r.UW = (u128)r.U * (u128)Wtot;
+            const uint32_t f0 = Wtot ? fcount(Ppre, r) : 0u;
+            const uint32_t f1 = Wtot ? fcount(Ppre + sc->W, r) : 0u;
+            sc->o_base[par ^ 1] = f0;
+            sc->n_own[par ^ 1] = f1 - f0;
+        }
+    }
     for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) / kPsGroup; li < Lc; li += ng) {
         const uint32_t m = L.np[li];
         if (m == 0) continue;
         RunInfo ri;
-        ri.P = L.P[li];
+        ri.P = Ppre + L.P[li];
         ri.bp = L.bp[li];
         ri.rpm = L.rp[li];
         ri.pre = 0u;

@@ -43,7 +43,13 @@ class dog_params(C.Structure):
                 ("v_max", C.c_float)]
 
 
+class dog_band(C.Structure):
+    _fields_ = [("row0", C.c_int32), ("row1", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("lo_row0", C.c_int32), ("hi_row1", C.c_int32), ("migrant_cap", C.c_uint32)]
+
+
 _vp, _f32p = C.c_void_p, C.POINTER(C.c_float)
+_u32p, _u64p, _vpp = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_void_p)
 _SIGS = {
     "dog_version": ([], C.c_int),
     "dog_error_string": ([C.c_int], C.c_char_p),
@@ -61,6 +67,15 @@ _SIGS = {
     "dog_profile_begin": ([_vp, C.c_int], C.c_int),
     "dog_profile_end": ([_vp, _vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
+    "dog_create_band": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
+                         C.POINTER(dog_band), C.POINTER(_vp)], C.c_int),
+    "dog_band_predict": ([_vp, C.c_float, _vp], C.c_int),
+    "dog_band_sizes": ([_vp, _u32p, _u32p, _u32p, _u32p, _vp], C.c_int),
+    "dog_band_buffers": ([_vp, C.c_uint32, C.c_uint32, _vpp, _vpp, _vpp, _vpp, _vp], C.c_int),
+    "dog_band_assign": ([_vp, _vp, _vpp, _vp], C.c_int),
+    "dog_band_joint": ([_vp, _vp, _vpp, _vp], C.c_int),
+    "dog_band_resample": ([_vp, _vp, _vp], C.c_int),
+    "dog_band_particles": ([_vp, _vp, C.c_uint64, _u32p, _u64p], C.c_int),
 }
 DOG_MAX_STAGES = 16
 for _name, (_args, _res) in _SIGS.items():
@@ -202,3 +217,94 @@ class Filter:
         return dict(W=int(s[0]), U=int(s[1]), A=int(s[2]), meas_bad=int(s[3]),
                     w_pred=np.uint32(s[4]).view(np.float32), w_bar=np.uint32(s[5]).view(np.float32),
                     k=int(s[6]), n_in=int(s[7]))
+
+
+class DeviceArray:
+    """A zero-copy torch view of device memory the library owns (``__cuda_array_interface__``)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+    @staticmethod
+    def tensor(ptr: int, n: int, dtype: torch.dtype) -> torch.Tensor:
+        ts = {torch.float32: "<f4", torch.int64: "<i8", torch.uint8: "|u1"}[dtype]
+        if n == 0:
+            return torch.empty(0, dtype=dtype, device="cuda")
+        return torch.as_tensor(DeviceArray(ptr, n, ts), device="cuda")
+
+
+class BandFilter:
+    """One row band of the grid (a band dog_ctx, include/dog.h); the cycle's phases map 1:1 onto the
+    C calls.  The exchanges between bands are the caller's (paper_1605_02406_b200/shard.py)."""
+
+    def __init__(self, width: int, height: int, nu: int, nu_b: int, row0: int, row1: int, rank: int, world: int,
+                 lo_row0: int, hi_row1: int, migrant_cap: int, *, cell_size: float = 0.1, p_s: float = 0.99,
+                 p_b: float = 0.02, sigma_pos: float = 0.02, sigma_vel: float = 0.8, sigma_birth_vel: float = 4.0,
+                 free_tau: float = 2.0, occ_max: float = 1.0, v_max: float = 0.0, seed: int = 2406):
+        self.width, self.height, self.nu, self.nu_b = width, height, nu, nu_b
+        self.row0, self.row1, self.rank, self.world = row0, row1, rank, world
+        self.C = width * (row1 - row0)
+        g = dog_grid(width, height, cell_size)
+        p = dog_params(p_s, p_b, sigma_pos, sigma_vel, sigma_birth_vel, free_tau, occ_max, v_max)
+        b = dog_band(row0, row1, rank, world, lo_row0, hi_row1, migrant_cap)
+        h = _vp()
+        _check(dog_create_band(C.byref(g), nu, nu_b, C.byref(p), seed, 0, C.byref(b), C.byref(h)), "dog_create_band")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            dog_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def predict(self, dt: float, stream=None):
+        _check(dog_band_predict(self._h, dt, _stream_ptr(stream)), "dog_band_predict")
+
+    def sizes(self, stream=None) -> tuple[int, int, int, int]:
+        a, b, c, d = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(dog_band_sizes(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d), _stream_ptr(stream)),
+               "dog_band_sizes")
+        return a.value, b.value, c.value, d.value
+
+    def buffers(self, n_down: int, n_up: int, n_lo: int, n_hi: int, stream=None):
+        """(send_down, send_up, recv_lo, recv_hi) as float32 [n, 4] device tensors (views)."""
+        sd, su, rl, rh = _vp(), _vp(), _vp(), _vp()
+        _check(dog_band_buffers(self._h, n_lo, n_hi, C.byref(sd), C.byref(su), C.byref(rl), C.byref(rh),
+                                _stream_ptr(stream)), "dog_band_buffers")
+        v = lambda ptr, n: DeviceArray.tensor(ptr.value or 0, 4 * n, torch.float32).view(-1, 4)
+        return v(sd, n_down), v(su, n_up), v(rl, n_lo), v(rh, n_hi)
+
+    def assign(self, meas_band: torch.Tensor, stream=None) -> torch.Tensor:
+        assert meas_band.is_cuda and meas_band.dtype == torch.float32 and meas_band.is_contiguous()
+        assert meas_band.numel() == 2 * self.C
+        m = _vp()
+        _check(dog_band_assign(self._h, meas_band.data_ptr(), C.byref(m), _stream_ptr(stream)), "dog_band_assign")
+        return DeviceArray.tensor(m.value, 1, torch.int64)
+
+    def joint(self, mass_all: torch.Tensor, stream=None) -> torch.Tensor:
+        assert mass_all.is_cuda and mass_all.dtype == torch.int64 and mass_all.numel() == self.world
+        w = _vp()
+        _check(dog_band_joint(self._h, mass_all.data_ptr(), C.byref(w), _stream_ptr(stream)), "dog_band_joint")
+        return DeviceArray.tensor(w.value, 1, torch.int64)
+
+    def resample(self, weight_all: torch.Tensor, stream=None):
+        assert weight_all.is_cuda and weight_all.dtype == torch.int64 and weight_all.numel() == self.world
+        _check(dog_band_resample(self._h, weight_all.data_ptr(), _stream_ptr(stream)), "dog_band_resample")
+
+    def particles(self) -> tuple[np.ndarray, int]:
+        """Own particles of the current state as float32 [n, 4] (x, y, vx, vy) and the global index of the first."""
+        n, g = C.c_uint32(), C.c_uint64()
+        _check(dog_band_particles(self._h, None, 0, C.byref(n), C.byref(g)), "dog_band_particles")
+        a = np.zeros((n.value, 4), np.float32)
+        _check(dog_band_particles(self._h, _np_ptr(a), n.value, C.byref(n), C.byref(g)), "dog_band_particles")
+        return a, g.value
+
+    def read_cells(self, stream=None, check: bool = True) -> dict:
+        return Filter.read_cells(self, stream, check)
+
+    def m_free(self) -> np.ndarray:
+        mf = np.zeros(self.C, np.float32)
+        _check(dog_get_state(self._h, None, None, None, None, None, _np_ptr(mf), None), "dog_get_state")
+        return mf

@@ -1,0 +1,184 @@
+"""Row-band multi-GPU driver: one band context per rank.
+
+The grid is cut into horizontal bands of rows, one per GPU.  Per cycle the bands exchange exactly what
+the method couples (include/dog.h, "row-band contexts"):
+
+1. after predict, the particles that moved into the band below / above (16-byte records, in global
+   index order) -- point-to-point with the two neighbours;
+2. after the cell update, every band's fixed-point born mass (one u64 each) -- all-gather; each band
+   allocates its birth slots on the global born-mass CDF (Alg. 5, A-15);
+3. after the joint-CDF scan, every band's joint weight (one u64 each) -- all-gather; each band then
+   produces its contiguous share [F(P'), F(P' + W_band)) of the global systematic resampling (A-24).
+
+Philox counters use global particle / slot indices, so the bands together reproduce the whole-grid
+filter bit for bit (tests/test_band_gpu.py).  The transport is torch.distributed (NCCL between GPUs,
+gloo on CPU for the protocol tests); ``LocalBands`` drives several bands in one process on one device
+(sequential phases, host-mediated copies: no kernel waits on another).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import dog
+
+
+def band_rows(height: int, world: int) -> list[tuple[int, int]]:
+    """Rows [row0, row1) of each band, bottom-up; the first height % world bands get one extra row."""
+    if world < 1 or world > height:
+        raise ValueError(f"cannot split {height} rows into {world} bands")
+    base, extra = divmod(height, world)
+    rows, r = [], 0
+    for b in range(world):
+        n = base + (1 if b < extra else 0)
+        rows.append((r, r + n))
+        r += n
+    return rows
+
+
+def neighbour_counts(counts: list[tuple[int, int]], rank: int) -> tuple[int, int]:
+    """Given every band's (n_down, n_up) migrant counts, the records band `rank` receives from below
+    (the lower band's n_up) and from above (the upper band's n_down)."""
+    world = len(counts)
+    n_lo = counts[rank - 1][1] if rank > 0 else 0
+    n_hi = counts[rank + 1][0] if rank < world - 1 else 0
+    return n_lo, n_hi
+
+
+class DistTransport:
+    """Exchanges of one band over torch.distributed (rank = band index)."""
+
+    def __init__(self, rank: int, world: int, device: torch.device, group=None):
+        self.rank, self.world, self.device, self.group = rank, world, device, group
+
+    def counts(self, n_down: int, n_up: int) -> tuple[int, int]:
+        mine = torch.tensor([n_down, n_up], dtype=torch.int64, device=self.device)
+        allc = torch.empty(2 * self.world, dtype=torch.int64, device=self.device)
+        dist.all_gather(list(allc.chunk(self.world)), mine, group=self.group)
+        c = allc.view(self.world, 2).tolist()
+        return neighbour_counts([(int(a), int(b)) for a, b in c], self.rank)
+
+    def migrate(self, send_down: torch.Tensor, send_up: torch.Tensor, recv_lo: torch.Tensor, recv_hi: torch.Tensor):
+        ops = []
+        if self.rank > 0:
+            if send_down.numel():
+                ops.append(dist.P2POp(dist.isend, send_down, self.rank - 1, group=self.group))
+            if recv_lo.numel():
+                ops.append(dist.P2POp(dist.irecv, recv_lo, self.rank - 1, group=self.group))
+        if self.rank < self.world - 1:
+            if send_up.numel():
+                ops.append(dist.P2POp(dist.isend, send_up, self.rank + 1, group=self.group))
+            if recv_hi.numel():
+                ops.append(dist.P2POp(dist.irecv, recv_hi, self.rank + 1, group=self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def allgather_u64(self, x: torch.Tensor, out: torch.Tensor):
+        dist.all_gather(list(out.chunk(self.world)), x.reshape(1), group=self.group)
+
+
+class ShardedFilter:
+    """The filter of one rank: its band of the grid, exchanging with the neighbour ranks."""
+
+    def __init__(self, width: int, height: int, nu: int, nu_b: int, rank: int, world: int,
+                 transport: DistTransport, migrant_cap: int | None = None, **params):
+        rows = band_rows(height, world)
+        self.rows = rows
+        self.row0, self.row1 = rows[rank]
+        lo_row0 = rows[rank - 1][0] if rank > 0 else self.row0
+        hi_row1 = rows[rank + 1][1] if rank < world - 1 else self.row1
+        cap = migrant_cap or max(4096, nu // 8)
+        self.f = dog.BandFilter(width, height, nu, nu_b, self.row0, self.row1, rank, world, lo_row0, hi_row1, cap,
+                                **params)
+        self.t = transport
+        self.world, self.rank = world, rank
+        dev = transport.device
+        self.mass_all = torch.zeros(world, dtype=torch.int64, device=dev)
+        self.weight_all = torch.zeros(world, dtype=torch.int64, device=dev)
+        self.n_far = 0
+
+    @classmethod
+    def from_config(cls, cfg, rank: int, world: int, transport: DistTransport, **over) -> "ShardedFilter":
+        kw = dict(cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params())
+        kw.update(over)
+        return cls(cfg.width, cfg.height, cfg.nu, cfg.nu_b, rank, world, transport, **kw)
+
+    def band_of(self, meas_full: torch.Tensor) -> torch.Tensor:
+        """The band's rows of a full-grid measurement tensor [H][W][2] (a contiguous view)."""
+        return meas_full[self.row0:self.row1]
+
+    def step(self, meas_band: torch.Tensor, dt: float, stream=None):
+        f = self.f
+        f.predict(dt, stream)
+        n_down, n_up, n_own, n_far = f.sizes(stream)
+        self.n_far = n_far
+        n_lo, n_hi = self.t.counts(n_down, n_up)
+        sd, su, rl, rh = f.buffers(n_down, n_up, n_lo, n_hi, stream)
+        self.t.migrate(sd, su, rl, rh)
+        mass = f.assign(meas_band, stream)
+        self.t.allgather_u64(mass, self.mass_all)
+        weight = f.joint(self.mass_all, stream)
+        self.t.allgather_u64(weight, self.weight_all)
+        f.resample(self.weight_all, stream)
+
+
+class LocalBands:
+    """Several bands of one grid in one process on one device: the phases run band after band and the
+    exchanges are device copies (for tests and single-GPU emulation; no kernel waits on another)."""
+
+    def __init__(self, width: int, height: int, nu: int, nu_b: int, world: int, migrant_cap: int | None = None,
+                 **params):
+        self.rows = band_rows(height, world)
+        cap = migrant_cap or max(4096, nu // 8)
+        self.bands = []
+        for b, (r0, r1) in enumerate(self.rows):
+            lo = self.rows[b - 1][0] if b > 0 else r0
+            hi = self.rows[b + 1][1] if b < world - 1 else r1
+            self.bands.append(dog.BandFilter(width, height, nu, nu_b, r0, r1, b, world, lo, hi, cap, **params))
+        self.world = world
+        self.mass_all = torch.zeros(world, dtype=torch.int64, device="cuda")
+        self.weight_all = torch.zeros(world, dtype=torch.int64, device="cuda")
+        self.n_far = 0
+
+    @classmethod
+    def from_config(cls, cfg, world: int, **over) -> "LocalBands":
+        kw = dict(cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params())
+        kw.update(over)
+        return cls(cfg.width, cfg.height, cfg.nu, cfg.nu_b, world, **kw)
+
+    def step(self, meas_full: torch.Tensor, dt: float):
+        B = self.bands
+        for f in B:
+            f.predict(dt)
+        sizes = [f.sizes() for f in B]
+        self.n_far = max(s[3] for s in sizes)
+        counts = [(s[0], s[1]) for s in sizes]
+        bufs = []
+        for b, f in enumerate(B):
+            n_lo, n_hi = neighbour_counts(counts, b)
+            bufs.append(f.buffers(counts[b][0], counts[b][1], n_lo, n_hi))
+        for b in range(self.world):                   # band b's down-migrants become band b-1's "from above"
+            if b > 0:
+                bufs[b - 1][3].copy_(bufs[b][0])
+            if b < self.world - 1:
+                bufs[b + 1][2].copy_(bufs[b][1])
+        for b, f in enumerate(B):
+            r0, r1 = self.rows[b]
+            m = f.assign(meas_full[r0:r1])
+            self.mass_all[b:b + 1].copy_(m)
+        for b, f in enumerate(B):
+            w = f.joint(self.mass_all)
+            self.weight_all[b:b + 1].copy_(w)
+        for f in B:
+            f.resample(self.weight_all)
+
+    def particles(self):
+        """All own particles in global index order: float32 [n, 4], and each band's (first index, count)."""
+        import numpy as np
+        parts, spans = [], []
+        for f in self.bands:
+            a, g = f.particles()
+            parts.append(a)
+            spans.append((g, a.shape[0]))
+        return np.concatenate(parts, axis=0), spans
