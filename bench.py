@@ -176,16 +176,14 @@ def bench_ours(args, cfg):
     import numpy as np
     import torch
     rank, local_rank, world = dist_env()
+    if world > 1:
+        return bench_sharded(args, cfg)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
     from paper_1605_02406_b200 import dog
     from paper_1605_02406_b200 import inputs as I
 
-    # replicas: each rank runs the full workload with its own filter seed (multi-GPU)
-    cfg_r = I.config(cfg.name, seed=cfg.seed + 7919 * rank) if world > 1 else cfg
+    cfg_r = cfg
     sc = I.scene(cfg_r)
     settle, W, K = args.settle, args.warmup, args.steps
     nframes = settle + W + K
@@ -199,8 +197,6 @@ def bench_ours(args, cfg):
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     clocks = ClockSampler(local_rank)
-    if world > 1:
-        torch.distributed.barrier()
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
@@ -220,14 +216,9 @@ def bench_ours(args, cfg):
         f.step(frames[settle + W + i], cfg.dt, stream)
     torch.cuda.synchronize()
     stages, nprof = f.profile_end()
-    if world > 1:
-        torch.distributed.barrier()
     step_ms = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(K))
     ms_mean = float(np.mean(step_ms))
-    ms_all = torch.tensor([ms_mean], device=dev, dtype=torch.float64)
-    if world > 1:
-        torch.distributed.all_reduce(ms_all, op=torch.distributed.ReduceOp.MAX)
-    ms_max = float(ms_all.item())
+    ms_max = ms_mean
 
     # end-to-end through the public host entry point: pinned host meas in, host occupancy out
     e2e = None
@@ -236,8 +227,6 @@ def bench_ours(args, cfg):
         occ_host = torch.empty(cfg.C, dtype=torch.float32).pin_memory()
         f.step_host(host_frames[0], cfg.dt, occ_host, stream)   # warm the staging buffer
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
         t0 = time.perf_counter()
         s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
@@ -246,10 +235,8 @@ def bench_ours(args, cfg):
         s1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = s0.elapsed_time(s1) / args.e2e_steps
-        e2e_t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-        if world > 1:
-            torch.distributed.all_reduce(e2e_t, op=torch.distributed.ReduceOp.MAX)
-        e2e = {"value": world * cfg.nu / (float(e2e_t.item()) * 1e-3), "unit": UNIT,
+        e2e_t = torch.tensor([e2e_ms], dtype=torch.float64)
+        e2e = {"value": cfg.nu / (float(e2e_t.item()) * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 4 * cfg.C,
                "ms_per_step": float(e2e_t.item()), "steps": args.e2e_steps,
                "entry": "dog_step_host (pinned host meas -> device, cycle, occupancy -> pinned host)"}
@@ -270,19 +257,15 @@ def bench_ours(args, cfg):
                  "frac": a_alg(cfg) / (ms_mean * 1e-3) / 1e9 / hbm, "unit": "GB/s",
                  "formula": "64 nu + 32 nu_b + 56 C (SURVEY.md 8(d))"}
 
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
     cpu = None
-    if world == 1 and args.cpu_baseline_steps > 0:
+    if args.cpu_baseline_steps > 0:
         st = f.get_state()
         ts = run_oracle_steps(cfg, sc, lambda k: sc.frame(k).numpy(), args.cpu_baseline_steps, 0, state=st)
         t = sum(ts) / len(ts)
         cpu = {"value": cfg.nu / t, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{len(ts)} full {cfg.name} cycles ({cfg.width}x{cfg.height}, {cfg.nu} + {cfg.nu_b}) from "
                          f"the GPU's warmed state, single-threaded C oracle", "ms_per_step": t * 1e3}
-    value = world * cfg.nu / (ms_max * 1e-3)
+    value = cfg.nu / (ms_max * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -291,7 +274,7 @@ def bench_ours(args, cfg):
                                f"particles, urban ray-cast scene", "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu,
                    "nu_b": cfg.nu_b, "dt_s": cfg.dt, "settle_cycles": settle,
                    "l2": "flushed between timed cycles (256 MiB write outside the cycle events)",
-                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "parallelism": "single GPU",
                    "p10_p90_ms": [step_ms[int(0.1 * (K - 1))], step_ms[int(0.9 * (K - 1))]]},
         "roofline": roof, "step_roofline": step_roof,
         "stages_ms": {k: round(v, 5) for k, v in st_avg.items()},
@@ -301,8 +284,96 @@ def bench_ours(args, cfg):
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+
+
+def bench_sharded(args, cfg):
+    """N > 1: the cfg's single scene split into N row bands, one per rank; migrants by
+    NCCL send/recv between neighbour ranks, born mass and joint weight by NCCL all-gathers.  Strong
+    scaling: value = the scene's nu / cycle time, the time being the max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    from paper_1605_02406_b200 import inputs as I
+    from paper_1605_02406_b200 import shard
+
+    sc = I.scene(cfg)
+    settle, W, K = args.settle, args.warmup, args.steps
+    t = shard.DistTransport(rank, world, dev)
+    f = shard.ShardedFilter.from_config(cfg, rank, world, t)
+    bands = [f.band_of(sc.frame(k, device=dev).contiguous()).contiguous() for k in range(settle + W + K)]
+    stream = torch.cuda.current_stream()
+    for k in range(settle + W):
+        f.step(bands[k], cfg.dt, stream)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    clocks = ClockSampler(local_rank)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(K):
+        flush.zero_()
+        ev0[i].record(stream)
+        f.step(bands[settle + W + i], cfg.dt, stream)
+        ev1[i].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dist.barrier()
+    step_ms = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(K))
+    ms_all = torch.tensor([float(np.mean(step_ms))], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms_all, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_all.item())
+    n_own = torch.tensor([f.f.particles()[0].shape[0]], device=dev, dtype=torch.int64)
+    own_all = torch.zeros(world, device=dev, dtype=torch.int64)
+    dist.all_gather(list(own_all.chunk(world)), n_own)
+
+    # end to end: the band's measurement from pinned host memory, the cycle, the band's occupancy back
+    e2e = None
+    if args.e2e_steps > 0:
+        host = [bands[settle + W + (i % K)].cpu().pin_memory() for i in range(min(args.e2e_steps, K))]
+        occ_host = torch.empty(f.f.C, dtype=torch.float32).pin_memory()
+        dist.barrier()
+        s0 = torch.cuda.Event(enable_timing=True); s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for i in range(args.e2e_steps):
+            m = host[i % len(host)].to(dev, non_blocking=True)
+            f.step(m, cfg.dt, stream)
+            occ_host.copy_(f.f.read_cells(stream)["occ"], non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        e2e_t = torch.tensor([s0.elapsed_time(s1) / args.e2e_steps], device=dev, dtype=torch.float64)
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": cfg.nu / (float(e2e_t.item()) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 4 * cfg.C,
+               "ms_per_step": float(e2e_t.item()), "steps": args.e2e_steps,
+               "entry": "BandFilter phases per rank (pinned host band meas -> device, cycle, band occupancy -> host)"}
+    hbm, peak_src = peaks()
+    per_gpu = a_alg(cfg) / world / (ms_max * 1e-3) / 1e9
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": cfg.nu / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded ray-cast urban scene, inputs.py)",
+            "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} grid, {cfg.nu} persistent + {cfg.nu_b} "
+                                   f"birth particles, urban ray-cast scene", "grid": f"{cfg.width}x{cfg.height}",
+                       "nu": cfg.nu, "nu_b": cfg.nu_b, "dt_s": cfg.dt, "settle_cycles": settle,
+                       "l2": "flushed between timed cycles (256 MiB write outside the cycle events)",
+                       "parallelism": f"row bands x{world} (migrants: NCCL send/recv; prefixes: NCCL all-gather)",
+                       "rows": shard.band_rows(cfg.height, world), "own_particles": own_all.tolist(),
+                       "p10_p90_ms": [step_ms[int(0.1 * (K - 1))], step_ms[int(0.9 * (K - 1))]]},
+            "roofline": {"bound": "hbm", "kernel": "cycle per GPU (A_alg / N)", "achieved": per_gpu, "peak": hbm,
+                         "unit": "GB/s", "frac": per_gpu / hbm, "traffic": None, "peak_source": peak_src},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": 10 * K * world, "clocks": clk,
+            "far_migrants": f.n_far,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def dog_scalars(f):

@@ -126,16 +126,18 @@ bool finite(float v) { return std::isfinite(v); }
 
 // Every kernel of a cycle is launched with programmatic stream serialization (PDL, dog_common.cuh):
 // its CTAs may start while the previous kernel drains and wait in griddepcontrol.wait for its results.
+// Measured exception: k_resample_tiles is launched WITHOUT the attribute -- its CTAs resident early
+// beside k_pair_sort's cost ~50 us at cfg T (smem/L1 carveout of the co-resident kernels).
 bool g_pdl = getenv("DOG_NO_PDL") == nullptr;
 
 template <typename... KArgs, typename... Args>
-cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, uint32_t cluster,
-                   Args&&... args)
+cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      uint32_t cluster, Args&&... args)
 {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (g_pdl) {
+    if (g_pdl && pdl) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -148,6 +150,13 @@ cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
     cfg.gridDim = grid; cfg.blockDim = block; cfg.dynamicSmemBytes = smem; cfg.stream = st;
     cfg.attrs = at; cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, uint32_t cluster,
+                   Args&&... args)
+{
+    return launch_ex(true, kern, grid, block, smem, st, cluster, std::forward<Args>(args)...);
 }
 
 StepArgs step_args(const dog_ctx* ctx, float dt)
@@ -467,11 +476,11 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     const int par = (int)(a.k & 1);
     if (dbg)
-        CK(launch(k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
+        CK(launch_ex(false, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
                   ctx->tp, (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
                   (const DevScalars*)ctx->sc, fc, par));
     else
-        CK(launch(k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
+        CK(launch_ex(false, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
                   ctx->tp, (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
                   (const DevScalars*)ctx->sc, fc, par));
     return DOG_OK;
