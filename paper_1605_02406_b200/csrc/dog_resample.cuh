@@ -94,6 +94,9 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
     }
 }
 
+#ifndef RT_MINB
+#define RT_MINB 4
+#endif
 constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
 constexpr int kRtRunCache = 64;                                       // runs whose RunF sits in smem (rest: global)
 constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
@@ -174,7 +177,7 @@ __device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
 //     block max-scan spreads the owner over its outputs; threads write consecutive outputs (coalesced,
 //     balanced whatever the copy counts).
 template <bool kDbg>
-__global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
+__global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
     uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
     const DevScalars* __restrict__ sc, FilterConst fc, int par)
@@ -201,9 +204,13 @@ __global__ __launch_bounds__(kRtThreads, 3) void k_resample_tiles(
     const uint32_t p0 = tid * kRtItems;
     const RunInfo* __restrict__ runs = tp.run + base;
     PHASE_BEGIN();
-    // ---- phase A: local permutation, run starts, run parameters, and this thread's velocity gathers
-    //      (its 16 sorted positions are the 16 local-permutation entries it loads)
+    // ---- phase A: local permutation, run starts; the tile's predicted states (64 KB, read twice in
+    //      permuted order below) are prefetched into L2 meanwhile
     const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
+#ifndef RT_NO_PREFETCH
+    for (uint32_t l = tid; l < (n * 16u + 127u) / 128u; l += kRtThreads)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(pred + pbase) + 128u * l));
+#endif
     {
         uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
         if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }

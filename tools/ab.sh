@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B timing on the GPU box: variant A = sources in paper_1605_02406_b200/csrc_ab/ (e.g. the last
 # commit) run with $AB_ENV_A, B = the working tree run with $AB_ENV_B.
-DOG_CSRC=$PWD/paper_1605_02406_b200/csrc_ab DOG_LIB=$PWD/paper_1605_02406_b200/csrc_ab/libdog.so python -m paper_1605_02406_b200.build > /dev/null 2>&1 || echo build_A_failed
+DOG_NVCC_EXTRA="${AB_NVCC_A:-}" DOG_CSRC=$PWD/paper_1605_02406_b200/csrc_ab DOG_LIB=$PWD/paper_1605_02406_b200/csrc_ab/libdog.so python -m paper_1605_02406_b200.build > /dev/null 2>&1 || echo build_A_failed
 python -m paper_1605_02406_b200.build > /dev/null 2>&1 || echo build_B_failed
 for r in 1 2; do
   for v in A B; do
