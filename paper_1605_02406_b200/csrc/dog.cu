@@ -285,7 +285,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     ctx->tiles = (uint32_t)(ctx->nu_cap / kSortTile);
     ctx->own_tiles = ctx->own_cap / kSortTile;
     {   // cell chunks of 2048 cells (at most kMaxCellBlocks chunks)
-        uint32_t chunk = 2u * kCellIter;
+        uint32_t chunk = kCellIter;
         uint32_t nblk = cdiv(ctx->C, chunk);
         while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(ctx->C, chunk); }
         ctx->cell_chunk = chunk;

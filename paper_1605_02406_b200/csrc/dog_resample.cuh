@@ -204,13 +204,8 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     const uint32_t p0 = tid * kRtItems;
     const RunInfo* __restrict__ runs = tp.run + base;
     PHASE_BEGIN();
-    // ---- phase A: local permutation, run starts; the tile's predicted states (64 KB, read twice in
-    //      permuted order below) are prefetched into L2 meanwhile
+    // ---- phase A: local permutation, run starts
     const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
-#ifndef RT_NO_PREFETCH
-    for (uint32_t l = tid; l < (n * 16u + 127u) / 128u; l += kRtThreads)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(pred + pbase) + 128u * l));
-#endif
     {
         uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
         if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }
