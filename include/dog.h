@@ -66,7 +66,8 @@ typedef struct {
 
 /* dog_create -- allocate a filter on the current CUDA device in the empty initial state (A-19):
  * all nu particles at the sentinel position (-2^30 cells) with weight 0, m_F = 0, k = 0.
- *   grid, params : validated copies are kept (DOG_E_INVAL on violation).
+ *   grid, params : validated copies are kept (DOG_E_INVAL on violation; width, height <= 65535 and
+ *                  width * height < 2^24).
  *   n_particles  : nu >= 1, persistent particles per cycle (< 2^31).
  *   n_birth      : nu_b >= 0, new-born particles per cycle ("remains constant").
  *   seed         : Philox key (low 32 bits, high 32 bits).

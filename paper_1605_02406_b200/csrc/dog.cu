@@ -244,8 +244,8 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     const dog_params& p = *params;
     const int64_t C = (int64_t)grid->width * grid->height;
     if (grid->width <= 0 || grid->height <= 0 || C >= (1ll << 24) || !(grid->cell_size > 0.0f) ||
-        !finite(grid->cell_size))
-        return DOG_E_INVAL;   // C < 2^24 keeps every fixed-point total below 2^64 (A-23)
+        !finite(grid->cell_size) || grid->width > 65535 || grid->height > 65535)
+        return DOG_E_INVAL;   // C < 2^24 keeps every fixed-point total below 2^64 (A-23); 16-bit rows/cols
     if (n_particles < 1 || n_particles >= (1ll << 30) || n_birth < 0 || n_birth >= (1ll << 30))
         return DOG_E_INVAL;
     if (!(p.p_s > 0.0f && p.p_s <= 1.0f) || !(p.p_b >= 0.0f && p.p_b < 1.0f) ||

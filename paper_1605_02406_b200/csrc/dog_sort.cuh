@@ -118,8 +118,12 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     }
 
     PHASE_BEGIN();
-    // ---- predict (Alg. 1) or load: position p = local index (input order)
-    uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
+    // ---- predict (Alg. 1) or load: position p = local index (input order).  The sort key is the
+    //      (row, col) of the particle's cell, packed, remapped below onto the tile's bounding box of
+    //      cells: (row - rmin) * span + (col - cmin) preserves the cell order and usually needs 8-10 bits
+    //      (one or two radix passes instead of the 13+ bits of the cell index itself).
+    constexpr uint32_t kOut = 0xFFFFFFFEu;                  // outside the context's band (or the grid)
+    uint32_t rmin = 0xFFFFu, rmax = 0u, cmin = 0xFFFFu, cmax = 0u, anyout = 0u;
 #pragma unroll 2
     for (int i = 0; i < kPsRows; ++i) {
         const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
@@ -135,29 +139,54 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
             }
             const uint32_t kg = global_key(P, fc);
             if (keys_dbg) keys_dbg[g] = kg;
-            key = local_key(kg, fc);
-            kmin = min(kmin, key);
-            kmax = max(kmax, key);
+            if (local_key(kg, fc) < fc.C) {
+                const uint32_t row = (uint32_t)__float2int_rz(P.y), col = (uint32_t)__float2int_rz(P.x);
+                key = (row << 16) | col;
+                rmin = min(rmin, row); rmax = max(rmax, row); cmin = min(cmin, col); cmax = max(cmax, col);
+            } else {
+                key = kOut;
+                anyout = 1u;
+            }
         }
         S.k[0][p] = key;
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
-        kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, off));
-        kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, off));
+        rmin = min(rmin, __shfl_xor_sync(0xffffffffu, rmin, off));
+        rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, off));
+        cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, off));
+        cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, off));
+        anyout |= __shfl_xor_sync(0xffffffffu, anyout, off);
     }
-    if (lane == 0) { S.mn[warp] = kmin; S.mx[warp] = kmax; }
+    if (lane == 0) { S.mn[warp] = (rmin << 16) | cmin; S.mx[warp] = (rmax << 16) | cmax; S.rank[warp] = (uint16_t)anyout; }
     __syncthreads();
-    kmin = S.mn[0]; kmax = S.mx[0];
 #pragma unroll
-    for (int w = 1; w < kPsWarps; ++w) { kmin = min(kmin, S.mn[w]); kmax = max(kmax, S.mx[w]); }
+    for (int w = 0; w < kPsWarps; ++w) {
+        rmin = min(rmin, S.mn[w] >> 16); cmin = min(cmin, S.mn[w] & 0xFFFFu);
+        rmax = max(rmax, S.mx[w] >> 16); cmax = max(cmax, S.mx[w] & 0xFFFFu);
+        anyout |= S.rank[w];
+    }
     if (n == 0) {                                           // beyond the particles of this cycle
         if (tid == 0) tp.nd[blockIdx.x] = 0u;
         return;
     }
     PHASE_MARK(8);
-    const uint32_t range = kmax - kmin;
+    const bool anyin = rmin <= rmax;
+    const uint32_t span = anyin ? cmax - cmin + 1u : 1u, rows = anyin ? rmax - rmin + 1u : 0u;
+    const uint32_t kout = rows * span;                      // the remapped key of "outside": after every cell
+    __syncthreads();                                        // S.rank reused below
+#pragma unroll 4
+    for (int i = 0; i < kPsRows; ++i) {                     // remap in place
+        const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+        const uint32_t key = S.k[0][p];
+        if (p < n) S.k[0][p] = key == kOut ? kout : ((key >> 16) - rmin) * span + ((key & 0xFFFFu) - cmin);
+    }
+    __syncthreads();
+    const uint32_t kmin = 0u, range = anyout ? kout : (anyin ? kout - 1u : 0u);
     const int bits = range ? 32 - __clz(range) : 0;
+#ifdef DOG_TIMING
+    if (tid == 0) { atomicAdd(&g_phase_ns[30], (unsigned long long)((bits + 7) / 8)); atomicAdd(&g_phase_ns[31], 1ull); }
+#endif
 
     // ---- stable LSD radix passes (positions >= n carry key 0xFFFFFFFF and stay at the end)
     int cur = 0;
@@ -228,7 +257,9 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     __syncthreads();
     for (uint32_t r = tid; r < nd; r += kPsThreads) {
         const uint32_t f = s_start[r], e = r + 1 < nd ? (uint32_t)s_start[r + 1] : n, c = e - f;
-        const uint32_t key = sk[f];
+        const uint32_t kr = sk[f];                         // remapped key -> the context's cell index
+        const uint32_t key = kr >= kout ? fc.C
+                           : (rmin + kr / span - fc.row0) * (uint32_t)fc.W + cmin + kr % span;
         tp.key[tb + r] = key;
         tp.first[tb + r] = (uint16_t)f;
         tp.cnt[tb + r] = (uint16_t)(c - 1);

@@ -28,6 +28,6 @@ torch.cuda.synchronize()
 dog._lib.dog_timing_dump(buf, 64, 0)
 t = np.frombuffer(buf, dtype=np.uint64).astype(np.float64)
 blocks = (cfg.nu + 4095) // 4096 * 10
-print("windows", int(t[21]), "slow windows", int(t[20]))
+print("windows", int(t[21]), "slow windows", int(t[20]), "radix passes per tile", t[30] / max(t[31], 1))
 for i, nm in NAMES.items():
     print(f"{nm:28s} {t[i] / blocks / 1000:8.2f} us per block")
