@@ -91,6 +91,14 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream);
  * synchronous on `stream`.  This is the end-to-end entry point (host buffers in, host result out). */
 int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream);
 
+/* dog_step_host_async -- the pipelined end-to-end entry: the frame is copied host -> device on a copy
+ * stream of the context (double-buffered staging) while the previous cycle runs on `stream`, and the
+ * occupancy is snapshot on the device and copied device -> host on a second copy stream while the next
+ * cycle runs.  Returns after enqueueing; meas_host must stay valid and unmodified, and occ_host is
+ * complete, only after dog_sync(ctx, stream).  Use PINNED host buffers for overlap.  Whole-grid
+ * contexts only. */
+int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream);
+
 /* ---- row-band contexts (multi-GPU) ----
  * The grid is split into horizontal bands of rows, one context (and one GPU) per band.  A band context
  * owns its cells (m_F, readouts; the caller passes the band's measurement rows) and the particles whose

@@ -80,6 +80,12 @@ struct dog_ctx {
     DevScalars* sc = nullptr;
     // end-to-end staging
     float* meas_dev = nullptr;
+    // pipelined host entry (dog_step_host_async): double-buffered staging, copy streams, events
+    float* hmeas[2] = {nullptr, nullptr};
+    float* hocc[2] = {nullptr, nullptr};
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
+    int hbuf = 0;
     // profiling: events[step][stage boundary]
     std::vector<cudaEvent_t> pev;
     int prof_max = 0, prof_steps = 0, prof_nst = 0;
@@ -419,6 +425,11 @@ int dog_destroy(dog_ctx* ctx)
     set_device(ctx);
     cudaDeviceSynchronize();
     for (cudaEvent_t e : ctx->pev) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t e : {ctx->ev_in[b], ctx->ev_used[b], ctx->ev_out[b], ctx->ev_read[b]})
+            if (e) cudaEventDestroy(e);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     free_all(ctx);
     delete ctx;
     return DOG_OK;
@@ -733,12 +744,57 @@ int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_hos
     return DOG_OK;
 }
 
+int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream)
+{
+    if (!ctx || !meas_host) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t C = ctx->C;
+    if (!ctx->h2d) {   // first use: staging buffers, copy streams and events
+        for (int b = 0; b < 2; ++b) {
+            if (int rc = dalloc(ctx, &ctx->hmeas[b], 2 * C)) return rc;
+            if (int rc = dalloc(ctx, &ctx->hocc[b], C)) return rc;
+            CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_used[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_read[b], cudaEventDisableTiming));
+            CK(cudaEventRecord(ctx->ev_used[b], st));
+            CK(cudaEventRecord(ctx->ev_read[b], st));
+        }
+        CK(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+    }
+    const int b = ctx->hbuf;
+    ctx->hbuf ^= 1;
+    // in: wait until the cycle that last read this staging buffer is done, then copy the frame
+    CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev_used[b], 0));
+    CK(cudaMemcpyAsync(ctx->hmeas[b], meas_host, 8 * C, cudaMemcpyHostToDevice, ctx->h2d));
+    CK(cudaEventRecord(ctx->ev_in[b], ctx->h2d));
+    // the cycle, on the caller's stream, once its frame has landed
+    CK(cudaStreamWaitEvent(st, ctx->ev_in[b], 0));
+    if (int rc = dog_step(ctx, ctx->hmeas[b], dt, stream)) return rc;
+    CK(cudaEventRecord(ctx->ev_used[b], st));
+    if (occ_host) {   // out: snapshot the occupancy on the device, copy it to the host meanwhile
+        CK(cudaStreamWaitEvent(st, ctx->ev_read[b], 0));
+        CK(cudaMemcpyAsync(ctx->hocc[b], ctx->occ, 4 * C, cudaMemcpyDeviceToDevice, st));
+        CK(cudaEventRecord(ctx->ev_out[b], st));
+        CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_out[b], 0));
+        CK(cudaMemcpyAsync(occ_host, ctx->hocc[b], 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+        CK(cudaEventRecord(ctx->ev_read[b], ctx->d2h));
+    }
+    return DOG_OK;
+}
+
 int dog_sync(dog_ctx* ctx, void* stream)
 {
     if (!ctx) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaStreamSynchronize((cudaStream_t)stream));
+    if (ctx->d2h) CK(cudaStreamSynchronize(ctx->d2h));
+    if (ctx->h2d) CK(cudaStreamSynchronize(ctx->h2d));
     return report_meas(ctx);
 }
 

@@ -57,6 +57,7 @@ _SIGS = {
                     C.POINTER(_vp)], C.c_int),
     "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
+    "dog_step_host_async": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_read_cells": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "dog_sync": ([_vp, _vp], C.c_int),
     "dog_destroy": ([_vp], C.c_int),
@@ -165,6 +166,14 @@ class Filter:
         assert not meas_host.is_cuda and meas_host.dtype == torch.float32 and meas_host.is_contiguous()
         occ_ptr = occ_host.data_ptr() if occ_host is not None else None
         _check(dog_step_host(self._h, meas_host.data_ptr(), dt, occ_ptr, _stream_ptr(stream)), "dog_step_host")
+
+    def step_host_async(self, meas_host: torch.Tensor, dt: float, occ_host: torch.Tensor | None = None,
+                        stream=None):
+        """Pipelined host entry (include/dog.h): complete after sync(); use pinned tensors."""
+        assert not meas_host.is_cuda and meas_host.dtype == torch.float32 and meas_host.is_contiguous()
+        occ_ptr = occ_host.data_ptr() if occ_host is not None else None
+        _check(dog_step_host_async(self._h, meas_host.data_ptr(), dt, occ_ptr, _stream_ptr(stream)),
+               "dog_step_host_async")
 
     def sync(self, stream=None) -> int:
         return dog_sync(self._h, _stream_ptr(stream))
