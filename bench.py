@@ -251,6 +251,25 @@ def bench_ours(args, cfg):
                         "pinned host on a second copy stream; overlapped across cycles; wall clock incl. final sync)",
                "sync_entry_ms_per_step": sync_ms}
 
+    # NEXT-2 (ego-motion compensation): one scroll of grid and particles at this size, device-timed
+    ego = None
+    try:
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        n_ego = 6
+        e0.record(stream)
+        for i in range(n_ego):
+            f.ego_scroll(0.35 if i % 2 == 0 else -0.35, 0.15 if i % 2 == 0 else -0.15, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ego_ms = e0.elapsed_time(e1) / n_ego
+        ego_bytes = 32.0 * cfg.nu + 8.0 * cfg.C              # particles read + written, m_F read + written
+        hbm0, _ = peaks()
+        ego = {"ms": ego_ms, "algorithmic_bytes": ego_bytes, "achieved_GBps": ego_bytes / (ego_ms * 1e-3) / 1e9,
+               "frac": ego_bytes / (ego_ms * 1e-3) / 1e9 / hbm0, "shift_cells": [3, 1]}
+    except Exception as exc:   # noqa: BLE001 -- reported, not fatal to the main line
+        ego = {"error": str(exc)}
+
     # per-stage times and roofline of the dominant kernel
     st_avg = {k: v / max(nprof, 1) for k, v in stages.items()}
     kern = {k: v for k, v in st_avg.items() if k != "memset"}
@@ -290,6 +309,7 @@ def bench_ours(args, cfg):
         "stages_ms": {k: round(v, 5) for k, v in st_avg.items()},
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
+        "next_rows": {"ego_scroll": ego},
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }

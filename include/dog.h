@@ -145,6 +145,18 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
  * first one; xyvv_host may be NULL to query the count. */
 int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n_own, uint64_t* global_first);
 
+/* ---- ego-motion compensation (SPEC ego_scroll) ----
+ * dog_ego_scroll -- between cycles, move the grid content and the particles by the whole-cell part of
+ * (dx, dy) + the stored residual (metres, grid axes; content moves by +shift): the integer part is fp64
+ * truncation toward zero of (delta + residual) / cell_size, the fraction becomes the new residual
+ * (A-32).  Cells scrolled in at the leading edge become vacuous (m_F = 0) with no particles;
+ * particles leaving the grid become sentinel particles.  *shift_x / *shift_y (may be NULL) receive the
+ * applied shift in cells.  DOG_E_INVAL (nothing changed) if a shift would reach half the grid side or
+ * dx, dy are not finite.  Stream-ordered; whole-grid contexts only (DOG_E_STATE for a band).  The
+ * readouts of the last cycle are not moved (they describe the cycle that produced them). */
+int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t* shift_y, void* stream);
+int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry);
+
 /* dog_read_cells -- copy the readouts of the last completed cycle (posterior, before resampling,
  * P:1444) into caller DEVICE buffers (any may be NULL):
  *   occ[C] = m_O, free_mass[C] = m_F (Eq. 63); vel_mean[C][2] = (mean_vx, mean_vy) (Eq. 81);

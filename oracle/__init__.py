@@ -87,6 +87,9 @@ def _declare(L):
     L.orc_set_state.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p, C.c_float, f32p, C.c_int64]
     L.orc_get_state.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p, f32p, f32p, _p(C.c_int64)]
     L.orc_step.argtypes = [C.c_void_p, f32p, C.c_float]; L.orc_step.restype = C.c_int
+    L.orc_ego_scroll.argtypes = [C.c_void_p, C.c_double, C.c_double, _p(C.c_int32), _p(C.c_int32)]
+    L.orc_ego_scroll.restype = C.c_int
+    L.orc_ego_residual.argtypes = [C.c_void_p, _p(C.c_double), _p(C.c_double)]
     L.orc_read_cells.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p]
     L.orc_get_dump.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]
     L.orc_get_dump.restype = C.c_int64
@@ -222,6 +225,17 @@ class Oracle:
         m = np.ascontiguousarray(meas, dtype=np.float32).reshape(-1)
         assert m.size == 2 * self.C
         return lib().orc_step(self._h, _ptr(m, C.c_float), C.c_float(dt))
+
+    def ego_scroll(self, dx: float, dy: float):
+        """Ego-motion compensation (NEXT-2): (shift_x, shift_y) in cells, or None if refused."""
+        sx, sy = C.c_int32(), C.c_int32()
+        rc = lib().orc_ego_scroll(self._h, float(dx), float(dy), C.byref(sx), C.byref(sy))
+        return None if rc != 0 else (sx.value, sy.value)
+
+    def ego_residual(self):
+        rx, ry = C.c_double(), C.c_double()
+        lib().orc_ego_residual(self._h, C.byref(rx), C.byref(ry))
+        return rx.value, ry.value
 
     def read_cells(self):
         Cc = self.C

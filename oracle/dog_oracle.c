@@ -229,6 +229,7 @@ struct orc_ctx {
     float *mean, *cov;
     uint32_t* jidx;
     uint64_t scal[8];
+    double res_x, res_y;     /* ego-motion residual, metres (NEXT-2) */
 };
 
 static void draw(const orc_ctx* h, uint32_t index, int64_t k, uint32_t stage, uint32_t r[4])
@@ -528,4 +529,56 @@ int64_t orc_get_dump(orc_ctx* h, int what, void* dst, size_t bytes)
     if (bytes < n) return -2;
     memcpy(dst, src, n);
     return (int64_t)n;
+}
+
+/* ======================================================================================
+ * Ego-motion compensation.  P:1550: "The vehicle speed and yaw rate are available
+ * via CAN messages, so the ego movement of the test vehicle can be compensated in the grid map."  The
+ * operation follows SPEC S:171-179 (ego_scroll): the grid content shifts by the integer-cell part of
+ * (delta + residual) and the fraction is kept as the new residual; cells scrolled in at the leading edge
+ * become vacuous (m_F = 0) and hold no particles; particles move by the same whole number of cells and
+ * those that leave the grid become sentinel particles (A-19).  Readings (A-32): the integer
+ * part is fp64 truncation toward zero of (delta + residual) / cell_size, the residual is
+ * (delta + residual) - shift * cell_size in fp64; a particle moves by one f32 addition per coordinate;
+ * a particle already at the sentinel position stays there; a shift of half the grid side or more is an
+ * error and changes nothing.
+ * ====================================================================================== */
+int orc_ego_scroll(orc_ctx* h, double dx, double dy, int32_t* shift_x, int32_t* shift_y)
+{
+    const double cs = (double)h->p.cell_size;
+    const double tx = dx + h->res_x, ty = dy + h->res_y;
+    const double qx = trunc(tx / cs), qy = trunc(ty / cs);
+    const int32_t W = h->p.width, H = h->p.height;
+    if (!(fabs(qx) * 2.0 < (double)W) || !(fabs(qy) * 2.0 < (double)H)) return -1;
+    const int32_t sx = (int32_t)qx, sy = (int32_t)qy;
+    h->res_x = tx - qx * cs;
+    h->res_y = ty - qy * cs;
+    if (shift_x) *shift_x = sx;
+    if (shift_y) *shift_y = sy;
+    /* grid: the content of cell (r, c) moves to (r + sy, c + sx) */
+    float* tmp = (float*)xcalloc(h->C, 4);
+    for (int32_t r = 0; r < H; ++r)
+        for (int32_t c = 0; c < W; ++c) {
+            const int32_t r0 = r - sy, c0 = c - sx;
+            tmp[(int64_t)r * W + c] = (r0 >= 0 && r0 < H && c0 >= 0 && c0 < W) ? h->m_free[(int64_t)r0 * W + c0] : 0.0f;
+        }
+    memcpy(h->m_free, tmp, h->C * 4);
+    free(tmp);
+    /* particles */
+    for (int64_t i = 0; i < h->p.nu; ++i) {
+        if (h->x[i] == SENTINEL_POS && h->y[i] == SENTINEL_POS) continue;
+        const float xn = h->x[i] + (float)sx, yn = h->y[i] + (float)sy;
+        if (xn >= 0.0f && xn < (float)W && yn >= 0.0f && yn < (float)H) {
+            h->x[i] = xn; h->y[i] = yn;
+        } else {
+            h->x[i] = SENTINEL_POS; h->y[i] = SENTINEL_POS; h->vx[i] = 0.0f; h->vy[i] = 0.0f;
+        }
+    }
+    return 0;
+}
+
+void orc_ego_residual(const orc_ctx* h, double* rx, double* ry)
+{
+    if (rx) *rx = h->res_x;
+    if (ry) *ry = h->res_y;
 }

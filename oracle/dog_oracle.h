@@ -85,6 +85,10 @@ int  orc_get_state(orc_ctx* h, float* x, float* y, float* vx, float* vy, float* 
                    float* m_free, int64_t* k);
 /* meas: float[C][2] = (m_zO, m_zF) row-major; dt > 0 seconds */
 int  orc_step(orc_ctx* h, const float* meas, float dt);
+/* Ego-motion compensation (NEXT-2): scroll grid and particles by the whole-cell part of (dx, dy) plus the
+ * stored residual (metres); returns -1 (nothing changed) if a shift would reach half the grid side. */
+int  orc_ego_scroll(orc_ctx* h, double dx, double dy, int32_t* shift_x, int32_t* shift_y);
+void orc_ego_residual(const orc_ctx* h, double* rx, double* ry);
 /* readouts of the last step: occ[C], free[C], mean[C][2], cov[C][3] */
 int  orc_read_cells(orc_ctx* h, float* occ, float* free_mass, float* mean, float* cov);
 /* copy a stage dump of the last step; returns bytes copied or <0 */

@@ -18,6 +18,7 @@
 #include "dog_sort.cuh"
 #include "dog_cells.cuh"
 #include "dog_resample.cuh"
+#include "dog_ego.cuh"
 
 using namespace dog;
 
@@ -80,6 +81,9 @@ struct dog_ctx {
     DevScalars* sc = nullptr;
     // end-to-end staging
     float* meas_dev = nullptr;
+    // ego-motion compensation (dog_ego_scroll)
+    double res_x = 0.0, res_y = 0.0;
+    float* m_free_tmp = nullptr;
     // pipelined host entry (dog_step_host_async): double-buffered staging, copy streams, events
     float* hmeas[2] = {nullptr, nullptr};
     float* hocc[2] = {nullptr, nullptr};
@@ -349,6 +353,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
         AL(ctx->bx, NB); AL(ctx->by, NB); AL(ctx->bvx, NB); AL(ctx->bvy, NB);
     }
     AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs);
+    if (ctx->world == 1) AL(ctx->m_free_tmp, Cs);   // ego-motion compensation scrolls into it
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
     AL(ctx->mvalid, Cs / 32 + 1);
     const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
@@ -784,6 +789,41 @@ int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* o
         CK(cudaMemcpyAsync(occ_host, ctx->hocc[b], 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
         CK(cudaEventRecord(ctx->ev_read[b], ctx->d2h));
     }
+    return DOG_OK;
+}
+
+int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t* shift_y, void* stream)
+{
+    if (!ctx || !std::isfinite(dx) || !std::isfinite(dy)) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1) return DOG_E_STATE;                 // whole-grid contexts only
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    // integer-cell part of (delta + residual), fp64 truncation toward zero; the fraction is kept (A-32)
+    const double cs = (double)ctx->grid.cell_size;
+    const double tx = dx + ctx->res_x, ty = dy + ctx->res_y;
+    const double qx = std::trunc(tx / cs), qy = std::trunc(ty / cs);
+    const int32_t W = ctx->grid.width, H = ctx->grid.height;
+    if (!(std::fabs(qx) * 2.0 < (double)W) || !(std::fabs(qy) * 2.0 < (double)H)) return DOG_E_INVAL;
+    const int32_t sx = (int32_t)qx, sy = (int32_t)qy;
+    ctx->res_x = tx - qx * cs;
+    ctx->res_y = ty - qy * cs;
+    if (shift_x) *shift_x = sx;
+    if (shift_y) *shift_y = sy;
+    if (sx == 0 && sy == 0) return DOG_OK;
+    const uint32_t sms = ctx->flat_blocks / 4u;
+    CK(launch_ex(false, k_ego_grid, 8u * (uint32_t)sms, 256, 0, st, 0, (const float*)ctx->m_free, ctx->m_free_tmp,
+                 sx, sy, W, H));
+    CK(launch_ex(false, k_ego_particles, 8u * (uint32_t)sms, 256, 0, st, 0, ctx->st, (uint32_t)ctx->nu, sx, sy, W, H));
+    std::swap(ctx->m_free, ctx->m_free_tmp);
+    return DOG_OK;
+}
+
+int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (rx) *rx = ctx->res_x;
+    if (ry) *ry = ctx->res_y;
     return DOG_OK;
 }
 

@@ -68,6 +68,8 @@ _SIGS = {
     "dog_profile_begin": ([_vp, C.c_int], C.c_int),
     "dog_profile_end": ([_vp, _vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
+    "dog_ego_scroll": ([_vp, C.c_double, C.c_double, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _vp], C.c_int),
+    "dog_ego_residual": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "dog_create_band": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
                          C.POINTER(dog_band), C.POINTER(_vp)], C.c_int),
     "dog_band_predict": ([_vp, C.c_float, _vp], C.c_int),
@@ -174,6 +176,18 @@ class Filter:
         occ_ptr = occ_host.data_ptr() if occ_host is not None else None
         _check(dog_step_host_async(self._h, meas_host.data_ptr(), dt, occ_ptr, _stream_ptr(stream)),
                "dog_step_host_async")
+
+    def ego_scroll(self, dx: float, dy: float, stream=None) -> tuple[int, int]:
+        """Ego-motion compensation between cycles (include/dog.h); the applied shift in cells."""
+        sx, sy = C.c_int32(), C.c_int32()
+        _check(dog_ego_scroll(self._h, float(dx), float(dy), C.byref(sx), C.byref(sy), _stream_ptr(stream)),
+               "dog_ego_scroll")
+        return sx.value, sy.value
+
+    def ego_residual(self) -> tuple[float, float]:
+        rx, ry = C.c_double(), C.c_double()
+        _check(dog_ego_residual(self._h, C.byref(rx), C.byref(ry)), "dog_ego_residual")
+        return rx.value, ry.value
 
     def sync(self, stream=None) -> int:
         return dog_sync(self._h, _stream_ptr(stream))

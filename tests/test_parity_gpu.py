@@ -79,12 +79,20 @@ def compare_cycle(o, g, rc_gpu=None):
     assert sto["k"] == stg["k"]
 
 
-def run_lockstep(cfg, steps, st=None, frames=None, **over):
+def run_lockstep(cfg, steps, st=None, frames=None, ego=None, **over):
     o, g = pair(cfg, **over)
     if st is not None:
         inject(o, g, st)
     sc = I.scene(cfg) if frames is None else None
     for k in range(steps):
+        if ego is not None and k > 0:                        # ego-motion compensation between cycles (NEXT-2)
+            dx, dy = ego[k]
+            so, sg = o.ego_scroll(dx, dy), g.ego_scroll(dx, dy)
+            assert so == sg, (k, so, sg)
+            assert o.ego_residual() == g.ego_residual(), k
+            a, b = o.get_state(), g.get_state()
+            for key in ("x", "y", "vx", "vy", "m_free"):
+                assert_bits(a[key], b[key], f"ego scroll {k}: {key}")
         meas = frames[k] if frames is not None else sc.frame(k).numpy()
         o.step(meas, cfg.dt)
         g.step(torch.from_numpy(np.ascontiguousarray(meas, np.float32)).cuda(), cfg.dt)
@@ -95,6 +103,16 @@ def run_lockstep(cfg, steps, st=None, frames=None, **over):
 def test_cfg1_lockstep_10_cycles():
     """BASELINE configs[0]: 32x32, 10k + 1k particles, moving box, 10 cycles from the empty state."""
     run_lockstep(I.CONFIGS["cfg1"], 10)
+
+
+def test_ego_motion_compensation():
+    """NEXT-2: the grid and the particles scrolled between cycles (positive, negative, zero and sub-cell
+    deltas; the residual carries over) -- scroll result and every following cycle bit-exact."""
+    rng = np.random.default_rng(11)
+    ego = [tuple(rng.uniform(-0.35, 0.35, 2)) for _ in range(8)]
+    ego[3] = (0.0, 0.0)
+    ego[5] = (0.04, -0.03)
+    run_lockstep(I.CONFIGS["cfg1"], 8, ego=ego)
 
 
 def test_ragged_sizes():
