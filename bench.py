@@ -270,6 +270,28 @@ def bench_ours(args, cfg):
     except Exception as exc:   # noqa: BLE001 -- reported, not fatal to the main line
         ego = {"error": str(exc)}
 
+    # NEXT-4 (evaluation workload): Mahalanobis per cell, 64 ROC thresholds, cluster sums -- device-timed
+    evaluation = None
+    try:
+        labels = torch.ones(cfg.C, dtype=torch.uint8, device=dev)
+        mask = torch.zeros(cfg.C, dtype=torch.uint8, device=dev)
+        mask[: cfg.C // 100] = 1
+        thr = np.logspace(-3, 3, 64).astype(np.float32)
+        f.evaluate(labels=labels, mask=mask, thresholds=thr, stream=stream)          # warm
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = f.evaluate(labels=labels, mask=mask, thresholds=thr, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ev_ms = e0.elapsed_time(e1)
+        ev_bytes = 22.0 * cfg.C                                  # mean 8 + cov 12 + label 1 + mask 1 (+ m 4 out)
+        evaluation = {"ms": ev_ms, "algorithmic_bytes": ev_bytes + 4.0 * cfg.C, "thresholds": 64,
+                      "achieved_GBps": (ev_bytes + 4.0 * cfg.C) / (ev_ms * 1e-3) / 1e9,
+                      "labelled_cells": int(r["counts"][0].sum())}
+    except Exception as exc:   # noqa: BLE001
+        evaluation = {"error": str(exc)}
+
     # per-stage times and roofline of the dominant kernel
     st_avg = {k: v / max(nprof, 1) for k, v in stages.items()}
     kern = {k: v for k, v in st_avg.items() if k != "memset"}
@@ -309,7 +331,7 @@ def bench_ours(args, cfg):
         "stages_ms": {k: round(v, 5) for k, v in st_avg.items()},
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
-        "next_rows": {"ego_scroll": ego},
+        "next_rows": {"ego_scroll": ego, "evaluate": evaluation},
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }

@@ -157,6 +157,22 @@ int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n
 int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t* shift_y, void* stream);
 int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry);
 
+/* ---- evaluation workload (PAPER section VIII, Eqs. 85-88) ----
+ * dog_eval_cells -- per cell c of the context: the Mahalanobis distance m = v P^-1 v^T of the velocity
+ * estimate (mean[c][2], cov[c][3] = var_x, var_y, cov_xy, Eqs. 81-84) from v = 0 (Eq. 88), computed in
+ * fp64 and rounded to f32; P + 1e-6 I when det P <= 1e-12; m = 0 for a cell without moments (DESIGN.md
+ * A-33).  mean_dev / cov_dev: DEVICE readouts (NULL: the filter's own, from its last cycle).  Which cells
+ * have moments: valid_mode 1 = the filter's own record of its last cycle; valid_mode 0 = valid_dev[c] != 0
+ * (u8, device), or if valid_dev is NULL, mean or cov nonzero.  Optional outputs: m_dev[C] (device f32);
+ * with labels_dev[C] (u8: 0 unlabeled, 1 static, 2 dynamic) counts_host[n_thr][4] = (TP, FN, FP, TN) per
+ * threshold thr_host[t] (dynamic detection: m >= thr; n_thr <= 64); with mask_dev[C] (u8: the cluster S)
+ * sums_host[5] = (|S|, sum mean_x, sum var_x + mean_x^2, sum mean_y, sum var_y + mean_y^2) over cells of
+ * S with moments (fp64, summation order unspecified), from which paper_1605_02406_b200/evaluate.py forms
+ * Eqs. 85-87 and the ROC.  Synchronises `stream` when counts or sums are requested. */
+int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, const uint8_t* valid_dev, int valid_mode,
+                   const uint8_t* labels_dev, const uint8_t* mask_dev, const float* thr_host, int n_thr,
+                   float* m_dev, uint64_t* counts_host, double* sums_host, void* stream);
+
 /* dog_read_cells -- copy the readouts of the last completed cycle (posterior, before resampling,
  * P:1444) into caller DEVICE buffers (any may be NULL):
  *   occ[C] = m_O, free_mass[C] = m_F (Eq. 63); vel_mean[C][2] = (mean_vx, mean_vy) (Eq. 81);

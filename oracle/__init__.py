@@ -90,6 +90,8 @@ def _declare(L):
     L.orc_ego_scroll.argtypes = [C.c_void_p, C.c_double, C.c_double, _p(C.c_int32), _p(C.c_int32)]
     L.orc_ego_scroll.restype = C.c_int
     L.orc_ego_residual.argtypes = [C.c_void_p, _p(C.c_double), _p(C.c_double)]
+    L.orc_eval_cells.argtypes = [C.c_int64, f32p, f32p, C.c_void_p, C.c_void_p, C.c_void_p, f32p, C.c_int, f32p,
+                                 u64p, _p(C.c_double)]
     L.orc_read_cells.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p]
     L.orc_get_dump.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t]
     L.orc_get_dump.restype = C.c_int64
@@ -179,6 +181,25 @@ class Params:
         return OrcParams(self.width, self.height, self.cell_size, self.nu, self.nu_b, self.p_s,
                          self.p_b, self.sigma_pos, self.sigma_vel, self.sigma_birth_vel,
                          self.free_tau, self.occ_max, self.v_max, self.seed)
+
+
+def eval_cells(mean, cov, valid=None, labels=None, mask=None, thresholds=()):
+    """Evaluation workload (NEXT-4): per-cell Mahalanobis m (f32), per-threshold (TP, FN, FP, TN), cluster
+    sums (|S|, sum mean_x, sum var_x + mean_x^2, sum mean_y, sum var_y + mean_y^2)."""
+    mean = np.ascontiguousarray(mean, np.float32).reshape(-1, 2)
+    cov = np.ascontiguousarray(cov, np.float32).reshape(-1, 3)
+    Cn = mean.shape[0]
+    u8 = lambda a: None if a is None else np.ascontiguousarray(a, np.uint8).reshape(-1)
+    valid, labels, mask = u8(valid), u8(labels), u8(mask)
+    thr = np.ascontiguousarray(thresholds, np.float32).reshape(-1)
+    m = np.zeros(Cn, np.float32)
+    counts = np.zeros((max(thr.size, 1), 4), np.uint64)
+    sums = np.zeros(5, np.float64)
+    vp = lambda a: None if a is None else a.ctypes.data
+    lib().orc_eval_cells(Cn, _ptr(mean, C.c_float), _ptr(cov, C.c_float), vp(valid), vp(labels), vp(mask),
+                         _ptr(thr, C.c_float) if thr.size else None, int(thr.size), _ptr(m, C.c_float),
+                         _ptr(counts, C.c_uint64), sums.ctypes.data_as(C.POINTER(C.c_double)))
+    return m, counts[:thr.size], sums
 
 
 def step_scalars(p: Params, dt: float) -> np.ndarray:

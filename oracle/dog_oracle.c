@@ -582,3 +582,53 @@ void orc_ego_residual(const orc_ctx* h, double* rx, double* ry)
     if (rx) *rx = h->res_x;
     if (ry) *ry = h->res_y;
 }
+
+/* ======================================================================================
+ * Evaluation workload (PAPER section VIII, SPEC S:456-543 module "evaluation").
+ * Mahalanobis distance (Eq. 88 `eq:mahadist`): m = v P^-1 v^T with P = [[var_x, cov_xy],
+ * [cov_xy, var_y]] from Eqs. 81-84; written out for the 2x2 case in fp64:
+ *   det = var_x var_y - cov_xy^2, m = (v_x^2 var_y - 2 v_x v_y cov_xy + v_y^2 var_x) / det.
+ * Readings (A-33): P is regularised to P + 1e-6 I when det <= 1e-12; a cell
+ * without reported moments has m = 0 (no velocity estimate: static); m is rounded once to f32.
+ * Classification: dynamic detection iff m >= tau_m.  Cluster sums feed Eq. 85
+ * `eq:mean_cluster` and Eq. 86 `eq:gaussian_mixture_x` on the host.
+ * ====================================================================================== */
+void orc_eval_cells(int64_t C, const float* mean, const float* cov, const uint8_t* valid, const uint8_t* labels,
+                    const uint8_t* mask, const float* thr, int n_thr, float* m_out, uint64_t* counts, double* sums)
+{
+    if (counts) memset(counts, 0, sizeof(uint64_t) * 4 * (size_t)(n_thr > 0 ? n_thr : 0));
+    if (sums) for (int i = 0; i < 5; ++i) sums[i] = 0.0;
+    for (int64_t c = 0; c < C; ++c) {
+        const double vx = mean[2 * c], vy = mean[2 * c + 1];
+        double pxx = cov[3 * c], pyy = cov[3 * c + 1];
+        const double pxy = cov[3 * c + 2];
+        const int ok = valid ? valid[c] != 0 : (vx != 0.0 || vy != 0.0 || pxx != 0.0 || pyy != 0.0 || pxy != 0.0);
+        double m = 0.0;
+        if (ok) {
+            double det = pxx * pyy - pxy * pxy;
+            if (det <= 1e-12) {
+                pxx = pxx + 1e-6;
+                pyy = pyy + 1e-6;
+                det = pxx * pyy - pxy * pxy;
+            }
+            const double num = (vx * vx * pyy - 2.0 * vx * vy * pxy) + vy * vy * pxx;
+            m = num / det;
+        }
+        const float mf = (float)m;
+        if (m_out) m_out[c] = mf;
+        if (labels && counts && (labels[c] == 1 || labels[c] == 2)) {
+            const int dyn = labels[c] == 2;
+            for (int t = 0; t < n_thr; ++t) {
+                const int det_dyn = mf >= thr[t];
+                counts[4 * t + (dyn ? (det_dyn ? 0 : 1) : (det_dyn ? 2 : 3))] += 1;
+            }
+        }
+        if (mask && sums && mask[c] && ok) {
+            sums[0] += 1.0;
+            sums[1] += vx;
+            sums[2] += (double)cov[3 * c] + vx * vx;
+            sums[3] += vy;
+            sums[4] += (double)cov[3 * c + 1] + vy * vy;
+        }
+    }
+}

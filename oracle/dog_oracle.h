@@ -89,6 +89,17 @@ int  orc_step(orc_ctx* h, const float* meas, float dt);
  * stored residual (metres); returns -1 (nothing changed) if a shift would reach half the grid side. */
 int  orc_ego_scroll(orc_ctx* h, double dx, double dy, int32_t* shift_x, int32_t* shift_y);
 void orc_ego_residual(const orc_ctx* h, double* rx, double* ry);
+
+/* Evaluation workload (NEXT-4): per-cell Mahalanobis distance of the velocity estimate
+ * from v = 0 (Eq. 88), static/dynamic classification counts per threshold, and the sums behind the
+ * cluster statistics (Eqs. 85-86).  A pure function of the readouts:
+ *   mean[C][2], cov[C][3] (var_x, var_y, cov_xy), valid[C] (moments reported; NULL: mean or cov != 0),
+ *   labels[C] (0 unlabeled, 1 static, 2 dynamic; NULL: no counts), mask[C] (cluster S; NULL: no sums),
+ *   thr[n_thr] -> m[C] (f32, may be NULL), counts[n_thr][4] = (TP, FN, FP, TN) with "dynamic
+ *   detection" = m >= thr, sums[5] = (|S|, sum mean_x, sum (var_x + mean_x^2), sum mean_y,
+ *   sum (var_y + mean_y^2)). */
+void orc_eval_cells(int64_t C, const float* mean, const float* cov, const uint8_t* valid, const uint8_t* labels,
+                    const uint8_t* mask, const float* thr, int n_thr, float* m, uint64_t* counts, double* sums);
 /* readouts of the last step: occ[C], free[C], mean[C][2], cov[C][3] */
 int  orc_read_cells(orc_ctx* h, float* occ, float* free_mass, float* mean, float* cov);
 /* copy a stage dump of the last step; returns bytes copied or <0 */

@@ -19,6 +19,7 @@
 #include "dog_cells.cuh"
 #include "dog_resample.cuh"
 #include "dog_ego.cuh"
+#include "dog_eval.cuh"
 
 using namespace dog;
 
@@ -83,6 +84,8 @@ struct dog_ctx {
     float* meas_dev = nullptr;
     // ego-motion compensation (dog_ego_scroll)
     double res_x = 0.0, res_y = 0.0;
+    unsigned long long* ev_counts = nullptr;      // dog_eval_cells reductions
+    double* ev_sums = nullptr;
     float* m_free_tmp = nullptr;
     // pipelined host entry (dog_step_host_async): double-buffered staging, copy streams, events
     float* hmeas[2] = {nullptr, nullptr};
@@ -354,6 +357,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     }
     AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs);
     if (ctx->world == 1) AL(ctx->m_free_tmp, Cs);   // ego-motion compensation scrolls into it
+    AL(ctx->ev_counts, 4 * kEvalMaxThr); AL(ctx->ev_sums, 5);
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
     AL(ctx->mvalid, Cs / 32 + 1);
     const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
@@ -816,6 +820,34 @@ int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t
                  sx, sy, W, H));
     CK(launch_ex(false, k_ego_particles, 8u * (uint32_t)sms, 256, 0, st, 0, ctx->st, (uint32_t)ctx->nu, sx, sy, W, H));
     std::swap(ctx->m_free, ctx->m_free_tmp);
+    return DOG_OK;
+}
+
+int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, const uint8_t* valid_dev, int valid_mode,
+                   const uint8_t* labels_dev, const uint8_t* mask_dev, const float* thr_host, int n_thr,
+                   float* m_dev, uint64_t* counts_host, double* sums_host, void* stream)
+{
+    if (!ctx || n_thr < 0 || n_thr > kEvalMaxThr || (n_thr && !thr_host) || (valid_mode != 0 && valid_mode != 1))
+        return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const float2* mean = mean_dev ? (const float2*)mean_dev : ctx->mean;   // NULL: the filter's readouts
+    const float* cov = cov_dev ? cov_dev : ctx->cov;
+    EvalThr thr{};
+    for (int t = 0; t < n_thr; ++t) thr.v[t] = thr_host[t];
+    CK(cudaMemsetAsync(ctx->ev_counts, 0, sizeof(unsigned long long) * 4 * kEvalMaxThr, st));
+    CK(cudaMemsetAsync(ctx->ev_sums, 0, sizeof(double) * 5, st));
+    const uint32_t sms = ctx->flat_blocks / 4u;
+    CK(launch_ex(false, k_eval_cells, 4u * sms, 256, 0, st, 0, mean, cov, valid_dev,
+                 valid_mode == 1 ? (const uint32_t*)ctx->mvalid : (const uint32_t*)nullptr, labels_dev, mask_dev, thr,
+                 n_thr, m_dev, ctx->ev_counts, ctx->ev_sums, ctx->C));
+    if (counts_host || sums_host) {
+        if (counts_host) CK(cudaMemcpyAsync(counts_host, ctx->ev_counts, sizeof(uint64_t) * 4 * (size_t)n_thr,
+                                            cudaMemcpyDeviceToHost, st));
+        if (sums_host) CK(cudaMemcpyAsync(sums_host, ctx->ev_sums, sizeof(double) * 5, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
     return DOG_OK;
 }
 

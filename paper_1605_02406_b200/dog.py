@@ -70,6 +70,7 @@ _SIGS = {
     "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
     "dog_ego_scroll": ([_vp, C.c_double, C.c_double, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _vp], C.c_int),
     "dog_ego_residual": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+    "dog_eval_cells": ([_vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp], C.c_int),
     "dog_create_band": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
                          C.POINTER(dog_band), C.POINTER(_vp)], C.c_int),
     "dog_band_predict": ([_vp, C.c_float, _vp], C.c_int),
@@ -188,6 +189,24 @@ class Filter:
         rx, ry = C.c_double(), C.c_double()
         _check(dog_ego_residual(self._h, C.byref(rx), C.byref(ry)), "dog_ego_residual")
         return rx.value, ry.value
+
+    def evaluate(self, labels: torch.Tensor | None = None, mask: torch.Tensor | None = None, thresholds=(),
+                 mean: torch.Tensor | None = None, cov: torch.Tensor | None = None, valid: torch.Tensor | None = None,
+                 stream=None) -> dict:
+        """Evaluation workload (NEXT-4, include/dog.h dog_eval_cells) on the filter's last readouts, or on
+        the given device readouts (mean [C,2], cov [C,3], valid u8 [C]).  Returns the per-cell Mahalanobis
+        distance (device), per-threshold (TP, FN, FP, TN) and the cluster sums."""
+        dev = torch.device("cuda", torch.cuda.current_device())
+        m = torch.empty(self.C, dtype=torch.float32, device=dev)
+        thr = np.ascontiguousarray(thresholds, np.float32).reshape(-1)
+        counts = np.zeros((max(thr.size, 1), 4), np.uint64)
+        sums = np.zeros(5, np.float64)
+        ptr = lambda t: None if t is None else t.data_ptr()
+        own = mean is None
+        _check(dog_eval_cells(self._h, ptr(mean), ptr(cov), ptr(valid), 1 if own else 0, ptr(labels), ptr(mask),
+                              _np_ptr(thr) if thr.size else None, int(thr.size), m.data_ptr(),
+                              _np_ptr(counts), _np_ptr(sums), _stream_ptr(stream)), "dog_eval_cells")
+        return {"m": m, "counts": counts[:thr.size], "sums": sums}
 
     def sync(self, stream=None) -> int:
         return dog_sync(self._h, _stream_ptr(stream))
