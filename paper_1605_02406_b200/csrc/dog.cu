@@ -84,7 +84,8 @@ struct dog_ctx {
     float* meas_dev = nullptr;
     // ego-motion compensation (dog_ego_scroll)
     double res_x = 0.0, res_y = 0.0;
-    unsigned long long* ev_counts = nullptr;      // dog_eval_cells reductions
+    unsigned long long* ev_counts = nullptr;      // dog_eval_cells results
+    EvalAcc* ev_acc = nullptr;                    // dog_eval_cells accumulator (self-resetting)
     double* ev_sums = nullptr;
     float* m_free_tmp = nullptr;
     // pipelined host entry (dog_step_host_async): double-buffered staging, copy streams, events
@@ -308,6 +309,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     cudaFuncSetAttribute(k_predict_sort<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPsSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
+    cudaFuncSetAttribute(k_eval_cells_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEvSmem);
     if (const char* cv = getenv("DOG_RS_CARVEOUT")) {   // experiments: shared-memory share of the L1/smem array
         cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
@@ -357,7 +359,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     }
     AL(ctx->m_free, Cs); AL(ctx->occ, Cs); AL(ctx->fre, Cs);
     if (ctx->world == 1) AL(ctx->m_free_tmp, Cs);   // ego-motion compensation scrolls into it
-    AL(ctx->ev_counts, 4 * kEvalMaxThr); AL(ctx->ev_sums, 5);
+    AL(ctx->ev_counts, 4 * kEvalMaxThr); AL(ctx->ev_sums, 5); AL(ctx->ev_acc, 1);
     AL(ctx->mean, Cs); AL(ctx->cov, 3 * Cs);
     AL(ctx->mvalid, Cs / 32 + 1);
     const size_t LC = (size_t)ctx->cell_blocks * ctx->cell_chunk;   // staging capacity >= C
@@ -402,6 +404,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     if (e == cudaSuccess) e = cudaMemset(ctx->counts, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->npairs, 0, (Cs + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
+    if (e == cudaSuccess) e = cudaMemset(ctx->ev_acc, 0, sizeof(EvalAcc));
 
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -835,13 +838,38 @@ int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, co
     const float2* mean = mean_dev ? (const float2*)mean_dev : ctx->mean;   // NULL: the filter's readouts
     const float* cov = cov_dev ? cov_dev : ctx->cov;
     EvalThr thr{};
-    for (int t = 0; t < n_thr; ++t) thr.v[t] = thr_host[t];
-    CK(cudaMemsetAsync(ctx->ev_counts, 0, sizeof(unsigned long long) * 4 * kEvalMaxThr, st));
-    CK(cudaMemsetAsync(ctx->ev_sums, 0, sizeof(double) * 5, st));
+    int n_sorted = 0;
+    {   // stable ascending sort of the non-NaN thresholds (-0 as +0); pos[t] = sorted position (-1: NaN)
+        int idx[kEvalMaxThr];
+        for (int t = 0; t < n_thr; ++t) { thr.pos[t] = -1; if (thr_host[t] == thr_host[t]) idx[n_sorted++] = t; }
+        std::stable_sort(idx, idx + n_sorted, [&](int a, int b) { return thr_host[a] < thr_host[b]; });
+        for (int p = 0; p < n_sorted; ++p) {
+            const float v = thr_host[idx[p]];
+            thr.v[p] = v == 0.f ? 0.f : v;
+            thr.pos[idx[p]] = (int8_t)p;
+        }
+        // tab[b] = #{sorted thresholds with key < b 2^(32-bits)} (keys nondecreasing along the sorted list)
+        int j = 0;
+        for (int bkt = 0; bkt <= kEvBuckets; ++bkt) {
+            const uint64_t lo = (uint64_t)bkt << (32 - kEvBucketBits);
+            while (j < n_sorted && (uint64_t)eval_key(thr.v[j]) < lo) ++j;
+            thr.tab[bkt] = (uint8_t)j;
+        }
+    }
     const uint32_t sms = ctx->flat_blocks / 4u;
-    CK(launch_ex(false, k_eval_cells, 4u * sms, 256, 0, st, 0, mean, cov, valid_dev,
-                 valid_mode == 1 ? (const uint32_t*)ctx->mvalid : (const uint32_t*)nullptr, labels_dev, mask_dev, thr,
-                 n_thr, m_dev, ctx->ev_counts, ctx->ev_sums, ctx->C));
+    auto al = [](const void* p, uintptr_t a) { return ((uintptr_t)p % a) == 0; };
+    const uint32_t* vbits = valid_mode == 1 ? (const uint32_t*)ctx->mvalid : (const uint32_t*)nullptr;
+    const bool tma = !getenv("DOG_EVAL_NO_TMA") && al(mean, 16) && al(cov, 16) && al(valid_dev, 16) &&
+                     al(labels_dev, 16) && al(mask_dev, 16) && ctx->C >= (uint32_t)kEvT;
+    if (tma) {
+        const uint32_t blocks = std::max<uint32_t>(1u, std::min<uint32_t>(2u * sms, ctx->C / kEvT));
+        CK(launch_ex(false, k_eval_cells_tma, blocks, kEvThreads, kEvSmem, st, 0, mean, cov, valid_dev, vbits,
+                     labels_dev, mask_dev, thr, n_thr, m_dev, ctx->ev_acc, ctx->ev_counts, ctx->ev_sums, ctx->C));
+    } else {
+        const uint32_t blocks = std::max<uint32_t>(1u, std::min<uint32_t>(8u * sms, (ctx->C + 255u) / 256u));
+        CK(launch_ex(false, k_eval_cells, blocks, 256, 0, st, 0, mean, cov, valid_dev, vbits, labels_dev, mask_dev,
+                     thr, n_thr, m_dev, ctx->ev_acc, ctx->ev_counts, ctx->ev_sums, ctx->C));
+    }
     if (counts_host || sums_host) {
         if (counts_host) CK(cudaMemcpyAsync(counts_host, ctx->ev_counts, sizeof(uint64_t) * 4 * (size_t)n_thr,
                                             cudaMemcpyDeviceToHost, st));

@@ -192,12 +192,14 @@ class Filter:
 
     def evaluate(self, labels: torch.Tensor | None = None, mask: torch.Tensor | None = None, thresholds=(),
                  mean: torch.Tensor | None = None, cov: torch.Tensor | None = None, valid: torch.Tensor | None = None,
-                 stream=None) -> dict:
+                 stream=None, fetch: bool = True, m: torch.Tensor | None = None) -> dict:
         """Evaluation workload (NEXT-4, include/dog.h dog_eval_cells) on the filter's last readouts, or on
         the given device readouts (mean [C,2], cov [C,3], valid u8 [C]).  Returns the per-cell Mahalanobis
-        distance (device), per-threshold (TP, FN, FP, TN) and the cluster sums."""
+        distance (device), per-threshold (TP, FN, FP, TN) and the cluster sums.  fetch=False leaves the
+        reductions on the device (no host synchronisation; counts/sums are returned as None)."""
         dev = torch.device("cuda", torch.cuda.current_device())
-        m = torch.empty(self.C, dtype=torch.float32, device=dev)
+        if m is None:
+            m = torch.empty(self.C, dtype=torch.float32, device=dev)
         thr = np.ascontiguousarray(thresholds, np.float32).reshape(-1)
         counts = np.zeros((max(thr.size, 1), 4), np.uint64)
         sums = np.zeros(5, np.float64)
@@ -205,7 +207,10 @@ class Filter:
         own = mean is None
         _check(dog_eval_cells(self._h, ptr(mean), ptr(cov), ptr(valid), 1 if own else 0, ptr(labels), ptr(mask),
                               _np_ptr(thr) if thr.size else None, int(thr.size), m.data_ptr(),
-                              _np_ptr(counts), _np_ptr(sums), _stream_ptr(stream)), "dog_eval_cells")
+                              _np_ptr(counts) if fetch else None, _np_ptr(sums) if fetch else None,
+                              _stream_ptr(stream)), "dog_eval_cells")
+        if not fetch:
+            return {"m": m, "counts": None, "sums": None}
         return {"m": m, "counts": counts[:thr.size], "sums": sums}
 
     def sync(self, stream=None) -> int:
