@@ -230,6 +230,13 @@ const char* dog_profile_stage_name(dog_ctx* ctx, int i);
 int dog_version(void);                 /* ABI version, currently 1 */
 int dog_launches_per_step(dog_ctx* ctx); /* kernels one dog_step launches (bench evidence) */
 
+/* dog_check_transforms -- device self-check of the random-number transforms: the
+ * kernels' range-specialised division and square root inside ln(m 2^-24) and the Box-Muller radius are
+ * compared with IEEE div.rn / sqrt.rn for EVERY odd m in [1, 2^24) (the full input domain).  Writes
+ * host bad[3] = (ln mismatches, sqrt mismatches, first mismatching m or ~0).  Runs on the current
+ * device, synchronously; no context needed. */
+int dog_check_transforms(uint64_t* bad_host);
+
 #ifdef __cplusplus
 }
 #endif

@@ -879,6 +879,19 @@ int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, co
     return DOG_OK;
 }
 
+int dog_check_transforms(uint64_t* bad_host)
+{
+    if (!bad_host) return DOG_E_INVAL;
+    unsigned long long* d = nullptr;
+    const unsigned long long init[3] = {0ull, 0ull, ~0ull};
+    if (cudaMalloc(&d, sizeof(init)) != cudaSuccess) return DOG_E_NOMEM;
+    cudaError_t e = cudaMemcpy(d, init, sizeof(init), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) { k_check_transforms<<<1184, 256>>>(d); e = cudaGetLastError(); }
+    if (e == cudaSuccess) e = cudaMemcpy(bad_host, d, sizeof(init), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? DOG_OK : DOG_E_CUDA;
+}
+
 int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry)
 {
     if (!ctx) return DOG_E_INVAL;

@@ -65,6 +65,7 @@ _SIGS = {
     "dog_set_state": ([_vp, _vp, _vp, _vp, _vp, C.c_float, _vp, C.c_int64], C.c_int),
     "dog_get_debug": ([_vp, C.c_int, _vp, C.c_size_t], C.c_int64),
     "dog_launches_per_step": ([_vp], C.c_int),
+    "dog_check_transforms": ([_vp], C.c_int),
     "dog_profile_begin": ([_vp, C.c_int], C.c_int),
     "dog_profile_end": ([_vp, _vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
@@ -87,6 +88,13 @@ for _name, (_args, _res) in _SIGS.items():
     _f.argtypes = _args
     _f.restype = _res
     globals()[_name] = _f
+
+
+def check_transforms() -> tuple[int, int, int]:
+    """include/dog.h dog_check_transforms: (ln mismatches, sqrt mismatches, first bad m or 2^64-1)."""
+    bad = np.zeros(3, np.uint64)
+    _check(dog_check_transforms(_np_ptr(bad)), "dog_check_transforms")
+    return int(bad[0]), int(bad[1]), int(bad[2])
 
 
 class DogError(RuntimeError):

@@ -245,3 +245,11 @@ def test_full_size_cfgT_one_cycle():
     o.step(meas, cfg.dt)
     g.step(torch.from_numpy(meas).cuda(), cfg.dt)
     compare_cycle(o, g)
+
+
+def test_transforms_exhaustive():
+    """The kernels' range-specialised division and square root (ln spec, Box-Muller radius) equal IEEE
+    div.rn / sqrt.rn on the whole input domain: every odd m in [1, 2^24)."""
+    from paper_1605_02406_b200 import dog
+    bad_ln, bad_sqrt, first = dog.check_transforms()
+    assert (bad_ln, bad_sqrt) == (0, 0), (bad_ln, bad_sqrt, first)
