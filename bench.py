@@ -206,6 +206,16 @@ def bench_ours(args, cfg):
         f.step(frames[settle + W + i], cfg.dt, stream)
         ev1[i].record(stream)
     torch.cuda.synchronize()
+    # continuous operation (the filter at frame rate with nothing in between): K cycles back to back, no
+    # flush (the per-cycle working set, ~0.6 GB at cfg T, exceeds the 126 MB L2)
+    c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
+    flush.zero_()
+    c0.record(stream)
+    for i in range(K):
+        f.step(frames[settle + W + i], cfg.dt, stream)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    cont_ms = c0.elapsed_time(c1) / K
     clk = clocks.stop()
     # per-stage times from a separate, shorter run with stage events between the kernels (the events
     # themselves break the programmatic launch overlap, so they stay out of the timed steps above)
@@ -339,6 +349,8 @@ def bench_ours(args, cfg):
         "roofline": roof, "step_roofline": step_roof,
         "stages_ms": {k: round(v, 5) for k, v in st_avg.items()},
         "cpu_baseline": cpu, "e2e": e2e,
+        "continuous": {"ms_per_step": cont_ms, "value": cfg.nu / (cont_ms * 1e-3), "unit": UNIT,
+                       "note": "K cycles back to back, no flush between them (working set > L2)"},
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
         "next_rows": {"ego_scroll": ego, "evaluate": evaluation},
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,

@@ -232,9 +232,11 @@ int dog_launches_per_step(dog_ctx* ctx); /* kernels one dog_step launches (bench
 
 /* dog_check_transforms -- device self-check of the random-number transforms: the
  * kernels' range-specialised division and square root inside ln(m 2^-24) and the Box-Muller radius are
- * compared with IEEE div.rn / sqrt.rn for EVERY odd m in [1, 2^24) (the full input domain).  Writes
- * host bad[3] = (ln mismatches, sqrt mismatches, first mismatching m or ~0).  Runs on the current
- * device, synchronously; no context needed. */
+ * compared with IEEE div.rn / sqrt.rn for EVERY odd m in [1, 2^24) (the full input domain), and the
+ * packed two-lane Box-Muller used by the predict kernel with two scalar evaluations over every odd m
+ * and every sincos argument n in [0, 2^24).  Writes host bad[4] = (ln mismatches, sqrt mismatches,
+ * packed mismatches, first failing index or ~0).  Runs on the current device, synchronously; no
+ * context needed. */
 int dog_check_transforms(uint64_t* bad_host);
 
 #ifdef __cplusplus

@@ -92,6 +92,9 @@ struct dog_ctx {
     float* hmeas[2] = {nullptr, nullptr};
     float* hocc[2] = {nullptr, nullptr};
     cudaStream_t h2d = nullptr, d2h = nullptr;
+    // births run on a side stream beside resampling (independent outputs; joined before the step ends)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
     int hbuf = 0;
     // profiling: events[step][stage boundary]
@@ -406,6 +409,11 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     if (e == cudaSuccess) e = cudaMemset(ctx->mvalid, 0, (Cs / 32 + 1) * 4);
     if (e == cudaSuccess) e = cudaMemset(ctx->ev_acc, 0, sizeof(EvalAcc));
 
+    if (e == cudaSuccess && ctx->world == 1 && ctx->nu_b > 0 && !getenv("DOG_NO_FORK")) {
+        e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         fprintf(stderr, "libdog: dog_create init failed: %s\n", cudaGetErrorString(e));
@@ -442,6 +450,9 @@ int dog_destroy(dog_ctx* ctx)
             if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     free_all(ctx);
     delete ctx;
     return DOG_OK;
@@ -558,13 +569,26 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     // 5. each cell's runs in tile order -> stable within-cell ranks; global totals (w_bar)
     if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
     CK(mark("pairs"));
-    // 6. persistent particles: moments + resampling copies; births
+    // 6. persistent particles: moments + resampling copies; births.  Births depend only on the list and
+    // the totals (both final here) and write disjoint output slots, so outside profiling they run on the
+    // side stream concurrently with resampling and are joined before the step ends.
+    const bool fork = ctx->side && !prof;
+    if (fork) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        if (int r = L_births(ctx, a, fc, ctx->side)) return r;
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    }
     if (int r = L_resample(ctx, a, fc, st)) return r;
     CK(mark("resample"));
     if (int r = L_moments(ctx, st)) return r;
     CK(mark("moments"));
-    if (int r = L_births(ctx, a, fc, st)) return r;
-    CK(mark("births"));
+    if (fork) {
+        CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    } else {
+        if (int r = L_births(ctx, a, fc, st)) return r;
+        CK(mark("births"));
+    }
     if (prof) {
         ctx->prof_nst = mark_i - 1;
         ctx->prof_steps += 1;
@@ -883,7 +907,7 @@ int dog_check_transforms(uint64_t* bad_host)
 {
     if (!bad_host) return DOG_E_INVAL;
     unsigned long long* d = nullptr;
-    const unsigned long long init[3] = {0ull, 0ull, ~0ull};
+    const unsigned long long init[4] = {0ull, 0ull, 0ull, ~0ull};
     if (cudaMalloc(&d, sizeof(init)) != cudaSuccess) return DOG_E_NOMEM;
     cudaError_t e = cudaMemcpy(d, init, sizeof(init), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) { k_check_transforms<<<1184, 256>>>(d); e = cudaGetLastError(); }

@@ -69,8 +69,7 @@ __device__ __forceinline__ float4 predict_one(float4 X, uint64_t gidx, const Fil
 {
     const Philox4 r = draw(fc.seed, (uint32_t)gidx, a.k, STAGE_PREDICT);
     float n0, n1, n2, n3;
-    box_muller(r.r0, r.r1, n0, n1);
-    box_muller(r.r2, r.r3, n2, n3);
+    box_muller2(r.r0, r.r1, r.r2, r.r3, n0, n1, n2, n3);   // == box_muller(r0, r1), box_muller(r2, r3)
     const float xn = __fmaf_rn(a.s_p, n0, __fmaf_rn(X.z, a.Tc, X.x));
     const float yn = __fmaf_rn(a.s_p, n1, __fmaf_rn(X.w, a.Tc, X.y));
     return make_float4(xn, yn, __fmaf_rn(a.s_v, n2, X.z), __fmaf_rn(a.s_v, n3, X.w));

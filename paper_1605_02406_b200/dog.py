@@ -90,11 +90,12 @@ for _name, (_args, _res) in _SIGS.items():
     globals()[_name] = _f
 
 
-def check_transforms() -> tuple[int, int, int]:
-    """include/dog.h dog_check_transforms: (ln mismatches, sqrt mismatches, first bad m or 2^64-1)."""
-    bad = np.zeros(3, np.uint64)
+def check_transforms() -> tuple[int, int, int, int]:
+    """include/dog.h dog_check_transforms: (ln mismatches, sqrt mismatches, packed Box-Muller mismatches,
+    first failing index or 2^64-1)."""
+    bad = np.zeros(4, np.uint64)
     _check(dog_check_transforms(_np_ptr(bad)), "dog_check_transforms")
-    return int(bad[0]), int(bad[1]), int(bad[2])
+    return tuple(int(b) for b in bad)
 
 
 class DogError(RuntimeError):
