@@ -59,7 +59,7 @@ class OrcParams(C.Structure):
 DUMPS = [
     "PRED_X", "PRED_Y", "PRED_VX", "PRED_VY", "KEY", "PERM", "OFFSETS", "S", "MP", "MFP", "OCC",
     "FREE", "RHO_P", "RHO_B", "RP", "RB", "NB", "BIRTH_X", "BIRTH_Y", "BIRTH_VX", "BIRTH_VY",
-    "BIRTH_CELL", "MEAN", "COV", "JOINT_IDX", "SCALARS",
+    "BIRTH_CELL", "MEAN", "COV", "JOINT_IDX", "SCALARS", "GFX", "GS", "NA", "RBA",
 ]
 DUMP_ID = {n: i + 1 for i, n in enumerate(DUMPS)}
 
@@ -87,6 +87,14 @@ def _declare(L):
     L.orc_set_state.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p, C.c_float, f32p, C.c_int64]
     L.orc_get_state.argtypes = [C.c_void_p, f32p, f32p, f32p, f32p, f32p, f32p, _p(C.c_int64)]
     L.orc_step.argtypes = [C.c_void_p, f32p, C.c_float]; L.orc_step.restype = C.c_int
+    L.orc_step_doppler.argtypes = [C.c_void_p, f32p, C.c_void_p, C.c_void_p, C.c_float]
+    L.orc_step_doppler.restype = C.c_int
+    L.orc_exp_spec.argtypes = [C.c_float]; L.orc_exp_spec.restype = C.c_float
+    L.orc_doppler_g.argtypes = [C.c_float] * 6; L.orc_doppler_g.restype = C.c_float
+    L.orc_doppler_gfx.argtypes = [C.c_float]; L.orc_doppler_gfx.restype = C.c_uint32
+    L.orc_doppler_Q.argtypes = [C.c_uint64, C.c_float, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]
+    L.orc_doppler_Q.restype = C.c_uint64
+    L.orc_birth_assoc.argtypes = [C.c_uint64, C.c_uint32, C.c_float, u32p, u64p]
     L.orc_ego_scroll.argtypes = [C.c_void_p, C.c_double, C.c_double, _p(C.c_int32), _p(C.c_int32)]
     L.orc_ego_scroll.restype = C.c_int
     L.orc_ego_residual.argtypes = [C.c_void_p, _p(C.c_double), _p(C.c_double)]
@@ -150,6 +158,28 @@ def birth_slots(Rb, nu_b: int) -> np.ndarray:
     nb = np.zeros(len(Rb), np.uint32)
     lib().orc_birth_slots(_ptr(Rb, C.c_uint64), len(Rb), nu_b, _ptr(nb, C.c_uint32))
     return nb
+
+
+def exp_spec(q: float) -> float:
+    return lib().orc_exp_spec(q)
+
+
+def doppler_g(vx, vy, ux, uy, vr, sd) -> float:
+    return lib().orc_doppler_g(vx, vy, ux, uy, vr, sd)
+
+
+def doppler_gfx(g: float) -> int:
+    return lib().orc_doppler_gfx(g)
+
+
+def doppler_Q(Rp: int, pA: float, GSj: int, GS: int, j: int, n: int) -> int:
+    return lib().orc_doppler_Q(Rp, pA, GSj, GS, j, n)
+
+
+def birth_assoc(Rb: int, nb: int, pA: float):
+    na, ra = C.c_uint32(), C.c_uint64()
+    lib().orc_birth_assoc(Rb, nb, pA, C.byref(na), C.byref(ra))
+    return na.value, ra.value
 
 
 def systematic_resample(q, nu: int, U: int):
@@ -247,6 +277,17 @@ class Oracle:
         assert m.size == 2 * self.C
         return lib().orc_step(self._h, _ptr(m, C.c_float), C.c_float(dt))
 
+    def step_doppler(self, meas: np.ndarray, dop, pA, dt: float) -> int:
+        """NEXT-1 cycle: dop [C,4] = (u_x, u_y, v_r, sd), pA [C] association probability (0: none)."""
+        m = np.ascontiguousarray(meas, dtype=np.float32).reshape(-1)
+        assert m.size == 2 * self.C
+        d = None if dop is None else np.ascontiguousarray(dop, dtype=np.float32).reshape(-1)
+        a = None if pA is None else np.ascontiguousarray(pA, dtype=np.float32).reshape(-1)
+        assert d is None or d.size == 4 * self.C
+        assert a is None or a.size == self.C
+        return lib().orc_step_doppler(self._h, _ptr(m, C.c_float), None if d is None else d.ctypes.data,
+                                      None if a is None else a.ctypes.data, C.c_float(dt))
+
     def ego_scroll(self, dx: float, dy: float):
         """Ego-motion compensation (NEXT-2): (shift_x, shift_y) in cells, or None if refused."""
         sx, sy = C.c_int32(), C.c_int32()
@@ -272,14 +313,15 @@ class Oracle:
         "RHO_P": np.float32, "RHO_B": np.float32, "RP": np.uint64, "RB": np.uint64,
         "NB": np.uint32, "BIRTH_X": np.float32, "BIRTH_Y": np.float32, "BIRTH_VX": np.float32,
         "BIRTH_VY": np.float32, "BIRTH_CELL": np.uint32, "MEAN": np.float32, "COV": np.float32,
-        "JOINT_IDX": np.uint32, "SCALARS": np.uint64,
+        "JOINT_IDX": np.uint32, "SCALARS": np.uint64, "GFX": np.uint32, "GS": np.uint64, "NA": np.uint32,
+        "RBA": np.uint64,
     }
 
     def dump(self, name: str) -> np.ndarray:
         nu, nb, Cc = self.p.nu, self.p.nu_b, self.C
         n = {"OFFSETS": Cc + 1, "MEAN": 2 * Cc, "COV": 3 * Cc, "SCALARS": 8}.get(name)
         if n is None:
-            if name.startswith("PRED") or name in ("KEY", "PERM", "JOINT_IDX"):
+            if name.startswith("PRED") or name in ("KEY", "PERM", "JOINT_IDX", "GFX"):
                 n = nu
             elif name.startswith("BIRTH"):
                 n = nb

@@ -118,6 +118,76 @@ void orc_box_muller(uint32_t ra, uint32_t rb, float* z0, float* z1)
     *z1 = rho * s;
 }
 
+/* exp(q) for q <= 0 -- DESIGN.md A-34 "exp spec": q < -87 -> 0 (no subnormals); otherwise
+ * k = rint(q log2 e), r = (q - k ln2_hi) - k ln2_lo (two fma), e^r = 1 + r + r^2 P(r) with the cephes
+ * expf coefficients (fma Horner), times 2^k (exact power of two).  IEEE single operations only. */
+float orc_exp_spec(float q)
+{
+    if (!(q >= -87.0f)) return 0.0f;
+    if (q > 0.0f) q = 0.0f;
+    float kf = rintf(q * 1.44269504088896341f);
+    float r = fmaf(-kf, 0.693359375f, q);
+    r = fmaf(-kf, -2.12194440e-4f, r);
+    float z = r * r;
+    float y = 1.9875691500e-4f;
+    y = fmaf(y, r, 1.3981999507e-3f);
+    y = fmaf(y, r, 8.3334519073e-3f);
+    y = fmaf(y, r, 4.1665795894e-2f);
+    y = fmaf(y, r, 1.6666665459e-1f);
+    y = fmaf(y, r, 5.0000001201e-1f);
+    y = fmaf(y, z, r);
+    y = y + 1.0f;
+    int k = (int)kf;                       /* -126 <= k <= 0 here */
+    uint32_t bits = (uint32_t)(127 + k) << 23;
+    float scale; memcpy(&scale, &bits, 4);
+    return y * scale;
+}
+
+/* Doppler likelihood g(z|x) of a predicted velocity (NEXT-1; Eq. 69):
+ * Gaussian density of e = v . u - v_r with SD sd, in this operation order (A-34):
+ * e = fma(vx, ux, vy*uy) - v_r; t = e / sd; g = exp_spec((t*t) * -0.5) / (sd * sqrt(2 pi)). */
+float orc_doppler_g(float vx, float vy, float ux, float uy, float vr, float sd)
+{
+    float e = fmaf(vx, ux, vy * uy) - vr;
+    float t = e / sd;
+    float q = (t * t) * -0.5f;
+    return orc_exp_spec(q) / (sd * 2.50662827463100050f);
+}
+
+/* Fixed-point likelihood gfx = floor(min(g, 256 - 2^-16) 2^24) (u32, A-34): sums over a cell are
+ * exact integers, so they do not depend on summation order. */
+uint32_t orc_doppler_gfx(float g)
+{
+    float gc = g < 0x1.fffffep+7f ? g : 0x1.fffffep+7f;
+    if (!(gc > 0.0f)) return 0u;
+    return (uint32_t)(gc * 16777216.0f);
+}
+
+/* Cumulative weight fraction of member j of n in a Doppler cell (Eqs. 71-73 with p_A > 0, A-35):
+ * G_j = p_A GS_j / GS + (1 - p_A) j / n in fp64 (one fma); Q_j = floor(R_p G_j).  G_0 = 0, G_n = 1
+ * exactly, and G is nondecreasing in j, so the members' weights Q_{j+1} - Q_j sum to R_p exactly. */
+uint64_t orc_doppler_Q(uint64_t Rp, float pA, uint64_t GSj, uint64_t GS, uint32_t j, uint32_t n)
+{
+    double pa = (double)pA;
+    double a = (double)GSj / (double)GS;
+    double b = (1.0 - pa) * ((double)j / (double)n);
+    double G = fma(pa, a, b);
+    return (uint64_t)((double)Rp * G);
+}
+
+/* Split of a cell's nb birth slots and born mass into the associated (A) and unassociated (A-bar)
+ * sets (Eqs. 74-80; A-36): nu_A = floor(p_A nb + 1/2) (round half up), R_bA =
+ * floor(R_b p_A) in fp64 (0 if nu_A = 0, R_b if nu_A = nb). */
+void orc_birth_assoc(uint64_t Rb, uint32_t nb, float pA, uint32_t* nA, uint64_t* RbA)
+{
+    uint32_t na = (uint32_t)floor((double)pA * (double)nb + 0.5);
+    if (na > nb) na = nb;
+    uint64_t ra = (uint64_t)((double)Rb * (double)pA);
+    if (na == 0) ra = 0;
+    else if (na == nb) ra = Rb;
+    *nA = na; *RbA = ra;
+}
+
 /* ======================================================================================
  * Dempster's rule on {O, F, Omega} (Eq. 63 `eq:DS_comb`; A-10) in the canonical
  * operation order of DESIGN.md 3.2.  Total conflict (1-K <= 0) returns the measurement BBA.
@@ -228,6 +298,10 @@ struct orc_ctx {
     uint32_t* bcell;
     float *mean, *cov;
     uint32_t* jidx;
+    uint32_t* gfx;           /* [nu] fixed-point Doppler likelihood of each predicted particle (NEXT-1) */
+    uint64_t* GS;            /* [C] its sum over the cell's members                            */
+    uint32_t* nA;            /* [C] associated birth slots (NEXT-1)                            */
+    uint64_t* RbA;           /* [C] born mass of the associated set                            */
     uint64_t scal[8];
     double res_x, res_y;     /* ego-motion residual, metres (NEXT-2) */
 };
@@ -261,6 +335,7 @@ int orc_create(const orc_params* p, orc_ctx** out)
     h->bcell = xcalloc(nb, 4);
     h->mean = xcalloc(2 * C, 4); h->cov = xcalloc(3 * C, 4);
     h->jidx = xcalloc(nu, 4);
+    h->gfx = xcalloc(nu, 4); h->GS = xcalloc(C, 8); h->nA = xcalloc(C, 4); h->RbA = xcalloc(C, 8);
     *out = h;
     return 0;
 }
@@ -271,7 +346,7 @@ void orc_destroy(orc_ctx* h)
     void* ptrs[] = { h->x, h->y, h->vx, h->vy, h->m_free, h->px, h->py, h->pvx, h->pvy, h->key,
                      h->perm, h->offsets, h->S, h->mp, h->mfp, h->occ, h->fre, h->rho_p, h->rho_b,
                      h->Rp, h->Rb, h->nb, h->bx, h->by, h->bvx, h->bvy, h->bcell, h->mean, h->cov,
-                     h->jidx };
+                     h->jidx, h->gfx, h->GS, h->nA, h->RbA };
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) free(ptrs[i]);
     free(h);
 }
@@ -311,6 +386,14 @@ static int cmp_kv(const void* a, const void* b)
 }
 
 int orc_step(orc_ctx* h, const float* meas, float dt)
+{
+    return orc_step_doppler(h, meas, NULL, NULL, dt);
+}
+
+/* One cycle with the Doppler / association branch (NEXT-1).  dop[C][4] = (u_x, u_y, v_r, sd): unit
+ * radial direction, measured radial speed (m/s), its SD; pA[C] = association probability p_A (0: the
+ * cell has no Doppler measurement).  dop == NULL or pA == NULL: no cell has one (orc_step). */
+int orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const float* pA, float dt)
 {
     const orc_params* P = &h->p;
     const int64_t W = P->width, H = P->height, C = h->C, nu = P->nu, nu_b = P->nu_b;
@@ -373,23 +456,59 @@ int orc_step(orc_ctx* h, const float* meas, float dt)
         h->Rb[c] = (zO > 0.0f) ? fx40(rb) : 0;                 /* P:1197 gate (A-13) */
     }
 
-    /* ---- O4 Persistent update (Alg. 4; Eqs. 71, 73 with p_A = 0, g = 1) and
-     *      O6 Moments (Alg. 6; Eqs. 81-84; A-18) ---- */
+    /* ---- O4 Persistent update (Alg. 4; Eqs. 69-73) and
+     *      O6 Moments (Alg. 6; Eqs. 81-84; A-18) ----
+     * Cells without Doppler (p_A = 0, g = 1): every member has w = mu_Abar w_pred (Eq. 71).  Doppler
+     * cells (p_A > 0, NEXT-1): w~ = g w_pred (Eq. 69) with g from orc_doppler_g, held as fixed-point
+     * gfx; the members' fixed-point weights are the differences of Q_j (orc_doppler_Q, A-35), and the
+     * moments weight each member by q_j / R_p.  Sum of gfx = 0 (no member compatible with the
+     * measurement): the mu_A term is dropped -- the cell is treated as p_A = 0. */
+    for (int64_t i = 0; i < nu; ++i) h->gfx[i] = 0u;
+    for (int64_t c = 0; c < C; ++c) {
+        uint32_t a = h->offsets[c], b = h->offsets[c + 1];
+        h->GS[c] = 0;
+        if (!(dop && pA && pA[c] > 0.0f)) continue;
+        const float* d = dop + 4 * c;
+        uint64_t gs = 0;
+        for (uint32_t j = a; j < b; ++j) {
+            uint32_t i = h->perm[j];
+            h->gfx[i] = orc_doppler_gfx(orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]));
+            gs += h->gfx[i];
+        }
+        h->GS[c] = gs;
+    }
     for (int64_t c = 0; c < C; ++c) {
         uint32_t a = h->offsets[c], b = h->offsets[c + 1];
         float* mean = h->mean + 2 * c; float* cov = h->cov + 3 * c;
         mean[0] = mean[1] = 0.0f; cov[0] = cov[1] = cov[2] = 0.0f;
         float rp = h->rho_p[c], S = h->S[c];
         if (b == a || !(rp > 0.0f) || !(S > 0.0f)) continue;
-        double Mx = 0, My = 0, Mxx = 0, Myy = 0, Mxy = 0;
-        for (uint32_t j = a; j < b; ++j) {
-            uint32_t i = h->perm[j];
-            float w = (rp / S) * w_pred;                       /* Eq. 71: w = mu_Abar w_pred */
-            double wd = (double)w, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
-            Mx += wd * vx; My += wd * vy;
-            Mxx += wd * vx * vx; Myy += wd * vy * vy; Mxy += wd * vx * vy;
+        double Mx = 0, My = 0, Mxx = 0, Myy = 0, Mxy = 0, rd;
+        if (h->GS[c] > 0) {                                    /* Doppler cell: weights q_j / R_p */
+            const uint32_t n = b - a;
+            const uint64_t Rp = h->Rp[c], GS = h->GS[c];
+            if (Rp == 0) continue;
+            uint64_t gsj = 0, Qj = 0;
+            for (uint32_t j = 0; j < n; ++j) {
+                uint32_t i = h->perm[a + j];
+                gsj += h->gfx[i];
+                uint64_t Qn = orc_doppler_Q(Rp, pA[c], gsj, GS, j + 1, n);
+                double wd = (double)(Qn - Qj) * 0x1p-40, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
+                Mx += wd * vx; My += wd * vy;
+                Mxx += wd * vx * vx; Myy += wd * vy * vy; Mxy += wd * vx * vy;
+                Qj = Qn;
+            }
+            rd = (double)Rp * 0x1p-40;
+        } else {
+            for (uint32_t j = a; j < b; ++j) {
+                uint32_t i = h->perm[j];
+                float w = (rp / S) * w_pred;                   /* Eq. 71: w = mu_Abar w_pred */
+                double wd = (double)w, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
+                Mx += wd * vx; My += wd * vy;
+                Mxx += wd * vx * vx; Myy += wd * vy * vy; Mxy += wd * vx * vy;
+            }
+            rd = (double)rp;
         }
-        double rd = (double)rp;
         double mx = Mx / rd, my = My / rd;
         mean[0] = (float)mx; mean[1] = (float)my;
         cov[0] = (float)(Mxx / rd - mx * mx);
@@ -397,10 +516,17 @@ int orc_step(orc_ctx* h, const float* meas, float dt)
         cov[2] = (float)(Mxy / rd - mx * my);
     }
 
-    /* ---- O5 Births (Alg. 5; Eq. 77; A-14..A-17) ---- */
+    /* ---- O5 Births (Alg. 5; Eqs. 74-80; A-14..A-17, A-36) ----
+     * Slot r of cell c: r < nu_A -> associated set (NEXT-1): velocity from p(x|z), radial component
+     * v_r + sd n0 along u, tangential sigma_B n1 along u_perp = (-u_y, u_x); otherwise the birth prior
+     * N(0, sigma_B^2) per axis.  Positions uniform in the cell for both. */
     uint64_t A = orc_birth_slots(h->Rb, C, nu_b, h->nb);
     for (int64_t j = 0; j < nu_b; ++j) {
         h->bx[j] = h->by[j] = h->bvx[j] = h->bvy[j] = 0.0f; h->bcell[j] = (uint32_t)C;
+    }
+    for (int64_t c = 0; c < C; ++c) {
+        h->nA[c] = 0; h->RbA[c] = 0;
+        if (dop && pA && pA[c] > 0.0f && h->nb[c] > 0) orc_birth_assoc(h->Rb[c], h->nb[c], pA[c], &h->nA[c], &h->RbA[c]);
     }
     {
         int64_t j = 0;
@@ -416,7 +542,16 @@ int orc_step(orc_ctx* h, const float* meas, float dt)
                 if (byv >= rowf + 1.0f) byv = nextafterf(rowf + 1.0f, 0.0f);
                 float n0, n1;
                 orc_box_muller(R[2], R[3], &n0, &n1);
-                float bvx = P->sigma_birth_vel * n0, bvy = P->sigma_birth_vel * n1;
+                float bvx, bvy;
+                if (r < h->nA[c]) {                            /* associated: p(x | z), Eq. 74 */
+                    const float* d = dop + 4 * c;
+                    float sr = fmaf(d[3], n0, d[2]);           /* radial speed */
+                    float st = P->sigma_birth_vel * n1;        /* tangential speed */
+                    bvx = fmaf(sr, d[0], -(st * d[1]));
+                    bvy = fmaf(sr, d[1], st * d[0]);
+                } else {                                       /* unassociated: birth prior, Eq. 76 */
+                    bvx = P->sigma_birth_vel * n0; bvy = P->sigma_birth_vel * n1;
+                }
                 if (P->v_max > 0.0f) {
                     bvx = fminf(fmaxf(bvx, -P->v_max), P->v_max);
                     bvy = fminf(fmaxf(bvy, -P->v_max), P->v_max);
@@ -439,13 +574,27 @@ int orc_step(orc_ctx* h, const float* meas, float dt)
         int64_t jj = 0, slot = 0;
         for (int64_t c = 0; c < C; ++c) {
             uint32_t a = h->offsets[c], b = h->offsets[c + 1], n = b - a;
-            for (uint32_t r = 0; r < n; ++r, ++jj) {
-                q[jj] = h->Rp[c] / n + ((uint64_t)r < h->Rp[c] % n ? 1u : 0u);
-                src[jj] = h->perm[a + r];
+            if (h->GS[c] > 0) {                                /* Doppler cell (A-35) */
+                uint64_t gsj = 0, Qj = 0;
+                for (uint32_t r = 0; r < n; ++r, ++jj) {
+                    gsj += h->gfx[h->perm[a + r]];
+                    uint64_t Qn = orc_doppler_Q(h->Rp[c], pA[c], gsj, h->GS[c], r + 1, n);
+                    q[jj] = Qn - Qj;
+                    Qj = Qn;
+                    src[jj] = h->perm[a + r];
+                }
+            } else {
+                for (uint32_t r = 0; r < n; ++r, ++jj) {
+                    q[jj] = h->Rp[c] / n + ((uint64_t)r < h->Rp[c] % n ? 1u : 0u);
+                    src[jj] = h->perm[a + r];
+                }
             }
-            uint32_t m = h->nb[c];
+            /* births: the associated set first (nu_A slots sharing R_bA), then the unassociated set */
+            uint32_t m = h->nb[c], mA = h->nA[c], mB = m - mA;
+            uint64_t RA = h->RbA[c], RB = h->Rb[c] - RA;
             for (uint32_t r = 0; r < m; ++r, ++jj, ++slot) {
-                q[jj] = h->Rb[c] / m + ((uint64_t)r < h->Rb[c] % m ? 1u : 0u);
+                if (r < mA) q[jj] = RA / mA + ((uint64_t)r < RA % mA ? 1u : 0u);
+                else q[jj] = RB / mB + ((uint64_t)(r - mA) < RB % mB ? 1u : 0u);
                 src[jj] = -1 - slot;
             }
         }
@@ -524,6 +673,10 @@ int64_t orc_get_dump(orc_ctx* h, int what, void* dst, size_t bytes)
     case ORC_COV: src = h->cov; n = 3 * C * 4; break;
     case ORC_JOINT_IDX: src = h->jidx; n = nu * 4; break;
     case ORC_SCALARS: src = h->scal; n = 8 * 8; break;
+    case ORC_GFX: src = h->gfx; n = nu * 4; break;
+    case ORC_GS: src = h->GS; n = C * 8; break;
+    case ORC_NA: src = h->nA; n = C * 4; break;
+    case ORC_RBA: src = h->RbA; n = C * 8; break;
     default: return -1;
     }
     if (bytes < n) return -2;

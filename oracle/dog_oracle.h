@@ -58,7 +58,11 @@ enum {
     ORC_MEAN,         /* f32 [C][2] (Eq. 81)                                           */
     ORC_COV,          /* f32 [C][3] var_x, var_y, cov_xy (Eqs. 83-84)                  */
     ORC_JOINT_IDX,    /* u32 [nu] selected joint index j(i) (Alg. 7, A-24, A-25)       */
-    ORC_SCALARS       /* u64 [8]: W, U, A, meas_bad_count, w_pred bits, w_bar bits, k, n_in */
+    ORC_SCALARS,      /* u64 [8]: W, U, A, meas_bad_count, w_pred bits, w_bar bits, k, n_in */
+    ORC_GFX,          /* u32 [nu] fixed-point Doppler likelihood, input order (NEXT-1, A-34) */
+    ORC_GS,           /* u64 [C] its sum over the cell's members (0: no Doppler / guard)  */
+    ORC_NA,           /* u32 [C] associated birth slots nu_A (A-36)                    */
+    ORC_RBA           /* u64 [C] born mass of the associated set R_bA (A-36)           */
 };
 
 /* --- primitives (exported for the pins in tests/) --- */
@@ -85,6 +89,16 @@ int  orc_get_state(orc_ctx* h, float* x, float* y, float* vx, float* vy, float* 
                    float* m_free, int64_t* k);
 /* meas: float[C][2] = (m_zO, m_zF) row-major; dt > 0 seconds */
 int  orc_step(orc_ctx* h, const float* meas, float dt);
+/* Doppler / association branch (NEXT-1; Eqs. 69-80):
+ * dop[C][4] = (u_x, u_y, v_r, sd) radial unit direction, measured radial speed (m/s) and its SD;
+ * pA[C] = association probability p_A in [0, 1] (0: no Doppler in the cell).  NULL: orc_step. */
+int  orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const float* pA, float dt);
+/* NEXT-1 primitives (exported for the pins) */
+float    orc_exp_spec(float q);                                             /* e^q, q <= 0 (A-34) */
+float    orc_doppler_g(float vx, float vy, float ux, float uy, float vr, float sd);   /* Eq. 69 g */
+uint32_t orc_doppler_gfx(float g);                                          /* floor(g 2^24)      */
+uint64_t orc_doppler_Q(uint64_t Rp, float pA, uint64_t GSj, uint64_t GS, uint32_t j, uint32_t n);
+void     orc_birth_assoc(uint64_t Rb, uint32_t nb, float pA, uint32_t* nA, uint64_t* RbA);
 /* Ego-motion compensation (NEXT-2): scroll grid and particles by the whole-cell part of (dx, dy) plus the
  * stored residual (metres); returns -1 (nothing changed) if a shift would reach half the grid side. */
 int  orc_ego_scroll(orc_ctx* h, double dx, double dy, int32_t* shift_x, int32_t* shift_y);
