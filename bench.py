@@ -261,6 +261,34 @@ def bench_ours(args, cfg):
                         "pinned host on a second copy stream; overlapped across cycles; wall clock incl. final sync)",
                "sync_entry_ms_per_step": sync_ms}
 
+    # NEXT-1 (Doppler / association branch): cycles with a radar overlay on half the occupied cells,
+    # device-timed like the main line (L2 flushed between cycles); continues the same filter
+    doppler = None
+    try:
+        nd = min(K, 10)
+        dops = [sc.doppler(settle + W + i, frames[settle + W + i], frac=0.5, p_assoc=0.8, sd=0.25, device=dev)
+                for i in range(nd)]
+        for i in range(2):
+            f.step_doppler(frames[settle + W + i], dops[i][0], dops[i][1], cfg.dt, stream)
+        torch.cuda.synchronize()
+        d0 = [torch.cuda.Event(enable_timing=True) for _ in range(nd)]
+        d1 = [torch.cuda.Event(enable_timing=True) for _ in range(nd)]
+        for i in range(nd):
+            flush.zero_()
+            d0[i].record(stream)
+            f.step_doppler(frames[settle + W + i], dops[i][0], dops[i][1], cfg.dt, stream)
+            d1[i].record(stream)
+        torch.cuda.synchronize()
+        dms = float(np.mean([d0[i].elapsed_time(d1[i]) for i in range(nd)]))
+        dop_bytes = a_alg(cfg) + 20.0 * cfg.C                  # + the Doppler grid (16 B + p_A 4 B per cell)
+        doppler = {"ms_per_step": dms, "value": cfg.nu / (dms * 1e-3), "unit": UNIT,
+                   "doppler_cells": int(sum(int((d[1] > 0).sum()) for d in dops) / nd),
+                   "algorithmic_bytes": dop_bytes, "achieved_GBps": dop_bytes / (dms * 1e-3) / 1e9,
+                   "frac": dop_bytes / (dms * 1e-3) / 1e9 / peaks()[0],
+                   "input": "radar overlay on 50 % of the occupied cells, p_A 0.8, sd 0.25 m/s (inputs.Scene.doppler)"}
+    except Exception as exc:   # noqa: BLE001
+        doppler = {"error": str(exc)}
+
     # NEXT-2 (ego-motion compensation): one scroll of grid and particles at this size, device-timed
     ego = None
     try:
@@ -352,7 +380,7 @@ def bench_ours(args, cfg):
         "continuous": {"ms_per_step": cont_ms, "value": cfg.nu / (cont_ms * 1e-3), "unit": UNIT,
                        "note": "K cycles back to back, no flush between them (working set > L2)"},
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
-        "next_rows": {"ego_scroll": ego, "evaluate": evaluation},
+        "next_rows": {"doppler": doppler, "ego_scroll": ego, "evaluate": evaluation},
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }

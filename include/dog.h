@@ -173,6 +173,20 @@ int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, co
                    const uint8_t* labels_dev, const uint8_t* mask_dev, const float* thr_host, int n_thr,
                    float* m_dev, uint64_t* counts_host, double* sums_host, void* stream);
 
+/* dog_step_doppler -- one cycle with the Doppler / association branch (Eqs. 69-80,
+ * P:1157-1232; A-34..A-36).  As dog_step, plus two DEVICE arrays:
+ *   doppler[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) per cell -- unit radial direction, measured
+ *                 radial speed (m/s) and its SD (> 0), read only where p_assoc > 0;
+ *   p_assoc[C]    f32: association probability p_A in [0, 1]; 0 = the cell has no Doppler measurement.
+ * In a cell with p_A > 0 the persistent members are weighted by the Doppler likelihood g of their
+ * predicted velocity (Eq. 71: w = p_A mu_A g w + (1 - p_A) mu_Abar w; A-35) and its birth slots split
+ * into associated (velocity drawn around the measured radial speed) and unassociated ones (A-36).
+ * p_assoc all 0 gives exactly dog_step's cycle.  Whole-grid contexts only (DOG_E_STATE for bands);
+ * the three working buffers (16 B per particle slot + 8 B per cell) are allocated on first use
+ * (DOG_E_NOMEM).  DOG_E_INVAL for a NULL or misaligned argument or an invalid dt. */
+int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, const float* p_assoc, float dt,
+                     void* stream);
+
 /* dog_read_cells -- copy the readouts of the last completed cycle (posterior, before resampling,
  * P:1444) into caller DEVICE buffers (any may be NULL):
  *   occ[C] = m_O, free_mass[C] = m_F (Eq. 63); vel_mean[C][2] = (mean_vx, mean_vy) (Eq. 81);

@@ -9,7 +9,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.environ.get("DOG_CSRC") or os.path.join(PKG, "csrc")   # DOG_CSRC: alternative sources (A/B)
 LIB = os.environ.get("DOG_LIB") or os.path.join(PKG, "libdog.so")
 SOURCES = ["dog.cu"]
-HEADERS = ["dog_common.cuh", "dog_rng.cuh", "dog_kernels.cuh", "dog_cells.cuh", "dog_resample.cuh", "dog_sort.cuh", "dog_fcount.cuh", "dog_ego.cuh", "dog_eval.cuh"]
+HEADERS = ["dog_common.cuh", "dog_rng.cuh", "dog_kernels.cuh", "dog_cells.cuh", "dog_resample.cuh", "dog_sort.cuh", "dog_fcount.cuh", "dog_ego.cuh", "dog_eval.cuh", "dog_doppler.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -20,6 +20,7 @@
 #include "dog_resample.cuh"
 #include "dog_ego.cuh"
 #include "dog_eval.cuh"
+#include "dog_doppler.cuh"
 
 using namespace dog;
 
@@ -93,6 +94,10 @@ struct dog_ctx {
     float* hocc[2] = {nullptr, nullptr};
     cudaStream_t h2d = nullptr, d2h = nullptr;
     // births run on a side stream beside resampling (independent outputs; joined before the step ends)
+    // Doppler / association branch (NEXT-1), allocated on the first dog_step_doppler
+    uint64_t* d_rg = nullptr;                     // per run slot: gfx sum, then exclusive cell prefix
+    uint64_t* d_rs = nullptr;                     // per run slot: block prefix at the run's first member
+    uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
@@ -451,6 +456,9 @@ int dog_destroy(dog_ctx* ctx)
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->d_rg) cudaFree(ctx->d_rg);
+    if (ctx->d_rs) cudaFree(ctx->d_rs);
+    if (ctx->d_GS) cudaFree(ctx->d_GS);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     free_all(ctx);
@@ -520,21 +528,22 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     return DOG_OK;
 }
 
-static int L_moments(dog_ctx* ctx, cudaStream_t st)
+static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullptr)
 {
     CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
-              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc));
+              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
     return DOG_OK;
 }
 
-static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
+                    const DopIn* din = nullptr)
 {
     if (ctx->nu_b == 0) return DOG_OK;
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
     CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
-              (int64_t)a.k));
+              (int64_t)a.k, din ? din->pA : (const float*)nullptr, din ? din->dop : (const float4*)nullptr));
     return DOG_OK;
 }
 
@@ -593,6 +602,44 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
         ctx->prof_nst = mark_i - 1;
         ctx->prof_steps += 1;
     }
+    ctx->k += 1;
+    return DOG_OK;
+}
+
+// ---- Doppler / association branch (NEXT-1): the cycle with per-member weights in Doppler cells
+int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, const float* p_assoc, float dt,
+                     void* stream)
+{
+    if (!ctx || !meas || !doppler || !p_assoc) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1) return DOG_E_STATE;                 // whole-grid contexts only
+    if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
+    if (((uintptr_t)doppler & 15u) != 0) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!ctx->d_rg) {
+        if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
+            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess)
+            return DOG_E_NOMEM;
+    }
+    const StepArgs a = step_args(ctx, dt);
+    const FilterConst fc = filter_const(ctx);
+    const DopIn din{(const float4*)doppler, p_assoc};
+    const int par = (int)(a.k & 1);
+    if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
+    if (int r = L_cells(ctx, meas, a, fc, st)) return r;
+    if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
+    if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
+    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
+              din, ctx->d_rg, (const DevScalars*)ctx->sc, fc, par));
+    CK(launch(k_dopp_cells, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist, din, ctx->d_rg,
+              ctx->d_GS, (const DevScalars*)ctx->sc));
+    NextState ns{ctx->st, nullptr};
+    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, sizeof(RdSmem), st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+                 (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
+                 (const uint64_t*)ctx->d_GS, (const DevScalars*)ctx->sc, fc, par));
+    if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
+    if (int r = L_births(ctx, a, fc, st, &din)) return r;
     ctx->k += 1;
     return DOG_OK;
 }

@@ -1,0 +1,311 @@
+// dog_doppler.cuh -- the Doppler / association branch of the cycle (Eqs. 69-80,
+// P:1157-1232; A-34..A-36).  Measurement cells may carry a radial-velocity measurement
+// (u, v_r, sd) with association probability p_A > 0.  Then:
+//   * persistent members get w~ = g w_pred (Eq. 69) and w = p_A mu_A w~ + (1 - p_A) mu_Abar w_pred
+//     (Eqs. 71-73): member j of the cell owns [Q_j, Q_{j+1}) of the cell's fixed-point mass R_p with
+//     Q_j = floor(R_p G_j), G_j = fma(p_A, GS_j / GS, (1 - p_A) j / n) (A-35), GS_j the exclusive
+//     prefix of the fixed-point likelihoods gfx = floor(g 2^24) (A-34) in cell order;
+//   * the cell's nu_b birth slots split into nu_A associated slots (velocity from p(x | z)) and
+//     nu_b - nu_A unassociated ones, sharing R_bA and R_b - R_bA (A-36).
+// Weights are no longer uniform within a cell, so the closed-form per-run resampling of
+// k_resample_tiles does not apply; this path uses
+//   k_dopp_runs    per tile: gfx of every member, summed per run (integer atomics: order-free)
+//   k_dopp_cells   per active cell: the runs' gfx sums in tile order -> exclusive prefixes, cell total GS
+//   k_resample_dopp per tile: block prefix of gfx -> GS_j of every member -> Q_j, Q_{j+1} -> F(.) ->
+//                  copies; weighted velocity sums per run for the moments
+//   k_moments<true>, k_births<true>.
+// Every floating-point step uses explicit round-to-nearest intrinsics in the oracle's operation order,
+// so the next state is bit-identical to orc_step_doppler.
+#pragma once
+#include <cstdint>
+#include "dog_cells.cuh"
+#include "dog_common.cuh"
+#include "dog_fcount.cuh"
+#include "dog_resample.cuh"
+#include "dog_sort.cuh"
+
+namespace dog {
+
+struct DopIn {
+    const float4* dop;    // [C] (u_x, u_y, v_r, sd)
+    const float* pA;      // [C] association probability (0: no Doppler in the cell)
+};
+
+// e^q for q <= 0 (A-34 "exp spec")
+__device__ __forceinline__ float exp_spec(float q)
+{
+    if (!(q >= -87.0f)) return 0.0f;
+    if (q > 0.0f) q = 0.0f;
+    const float kf = rintf(__fmul_rn(q, 1.44269504088896341f));
+    float r = __fmaf_rn(-kf, 0.693359375f, q);
+    r = __fmaf_rn(-kf, -2.12194440e-4f, r);
+    const float z = __fmul_rn(r, r);
+    float y = 1.9875691500e-4f;
+    y = __fmaf_rn(y, r, 1.3981999507e-3f);
+    y = __fmaf_rn(y, r, 8.3334519073e-3f);
+    y = __fmaf_rn(y, r, 4.1665795894e-2f);
+    y = __fmaf_rn(y, r, 1.6666665459e-1f);
+    y = __fmaf_rn(y, r, 5.0000001201e-1f);
+    y = __fmaf_rn(y, z, r);
+    y = __fadd_rn(y, 1.0f);
+    const int k = (int)kf;                                   // -126 <= k <= 0
+    return __fmul_rn(y, __int_as_float((127 + k) << 23));
+}
+
+// Doppler likelihood g(z | x) of a predicted velocity (Eq. 69; A-34), fixed point
+__device__ __forceinline__ uint32_t doppler_gfx(float vx, float vy, float4 d)
+{
+    const float e = __fsub_rn(__fmaf_rn(vx, d.x, __fmul_rn(vy, d.y)), d.z);
+    const float t = __fdiv_rn(e, d.w);
+    const float q = __fmul_rn(__fmul_rn(t, t), -0.5f);
+    const float g = __fdiv_rn(exp_spec(q), __fmul_rn(d.w, 2.50662827463100050f));
+    const float gc = g < 0x1.fffffep+7f ? g : 0x1.fffffep+7f;
+    if (!(gc > 0.0f)) return 0u;
+    return __float2uint_rz(__fmul_rn(gc, 16777216.0f));
+}
+
+// Q_j = floor(R_p G_j) (A-35)
+__device__ __forceinline__ uint64_t doppler_Q(uint64_t Rp, float pA, uint64_t GSj, uint64_t GS, uint32_t j, uint32_t n)
+{
+    const double pa = (double)pA;
+    const double a = __ddiv_rn(__ull2double_rn(GSj), __ull2double_rn(GS));
+    const double b = __dmul_rn(__dsub_rn(1.0, pa), __ddiv_rn((double)j, (double)n));
+    const double G = __fma_rn(pa, a, b);
+    return __double2ull_rz(__dmul_rn(__ull2double_rn(Rp), G));
+}
+
+// particles of tile t (input order) and its slot base in the local array, as in k_resample_tiles
+__device__ __forceinline__ uint32_t tile_count(const DevScalars* sc, int par, uint32_t base)
+{
+    const uint32_t n_loc = sc->n_lo + sc->n_own[par] + sc->n_hi;
+    return n_loc > base ? min((uint32_t)kSortTile, n_loc - base) : 0u;
+}
+
+// run of sorted position p among first[0..nd) (first[0] = 0)
+__device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, uint32_t p)
+{
+    uint32_t lo = 0, hi = nd;
+    while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (first[m] <= p) lo = m; else hi = m; }
+    return lo;
+}
+
+// ---- k_dopp_runs: gfx of every member of a Doppler cell, summed per run (rg[run slot]) ----------------
+__global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ lperm, TilePairs tp,
+                                                   const float4* __restrict__ pred, DopIn din,
+                                                   uint64_t* __restrict__ rg, const DevScalars* __restrict__ sc,
+                                                   FilterConst fc, int par)
+{
+    PDL_ENTER();
+    __shared__ uint16_t s_first[kSortTile + 1];
+    const uint32_t t = blockIdx.x, base = t * kSortTile;
+    const uint32_t n = tile_count(sc, par, base);
+    if (n == 0) return;
+    const uint32_t nd = tp.nd[t];
+    const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) { s_first[r] = tp.first[base + r]; rg[base + r] = 0ull; }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
+        const uint32_t j = run_of(s_first, nd, p);
+        const uint32_t key = tp.key[base + j];
+        if (key >= fc.C) continue;
+        const float pa = din.pA[key];
+        if (!(pa > 0.0f)) continue;
+        const float4 X = pred[pbase + lperm[base + p]];
+        const uint32_t gf = doppler_gfx(X.z, X.w, din.dop[key]);
+        if (gf) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)gf);
+    }
+}
+
+// ---- k_dopp_cells: per active Doppler cell, its runs in tile order -> exclusive gfx prefix per run,
+//      cell total GS[li] (0: not a Doppler cell, or no member compatible: even split, A-35) ---------------
+__global__ __launch_bounds__(256) void k_dopp_cells(CellList L, const uint32_t* __restrict__ plist, DopIn din,
+                                                    uint64_t* __restrict__ rg, uint64_t* __restrict__ GS,
+                                                    const DevScalars* __restrict__ sc)
+{
+    PDL_ENTER();
+    const uint32_t Lc = sc->Lc;
+    for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < Lc; li += gridDim.x * blockDim.x) {
+        const uint32_t m = L.np[li];
+        uint64_t acc = 0;
+        if (m > 0 && din.pA[L.c[li]] > 0.0f) {
+            const uint32_t* pl = plist + L.ps[li];
+            for (uint32_t a = 0; a < m; ++a) {
+                const uint32_t v = pl[a];
+                const uint64_t s = rg[v];
+                rg[v] = acc;
+                acc += s;
+            }
+        }
+        GS[li] = acc;
+    }
+}
+
+// ---- k_resample_dopp: persistent members with per-member weights ---------------------------------------
+constexpr int kRdItems = kSortTile / 256;   // 16 sorted positions per thread
+
+struct RdSmem {
+    uint16_t first[kSortTile + 1];
+    uint16_t lp[kSortTile];
+    MomPartial pa[256], pb[256];   // first / last run segment of each thread (spanning runs)
+    uint64_t scan[9];
+};
+
+__global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restrict__ lperm, TilePairs tp,
+                                                       const float4* __restrict__ pred, CellList L, NextState out,
+                                                       MomPartial* __restrict__ ppart, DopIn din,
+                                                       const uint64_t* __restrict__ rg, uint64_t* __restrict__ rs,
+                                                       const uint64_t* __restrict__ GS,
+                                                       const DevScalars* __restrict__ sc, FilterConst fc, int par)
+{
+    PDL_ENTER();
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    RdSmem& S = *reinterpret_cast<RdSmem*>(smem_raw);
+    const int tid = threadIdx.x;
+    const uint32_t t = blockIdx.x, base = t * kSortTile;
+    const RsConst rc = make_rsconst(sc, fc.nu);
+    out.s += fc.lo_cap - sc->o_base[par ^ 1];
+    if (rc.W == 0 && fc.world == 1) {   // empty world (A-26)
+        for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x)
+            out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
+    }
+    const uint32_t n = tile_count(sc, par, base);
+    if (n == 0) return;
+    const uint32_t nd = tp.nd[t];
+    const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
+    const RunInfo* __restrict__ runs = tp.run + base;
+    for (uint32_t p = tid; p < n; p += 256) S.lp[p] = lperm[base + p];
+    for (uint32_t r = tid; r < nd; r += 256) S.first[r] = tp.first[base + r];
+    if (tid == 0) S.first[nd] = (uint16_t)n;
+    __syncthreads();
+    const uint32_t p0 = tid * kRdItems;
+    const uint32_t p1 = min(p0 + kRdItems, n);
+
+    // pass 1: gfx of the owned positions, thread total, block prefix; run starts -> rs[run]
+    uint32_t gf[kRdItems];
+    uint64_t tsum = 0;
+    {
+        uint32_t j = p0 < n ? run_of(S.first, nd, p0) : 0u;
+        uint32_t key = 0, end = 0;
+        float pa = 0.0f;
+        float4 d = make_float4(0.f, 0.f, 0.f, 1.f);
+        bool first_run = true;
+#pragma unroll
+        for (int u = 0; u < kRdItems; ++u) {
+            const uint32_t p = p0 + u;
+            gf[u] = 0u;
+            if (p >= p1) continue;
+            if (first_run || p >= end) {
+                if (!first_run) ++j;
+                first_run = false;
+                end = S.first[j + 1];
+                key = tp.key[base + j];
+                pa = key < fc.C ? din.pA[key] : 0.0f;
+                if (pa > 0.0f) d = din.dop[key];
+            }
+            if (pa > 0.0f) {
+                const float4 X = pred[pbase + S.lp[p]];
+                gf[u] = doppler_gfx(X.z, X.w, d);
+            }
+            tsum += gf[u];
+        }
+    }
+    uint64_t tot;
+    const uint64_t tb = block_excl_scan<uint64_t, 8>(tsum, S.scan, tot);
+    {
+        uint64_t x = tb;
+        uint32_t j = p0 < n ? run_of(S.first, nd, p0) : 0u;
+        for (int u = 0; u < kRdItems; ++u) {
+            const uint32_t p = p0 + u;
+            if (p >= p1) break;
+            while (S.first[j + 1] <= p) ++j;
+            if (S.first[j] == p) rs[base + j] = x;            // block prefix at the run's first member
+            x += gf[u];
+        }
+    }
+    __syncthreads();                                          // rs[] visible to the block
+
+    // pass 2: Q_j, Q_{j+1} -> outputs [F(P + Q_j), F(P + Q_{j+1})); velocity sums per run segment
+    if (p0 < n) {
+        uint32_t j = run_of(S.first, nd, p0);
+        uint32_t first = S.first[j], end = S.first[j + 1];
+        double acc[5] = {0, 0, 0, 0, 0};
+        bool first_seg = true;
+        uint64_t x = tb;
+        auto load_run = [&](RunInfo& q, uint32_t& key, uint64_t& Rp, uint32_t& nm, uint64_t& gsc, float& pa) {
+            key = tp.key[base + j];
+            if (key < fc.C) {
+                q = runs[j];
+                Rp = L.Rp[q.li]; nm = L.n[q.li]; gsc = GS[q.li];
+                pa = din.pA[key];
+            }
+        };
+        RunInfo q{};
+        uint32_t key = 0, nm = 0;
+        uint64_t Rp = 0, gsc = 0;
+        float pa = 0.0f;
+        load_run(q, key, Rp, nm, gsc, pa);
+        auto flush = [&]() {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
+            if (key < fc.C) {
+                if (first >= p0 && end <= p0 + kRdItems) ppart[base + j] = mp;   // run inside this thread
+                else if (first_seg) S.pa[tid] = mp;
+                else S.pb[tid] = mp;
+            }
+            first_seg = false;
+        };
+        for (int u = 0; u < kRdItems; ++u) {
+            const uint32_t p = p0 + u;
+            if (p >= p1) break;
+            if (p >= end) {
+                flush();
+                ++j; first = end; end = S.first[j + 1];
+                load_run(q, key, Rp, nm, gsc, pa);
+            }
+            const uint64_t xp = x;
+            x += gf[u];
+            if (key >= fc.C) continue;                        // outside the grid: no weight
+            const uint32_t mr = q.pre + (p - first);
+            uint64_t Q0, Q1;
+            if (gsc > 0) {
+                const uint64_t g0 = rg[base + j] + (xp - rs[base + j]);
+                Q0 = doppler_Q(Rp, pa, g0, gsc, mr, nm);
+                Q1 = doppler_Q(Rp, pa, g0 + gf[u], gsc, mr + 1, nm);
+            } else {
+                Q0 = (uint64_t)mr * q.bp + min(mr, q.rpm);
+                Q1 = (uint64_t)(mr + 1) * q.bp + min(mr + 1, q.rpm);
+            }
+            const float4 X = pred[pbase + S.lp[p]];
+            if (rc.W) {
+                const uint32_t F0 = fcount(q.P + Q0, rc), F1 = fcount(q.P + Q1, rc);
+                for (uint32_t o = F0; o < F1; ++o) out.s[o] = X;
+            }
+            const double w = gsc > 0 ? (double)(Q1 - Q0) : 1.0;
+            const double a = (double)X.z, b = (double)X.w;
+            acc[0] += w * a; acc[1] += w * b; acc[2] += w * a * a; acc[3] += w * b * b; acc[4] += w * a * b;
+        }
+        flush();
+    }
+    __syncthreads();
+    // spanning runs: segments over threads tf..tl combined in thread order -> ppart
+    for (uint32_t r = tid; r < nd; r += 256) {
+        const uint32_t f = S.first[r], e = S.first[r + 1];
+        if (tp.key[base + r] >= fc.C) continue;
+        const uint32_t tf = f / kRdItems, tl = (e - 1) / kRdItems;
+        if (tf == tl) continue;
+        const MomPartial& m0 = (f > tf * kRdItems) ? S.pb[tf] : S.pa[tf];
+        double s5[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) s5[i] = m0.s[i];
+        for (uint32_t u = tf + 1; u <= tl; ++u)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += S.pa[u].s[i];
+        MomPartial mp;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+        ppart[base + r] = mp;
+    }
+}
+
+}  // namespace dog

@@ -39,6 +39,24 @@ __device__ __forceinline__ void finalize_cell(uint32_t c, double s0, double s1, 
     cov[3 * (size_t)c + 2] = (float)(wd * s4 / rd - mx * my);
 }
 
+// Moments of a Doppler cell (NEXT-1, A-35): sums weighted by the members' fixed-point weights q_j,
+// normalised by their total R_p.
+__device__ __forceinline__ void finalize_cell_dop(uint32_t c, double s0, double s1, double s2, double s3, double s4,
+                                                  uint64_t Rp, float2* __restrict__ mean, float* __restrict__ cov)
+{
+    if (Rp == 0) {
+        mean[c] = make_float2(0.0f, 0.0f);
+        cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
+        return;
+    }
+    const double rd = (double)Rp;
+    const double mx = s0 / rd, my = s1 / rd;
+    mean[c] = make_float2((float)mx, (float)my);
+    cov[3 * (size_t)c] = (float)(s2 / rd - mx * mx);
+    cov[3 * (size_t)c + 1] = (float)(s3 / rd - my * my);
+    cov[3 * (size_t)c + 2] = (float)(s4 / rd - mx * my);
+}
+
 struct NextState { float4* s; uint32_t* jidx; };   // (x, y, vx, vy) per particle; joint index (debug)
 struct BirthDebug { float *x, *y, *vx, *vy; };
 
@@ -443,7 +461,8 @@ constexpr int kMoGroup = 8;
 
 __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
                                                  const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
-                                                 float* __restrict__ cov, const DevScalars* __restrict__ sc)
+                                                 float* __restrict__ cov, const DevScalars* __restrict__ sc,
+                                                 const uint64_t* __restrict__ GSd)
 {
     PDL_ENTER();
     const int lane = threadIdx.x & 31, gl = lane & (kMoGroup - 1);
@@ -467,14 +486,35 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
 #pragma unroll
                 for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(gmask, s5[i], d, kMoGroup);
         }
-        if (gl == 0) finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
+        if (gl == 0) {
+            if (GSd && GSd[li] > 0)    // Doppler cell (NEXT-1): weighted sums
+                finalize_cell_dop(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.Rp[li], mean, cov);
+            else
+                finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
+        }
     }
+}
+
+// Split of a cell's birth slots / born mass into the associated and unassociated sets (NEXT-1, A-36):
+// nu_A = floor(p_A nb + 1/2), R_bA = floor(R_b p_A) (fp64), 0 if nu_A = 0, R_b if nu_A = nb.
+__device__ __forceinline__ void birth_assoc_split(uint64_t Rb, uint32_t nb, float pA, uint32_t& nA, uint64_t& RbA)
+{
+    uint32_t na = (uint32_t)floor(__dadd_rn(__dmul_rn((double)pA, (double)nb), 0.5));
+    if (na > nb) na = nb;
+    uint64_t ra = __double2ull_rz(__dmul_rn(__ull2double_rn(Rb), (double)pA));
+    if (na == 0) ra = 0;
+    else if (na == nb) ra = Rb;
+    nA = na;
+    RbA = ra;
 }
 
 // New-born particles (Alg. 5): work items of <= 256 birth slots of one cell; each warp takes a
 // contiguous range of items.  State from the slot's Philox draw; copies as for persistent members.
+// dpA / ddop: the Doppler grid of the cycle (NEXT-1) or nullptr: slots r < nu_A of a cell with p_A > 0
+// form the associated set (velocity from p(x | z)), sharing R_bA; the rest share R_b - R_bA (A-36).
 __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, BirthDebug bdbg,
-                                                const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+                                                const DevScalars* __restrict__ sc, FilterConst fc, int64_t k,
+                                                const float* __restrict__ dpA, const float4* __restrict__ ddop)
 {
     PDL_ENTER();
     const int tid = threadIdx.x, lane = tid & 31;
@@ -499,6 +539,26 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
         const uint32_t rbm = L.rb[li], sb = L.sb[li];
         const uint64_t PB = P + L.Rp[li];
         const uint32_t jbase = start + sb + n;
+        uint32_t nA = 0;                                              // associated slots (NEXT-1)
+        uint64_t RbA = 0, bbA = 0, bbB = bb;
+        uint32_t rbA = 0, rbB = rbm;
+        float4 dz = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (dpA) {
+            const float pa = dpA[c];
+            if (pa > 0.0f) {
+                birth_assoc_split((uint64_t)nb * bb + rbm, nb, pa, nA, RbA);
+                if (nA) { bbA = RbA / nA; rbA = (uint32_t)(RbA % nA); dz = ddop[c]; }
+                const uint32_t nB = nb - nA;
+                const uint64_t RbB = (uint64_t)nb * bb + rbm - RbA;
+                if (nB) { bbB = RbB / nB; rbB = (uint32_t)(RbB % nB); }
+            }
+        }
+        // fixed-point joint CDF of slot r within the cell's births
+        auto slotQ = [&](uint32_t r) -> uint64_t {
+            if (r < nA) return (uint64_t)r * bbA + min(r, rbA);
+            const uint32_t rr = r - nA;
+            return RbA + (uint64_t)rr * bbB + min(rr, rbB);
+        };
         const uint32_t cg = c + fc.c_off;                             // global cell
         const uint32_t col = cg % (uint32_t)fc.W, row = cg / (uint32_t)fc.W;
         const float colf = (float)col, rowf = (float)row;
@@ -514,17 +574,25 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
             if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
             float n0, n1;
             box_muller(d.r2, d.r3, n0, n1);
-            float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
+            float bvx, bvy;
+            if (r < nA) {                                             // associated: p(x | z), Eq. 74 (A-36)
+                const float sr = __fmaf_rn(dz.w, n0, dz.z);
+                const float st = __fmul_rn(fc.sigma_b, n1);
+                bvx = __fmaf_rn(sr, dz.x, -__fmul_rn(st, dz.y));
+                bvy = __fmaf_rn(sr, dz.y, __fmul_rn(st, dz.x));
+            } else {
+                bvx = __fmul_rn(fc.sigma_b, n0); bvy = __fmul_rn(fc.sigma_b, n1);
+            }
             if (fc.v_max > 0.0f) {
                 bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
                 bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
             }
             if (valid && bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
             if (rc.W) {
-                const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
+                const uint64_t Q0 = PB + slotQ(r);
                 const uint32_t F0 = valid ? fcount(Q0, rc) : 0u;
                 uint32_t F1 = __shfl_down_sync(0xffffffffu, F0, 1);
-                if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(Q0 + bb + (r < rbm ? 1u : 0u), rc);
+                if (valid && (lane == 31 || t + lane + 1 == m)) F1 = fcount(PB + slotQ(r + 1), rc);
                 write_copies(valid, F0, F1, bx, by, bvx, bvy, jbase + r, out);
             }
         }

@@ -56,6 +56,7 @@ _SIGS = {
     "dog_create": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
                     C.POINTER(_vp)], C.c_int),
     "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
+    "dog_step_doppler": ([_vp, _vp, _vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_step_host_async": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_read_cells": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -173,6 +174,13 @@ class Filter:
         assert meas.is_cuda and meas.dtype == torch.float32 and meas.is_contiguous()
         assert meas.numel() == 2 * self.C
         _check(dog_step(self._h, meas.data_ptr(), dt, _stream_ptr(stream)), "dog_step")
+
+    def step_doppler(self, meas: torch.Tensor, doppler: torch.Tensor, p_assoc: torch.Tensor, dt: float, stream=None):
+        """include/dog.h dog_step_doppler (NEXT-1): doppler [C, 4] = (u_x, u_y, v_r, sd), p_assoc [C]."""
+        for t, n in ((meas, 2), (doppler, 4), (p_assoc, 1)):
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == n * self.C
+        _check(dog_step_doppler(self._h, meas.data_ptr(), doppler.data_ptr(), p_assoc.data_ptr(), dt,
+                                _stream_ptr(stream)), "dog_step_doppler")
 
     def step_host(self, meas_host: torch.Tensor, dt: float, occ_host: torch.Tensor | None = None, stream=None):
         assert not meas_host.is_cuda and meas_host.dtype == torch.float32 and meas_host.is_contiguous()

@@ -247,6 +247,37 @@ class Scene:
             out[unobs] = torch.tensor([0.6, 0.0], device=dev)
         return out
 
+    def doppler(self, k: int, meas: torch.Tensor, frac: float = 0.5, p_assoc: float = 0.8, sd: float = 0.25,
+                device="cpu"):
+        """Radar Doppler overlay of frame k (NEXT-1 input; SPEC S:151-159 radar_overlay, S:440 defaults):
+        a seeded fraction `frac` of the cells with m_zO > 0 carry a radial-velocity measurement --
+        unit direction from the sensor to the cell centre, radial speed = the true object velocity (a
+        mover covering the cell, else 0) projected on it plus N(0, sd^2) noise, SD sd -- and association
+        probability p_assoc.  Returns (doppler [H, W, 4] f32 = (u_x, u_y, v_r, sd), p_A [H, W] f32)."""
+        cfg = self.cfg
+        W, H, cs, dt = cfg.width, cfg.height, cfg.cell_size, cfg.dt
+        rng = np.random.default_rng((cfg.scene_seed * 1_000_003 + k) & 0xFFFFFFFF)
+        vel = np.zeros((H, W, 2), np.float64)
+        for b in self.boxes:
+            if not b.mover:
+                continue
+            x, y = self._pos(b, k)
+            c0, c1 = max(int(math.floor(x)), 0), min(int(math.ceil(x + b.w)), W)
+            r0, r1 = max(int(math.floor(y)), 0), min(int(math.ceil(y + b.h)), H)
+            if c1 > c0 and r1 > r0:
+                vel[r0:r1, c0:c1] = (b.vx * cs / dt, b.vy * cs / dt)
+        yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+        dx = xx + 0.5 - self.sensor[0]; dy = yy + 0.5 - self.sensor[1]
+        d = np.sqrt(dx * dx + dy * dy)
+        d[d == 0] = 1.0
+        ux, uy = dx / d, dy / d
+        vr = vel[..., 0] * ux + vel[..., 1] * uy + rng.normal(0.0, sd, (H, W))
+        occ = meas.detach().cpu().numpy().reshape(H, W, 2)[..., 0] > 0
+        has = occ & (rng.random((H, W)) < frac)
+        dop = np.stack([ux, uy, vr, np.full((H, W), sd)], -1).astype(np.float32)
+        pA = np.where(has, np.float32(p_assoc), np.float32(0.0)).astype(np.float32)
+        return torch.from_numpy(dop).to(device), torch.from_numpy(pA).to(device)
+
     def frames(self, k0: int, n: int, device="cpu") -> torch.Tensor:
         return torch.stack([self.frame(k0 + i, device) for i in range(n)])
 
