@@ -98,6 +98,7 @@ struct dog_ctx {
     uint64_t* d_rg = nullptr;                     // per run slot: gfx sum, then exclusive cell prefix
     uint64_t* d_rs = nullptr;                     // per run slot: block prefix at the run's first member
     uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
+    uint8_t* d_tflag = nullptr;                   // per sort tile: holds members of a Doppler cell
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
@@ -318,6 +319,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRtSmemBytes);
     cudaFuncSetAttribute(k_eval_cells_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEvSmem);
+    cudaFuncSetAttribute(k_resample_dopp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRdSmemBytes);
     if (const char* cv = getenv("DOG_RS_CARVEOUT")) {   // experiments: shared-memory share of the L1/smem array
         cudaFuncSetAttribute(k_resample_tiles<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
         cudaFuncSetAttribute(k_resample_tiles<true>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
@@ -459,6 +461,7 @@ int dog_destroy(dog_ctx* ctx)
     if (ctx->d_rg) cudaFree(ctx->d_rg);
     if (ctx->d_rs) cudaFree(ctx->d_rs);
     if (ctx->d_GS) cudaFree(ctx->d_GS);
+    if (ctx->d_tflag) cudaFree(ctx->d_tflag);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     free_all(ctx);
@@ -512,7 +515,8 @@ static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const
     return DOG_OK;
 }
 
-static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
+                      const uint8_t* tskip = nullptr)
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
@@ -520,11 +524,11 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     if (dbg)
         CK(launch_ex(false, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
                   ctx->tp, (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
-                  (const DevScalars*)ctx->sc, fc, par));
+                  (const DevScalars*)ctx->sc, fc, par, tskip));
     else
         CK(launch_ex(false, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
                   ctx->tp, (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
-                  (const DevScalars*)ctx->sc, fc, par));
+                  (const DevScalars*)ctx->sc, fc, par, tskip));
     return DOG_OK;
 }
 
@@ -619,7 +623,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     cudaStream_t st = (cudaStream_t)stream;
     if (!ctx->d_rg) {
         if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
-            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess)
+            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess)
             return DOG_E_NOMEM;
     }
     const StepArgs a = step_args(ctx, dt);
@@ -631,13 +635,15 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
     if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
     CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
-              din, ctx->d_rg, (const DevScalars*)ctx->sc, fc, par));
+              din, ctx->d_rg, ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
     CK(launch(k_dopp_cells, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist, din, ctx->d_rg,
-              ctx->d_GS, (const DevScalars*)ctx->sc));
+              ctx->d_GS, ctx->d_tflag, (const DevScalars*)ctx->sc));
+    // tiles without a Doppler cell's members: the closed-form kernel; the others: per-member weights
+    if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
     NextState ns{ctx->st, nullptr};
-    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, sizeof(RdSmem), st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
                  (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
-                 (const uint64_t*)ctx->d_GS, (const DevScalars*)ctx->sc, fc, par));
+                 (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
     if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
     if (int r = L_births(ctx, a, fc, st, &din)) return r;
     ctx->k += 1;

@@ -11,8 +11,9 @@
 // k_resample_tiles does not apply; this path uses
 //   k_dopp_runs    per tile: gfx of every member, summed per run (integer atomics: order-free)
 //   k_dopp_cells   per active cell: the runs' gfx sums in tile order -> exclusive prefixes, cell total GS
-//   k_resample_dopp per tile: block prefix of gfx -> GS_j of every member -> Q_j, Q_{j+1} -> F(.) ->
-//                  copies; weighted velocity sums per run for the moments
+//   k_resample_dopp per tile holding a Doppler cell's members: block prefix of gfx -> GS_j of every
+//                  member -> Q_j, Q_{j+1} -> F(.) -> copies; weighted velocity sums per run for the
+//                  moments.  Every other tile goes through k_resample_tiles (closed form, even split).
 //   k_moments<true>, k_births<true>.
 // Every floating-point step uses explicit round-to-nearest intrinsics in the oracle's operation order,
 // so the next state is bit-identical to orc_step_doppler.
@@ -92,12 +93,13 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
 // ---- k_dopp_runs: gfx of every member of a Doppler cell, summed per run (rg[run slot]) ----------------
 __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ lperm, TilePairs tp,
                                                    const float4* __restrict__ pred, DopIn din,
-                                                   uint64_t* __restrict__ rg, const DevScalars* __restrict__ sc,
-                                                   FilterConst fc, int par)
+                                                   uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
+                                                   const DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
     const uint32_t t = blockIdx.x, base = t * kSortTile;
+    if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_dopp_cells for Doppler tiles
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
@@ -120,7 +122,7 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
 //      cell total GS[li] (0: not a Doppler cell, or no member compatible: even split, A-35) ---------------
 __global__ __launch_bounds__(256) void k_dopp_cells(CellList L, const uint32_t* __restrict__ plist, DopIn din,
                                                     uint64_t* __restrict__ rg, uint64_t* __restrict__ GS,
-                                                    const DevScalars* __restrict__ sc)
+                                                    uint8_t* __restrict__ tflag, const DevScalars* __restrict__ sc)
 {
     PDL_ENTER();
     const uint32_t Lc = sc->Lc;
@@ -137,6 +139,10 @@ __global__ __launch_bounds__(256) void k_dopp_cells(CellList L, const uint32_t* 
             }
         }
         GS[li] = acc;
+        if (acc > 0) {                                       // the tiles holding this cell's members
+            const uint32_t* pl = plist + L.ps[li];
+            for (uint32_t a = 0; a < m; ++a) tflag[pl[a] >> 12] = 1;
+        }
     }
 }
 
@@ -144,17 +150,18 @@ __global__ __launch_bounds__(256) void k_dopp_cells(CellList L, const uint32_t* 
 constexpr int kRdItems = kSortTile / 256;   // 16 sorted positions per thread
 
 struct RdSmem {
-    uint16_t first[kSortTile + 1];
-    uint16_t lp[kSortTile];
     MomPartial pa[256], pb[256];   // first / last run segment of each thread (spanning runs)
     uint64_t scan[9];
+    uint16_t first[kSortTile + 1];
+    uint16_t lp[kSortTile];
 };
+constexpr size_t kRdSmemBytes = sizeof(RdSmem);
 
-__global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restrict__ lperm, TilePairs tp,
+__global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __restrict__ lperm, TilePairs tp,
                                                        const float4* __restrict__ pred, CellList L, NextState out,
                                                        MomPartial* __restrict__ ppart, DopIn din,
                                                        const uint64_t* __restrict__ rg, uint64_t* __restrict__ rs,
-                                                       const uint64_t* __restrict__ GS,
+                                                       const uint64_t* __restrict__ GS, const uint8_t* __restrict__ tflag,
                                                        const DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
@@ -169,7 +176,7 @@ __global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restric
             out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
     }
     const uint32_t n = tile_count(sc, par, base);
-    if (n == 0) return;
+    if (n == 0 || !tflag[t]) return;                          // tiles without Doppler runs: k_resample_tiles
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
     const RunInfo* __restrict__ runs = tp.run + base;
@@ -255,6 +262,9 @@ __global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restric
             }
             first_seg = false;
         };
+        uint64_t Qc = 0;                                      // Q_{j+1} / F(P + Q_{j+1}) of the previous member
+        uint32_t Fc = 0;                                      // of the same run: the next member's Q_j / F
+        bool have = false;
         for (int u = 0; u < kRdItems; ++u) {
             const uint32_t p = p0 + u;
             if (p >= p1) break;
@@ -262,6 +272,7 @@ __global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restric
                 flush();
                 ++j; first = end; end = S.first[j + 1];
                 load_run(q, key, Rp, nm, gsc, pa);
+                have = false;
             }
             const uint64_t xp = x;
             x += gf[u];
@@ -270,7 +281,7 @@ __global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restric
             uint64_t Q0, Q1;
             if (gsc > 0) {
                 const uint64_t g0 = rg[base + j] + (xp - rs[base + j]);
-                Q0 = doppler_Q(Rp, pa, g0, gsc, mr, nm);
+                Q0 = have ? Qc : doppler_Q(Rp, pa, g0, gsc, mr, nm);
                 Q1 = doppler_Q(Rp, pa, g0 + gf[u], gsc, mr + 1, nm);
             } else {
                 Q0 = (uint64_t)mr * q.bp + min(mr, q.rpm);
@@ -278,9 +289,12 @@ __global__ __launch_bounds__(256) void k_resample_dopp(const uint16_t* __restric
             }
             const float4 X = pred[pbase + S.lp[p]];
             if (rc.W) {
-                const uint32_t F0 = fcount(q.P + Q0, rc), F1 = fcount(q.P + Q1, rc);
+                const uint32_t F0 = have ? Fc : fcount(q.P + Q0, rc), F1 = fcount(q.P + Q1, rc);
+                Fc = F1;
                 for (uint32_t o = F0; o < F1; ++o) out.s[o] = X;
             }
+            Qc = Q1;
+            have = true;
             const double w = gsc > 0 ? (double)(Q1 - Q0) : 1.0;
             const double a = (double)X.z, b = (double)X.w;
             acc[0] += w * a; acc[1] += w * b; acc[2] += w * a * a; acc[3] += w * b * b; acc[4] += w * a * b;
