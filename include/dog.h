@@ -144,6 +144,15 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
 /* synchronous: own particles of the current state (float4 records, host) and the global index of the
  * first one; xyvv_host may be NULL to query the count. */
 int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n_own, uint64_t* global_first);
+/* synchronous, between cycles (band rebalancing; resume): install a band's
+ * state -- its own particles (n_own float4 records (x, y, vx, vy) from host, in global index order,
+ * the first being global index global_first), m_free of its cells (host, C_band f32), the uniform
+ * weight w_bar and the cycle counter k.  The particles must lie in the band's rows (the union of the
+ * bands' states is the whole-grid state, cell-ordered).  DOG_E_INVAL for n_own beyond the band's
+ * particle capacity or invalid values, DOG_E_STATE mid-cycle or on a whole-grid context.  The
+ * readouts of the previous cycle are not moved (the next cycle rewrites them). */
+int dog_band_set_state(dog_ctx* ctx, const float* xyvv_host, uint32_t n_own, uint64_t global_first,
+                       const float* m_free_host, float w_bar, int64_t k);
 
 /* ---- ego-motion compensation (SPEC ego_scroll) ----
  * dog_ego_scroll -- between cycles, move the grid content and the particles by the whole-cell part of

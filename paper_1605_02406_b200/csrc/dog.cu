@@ -773,6 +773,32 @@ int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n
     return report_meas(ctx);
 }
 
+int dog_band_set_state(dog_ctx* ctx, const float* xyvv_host, uint32_t n_own, uint64_t global_first,
+                       const float* m_free_host, float w_bar, int64_t k)
+{
+    if (!ctx || (n_own && !xyvv_host) || !m_free_host || !(w_bar >= 0.0f) || !finite(w_bar) || k < 0)
+        return DOG_E_INVAL;
+    if (ctx->world < 2) return DOG_E_STATE;
+    if (ctx->phase != 0) return DOG_E_STATE;
+    if (n_own > ctx->own_cap) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (int r = set_device(ctx)) return r;
+    CK(cudaDeviceSynchronize());
+    const int par = (int)(k & 1);
+    if (n_own) CK(cudaMemcpy(ctx->st + ctx->lo_cap, xyvv_host, (size_t)n_own * 16, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->m_free, m_free_host, (size_t)ctx->C * 4, cudaMemcpyHostToDevice));
+    DevScalars s;
+    CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
+    s.w_bar = w_bar;
+    s.n_own[par] = n_own;
+    s.o_base[par] = global_first;
+    s.n_lo = 0; s.n_hi = 0;
+    CK(cudaMemcpy(ctx->sc, &s, sizeof(s), cudaMemcpyHostToDevice));
+    ctx->k = k;
+    ctx->n_own_host = n_own;
+    return DOG_OK;
+}
+
 int dog_profile_begin(dog_ctx* ctx, int max_steps)
 {
     if (!ctx || max_steps < 0) return DOG_E_INVAL;

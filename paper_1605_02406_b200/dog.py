@@ -82,6 +82,7 @@ _SIGS = {
     "dog_band_joint": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_resample": ([_vp, _vp, _vp], C.c_int),
     "dog_band_particles": ([_vp, _vp, C.c_uint64, _u32p, _u64p], C.c_int),
+    "dog_band_set_state": ([_vp, _vp, C.c_uint32, C.c_uint64, _vp, C.c_float, C.c_int64], C.c_int),
 }
 DOG_MAX_STAGES = 16
 for _name, (_args, _res) in _SIGS.items():
@@ -367,6 +368,22 @@ class BandFilter:
 
     def read_cells(self, stream=None, check: bool = True) -> dict:
         return Filter.read_cells(self, stream, check)
+
+    def set_state(self, xyvv: np.ndarray, global_first: int, m_free: np.ndarray, w_bar: float, k: int):
+        """include/dog.h dog_band_set_state: own particles (float32 [n, 4], global index order starting at
+        global_first), m_free of the band's cells, w_bar, k."""
+        a = np.ascontiguousarray(xyvv, np.float32).reshape(-1, 4)
+        mf = np.ascontiguousarray(m_free, np.float32).reshape(-1)
+        assert mf.size == self.C
+        _check(dog_band_set_state(self._h, _np_ptr(a) if a.shape[0] else None, a.shape[0], int(global_first),
+                                  _np_ptr(mf), float(w_bar), int(k)), "dog_band_set_state")
+
+    def w_bar_k(self) -> tuple[float, int]:
+        """The uniform weight of the current state and the cycle counter."""
+        wb = np.zeros(1, np.float32)
+        k = C.c_int64()
+        _check(dog_get_state(self._h, None, None, None, None, _np_ptr(wb), None, C.byref(k)), "dog_get_state")
+        return float(wb[0]), k.value
 
     def m_free(self) -> np.ndarray:
         mf = np.zeros(self.C, np.float32)

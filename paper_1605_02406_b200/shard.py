@@ -36,6 +36,32 @@ def band_rows(height: int, world: int) -> list[tuple[int, int]]:
     return rows
 
 
+def plan_bands(row_particles, width: int, world: int, min_rows: int = 8, particle_bytes: float = 64.0,
+               cell_bytes: float = 56.0) -> list[tuple[int, int]]:
+    """Band rebalancing: contiguous row bands of near-equal work, from the
+    particles per row.  A row costs particle_bytes per particle plus cell_bytes per cell (the
+    algorithmic bytes of one cycle: 64 per particle, 56 per cell).  Boundary b is the
+    first row whose cost prefix reaches b/world of the total, clamped so every band keeps at least
+    min_rows rows (one-hop migration needs bands at least as tall as a cycle's motion).  Deterministic:
+    every rank computes the same plan from the same counts."""
+    import numpy as np
+    cnt = np.asarray(row_particles, dtype=np.float64).reshape(-1)
+    H = cnt.size
+    if world < 1 or world * min_rows > H:
+        raise ValueError(f"cannot split {H} rows into {world} bands of >= {min_rows} rows")
+    cost = cnt * particle_bytes + cell_bytes * width
+    prefix = np.concatenate([[0.0], np.cumsum(cost)])          # prefix[r] = cost of rows < r
+    total = prefix[-1]
+    bounds = [0]
+    for b in range(1, world):
+        r = int(np.searchsorted(prefix, total * b / world, side="left"))
+        r = max(r, bounds[-1] + min_rows)
+        r = min(r, H - (world - b) * min_rows)
+        bounds.append(r)
+    bounds.append(H)
+    return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
 def neighbour_counts(counts: list[tuple[int, int]], rank: int) -> tuple[int, int]:
     """Given every band's (n_down, n_up) migrant counts, the records band `rank` receives from below
     (the lower band's n_up) and from above (the upper band's n_down)."""
@@ -77,26 +103,84 @@ class DistTransport:
     def allgather_u64(self, x: torch.Tensor, out: torch.Tensor):
         dist.all_gather(list(out.chunk(self.world)), x.reshape(1), group=self.group)
 
+    def allgather_var(self, x: torch.Tensor) -> list[torch.Tensor]:
+        """Every rank's tensor [n_r, ...] (n_r may differ; same trailing shape and dtype), in rank order."""
+        n = torch.tensor([x.shape[0]], dtype=torch.int64, device=self.device)
+        ns = torch.zeros(self.world, dtype=torch.int64, device=self.device)
+        dist.all_gather(list(ns.chunk(self.world)), n, group=self.group)
+        ns = [int(v) for v in ns.tolist()]
+        m = max(ns)
+        pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=self.device)
+        pad[:x.shape[0]] = x.to(self.device)
+        outs = [torch.zeros_like(pad) for _ in range(self.world)]
+        dist.all_gather(outs, pad, group=self.group)
+        return [o[:k] for o, k in zip(outs, ns)]
+
+    def allreduce_sum(self, x: torch.Tensor) -> torch.Tensor:
+        y = x.to(self.device).clone()
+        dist.all_reduce(y, group=self.group)
+        return y
+
 
 class ShardedFilter:
     """The filter of one rank: its band of the grid, exchanging with the neighbour ranks."""
 
     def __init__(self, width: int, height: int, nu: int, nu_b: int, rank: int, world: int,
                  transport: DistTransport, migrant_cap: int | None = None, **params):
-        rows = band_rows(height, world)
-        self.rows = rows
-        self.row0, self.row1 = rows[rank]
-        lo_row0 = rows[rank - 1][0] if rank > 0 else self.row0
-        hi_row1 = rows[rank + 1][1] if rank < world - 1 else self.row1
-        cap = migrant_cap or max(4096, nu // 8)
-        self.f = dog.BandFilter(width, height, nu, nu_b, self.row0, self.row1, rank, world, lo_row0, hi_row1, cap,
-                                **params)
+        self._args = (width, height, nu, nu_b, migrant_cap or max(4096, nu // 8), params)
+        self.rank = rank
+        self._make(band_rows(height, world), world)
         self.t = transport
         self.world, self.rank = world, rank
         dev = transport.device
         self.mass_all = torch.zeros(world, dtype=torch.int64, device=dev)
         self.weight_all = torch.zeros(world, dtype=torch.int64, device=dev)
         self.n_far = 0
+
+    def _make(self, rows, world):
+        width, height, nu, nu_b, cap, params = self._args
+        rank = self.rank
+        self.rows = rows
+        self.row0, self.row1 = rows[rank]
+        lo_row0 = rows[rank - 1][0] if rank > 0 else self.row0
+        hi_row1 = rows[rank + 1][1] if rank < world - 1 else self.row1
+        self.f = dog.BandFilter(width, height, nu, nu_b, self.row0, self.row1, rank, world, lo_row0, hi_row1, cap,
+                                **params)
+
+    def rebalance(self, min_rows: int = 8) -> bool:
+        """Move the band boundaries to equalise the per-band work (plan_bands over the all-reduced
+        particles per row), between cycles.  The bands' states are exchanged (all-gather of particles and
+        m_F rows) and each rank re-creates its band context with its new rows; the global particle order
+        is unchanged, so the filter continues bit-exactly.  Returns False (nothing moved) if the plan
+        keeps the current bands or the state holds particles outside the grid (an empty world)."""
+        import numpy as np
+        width, height = self._args[0], self._args[1]
+        parts, g0 = self.f.particles()
+        rows_of = np.floor(parts[:, 1]).astype(np.int64)
+        if parts.shape[0] and (rows_of.min() < self.row0 or rows_of.max() >= self.row1):
+            ok = 0
+        else:
+            ok = 1
+        local = np.bincount(rows_of - 0, minlength=height)[:height] if ok and parts.shape[0] else np.zeros(height, np.int64)
+        flags = self.t.allreduce_sum(torch.tensor([ok], dtype=torch.int64))
+        if int(flags.item()) != self.world:
+            return False
+        counts = self.t.allreduce_sum(torch.from_numpy(local.astype(np.int64))).cpu().numpy()
+        new_rows = plan_bands(counts, width, self.world, min_rows)
+        if new_rows == self.rows:
+            return False
+        wb, k = self.f.w_bar_k()
+        all_parts = [t.cpu().numpy() for t in self.t.allgather_var(torch.from_numpy(parts))]
+        all_mf = [t.cpu().numpy() for t in self.t.allgather_var(torch.from_numpy(self.f.m_free()))]
+        P = np.concatenate(all_parts, axis=0)
+        MF = np.concatenate(all_mf).reshape(height, width)
+        self.f.close()
+        self._make(new_rows, self.world)
+        r0, r1 = new_rows[self.rank]
+        first = int(counts[:r0].sum())
+        n = int(counts[r0:r1].sum())
+        self.f.set_state(P[first:first + n], first, MF[r0:r1], wb, k)
+        return True
 
     @classmethod
     def from_config(cls, cfg, rank: int, world: int, transport: DistTransport, **over) -> "ShardedFilter":
@@ -129,17 +213,47 @@ class LocalBands:
 
     def __init__(self, width: int, height: int, nu: int, nu_b: int, world: int, migrant_cap: int | None = None,
                  **params):
-        self.rows = band_rows(height, world)
-        cap = migrant_cap or max(4096, nu // 8)
-        self.bands = []
-        for b, (r0, r1) in enumerate(self.rows):
-            lo = self.rows[b - 1][0] if b > 0 else r0
-            hi = self.rows[b + 1][1] if b < world - 1 else r1
-            self.bands.append(dog.BandFilter(width, height, nu, nu_b, r0, r1, b, world, lo, hi, cap, **params))
+        self._args = (width, height, nu, nu_b, migrant_cap or max(4096, nu // 8), params)
         self.world = world
+        self._make(band_rows(height, world))
         self.mass_all = torch.zeros(world, dtype=torch.int64, device="cuda")
         self.weight_all = torch.zeros(world, dtype=torch.int64, device="cuda")
         self.n_far = 0
+
+    def _make(self, rows):
+        width, height, nu, nu_b, cap, params = self._args
+        world = self.world
+        self.rows = rows
+        self.bands = []
+        for b, (r0, r1) in enumerate(rows):
+            lo = rows[b - 1][0] if b > 0 else r0
+            hi = rows[b + 1][1] if b < world - 1 else r1
+            self.bands.append(dog.BandFilter(width, height, nu, nu_b, r0, r1, b, world, lo, hi, cap, **params))
+
+    def rebalance(self, min_rows: int = 8, rows=None) -> bool:
+        """Band rebalancing (see ShardedFilter.rebalance) for the bands of this process; `rows` forces a
+        given partition instead of plan_bands'."""
+        import numpy as np
+        width, height = self._args[0], self._args[1]
+        P, _ = self.particles()
+        rows_of = np.floor(P[:, 1]).astype(np.int64)
+        if P.shape[0] and (rows_of.min() < 0 or rows_of.max() >= height):
+            return False
+        counts = np.bincount(rows_of, minlength=height)[:height]
+        new_rows = rows if rows is not None else plan_bands(counts, width, self.world, min_rows)
+        if new_rows == self.rows:
+            return False
+        MF = np.concatenate([f.m_free() for f in self.bands]).reshape(height, width)
+        wb, k = self.bands[0].w_bar_k()
+        for f in self.bands:
+            f.close()
+        self._make(new_rows)
+        for b, f in enumerate(self.bands):
+            r0, r1 = new_rows[b]
+            first = int(counts[:r0].sum())
+            n = int(counts[r0:r1].sum())
+            f.set_state(P[first:first + n], first, MF[r0:r1], wb, k)
+        return True
 
     @classmethod
     def from_config(cls, cfg, world: int, **over) -> "LocalBands":

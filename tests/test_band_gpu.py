@@ -27,12 +27,17 @@ def _bits(a, b, what):
     assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[:5]}"
 
 
-def run_bands_vs_whole(cfg, world, cycles, frames=None, migrant_cap=None):
+def run_bands_vs_whole(cfg, world, cycles, frames=None, migrant_cap=None, rebalance=None):
+    """rebalance: {cycle: rows or None} -- after that cycle, move the band boundaries (None: plan_bands)."""
     from paper_1605_02406_b200 import dog, shard
     g = dog.Filter.from_config(cfg)
     lb = shard.LocalBands.from_config(cfg, world, migrant_cap=migrant_cap)
     sc = I.scene(cfg) if frames is None else None
     for k in range(cycles):
+        if rebalance and (k - 1) in rebalance:
+            before = list(lb.rows)
+            assert lb.rebalance(min_rows=8, rows=rebalance[k - 1]), (k, before)
+            assert lb.rows != before and lb.rows[0][0] == 0 and lb.rows[-1][1] == cfg.height
         meas = (sc.frame(k, device="cuda") if frames is None
                 else torch.as_tensor(frames[k]).reshape(cfg.height, cfg.width, 2).cuda())
         g.step(meas.contiguous(), cfg.dt)
@@ -80,3 +85,11 @@ def test_four_bands_fast_movers():
     """Large process noise (4x Table I, SURVEY cfg 5 settings) on a small grid: many migrants per cycle."""
     cfg = I.config("cfg1", width=64, height=64, nu=40_000, nu_b=4_000, sigma_pos=0.08, sigma_vel=3.2)
     run_bands_vs_whole(cfg, 4, 8)
+
+
+def test_rebalance_bands_bit_exact():
+    """NEXT-4 band rebalancing: boundaries moved between cycles -- by plan_bands from the particles per row,
+    then to a forced skewed partition -- and the bands keep reproducing the whole grid bit for bit."""
+    cfg = I.config("cfg2", width=256, height=256, nu=300_000, nu_b=30_000, beams=400, movers=6, peds=4,
+                   boxes=15)
+    run_bands_vs_whole(cfg, 3, 7, rebalance={2: None, 4: [(0, 40), (40, 200), (200, 256)]})

@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1605_02406_b200.shard import DistTransport, band_rows, neighbour_counts
+from paper_1605_02406_b200.shard import DistTransport, band_rows, neighbour_counts, plan_bands
 
 
 def test_band_rows_partition():
@@ -28,6 +28,32 @@ def test_neighbour_counts():
     assert neighbour_counts(counts, 0) == (0, 3)
     assert neighbour_counts(counts, 1) == (5, 2)
     assert neighbour_counts(counts, 2) == (7, 0)
+
+
+def test_plan_bands_balances_work():
+    import numpy as np
+    rng = np.random.default_rng(0)
+    W, H = 64, 256
+    for world in (1, 2, 3, 5, 8):
+        cnt = rng.integers(0, 5000, H) * (rng.random(H) < 0.3)
+        cnt[100:120] += 40000                       # a dense stripe
+        rows = plan_bands(cnt, W, world, min_rows=8)
+        assert len(rows) == world and rows[0][0] == 0 and rows[-1][1] == H
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        assert all(r1 - r0 >= 8 for r0, r1 in rows)
+        cost = cnt * 64.0 + 56.0 * W
+        per = [cost[r0:r1].sum() for r0, r1 in rows]
+        # each boundary is the first row reaching its share: no band exceeds its share by more than one row
+        # (unless the min_rows clamp applies)
+        assert max(per) <= cost.sum() / world + cost.max() + 8 * cost.max()
+    # uniform rows -> the even partition
+    assert plan_bands(np.full(256, 100), W, 4, 8) == [(0, 64), (64, 128), (128, 192), (192, 256)]
+    # everything in one row: the clamp keeps min_rows per band
+    one = np.zeros(64, np.int64); one[10] = 10 ** 6
+    rows = plan_bands(one, W, 4, 8)
+    assert all(r1 - r0 >= 8 for r0, r1 in rows) and rows[-1][1] == 64
+    with pytest.raises(ValueError):
+        plan_bands(np.zeros(20), W, 3, 8)
 
 
 def _free_port():
@@ -56,6 +82,14 @@ def _worker(rank, world, port):
         out = torch.zeros(world, dtype=torch.int64)
         t.allgather_u64(torch.tensor([10 ** 12 + rank], dtype=torch.int64), out)
         assert out.tolist() == [10 ** 12 + r for r in range(world)]
+        # rebalancing exchanges: variable-length all-gather and all-reduce (ShardedFilter.rebalance)
+        mine = torch.arange(4 * (rank + 1), dtype=torch.float32).view(rank + 1, 4) + 100 * rank
+        got = t.allgather_var(mine)
+        assert [g.shape[0] for g in got] == [r + 1 for r in range(world)]
+        for r, g in enumerate(got):
+            assert torch.equal(g, torch.arange(4 * (r + 1), dtype=torch.float32).view(r + 1, 4) + 100 * r)
+        s = t.allreduce_sum(torch.tensor([rank, 1], dtype=torch.int64))
+        assert s.tolist() == [world * (world - 1) // 2, world]
     finally:
         dist.destroy_process_group()
 
