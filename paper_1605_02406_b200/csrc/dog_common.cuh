@@ -32,7 +32,6 @@ struct DevScalars {
 
 constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
 constexpr float kMeasSumMax = 0x1.00001p+0f;    // 1 + 2^-20 (= 1.0f + 1e-6f rounded), A-27
-constexpr uint32_t kStAgg = 1u << 30, kStInc = 2u << 30, kStMask = (1u << 30) - 1u;
 
 // Per-step scalars computed on the host in fp64 and rounded once to f32.
 struct StepArgs {
@@ -56,40 +55,6 @@ struct FilterConst {
     float p_s, p_b, sigma_b, occ_max, v_max;
     uint64_t seed;
 };
-
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p)
-{
-    uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v)
-{
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p)
-{
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v)
-{
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed64(const uint64_t* p)
-{
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ ulonglong2 ld_relaxed128(const ulonglong2* p)
-{
-    ulonglong2 v;
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
-    return v;
-}
 
 // Diagnostics build only (DOG_NVCC_EXTRA=-DDOG_TIMING, tools/phase_timing.py): per-phase block time,
 // accumulated by thread 0 of every block into g_phase_ns[slot].
@@ -122,73 +87,6 @@ __device__ __forceinline__ T warp_sum(T v)
 #pragma unroll
     for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     return v;
-}
-
-// Decoupled look-back (Merrill & Garland), warp-parallel: the calling WARP inspects 32 predecessor
-// tiles per step.  Packed variant: a tile aggregate < 2^30 shares one u32 with a 2-bit status.
-// Returns the exclusive prefix of `tile`; publishes the tile's inclusive prefix.  Call with all 32
-// lanes of one warp; every lane gets the result.
-__device__ __forceinline__ uint32_t lookback_u30(uint32_t* status, uint32_t tile, uint32_t total)
-{
-    const int lane = threadIdx.x & 31;
-    if (tile == 0) {
-        if (lane == 0) st_relaxed(status, kStInc | total);
-        return 0;
-    }
-    if (lane == 0) st_relaxed(status + tile, kStAgg | total);
-    uint32_t excl = 0;
-    int j = (int)tile - 1;
-    while (true) {
-        const int p = j - lane;
-        const uint32_t s = p >= 0 ? ld_relaxed(status + p) : kStInc;
-        const uint32_t incm = __ballot_sync(0xffffffffu, (s & kStInc) != 0);
-        const int first = incm ? __ffs(incm) - 1 : 31;
-        const uint32_t zm = __ballot_sync(0xffffffffu, (s & ~kStMask) == 0);
-        if (zm & ((2u << first) - 1u)) continue;       // a needed predecessor has not published yet
-        excl += warp_sum(lane <= first ? (s & kStMask) : 0u);
-        if (incm) break;
-        j -= 32;
-    }
-    if (lane == 0) st_relaxed(status + tile, kStInc | (excl + total));
-    return excl;
-}
-
-// Pair-of-u64 variant: status flag + 16-byte value slots written before the flag with release
-// semantics.  Flags carry the cycle's epoch (flag = epoch << 2 | 1 aggregate / 2 inclusive), so they
-// never need resetting between cycles.
-struct LookbackPair {
-    uint32_t* flag;
-    ulonglong2* agg;
-    ulonglong2* inc;
-};
-
-__device__ __forceinline__ ulonglong2 lookback_pair(LookbackPair s, uint32_t tile, ulonglong2 total, uint32_t epoch)
-{
-    const int lane = threadIdx.x & 31;
-    const uint32_t fa = (epoch << 2) | 1u, fi = (epoch << 2) | 2u;
-    if (tile == 0) {
-        if (lane == 0) { s.inc[0] = total; st_release(s.flag, fi); }
-        return make_ulonglong2(0ull, 0ull);
-    }
-    if (lane == 0) { s.agg[tile] = total; st_release(s.flag + tile, fa); }
-    unsigned long long ex = 0, ey = 0;
-    int j = (int)tile - 1;
-    while (true) {
-        const int p = j - lane;
-        const uint32_t f = p >= 0 ? ld_acquire(s.flag + p) : fi;
-        const uint32_t incm = __ballot_sync(0xffffffffu, f == fi);
-        const int first = incm ? __ffs(incm) - 1 : 31;
-        const uint32_t zm = __ballot_sync(0xffffffffu, f != fi && f != fa);
-        if (zm & ((2u << first) - 1u)) continue;
-        ulonglong2 v = make_ulonglong2(0ull, 0ull);
-        if (lane <= first && p >= 0) v = ld_relaxed128(f == fi ? s.inc + p : s.agg + p);
-        ex += warp_sum(v.x);
-        ey += warp_sum(v.y);
-        if (incm) break;
-        j -= 32;
-    }
-    if (lane == 0) { s.inc[tile] = make_ulonglong2(ex + total.x, ey + total.y); st_release(s.flag + tile, fi); }
-    return make_ulonglong2(ex, ey);
 }
 
 // Warp inclusive scan (add) of T via shuffles.

@@ -112,57 +112,6 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
     }
 }
 
-// As write_copies, for lanes whose ranges may leave gaps between them (members of different cells
-// with the first cell's births in between): an output is written only if it lies inside its owner's
-// range [F0, F1).
-__device__ __forceinline__ void write_copies_gaps(bool valid, uint32_t F0, uint32_t F1, float4 X, NextState& out)
-{
-    const int lane = threadIdx.x & 31;
-    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-    if (!vm) return;
-    const int lastv = 31 - __clz(vm);
-    const uint32_t lo = __shfl_sync(0xffffffffu, F0, __ffs(vm) - 1);
-    const uint32_t hi = __shfl_sync(0xffffffffu, F1, lastv);
-    // invalid lanes are transparent: carry the last valid lane's F0 and index (inclusive max-scans)
-    uint32_t f0s = valid ? F0 : 0u;
-    int oid = valid ? lane : -1;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, f0s, d);
-        const int u = __shfl_up_sync(0xffffffffu, oid, d);
-        if (lane >= d) { f0s = max(f0s, t); oid = max(oid, u); }
-    }
-    uint32_t o0 = lo;
-    while (o0 < hi) {
-        const uint32_t o = o0 + lane;
-        int own = 0;
-#pragma unroll
-        for (int step = 16; step; step >>= 1) {
-            const int cand = own + step;
-            const uint32_t f = __shfl_sync(0xffffffffu, f0s, cand);
-            if (f <= o) own = cand;
-        }
-        int ow = __shfl_sync(0xffffffffu, oid, own);
-        const bool has = ow >= 0;
-        ow = has ? ow : 0;
-        const float x = __shfl_sync(0xffffffffu, X.x, ow), y = __shfl_sync(0xffffffffu, X.y, ow);
-        const float vx = __shfl_sync(0xffffffffu, X.z, ow), vy = __shfl_sync(0xffffffffu, X.w, ow);
-        const uint32_t b = __shfl_sync(0xffffffffu, F0, ow), e = __shfl_sync(0xffffffffu, F1, ow);
-        const bool in = has && o < hi && o >= b && o < e;
-        if (in) out.s[o] = make_float4(x, y, vx, vy);
-        // next chunk; if the chunk's last output falls in a gap (other cells' outputs), jump to the
-        // next member range starting after it
-        const bool last_in = __shfl_sync(0xffffffffu, in, 31);
-        o0 += 32;
-        if (!last_in && o0 < hi) {
-            uint32_t nx = (valid && F1 > o0) ? max(F0, o0) : hi;
-#pragma unroll
-            for (int d = 16; d; d >>= 1) nx = min(nx, __shfl_xor_sync(0xffffffffu, nx, d));
-            o0 = nx;
-        }
-    }
-}
-
 #ifndef RT_MINB
 #define RT_MINB 4
 #endif
