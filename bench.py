@@ -289,6 +289,33 @@ def bench_ours(args, cfg):
     except Exception as exc:   # noqa: BLE001
         doppler = {"error": str(exc)}
 
+    # NEXT-3 (exact PHD/MIB, uniform likelihood): cycles from observation grids of the same frames,
+    # device-timed like the main line; births go to every cell (r_b > 0 everywhere), so the active-cell
+    # list holds the whole grid
+    exact = None
+    try:
+        ne = min(K, 6)
+        obs = [I.Scene.exact_obs(frames[settle + W + i]) for i in range(ne)]
+        for i in range(2):
+            f.step_exact(obs[i], cfg.dt, stream)
+        torch.cuda.synchronize()
+        x0 = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
+        x1 = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
+        for i in range(ne):
+            flush.zero_()
+            x0[i].record(stream)
+            f.step_exact(obs[i], cfg.dt, stream)
+            x1[i].record(stream)
+        torch.cuda.synchronize()
+        xms = float(np.mean([x0[i].elapsed_time(x1[i]) for i in range(ne)]))
+        ex_bytes = a_alg(cfg) + 16.0 * cfg.C               # obs grid is 16 B per cell instead of 8
+        exact = {"ms_per_step": xms, "value": cfg.nu / (xms * 1e-3), "unit": UNIT,
+                 "algorithmic_bytes": ex_bytes, "achieved_GBps": ex_bytes / (xms * 1e-3) / 1e9,
+                 "frac": ex_bytes / (xms * 1e-3) / 1e9 / peaks()[0],
+                 "input": "inputs.Scene.exact_obs of the same frames (DESIGN.md A-37 recipe)"}
+    except Exception as exc:   # noqa: BLE001
+        exact = {"error": str(exc)}
+
     # NEXT-2 (ego-motion compensation): one scroll of grid and particles at this size, device-timed
     ego = None
     try:
@@ -380,7 +407,7 @@ def bench_ours(args, cfg):
         "continuous": {"ms_per_step": cont_ms, "value": cfg.nu / (cont_ms * 1e-3), "unit": UNIT,
                        "note": "K cycles back to back, no flush between them (working set > L2)"},
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
-        "next_rows": {"doppler": doppler, "ego_scroll": ego, "evaluate": evaluation},
+        "next_rows": {"doppler": doppler, "exact_phd_mib": exact, "ego_scroll": ego, "evaluate": evaluation},
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }

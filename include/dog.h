@@ -182,6 +182,16 @@ int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, co
                    const uint8_t* labels_dev, const uint8_t* mask_dev, const float* thr_host, int n_thr,
                    float* m_dev, uint64_t* counts_host, double* sums_host, void* stream);
 
+/* dog_step_exact -- one cycle of the EXACT PHD/MIB filter (section V)
+ * for a uniform single-object likelihood equal to the clutter density (the section IV-F setting,
+ * P:795-867), on the same particle pipeline: the cell update is the Bernoulli update of Eqs. 31-32,
+ * 38-42 instead of Dempster's rule (A-37), births are allocated wherever r_b > 0 (also in
+ * unobserved cells), and m_F is not used.  obs: DEVICE f32 [C][4], 16-byte aligned, per cell
+ * (occurred 0/1, p_TP, p_FP, unused) -- whether a measurement occurred in the cell and its true- /
+ * false-positive probabilities, caller-guaranteed in [0, 1].  Readouts: occ = posterior
+ * existence probability r (Eq. 42), free = 1 - r, moments as dog_step.  DOG_E_STATE for bands. */
+int dog_step_exact(dog_ctx* ctx, const float* obs, float dt, void* stream);
+
 /* dog_step_doppler -- one cycle with the Doppler / association branch (Eqs. 69-80,
  * P:1157-1232; A-34..A-36).  As dog_step, plus two DEVICE arrays:
  *   doppler[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) per cell -- unit radial direction, measured

@@ -90,6 +90,8 @@ def _declare(L):
     L.orc_step_doppler.argtypes = [C.c_void_p, f32p, C.c_void_p, C.c_void_p, C.c_float]
     L.orc_step_doppler.restype = C.c_int
     L.orc_exp_spec.argtypes = [C.c_float]; L.orc_exp_spec.restype = C.c_float
+    L.orc_step_exact.argtypes = [C.c_void_p, f32p, C.c_float]; L.orc_step_exact.restype = C.c_int
+    L.orc_exact_cell.argtypes = [C.c_float] * 6 + [f32p, f32p]
     L.orc_doppler_g.argtypes = [C.c_float] * 6; L.orc_doppler_g.restype = C.c_float
     L.orc_doppler_gfx.argtypes = [C.c_float]; L.orc_doppler_gfx.restype = C.c_uint32
     L.orc_doppler_Q.argtypes = [C.c_uint64, C.c_float, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]
@@ -162,6 +164,12 @@ def birth_slots(Rb, nu_b: int) -> np.ndarray:
 
 def exp_spec(q: float) -> float:
     return lib().orc_exp_spec(q)
+
+
+def exact_cell(S, occ_max, p_b, occurred, pTP, pFP):
+    rp, rb = C.c_float(), C.c_float()
+    lib().orc_exact_cell(S, occ_max, p_b, occurred, pTP, pFP, C.byref(rp), C.byref(rb))
+    return rp.value, rb.value
 
 
 def doppler_g(vx, vy, ux, uy, vr, sd) -> float:
@@ -287,6 +295,12 @@ class Oracle:
         assert a is None or a.size == self.C
         return lib().orc_step_doppler(self._h, _ptr(m, C.c_float), None if d is None else d.ctypes.data,
                                       None if a is None else a.ctypes.data, C.c_float(dt))
+
+    def step_exact(self, obs, dt: float) -> int:
+        """NEXT-3 exact PHD/MIB cycle: obs [C, 4] = (occurred, p_TP, p_FP, 0)."""
+        o = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1)
+        assert o.size == 4 * self.C
+        return lib().orc_step_exact(self._h, _ptr(o, C.c_float), C.c_float(dt))
 
     def ego_scroll(self, dx: float, dy: float):
         """Ego-motion compensation (NEXT-2): (shift_x, shift_y) in cells, or None if refused."""

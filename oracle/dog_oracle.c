@@ -393,7 +393,44 @@ int orc_step(orc_ctx* h, const float* meas, float dt)
 /* One cycle with the Doppler / association branch (NEXT-1).  dop[C][4] = (u_x, u_y, v_r, sd): unit
  * radial direction, measured radial speed (m/s), its SD; pA[C] = association probability p_A (0: the
  * cell has no Doppler measurement).  dop == NULL or pA == NULL: no cell has one (orc_step). */
+static int step_impl(orc_ctx* h, const float* meas, const float* obs, const float* dop, const float* pA, float dt);
+
 int orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const float* pA, float dt)
+{
+    return step_impl(h, meas, NULL, dop, pA, dt);
+}
+
+/* The exact PHD/MIB filter (NEXT-3; section V) for a uniform single-object likelihood equal
+ * to the clutter density (the setting of the section IV-F proposition): the cycle of
+ * orc_step with the Bernoulli update of Eqs. (38)-(42) in place of Dempster's rule (A-37).
+ * obs[C][4] = (occurred, p_TP, p_FP, unused): a measurement occurred in the cell (1) or not (0),
+ * its true- and false-positive probabilities. */
+int orc_step_exact(orc_ctx* h, const float* obs, float dt)
+{
+    return step_impl(h, NULL, obs, NULL, NULL, dt);
+}
+
+/* Cell update of the exact filter (A-37): r_p+ = min(S, occ_max) (Eq. 31 with the truncation of
+ * P:938-939), r_b+ = p_B (1 - r_p+) (Eq. 32); r+ = r_p+ + r_b+; the common weight factor
+ * f = p_TP / (p_FP (1 - r+) + p_TP r+) if a measurement occurred (Eqs. 38-40; the uniform likelihood
+ * g_A = p_cl cancels), else (1 - p_TP) / ((1 - p_FP)(1 - r+) + (1 - p_TP) r+) (Eq. 41); rho_p = r_p+ f,
+ * rho_b = r_b+ f (Eq. 42: their sum is the posterior occupancy).  f32, in this order. */
+void orc_exact_cell(float S, float occ_max, float p_b, float occurred, float pTP, float pFP, float* rho_p,
+                    float* rho_b)
+{
+    float rpp = fminf(S, occ_max);
+    float rbp = p_b * (1.0f - rpp);
+    float rplus = rpp + rbp;
+    float rbar = 1.0f - rplus;
+    float num, den;
+    if (occurred > 0.0f) { num = pTP; den = pFP * rbar + pTP * rplus; }
+    else { num = 1.0f - pTP; den = (1.0f - pFP) * rbar + (1.0f - pTP) * rplus; }
+    float f = den > 0.0f ? num / den : 0.0f;
+    *rho_p = rpp * f;
+    *rho_b = rbp * f;
+}
+
+static int step_impl(orc_ctx* h, const float* meas, const float* obs, const float* dop, const float* pA, float dt)
 {
     const orc_params* P = &h->p;
     const int64_t W = P->width, H = P->height, C = h->C, nu = P->nu, nu_b = P->nu_b;
@@ -436,7 +473,20 @@ int orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const floa
 
     /* ---- O3 Cells (Alg. 3; Eqs. 61-63, 67-68; A-7..A-13, A-22, A-23, A-27) ---- */
     uint64_t bad = 0;
-    for (int64_t c = 0; c < C; ++c) {
+    for (int64_t c = 0; c < C && obs; ++c) {                  /* exact PHD/MIB (NEXT-3, A-37) */
+        uint32_t a = h->offsets[c], b = h->offsets[c + 1];
+        double sum = 0.0;                                      /* Eq. 31: sum of predicted weights */
+        for (uint32_t j = a; j < b; ++j) sum += (double)w_pred;
+        float S = (float)sum;
+        const float* ob = obs + 4 * c;
+        float rp, rb;
+        orc_exact_cell(S, P->occ_max, P->p_b, ob[0], ob[1], ob[2], &rp, &rb);
+        h->S[c] = S; h->mp[c] = fminf(S, P->occ_max); h->mfp[c] = 0.0f;
+        h->occ[c] = rp + rb; h->fre[c] = 1.0f - (rp + rb); h->rho_p[c] = rp; h->rho_b[c] = rb;
+        h->Rp[c] = (b > a) ? fx40(rp) : 0;                     /* A-23 */
+        h->Rb[c] = fx40(rb);                                   /* births wherever r_b > 0 */
+    }
+    for (int64_t c = 0; c < C && !obs; ++c) {
         uint32_t a = h->offsets[c], b = h->offsets[c + 1];
         double sum = 0.0;                                      /* Eq. 61: sum of predicted weights */
         for (uint32_t j = a; j < b; ++j) sum += (double)w_pred;

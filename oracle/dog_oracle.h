@@ -93,6 +93,12 @@ int  orc_step(orc_ctx* h, const float* meas, float dt);
  * dop[C][4] = (u_x, u_y, v_r, sd) radial unit direction, measured radial speed (m/s) and its SD;
  * pA[C] = association probability p_A in [0, 1] (0: no Doppler in the cell).  NULL: orc_step. */
 int  orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const float* pA, float dt);
+/* The exact PHD/MIB filter (NEXT-3; section V) with a uniform likelihood equal to the
+ * clutter density (section IV-F setting): obs[C][4] = (occurred 0/1, p_TP, p_FP, unused) (A-37).
+ * m_F is not used (left unchanged); occupancy readout = rho_p + rho_b, free = 1 - occupancy. */
+int  orc_step_exact(orc_ctx* h, const float* obs, float dt);
+void orc_exact_cell(float S, float occ_max, float p_b, float occurred, float pTP, float pFP, float* rho_p,
+                    float* rho_b);
 /* NEXT-1 primitives (exported for the pins) */
 float    orc_exp_spec(float q);                                             /* e^q, q <= 0 (A-34) */
 float    orc_doppler_g(float vx, float vy, float ux, float uy, float vr, float sd);   /* Eq. 69 g */

@@ -489,13 +489,19 @@ static int L_predict_sort(dog_ctx* ctx, bool fused, const StepArgs& a, const Fil
     return DOG_OK;
 }
 
-static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
+                   const float* obs = nullptr)
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
-    CK(launch(k_cells, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
-              (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-              ctx->cell_chunk, ctx->sc, fc, a.alpha));
+    if (obs)
+        CK(launch(k_cells<true>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
+                  (const float2*)nullptr, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)obs));
+    else
+        CK(launch(k_cells<false>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
+                  (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)nullptr));
     return DOG_OK;
 }
 
@@ -551,9 +557,23 @@ static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cuda
     return DOG_OK;
 }
 
+static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt, void* stream);
+
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
 {
-    if (!ctx || !meas) return DOG_E_INVAL;
+    if (!meas) return DOG_E_INVAL;
+    return step_impl(ctx, meas, nullptr, dt, stream);
+}
+
+int dog_step_exact(dog_ctx* ctx, const float* obs, float dt, void* stream)
+{
+    if (!obs || ((uintptr_t)obs & 15u) != 0) return DOG_E_INVAL;
+    return step_impl(ctx, nullptr, obs, dt, stream);
+}
+
+static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt, void* stream)
+{
+    if (!ctx) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
     if (ctx->world > 1) return DOG_E_STATE;                 // band contexts run the dog_band_* phases
     if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
@@ -574,7 +594,7 @@ int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
     if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
     CK(mark("predict_sort"));
     // 3. cells: DS predict/update, birth split, fixed point, active-cell staging (Alg. 3)
-    if (int r = L_cells(ctx, meas, a, fc, st)) return r;
+    if (int r = L_cells(ctx, meas, a, fc, st, obs)) return r;
     CK(mark("cells"));
     // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;

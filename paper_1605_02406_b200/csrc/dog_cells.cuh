@@ -110,6 +110,36 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     return o;
 }
 
+// The exact PHD/MIB cell update (NEXT-3, A-37; Eqs. 31-32, 38-42 with a uniform likelihood equal to
+// the clutter density, the section IV-F setting): obs = (occurred, p_TP, p_FP, -).  f32 in the order of
+// orc_exact_cell.  occupancy = rho_p + rho_b (mO), free = 1 - occupancy (mF); births wherever r_b > 0.
+__device__ __forceinline__ CellOut cell_math_exact(uint32_t n, float4 obs, float w_pred, const FilterConst& fc)
+{
+    CellOut o;
+    o.n = n;
+    o.S = __double2float_rn(__dmul_rn((double)n, (double)w_pred));        // Eq. 31, exact
+    const float rpp = fminf(o.S, fc.occ_max);                              // truncation
+    const float rbp = __fmul_rn(fc.p_b, __fsub_rn(1.0f, rpp));             // Eq. 32
+    const float rplus = __fadd_rn(rpp, rbp), rbar = __fsub_rn(1.0f, rplus);
+    float num, den;
+    if (obs.x > 0.0f) {                                                    // Eqs. 38-40 (g_A = p_cl cancels)
+        num = obs.y;
+        den = __fadd_rn(__fmul_rn(obs.z, rbar), __fmul_rn(obs.y, rplus));
+    } else {                                                               // Eq. 41
+        num = __fsub_rn(1.0f, obs.y);
+        den = __fadd_rn(__fmul_rn(__fsub_rn(1.0f, obs.z), rbar), __fmul_rn(num, rplus));
+    }
+    const float f = den > 0.0f ? __fdiv_rn(num, den) : 0.0f;
+    o.rp = __fmul_rn(rpp, f);
+    o.rb = __fmul_rn(rbp, f);
+    o.mO = __fadd_rn(o.rp, o.rb);                                          // Eq. 42
+    o.mF = __fsub_rn(1.0f, o.mO);
+    o.Rp = n > 0 ? fx40(o.rp) : 0ull;
+    o.Rb = fx40(o.rb);
+    o.bad = false;
+    return o;
+}
+
 constexpr int kCellThreads = 256, kCellItems = 8, kCellIter = kCellThreads * kCellItems;   // 2048 cells
 constexpr int kMaxCellBlocks = 4096;
 
@@ -139,10 +169,13 @@ __device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
 // loads of an iteration are issued up front.  Active cells (~1 %) keep their inputs (n_c, m_F) untouched
 // in the first pass; after the block's staging offsets are known they are recomputed from them
 // (identical arithmetic) and staged, and only then is m_F updated and n_c cleared.
+// kExact: the exact PHD/MIB update from obs[C] (NEXT-3) instead of Dempster's rule from meas; m_F untouched.
+template <bool kExact>
 __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
-    uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha)
+    uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha,
+    const float4* __restrict__ obs)
 {
     PDL_ENTER();
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
@@ -163,13 +196,18 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         uint32_t n[kCellItems], prev[kCellItems];
         float mf[kCellItems];
         float2 z[kCellItems];
+        float4 ob[kCellItems];
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
             n[i] = valid ? counts[c] : 0u;
-            mf[i] = valid ? m_free[c] : 0.0f;
-            z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
+            if (kExact) {
+                ob[i] = valid ? obs[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            } else {
+                mf[i] = valid ? m_free[c] : 0.0f;
+                z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
+            }
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
             prev[i] = (lane == 0 && (word << 5) < c1) ? mvalid[word] : 0u;
         }
@@ -178,7 +216,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
-            const CellOut o = cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
+            const CellOut o = kExact ? cell_math_exact(n[i], ob[i], w_pred, fc) : cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
             const bool vnow = valid && o.n > 0 && o.rp > 0.0f && o.S > 0.0f;
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
             const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
@@ -187,7 +225,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
             if (valid) {
                 occ[c] = o.mO;
                 free_out[c] = o.mF;
-                if (!act) m_free[c] = o.mF;             // Alg. 3 store_values (active cells: below)
+                if (!kExact && !act) m_free[c] = o.mF;  // Alg. 3 store_values (active cells: below)
                 if (!vnow && ((pw >> lane) & 1u)) {     // moments were reported last cycle: clear (A-18)
                     mean[c] = make_float2(0.0f, 0.0f);
                     cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
@@ -217,8 +255,9 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         for (int i = 0; i < kCellItems; ++i) {
             if ((abal[i] >> lane) & 1u) {               // active cell: same inputs (untouched), same arithmetic
                 const uint32_t c = base + i * kCellThreads + tid;
-                const CellOut o = cell_math(__ldcg(counts + c), __ldcg(m_free + c), meas[c], w_pred, alpha, fc);
-                m_free[c] = o.mF;
+                const CellOut o = kExact ? cell_math_exact(__ldcg(counts + c), obs[c], w_pred, fc)
+                                         : cell_math(__ldcg(counts + c), __ldcg(m_free + c), meas[c], w_pred, alpha, fc);
+                if (!kExact) m_free[c] = o.mF;
                 if (o.n) counts[c] = 0u;                // ready for the next cycle's k_predict_sort
                 const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
                 L.c[li] = c; L.n[li] = o.n; L.Rp[li] = o.Rp; L.Rb[li] = o.Rb; L.rho_p[li] = o.rp;

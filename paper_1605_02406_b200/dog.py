@@ -57,6 +57,7 @@ _SIGS = {
                     C.POINTER(_vp)], C.c_int),
     "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_doppler": ([_vp, _vp, _vp, _vp, C.c_float, _vp], C.c_int),
+    "dog_step_exact": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_step_host_async": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_read_cells": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -175,6 +176,11 @@ class Filter:
         assert meas.is_cuda and meas.dtype == torch.float32 and meas.is_contiguous()
         assert meas.numel() == 2 * self.C
         _check(dog_step(self._h, meas.data_ptr(), dt, _stream_ptr(stream)), "dog_step")
+
+    def step_exact(self, obs: torch.Tensor, dt: float, stream=None):
+        """include/dog.h dog_step_exact (NEXT-3): obs [C, 4] = (occurred, p_TP, p_FP, 0) on the device."""
+        assert obs.is_cuda and obs.dtype == torch.float32 and obs.is_contiguous() and obs.numel() == 4 * self.C
+        _check(dog_step_exact(self._h, obs.data_ptr(), dt, _stream_ptr(stream)), "dog_step_exact")
 
     def step_doppler(self, meas: torch.Tensor, doppler: torch.Tensor, p_assoc: torch.Tensor, dt: float, stream=None):
         """include/dog.h dog_step_doppler (NEXT-1): doppler [C, 4] = (u_x, u_y, v_r, sd), p_assoc [C]."""

@@ -278,6 +278,24 @@ class Scene:
         pA = np.where(has, np.float32(p_assoc), np.float32(0.0)).astype(np.float32)
         return torch.from_numpy(dop).to(device), torch.from_numpy(pA).to(device)
 
+    @staticmethod
+    def exact_obs(meas: torch.Tensor, kappa: float = 0.9) -> torch.Tensor:
+        """Observation grid of the exact PHD/MIB filter (NEXT-3 input) from a measurement grid
+        [..., 2] = (m_zO, m_zF), A-37 input recipe: a cell with a return (m_zO > 0) has a
+        measurement (occurred = 1) with p_TP = kappa and p_FP = kappa (1 - m_zO) / m_zO capped at kappa
+        (likelihood ratio m_zO / (1 - m_zO)); a cell seen free has none, with p_TP = m_zF and p_FP = 0.01;
+        an unobserved cell has none with p_TP = p_FP = 0.05 (ratio 1: uninformative).  Returns f32
+        [..., 4] = (occurred, p_TP, p_FP, 0) on the input's device."""
+        mO, mF = meas[..., 0], meas[..., 1]
+        hit = mO > 0
+        seen = (~hit) & (mF > 0)
+        out = torch.zeros(meas.shape[:-1] + (4,), dtype=torch.float32, device=meas.device)
+        out[..., 0] = hit.float()
+        pfp_hit = torch.clamp(kappa * (1.0 - mO) / torch.clamp(mO, min=1e-6), max=kappa)
+        out[..., 1] = torch.where(hit, torch.full_like(mO, kappa), torch.where(seen, mF, torch.full_like(mO, 0.05)))
+        out[..., 2] = torch.where(hit, pfp_hit, torch.where(seen, torch.full_like(mO, 0.01), torch.full_like(mO, 0.05)))
+        return out.contiguous()
+
     def frames(self, k0: int, n: int, device="cpu") -> torch.Tensor:
         return torch.stack([self.frame(k0 + i, device) for i in range(n)])
 
