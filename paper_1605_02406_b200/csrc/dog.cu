@@ -71,6 +71,7 @@ struct dog_ctx {
     StageList stage{};                            // k_cells staging (per cell chunk)
     CellList list{};                              // flat active-cell list
     BlockTotals bt{};
+    WideScan ws{};                                // grid-wide list scan (large active lists)
     uint32_t ls_cluster = 0, flat_blocks = 0;     // k_list_scan cluster size; lane-per-cell grids
     uint32_t* cell2list = nullptr;
     MomPartial* ppart = nullptr;                  // velocity sums per run
@@ -381,6 +382,10 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     AL(ctx->list.rb, Cs); AL(ctx->list.np, Cs); AL(ctx->list.ps, Cs); AL(ctx->list.pfill, Cs);
     AL(ctx->cell2list, Cs);
     AL(ctx->bt.cnt, ctx->cell_blocks); AL(ctx->bt.n0, ctx->cell_blocks); AL(ctx->bt.rb0, ctx->cell_blocks);
+    AL(ctx->bt.np0, ctx->cell_blocks);
+    AL(ctx->ws.pcnt, ctx->cell_blocks); AL(ctx->ws.pn, ctx->cell_blocks); AL(ctx->ws.pnp, ctx->cell_blocks);
+    AL(ctx->ws.prb, ctx->cell_blocks); AL(ctx->ws.tJ, ctx->cell_blocks); AL(ctx->ws.tit, ctx->cell_blocks);
+    AL(ctx->ws.pJ, ctx->cell_blocks); AL(ctx->ws.pit, ctx->cell_blocks);
 
     if (ctx->world > 1) {
         for (int d = 0; d < 2; ++d) {
@@ -505,8 +510,18 @@ static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const Fil
     return DOG_OK;
 }
 
-static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
+                       bool wide = false)
 {
+    if (wide && !A_all) {   // every cell may be active (exact filter): grid-wide scan over k_cells' chunks
+        CK(launch(k_ls_prefix1, 1, 1024, 0, st, 0, ctx->bt, ctx->cell_blocks, ctx->ws, ctx->sc));
+        CK(launch(k_ls_chunks1, ctx->cell_blocks, 256, 0, st, 0, ctx->stage, ctx->list, ctx->bt, ctx->cell_chunk,
+                  ctx->cell2list, ctx->ws, (const DevScalars*)ctx->sc, fc));
+        CK(launch(k_ls_prefix2, 1, 1024, 0, st, 0, ctx->cell_blocks, ctx->ws));
+        CK(launch(k_ls_chunks2, ctx->cell_blocks, 256, 0, st, 0, ctx->list, ctx->bt, ctx->ws, ctx->sc, fc,
+                  (int64_t)a.k));
+        return DOG_OK;
+    }
     CK(launch(k_list_scan, ctx->ls_cluster, kLsThreads, 0, st, ctx->ls_cluster, ctx->stage, ctx->list, ctx->bt,
               ctx->cell_blocks, ctx->cell_chunk, ctx->cell2list, A_all, ctx->sc, fc, (int64_t)a.k));
     return DOG_OK;
@@ -546,14 +561,18 @@ static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullpt
 }
 
 static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                    const DopIn* din = nullptr)
+                    const DopIn* din = nullptr, bool per_slot = false)
 {
     if (ctx->nu_b == 0) return DOG_OK;
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
-    CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
-              (int64_t)a.k, din ? din->pA : (const float*)nullptr, din ? din->dop : (const float4*)nullptr));
+    if (per_slot)
+        CK(launch(k_births_slots, (uint32_t)std::max<int64_t>(1, std::min<int64_t>((ctx->nu_b + 255) / 256, 8 * 148)), 256, 0,
+                  st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc, (int64_t)a.k));
+    else
+        CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
+                  (int64_t)a.k, din ? din->pA : (const float*)nullptr, din ? din->dop : (const float4*)nullptr));
     return DOG_OK;
 }
 
@@ -597,7 +616,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (int r = L_cells(ctx, meas, a, fc, st, obs)) return r;
     CK(mark("cells"));
     // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
-    if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
+    if (int r = L_list_scan(ctx, nullptr, a, fc, st, obs != nullptr)) return r;
     CK(mark("list_scan"));
     // 5. each cell's runs in tile order -> stable within-cell ranks; global totals (w_bar)
     if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
@@ -609,7 +628,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (fork) {
         CK(cudaEventRecord(ctx->ev_fork, st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-        if (int r = L_births(ctx, a, fc, ctx->side)) return r;
+        if (int r = L_births(ctx, a, fc, ctx->side, nullptr, obs != nullptr)) return r;
         CK(cudaEventRecord(ctx->ev_join, ctx->side));
     }
     if (int r = L_resample(ctx, a, fc, st)) return r;
@@ -619,7 +638,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (fork) {
         CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     } else {
-        if (int r = L_births(ctx, a, fc, st)) return r;
+        if (int r = L_births(ctx, a, fc, st, nullptr, obs != nullptr)) return r;
         CK(mark("births"));
     }
     if (prof) {

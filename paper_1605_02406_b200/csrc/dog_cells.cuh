@@ -56,6 +56,7 @@ struct BlockTotals {        // one entry per cell chunk (k_cells); prefixes / to
     uint32_t* cnt;          // active cells staged by the block
     uint64_t* n0;           // sum of n_c over them
     uint64_t* rb0;          // sum of R_b over them
+    uint32_t* np0;          // sum of their run counts
 };
 
 __device__ __forceinline__ uint64_t fx40(float m)
@@ -191,7 +192,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     if (tid == 0) s_run = 0;
 
     uint64_t A_loc = 0, N_loc = 0;
-    uint32_t bad_loc = 0;
+    uint32_t bad_loc = 0, P_loc = 0;
     for (uint32_t base = c0; base < c1; base += kCellIter) {
         uint32_t n[kCellItems], prev[kCellItems];
         float mf[kCellItems];
@@ -266,6 +267,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
                 L.np[li] = npc;
                 A_loc += o.Rb;
                 N_loc += o.n;
+                P_loc += npc;
             }
         }
         __syncthreads();
@@ -273,13 +275,17 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     // block totals (integers: order-independent)
     A_loc = warp_sum(A_loc);
     N_loc = warp_sum(N_loc);
+    P_loc = warp_sum(P_loc);
     bad_loc = warp_sum(bad_loc);
-    if (lane == 0) { s_A[warp] = A_loc; s_N[warp] = N_loc; s_bad[warp] = bad_loc; }
+    __shared__ uint32_t s_P[8];
+    if (lane == 0) { s_A[warp] = A_loc; s_N[warp] = N_loc; s_bad[warp] = bad_loc; s_P[warp] = P_loc; }
     __syncthreads();
     if (tid == 0) {
         uint64_t A = 0, N = 0; uint32_t b = 0;
-        for (int w = 0; w < kCellThreads / 32; ++w) { A += s_A[w]; N += s_N[w]; b += s_bad[w]; }
+        uint32_t np = 0;
+        for (int w = 0; w < kCellThreads / 32; ++w) { A += s_A[w]; N += s_N[w]; b += s_bad[w]; np += s_P[w]; }
         bt.cnt[blockIdx.x] = s_run;
+        bt.np0[blockIdx.x] = np;
         bt.n0[blockIdx.x] = N;
         bt.rb0[blockIdx.x] = A;
         if (b) atomicAdd(&sc->meas_bad, b);
@@ -538,6 +544,168 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
         sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
     }
     cluster.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+// ------------------------------------------------------------------------------------------------
+// The same flat active list for LARGE lists (the exact PHD/MIB filter stages every cell: r_b > 0
+// everywhere), grid-wide instead of one cluster: the tiles are k_cells' chunks, whose pair-1 totals
+// (entries, n_c, runs, R_b) k_cells already wrote (BlockTotals).
+//   k_ls_prefix1  (1 block): exclusive prefixes of the chunk totals; Lc, n_in, A
+//   k_ls_chunks1  (chunk per block): local scans + chunk prefix -> start, ps, A_c -> slots, split, J, items
+//                 -> the list entries; chunk totals of (J, items)
+//   k_ls_prefix2  (1 block): exclusive prefixes of (J, items)
+//   k_ls_chunks2  (chunk per block): local scans of (J, items) -> P, it; the last entry publishes W, U
+// Integer sums, so every prefix equals the cluster kernel's (and the oracle's) exactly.
+struct WideScan {
+    uint32_t* pcnt; uint64_t* pn; uint32_t* pnp; uint64_t* prb;   // chunk prefixes, pair 1
+    uint64_t* tJ; uint32_t* tit;                                  // chunk totals, pair 2
+    uint64_t* pJ; uint32_t* pit;                                  // chunk prefixes, pair 2
+};
+
+__global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nblk, WideScan ws,
+                                                     DevScalars* __restrict__ sc)
+{
+    PDL_ENTER();
+    __shared__ uint64_t s_w[33];
+    constexpr int kI = (kMaxCellBlocks + 1023) / 1024;
+    const int tid = threadIdx.x;
+    uint64_t c[kI], n[kI], p[kI], r[kI], sc_ = 0, sn = 0, sp = 0, sr = 0;
+#pragma unroll
+    for (int i = 0; i < kI; ++i) {
+        const uint32_t b = tid * kI + i;
+        const bool ok = b < nblk;
+        c[i] = ok ? bt.cnt[b] : 0u; n[i] = ok ? bt.n0[b] : 0ull; p[i] = ok ? bt.np0[b] : 0u; r[i] = ok ? bt.rb0[b] : 0ull;
+        sc_ += c[i]; sn += n[i]; sp += p[i]; sr += r[i];
+    }
+    uint64_t tc, tn, tp, tr;
+    uint64_t oc = block_excl_scan<uint64_t, 32>(sc_, s_w, tc);
+    uint64_t on = block_excl_scan<uint64_t, 32>(sn, s_w, tn);
+    uint64_t op = block_excl_scan<uint64_t, 32>(sp, s_w, tp);
+    uint64_t orb = block_excl_scan<uint64_t, 32>(sr, s_w, tr);
+#pragma unroll
+    for (int i = 0; i < kI; ++i) {
+        const uint32_t b = tid * kI + i;
+        if (b < nblk) { ws.pcnt[b] = (uint32_t)oc; ws.pn[b] = on; ws.pnp[b] = (uint32_t)op; ws.prb[b] = orb; }
+        oc += c[i]; on += n[i]; op += p[i]; orb += r[i];
+    }
+    if (tid == 0) { sc->Lc = (uint32_t)tc; sc->A = tr; sc->n_in = tn; }
+}
+
+__global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, BlockTotals bt, uint32_t chunk,
+                                                    uint32_t* __restrict__ cell2list, WideScan ws,
+                                                    const DevScalars* __restrict__ sc, FilterConst fc)
+{
+    PDL_ENTER();
+    __shared__ uint64_t s_w[9];
+    const uint32_t b = blockIdx.x, m = bt.cnt[b];
+    const uint64_t A = sc->A, nu_b = fc.nu_b;
+    const double rcpA = A ? 1.0 / (double)A : 0.0;
+    uint64_t carryX = ((uint64_t)ws.pnp[b] << 32) | ws.pn[b], carryB = ws.prb[b], sJ = 0, sI = 0;
+    for (uint32_t j0 = 0; j0 < m; j0 += 256) {             // block-uniform trip count
+        const uint32_t j = j0 + threadIdx.x;
+        const bool ok = j < m;
+        const uint32_t si = b * chunk + j;
+        uint32_t c = 0, n = 0, npv = 0;
+        uint64_t Rp = 0, Rb = 0;
+        float rho = 0.0f;
+        if (ok) { c = Ls.c[si]; n = Ls.n[si]; npv = Ls.np[si]; Rp = Ls.Rp[si]; Rb = Ls.Rb[si]; rho = Ls.rho_p[si]; }
+        const uint64_t X = (uint64_t)n | ((uint64_t)npv << 32);
+        uint64_t tX, tB;
+        const uint64_t exX = block_excl_scan<uint64_t, 8>(X, s_w, tX);
+        const uint64_t exB = block_excl_scan<uint64_t, 8>(Rb, s_w, tB);
+        if (ok) {
+            const uint32_t g = ws.pcnt[b] + j;
+            const uint64_t x0 = carryX + exX, Ax = carryB + exB;
+            const uint64_t sp = slot_of(Ax, A, nu_b, rcpA);
+            const uint64_t s_next = Rb ? slot_of(Ax + Rb, A, nu_b, rcpA) : sp;
+            const uint32_t nbv = (uint32_t)(s_next - sp);
+            L.c[g] = c; L.n[g] = n; L.Rp[g] = Rp; L.rho_p[g] = rho;
+            L.np[g] = npv; L.ps[g] = (uint32_t)(x0 >> 32); L.pfill[g] = 0u;
+            L.start[g] = (uint32_t)x0;
+            L.sb[g] = (uint32_t)sp;
+            L.nb[g] = nbv;
+            uint32_t rem = 0;
+            L.bp[g] = n ? divmod53(Rp, n, rem) : 0ull;
+            L.rp[g] = rem;
+            rem = 0;
+            L.bb[g] = nbv ? divmod53(Rb, nbv, rem) : 0ull;
+            L.rb[g] = rem;
+            cell2list[c] = g;
+            sJ += Rp + (nbv ? Rb : 0ull);
+            sI += (nbv + kItem - 1) / kItem;
+        }
+        carryX += tX; carryB += tB;
+    }
+    uint64_t tJ, tI;
+    block_excl_scan<uint64_t, 8>(sJ, s_w, tJ);
+    block_excl_scan<uint64_t, 8>(sI, s_w, tI);
+    if (threadIdx.x == 0) { ws.tJ[b] = tJ; ws.tit[b] = (uint32_t)tI; }
+}
+
+__global__ __launch_bounds__(1024) void k_ls_prefix2(uint32_t nblk, WideScan ws)
+{
+    PDL_ENTER();
+    __shared__ uint64_t s_w[33];
+    constexpr int kI = (kMaxCellBlocks + 1023) / 1024;
+    const int tid = threadIdx.x;
+    uint64_t J[kI], I[kI], sJ = 0, sI = 0;
+#pragma unroll
+    for (int i = 0; i < kI; ++i) {
+        const uint32_t b = tid * kI + i;
+        J[i] = b < nblk ? ws.tJ[b] : 0ull; I[i] = b < nblk ? ws.tit[b] : 0u;
+        sJ += J[i]; sI += I[i];
+    }
+    uint64_t tJ, tI;
+    uint64_t oJ = block_excl_scan<uint64_t, 32>(sJ, s_w, tJ);
+    uint64_t oI = block_excl_scan<uint64_t, 32>(sI, s_w, tI);
+#pragma unroll
+    for (int i = 0; i < kI; ++i) {
+        const uint32_t b = tid * kI + i;
+        if (b < nblk) { ws.pJ[b] = oJ; ws.pit[b] = (uint32_t)oI; }
+        oJ += J[i]; oI += I[i];
+    }
+}
+
+__global__ __launch_bounds__(256) void k_ls_chunks2(CellList L, BlockTotals bt, WideScan ws,
+                                                    DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+{
+    PDL_ENTER();
+    __shared__ uint64_t s_w[9];
+    const uint32_t b = blockIdx.x, m = bt.cnt[b];
+    const uint32_t Lc = sc->Lc;
+    const uint64_t A = sc->A;
+    uint64_t carryJ = ws.pJ[b], carryI = ws.pit[b];
+    for (uint32_t j0 = 0; j0 < m; j0 += 256) {
+        const uint32_t j = j0 + threadIdx.x;
+        const bool ok = j < m;
+        const uint32_t g = ws.pcnt[b] + j;
+        uint64_t J = 0, I = 0;
+        if (ok) {
+            const uint32_t nbv = L.nb[g];
+            J = L.Rp[g] + (nbv ? L.bb[g] * nbv + L.rb[g] : 0ull);   // R_p + gated R_b = bb nb + rb
+            I = (nbv + kItem - 1) / kItem;
+        }
+        uint64_t tJ, tI;
+        const uint64_t eJ = block_excl_scan<uint64_t, 8>(J, s_w, tJ);
+        const uint64_t eI = block_excl_scan<uint64_t, 8>(I, s_w, tI);
+        if (ok) {
+            const uint64_t P = carryJ + eJ;
+            const uint32_t it0 = (uint32_t)(carryI + eI);
+            L.P[g] = P;
+            L.it[g] = it0;
+            if (g == Lc - 1) {
+                sc->W = P + J;
+                sc->n_items = it0 + (uint32_t)I;
+                sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
+                sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
+            }
+        }
+        carryJ += tJ; carryI += tI;
+    }
+    if (Lc == 0 && b == 0 && threadIdx.x == 0) {   // empty list (A-26)
+        sc->W = 0; sc->n_items = 0; sc->s_total = A ? (uint64_t)fc.nu_b : 0ull;
+        sc->U = draw(fc.seed, 0u, k, STAGE_RESAMPLE).r0;
+    }
 }
 
 }  // namespace dog

@@ -605,4 +605,58 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
     }
 }
 
+// New-born particles, one thread per birth SLOT (lists where most cells get one or two slots -- the
+// exact filter spreads nu_b over the whole grid, so k_births' per-cell work items would leave most lanes
+// idle).  Slot s belongs to the last list entry with sb <= s; same draws, state and joint CDF as
+// k_births (no Doppler split); copies written by the slot's own thread.
+__global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out, BirthDebug bdbg,
+                                                      const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+{
+    PDL_ENTER();
+    const RsConst rc = make_rsconst(sc, fc.nu);
+    const int par = (int)(k & 1);
+    out.s += fc.lo_cap - sc->o_base[par ^ 1];
+    const uint64_t Ppre = sc->Ppre;
+    const uint32_t Lc = sc->Lc;
+    const uint32_t ns = (uint32_t)sc->s_total;
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = Lc;                                   // last entry with sb <= s
+        while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (L.sb[m] <= s) lo = m; else hi = m; }
+        const uint32_t li = lo;
+        const uint32_t c = L.c[li], nb = L.nb[li], sb = L.sb[li];
+        if (s - sb >= nb) continue;                                 // (not reached: slots are dense)
+        const uint32_t r = s - sb;
+        const uint64_t bb = L.bb[li];
+        const uint32_t rbm = L.rb[li];
+        const uint64_t PB = Ppre + L.P[li] + L.Rp[li];
+        const uint32_t cg = c + fc.c_off;
+        const uint32_t col = cg % (uint32_t)fc.W, row = cg / (uint32_t)fc.W;
+        const float colf = (float)col, rowf = (float)row;
+        const float cx1 = __fadd_rn(colf, 1.0f), cy1 = __fadd_rn(rowf, 1.0f);
+        const Philox4 d = draw(fc.seed, s, k, STAGE_BIRTH);
+        float bx = __fadd_rn(colf, unit24(d.r0));
+        float by = __fadd_rn(rowf, unit24(d.r1));
+        if (bx >= cx1) bx = __int_as_float(__float_as_int(cx1) - 1);
+        if (by >= cy1) by = __int_as_float(__float_as_int(cy1) - 1);
+        float n0, n1;
+        box_muller(d.r2, d.r3, n0, n1);
+        float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
+        if (fc.v_max > 0.0f) {
+            bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
+            bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);
+        }
+        if (bdbg.x) { bdbg.x[s] = bx; bdbg.y[s] = by; bdbg.vx[s] = bvx; bdbg.vy[s] = bvy; }
+        if (rc.W) {
+            const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
+            const uint64_t Q1 = Q0 + bb + (r < rbm ? 1u : 0u);
+            const uint32_t F0 = fcount(Q0, rc), F1 = fcount(Q1, rc);
+            const uint32_t J = L.start[li] + sb + L.n[li] + r;
+            for (uint32_t o = F0; o < F1; ++o) {
+                out.s[o] = make_float4(bx, by, bvx, bvy);
+                if (out.jidx) out.jidx[o] = J;
+            }
+        }
+    }
+}
+
 }  // namespace dog
