@@ -96,6 +96,7 @@ struct dog_ctx {
     cudaStream_t h2d = nullptr, d2h = nullptr;
     // births run on a side stream beside resampling (independent outputs; joined before the step ends)
     // Doppler / association branch (NEXT-1), allocated on the first dog_step_doppler
+    uint32_t* kscr = nullptr;                     // k_predict_sort: full keys of tiles with > 2^20-cell boxes
     uint64_t* d_rg = nullptr;                     // per run slot: gfx sum, then exclusive cell prefix
     uint64_t* d_rs = nullptr;                     // per run slot: block prefix at the run's first member
     uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
@@ -359,7 +360,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
     AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rfg, N);
-    AL(ctx->lperm, N);
+    AL(ctx->lperm, N); AL(ctx->kscr, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
     AL(ctx->counts, Cs + 1); AL(ctx->npairs, Cs + 1);
@@ -487,10 +488,10 @@ static int L_predict_sort(dog_ctx* ctx, bool fused, const StepArgs& a, const Fil
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     if (fused)
         CK(launch(k_predict_sort<true>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
-                  dbg ? ctx->keys : nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
+                  dbg ? ctx->keys : nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a, ctx->kscr));
     else
         CK(launch(k_predict_sort<false>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
-                  (uint32_t*)nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a));
+                  (uint32_t*)nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a, ctx->kscr));
     return DOG_OK;
 }
 

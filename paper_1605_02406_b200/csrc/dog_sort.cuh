@@ -52,9 +52,13 @@ struct TilePairs {          // per tile t: entries [t*4096, t*4096 + nd[t])
 // ------------------------------------------------------------------------------------------------
 constexpr int kPsThreads = 256, kPsWarps = kPsThreads / 32, kPsRows = kSortTile / kPsThreads;   // 16
 
+// Sort records are packed (field << 12 | local index) in one u32 (a tile holds 4096 = 2^12 particles):
+// one word moves per element and pass.  A remapped key of <= 20 bits is the field itself (the usual
+// case); wider keys (a tile spread over > 2^20 cells of its bounding box) are sorted in two stable
+// phases -- low 20 bits, then the high bits -- with the full keys kept in global scratch (kscr).
+constexpr int kPkIdx = 12, kPkField = 32 - kPkIdx;   // 20-bit field
 struct PsSmem {
-    uint32_t k[2][kSortTile];          // keys, ping-pong
-    uint16_t v[2][kSortTile];          // local input index, ping-pong
+    uint32_t k[2][kSortTile];          // packed records, ping-pong (k[0] holds the raw keys first)
     uint16_t rank[kSortTile];          // rank of each element among its warp's equal digits
     uint32_t hist[kPsWarps][256];      // per-warp digit counters -> scatter offsets
     uint32_t scan[kPsWarps + 1];
@@ -96,7 +100,7 @@ template <bool kPredict>
 __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     const float4* __restrict__ st, float4* __restrict__ pst, uint32_t* __restrict__ keys_dbg,
     uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs,
-    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a)
+    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a, uint32_t* __restrict__ kscr)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -174,64 +178,87 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     const uint32_t span = anyin ? cmax - cmin + 1u : 1u, rows = anyin ? rmax - rmin + 1u : 0u;
     const uint32_t kout = rows * span;                      // the remapped key of "outside": after every cell
     __syncthreads();                                        // S.rank reused below
+    const uint32_t range = anyout ? kout : (anyin ? kout - 1u : 0u);
+    const int bits = range ? 32 - __clz(range) : 0;
+    const bool wide = bits > kPkField;                      // rare: two-phase sort, keys in kscr
 #pragma unroll 4
-    for (int i = 0; i < kPsRows; ++i) {                     // remap in place
+    for (int i = 0; i < kPsRows; ++i) {                     // remap in place, pack (field << 12 | p)
         const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
         const uint32_t key = S.k[0][p];
-        if (p < n) S.k[0][p] = key == kOut ? kout : ((key >> 16) - rmin) * span + ((key & 0xFFFFu) - cmin);
+        if (p < n) {
+            const uint32_t rk = key == kOut ? kout : ((key >> 16) - rmin) * span + ((key & 0xFFFFu) - cmin);
+            if (wide) kscr[tb + p] = rk;
+            S.k[0][p] = ((wide ? (rk & ((1u << kPkField) - 1u)) : rk) << kPkIdx) | p;
+        } else {
+            S.k[0][p] = 0xFFFFFFFFu;                         // stays last
+        }
     }
     __syncthreads();
-    const uint32_t kmin = 0u, range = anyout ? kout : (anyin ? kout - 1u : 0u);
-    const int bits = range ? 32 - __clz(range) : 0;
 #ifdef DOG_TIMING
     if (tid == 0) { atomicAdd(&g_phase_ns[30], (unsigned long long)((bits + 7) / 8)); atomicAdd(&g_phase_ns[31], 1ull); }
 #endif
 
-    // ---- stable LSD radix passes (positions >= n carry key 0xFFFFFFFF and stay at the end)
+    // ---- stable LSD radix passes over the packed field (positions >= n stay at the end)
     int cur = 0;
-    for (int shift = 0; shift < bits; shift += 8, cur ^= 1) {
-        for (int i = tid; i < kPsWarps * 256; i += kPsThreads) (&S.hist[0][0])[i] = 0;
-        __syncthreads();
+    auto passes = [&](int nbits) {
+        for (int shift = 0; shift < nbits; shift += 8, cur ^= 1) {
+            for (int i = tid; i < kPsWarps * 256; i += kPsThreads) (&S.hist[0][0])[i] = 0;
+            __syncthreads();
 #pragma unroll 4
-        for (int i = 0; i < kPsRows; ++i) {                  // count + per-warp ranks
-            const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
-            const uint32_t key = S.k[cur][p];
-            const uint32_t dig = p < n ? ((key - kmin) >> shift) & 255u : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, dig);
-            uint32_t prev = 0;
-            if (dig < 256u) prev = S.hist[warp][dig];
-            __syncwarp();
-            if (dig < 256u && (peers & lt) == 0) S.hist[warp][dig] = prev + __popc(peers);
-            __syncwarp();
-            S.rank[p] = (uint16_t)(prev + __popc(peers & lt));
-        }
-        __syncthreads();
-        {   // digit d = tid: offsets over (digit, warp) in that order
-            uint32_t run = 0;
+            for (int i = 0; i < kPsRows; ++i) {              // count + per-warp ranks
+                const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+                const uint32_t w = S.k[cur][p];
+                const uint32_t dig = p < n ? (w >> (kPkIdx + shift)) & 255u : 256u;
+                const uint32_t peers = __match_any_sync(0xffffffffu, dig);
+                uint32_t prev = 0;
+                if (dig < 256u) prev = S.hist[warp][dig];
+                __syncwarp();
+                if (dig < 256u && (peers & lt) == 0) S.hist[warp][dig] = prev + __popc(peers);
+                __syncwarp();
+                S.rank[p] = (uint16_t)(prev + __popc(peers & lt));
+            }
+            __syncthreads();
+            {   // digit d = tid: offsets over (digit, warp) in that order
+                uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < kPsWarps; ++w) { const uint32_t c = S.hist[w][tid]; S.hist[w][tid] = run; run += c; }
-            uint32_t tot;
-            const uint32_t ds = block_excl_scan<uint32_t, kPsWarps>(run, S.scan, tot);
+                for (int w = 0; w < kPsWarps; ++w) { const uint32_t c = S.hist[w][tid]; S.hist[w][tid] = run; run += c; }
+                uint32_t tot;
+                const uint32_t ds = block_excl_scan<uint32_t, kPsWarps>(run, S.scan, tot);
 #pragma unroll
-            for (int w = 0; w < kPsWarps; ++w) S.hist[w][tid] += ds;
-        }
-        __syncthreads();
+                for (int w = 0; w < kPsWarps; ++w) S.hist[w][tid] += ds;
+            }
+            __syncthreads();
 #pragma unroll 4
-        for (int i = 0; i < kPsRows; ++i) {                  // scatter
+            for (int i = 0; i < kPsRows; ++i) {              // scatter
+                const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+                if (p >= n) continue;
+                const uint32_t w = S.k[cur][p];
+                const uint32_t dig = (w >> (kPkIdx + shift)) & 255u;
+                S.k[cur ^ 1][S.hist[warp][dig] + S.rank[p]] = w;
+            }
+            __syncthreads();
+        }
+    };
+    if (!wide) {
+        passes(bits);
+    } else {
+        passes(kPkField);                                   // low 20 bits
+        for (int i = 0; i < kPsRows; ++i) {                 // repack with the high bits
             const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
-            if (p >= n) continue;
-            const uint32_t key = S.k[cur][p];
-            const uint32_t dig = ((key - kmin) >> shift) & 255u;
-            const uint32_t pos = S.hist[warp][dig] + S.rank[p];
-            S.k[cur ^ 1][pos] = key;
-            S.v[cur ^ 1][pos] = shift == 0 ? (uint16_t)p : S.v[cur][p];
+            if (p < n) {
+                const uint32_t w = S.k[cur][p], q = w & ((1u << kPkIdx) - 1u);
+                S.k[cur][p] = ((kscr[tb + q] >> kPkField) << kPkIdx) | q;
+            }
         }
         __syncthreads();
+        passes(bits - kPkField);
     }
     PHASE_MARK(9);
-    const uint32_t* sk = S.k[cur];
-    const uint16_t* sv = S.v[cur];
-    const bool identity = bits == 0;                        // one key: input order is sorted order
+    const uint32_t* sw = S.k[cur];                          // sorted packed records
+    auto skey = [&](uint32_t p) -> uint32_t {               // remapped key of sorted position p
+        const uint32_t w = sw[p];
+        return wide ? kscr[tb + (w & ((1u << kPkIdx) - 1u))] : (w >> kPkIdx);
+    };
 
     // ---- runs of equal keys (warp rows -> heads in position order)
     uint32_t hb[kPsRows];
@@ -239,7 +266,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
 #pragma unroll
     for (int i = 0; i < kPsRows; ++i) {
         const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
-        const bool head = p < n && (p == 0 || sk[p] != sk[p - 1]);
+        const bool head = p < n && (p == 0 || skey(p) != skey(p - 1));
         hb[i] = __ballot_sync(0xffffffffu, head);
         wc += __popc(hb[i]);
     }
@@ -256,7 +283,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     __syncthreads();
     for (uint32_t r = tid; r < nd; r += kPsThreads) {
         const uint32_t f = s_start[r], e = r + 1 < nd ? (uint32_t)s_start[r + 1] : n, c = e - f;
-        const uint32_t kr = sk[f];                         // remapped key -> the context's cell index
+        const uint32_t kr = skey(f);                       // remapped key -> the context's cell index
         const uint32_t key = kr >= kout ? fc.C
                            : (rmin + kr / span - fc.row0) * (uint32_t)fc.W + cmin + kr % span;
         tp.key[tb + r] = key;
@@ -272,7 +299,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     // ---- local permutation (sorted position -> local input index), two per thread-step
     for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
         const uint32_t p = 2 * q;
-        const uint32_t v0 = identity ? p : sv[p], v1 = identity ? p + 1 : sv[p + 1];
+        const uint32_t v0 = sw[p] & ((1u << kPkIdx) - 1u), v1 = sw[p + 1] & ((1u << kPkIdx) - 1u);
         reinterpret_cast<uint32_t*>(lperm + tb)[q] = v0 | (v1 << 16);
     }
     PHASE_MARK(11);

@@ -254,3 +254,21 @@ def test_transforms_exhaustive():
     from paper_1605_02406_b200 import dog
     bad_ln, bad_sqrt, bad_pair, first = dog.check_transforms()
     assert (bad_ln, bad_sqrt, bad_pair) == (0, 0, 0), (bad_ln, bad_sqrt, bad_pair, first)
+
+
+def test_wide_tile_bounding_box():
+    """A sort tile whose particles span more than 2^20 cells of its bounding box (opposite corners of a
+    2048 x 1024 grid): the tile sort takes its two-phase path (full keys in global scratch)."""
+    cfg = I.config("cfg1", width=2048, height=1024, nu=8192, nu_b=512)
+    rng = np.random.default_rng(21)
+    i = np.arange(cfg.nu)
+    corner = (i % 3 == 0)
+    x = np.where(corner, rng.uniform(0, 3, cfg.nu), rng.uniform(2044, 2048, cfg.nu)).astype(np.float32)
+    y = np.where(corner, rng.uniform(0, 3, cfg.nu), rng.uniform(1020, 1024, cfg.nu)).astype(np.float32)
+    st = dict(x=x, y=y, vx=rng.normal(0, 1, cfg.nu).astype(np.float32), vy=rng.normal(0, 1, cfg.nu).astype(np.float32),
+              w_bar=np.float32(1e-4), m_free=np.zeros(cfg.C, np.float32), k=2)
+    frames = [np.zeros((cfg.C, 2), np.float32) for _ in range(3)]
+    for f in frames:
+        f.reshape(cfg.height, cfg.width, 2)[:3, :3, 0] = 0.9
+        f.reshape(cfg.height, cfg.width, 2)[1020:, 2044:, 0] = 0.9
+    run_lockstep(cfg, 3, st=st, frames=frames)
