@@ -90,7 +90,9 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
     return lo;
 }
 
-// ---- k_dopp_runs: gfx of every member of a Doppler cell, summed per run (rg[run slot]) ----------------
+// ---- k_dopp_runs: gfx of every member of a Doppler cell, summed per run (rg[run slot]).  Thread t takes
+//      sorted positions [16t, 16t+16) (one run search, then sequential), sums its run segments and adds
+//      each segment once (integer atomics: order-free).
 __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ lperm, TilePairs tp,
                                                    const float4* __restrict__ pred, DopIn din,
                                                    uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
@@ -98,6 +100,7 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
+    __shared__ __align__(16) uint16_t s_lp[kSortTile];
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_dopp_cells for Doppler tiles
     const uint32_t n = tile_count(sc, par, base);
@@ -105,17 +108,32 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
     for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) { s_first[r] = tp.first[base + r]; rg[base + r] = 0ull; }
+    for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) s_lp[p] = lperm[base + p];
+    if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
     __syncthreads();
-    for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) {
-        const uint32_t j = run_of(s_first, nd, p);
-        const uint32_t key = tp.key[base + j];
-        if (key >= fc.C) continue;
-        const float pa = din.pA[key];
-        if (!(pa > 0.0f)) continue;
-        const float4 X = pred[pbase + lperm[base + p]];
-        const uint32_t gf = doppler_gfx(X.z, X.w, din.dop[key]);
-        if (gf) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)gf);
+    const uint32_t p0 = threadIdx.x * 16u, p1 = min(p0 + 16u, n);
+    if (p0 >= n) return;
+    uint32_t j = run_of(s_first, nd, p0);
+    uint32_t end = s_first[j + 1];
+    uint32_t key = tp.key[base + j];
+    float pa = key < fc.C ? din.pA[key] : 0.0f;
+    float4 d = pa > 0.0f ? din.dop[key] : make_float4(0.f, 0.f, 0.f, 1.f);
+    uint64_t acc = 0;
+    for (uint32_t p = p0; p < p1; ++p) {
+        if (p >= end) {
+            if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+            acc = 0;
+            ++j; end = s_first[j + 1];
+            key = tp.key[base + j];
+            pa = key < fc.C ? din.pA[key] : 0.0f;
+            if (pa > 0.0f) d = din.dop[key];
+        }
+        if (pa > 0.0f) {
+            const float4 X = pred[pbase + s_lp[p]];
+            acc += doppler_gfx(X.z, X.w, d);
+        }
     }
+    if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
 }
 
 // ---- k_dopp_cells: per active Doppler cell, its runs in tile order -> exclusive gfx prefix per run,
