@@ -528,12 +528,17 @@ static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, c
     return DOG_OK;
 }
 
-static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st)
+static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
+                   bool long_list = false)
 {
     CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist,
               ctx->C));
-    CK(launch(k_pair_sort, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all, ctx->sc,
-              fc, (int)(a.k & 1)));
+    if (long_list)   // every cell listed, most without runs (the exact filter)
+        CK(launch(k_pair_sort<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
+                  ctx->sc, fc, (int)(a.k & 1)));
+    else
+        CK(launch(k_pair_sort<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
+                  ctx->sc, fc, (int)(a.k & 1)));
     return DOG_OK;
 }
 
@@ -554,10 +559,14 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     return DOG_OK;
 }
 
-static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullptr)
+static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullptr, bool long_list = false)
 {
-    CK(launch(k_moments, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
-              (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
+    if (long_list)
+        CK(launch(k_moments<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
+                  (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
+    else
+        CK(launch(k_moments<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
+                  (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
     return DOG_OK;
 }
 
@@ -620,7 +629,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (int r = L_list_scan(ctx, nullptr, a, fc, st, obs != nullptr)) return r;
     CK(mark("list_scan"));
     // 5. each cell's runs in tile order -> stable within-cell ranks; global totals (w_bar)
-    if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, obs != nullptr)) return r;
     CK(mark("pairs"));
     // 6. persistent particles: moments + resampling copies; births.  Births depend only on the list and
     // the totals (both final here) and write disjoint output slots, so outside profiling they run on the
@@ -634,7 +643,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     }
     if (int r = L_resample(ctx, a, fc, st)) return r;
     CK(mark("resample"));
-    if (int r = L_moments(ctx, st)) return r;
+    if (int r = L_moments(ctx, st, nullptr, obs != nullptr)) return r;
     CK(mark("moments"));
     if (fork) {
         CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));

@@ -89,6 +89,35 @@ __device__ __forceinline__ T warp_sum(T v)
     return v;
 }
 
+// Calls body(li, m) for every active-list entry with runs (m = np[li] > 0), by groups of G lanes (G a
+// power of two <= 32; the group's lanes all call body for the same entry).  kBatch: each group reads G
+// consecutive entries per step (one coalesced load) and works through those with runs -- for long lists
+// whose entries mostly have none (the exact filter's); otherwise one entry per group per step.
+template <bool kBatch, int G, typename F>
+__device__ __forceinline__ void for_run_entries(const uint32_t* __restrict__ np, uint32_t Lc, F&& body)
+{
+    const int lane = threadIdx.x & 31, gl = lane & (G - 1);
+    const uint32_t gmask = (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u)) << (lane & ~(G - 1));
+    const uint32_t ng = (gridDim.x * blockDim.x) / G;
+    const uint32_t gi = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    if (kBatch) {
+        for (uint32_t q0 = gi * G; q0 < Lc; q0 += ng * G) {
+            const uint32_t mine = q0 + gl < Lc ? np[q0 + gl] : 0u;
+            uint32_t todo = (__ballot_sync(gmask, mine > 0) >> (lane & ~(G - 1))) & (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u));
+            while (todo) {
+                const int b = __ffs(todo) - 1;
+                todo &= todo - 1;
+                body(q0 + (uint32_t)b, __shfl_sync(gmask, mine, (lane & ~(G - 1)) + b));
+            }
+        }
+    } else {
+        for (uint32_t li = gi; li < Lc; li += ng) {
+            const uint32_t m = np[li];
+            if (m) body(li, m);
+        }
+    }
+}
+
 // Warp inclusive scan (add) of T via shuffles.
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v, int lane)

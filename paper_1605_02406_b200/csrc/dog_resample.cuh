@@ -460,6 +460,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
 // the run list in that order) in a fixed summation order.  Groups of 8 lanes take one cell each.
 constexpr int kMoGroup = 8;
 
+template <bool kBatch>
 __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
                                                  const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
                                                  float* __restrict__ cov, const DevScalars* __restrict__ sc,
@@ -470,10 +471,7 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
     const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
     const uint32_t Lc = sc->Lc;
     const float w_pred = sc->w_pred;
-    const uint32_t ng = (gridDim.x * blockDim.x) / kMoGroup;
-    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) / kMoGroup; li < Lc; li += ng) {
-        const uint32_t m = L.np[li];
-        if (m == 0) continue;
+    for_run_entries<kBatch, kMoGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const uint32_t* pl = plist + L.ps[li];
         double s5[5] = {0, 0, 0, 0, 0};
         for (uint32_t q = gl; q < m; q += kMoGroup) {
@@ -493,7 +491,7 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
             else
                 finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
         }
-    }
+    });
 }
 
 // Split of a cell's birth slots / born mass into the associated and unassociated sets (NEXT-1, A-36):

@@ -434,6 +434,7 @@ constexpr int kPsGroup = 8, kPsBuf = 128;
 // Block 0 also publishes the cycle's global totals: W over all shards, the joint prefix of the shards
 // below, w_bar = W 2^-40 / nu (Eq. 57), and -- band contexts -- the next cycle's own particles: the
 // global outputs [F(P'), F(P' + W_local)) (A-24).
+template <bool kBatch>
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
                                                    uint32_t* __restrict__ ptmp, const uint64_t* __restrict__ W_all,
                                                    DevScalars* __restrict__ sc, FilterConst fc, int par)
@@ -443,7 +444,6 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     const int lane = threadIdx.x & 31, gl = lane & (kPsGroup - 1), grp = threadIdx.x / kPsGroup;
     const uint32_t gmask = 0xFFu << (lane & ~(kPsGroup - 1));
     const uint32_t Lc = sc->Lc;
-    const uint32_t ng = (gridDim.x * blockDim.x) / kPsGroup;
     uint64_t Ppre = 0, Wtot = sc->W;
     if (W_all) {
         Wtot = 0;
@@ -465,9 +465,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             sc->n_own[par ^ 1] = f1 - f0;
         }
     }
-    for (uint32_t li = (blockIdx.x * blockDim.x + threadIdx.x) / kPsGroup; li < Lc; li += ng) {
-        const uint32_t m = L.np[li];
-        if (m == 0) continue;
+    for_run_entries<kBatch, kPsGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         RunInfo ri;
         ri.P = Ppre + L.P[li];
         ri.bp = L.bp[li];
@@ -478,7 +476,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         uint32_t* pl = plist + L.ps[li];
         if (m == 1) {                                 // (tile << 12 | run) is the run's slot index
             if (gl == 0) tp.run[pl[0]] = ri;
-            continue;
+            return;
         }
         const bool sm = m <= (uint32_t)kPsBuf;
         uint32_t* src = sm ? s_buf[grp][0] : pl;
@@ -519,7 +517,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             carry += __shfl_sync(gmask, incl, kPsGroup - 1, kPsGroup);
         }
         __syncwarp(gmask);
-    }
+    });
 }
 
 }  // namespace dog
