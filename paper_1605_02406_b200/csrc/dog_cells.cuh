@@ -198,6 +198,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         float mf[kCellItems];
         float2 z[kCellItems];
         float4 ob[kCellItems];
+        uint32_t npf[kCellItems];            // kExact: every cell is active -> run counts loaded up front
 #pragma unroll
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
@@ -205,6 +206,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
             n[i] = valid ? counts[c] : 0u;
             if (kExact) {
                 ob[i] = valid ? obs[c] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                npf[i] = valid ? npairs[c] : 0u;
             } else {
                 mf[i] = valid ? m_free[c] : 0.0f;
                 z[i] = valid ? meas[c] : make_float2(0.0f, 0.0f);
@@ -256,18 +258,19 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         for (int i = 0; i < kCellItems; ++i) {
             if ((abal[i] >> lane) & 1u) {               // active cell: same inputs (untouched), same arithmetic
                 const uint32_t c = base + i * kCellThreads + tid;
-                const CellOut o = kExact ? cell_math_exact(__ldcg(counts + c), obs[c], w_pred, fc)
+                // exact filter: the inputs are still in registers (no reload: every cell comes here)
+                const CellOut o = kExact ? cell_math_exact(n[i], ob[i], w_pred, fc)
                                          : cell_math(__ldcg(counts + c), __ldcg(m_free + c), meas[c], w_pred, alpha, fc);
                 if (!kExact) m_free[c] = o.mF;
                 if (o.n) counts[c] = 0u;                // ready for the next cycle's k_predict_sort
                 const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
                 L.c[li] = c; L.n[li] = o.n; L.Rp[li] = o.Rp; L.Rb[li] = o.Rb; L.rho_p[li] = o.rp;
                 uint32_t npc = 0;
-                if (o.n) { npc = npairs[c]; npairs[c] = 0u; }
+                if (o.n) { npc = kExact ? npf[i] : npairs[c]; npairs[c] = 0u; }
                 L.np[li] = npc;
                 A_loc += o.Rb;
                 N_loc += o.n;
-                P_loc += npc;
+                if (kExact) P_loc += npc;                   // (the grid-wide list scan's chunk totals)
             }
         }
         __syncthreads();
@@ -275,7 +278,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     // block totals (integers: order-independent)
     A_loc = warp_sum(A_loc);
     N_loc = warp_sum(N_loc);
-    P_loc = warp_sum(P_loc);
+    if (kExact) P_loc = warp_sum(P_loc);
     bad_loc = warp_sum(bad_loc);
     __shared__ uint32_t s_P[8];
     if (lane == 0) { s_A[warp] = A_loc; s_N[warp] = N_loc; s_bad[warp] = bad_loc; s_P[warp] = P_loc; }
