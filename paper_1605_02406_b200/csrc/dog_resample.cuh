@@ -203,7 +203,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;     // this tile's slot in the per-tile arrays
     const RsConst rc = make_rsconst(sc, fc.nu);
     const uint32_t n_lo = sc->n_lo, n_loc = n_lo + sc->n_own[par] + sc->n_hi;
@@ -352,27 +352,33 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
         for (int i = 0; i < kRtWinItems / 8; ++i) reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         bool amb = false;
-#pragma unroll 2
-        for (int it = 0; it < kRtItems; ++it) {   // members with copies mark their first output in the window
-            const uint32_t p = it * kRtThreads + tid;
-            const bool inb = p < n;
-            const uint32_t j = inb ? S.runof[p] : srun;
-            const bool live = inb && j != srun;
-            uint32_t F0 = 0, F1 = 0, D = 0, e = 0;
-            double y1 = 0.0;
-            if (live) {
-                const RunF& x = runf(j);
+        if (p0 < n) {   // members with copies mark their first output in the window: thread-contiguous
+                        // positions, the run's F parameters held in registers, F(Q_{r+1}) reused as the next
+                        // member's F(Q_r)
+            const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
+            uint32_t j = S.runof[p0], end = S.first[j + 1];
+            RunF x{};
+            if (j != srun) x = runf(j);
+            bool have = false;
+            uint32_t Fc = 0;
+            for (uint32_t p = p0; p < pend; ++p) {
+                if (p >= end) {
+                    j = S.runof[p]; end = S.first[j + 1];
+                    if (j != srun) x = runf(j);
+                    have = false;
+                }
+                if (j == srun) continue;
                 const uint32_t mr = x.pre + (p - x.first);
-                const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), x.d2, x.yR);
-                y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), x.d2, x.yR);
-                F0 = fast_ceil(y, rc.nu, amb);
-                D = x.D;
-                e = x.end;
-            }
-            const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);   // the next position's F(Q)
-            if (live) {
-                F1 = (lane < 31 && p + 1 < e) ? Fn : fast_ceil(y1, rc.nu, amb);
-                const uint32_t C0 = F0 - D, C1 = F1 - D;
+                uint32_t F0 = Fc;
+                if (!have) {
+                    const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), x.d2, x.yR);
+                    F0 = fast_ceil(y, rc.nu, amb);
+                }
+                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), x.d2, x.yR);
+                const uint32_t F1 = fast_ceil(y1, rc.nu, amb);
+                Fc = F1;
+                have = true;
+                const uint32_t C0 = F0 - x.D, C1 = F1 - x.D;
                 if (C1 > C0 && C1 > w0 && C0 < w0 + kRtWin) os[max(C0, w0) - w0] = (uint16_t)(p + 1u);
             }
         }
