@@ -272,3 +272,23 @@ def test_wide_tile_bounding_box():
         f.reshape(cfg.height, cfg.width, 2)[:3, :3, 0] = 0.9
         f.reshape(cfg.height, cfg.width, 2)[1020:, 2044:, 0] = 0.9
     run_lockstep(cfg, 3, st=st, frames=frames)
+
+
+def test_maximum_width_grid():
+    """The widest grid the ABI accepts (65535 columns; the packed (row, col) key uses 16 bits each) with
+    particles spread along it: keys, sort (wide bounding boxes) and the whole cycle bit-exact."""
+    cfg = I.config("cfg1", width=65535, height=3, nu=20_000, nu_b=1_000)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, cfg.width, cfg.nu).astype(np.float32)
+    y = rng.uniform(0, cfg.height, cfg.nu).astype(np.float32)
+    x[:50] = np.float32(65534.999)                          # the last column
+    st = dict(x=x, y=y, vx=rng.normal(0, 3, cfg.nu).astype(np.float32), vy=rng.normal(0, 1, cfg.nu).astype(np.float32),
+              w_bar=np.float32(2e-5), m_free=np.zeros(cfg.C, np.float32), k=1)
+    frames = []
+    for k in range(2):
+        f = np.zeros((cfg.C, 2), np.float32)
+        hit = rng.random(cfg.C) < 0.05
+        f[hit, 0] = 0.95
+        f[~hit, 1] = 0.3
+        frames.append(f)
+    run_lockstep(cfg, 2, st=st, frames=frames)
