@@ -1,6 +1,6 @@
 // dog_cells.cuh -- per-cell stages of the cycle (Alg. 3, Alg. 5 slot allocation, Alg. 7 joint CDF).
 //
-// k_cells: one pass over the grid.  For every cell: n_c (from k_tilesort's counts), S_c = n_c w_pred
+// k_cells: one pass over the grid.  For every cell: n_c (from k_predict_sort's counts), S_c = n_c w_pred
 // (Eq. 61, exact), m_p = min(S_c, occ_max) (Eq. 17), m_Fp = min(alpha m_F, 1 - m_p) (Eq. 62),
 // Dempster update (Eq. 63), birth split (Eqs. 67-68), fixed-point masses (A-23) and the readouts.
 // Cells holding particles or receiving born mass ("active" cells, typically ~1 % of the grid) are

@@ -5,9 +5,10 @@
 // stable rank among the particles of that cell (A-6: ties by input index).  Because the input is the
 // previous resampling output -- already ordered by source cell -- and particles move a few cells per
 // step, every 4096-particle tile holds few distinct cells.  So:
-//   k_tilesort  : per tile, a stable LSD radix sort of the tile's keys in shared memory (only the
-//                 digits the tile's key range needs), runs of equal keys -> "pairs" (tile, cell, count,
-//                 first local position), the local permutation, and per-cell counts n_c / pair counts.
+//   k_predict_sort : per tile, predict (Alg. 1) fused with a stable LSD radix sort of the tile's keys in
+//                 shared memory (only the digits the tile's key range needs), runs of equal keys ->
+//                 "pairs" (tile, cell, count, first local position), the local permutation, and per-cell
+//                 counts n_c / pair counts.
 //   k_pair_fill : each pair appends itself to its cell's pair list (position by atomic, unordered).
 //   k_pair_sort : per active cell, its pair list sorted by tile (keys are unique: one run per tile per
 //                 cell) and the exclusive prefix of the counts = the rank of each run's first particle
