@@ -49,7 +49,7 @@ extern "C" {
 typedef struct dog_ctx dog_ctx;   /* opaque; created and owned by the library */
 
 typedef struct {
-    int32_t width, height;        /* cells; C = width*height, 1 <= C < 2^31 - 1                */
+    int32_t width, height;        /* cells; C = width*height, 1 <= C < 2^24 (see dog_create)   */
     float   cell_size;            /* metres per cell, > 0 (Table I: 0.1 m)             */
 } dog_grid;
 
