@@ -112,10 +112,14 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
     }
 }
 
-#ifndef RT_MINB
-#define RT_MINB 4
+#ifndef RT_THREADS
+#define RT_THREADS 256
 #endif
-constexpr int kRtThreads = 256, kRtItems = kSortTile / kRtThreads;   // 16 sorted positions per thread
+#ifndef RT_MINB
+#define RT_MINB (1024 / RT_THREADS)
+#endif
+constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // sorted positions per thread
+static_assert(kRtItems % 8 == 0, "phase B works in batches of 8 positions");
 constexpr int kRtRunCache = 64;                                       // runs whose RunF sits in smem (rest: global)
 constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
 constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 window entries per thread
@@ -227,10 +231,12 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
     {
         uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
-        if (p0 < n) { const uint4* lp4 = reinterpret_cast<const uint4*>(lperm + base + p0); a = lp4[0]; b = lp4[1]; }
-        if (p0 < nd) { const uint4* f4 = reinterpret_cast<const uint4*>(tp.first + base + p0); c = f4[0]; d = f4[1]; }
-        if (p0 < n) { reinterpret_cast<uint4*>(S.lp + p0)[0] = a; reinterpret_cast<uint4*>(S.lp + p0)[1] = b; }
-        if (p0 < nd) { reinterpret_cast<uint4*>(S.first + p0)[0] = c; reinterpret_cast<uint4*>(S.first + p0)[1] = d; }
+#pragma unroll
+        for (int h = 0; h < kRtItems / 8; ++h) {
+            if (p0 < n) { a = reinterpret_cast<const uint4*>(lperm + base + p0)[h]; reinterpret_cast<uint4*>(S.lp + p0)[h] = a; }
+            if (p0 < nd) { c = reinterpret_cast<const uint4*>(tp.first + base + p0)[h]; reinterpret_cast<uint4*>(S.first + p0)[h] = c; }
+        }
+        (void)b; (void)d;
         if (tid == 0) S.slow = 0u;
         if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
@@ -260,7 +266,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
             first_seg = false;
         };
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {                       // two batches of 8 positions
+        for (int h = 0; h < kRtItems / 8; ++h) {            // batches of 8 positions
             uint32_t src[8], rpk[4];
             {
                 const uint4 a = reinterpret_cast<const uint4*>(S.lp + p0)[h];
