@@ -483,6 +483,17 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
     const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
     const uint32_t Lc = sc->Lc;
     const float w_pred = sc->w_pred;
+    auto finalize = [&](uint32_t li, const double (&s5)[5]) {
+        if (GSd && GSd[li] > 0)    // Doppler cell (NEXT-1): weighted sums
+            finalize_cell_dop(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.Rp[li], mean, cov);
+        else
+            finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
+    };
+    auto single = [&](uint32_t li) {                       // one run: its sums are the cell's
+        const double* ps = ppart[plist[L.ps[li]]].s;
+        const double s5[5] = {ps[0], ps[1], ps[2], ps[3], ps[4]};
+        finalize(li, s5);
+    };
     for_run_entries<kBatch, kMoGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const uint32_t* pl = plist + L.ps[li];
         double s5[5] = {0, 0, 0, 0, 0};
@@ -497,13 +508,8 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
 #pragma unroll
                 for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(gmask, s5[i], d, kMoGroup);
         }
-        if (gl == 0) {
-            if (GSd && GSd[li] > 0)    // Doppler cell (NEXT-1): weighted sums
-                finalize_cell_dop(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.Rp[li], mean, cov);
-            else
-                finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
-        }
-    });
+        if (gl == 0) finalize(li, s5);
+    }, single);
 }
 
 // Split of a cell's birth slots / born mass into the associated and unassociated sets (NEXT-1, A-36):

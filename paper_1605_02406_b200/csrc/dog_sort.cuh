@@ -466,7 +466,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             sc->n_own[par ^ 1] = f1 - f0;
         }
     }
-    for_run_entries<kBatch, kPsGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
+    auto run_info = [&](uint32_t li) {
         RunInfo ri;
         ri.P = Ppre + L.P[li];
         ri.bp = L.bp[li];
@@ -474,6 +474,11 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         ri.pre = 0u;
         ri.jbase = L.start[li] + L.sb[li];
         ri.li = li;
+        return ri;
+    };
+    auto single = [&](uint32_t li) { tp.run[plist[L.ps[li]]] = run_info(li); };   // one run: pre = 0
+    for_run_entries<kBatch, kPsGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
+        const RunInfo ri = run_info(li);
         uint32_t* pl = plist + L.ps[li];
         if (m == 1) {                                 // (tile << 12 | run) is the run's slot index
             if (gl == 0) tp.run[pl[0]] = ri;
@@ -518,7 +523,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             carry += __shfl_sync(gmask, incl, kPsGroup - 1, kPsGroup);
         }
         __syncwarp(gmask);
-    });
+    }, single);
 }
 
 }  // namespace dog
