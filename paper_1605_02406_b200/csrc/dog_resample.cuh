@@ -121,6 +121,7 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // sorted positions per thread
 static_assert(kRtItems % 8 == 0, "phase B works in batches of 8 positions");
 constexpr int kRtRunCache = 64;                                       // runs whose RunF sits in smem (rest: global)
+constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
 constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
 constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 window entries per thread
 
@@ -145,6 +146,8 @@ struct RtSmem {   // dynamic shared memory of k_resample_tiles (~47 KB: three bl
     } u;
     uint32_t scan[kRtThreads / 32 + 1];
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
+    uint32_t nlong;                    // runs spanning more than kRtShortSpan threads (phase R)
+    uint16_t longr[32];
     uint32_t slow;                     // an estimate was too close to an integer: exact marks needed
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
@@ -237,7 +240,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
             if (p0 < nd) { c = reinterpret_cast<const uint4*>(tp.first + base + p0)[h]; reinterpret_cast<uint4*>(S.first + p0)[h] = c; }
         }
         (void)b; (void)d;
-        if (tid == 0) S.slow = 0u;
+        if (tid == 0) { S.slow = 0u; S.nlong = 0u; }
         if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     }
     __syncthreads();
@@ -312,7 +315,12 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
         if (live) {
             const uint32_t f = S.first[r], e = S.first[r + 1];
             const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
-            if (tf != tl) {                                 // segments over threads tf..tl, in thread order
+            bool by_warp = false;
+            if (tl - tf > kRtShortSpan) {                   // long run: combined by a warp after this loop
+                const uint32_t k = atomicAdd(&S.nlong, 1u);
+                if (k < 32u) { S.longr[k] = (uint16_t)r; by_warp = true; }
+            }
+            if (tf != tl && !by_warp) {                     // segments over threads tf..tl, in thread order
                 const MomPartial& m0 = (f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf];
                 double s5[5];
 #pragma unroll
@@ -348,6 +356,33 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
         carry += tot;
     }
     __syncthreads();
+    {   // long runs: their thread partials summed by one warp each (fixed lane tree: deterministic)
+        const uint32_t nlong = min(S.nlong, 32u);
+        if (nlong > 0u) {
+            const int warp = tid >> 5, lane = tid & 31;
+            for (uint32_t k = warp; k < nlong; k += kRtThreads / 32) {
+                const uint32_t r = S.longr[k];
+                const uint32_t f = S.first[r], e = S.first[r + 1];
+                const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
+                double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+                for (uint32_t u = tf + 1 + lane; u <= tl; u += 32)
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) s5[i] += S.u.m.pa[u].s[i];
+#pragma unroll
+                for (int d = 16; d; d >>= 1)
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], d);
+                if (lane == 0) {
+                    const MomPartial& m0 = (f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf];
+                    MomPartial mp;
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) mp.s[i] = m0.s[i] + s5[i];
+                    ppart[base + r] = mp;
+                }
+            }
+            __syncthreads();                                // phase C reuses the partials' memory
+        }
+    }
     const uint32_t Ot = carry;
     PHASE_MARK(2);
     // ---- phase C: windows of the compact output space
