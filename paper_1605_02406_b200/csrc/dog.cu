@@ -529,16 +529,16 @@ static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, c
 }
 
 static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                   bool long_list = false)
+                   bool long_list = false, DopPS dp = DopPS{nullptr, nullptr, nullptr, nullptr})
 {
     CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist,
               ctx->C));
     if (long_list)   // every cell listed, most without runs (the exact filter)
         CK(launch(k_pair_sort<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
-                  ctx->sc, fc, (int)(a.k & 1)));
+                  ctx->sc, fc, (int)(a.k & 1), dp));
     else
         CK(launch(k_pair_sort<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
-                  ctx->sc, fc, (int)(a.k & 1)));
+                  ctx->sc, fc, (int)(a.k & 1), dp));
     return DOG_OK;
 }
 
@@ -680,13 +680,28 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     const DopIn din{(const float4*)doppler, p_assoc};
     const int par = (int)(a.k & 1);
     if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
+    // the per-run likelihood sums need only the tile sort: on the side stream beside k_cells and the
+    // list scan (they touch nothing it reads or writes), joined before the pair sort consumes them
+    const bool fork = ctx->side != nullptr;
+    cudaStream_t ds = fork ? ctx->side : st;
+    if (fork) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    }
+    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, ds, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
+              din, ctx->d_rg, ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
+    if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if (int r = L_cells(ctx, meas, a, fc, st)) return r;
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
-    if (int r = L_pairs(ctx, nullptr, a, fc, st)) return r;
-    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
-              din, ctx->d_rg, ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
-    CK(launch(k_dopp_cells, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist, din, ctx->d_rg,
-              ctx->d_GS, ctx->d_tflag, (const DevScalars*)ctx->sc));
+    if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    // the pair sort also turns the run sums into in-cell prefixes, the cell totals GS and the tile flags
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, false, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag})) return r;
+    if (fork) {   // births beside the resampling (disjoint output slots), as in dog_step
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        if (int r = L_births(ctx, a, fc, ctx->side, &din)) return r;
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    }
     // tiles without a Doppler cell's members: the closed-form kernel; the others: per-member weights
     if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
     NextState ns{ctx->st, nullptr};
@@ -694,7 +709,8 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
                  (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
                  (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
     if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
-    if (int r = L_births(ctx, a, fc, st, &din)) return r;
+    if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    else if (int r = L_births(ctx, a, fc, st, &din)) return r;
     ctx->k += 1;
     return DOG_OK;
 }

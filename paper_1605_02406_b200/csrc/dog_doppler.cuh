@@ -10,7 +10,8 @@
 // Weights are no longer uniform within a cell, so the closed-form per-run resampling of
 // k_resample_tiles does not apply; this path uses
 //   k_dopp_runs    per tile: gfx of every member, summed per run (integer atomics: order-free)
-//   k_dopp_cells   per active cell: the runs' gfx sums in tile order -> exclusive prefixes, cell total GS
+//   k_pair_sort    (its Doppler branch) per active cell: the runs' gfx sums in tile order -> exclusive
+//                  prefixes, cell total GS, tile flags
 //   k_resample_dopp per tile holding a Doppler cell's members: block prefix of gfx -> GS_j of every
 //                  member -> Q_j, Q_{j+1} -> F(.) -> copies; weighted velocity sums per run for the
 //                  moments.  Every other tile goes through k_resample_tiles (closed form, even split).
@@ -102,7 +103,7 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
     __shared__ uint16_t s_first[kSortTile + 1];
     __shared__ __align__(16) uint16_t s_lp[kSortTile];
     const uint32_t t = blockIdx.x, base = t * kSortTile;
-    if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_dopp_cells for Doppler tiles
+    if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_pair_sort for Doppler tiles
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
@@ -134,34 +135,6 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
         }
     }
     if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
-}
-
-// ---- k_dopp_cells: per active Doppler cell, its runs in tile order -> exclusive gfx prefix per run,
-//      cell total GS[li] (0: not a Doppler cell, or no member compatible: even split, A-35) ---------------
-__global__ __launch_bounds__(256) void k_dopp_cells(CellList L, const uint32_t* __restrict__ plist, DopIn din,
-                                                    uint64_t* __restrict__ rg, uint64_t* __restrict__ GS,
-                                                    uint8_t* __restrict__ tflag, const DevScalars* __restrict__ sc)
-{
-    PDL_ENTER();
-    const uint32_t Lc = sc->Lc;
-    for (uint32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < Lc; li += gridDim.x * blockDim.x) {
-        const uint32_t m = L.np[li];
-        uint64_t acc = 0;
-        if (m > 0 && din.pA[L.c[li]] > 0.0f) {
-            const uint32_t* pl = plist + L.ps[li];
-            for (uint32_t a = 0; a < m; ++a) {
-                const uint32_t v = pl[a];
-                const uint64_t s = rg[v];
-                rg[v] = acc;
-                acc += s;
-            }
-        }
-        GS[li] = acc;
-        if (acc > 0) {                                       // the tiles holding this cell's members
-            const uint32_t* pl = plist + L.ps[li];
-            for (uint32_t a = 0; a < m; ++a) tflag[pl[a] >> 12] = 1;
-        }
-    }
 }
 
 // ---- k_resample_dopp: persistent members with per-member weights ---------------------------------------

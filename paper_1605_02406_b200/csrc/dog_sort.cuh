@@ -435,10 +435,20 @@ constexpr int kPsGroup = 8, kPsBuf = 128;
 // Block 0 also publishes the cycle's global totals: W over all shards, the joint prefix of the shards
 // below, w_bar = W 2^-40 / nu (Eq. 57), and -- band contexts -- the next cycle's own particles: the
 // global outputs [F(P'), F(P' + W_local)) (A-24).
+// Doppler branch (NEXT-1; pA == nullptr otherwise): the per-run likelihood sums rg (k_dopp_runs) of a
+// Doppler cell become, in the same tile-order walk, their exclusive prefixes within the cell; GS[li] =
+// the cell's total (0: no Doppler weighting, A-35) and tflag marks the tiles holding such a cell's runs.
+struct DopPS {
+    const float* pA;
+    uint64_t* rg;
+    uint64_t* GS;
+    uint8_t* tflag;
+};
+
 template <bool kBatch>
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
                                                    uint32_t* __restrict__ ptmp, const uint64_t* __restrict__ W_all,
-                                                   DevScalars* __restrict__ sc, FilterConst fc, int par)
+                                                   DevScalars* __restrict__ sc, FilterConst fc, int par, DopPS dp)
 {
     PDL_ENTER();
     __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
@@ -476,14 +486,26 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         ri.li = li;
         return ri;
     };
-    auto single = [&](uint32_t li) { tp.run[plist[L.ps[li]]] = run_info(li); };   // one run: pre = 0
+    auto dop_single = [&](uint32_t li, uint32_t v) {     // a one-run cell: its prefix is 0, its total the run's
+        if (!dp.pA) return;
+        const uint64_t gs = dp.pA[L.c[li]] > 0.0f ? dp.rg[v] : 0ull;
+        dp.rg[v] = 0ull;
+        dp.GS[li] = gs;
+        if (gs) dp.tflag[v >> 12] = 1;
+    };
+    auto single = [&](uint32_t li) {                      // one run: pre = 0
+        const uint32_t v = plist[L.ps[li]];
+        tp.run[v] = run_info(li);
+        dop_single(li, v);
+    };
     for_run_entries<kBatch, kPsGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const RunInfo ri = run_info(li);
         uint32_t* pl = plist + L.ps[li];
         if (m == 1) {                                 // (tile << 12 | run) is the run's slot index
-            if (gl == 0) tp.run[pl[0]] = ri;
+            if (gl == 0) { tp.run[pl[0]] = ri; dop_single(li, pl[0]); }
             return;
         }
+        const bool dcell = dp.pA && dp.pA[L.c[li]] > 0.0f;
         const bool sm = m <= (uint32_t)kPsBuf;
         uint32_t* src = sm ? s_buf[grp][0] : pl;
         uint32_t* tmp = sm ? s_buf[grp][1] : ptmp + L.ps[li];
@@ -499,28 +521,40 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             tmp[rank] = va;
         }
         __syncwarp(gmask);
-        // exclusive prefix of counts in tile order
+        // exclusive prefix of counts (and, Doppler cells, of the runs' likelihood sums) in tile order
         uint32_t carry = 0;
+        uint64_t gcarry = 0;
         for (uint32_t a0 = 0; a0 < mr; a0 += kPsGroup) {
             const uint32_t a = a0 + gl;
             uint32_t v = 0, c = 0;
+            uint64_t g = 0;
             if (a < m) {
                 v = tmp[a];
                 c = (uint32_t)tp.cnt[v] + 1u;
+                if (dcell) g = dp.rg[v];
             }
             uint32_t incl = c;
+            uint64_t gincl = g;
 #pragma unroll
             for (int d = 1; d < kPsGroup; d <<= 1) {
                 const uint32_t o = __shfl_up_sync(gmask, incl, d, kPsGroup);
-                if (gl >= d) incl += o;
+                const uint64_t go = __shfl_up_sync(gmask, gincl, d, kPsGroup);
+                if (gl >= d) { incl += o; gincl += go; }
             }
             if (a < m) {
                 RunInfo r2 = ri;
                 r2.pre = carry + incl - c;
                 tp.run[v] = r2;
                 pl[a] = v;                   // the cell's list, now in tile order
+                if (dp.pA) dp.rg[v] = gcarry + gincl - g;
             }
             carry += __shfl_sync(gmask, incl, kPsGroup - 1, kPsGroup);
+            gcarry += __shfl_sync(gmask, gincl, kPsGroup - 1, kPsGroup);
+        }
+        if (dp.pA) {
+            if (gl == 0) dp.GS[li] = gcarry;
+            if (gcarry)
+                for (uint32_t a = gl; a < m; a += kPsGroup) dp.tflag[pl[a] >> 12] = 1;
         }
         __syncwarp(gmask);
     }, single);

@@ -116,3 +116,9 @@ def test_doppler_all_zero_pA_is_the_plain_cycle():
             bits(sa[key], sb[key], f"cycle {k} {key}")
         ra, rb = a.read_cells(), b.read_cells()
         close(ra["mean"].cpu().numpy(), rb["mean"].cpu().numpy(), 1e-6, 1e-9, "mean")
+
+
+def test_doppler_without_side_stream(monkeypatch):
+    """The same cycles with every kernel on the caller's stream (DOG_NO_FORK: no side stream)."""
+    monkeypatch.setenv("DOG_NO_FORK", "1")
+    run(I.CONFIGS["cfg1"], 4, frac=0.7)
