@@ -101,6 +101,7 @@ struct dog_ctx {
     uint64_t* d_rs = nullptr;                     // per run slot: block prefix at the run's first member
     uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
     uint8_t* d_tflag = nullptr;                   // per sort tile: holds members of a Doppler cell
+    uint32_t* d_gfx = nullptr;                    // per sorted position: fixed-point Doppler likelihood
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
@@ -468,6 +469,7 @@ int dog_destroy(dog_ctx* ctx)
     if (ctx->d_rs) cudaFree(ctx->d_rs);
     if (ctx->d_GS) cudaFree(ctx->d_GS);
     if (ctx->d_tflag) cudaFree(ctx->d_tflag);
+    if (ctx->d_gfx) cudaFree(ctx->d_gfx);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     free_all(ctx);
@@ -672,7 +674,8 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     cudaStream_t st = (cudaStream_t)stream;
     if (!ctx->d_rg) {
         if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
-            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess)
+            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess ||
+            cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess)
             return DOG_E_NOMEM;
     }
     const StepArgs a = step_args(ctx, dt);
@@ -689,7 +692,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     }
     CK(launch(k_dopp_runs, ctx->tiles, 256, 0, ds, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
-              din, ctx->d_rg, ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
+              din, ctx->d_rg, ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
     if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if (int r = L_cells(ctx, meas, a, fc, st)) return r;
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
@@ -707,7 +710,8 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     NextState ns{ctx->st, nullptr};
     CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
                  (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
-                 (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const DevScalars*)ctx->sc, fc, par));
+                 (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const uint32_t*)ctx->d_gfx,
+                 (const DevScalars*)ctx->sc, fc, par));
     if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
     if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     else if (int r = L_births(ctx, a, fc, st, &din)) return r;

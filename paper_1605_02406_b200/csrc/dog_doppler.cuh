@@ -97,7 +97,8 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
 __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ lperm, TilePairs tp,
                                                    const float4* __restrict__ pred, DopIn din,
                                                    uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
-                                                   const DevScalars* __restrict__ sc, FilterConst fc, int par)
+                                                   uint32_t* __restrict__ gfx_out, const DevScalars* __restrict__ sc,
+                                                   FilterConst fc, int par)
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
@@ -129,10 +130,13 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
             pa = key < fc.C ? din.pA[key] : 0.0f;
             if (pa > 0.0f) d = din.dop[key];
         }
+        uint32_t gf = 0u;
         if (pa > 0.0f) {
             const float4 X = pred[pbase + s_lp[p]];
-            acc += doppler_gfx(X.z, X.w, d);
+            gf = doppler_gfx(X.z, X.w, d);
+            acc += gf;
         }
+        gfx_out[base + p] = gf;                              // per sorted position, for k_resample_dopp
     }
     if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
 }
@@ -153,6 +157,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
                                                        MomPartial* __restrict__ ppart, DopIn din,
                                                        const uint64_t* __restrict__ rg, uint64_t* __restrict__ rs,
                                                        const uint64_t* __restrict__ GS, const uint8_t* __restrict__ tflag,
+                                                       const uint32_t* __restrict__ gfx_in,
                                                        const DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
@@ -178,35 +183,21 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
     const uint32_t p0 = tid * kRdItems;
     const uint32_t p1 = min(p0 + kRdItems, n);
 
-    // pass 1: gfx of the owned positions, thread total, block prefix; run starts -> rs[run]
+    // pass 1: gfx of the owned positions (k_dopp_runs wrote them in sorted order), thread total, block
+    // prefix; run starts -> rs[run]
     uint32_t gf[kRdItems];
     uint64_t tsum = 0;
-    {
-        uint32_t j = p0 < n ? run_of(S.first, nd, p0) : 0u;
-        uint32_t key = 0, end = 0;
-        float pa = 0.0f;
-        float4 d = make_float4(0.f, 0.f, 0.f, 1.f);
-        bool first_run = true;
 #pragma unroll
-        for (int u = 0; u < kRdItems; ++u) {
-            const uint32_t p = p0 + u;
-            gf[u] = 0u;
-            if (p >= p1) continue;
-            if (first_run || p >= end) {
-                if (!first_run) ++j;
-                first_run = false;
-                end = S.first[j + 1];
-                key = tp.key[base + j];
-                pa = key < fc.C ? din.pA[key] : 0.0f;
-                if (pa > 0.0f) d = din.dop[key];
-            }
-            if (pa > 0.0f) {
-                const float4 X = pred[pbase + S.lp[p]];
-                gf[u] = doppler_gfx(X.z, X.w, d);
-            }
-            tsum += gf[u];
-        }
+    for (int h = 0; h < kRdItems / 4; ++h) {
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (p0 + 4 * h < n) w = reinterpret_cast<const uint4*>(gfx_in + base + p0)[h];   // past n: masked below
+        gf[4 * h] = p0 + 4 * h < p1 ? w.x : 0u;
+        gf[4 * h + 1] = p0 + 4 * h + 1 < p1 ? w.y : 0u;
+        gf[4 * h + 2] = p0 + 4 * h + 2 < p1 ? w.z : 0u;
+        gf[4 * h + 3] = p0 + 4 * h + 3 < p1 ? w.w : 0u;
     }
+#pragma unroll
+    for (int u = 0; u < kRdItems; ++u) tsum += gf[u];
     uint64_t tot;
     const uint64_t tb = block_excl_scan<uint64_t, 8>(tsum, S.scan, tot);
     {
