@@ -284,23 +284,29 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
         flush();
     }
     __syncthreads();
-    // spanning runs: segments over threads tf..tl combined in thread order -> ppart
-    for (uint32_t r = tid; r < nd; r += 256) {
+    // spanning runs: the segments over threads tf..tl, combined by one warp per run (fixed lane tree:
+    // deterministic) -> ppart
+    const int warp = tid >> 5, lane = tid & 31;
+    for (uint32_t r = warp; r < nd; r += 8) {
         const uint32_t f = S.first[r], e = S.first[r + 1];
         if (tp.key[base + r] >= fc.C) continue;
         const uint32_t tf = f / kRdItems, tl = (e - 1) / kRdItems;
         if (tf == tl) continue;
-        const MomPartial& m0 = (f > tf * kRdItems) ? S.pb[tf] : S.pa[tf];
-        double s5[5];
-#pragma unroll
-        for (int i = 0; i < 5; ++i) s5[i] = m0.s[i];
-        for (uint32_t u = tf + 1; u <= tl; ++u)
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (uint32_t u = tf + 1 + lane; u <= tl; u += 32)
 #pragma unroll
             for (int i = 0; i < 5; ++i) s5[i] += S.pa[u].s[i];
-        MomPartial mp;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
-        ppart[base + r] = mp;
+        for (int d = 16; d; d >>= 1)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], d);
+        if (lane == 0) {
+            const MomPartial& m0 = (f > tf * kRdItems) ? S.pb[tf] : S.pa[tf];
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] = m0.s[i] + s5[i];
+            ppart[base + r] = mp;
+        }
     }
 }
 
