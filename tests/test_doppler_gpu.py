@@ -122,3 +122,32 @@ def test_doppler_without_side_stream(monkeypatch):
     """The same cycles with every kernel on the caller's stream (DOG_NO_FORK: no side stream)."""
     monkeypatch.setenv("DOG_NO_FORK", "1")
     run(I.CONFIGS["cfg1"], 4, frac=0.7)
+
+
+@pytest.mark.slow
+def test_doppler_full_size_cfgT_one_cycle():
+    """The bench configuration (cfg T: 2048x2048, 8M + 800k) with the bench's radar overlay: warm the GPU
+    filter with plain cycles, inject its state into the oracle, run one Doppler cycle on both, compare
+    the next state bit for bit and the moments within 1e-4."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfgT"]
+    sc = I.scene(cfg)
+    g = dog.Filter.from_config(cfg)
+    for k in range(6):
+        g.step(sc.frame(k, device="cuda"), cfg.dt)
+    st = g.get_state()
+    o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b,
+                                    cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params()))
+    o.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+    meas = sc.frame(6)
+    dop, pA = sc.doppler(6, meas, frac=0.5, p_assoc=0.8, sd=0.25)
+    assert int((pA > 0).sum()) > 100
+    o.step_doppler(meas.numpy(), dop.numpy(), pA.numpy(), cfg.dt)
+    g.step_doppler(meas.cuda().contiguous(), dop.cuda().contiguous(), pA.cuda().contiguous(), cfg.dt)
+    sto, stg = o.get_state(), g.get_state()
+    for key in ("x", "y", "vx", "vy", "m_free"):
+        bits(sto[key], stg[key], "state." + key)
+    co = o.read_cells()
+    cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
+    bits(co["occ"], cg["occ"], "occ")
+    close(co["mean"], cg["mean"], 1e-4, 1e-6, "vel_mean")

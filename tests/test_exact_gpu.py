@@ -72,3 +72,28 @@ def test_exact_multitile_scene():
     r_b > 0): 4 cycles."""
     cfg = I.config("cfg2", width=256, height=256, nu=300_000, nu_b=30_000, beams=600, movers=4, peds=3, boxes=15)
     run(cfg, 4)
+
+
+@pytest.mark.slow
+def test_exact_full_size_cfgT_one_cycle():
+    """cfg T (2048x2048, 8M + 800k): the GPU filter warmed with plain cycles, its state injected into the
+    oracle, one exact PHD/MIB cycle on both (every cell in the active list): next state bit for bit."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfgT"]
+    sc = I.scene(cfg)
+    g = dog.Filter.from_config(cfg)
+    for k in range(6):
+        g.step(sc.frame(k, device="cuda"), cfg.dt)
+    st = g.get_state()
+    o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b,
+                                    cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params()))
+    o.set_state(st["x"], st["y"], st["vx"], st["vy"], st["w_bar"], st["m_free"], st["k"])
+    obs = I.Scene.exact_obs(sc.frame(6))
+    o.step_exact(obs.numpy(), cfg.dt)
+    g.step_exact(obs.cuda().contiguous(), cfg.dt)
+    sto, stg = o.get_state(), g.get_state()
+    for key in ("x", "y", "vx", "vy"):
+        bits(sto[key], stg[key], "state." + key)
+    co = o.read_cells()
+    cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
+    bits(co["occ"], cg["occ"], "occ")
