@@ -151,3 +151,16 @@ def test_doppler_full_size_cfgT_one_cycle():
     cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
     bits(co["occ"], cg["occ"], "occ")
     close(co["mean"], cg["mean"], 1e-4, 1e-6, "vel_mean")
+
+
+def test_doppler_incompatible_cells_fall_back():
+    """A radial-speed SD so small that almost every member's likelihood underflows to 0: those cells
+    take the GS = 0 guard (the mu_A term dropped, even split, A-35) -- bit-exact like the rest."""
+    cfg = I.config("cfg1", nu=20_000, nu_b=2_000)
+    o, g = run(cfg, 4, plain=3, frac=1.0, p_assoc=1.0, sd=0.002)
+    sc = I.scene(cfg)
+    _, pA = sc.doppler(6, sc.frame(6), frac=1.0, p_assoc=1.0, sd=0.002)   # the last cycle's overlay
+    off, gs = o.dump("OFFSETS"), o.dump("GS")
+    members = np.diff(off.astype(np.int64)) > 0
+    doppler_cells = (pA.numpy().reshape(-1) > 0) & members
+    assert doppler_cells.sum() > 0 and (gs[doppler_cells] == 0).sum() > 0
