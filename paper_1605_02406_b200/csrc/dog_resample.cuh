@@ -120,7 +120,7 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 #endif
 constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // sorted positions per thread
 static_assert(kRtItems % 8 == 0, "phase B works in batches of 8 positions");
-constexpr int kRtRunCache = 64;                                       // runs whose RunF sits in smem (rest: global)
+constexpr int kRtRunCache = 96;                                       // runs whose RunF sits in smem (rest: global)
 constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
 constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
 constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 window entries per thread
@@ -129,11 +129,10 @@ constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 wind
 // ceil(y) with y = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
 // pieces, steps bp + 1 and bp); D = F(Q_pre) - the run's offset in the tile's compact output space.
 struct RunF {
-    double y0, d1, yR, d2;
-    uint32_t pre, rpm;
-    uint16_t first, end;
-    uint32_t D;
+    double y0, d1;          // the second piece (members beyond rpm) is derived: yR = y0 + rpm d1, d2 = d1 - nu/W
+    uint32_t pre, rpm, D, pad;
 };
+static_assert(sizeof(RunF) == 32, "RunF: two per 64-byte line");
 
 struct RtSmem {   // dynamic shared memory of k_resample_tiles (~47 KB: three blocks per SM with a large L1)
     uint16_t lp[kSortTile];            // local sorted position -> local index
@@ -346,11 +345,9 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
             RunF x;
             x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
             x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
-            x.yR = __fma_rn((double)(q.P + (uint64_t)q.rpm * (q.bp + 1u)), rc.nu_over_W, -rc.U_frac);
-            x.d2 = __dmul_rn((double)q.bp, rc.nu_over_W);
             x.pre = q.pre; x.rpm = q.rpm;
-            x.first = S.first[r]; x.end = S.first[r + 1];
             x.D = Flo - (carry + ex);
+            x.pad = 0u;
             if (r < (uint32_t)kRtRunCache) S.rf[r] = x; else rf_g[base + r] = x;
         }
         carry += tot;
@@ -399,23 +396,26 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
             const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
             uint32_t j = S.runof[p0], end = S.first[j + 1];
             RunF x{};
-            if (j != srun) x = runf(j);
+            double yR = 0.0, d2 = 0.0;                      // the run's second piece (see RunF)
+            uint32_t xfirst = S.first[j];
+            auto load = [&]() { x = runf(j); yR = __fma_rn((double)x.rpm, x.d1, x.y0); d2 = x.d1 - rc.nu_over_W; };
+            if (j != srun) load();
             bool have = false;
             uint32_t Fc = 0;
             for (uint32_t p = p0; p < pend; ++p) {
                 if (p >= end) {
-                    j = S.runof[p]; end = S.first[j + 1];
-                    if (j != srun) x = runf(j);
+                    j = S.runof[p]; xfirst = end; end = S.first[j + 1];
+                    if (j != srun) load();
                     have = false;
                 }
                 if (j == srun) continue;
-                const uint32_t mr = x.pre + (p - x.first);
+                const uint32_t mr = x.pre + (p - xfirst);
                 uint32_t F0 = Fc;
                 if (!have) {
-                    const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), x.d2, x.yR);
+                    const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
                     F0 = fast_ceil(y, rc.nu, amb);
                 }
-                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), x.d2, x.yR);
+                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), d2, yR);
                 const uint32_t F1 = fast_ceil(y1, rc.nu, amb);
                 Fc = F1;
                 have = true;
@@ -440,7 +440,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
                 if (j == srun) continue;
                 const RunInfo q = runs[j];
                 const RunF& x = runf(j);
-                const uint32_t mr = q.pre + (p - x.first);
+                const uint32_t mr = q.pre + (p - S.first[j]);
                 const uint64_t Q0 = member_Q(q, mr);
                 const uint32_t C0 = fcount(Q0, rc) - x.D;
                 const uint32_t C1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc) - x.D;
