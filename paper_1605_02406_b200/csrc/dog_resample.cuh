@@ -152,15 +152,17 @@ struct RtSmem {   // dynamic shared memory of k_resample_tiles (~47 KB: three bl
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
 static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0, "vector smem access");
 
-// ceil(y) clamped to [0, nu] when y is provably within 2^-27 of the exact value and further than 2^-22
-// from an integer; otherwise *amb is set (the caller redoes the work with exact products).
-__device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, bool& amb)
+// ceil(y) clamped to [0, nu] when y is further than `margin` from an integer; otherwise *amb is set (the
+// caller redoes the work with exact products).  The per-run linear estimates are within ~nu 2^-50 of
+// the exact value, so margin = max(2^-22, nu 2^-48) keeps every accepted ceil exact.
+__device__ __forceinline__ double fast_ceil_margin(uint32_t nu) { return fmax(0x1p-22, (double)nu * 0x1p-48); }
+__device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, double margin, bool& amb)
 {
     if (y <= -0.5) return 0u;
     if (y >= (double)nu) return nu;
     const double cy = ceil(y);
     const double d = cy - y;
-    amb |= !(d > 0x1p-22 && d < 1.0 - 0x1p-22);
+    amb |= !(d > margin && d < 1.0 - margin);
     return (uint32_t)cy;
 }
 
@@ -207,6 +209,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     const DevScalars* __restrict__ sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip)
 {
     PDL_ENTER();
+    const double fmargin = fast_ceil_margin(fc.nu);
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
     const int tid = threadIdx.x;
@@ -413,10 +416,10 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
                 uint32_t F0 = Fc;
                 if (!have) {
                     const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
-                    F0 = fast_ceil(y, rc.nu, amb);
+                    F0 = fast_ceil(y, rc.nu, fmargin, amb);
                 }
                 const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), d2, yR);
-                const uint32_t F1 = fast_ceil(y1, rc.nu, amb);
+                const uint32_t F1 = fast_ceil(y1, rc.nu, fmargin, amb);
                 Fc = F1;
                 have = true;
                 const uint32_t C0 = F0 - x.D, C1 = F1 - x.D;
