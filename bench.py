@@ -59,16 +59,43 @@ def a_alg(cfg) -> float:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 5 ms around and during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML (the library
+    nvidia-smi reads) polled every ~0.5 ms from a thread; `nvidia-smi -lms 5` if NVML is unavailable."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.nv = None
+        self.lines = []              # (sm_mhz, max_mhz, {reason names})
+        self.running = False
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.nv, self.h = nv, h
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                         nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            self.running = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -78,34 +105,61 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nv, self.h
+        while self.running:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.lines.append((sm, self.max_mhz, {n for n, bit in zip(self.NAMES, self.bits) if r & bit}))
+            except Exception:
+                pass
+            time.sleep(0.0005)
+
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
+            parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
                 continue
             try:
-                sm.append(float(parts[0])); mx = float(parts[1])
+                self.lines.append((float(parts[0]), float(parts[1]),
+                                   {n for n, v in zip(self.NAMES, parts[2:6]) if v.lower().startswith("active")}))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+
+    def wait_ready(self, timeout: float = 15.0):
+        """Block until the sampler has produced its first sample."""
+        t0 = time.time()
+        while (self.nv is not None or self.proc is not None) and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
+    def mark(self) -> int:
+        return len(self.lines)
+
+    def stop(self, region=None) -> dict:
+        if self.nv is None and self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml and nvidia-smi unavailable"]}
+        time.sleep(0.01)
+        if self.nv is not None:
+            self.running = False
+            self.t.join(timeout=1)
+        else:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        samples = list(self.lines)
+        if region is not None and region[1] > region[0]:
+            samples = samples[region[0]:region[1]]       # the timed cycles only
+        sm = sorted(x[0] for x in samples)
+        reasons = set().union(*[x[2] for x in samples]) if samples else set()
+        out = {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": samples[-1][1] if samples else None,
+               "reasons": sorted(reasons), "samples": len(sm),
+               "source": "NVML polled every 0.5 ms" if self.nv is not None else "nvidia-smi -lms 5"}
+        if region is not None:
+            out["samples_in_timed_region"] = max(0, region[1] - region[0])
+        return out
 
 
 def dist_env():
@@ -199,13 +253,16 @@ def bench_ours(args, cfg):
     clocks = ClockSampler(local_rank)
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
+    clocks.wait_ready()
+    time.sleep(0.05)
+    m0 = clocks.mark()
     for i in range(K):
         flush.zero_()
         ev0[i].record(stream)
         f.step(frames[settle + W + i], cfg.dt, stream)
         ev1[i].record(stream)
     torch.cuda.synchronize()
+    m1 = clocks.mark()
     # continuous operation (the filter at frame rate with nothing in between): K cycles back to back, no
     # flush (the per-cycle working set, ~0.6 GB at cfg T, exceeds the 126 MB L2)
     c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
@@ -216,7 +273,7 @@ def bench_ours(args, cfg):
     c1.record(stream)
     torch.cuda.synchronize()
     cont_ms = c0.elapsed_time(c1) / K
-    clk = clocks.stop()
+    clk = clocks.stop((m0, m1))
     # per-stage times from a separate, shorter run with stage events between the kernels (the events
     # themselves break the programmatic launch overlap, so they stay out of the timed steps above)
     nprof_steps = min(K, 5)
@@ -455,17 +512,19 @@ def bench_sharded(args, cfg):
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
     clocks = ClockSampler(local_rank)
+    clocks.start()
+    clocks.wait_ready()
     dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
+    time.sleep(0.05)
+    m0 = clocks.mark()
     for i in range(K):
         flush.zero_()
         ev0[i].record(stream)
         f.step(bands[settle + W + i], cfg.dt, stream)
         ev1[i].record(stream)
     torch.cuda.synchronize()
-    clk = clocks.stop()
+    clk = clocks.stop((m0, clocks.mark()))
     dist.barrier()
     step_ms = sorted(ev0[i].elapsed_time(ev1[i]) for i in range(K))
     ms_all = torch.tensor([float(np.mean(step_ms))], device=dev, dtype=torch.float64)
