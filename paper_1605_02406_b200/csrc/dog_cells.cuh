@@ -264,6 +264,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
                 if (!kExact) m_free[c] = o.mF;
                 if (o.n) counts[c] = 0u;                // ready for the next cycle's k_predict_sort
                 const uint32_t li = lbase + s_cnt[i][warp] + __popc(abal[i] & lt);
+                DOG_ASSERT(li < lbase + chunk);
                 L.c[li] = c; L.n[li] = o.n; L.Rp[li] = o.Rp; L.Rb[li] = o.Rb; L.rho_p[li] = o.rp;
                 uint32_t npc = 0;
                 if (o.n) { npc = kExact ? npf[i] : npairs[c]; npairs[c] = 0u; }

@@ -74,6 +74,17 @@ __device__ __forceinline__ unsigned long long gtimer_ns()
 #define PHASE_MARK(slot) do { } while (0)
 #endif
 
+// Checked build (DOG_NVCC_EXTRA=-DDOG_CHECKED, tools/checked_tests.sh): device-side bounds assertions on
+// the writes whose index comes from a computed prefix (outputs, staging slots, run-list slots).  A
+// failed check prints and traps; the release build compiles them out.
+#ifdef DOG_CHECKED
+#include <cstdio>
+#define DOG_ASSERT(cond) do { if (!(cond)) { printf("libdog check failed: %s (%s:%d) block %d thread %d\n", \
+    #cond, __FILE__, __LINE__, (int)blockIdx.x, (int)threadIdx.x); __trap(); } } while (0)
+#else
+#define DOG_ASSERT(cond) do { } while (0)
+#endif
+
 // Programmatic dependent launch (every kernel of a cycle is launched with the PDL attribute): a kernel
 // lets the next one launch as soon as all its CTAs are running, and waits for its predecessor's results
 // (full completion and memory flush) before touching them.  Hides the launch gap between kernels.

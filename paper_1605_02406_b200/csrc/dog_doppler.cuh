@@ -272,6 +272,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
             const float4 X = pred[pbase + S.lp[p]];
             if (rc.W) {
                 const uint32_t F0 = have ? Fc : fcount(q.P + Q0, rc), F1 = fcount(q.P + Q1, rc);
+                DOG_ASSERT(F0 <= F1 && F1 <= fc.nu);
                 Fc = F1;
                 for (uint32_t o = F0; o < F1; ++o) out.s[o] = X;
             }

@@ -497,6 +497,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
                 if (!ok[h]) continue;
+                DOG_ASSERT(o[h] < fc.nu);
                 out.s[o[h]] = X[h];
                 if (kDbg) out.jidx[o[h]] = J[h];
             }
@@ -704,6 +705,7 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
             const uint64_t Q0 = PB + (uint64_t)r * bb + min(r, rbm);
             const uint64_t Q1 = Q0 + bb + (r < rbm ? 1u : 0u);
             const uint32_t F0 = fcount(Q0, rc), F1 = fcount(Q1, rc);
+            DOG_ASSERT(F0 <= F1 && F1 <= fc.nu);
             const uint32_t J = L.start[li] + sb + L.n[li] + r;
             for (uint32_t o = F0; o < F1; ++o) {
                 out.s[o] = make_float4(bx, by, bvx, bvy);

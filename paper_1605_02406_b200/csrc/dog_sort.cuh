@@ -421,6 +421,7 @@ __global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, con
         if (key >= C) continue;
         const uint32_t li = cell2list[key];
         const uint32_t slot = atomicAdd(&L.pfill[li], 1u);
+        DOG_ASSERT(slot < L.np[li]);
         plist[L.ps[li] + slot] = (t << 12) | r;
     }
 }

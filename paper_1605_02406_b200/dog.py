@@ -149,7 +149,8 @@ class Filter:
 
     def close(self):
         if getattr(self, "_h", None):
-            dog_destroy(self._h)
+            if dog_destroy is not None:          # None during interpreter shutdown: the process frees all
+                dog_destroy(self._h)
             self._h = None
 
     __del__ = close
@@ -325,7 +326,8 @@ class BandFilter:
 
     def close(self):
         if getattr(self, "_h", None):
-            dog_destroy(self._h)
+            if dog_destroy is not None:          # None during interpreter shutdown: the process frees all
+                dog_destroy(self._h)
             self._h = None
 
     __del__ = close
