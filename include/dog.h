@@ -137,6 +137,13 @@ int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** s
 /* phase 2: tile sort of [from below | own | from above], Alg. 3 on the band; *mass_dev = this band's
  * fixed-point born mass (device u64) to all-gather. */
 int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_dev, void* stream);
+/* phase 2 of a Doppler cycle (NEXT-1, dog_step_doppler's branch on a band): as dog_band_assign, plus the
+ * band's rows of the Doppler grid -- doppler_band[C_band][4] (16-byte aligned) and p_assoc_band[C_band],
+ * DEVICE, valid until dog_band_resample has been enqueued; that phase then weights the band's Doppler
+ * cells.  The joint weight of a band does not depend on the Doppler weights (A-35), so the exchanges
+ * are those of the plain cycle. */
+int dog_band_assign_doppler(dog_ctx* ctx, const float* meas_band, const float* doppler_band, const float* p_assoc_band,
+                            const uint64_t** mass_dev, void* stream);
 /* phase 3: slots on the global born-mass CDF, joint CDF of the band; *weight_dev = its joint weight. */
 int dog_band_joint(dog_ctx* ctx, const uint64_t* mass_all_dev, const uint64_t** weight_dev, void* stream);
 /* phase 4: moments, resampling of the band's share [F(P'), F(P' + W_band)) of the global outputs, births. */

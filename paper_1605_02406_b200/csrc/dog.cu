@@ -102,6 +102,8 @@ struct dog_ctx {
     uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
     uint8_t* d_tflag = nullptr;                   // per sort tile: holds members of a Doppler cell
     uint32_t* d_gfx = nullptr;                    // per sorted position: fixed-point Doppler likelihood
+    const float* band_dop = nullptr;              // band contexts: the cycle's Doppler grid (assign -> resample)
+    const float* band_pA = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
@@ -661,6 +663,17 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     return DOG_OK;
 }
 
+// Doppler working buffers, allocated on first use
+static int alloc_doppler(dog_ctx* ctx)
+{
+    if (ctx->d_rg) return DOG_OK;
+    if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
+        cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess ||
+        cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess)
+        return DOG_E_NOMEM;
+    return DOG_OK;
+}
+
 // ---- Doppler / association branch (NEXT-1): the cycle with per-member weights in Doppler cells
 int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, const float* p_assoc, float dt,
                      void* stream)
@@ -672,12 +685,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     if (((uintptr_t)doppler & 15u) != 0) return DOG_E_INVAL;
     if (int r = set_device(ctx)) return r;
     cudaStream_t st = (cudaStream_t)stream;
-    if (!ctx->d_rg) {
-        if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
-            cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess ||
-            cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess)
-            return DOG_E_NOMEM;
-    }
+    if (int r = alloc_doppler(ctx)) return r;
     const StepArgs a = step_args(ctx, dt);
     const FilterConst fc = filter_const(ctx);
     const DopIn din{(const float4*)doppler, p_assoc};
@@ -791,6 +799,27 @@ int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_
     return DOG_OK;
 }
 
+int dog_band_assign_doppler(dog_ctx* ctx, const float* meas_band, const float* doppler_band, const float* p_assoc_band,
+                            const uint64_t** mass_dev, void* stream)
+{
+    if (!ctx || !doppler_band || !p_assoc_band || ((uintptr_t)doppler_band & 15u) != 0) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 2) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    if (int r = alloc_doppler(ctx)) return r;
+    if (int r = dog_band_assign(ctx, meas_band, mass_dev, stream)) return r;
+    // the per-run likelihood sums of the band's tiles (same kernel as the whole-grid branch)
+    const StepArgs a = step_args(ctx, ctx->band_dt);
+    const FilterConst fc = filter_const(ctx);
+    const DopIn din{(const float4*)doppler_band, p_assoc_band};
+    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, (cudaStream_t)stream, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+              (const float4*)ctx->pst, din, ctx->d_rg, ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc,
+              (int)(a.k & 1)));
+    ctx->band_dop = doppler_band;
+    ctx->band_pA = p_assoc_band;
+    return DOG_OK;
+}
+
 int dog_band_joint(dog_ctx* ctx, const uint64_t* mass_all_dev, const uint64_t** weight_dev, void* stream)
 {
     if (!ctx || !mass_all_dev || !weight_dev) return DOG_E_INVAL;
@@ -815,10 +844,27 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
     cudaStream_t st = (cudaStream_t)stream;
     const StepArgs a = step_args(ctx, ctx->band_dt);
     const FilterConst fc = filter_const(ctx);
-    if (int r = L_pairs(ctx, weight_all_dev, a, fc, st)) return r;
-    if (int r = L_resample(ctx, a, fc, st)) return r;
-    if (int r = L_moments(ctx, st)) return r;
-    if (int r = L_births(ctx, a, fc, st)) return r;
+    if (ctx->band_pA) {   // Doppler cycle (dog_band_assign_doppler): as dog_step_doppler, on the band
+        const DopIn din{(const float4*)ctx->band_dop, ctx->band_pA};
+        const int par = (int)(a.k & 1);
+        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, false, DopPS{ctx->band_pA, ctx->d_rg, ctx->d_GS, ctx->d_tflag}))
+            return r;
+        if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
+        NextState ns{ctx->st, nullptr};
+        CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
+                     (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
+                     (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const uint32_t*)ctx->d_gfx,
+                     (const DevScalars*)ctx->sc, fc, par));
+        if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
+        if (int r = L_births(ctx, a, fc, st, &din)) return r;
+        ctx->band_dop = nullptr;
+        ctx->band_pA = nullptr;
+    } else {
+        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st)) return r;
+        if (int r = L_resample(ctx, a, fc, st)) return r;
+        if (int r = L_moments(ctx, st)) return r;
+        if (int r = L_births(ctx, a, fc, st)) return r;
+    }
     ctx->phase = 0;
     ctx->k += 1;
     return DOG_OK;

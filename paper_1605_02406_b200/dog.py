@@ -81,6 +81,7 @@ _SIGS = {
     "dog_band_buffers": ([_vp, C.c_uint32, C.c_uint32, _vpp, _vpp, _vpp, _vpp, _vp], C.c_int),
     "dog_band_assign": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_joint": ([_vp, _vp, _vpp, _vp], C.c_int),
+    "dog_band_assign_doppler": ([_vp, _vp, _vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_resample": ([_vp, _vp, _vp], C.c_int),
     "dog_band_particles": ([_vp, _vp, C.c_uint64, _u32p, _u64p], C.c_int),
     "dog_band_set_state": ([_vp, _vp, C.c_uint32, C.c_uint64, _vp, C.c_float, C.c_int64], C.c_int),
@@ -354,6 +355,16 @@ class BandFilter:
         assert meas_band.numel() == 2 * self.C
         m = _vp()
         _check(dog_band_assign(self._h, meas_band.data_ptr(), C.byref(m), _stream_ptr(stream)), "dog_band_assign")
+        return DeviceArray.tensor(m.value, 1, torch.int64)
+
+    def assign_doppler(self, meas_band: torch.Tensor, doppler_band: torch.Tensor, p_assoc_band: torch.Tensor,
+                       stream=None) -> torch.Tensor:
+        """include/dog.h dog_band_assign_doppler: the band's measurement, Doppler and p_A rows (device)."""
+        for t, k in ((meas_band, 2), (doppler_band, 4), (p_assoc_band, 1)):
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == k * self.C
+        m = _vp()
+        _check(dog_band_assign_doppler(self._h, meas_band.data_ptr(), doppler_band.data_ptr(), p_assoc_band.data_ptr(),
+                                       C.byref(m), _stream_ptr(stream)), "dog_band_assign_doppler")
         return DeviceArray.tensor(m.value, 1, torch.int64)
 
     def joint(self, mass_all: torch.Tensor, stream=None) -> torch.Tensor:

@@ -192,7 +192,8 @@ class ShardedFilter:
         """The band's rows of a full-grid measurement tensor [H][W][2] (a contiguous view)."""
         return meas_full[self.row0:self.row1]
 
-    def step(self, meas_band: torch.Tensor, dt: float, stream=None):
+    def step(self, meas_band: torch.Tensor, dt: float, stream=None, doppler=None):
+        """One cycle; doppler = (doppler_band [C_band, 4], p_assoc_band [C_band]) for the Doppler branch."""
         f = self.f
         f.predict(dt, stream)
         n_down, n_up, n_own, n_far = f.sizes(stream)
@@ -200,7 +201,7 @@ class ShardedFilter:
         n_lo, n_hi = self.t.counts(n_down, n_up)
         sd, su, rl, rh = f.buffers(n_down, n_up, n_lo, n_hi, stream)
         self.t.migrate(sd, su, rl, rh)
-        mass = f.assign(meas_band, stream)
+        mass = f.assign(meas_band, stream) if doppler is None else f.assign_doppler(meas_band, *doppler, stream)
         self.t.allgather_u64(mass, self.mass_all)
         weight = f.joint(self.mass_all, stream)
         self.t.allgather_u64(weight, self.weight_all)
@@ -261,7 +262,8 @@ class LocalBands:
         kw.update(over)
         return cls(cfg.width, cfg.height, cfg.nu, cfg.nu_b, world, **kw)
 
-    def step(self, meas_full: torch.Tensor, dt: float):
+    def step(self, meas_full: torch.Tensor, dt: float, doppler=None):
+        """One cycle of every band; doppler = (doppler [H, W, 4] or [C, 4], p_assoc [C]) full-grid."""
         B = self.bands
         for f in B:
             f.predict(dt)
@@ -277,15 +279,23 @@ class LocalBands:
                 bufs[b - 1][3].copy_(bufs[b][0])
             if b < self.world - 1:
                 bufs[b + 1][2].copy_(bufs[b][1])
+        width = self._args[0]
         for b, f in enumerate(B):
             r0, r1 = self.rows[b]
-            m = f.assign(meas_full[r0:r1])
+            if doppler is None:
+                m = f.assign(meas_full[r0:r1])
+            else:
+                dop = doppler[0].reshape(-1, 4)[r0 * width:r1 * width].contiguous()
+                pa = doppler[1].reshape(-1)[r0 * width:r1 * width].contiguous()
+                self._dop_keep = getattr(self, "_dop_keep", []) + [(dop, pa)]   # alive until resample
+                m = f.assign_doppler(meas_full[r0:r1], dop, pa)
             self.mass_all[b:b + 1].copy_(m)
         for b, f in enumerate(B):
             w = f.joint(self.mass_all)
             self.weight_all[b:b + 1].copy_(w)
         for f in B:
             f.resample(self.weight_all)
+        self._dop_keep = []
 
     def particles(self):
         """All own particles in global index order: float32 [n, 4], and each band's (first index, count)."""
