@@ -137,6 +137,10 @@ int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** s
 /* phase 2: tile sort of [from below | own | from above], Alg. 3 on the band; *mass_dev = this band's
  * fixed-point born mass (device u64) to all-gather. */
 int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_dev, void* stream);
+/* phase 2 of an exact PHD/MIB cycle (NEXT-3, dog_step_exact on a band): as dog_band_assign with the
+ * band's rows of the observation grid obs_band[C_band][4] (DEVICE, 16-byte aligned) instead of the
+ * measurement grid; the following joint and resample phases run the exact cycle's list handling. */
+int dog_band_assign_exact(dog_ctx* ctx, const float* obs_band, const uint64_t** mass_dev, void* stream);
 /* phase 2 of a Doppler cycle (NEXT-1, dog_step_doppler's branch on a band): as dog_band_assign, plus the
  * band's rows of the Doppler grid -- doppler_band[C_band][4] (16-byte aligned) and p_assoc_band[C_band],
  * DEVICE, valid until dog_band_resample has been enqueued; that phase then weights the band's Doppler

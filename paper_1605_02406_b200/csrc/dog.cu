@@ -104,6 +104,7 @@ struct dog_ctx {
     uint32_t* d_gfx = nullptr;                    // per sorted position: fixed-point Doppler likelihood
     const float* band_dop = nullptr;              // band contexts: the cycle's Doppler grid (assign -> resample)
     const float* band_pA = nullptr;
+    bool band_exact = false;                      // band contexts: this cycle runs the exact PHD/MIB update
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_in[2] = {}, ev_used[2] = {}, ev_out[2] = {}, ev_read[2] = {};
@@ -518,8 +519,8 @@ static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const Fil
 static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
                        bool wide = false)
 {
-    if (wide && !A_all) {   // every cell may be active (exact filter): grid-wide scan over k_cells' chunks
-        CK(launch(k_ls_prefix1, 1, 1024, 0, st, 0, ctx->bt, ctx->cell_blocks, ctx->ws, ctx->sc));
+    if (wide) {   // every cell may be active (exact filter): grid-wide scan over k_cells' chunks
+        CK(launch(k_ls_prefix1, 1, 1024, 0, st, 0, ctx->bt, ctx->cell_blocks, ctx->ws, ctx->sc, A_all, fc));
         CK(launch(k_ls_chunks1, ctx->cell_blocks, 256, 0, st, 0, ctx->stage, ctx->list, ctx->bt, ctx->cell_chunk,
                   ctx->cell2list, ctx->ws, (const DevScalars*)ctx->sc, fc));
         CK(launch(k_ls_prefix2, 1, 1024, 0, st, 0, ctx->cell_blocks, ctx->ws));
@@ -799,6 +800,23 @@ int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_
     return DOG_OK;
 }
 
+int dog_band_assign_exact(dog_ctx* ctx, const float* obs_band, const uint64_t** mass_dev, void* stream)
+{
+    if (!ctx || !obs_band || !mass_dev || ((uintptr_t)obs_band & 15u) != 0) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->phase != 2) return DOG_E_STATE;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    const StepArgs a = step_args(ctx, ctx->band_dt);
+    const FilterConst fc = filter_const(ctx);
+    if (int r = L_predict_sort(ctx, false, a, fc, st)) return r;
+    if (int r = L_cells(ctx, nullptr, a, fc, st, obs_band)) return r;
+    *mass_dev = &ctx->sc->A_acc;
+    ctx->band_exact = true;
+    ctx->phase = 3;
+    return DOG_OK;
+}
+
 int dog_band_assign_doppler(dog_ctx* ctx, const float* meas_band, const float* doppler_band, const float* p_assoc_band,
                             const uint64_t** mass_dev, void* stream)
 {
@@ -829,7 +847,7 @@ int dog_band_joint(dog_ctx* ctx, const uint64_t* mass_all_dev, const uint64_t** 
     cudaStream_t st = (cudaStream_t)stream;
     const StepArgs a = step_args(ctx, ctx->band_dt);
     const FilterConst fc = filter_const(ctx);
-    if (int r = L_list_scan(ctx, mass_all_dev, a, fc, st)) return r;
+    if (int r = L_list_scan(ctx, mass_all_dev, a, fc, st, ctx->band_exact)) return r;
     *weight_dev = &ctx->sc->W;
     ctx->phase = 4;
     return DOG_OK;
@@ -860,10 +878,12 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
         ctx->band_dop = nullptr;
         ctx->band_pA = nullptr;
     } else {
-        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st)) return r;
+        const bool ex = ctx->band_exact;          // exact filter: long lists, births in every cell
+        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, ex)) return r;
         if (int r = L_resample(ctx, a, fc, st)) return r;
-        if (int r = L_moments(ctx, st)) return r;
-        if (int r = L_births(ctx, a, fc, st)) return r;
+        if (int r = L_moments(ctx, st, nullptr, ex)) return r;
+        if (int r = L_births(ctx, a, fc, st, nullptr, ex)) return r;
+        ctx->band_exact = false;
     }
     ctx->phase = 0;
     ctx->k += 1;

@@ -566,8 +566,11 @@ struct WideScan {
     uint64_t* pJ; uint32_t* pit;                                  // chunk prefixes, pair 2
 };
 
+// A_all: born mass of every shard (band contexts) or nullptr: the born-mass CDF then starts at the
+// prefix of the shards below and A is the global total (as in k_list_scan).
 __global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nblk, WideScan ws,
-                                                     DevScalars* __restrict__ sc)
+                                                     DevScalars* __restrict__ sc, const uint64_t* __restrict__ A_all,
+                                                     FilterConst fc)
 {
     PDL_ENTER();
     __shared__ uint64_t s_w[33];
@@ -586,6 +589,12 @@ __global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nb
     uint64_t on = block_excl_scan<uint64_t, 32>(sn, s_w, tn);
     uint64_t op = block_excl_scan<uint64_t, 32>(sp, s_w, tp);
     uint64_t orb = block_excl_scan<uint64_t, 32>(sr, s_w, tr);
+    if (A_all) {                                   // global born-mass CDF over the shards
+        uint64_t pre = 0, tot = 0;
+        for (uint32_t r = 0; r < fc.world; ++r) { if (r < fc.rank) pre += A_all[r]; tot += A_all[r]; }
+        orb += pre;
+        tr = tot;
+    }
 #pragma unroll
     for (int i = 0; i < kI; ++i) {
         const uint32_t b = tid * kI + i;

@@ -82,6 +82,7 @@ _SIGS = {
     "dog_band_assign": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_joint": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_assign_doppler": ([_vp, _vp, _vp, _vp, _vpp, _vp], C.c_int),
+    "dog_band_assign_exact": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_resample": ([_vp, _vp, _vp], C.c_int),
     "dog_band_particles": ([_vp, _vp, C.c_uint64, _u32p, _u64p], C.c_int),
     "dog_band_set_state": ([_vp, _vp, C.c_uint32, C.c_uint64, _vp, C.c_float, C.c_int64], C.c_int),
@@ -365,6 +366,15 @@ class BandFilter:
         m = _vp()
         _check(dog_band_assign_doppler(self._h, meas_band.data_ptr(), doppler_band.data_ptr(), p_assoc_band.data_ptr(),
                                        C.byref(m), _stream_ptr(stream)), "dog_band_assign_doppler")
+        return DeviceArray.tensor(m.value, 1, torch.int64)
+
+    def assign_exact(self, obs_band: torch.Tensor, stream=None) -> torch.Tensor:
+        """include/dog.h dog_band_assign_exact: the band's rows of the exact filter's observation grid."""
+        assert obs_band.is_cuda and obs_band.dtype == torch.float32 and obs_band.is_contiguous()
+        assert obs_band.numel() == 4 * self.C
+        m = _vp()
+        _check(dog_band_assign_exact(self._h, obs_band.data_ptr(), C.byref(m), _stream_ptr(stream)),
+               "dog_band_assign_exact")
         return DeviceArray.tensor(m.value, 1, torch.int64)
 
     def joint(self, mass_all: torch.Tensor, stream=None) -> torch.Tensor:

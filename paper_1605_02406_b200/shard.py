@@ -192,8 +192,9 @@ class ShardedFilter:
         """The band's rows of a full-grid measurement tensor [H][W][2] (a contiguous view)."""
         return meas_full[self.row0:self.row1]
 
-    def step(self, meas_band: torch.Tensor, dt: float, stream=None, doppler=None):
-        """One cycle; doppler = (doppler_band [C_band, 4], p_assoc_band [C_band]) for the Doppler branch."""
+    def step(self, meas_band: torch.Tensor, dt: float, stream=None, doppler=None, obs=None):
+        """One cycle; doppler = (doppler_band [C_band, 4], p_assoc_band [C_band]) for the Doppler branch;
+        obs = obs_band [C_band, 4] for the exact PHD/MIB cycle (meas_band is then ignored)."""
         f = self.f
         f.predict(dt, stream)
         n_down, n_up, n_own, n_far = f.sizes(stream)
@@ -201,7 +202,12 @@ class ShardedFilter:
         n_lo, n_hi = self.t.counts(n_down, n_up)
         sd, su, rl, rh = f.buffers(n_down, n_up, n_lo, n_hi, stream)
         self.t.migrate(sd, su, rl, rh)
-        mass = f.assign(meas_band, stream) if doppler is None else f.assign_doppler(meas_band, *doppler, stream)
+        if obs is not None:
+            mass = f.assign_exact(obs, stream)
+        elif doppler is not None:
+            mass = f.assign_doppler(meas_band, *doppler, stream)
+        else:
+            mass = f.assign(meas_band, stream)
         self.t.allgather_u64(mass, self.mass_all)
         weight = f.joint(self.mass_all, stream)
         self.t.allgather_u64(weight, self.weight_all)
@@ -262,8 +268,9 @@ class LocalBands:
         kw.update(over)
         return cls(cfg.width, cfg.height, cfg.nu, cfg.nu_b, world, **kw)
 
-    def step(self, meas_full: torch.Tensor, dt: float, doppler=None):
-        """One cycle of every band; doppler = (doppler [H, W, 4] or [C, 4], p_assoc [C]) full-grid."""
+    def step(self, meas_full: torch.Tensor, dt: float, doppler=None, obs=None):
+        """One cycle of every band; doppler = (doppler [H, W, 4] or [C, 4], p_assoc [C]) full-grid; obs =
+        the exact filter's full-grid observation grid [C, 4] (or [H, W, 4])."""
         B = self.bands
         for f in B:
             f.predict(dt)
@@ -282,7 +289,11 @@ class LocalBands:
         width = self._args[0]
         for b, f in enumerate(B):
             r0, r1 = self.rows[b]
-            if doppler is None:
+            if obs is not None:
+                ob = obs.reshape(-1, 4)[r0 * width:r1 * width].contiguous()
+                self._dop_keep = getattr(self, "_dop_keep", []) + [ob]
+                m = f.assign_exact(ob)
+            elif doppler is None:
                 m = f.assign(meas_full[r0:r1])
             else:
                 dop = doppler[0].reshape(-1, 4)[r0 * width:r1 * width].contiguous()

@@ -128,3 +128,34 @@ def test_doppler_bands_bit_exact():
             _bits(f.m_free(), st["m_free"][sl], f"cycle {k} band {b}: m_F")
             mb, mw = f.read_cells()["mean"].cpu().numpy(), cw["mean"][sl].cpu().numpy()
             assert np.allclose(mb, mw, rtol=1e-4, atol=1e-6), f"cycle {k} band {b}: mean"
+
+
+def test_exact_bands_bit_exact():
+    """NEXT-3 on row bands: three bands running the exact PHD/MIB cycle (dog_band_assign_exact; every cell
+    of a band in its list, births over the whole grid on the global born-mass CDF) reproduce the
+    whole-grid dog_step_exact bit for bit."""
+    from paper_1605_02406_b200 import dog, shard
+    cfg = I.config("cfg2", width=128, height=96, nu=60_000, nu_b=6_000, beams=300, movers=3, peds=2, boxes=6)
+    g = dog.Filter.from_config(cfg)
+    lb = shard.LocalBands.from_config(cfg, 3)
+    sc = I.scene(cfg)
+    for k in range(6):
+        meas = sc.frame(k, device="cuda").contiguous()
+        if k < 2:
+            g.step(meas, cfg.dt)
+            lb.step(meas, cfg.dt)
+        else:
+            obs = I.Scene.exact_obs(meas)
+            g.step_exact(obs, cfg.dt)
+            lb.step(meas, cfg.dt, obs=obs)
+        torch.cuda.synchronize()
+        assert lb.n_far == 0
+        st = g.get_state()
+        whole = np.stack([st["x"], st["y"], st["vx"], st["vy"]], 1)
+        parts, _ = lb.particles()
+        _bits(parts, whole, f"cycle {k}: next state")
+        cw = g.read_cells()
+        for b, f in enumerate(lb.bands):
+            r0, r1 = lb.rows[b]
+            sl = slice(r0 * cfg.width, r1 * cfg.width)
+            _bits(f.read_cells()["occ"].cpu().numpy(), cw["occ"][sl].cpu().numpy(), f"cycle {k} band {b}: occ")
