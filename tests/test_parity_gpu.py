@@ -227,12 +227,16 @@ def test_profile_stages():
 
 
 @pytest.mark.slow
-def test_full_size_cfgT_one_cycle():
-    """The bench configuration (cfg T: 2048x2048, 8M + 800k) in the bench's launch configuration: warm
-    the GPU filter for 6 cycles, inject its state into the oracle, run one more cycle on both and
-    compare every stage element by element."""
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfgT", "cfg4", "cfg5"])
+def test_full_size_one_cycle(name):
+    """Every BASELINE.json configuration at its full size -- cfg2 (512x512, 2M + 200k), cfg3 (1024x1024,
+    8M + 800k), the bench's cfg T (2048x2048, 8M + 800k), cfg4 (2048x2048, 32M + 3.2M, on one GPU) and
+    the cfg5 stress case (1024x1024, 8M + 2M, 4x noise, p_B 0.1) -- in the bench's launch configuration:
+    warm the GPU filter for 6 cycles, inject its state into the oracle, run one more cycle on both and
+    compare every stage element by element.  Particles predicted within 2^-20 cells of a cell boundary
+    are counted and reported separately (north star); their keys are checked like every other one."""
     from paper_1605_02406_b200 import dog
-    cfg = I.CONFIGS["cfgT"]
+    cfg = I.CONFIGS[name]
     sc = I.scene(cfg)
     g = dog.Filter.from_config(cfg, debug=True)
     for k in range(6):
@@ -244,6 +248,10 @@ def test_full_size_cfgT_one_cycle():
     meas = sc.frame(6).numpy()
     o.step(meas, cfg.dt)
     g.step(torch.from_numpy(meas).cuda(), cfg.dt)
+    px, py = o.dump("PRED_X").astype(np.float64), o.dump("PRED_Y").astype(np.float64)
+    near = (np.abs(px - np.round(px)) < 2.0 ** -20) | (np.abs(py - np.round(py)) < 2.0 ** -20)
+    assert_bits(o.dump("KEY")[near], g.debug("KEY")[near], "keys of near-boundary particles")
+    print(f"{name}: {int(near.sum())} of {cfg.nu} particles within 2^-20 cells of a cell boundary")
     compare_cycle(o, g)
 
 
