@@ -210,19 +210,6 @@ constexpr uint32_t kEvOffMean = 0, kEvOffCov = 8 * kEvT, kEvOffLab = 20 * kEvT, 
                    kEvOffVal = 22 * kEvT, kEvStage = 23 * kEvT;
 constexpr uint32_t kEvSmem = kEvStages * kEvStage;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
-{
-    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-                 "@!p bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
-}
-
 __global__ __launch_bounds__(kEvThreads, 2) void k_eval_cells_tma(
     const float2* __restrict__ mean, const float* __restrict__ cov, const uint8_t* __restrict__ valid,
     const uint32_t* __restrict__ vbits, const uint8_t* __restrict__ labels, const uint8_t* __restrict__ mask,
