@@ -234,13 +234,19 @@ def test_full_size_one_cycle(name):
     the cfg5 stress case (1024x1024, 8M + 2M, 4x noise, p_B 0.1) -- in the bench's launch configuration:
     warm the GPU filter for 6 cycles, inject its state into the oracle, run one more cycle on both and
     compare every stage element by element.  Particles predicted within 2^-20 cells of a cell boundary
-    are counted and reported separately (north star); their keys are checked like every other one."""
+    are counted and reported separately (north star); their keys are checked like every other one.
+    A second filter in the release configuration bench.py times (no debug dumps: the kernels without
+    their debug stores) runs the same seven cycles; its next state and readouts must equal the oracle's
+    too (bit-exact; moments within 1e-4)."""
     from paper_1605_02406_b200 import dog
     cfg = I.CONFIGS[name]
     sc = I.scene(cfg)
     g = dog.Filter.from_config(cfg, debug=True)
+    r = dog.Filter.from_config(cfg)
     for k in range(6):
-        g.step(sc.frame(k, device="cuda"), cfg.dt)
+        m = sc.frame(k, device="cuda")
+        g.step(m, cfg.dt)
+        r.step(m, cfg.dt)
     st = g.get_state()
     o = oracle.Oracle(oracle.Params(width=cfg.width, height=cfg.height, nu=cfg.nu, nu_b=cfg.nu_b,
                                     cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params()))
@@ -253,6 +259,16 @@ def test_full_size_one_cycle(name):
     assert_bits(o.dump("KEY")[near], g.debug("KEY")[near], "keys of near-boundary particles")
     print(f"{name}: {int(near.sum())} of {cfg.nu} particles within 2^-20 cells of a cell boundary")
     compare_cycle(o, g)
+    r.step(torch.from_numpy(meas).cuda(), cfg.dt)
+    sto, str_ = o.get_state(), r.get_state()
+    for key in ("x", "y", "vx", "vy", "m_free"):
+        assert_bits(sto[key], str_[key], "release state." + key)
+    co = o.read_cells()
+    cr = {key: v.cpu().numpy() for key, v in r.read_cells(check=False).items() if key != "status"}
+    assert_bits(co["occ"], cr["occ"], "release occ")
+    assert_bits(co["free"], cr["free"], "release free")
+    rel_close(co["mean"].reshape(-1), cr["mean"].reshape(-1), 1e-4, 1e-6, "release vel_mean")
+    r.close()
 
 
 def test_transforms_exhaustive():
