@@ -82,3 +82,13 @@ def test_no_oracle_in_product():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "dog_oracle" not in txt, f
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """With the CUDA library missing the product path refuses to import (no silent CPU fallback)."""
+    import sys
+    env = dict(os.environ, DOG_LIB=str(tmp_path / "missing" / "libdog.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_1605_02406_b200.dog"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "libdog.so not found" in r.stderr and "no fallback" in r.stderr
