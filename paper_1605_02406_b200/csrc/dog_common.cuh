@@ -121,7 +121,8 @@ __device__ __forceinline__ T warp_sum(T v)
 // whose entries mostly have none (the exact filter's); otherwise one entry per group per step.
 // In batch mode an entry with exactly one run goes to single(li) on its own lane (no group work: the
 // exact filter's entries are mostly like that); body(li, m) gets those with two or more.
-template <bool kBatch, int G, typename F, typename S1>
+// kSmall > 1: entries with 1..kSmall runs go to single(li, m) (one lane each), the rest to body.
+template <bool kBatch, int G, int kSmall = 1, typename F, typename S1>
 __device__ __forceinline__ void for_run_entries(const uint32_t* __restrict__ np, uint32_t Lc, F&& body, S1&& single)
 {
     const int lane = threadIdx.x & 31, gl = lane & (G - 1);
@@ -131,8 +132,12 @@ __device__ __forceinline__ void for_run_entries(const uint32_t* __restrict__ np,
     if (kBatch) {
         for (uint32_t q0 = gi * G; q0 < Lc; q0 += ng * G) {
             const uint32_t mine = q0 + gl < Lc ? np[q0 + gl] : 0u;
-            if (mine == 1) single(q0 + gl);
-            uint32_t todo = (__ballot_sync(gmask, mine > 1) >> (lane & ~(G - 1))) & (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u));
+            if constexpr (kSmall == 1) {
+                if (mine == 1) single(q0 + gl);
+            } else {
+                if (mine >= 1 && mine <= (uint32_t)kSmall) single(q0 + gl, mine);
+            }
+            uint32_t todo = (__ballot_sync(gmask, mine > (uint32_t)kSmall) >> (lane & ~(G - 1))) & (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u));
             while (todo) {
                 const int b = __ffs(todo) - 1;
                 todo &= todo - 1;

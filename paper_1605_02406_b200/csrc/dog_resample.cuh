@@ -510,6 +510,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
 // Velocity moments per cell (Eqs. 81-84): the cell's run sums combined in tile order (k_pair_sort left
 // the run list in that order) in a fixed summation order.  Groups of 8 lanes take one cell each.
 constexpr int kMoGroup = 8;
+constexpr int kMoSmall = 4;   // kBatch (exact filter): cells with <= 4 runs summed by one lane each
 
 template <bool kBatch>
 __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
@@ -528,12 +529,18 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __r
         else
             finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
     };
-    auto single = [&](uint32_t li) {                       // one run: its sums are the cell's
-        const double* ps = ppart[plist[L.ps[li]]].s;
-        const double s5[5] = {ps[0], ps[1], ps[2], ps[3], ps[4]};
+    auto single = [&](uint32_t li, uint32_t m = 1u) {      // few runs: one lane sums them in list order
+        const uint32_t* pl = plist + L.ps[li];
+        const double* ps = ppart[pl[0]].s;
+        double s5[5] = {ps[0], ps[1], ps[2], ps[3], ps[4]};
+        for (uint32_t q = 1; q < m; ++q) {
+            const double* pq = ppart[pl[q]].s;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += pq[i];
+        }
         finalize(li, s5);
     };
-    for_run_entries<kBatch, kMoGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
+    for_run_entries<kBatch, kMoGroup, kBatch ? kMoSmall : 1>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const uint32_t* pl = plist + L.ps[li];
         double s5[5] = {0, 0, 0, 0, 0};
         for (uint32_t q = gl; q < m; q += kMoGroup) {

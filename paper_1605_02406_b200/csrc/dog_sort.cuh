@@ -446,6 +446,8 @@ struct DopPS {
     uint8_t* tflag;
 };
 
+constexpr int kPsSmall = 4;   // kBatch: cells with <= 4 runs handled by one lane (sorting network)
+static_assert(kPsSmall == 4, "the sorting network below is for 4 entries");
 template <bool kBatch>
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
                                                    uint32_t* __restrict__ ptmp, const uint64_t* __restrict__ W_all,
@@ -494,12 +496,34 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         dp.GS[li] = gs;
         if (gs) dp.tflag[v >> 12] = 1;
     };
-    auto single = [&](uint32_t li) {                      // one run: pre = 0
-        const uint32_t v = plist[L.ps[li]];
-        tp.run[v] = run_info(li);
-        dop_single(li, v);
+    auto single = [&](uint32_t li, uint32_t m = 1u) {     // one run: pre = 0
+        uint32_t* pl = plist + L.ps[li];
+        if (!kBatch || m == 1u) {
+            const uint32_t v = pl[0];
+            tp.run[v] = run_info(li);
+            dop_single(li, v);
+            return;
+        }
+        // kBatch (exact filter, no Doppler): 2..kPsSmall runs sorted by one lane in registers (a
+        // 4-element sorting network; entries are distinct), then the exclusive prefix of their counts
+        uint32_t v[kPsSmall];
+#pragma unroll
+        for (int q = 0; q < kPsSmall; ++q) v[q] = (uint32_t)q < m ? pl[q] : 0xFFFFFFFFu;
+        auto cs = [](uint32_t& x, uint32_t& y) { const uint32_t lo = min(x, y), hi = max(x, y); x = lo; y = hi; };
+        cs(v[0], v[1]); cs(v[2], v[3]); cs(v[0], v[2]); cs(v[1], v[3]); cs(v[1], v[2]);
+        RunInfo r2 = run_info(li);
+        uint32_t carry = 0;
+#pragma unroll
+        for (int q = 0; q < kPsSmall; ++q) {
+            if ((uint32_t)q < m) {
+                r2.pre = carry;
+                tp.run[v[q]] = r2;
+                pl[q] = v[q];                                 // the cell's list, now in tile order
+                carry += (uint32_t)tp.cnt[v[q]] + 1u;
+            }
+        }
     };
-    for_run_entries<kBatch, kPsGroup>(L.np, Lc, [&](uint32_t li, uint32_t m) {
+    for_run_entries<kBatch, kPsGroup, kBatch ? kPsSmall : 1>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const RunInfo ri = run_info(li);
         uint32_t* pl = plist + L.ps[li];
         if (m == 1) {                                 // (tile << 12 | run) is the run's slot index
