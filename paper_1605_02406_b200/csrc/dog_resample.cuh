@@ -314,6 +314,7 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
         const uint32_t r = r0 + tid;
         const bool live = r < nd && r != srun;
         uint32_t Flo = 0, c = 0;
+        RunF x{};
         if (live) {
             const uint32_t f = S.first[r], e = S.first[r + 1];
             const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
@@ -335,22 +336,31 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
                 for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
                 ppart[base + r] = mp;
             }
-            if (rc.W) {
+            if (rc.W) {   // F at the run's ends from the same linear estimate phase C uses (exact unless
+                          // ambiguous, then the exact 128-bit count)
                 const RunInfo q = runs[r];
-                Flo = fcount(member_Q(q, q.pre), rc);
-                c = fcount(member_Q(q, q.pre + (e - f)), rc) - Flo;
+                x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
+                x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
+                x.pre = q.pre; x.rpm = q.rpm;
+                x.pad = 0u;
+                const double yR = __fma_rn((double)x.rpm, x.d1, x.y0), d2 = x.d1 - rc.nu_over_W;
+                auto yof = [&](uint32_t mr) {
+                    return mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
+                };
+                bool amb = false;
+                Flo = fast_ceil(yof(q.pre), rc.nu, fmargin, amb);
+                uint32_t Fhi = fast_ceil(yof(q.pre + (e - f)), rc.nu, fmargin, amb);
+                if (amb) {
+                    Flo = fcount(member_Q(q, q.pre), rc);
+                    Fhi = fcount(member_Q(q, q.pre + (e - f)), rc);
+                }
+                c = Fhi - Flo;
             }
         }
         uint32_t tot;
         const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
         if (live && rc.W) {
-            const RunInfo q = runs[r];
-            RunF x;
-            x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
-            x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
-            x.pre = q.pre; x.rpm = q.rpm;
             x.D = Flo - (carry + ex);
-            x.pad = 0u;
             if (r < (uint32_t)kRtRunCache) S.rf[r] = x; else rf_g[base + r] = x;
         }
         carry += tot;

@@ -1,7 +1,8 @@
 """Per-phase block times of the instrumented kernels (diagnostics build: DOG_NVCC_EXTRA=-DDOG_TIMING).
 
 Runs the cfgT filter for 30 settle cycles, then 10 cycles with the phase counters reset; prints the
-average per-block microseconds of each phase slot."""
+average per-block microseconds of each phase slot.  With a second argument "exact": 30 plain cycles, 8
+exact PHD/MIB cycles, then 10 exact cycles measured (the run-heavy regime of NEXT-3)."""
 import ctypes as C
 import sys
 
@@ -17,13 +18,27 @@ cfg = I.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfgT"]
 sc = I.scene(cfg)
 f = dog.Filter.from_config(cfg)
 frames = [sc.frame(k, device="cuda") for k in range(40)]
-for k in range(30):
-    f.step(frames[k], cfg.dt)
+exact = len(sys.argv) > 2 and sys.argv[2] == "exact"
+if exact:
+    frames = frames + [sc.frame(k, device="cuda") for k in range(40, 48)]
+    for k in range(30, 48):
+        frames[k] = I.Scene.exact_obs(frames[k].contiguous())
+
+
+def cycle(k):
+    if exact and k >= 30:
+        f.step_exact(frames[k], cfg.dt)
+    else:
+        f.step(frames[k], cfg.dt)
+
+
+for k in range(38 if exact else 30):
+    cycle(k)
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * 64)()
 dog._lib.dog_timing_dump(buf, 64, 1)
-for k in range(30, 40):
-    f.step(frames[k], cfg.dt)
+for k in range(38, 48) if exact else range(30, 40):
+    cycle(k)
 torch.cuda.synchronize()
 dog._lib.dog_timing_dump(buf, 64, 0)
 t = np.frombuffer(buf, dtype=np.uint64).astype(np.float64)
