@@ -498,10 +498,14 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     };
     auto single = [&](uint32_t li, uint32_t m = 1u) {     // one run: pre = 0
         uint32_t* pl = plist + L.ps[li];
-        if (!kBatch || m == 1u) {
-            const uint32_t v = pl[0];
-            tp.run[v] = run_info(li);
-            dop_single(li, v);
+        if constexpr (!kBatch) {
+            tp.run[pl[0]] = run_info(li);
+            dop_single(li, pl[0]);
+            return;
+        }
+        if (m == 1u) {
+            tp.run[pl[0]] = run_info(li);
+            dop_single(li, pl[0]);
             return;
         }
         // kBatch (exact filter, no Doppler): 2..kPsSmall runs sorted by one lane in registers (a
