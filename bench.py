@@ -215,7 +215,7 @@ def bench_reference(args, cfg):
               f"{band.nu} + {band.nu_b} particles), {args.steps} timed oracle cycles after {args.warmup} warm-up")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu, "nu_b": cfg.nu_b,
                    "sample": sample},
@@ -464,7 +464,7 @@ def bench_ours(args, cfg):
     value = cfg.nu / (ms_max * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded ray-cast urban scene, inputs.py)",
         "config": {"workload": f"{cfg.name}: {cfg.width}x{cfg.height} grid, {cfg.nu} persistent + {cfg.nu_b} birth "
                                f"particles, urban ray-cast scene", "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu,
