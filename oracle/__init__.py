@@ -93,7 +93,7 @@ def _declare(L):
     L.orc_step_exact.argtypes = [C.c_void_p, f32p, C.c_float]; L.orc_step_exact.restype = C.c_int
     L.orc_exact_cell.argtypes = [C.c_float] * 6 + [f32p, f32p]
     L.orc_doppler_g.argtypes = [C.c_float] * 6; L.orc_doppler_g.restype = C.c_float
-    L.orc_doppler_gfx.argtypes = [C.c_float]; L.orc_doppler_gfx.restype = C.c_uint32
+    L.orc_doppler_gfx.argtypes = [C.c_float, C.c_float]; L.orc_doppler_gfx.restype = C.c_uint32
     L.orc_doppler_Q.argtypes = [C.c_uint64, C.c_float, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32]
     L.orc_doppler_Q.restype = C.c_uint64
     L.orc_birth_assoc.argtypes = [C.c_uint64, C.c_uint32, C.c_float, u32p, u64p]
@@ -176,8 +176,8 @@ def doppler_g(vx, vy, ux, uy, vr, sd) -> float:
     return lib().orc_doppler_g(vx, vy, ux, uy, vr, sd)
 
 
-def doppler_gfx(g: float) -> int:
-    return lib().orc_doppler_gfx(g)
+def doppler_gfx(g: float, gmax: float) -> int:
+    return lib().orc_doppler_gfx(g, gmax)
 
 
 def doppler_Q(Rp: int, pA: float, GSj: int, GS: int, j: int, n: int) -> int:

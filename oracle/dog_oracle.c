@@ -154,13 +154,19 @@ float orc_doppler_g(float vx, float vy, float ux, float uy, float vr, float sd)
     return orc_exp_spec(q) / (sd * 2.50662827463100050f);
 }
 
-/* Fixed-point likelihood gfx = floor(min(g, 256 - 2^-16) 2^24) (u32, A-34): sums over a cell are
- * exact integers, so they do not depend on summation order. */
-uint32_t orc_doppler_gfx(float g)
+/* Fixed-point likelihood of a member relative to the largest likelihood g_max of its cell (A-34):
+ * gfx = floor((g / g_max) 2^31), f32 division then an exact power-of-two scale, so 0 <= gfx <= 2^31.
+ * mu_A in Eq. 72 makes the weights invariant to a common scale of g, so the fractions
+ * gfx_j / sum gfx are Eqs. 71-72's g_j / sum g up to a relative quantum of 2^-31 of the cell's largest
+ * member; the sums stay exact integers (order-free).  g_max = 0 (every member's g underflowed in f32)
+ * gives 0: the sum(w~) = 0 guard of SPEC S:253. */
+uint32_t orc_doppler_gfx(float g, float gmax)
 {
-    float gc = g < 0x1.fffffep+7f ? g : 0x1.fffffep+7f;
-    if (!(gc > 0.0f)) return 0u;
-    return (uint32_t)(gc * 16777216.0f);
+    const float big = 0x1.fffffep+127f;                    /* inf -> FLT_MAX so the ratio stays defined */
+    float gc = g < big ? g : big, mc = gmax < big ? gmax : big;
+    if (!(gc > 0.0f) || !(mc > 0.0f)) return 0u;
+    float r = gc / mc;                                     /* <= 1: gc <= mc */
+    return (uint32_t)(r * 2147483648.0f);
 }
 
 /* Cumulative weight fraction of member j of n in a Doppler cell (Eqs. 71-73 with p_A > 0, A-35):
@@ -510,8 +516,9 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
      *      O6 Moments (Alg. 6; Eqs. 81-84; A-18) ----
      * Cells without Doppler (p_A = 0, g = 1): every member has w = mu_Abar w_pred (Eq. 71).  Doppler
      * cells (p_A > 0, NEXT-1): w~ = g w_pred (Eq. 69) with g from orc_doppler_g, held as fixed-point
-     * gfx; the members' fixed-point weights are the differences of Q_j (orc_doppler_Q, A-35), and the
-     * moments weight each member by q_j / R_p.  Sum of gfx = 0 (no member compatible with the
+     * gfx relative to the cell's largest g (orc_doppler_gfx, A-34); the members' fixed-point weights
+     * are the differences of Q_j (orc_doppler_Q, A-35), and the moments weight each member by
+     * q_j / R_p.  Sum of gfx = 0 (no member compatible with the
      * measurement): the mu_A term is dropped -- the cell is treated as p_A = 0. */
     for (int64_t i = 0; i < nu; ++i) h->gfx[i] = 0u;
     for (int64_t c = 0; c < C; ++c) {
@@ -519,10 +526,16 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
         h->GS[c] = 0;
         if (!(dop && pA && pA[c] > 0.0f)) continue;
         const float* d = dop + 4 * c;
+        float gmax = 0.0f;                                     /* the cell's largest likelihood (A-34) */
+        for (uint32_t j = a; j < b; ++j) {
+            uint32_t i = h->perm[j];
+            float g = orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]);
+            if (g > gmax) gmax = g;
+        }
         uint64_t gs = 0;
         for (uint32_t j = a; j < b; ++j) {
             uint32_t i = h->perm[j];
-            h->gfx[i] = orc_doppler_gfx(orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]));
+            h->gfx[i] = orc_doppler_gfx(orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]), gmax);
             gs += h->gfx[i];
         }
         h->GS[c] = gs;

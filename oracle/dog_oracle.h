@@ -102,7 +102,7 @@ void orc_exact_cell(float S, float occ_max, float p_b, float occurred, float pTP
 /* NEXT-1 primitives (exported for the pins) */
 float    orc_exp_spec(float q);                                             /* e^q, q <= 0 (A-34) */
 float    orc_doppler_g(float vx, float vy, float ux, float uy, float vr, float sd);   /* Eq. 69 g */
-uint32_t orc_doppler_gfx(float g);                                          /* floor(g 2^24)      */
+uint32_t orc_doppler_gfx(float g, float gmax);                              /* floor(g/gmax 2^31) */
 uint64_t orc_doppler_Q(uint64_t Rp, float pA, uint64_t GSj, uint64_t GS, uint32_t j, uint32_t n);
 void     orc_birth_assoc(uint64_t Rb, uint32_t nb, float pA, uint32_t* nA, uint64_t* RbA);
 /* Ego-motion compensation (NEXT-2): scroll grid and particles by the whole-cell part of (dx, dy) plus the

@@ -42,11 +42,54 @@ def test_doppler_g_spec_examples():
 
 
 def test_gfx_fixed_point():
-    assert oracle.doppler_gfx(0.5) == 1 << 23
-    assert oracle.doppler_gfx(0.0) == 0
-    assert oracle.doppler_gfx(1000.0) == int(float.fromhex("0x1.fffffep+7") * 2 ** 24)
-    g = 0.123456
-    assert oracle.doppler_gfx(g) == math.floor(float(np.float32(g)) * 2 ** 24)
+    # A-34: gfx = floor((g / g_max) 2^31) in f32 -- the cell's most likely member holds exactly 2^31
+    assert oracle.doppler_gfx(0.5, 0.5) == 1 << 31
+    assert oracle.doppler_gfx(0.25, 0.5) == 1 << 30
+    assert oracle.doppler_gfx(0.0, 0.5) == 0
+    assert oracle.doppler_gfx(0.0, 0.0) == 0                    # every member underflowed: the guard
+    g, m = 0.123456, 0.987654
+    r = np.float32(np.float32(g) / np.float32(m))
+    assert oracle.doppler_gfx(g, m) == math.floor(float(r) * 2 ** 31)
+    # tiny likelihoods keep their relative precision (the old absolute 2^-24 quantum floored them to 0)
+    assert oracle.doppler_gfx(1e-30, 4e-30) == 1 << 29
+
+
+def test_weights_concentrate_on_the_nearest_member():
+    """Eqs. 71-72 with p_A = 1: each member's share of rho_p is g_j / sum g, however
+    small every g is.  Five members of one cell whose velocities sit 6..10 SD from the measured radial
+    speed: the nearest one (6 SD) must carry all but ~exp(-6.5) of the mass, and the cell's mean velocity
+    is the g-weighted mean computed here from the normal density in fp64 (an independent formulation)."""
+    w, h = 8, 8
+    sd = 0.25
+    t = np.array([6.0, 7.0, 8.0, 9.0, 10.0])
+    nu = 5
+    vx = (t * sd).astype(np.float32)                             # e = v . u - v_r with u = (1, 0), v_r = 0
+    x = np.full(nu, 3.5, np.float32); y = np.full(nu, 4.5, np.float32)
+    vy = np.zeros(nu, np.float32)
+    p = oracle.Params(width=w, height=h, nu=nu, nu_b=0, cell_size=0.1, seed=3, p_b=0.0,
+                      sigma_pos=0.0, sigma_vel=0.0, p_s=1.0)
+    o = oracle.Oracle(p)
+    o.set_state(x, y, vx, vy, np.float32(0.1), np.zeros(w * h, np.float32), 0)
+    C = w * h
+    meas = np.zeros((C, 2), np.float32)
+    cell = 4 * w + 3
+    meas[cell, 0] = 0.9
+    dop = np.zeros((C, 4), np.float32); dop[:, 0] = 1.0; dop[:, 3] = sd
+    pA = np.zeros(C, np.float32); pA[cell] = 1.0
+    o.step_doppler(meas, dop, pA, 1e-9)                          # dt -> 0: positions stay in the cell
+    # each member's predicted velocity (sigma_vel = 0: unchanged) and its normal density in fp64
+    pv = o.dump("PRED_VX").astype(np.float64)
+    g = np.exp(-0.5 * ((pv - 0.0) / sd) ** 2) / (sd * math.sqrt(2 * math.pi))
+    assert (g > 0).all() and g.max() < 1e-7                      # every g below the old 2^-24 quantum
+    share = g / g.sum()
+    gfx, GS = o.dump("GFX"), o.dump("GS")
+    assert int(GS[cell]) > 0                                     # not the sum(w~) = 0 guard
+    q = gfx.astype(np.float64) / float(GS[cell])
+    assert np.allclose(q, share, rtol=1e-6, atol=1e-9)
+    assert q[0] > 0.998
+    mean = o.read_cells()["mean"][cell]
+    ref = float((share * pv).sum())
+    assert abs(mean[0] - ref) < 1e-5 * abs(ref) and mean[0] < 1.6  # ~ the nearest member's 1.5 m/s
 
 
 def test_Q_end_points_monotone_and_closed_forms():
@@ -75,7 +118,7 @@ def test_Q_end_points_monotone_and_closed_forms():
 def test_spec_two_particle_weights():
     # w_pred {0.2, 0.2}, likelihoods {2, 0}, p_A = 1, rho_p = 0.3 -> w = {0.3, 0}
     Rp = math.floor(float(np.float32(0.3)) * 2 ** 40)
-    gfx = [oracle.doppler_gfx(2.0), oracle.doppler_gfx(0.0)]
+    gfx = [oracle.doppler_gfx(2.0, 2.0), oracle.doppler_gfx(0.0, 2.0)]
     GS = sum(gfx)
     Q = [oracle.doppler_Q(Rp, 1.0, g, GS, j, 2) for j, g in enumerate([0, gfx[0], GS])]
     assert (Q[1] - Q[0], Q[2] - Q[1]) == (Rp, 0)
