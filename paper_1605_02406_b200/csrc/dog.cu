@@ -101,7 +101,8 @@ struct dog_ctx {
     uint64_t* d_rs = nullptr;                     // per run slot: block prefix at the run's first member
     uint64_t* d_GS = nullptr;                     // per active-list entry: the cell's gfx total (0: none)
     uint8_t* d_tflag = nullptr;                   // per sort tile: holds members of a Doppler cell
-    uint32_t* d_gfx = nullptr;                    // per sorted position: fixed-point Doppler likelihood
+    uint32_t* d_gfx = nullptr;                    // per sorted position: g (f32 bits), then fixed-point gfx
+    uint32_t* d_gmax = nullptr;                   // per cell: the largest member likelihood (f32 bits, A-34)
     const float* band_dop = nullptr;              // band contexts: the cycle's Doppler grid (assign -> resample)
     const float* band_pA = nullptr;
     bool band_exact = false;                      // band contexts: this cycle runs the exact PHD/MIB update
@@ -456,6 +457,8 @@ int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, 
     return create_impl(grid, n_particles, n_birth, params, seed, flags, band, out);
 }
 
+static void free_doppler(dog_ctx* ctx);
+
 int dog_destroy(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
@@ -468,11 +471,7 @@ int dog_destroy(dog_ctx* ctx)
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->side) cudaStreamDestroy(ctx->side);
-    if (ctx->d_rg) cudaFree(ctx->d_rg);
-    if (ctx->d_rs) cudaFree(ctx->d_rs);
-    if (ctx->d_GS) cudaFree(ctx->d_GS);
-    if (ctx->d_tflag) cudaFree(ctx->d_tflag);
-    if (ctx->d_gfx) cudaFree(ctx->d_gfx);
+    free_doppler(ctx);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     free_all(ctx);
@@ -664,14 +663,38 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     return DOG_OK;
 }
 
-// Doppler working buffers, allocated on first use
+// Doppler working buffers, allocated on first use; a partial failure frees them all (the next call retries)
+static void free_doppler(dog_ctx* ctx)
+{
+    for (void** p : {(void**)&ctx->d_rg, (void**)&ctx->d_rs, (void**)&ctx->d_GS, (void**)&ctx->d_tflag,
+                     (void**)&ctx->d_gfx, (void**)&ctx->d_gmax}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+}
+
 static int alloc_doppler(dog_ctx* ctx)
 {
-    if (ctx->d_rg) return DOG_OK;
+    if (ctx->d_rg && ctx->d_rs && ctx->d_GS && ctx->d_tflag && ctx->d_gfx && ctx->d_gmax) return DOG_OK;
+    free_doppler(ctx);
     if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
         cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess ||
-        cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess)
+        cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess || cudaMalloc(&ctx->d_gmax, (size_t)ctx->C * 4) != cudaSuccess) {
+        free_doppler(ctx);
+        cudaGetLastError();
         return DOG_E_NOMEM;
+    }
+    return DOG_OK;
+}
+
+// the members' likelihoods g, the cell maxima g_max, then gfx relative to g_max summed per run (A-34)
+static int L_dopp_runs(dog_ctx* ctx, const DopIn& din, const FilterConst& fc, int par, cudaStream_t st)
+{
+    CK(cudaMemsetAsync(ctx->d_gmax, 0, (size_t)ctx->C * 4, st));
+    CK(launch(k_dopp_g, ctx->tiles, 256, 0, st, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst, din,
+              ctx->d_gmax, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
+    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, ctx->tp, din, (const uint32_t*)ctx->d_gmax, ctx->d_rg,
+              ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
     return DOG_OK;
 }
 
@@ -700,8 +723,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
         CK(cudaEventRecord(ctx->ev_fork, st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
     }
-    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, ds, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst,
-              din, ctx->d_rg, ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
+    if (int r = L_dopp_runs(ctx, din, fc, par, ds)) return r;
     if (fork) CK(cudaEventRecord(ctx->ev_join, ctx->side));
     if (int r = L_cells(ctx, meas, a, fc, st)) return r;
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
@@ -830,9 +852,7 @@ int dog_band_assign_doppler(dog_ctx* ctx, const float* meas_band, const float* d
     const StepArgs a = step_args(ctx, ctx->band_dt);
     const FilterConst fc = filter_const(ctx);
     const DopIn din{(const float4*)doppler_band, p_assoc_band};
-    CK(launch(k_dopp_runs, ctx->tiles, 256, 0, (cudaStream_t)stream, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-              (const float4*)ctx->pst, din, ctx->d_rg, ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc,
-              (int)(a.k & 1)));
+    if (int r = L_dopp_runs(ctx, din, fc, (int)(a.k & 1), (cudaStream_t)stream)) return r;
     ctx->band_dop = doppler_band;
     ctx->band_pA = p_assoc_band;
     return DOG_OK;

@@ -4,11 +4,13 @@
 //   * persistent members get w~ = g w_pred (Eq. 69) and w = p_A mu_A w~ + (1 - p_A) mu_Abar w_pred
 //     (Eqs. 71-73): member j of the cell owns [Q_j, Q_{j+1}) of the cell's fixed-point mass R_p with
 //     Q_j = floor(R_p G_j), G_j = fma(p_A, GS_j / GS, (1 - p_A) j / n) (A-35), GS_j the exclusive
-//     prefix of the fixed-point likelihoods gfx = floor(g 2^24) (A-34) in cell order;
+//     prefix of the fixed-point likelihoods gfx = floor((g / g_max) 2^31) (A-34) in cell order, g_max
+//     the cell's largest likelihood;
 //   * the cell's nu_b birth slots split into nu_A associated slots (velocity from p(x | z)) and
 //     nu_b - nu_A unassociated ones, sharing R_bA and R_b - R_bA (A-36).
 // Weights are no longer uniform within a cell, so the closed-form per-run resampling of
 // k_resample_tiles does not apply; this path uses
+//   k_dopp_g       per tile: g of every member, the cell maxima g_max (integer atomicMax: order-free)
 //   k_dopp_runs    per tile: gfx of every member, summed per run (integer atomics: order-free)
 //   k_pair_sort    (its Doppler branch) per active cell: the runs' gfx sums in tile order -> exclusive
 //                  prefixes, cell total GS, tile flags
@@ -54,16 +56,21 @@ __device__ __forceinline__ float exp_spec(float q)
     return __fmul_rn(y, __int_as_float((127 + k) << 23));
 }
 
-// Doppler likelihood g(z | x) of a predicted velocity (Eq. 69; A-34), fixed point
-__device__ __forceinline__ uint32_t doppler_gfx(float vx, float vy, float4 d)
+// Doppler likelihood g(z | x) of a predicted velocity (Eq. 69; A-34), f32
+__device__ __forceinline__ float doppler_g(float vx, float vy, float4 d)
 {
     const float e = __fsub_rn(__fmaf_rn(vx, d.x, __fmul_rn(vy, d.y)), d.z);
     const float t = __fdiv_rn(e, d.w);
     const float q = __fmul_rn(__fmul_rn(t, t), -0.5f);
     const float g = __fdiv_rn(exp_spec(q), __fmul_rn(d.w, 2.50662827463100050f));
-    const float gc = g < 0x1.fffffep+7f ? g : 0x1.fffffep+7f;
-    if (!(gc > 0.0f)) return 0u;
-    return __float2uint_rz(__fmul_rn(gc, 16777216.0f));
+    return g < 0x1.fffffep+127f ? g : 0x1.fffffep+127f;      // inf -> FLT_MAX; NaN stays NaN
+}
+
+// fixed point relative to the cell's largest likelihood: floor((g / g_max) 2^31) (A-34)
+__device__ __forceinline__ uint32_t doppler_gfx(float g, float gmax)
+{
+    if (!(g > 0.0f) || !(gmax > 0.0f)) return 0u;
+    return __float2uint_rz(__fmul_rn(__fdiv_rn(g, gmax), 2147483648.0f));
 }
 
 // Q_j = floor(R_p G_j) (A-35)
@@ -91,26 +98,22 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
     return lo;
 }
 
-// ---- k_dopp_runs: gfx of every member of a Doppler cell, summed per run (rg[run slot]).  Thread t takes
-//      sorted positions [16t, 16t+16) (one run search, then sequential), sums its run segments and adds
-//      each segment once (integer atomics: order-free).
-__global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ lperm, TilePairs tp,
-                                                   const float4* __restrict__ pred, DopIn din,
-                                                   uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
-                                                   uint32_t* __restrict__ gfx_out, const DevScalars* __restrict__ sc,
-                                                   FilterConst fc, int par)
+// ---- k_dopp_g: the likelihood g of every member of a Doppler cell (f32 bits per sorted position, in
+//      gfx_out) and the cell's largest g (gmax[cell], integer atomicMax on the bits of a nonnegative float:
+//      order-free).  gmax must be zero on entry (the caller clears it).
+__global__ __launch_bounds__(256) void k_dopp_g(const uint16_t* __restrict__ lperm, TilePairs tp,
+                                                const float4* __restrict__ pred, DopIn din,
+                                                uint32_t* __restrict__ gmax, uint32_t* __restrict__ gfx_out,
+                                                const DevScalars* __restrict__ sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
-    __shared__ __align__(16) uint16_t s_lp[kSortTile];
     const uint32_t t = blockIdx.x, base = t * kSortTile;
-    if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_pair_sort for Doppler tiles
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
-    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) { s_first[r] = tp.first[base + r]; rg[base + r] = 0ull; }
-    for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) s_lp[p] = lperm[base + p];
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) s_first[r] = tp.first[base + r];
     if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
     __syncthreads();
     const uint32_t p0 = threadIdx.x * 16u, p1 = min(p0 + 16u, n);
@@ -120,6 +123,54 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
     uint32_t key = tp.key[base + j];
     float pa = key < fc.C ? din.pA[key] : 0.0f;
     float4 d = pa > 0.0f ? din.dop[key] : make_float4(0.f, 0.f, 0.f, 1.f);
+    uint32_t mx = 0u;
+    for (uint32_t p = p0; p < p1; ++p) {
+        if (p >= end) {
+            if (mx) atomicMax(&gmax[key], mx);
+            mx = 0u;
+            ++j; end = s_first[j + 1];
+            key = tp.key[base + j];
+            pa = key < fc.C ? din.pA[key] : 0.0f;
+            if (pa > 0.0f) d = din.dop[key];
+        }
+        uint32_t gb = 0u;
+        if (pa > 0.0f) {
+            const float4 X = pred[pbase + lperm[base + p]];
+            const float g = doppler_g(X.z, X.w, d);
+            gb = g > 0.0f ? __float_as_uint(g) : 0u;            // NaN / 0 -> no weight
+            mx = max(mx, gb);
+        }
+        gfx_out[base + p] = gb;
+    }
+    if (mx) atomicMax(&gmax[key], mx);
+}
+
+// ---- k_dopp_runs: gfx = floor((g / g_max) 2^31) of every member of a Doppler cell, summed per run
+//      (rg[run slot]).  Thread t takes sorted positions [16t, 16t+16) (one run search, then sequential),
+//      sums its run segments and adds each segment once (integer atomics: order-free).  gfx_io holds g
+//      (k_dopp_g) on entry and gfx on exit.
+__global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, const uint32_t* __restrict__ gmax,
+                                                   uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
+                                                   uint32_t* __restrict__ gfx_io, const DevScalars* __restrict__ sc,
+                                                   FilterConst fc, int par)
+{
+    PDL_ENTER();
+    __shared__ uint16_t s_first[kSortTile + 1];
+    const uint32_t t = blockIdx.x, base = t * kSortTile;
+    if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_pair_sort for Doppler tiles
+    const uint32_t n = tile_count(sc, par, base);
+    if (n == 0) return;
+    const uint32_t nd = tp.nd[t];
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) { s_first[r] = tp.first[base + r]; rg[base + r] = 0ull; }
+    if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
+    __syncthreads();
+    const uint32_t p0 = threadIdx.x * 16u, p1 = min(p0 + 16u, n);
+    if (p0 >= n) return;
+    uint32_t j = run_of(s_first, nd, p0);
+    uint32_t end = s_first[j + 1];
+    uint32_t key = tp.key[base + j];
+    float pa = key < fc.C ? din.pA[key] : 0.0f;
+    float gm = pa > 0.0f ? __uint_as_float(gmax[key]) : 0.0f;
     uint64_t acc = 0;
     for (uint32_t p = p0; p < p1; ++p) {
         if (p >= end) {
@@ -128,15 +179,14 @@ __global__ __launch_bounds__(256) void k_dopp_runs(const uint16_t* __restrict__ 
             ++j; end = s_first[j + 1];
             key = tp.key[base + j];
             pa = key < fc.C ? din.pA[key] : 0.0f;
-            if (pa > 0.0f) d = din.dop[key];
+            if (pa > 0.0f) gm = __uint_as_float(gmax[key]);
         }
         uint32_t gf = 0u;
         if (pa > 0.0f) {
-            const float4 X = pred[pbase + s_lp[p]];
-            gf = doppler_gfx(X.z, X.w, d);
+            gf = doppler_gfx(__uint_as_float(gfx_io[base + p]), gm);
             acc += gf;
         }
-        gfx_out[base + p] = gf;                              // per sorted position, for k_resample_dopp
+        gfx_io[base + p] = gf;                               // per sorted position, for k_resample_dopp
     }
     if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
 }
