@@ -154,12 +154,13 @@ def test_doppler_full_size_cfgT_one_cycle():
 
 
 def test_doppler_incompatible_cells_fall_back():
-    """A radial-speed SD so small that almost every member's likelihood underflows to 0: those cells
-    take the GS = 0 guard (the mu_A term dropped, even split, A-35) -- bit-exact like the rest."""
+    """A radial-speed SD so small (1e-5 m/s) that every member of most cells is more than 13.2 SD away,
+    so its f32 likelihood underflows to 0 (A-34): those cells take the GS = 0 guard (the mu_A term
+    dropped, even split, A-35) -- bit-exact like the rest."""
     cfg = I.config("cfg1", nu=20_000, nu_b=2_000)
-    o, g = run(cfg, 4, plain=3, frac=1.0, p_assoc=1.0, sd=0.002)
+    o, g = run(cfg, 4, plain=3, frac=1.0, p_assoc=1.0, sd=1e-5)
     sc = I.scene(cfg)
-    _, pA = sc.doppler(6, sc.frame(6), frac=1.0, p_assoc=1.0, sd=0.002)   # the last cycle's overlay
+    _, pA = sc.doppler(6, sc.frame(6), frac=1.0, p_assoc=1.0, sd=1e-5)   # the last cycle's overlay
     off, gs = o.dump("OFFSETS"), o.dump("GS")
     members = np.diff(off.astype(np.int64)) > 0
     doppler_cells = (pA.numpy().reshape(-1) > 0) & members
