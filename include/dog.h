@@ -35,11 +35,11 @@ extern "C" {
 #endif
 
 #define DOG_OK        0
-#define DOG_E_INVAL  (-1) /* invalid argument: sizes <= 0, C >= 2^31-1, probabilities out of range,
+#define DOG_E_INVAL  (-1) /* invalid argument: sizes <= 0, C >= 2^24, probabilities out of range,
                              non-positive dt, NaN parameters, null pointers                        */
 #define DOG_E_NOMEM  (-2) /* device or pinned-host allocation failed                             */
 #define DOG_E_CUDA   (-3) /* a CUDA call failed; the context is poisoned (only dog_destroy)     */
-#define DOG_E_NCCL   (-4) /* an NCCL call failed; the context is poisoned                        */
+#define DOG_E_NCCL   (-4) /* reserved: the library's own exchanges are peer-memory copies, not NCCL */
 #define DOG_E_MEAS   (-5) /* a measurement cell was invalid (m_zO < 0, m_zF < 0, m_zO + m_zF >
                              1 + 2^-20, or NaN); such cells were treated as vacuous (0, 0).  Sticky
                              device flag, reported by the next synchronous call (dog_read_cells,
@@ -64,19 +64,56 @@ typedef struct {
     float v_max;           /* clamp of new-born |vx|,|vy| in m/s; <= 0 disables (A-16)         */
 } dog_params;
 
-/* dog_create -- allocate a filter on the current CUDA device in the empty initial state (A-19):
- * all nu particles at the sentinel position (-2^30 cells) with weight 0, m_F = 0, k = 0.
+/* dog_create -- allocate a filter in the empty initial state (A-19): all nu particles at the sentinel
+ * position (-2^30 cells) with weight 0, m_F = 0, k = 0.
  *   grid, params : validated copies are kept (DOG_E_INVAL on violation; width, height <= 65535 and
- *                  width * height < 2^24).
- *   n_particles  : nu >= 1, persistent particles per cycle (< 2^31).
- *   n_birth      : nu_b >= 0, new-born particles per cycle ("remains constant").
+ *                  width * height < 2^24, which keeps every fixed-point total below 2^64, A-23).
+ *   n_particles  : nu, 1 <= nu < 2^30, persistent particles per cycle.
+ *   n_birth      : nu_b, 0 <= nu_b < 2^30, new-born particles per cycle ("remains constant").
  *   seed         : Philox key (low 32 bits, high 32 bits).
- *   flags        : DOG_FLAG_DEBUG keeps per-stage device arrays for dog_get_debug (parity tests);
- *                  0 for production (no extra traffic).
- *   out          : receives the context; the context owns every device allocation it makes. */
+ *   flags        : DOG_FLAG_DEBUG keeps per-stage device arrays for dog_get_debug (parity tests; whole-grid
+ *                  contexts only); 0 for production (no extra traffic).
+ *   n_devices, device_ids : 0 / NULL = one whole-grid context on the current device; 1 = on device_ids[0];
+ *                  n >= 2 (<= 16, <= height) = a SHARDED context: the grid is cut into n row bands of
+ *                  near-equal height (bottom-up), band s on device_ids[s] (ids may repeat: several bands on
+ *                  one GPU).  Peer access is enabled between distinct devices (DOG_E_INVAL if the GPUs
+ *                  cannot reach each other's memory).  Each band can hold all nu particles, so migration
+ *                  cannot overflow and the owner-bucketed exchange reaches any band (no particle is lost).
+ *                  A sharded context runs dog_step / dog_step_sharded / dog_read_cells(_sharded) /
+ *                  dog_get_state / dog_set_state / dog_set_bands / dog_sync / dog_destroy; every other call
+ *                  returns DOG_E_STATE.
+ *   out          : receives the context; the context owns every device allocation it makes.
+ * The caller's current device is unchanged on return. */
 #define DOG_FLAG_DEBUG 1u
 int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
-               uint64_t seed, uint32_t flags, dog_ctx** out);
+               uint64_t seed, uint32_t flags, int n_devices, const int* device_ids, dog_ctx** out);
+
+/* ---- sharded contexts (multi-GPU) ----
+ * dog_step_sharded -- one filter cycle on every band.  meas_band[s]: DEVICE pointer on device_ids[s] (or
+ * peer-readable from it), float[rows of band s][width][2]; streams[s]: a cudaStream_t on device_ids[s].
+ * Stream-ordered and asynchronous, with NO host synchronisation inside the cycle: the three couplings
+ * of the bands (migrants after predict, born-mass totals for Alg. 5, joint-weight totals for Alg. 7)
+ * move device to device over peer memory (NVLink), ordered by CUDA events between the streams.  The
+ * union of the bands reproduces the whole-grid cycle bit for bit (Philox counters use global indices).
+ * A failure mid-cycle poisons the context.
+ * dog_step on a sharded context takes the whole-grid meas on device_ids[0] (read by every band over peer
+ * memory) and a stream on device_ids[0]: the bands run on the context's own streams, forked from and
+ * joined back into `stream`. */
+int dog_step_sharded(dog_ctx* ctx, const float* const* meas_band, float dt, void* const* streams);
+/* dog_read_cells_sharded -- each band's readouts into per-band DEVICE buffers on its device (any array
+ * may be NULL; otherwise world entries, each possibly NULL).  Synchronises each band's stream.
+ * dog_read_cells on a sharded context writes whole-grid buffers on device_ids[0] (peer copies). */
+int dog_read_cells_sharded(dog_ctx* ctx, float* const* occ, float* const* free_mass, float* const* vel_mean,
+                           float* const* vel_cov, void* const* streams);
+/* dog_set_bands -- synchronous, between cycles (band rebalancing): move the band
+ * boundaries to rows[0..world] (rows[0] = 0 < rows[1] < ... < rows[world] = height; any band height).
+ * The state is carried over exactly (the global particle order does not change). */
+int dog_set_bands(dog_ctx* ctx, const int32_t* rows);
+/* dog_get_bands -- rows[world + 1] band bounds and (if devices != NULL) devices[world]; returns world
+ * (1 for a whole-grid context). */
+int dog_get_bands(dog_ctx* ctx, int32_t* rows, int* devices);
+/* dog_world -- number of bands (1 for a whole-grid context). */
+int dog_world(dog_ctx* ctx);
 
 /* dog_step -- run one filter cycle.
  *   meas   : DEVICE pointer (same device as the context), float[height][width][2] =
@@ -99,41 +136,56 @@ int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_hos
  * contexts only. */
 int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream);
 
-/* ---- row-band contexts (multi-GPU) ----
+/* ---- row-band contexts: the band phases for callers that move the data themselves (one process per
+ * GPU with a transport such as NCCL; paper_1605_02406_b200/shard.py).  A sharded context (above) drives
+ * exactly these phases itself. ----
  * The grid is split into horizontal bands of rows, one context (and one GPU) per band.  A band context
  * owns its cells (m_F, readouts; the caller passes the band's measurement rows) and the particles whose
- * cell lies in the band.  The coupling between bands is exactly (i) particles that move into the band
- * above or below during predict, (ii) the born-mass prefix of the bands below for the slot
- * allocation (Alg. 5, A-15) and (iii) the joint-weight prefix for systematic resampling (Alg. 7, A-24).
- * The cycle is therefore split into phases; between them the CALLER moves data between the contexts
- * (NCCL send/recv and all-gathers in paper_1605_02406_b200/shard.py).  Philox counters use global
- * particle / slot indices, so the union of the bands reproduces the whole-grid filter bit for bit.
+ * cell lies in the band.  The coupling between bands is exactly (i) particles that move into another
+ * band during predict, (ii) the born-mass prefix of the bands below for the slot allocation
+ * (Alg. 5, A-15) and (iii) the joint-weight prefix for systematic resampling (Alg. 7, A-24).  Philox
+ * counters use global particle / slot indices, so the union of the bands reproduces the whole-grid
+ * filter bit for bit.
  *   dog_band.row0/row1      : rows [row0, row1) of this band; rank/world: band index and count (bands
  *                             ordered bottom-up; rank 0 starts at row 0, the last ends at height).
- *   dog_band.lo_row0/hi_row1: first row of the band below / end row of the band above (one-hop reach;
- *                             particles predicted beyond it are counted in n_far and dropped).
- *   dog_band.migrant_cap    : capacity, in particles, for migrants per direction per cycle.
- * Call order per cycle: predict -> sizes -> buffers (+ caller's send/recv of the migrant records,
- * 16 bytes (x, y, vx, vy) each, in the order given) -> assign -> (caller all-gathers *mass_dev over the
- * bands into mass_all[world], device) -> joint -> (all-gather *weight_dev into weight_all[world]) ->
- * resample.  Out-of-order calls return DOG_E_STATE.  Band contexts have no debug dumps (flags must be
- * 0) and do not accept dog_step / dog_get_state particle arrays; m_F and readouts work as usual on
- * the band's cells. */
+ *   dog_band.lo_row0/hi_row1: first row of the band below / end row of the band above: migrants are
+ *                             packed into four buckets -- to the band below, above, further below,
+ *                             further above (owner-bucketed: no displacement is too large).
+ *   dog_band.migrant_cap    : capacity, in particles, per bucket sent and per side received (< 2^26).
+ * Call order per cycle: predict -> gather (the caller passes the neighbours' buckets, device pointers)
+ * -> assign -> (caller all-gathers *mass_dev over the bands into mass_all[world], device) -> joint ->
+ * (all-gather *weight_dev into weight_all[world]) -> resample.  Out-of-order calls return DOG_E_STATE.
+ * Band contexts have no debug dumps (flags must be 0) and do not accept dog_step / dog_get_state
+ * particle arrays; m_F and readouts work as usual on the band's cells.  A bucket or receive beyond
+ * migrant_cap raises a device flag: the next dog_band_sizes / dog_sync / dog_read_cells returns
+ * DOG_E_NOMEM and poisons the context (the cycle could not be completed exactly). */
 typedef struct {
     int32_t row0, row1, rank, world, lo_row0, hi_row1;
     uint32_t migrant_cap;
 } dog_band;
 int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
                     uint64_t seed, uint32_t flags, const dog_band* band, dog_ctx** out);
-/* phase 1: Alg. 1 for the own particles; migrants packed (device) for the neighbours. */
+/* phase 1: Alg. 1 for the own particles; migrants packed (device) into the four buckets. */
 int dog_band_predict(dog_ctx* ctx, float dt, void* stream);
-/* synchronises `stream`; migrant counts down/up, own particles of this cycle, far migrants so far.
- * DOG_E_NOMEM if a direction overflowed migrant_cap (the cycle cannot be completed exactly). */
-int dog_band_sizes(dog_ctx* ctx, uint32_t* n_down, uint32_t* n_up, uint32_t* n_own, uint32_t* n_far, void* stream);
-/* device buffers: packed migrants to send down / up (float4 records, counts from dog_band_sizes) and
- * where the n_lo / n_hi records received from the band below / above must be written (before assign). */
-int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** send_down, const float** send_up,
-                     float** recv_lo, float** recv_hi, void* stream);
+/* this band's four packed buckets (DEVICE float4 records (x, y, vx, vy) in global index order:
+ * 0 below, 1 above, 2 further below, 3 further above) and their DEVICE u32 counts; valid once the
+ * predict phase has run on its stream, until the next predict.  No synchronisation. */
+int dog_band_outbox(dog_ctx* ctx, const float** rec, const uint32_t** cnt);
+/* synchronises `stream` (after predict): the four bucket counts (host counts[4]) and the own particles of
+ * this cycle -- for transports that must size their messages on the host. */
+int dog_band_sizes(dog_ctx* ctx, uint32_t* counts, uint32_t* n_own, void* stream);
+/* phase 1b (stream-ordered, no sync): assemble [from below | own | from above] from the other bands'
+ * buckets -- DEVICE pointers readable from this band's device (its own memory, a peer GPU's, or a
+ * transport's receive buffer) with DEVICE u32 counts:
+ *   lo_near (+cnt): bucket 1 of band rank-1 (NULL for rank 0);  hi_near: bucket 0 of band rank+1 (NULL for
+ *   the last band);  lo_far[n_lo_far = max(0, rank-1)]: bucket 3 of bands 0 .. rank-2 in band order;
+ *   hi_far[n_hi_far = max(0, world-rank-2)]: bucket 2 of bands rank+2 .. world-1 in band order.
+ * The far buckets are filtered to this band's rows (stable), so the local array stays in global index
+ * order.  DOG_E_INVAL for a NULL / count mismatch. */
+int dog_band_gather(dog_ctx* ctx, const float* lo_near, const uint32_t* lo_near_cnt, const float* hi_near,
+                    const uint32_t* hi_near_cnt, int n_lo_far, const float* const* lo_far,
+                    const uint32_t* const* lo_far_cnt, int n_hi_far, const float* const* hi_far,
+                    const uint32_t* const* hi_far_cnt, void* stream);
 /* phase 2: tile sort of [from below | own | from above], Alg. 3 on the band; *mass_dev = this band's
  * fixed-point born mass (device u64) to all-gather. */
 int dog_band_assign(dog_ctx* ctx, const float* meas_band, const uint64_t** mass_dev, void* stream);

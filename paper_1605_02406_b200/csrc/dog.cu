@@ -51,7 +51,6 @@ struct dog_ctx {
     Migrants mg{};              // band contexts: migrants packed for the neighbours
     int phase = 0;              // band cycle: 0 idle, 1 predicted, 2 sizes read, 3 assigned, 4 joint
     float band_dt = 0.0f;
-    uint32_t n_own_host = 0;
 
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
@@ -115,6 +114,16 @@ struct dog_ctx {
     int prof_max = 0, prof_steps = 0, prof_nst = 0;
     const char* stage_names[DOG_MAX_STAGES] = {};
 
+    // sharded parent (dog_create with n_devices >= 2): one row-band context per device; the parent holds
+    // no particles itself and drives the bands' phases with device-side exchanges (no host sync)
+    std::vector<dog_ctx*> shards;
+    std::vector<int> shard_dev;
+    std::vector<int32_t> shard_rows;              // world + 1 row bounds, bottom-up
+    std::vector<cudaStream_t> shard_st;           // internal streams (dog_step on the parent)
+    std::vector<cudaEvent_t> sev_pred, sev_asg, sev_jnt, sev_done;
+    std::vector<uint64_t*> sh_mass, sh_weight;    // per band, on its device: the all-gathered u64 totals
+    cudaEvent_t ev_caller = nullptr;              // on device_ids[0]: the caller's stream -> band streams
+
     std::vector<void*> allocs;
 };
 
@@ -131,6 +140,11 @@ int fail(dog_ctx* c, cudaError_t e, const char* what)
     do {                                                      \
         cudaError_t _e = (call);                              \
         if (_e != cudaSuccess) return fail(ctx, _e, #call);   \
+    } while (0)
+#define CK2(c, call)                                          \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return fail((c), _e, #call);   \
     } while (0)
 
 template <typename T>
@@ -229,16 +243,24 @@ FilterConst filter_const(const dog_ctx* ctx)
 
 int set_device(dog_ctx* ctx)
 {
+    if (!ctx->shards.empty()) return DOG_E_STATE;   // a sharded parent: only the dog_*_sharded / state calls
     int cur = -1;
     cudaGetDevice(&cur);
     if (cur != ctx->device) CK(cudaSetDevice(ctx->device));
     return DOG_OK;
 }
 
+// deferred device-side conditions: a migrant receive beyond capacity (the cycle could not complete
+// exactly: the context is poisoned, DOG_E_NOMEM), then invalid measurement cells (DOG_E_MEAS, cleared)
 int report_meas(dog_ctx* ctx)
 {
-    uint32_t bad = 0;
+    uint32_t bad = 0, over = 0;
     CK(cudaMemcpy(&bad, &ctx->sc->meas_bad, 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&over, &ctx->sc->mig_over, 4, cudaMemcpyDeviceToHost));
+    if (over) {
+        ctx->poisoned = true;
+        return DOG_E_NOMEM;
+    }
     if (bad) {
         CK(cudaMemset(&ctx->sc->meas_bad, 0, 4));
         return DOG_E_MEAS;
@@ -394,7 +416,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     AL(ctx->ws.pJ, ctx->cell_blocks); AL(ctx->ws.pit, ctx->cell_blocks);
 
     if (ctx->world > 1) {
-        for (int d = 0; d < 2; ++d) {
+        for (int d = 0; d < kMigDirs; ++d) {
             AL(ctx->mg.scr[d], ctx->own_cap); AL(ctx->mg.cnt[d], ctx->own_tiles); AL(ctx->mg.send[d], ctx->lo_cap);
         }
         ctx->mg.cap = ctx->lo_cap;
@@ -443,10 +465,24 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     return DOG_OK;
 }
 
+static int create_sharded(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+                          uint64_t seed, uint32_t flags, int n_devices, const int* device_ids, dog_ctx** out);
+
 int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
-               uint64_t seed, uint32_t flags, dog_ctx** out)
+               uint64_t seed, uint32_t flags, int n_devices, const int* device_ids, dog_ctx** out)
 {
-    return create_impl(grid, n_particles, n_birth, params, seed, flags, nullptr, out);
+    if (!out || n_devices < 0 || (n_devices > 0 && !device_ids)) return DOG_E_INVAL;
+    if (n_devices >= 2)
+        return create_sharded(grid, n_particles, n_birth, params, seed, flags, n_devices, device_ids, out);
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (n_devices == 1 && cudaSetDevice(device_ids[0]) != cudaSuccess) {
+        cudaGetLastError();
+        return DOG_E_INVAL;
+    }
+    const int rc = create_impl(grid, n_particles, n_birth, params, seed, flags, nullptr, out);
+    if (prev >= 0) cudaSetDevice(prev);
+    return rc;
 }
 
 int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
@@ -459,9 +495,12 @@ int dog_create_band(const dog_grid* grid, int64_t n_particles, int64_t n_birth, 
 
 static void free_doppler(dog_ctx* ctx);
 
+static int destroy_sharded(dog_ctx* ctx);
+
 int dog_destroy(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return destroy_sharded(ctx);
     set_device(ctx);
     cudaDeviceSynchronize();
     for (cudaEvent_t e : ctx->pev) cudaEventDestroy(e);
@@ -482,6 +521,7 @@ int dog_destroy(dog_ctx* ctx)
 int dog_launches_per_step(dog_ctx* ctx)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return DOG_E_STATE;
     // predict_sort, cells, list_scan, pair_fill, pair_sort, resample_tiles, moments, births
     return ctx->nu_b > 0 ? 8 : 7;
 }
@@ -592,9 +632,12 @@ static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cuda
 
 static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt, void* stream);
 
+static int step_parent(dog_ctx* ctx, const float* meas, float dt, void* stream);
+
 int dog_step(dog_ctx* ctx, const float* meas, float dt, void* stream)
 {
     if (!meas) return DOG_E_INVAL;
+    if (ctx && !ctx->shards.empty()) return step_parent(ctx, meas, dt, stream);
     return step_impl(ctx, meas, nullptr, dt, stream);
 }
 
@@ -769,40 +812,65 @@ int dog_band_predict(dog_ctx* ctx, float dt, void* stream)
     return DOG_OK;
 }
 
-int dog_band_sizes(dog_ctx* ctx, uint32_t* n_down, uint32_t* n_up, uint32_t* n_own, uint32_t* n_far, void* stream)
+int dog_band_sizes(dog_ctx* ctx, uint32_t* counts, uint32_t* n_own, void* stream)
 {
-    if (!ctx || !n_down || !n_up || !n_own) return DOG_E_INVAL;
+    if (!ctx || !counts || !n_own) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
-    if (ctx->phase != 1) return DOG_E_STATE;
+    if (ctx->world < 2 || (ctx->phase != 1 && ctx->phase != 2)) return DOG_E_STATE;
     if (int r = set_device(ctx)) return r;
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     DevScalars s;
     CK(cudaMemcpy(&s, ctx->sc, sizeof(s), cudaMemcpyDeviceToHost));
-    *n_down = s.mig_cnt[0];
-    *n_up = s.mig_cnt[1];
+    for (int d = 0; d < kMigDirs; ++d) counts[d] = s.mig_cnt[d];
     *n_own = s.n_own[ctx->k & 1];
-    if (n_far) *n_far = s.far;
-    ctx->n_own_host = *n_own;
-    ctx->phase = 2;
-    if (s.mig_cnt[0] > ctx->mg.cap || s.mig_cnt[1] > ctx->mg.cap) return DOG_E_NOMEM;   // migrant capacity
+    if (s.mig_over) {   // a bucket overflowed migrant_cap: the cycle cannot be completed exactly
+        ctx->poisoned = true;
+        return DOG_E_NOMEM;
+    }
     return DOG_OK;
 }
 
-int dog_band_buffers(dog_ctx* ctx, uint32_t n_lo, uint32_t n_hi, const float** send_down, const float** send_up,
-                     float** recv_lo, float** recv_hi, void* stream)
+int dog_band_outbox(dog_ctx* ctx, const float** rec, const uint32_t** cnt)
 {
-    if (!ctx || !send_down || !send_up || !recv_lo || !recv_hi) return DOG_E_INVAL;
-    if (ctx->phase != 2) return DOG_E_STATE;
-    if (n_lo > ctx->lo_cap || n_hi > ctx->hi_cap || (ctx->rank == 0 && n_lo) || (ctx->rank == ctx->world - 1 && n_hi))
+    if (!ctx || !rec || !cnt) return DOG_E_INVAL;
+    if (ctx->world < 2 || !ctx->shards.empty()) return DOG_E_STATE;
+    for (int d = 0; d < kMigDirs; ++d) {
+        rec[d] = (const float*)ctx->mg.send[d];
+        cnt[d] = &ctx->sc->mig_cnt[d];
+    }
+    return DOG_OK;
+}
+
+int dog_band_gather(dog_ctx* ctx, const float* lo_near, const uint32_t* lo_near_cnt, const float* hi_near,
+                    const uint32_t* hi_near_cnt, int n_lo_far, const float* const* lo_far,
+                    const uint32_t* const* lo_far_cnt, int n_hi_far, const float* const* hi_far,
+                    const uint32_t* const* hi_far_cnt, void* stream)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world < 2 || ctx->phase != 1) return DOG_E_STATE;
+    const int r = ctx->rank, w = ctx->world;
+    if ((r > 0) != (lo_near != nullptr) || (r > 0 && !lo_near_cnt) || (r < w - 1) != (hi_near != nullptr) ||
+        (r < w - 1 && !hi_near_cnt) || n_lo_far != std::max(0, r - 1) || n_hi_far != std::max(0, w - r - 2) ||
+        (n_lo_far && (!lo_far || !lo_far_cnt)) || (n_hi_far && (!hi_far || !hi_far_cnt)))
         return DOG_E_INVAL;
-    if (int r = set_device(ctx)) return r;
-    const uint32_t nn[2] = {n_lo, n_hi};
-    CK(cudaMemcpyAsync(&ctx->sc->n_lo, nn, sizeof(nn), cudaMemcpyHostToDevice, (cudaStream_t)stream));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));   // nn lives on this stack frame
-    *send_down = (const float*)ctx->mg.send[0];
-    *send_up = (const float*)ctx->mg.send[1];
-    *recv_lo = (float*)(ctx->pst + ctx->lo_cap - n_lo);
-    *recv_hi = (float*)(ctx->pst + ctx->lo_cap + ctx->n_own_host);
+    MigGather g{};
+    g.lo_near = MigSrc{(const float4*)lo_near, lo_near_cnt};
+    g.hi_near = MigSrc{(const float4*)hi_near, hi_near_cnt};
+    g.n_lo_far = n_lo_far;
+    g.n_hi_far = n_hi_far;
+    for (int i = 0; i < n_lo_far; ++i) {
+        if (!lo_far[i] || !lo_far_cnt[i]) return DOG_E_INVAL;
+        g.lo_far[i] = MigSrc{(const float4*)lo_far[i], lo_far_cnt[i]};
+    }
+    for (int i = 0; i < n_hi_far; ++i) {
+        if (!hi_far[i] || !hi_far_cnt[i]) return DOG_E_INVAL;
+        g.hi_far[i] = MigSrc{(const float4*)hi_far[i], hi_far_cnt[i]};
+    }
+    if (int rc = set_device(ctx)) return rc;
+    CK(launch(k_gather_migrants, 1 + 2 * 148, 1024, 0, (cudaStream_t)stream, 0, g, ctx->pst, ctx->sc,
+              filter_const(ctx), ctx->own_cap + ctx->hi_cap, (int)(ctx->k & 1)));
+    ctx->phase = 2;
     return DOG_OK;
 }
 
@@ -925,7 +993,8 @@ int dog_band_particles(dog_ctx* ctx, float* xyvv_host, uint64_t cap, uint32_t* n
         if (cap < *n_own) return DOG_E_INVAL;
         if (*n_own) CK(cudaMemcpy(xyvv_host, ctx->st + ctx->lo_cap, (size_t)*n_own * 16, cudaMemcpyDeviceToHost));
     }
-    return report_meas(ctx);
+    return DOG_OK;   // measurement flags are reported by dog_read_cells / dog_sync (not here: rebalancing
+                     // calls this on every band and must not fail on one of them alone)
 }
 
 int dog_band_set_state(dog_ctx* ctx, const float* xyvv_host, uint32_t n_own, uint64_t global_first,
@@ -950,7 +1019,6 @@ int dog_band_set_state(dog_ctx* ctx, const float* xyvv_host, uint32_t n_own, uin
     s.n_lo = 0; s.n_hi = 0;
     CK(cudaMemcpy(ctx->sc, &s, sizeof(s), cudaMemcpyHostToDevice));
     ctx->k = k;
-    ctx->n_own_host = n_own;
     return DOG_OK;
 }
 
@@ -1158,9 +1226,17 @@ int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry)
     return DOG_OK;
 }
 
+static int sync_sharded(dog_ctx* ctx, void* stream);
+static int read_cells_parent(dog_ctx* ctx, float* occ, float* free_mass, float* vel_mean, float* vel_cov, void* stream);
+static int get_state_sharded(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float* w_bar, float* m_free,
+                             int64_t* k);
+static int set_state_sharded(dog_ctx* ctx, const float* x, const float* y, const float* vx, const float* vy,
+                             float w_bar, const float* m_free, int64_t k);
+
 int dog_sync(dog_ctx* ctx, void* stream)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return sync_sharded(ctx, stream);
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -1172,6 +1248,7 @@ int dog_sync(dog_ctx* ctx, void* stream)
 int dog_read_cells(dog_ctx* ctx, float* occ, float* free_mass, float* vel_mean, float* vel_cov, void* stream)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return read_cells_parent(ctx, occ, free_mass, vel_mean, vel_cov, stream);
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
     cudaStream_t st = (cudaStream_t)stream;
@@ -1188,6 +1265,7 @@ int dog_get_state(dog_ctx* ctx, float* x, float* y, float* vx, float* vy, float*
                   int64_t* k)
 {
     if (!ctx) return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return get_state_sharded(ctx, x, y, vx, vy, w_bar, m_free, k);
     if (ctx->world > 1 && (x || y || vx || vy)) return DOG_E_STATE;   // band particles: dog_band_particles
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
@@ -1206,6 +1284,7 @@ int dog_set_state(dog_ctx* ctx, const float* x, const float* y, const float* vx,
 {
     if (!ctx || !x || !y || !vx || !vy || !m_free || !(w_bar >= 0.0f) || !finite(w_bar) || k < 0)
         return DOG_E_INVAL;
+    if (!ctx->shards.empty()) return set_state_sharded(ctx, x, y, vx, vy, w_bar, m_free, k);
     if (ctx->world > 1) return DOG_E_STATE;
     if (ctx->poisoned) return DOG_E_CUDA;
     if (int r = set_device(ctx)) return r;
@@ -1325,6 +1404,457 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
     if (bytes < n) return DOG_E_INVAL;
     if (n) CK(cudaMemcpy(host_dst, src, n, cudaMemcpyDeviceToHost));
     return (int64_t)n;
+}
+
+
+// ================================================================================================
+// Sharded parent context: dog_create with n_devices >= 2 makes one
+// row-band context per device (bottom-up bands of near-equal height).  dog_step_sharded runs the four
+// band phases on every device and moves what the bands couple ENTIRELY ON THE DEVICES, ordered only by
+// CUDA events: (1) the receivers' k_gather_migrants read the senders' packed migrant buckets and their
+// device counts over peer memory (NVLink; the same memory when bands share a device), (2)/(3) a
+// one-warp k_gather_u64 reads every band's born-mass / joint-weight total.  No host synchronisation
+// inside a cycle.  Every band can hold all nu particles in each of its three regions (migrant_cap = nu),
+// so a receive cannot overflow, and the owner-bucketed migration reaches any band: no particle is lost.
+// ================================================================================================
+struct U64Gather {
+    const uint64_t* p[kMaxBands];
+    int n;
+};
+
+__global__ void k_gather_u64(U64Gather g, uint64_t* __restrict__ out)
+{
+    PDL_ENTER();
+    if ((int)threadIdx.x < g.n) out[threadIdx.x] = *g.p[threadIdx.x];
+}
+
+namespace {
+
+struct DevGuard {   // restores the caller's current device
+    int prev = -1;
+    DevGuard() { cudaGetDevice(&prev); }
+    ~DevGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+void destroy_shards(dog_ctx* P)
+{
+    for (size_t s = 0; s < P->shards.size(); ++s) {
+        cudaSetDevice(P->shard_dev[s]);
+        cudaDeviceSynchronize();
+        for (auto* v : {&P->sev_pred, &P->sev_asg, &P->sev_jnt, &P->sev_done})
+            if (s < v->size() && (*v)[s]) cudaEventDestroy((*v)[s]);
+        if (s < P->shard_st.size() && P->shard_st[s]) cudaStreamDestroy(P->shard_st[s]);
+        if (P->shards[s]) dog_destroy(P->shards[s]);
+    }
+    P->shards.clear();
+    P->shard_st.clear();
+    P->sev_pred.clear(); P->sev_asg.clear(); P->sev_jnt.clear(); P->sev_done.clear();
+    P->sh_mass.clear(); P->sh_weight.clear();
+}
+
+// (re)create the band contexts of a parent on rows[0..world] (validated by the caller)
+int make_shards(dog_ctx* P, const std::vector<int32_t>& rows)
+{
+    const int w = (int)P->shard_dev.size();
+    P->shard_rows = rows;
+    P->shards.assign(w, nullptr);
+    P->shard_st.assign(w, nullptr);
+    P->sev_pred.assign(w, nullptr); P->sev_asg.assign(w, nullptr); P->sev_jnt.assign(w, nullptr);
+    P->sev_done.assign(w, nullptr);
+    P->sh_mass.assign(w, nullptr); P->sh_weight.assign(w, nullptr);
+    const uint32_t cap = (uint32_t)std::min<int64_t>(P->nu, (1 << 26) - 1);
+    for (int s = 0; s < w; ++s) {
+        if (cudaSetDevice(P->shard_dev[s]) != cudaSuccess) { cudaGetLastError(); return DOG_E_INVAL; }
+        dog_band b{rows[s], rows[s + 1], s, w, s > 0 ? rows[s - 1] : rows[s], s < w - 1 ? rows[s + 2] : rows[s + 1], cap};
+        if (int rc = create_impl(&P->grid, P->nu, P->nu_b, &P->params, P->seed, 0, &b, &P->shards[s])) return rc;
+        dog_ctx* S = P->shards[s];
+        int rc = dalloc(S, &P->sh_mass[s], (size_t)w);
+        if (rc == DOG_OK) rc = dalloc(S, &P->sh_weight[s], (size_t)w);
+        if (rc) return rc;
+        for (auto* v : {&P->sev_pred, &P->sev_asg, &P->sev_jnt, &P->sev_done})
+            if (cudaEventCreateWithFlags(&(*v)[s], cudaEventDisableTiming) != cudaSuccess) return fail(P, cudaGetLastError(), "cudaEventCreate");
+        if (cudaStreamCreateWithFlags(&P->shard_st[s], cudaStreamNonBlocking) != cudaSuccess)
+            return fail(P, cudaGetLastError(), "cudaStreamCreate");
+    }
+    return DOG_OK;
+}
+
+std::vector<int32_t> even_rows(int32_t H, int w)
+{
+    std::vector<int32_t> r(w + 1, 0);
+    const int32_t base = H / w, extra = H % w;
+    for (int s = 0; s < w; ++s) r[s + 1] = r[s] + base + (s < extra ? 1 : 0);
+    return r;
+}
+
+bool rows_valid(const int32_t* rows, int w, int32_t H)
+{
+    if (rows[0] != 0 || rows[w] != H) return false;
+    for (int s = 0; s < w; ++s)
+        if (rows[s + 1] <= rows[s]) return false;
+    return true;
+}
+
+// one band of the cycle: phase `ph` (0 predict, 1 gather + assign, 2 totals + joint, 3 totals + resample)
+int shard_phase(dog_ctx* P, int s, int ph, const float* meas_band, float dt, cudaStream_t st)
+{
+    dog_ctx* S = P->shards[s];
+    const int w = (int)P->shards.size();
+    if (cudaSetDevice(P->shard_dev[s]) != cudaSuccess) return fail(P, cudaGetLastError(), "cudaSetDevice");
+    auto wait_all = [&](std::vector<cudaEvent_t>& ev) -> int {
+        for (int t = 0; t < w; ++t)
+            if (t != s) CK2(P, cudaStreamWaitEvent(st, ev[t], 0));
+        return DOG_OK;
+    };
+    int rc = DOG_OK;
+    switch (ph) {
+    case 0:
+        rc = dog_band_predict(S, dt, st);
+        if (!rc) CK2(P, cudaEventRecord(P->sev_pred[s], st));
+        return rc;
+    case 1: {
+        if (int r = wait_all(P->sev_pred)) return r;
+        const float* rec[kMaxBands][kMigDirs];
+        const uint32_t* cnt[kMaxBands][kMigDirs];
+        for (int t = 0; t < w; ++t) dog_band_outbox(P->shards[t], rec[t], cnt[t]);
+        const float* lof[kMaxBands]; const uint32_t* lofc[kMaxBands];
+        const float* hif[kMaxBands]; const uint32_t* hifc[kMaxBands];
+        int nl = 0, nh = 0;
+        for (int t = 0; t < s - 1; ++t) { lof[nl] = rec[t][3]; lofc[nl++] = cnt[t][3]; }
+        for (int t = s + 2; t < w; ++t) { hif[nh] = rec[t][2]; hifc[nh++] = cnt[t][2]; }
+        rc = dog_band_gather(S, s > 0 ? rec[s - 1][1] : nullptr, s > 0 ? cnt[s - 1][1] : nullptr,
+                             s < w - 1 ? rec[s + 1][0] : nullptr, s < w - 1 ? cnt[s + 1][0] : nullptr,
+                             nl, lof, lofc, nh, hif, hifc, st);
+        const uint64_t* mass = nullptr;
+        if (!rc) rc = dog_band_assign(S, meas_band, &mass, st);
+        if (!rc) CK2(P, cudaEventRecord(P->sev_asg[s], st));
+        return rc;
+    }
+    case 2:
+    case 3: {
+        if (int r = wait_all(ph == 2 ? P->sev_asg : P->sev_jnt)) return r;
+        U64Gather g{};
+        g.n = w;
+        for (int t = 0; t < w; ++t) g.p[t] = ph == 2 ? &P->shards[t]->sc->A_acc : &P->shards[t]->sc->W;
+        uint64_t* dst = ph == 2 ? P->sh_mass[s] : P->sh_weight[s];
+        CK2(P, launch(k_gather_u64, 1, 32, 0, st, 0, g, dst));
+        if (ph == 2) {
+            const uint64_t* wd = nullptr;
+            rc = dog_band_joint(S, dst, &wd, st);
+            if (!rc) CK2(P, cudaEventRecord(P->sev_jnt[s], st));
+        } else {
+            rc = dog_band_resample(S, dst, st);
+        }
+        return rc;
+    }
+    }
+    return DOG_E_INVAL;
+}
+
+int sharded_cycle(dog_ctx* P, const float* const* meas_band, float dt, const cudaStream_t* st)
+{
+    if (P->poisoned) return DOG_E_CUDA;
+    if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
+    const int w = (int)P->shards.size();
+    for (int ph = 0; ph < 4; ++ph)
+        for (int s = 0; s < w; ++s)
+            if (int rc = shard_phase(P, s, ph, meas_band[s], dt, st[s])) {
+                P->poisoned = true;   // bands are mid-cycle: only dog_destroy
+                return rc;
+            }
+    P->k += 1;
+    return DOG_OK;
+}
+
+}  // namespace
+
+static int create_sharded(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
+                          uint64_t seed, uint32_t flags, int n_devices, const int* device_ids, dog_ctx** out)
+{
+    if (!grid || !params || n_devices > kMaxBands || (flags & DOG_FLAG_DEBUG)) return DOG_E_INVAL;
+    if (grid->height < n_devices) return DOG_E_INVAL;
+    *out = nullptr;
+    DevGuard guard;
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    for (int s = 0; s < n_devices; ++s)
+        if (device_ids[s] < 0 || device_ids[s] >= ndev) return DOG_E_INVAL;
+    // peer access between every pair of distinct devices (NVLink / NVSwitch); required
+    for (int a = 0; a < n_devices; ++a)
+        for (int b = 0; b < n_devices; ++b) {
+            const int da = device_ids[a], db = device_ids[b];
+            if (da == db) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, da, db);
+            if (!can) return DOG_E_INVAL;
+            cudaSetDevice(da);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(nullptr, e, "cudaDeviceEnablePeerAccess");
+            cudaGetLastError();
+        }
+    dog_ctx* P = new (std::nothrow) dog_ctx();
+    if (!P) return DOG_E_NOMEM;
+    P->device = device_ids[0];
+    P->grid = *grid;
+    P->params = *params;
+    P->seed = seed;
+    P->nu = n_particles;
+    P->nu_b = n_birth;
+    P->Cg = (uint32_t)((int64_t)grid->width * grid->height);
+    P->C = P->Cg;
+    P->world = n_devices;
+    P->shard_dev.assign(device_ids, device_ids + n_devices);
+    int rc = make_shards(P, even_rows(grid->height, n_devices));
+    if (rc == DOG_OK) {
+        cudaSetDevice(device_ids[0]);
+        if (cudaEventCreateWithFlags(&P->ev_caller, cudaEventDisableTiming) != cudaSuccess) rc = DOG_E_CUDA;
+    }
+    if (rc != DOG_OK) {
+        destroy_shards(P);
+        delete P;
+        return rc;
+    }
+    *out = P;
+    return DOG_OK;
+}
+
+static int destroy_sharded(dog_ctx* P)
+{
+    DevGuard guard;
+    destroy_shards(P);
+    if (P->ev_caller) { cudaSetDevice(P->device); cudaEventDestroy(P->ev_caller); }
+    delete P;
+    return DOG_OK;
+}
+
+int dog_world(dog_ctx* ctx)
+{
+    if (!ctx) return DOG_E_INVAL;
+    return ctx->shards.empty() ? 1 : (int)ctx->shards.size();
+}
+
+int dog_get_bands(dog_ctx* ctx, int32_t* rows, int* devices)
+{
+    if (!ctx || !rows) return DOG_E_INVAL;
+    if (ctx->shards.empty()) {
+        rows[0] = 0; rows[1] = ctx->grid.height;
+        if (devices) devices[0] = ctx->device;
+        return 1;
+    }
+    for (size_t s = 0; s <= ctx->shards.size(); ++s) rows[s] = ctx->shard_rows[s];
+    if (devices)
+        for (size_t s = 0; s < ctx->shards.size(); ++s) devices[s] = ctx->shard_dev[s];
+    return (int)ctx->shards.size();
+}
+
+int dog_step_sharded(dog_ctx* ctx, const float* const* meas_band, float dt, void* const* streams)
+{
+    if (!ctx || !meas_band || !streams) return DOG_E_INVAL;
+    if (ctx->shards.empty()) return DOG_E_STATE;
+    const int w = (int)ctx->shards.size();
+    for (int s = 0; s < w; ++s)
+        if (!meas_band[s]) return DOG_E_INVAL;
+    DevGuard guard;
+    std::vector<cudaStream_t> st(w);
+    for (int s = 0; s < w; ++s) st[s] = (cudaStream_t)streams[s];
+    return sharded_cycle(ctx, meas_band, dt, st.data());
+}
+
+int dog_read_cells_sharded(dog_ctx* ctx, float* const* occ, float* const* free_mass, float* const* vel_mean,
+                           float* const* vel_cov, void* const* streams)
+{
+    if (!ctx || !streams) return DOG_E_INVAL;
+    if (ctx->shards.empty()) return DOG_E_STATE;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    DevGuard guard;
+    int first = DOG_OK;
+    for (size_t s = 0; s < ctx->shards.size(); ++s) {
+        const int rc = dog_read_cells(ctx->shards[s], occ ? occ[s] : nullptr, free_mass ? free_mass[s] : nullptr,
+                                      vel_mean ? vel_mean[s] : nullptr, vel_cov ? vel_cov[s] : nullptr, streams[s]);
+        if (rc && !first) first = rc;
+    }
+    return first;
+}
+
+int dog_set_bands(dog_ctx* ctx, const int32_t* rows)
+{
+    if (!ctx || !rows) return DOG_E_INVAL;
+    if (ctx->shards.empty()) return DOG_E_STATE;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    const int w = (int)ctx->shards.size();
+    if (!rows_valid(rows, w, ctx->grid.height)) return DOG_E_INVAL;
+    const size_t nu = (size_t)ctx->nu, C = ctx->Cg;
+    std::vector<float> x(nu), y(nu), vx(nu), vy(nu), mf(C);
+    float wb = 0.0f;
+    int64_t k = 0;
+    if (int rc = get_state_sharded(ctx, x.data(), y.data(), vx.data(), vy.data(), &wb, mf.data(), &k)) return rc;
+    DevGuard guard;
+    destroy_shards(ctx);
+    if (int rc = make_shards(ctx, std::vector<int32_t>(rows, rows + w + 1))) {
+        ctx->poisoned = true;
+        return rc;
+    }
+    return set_state_sharded(ctx, x.data(), y.data(), vx.data(), vy.data(), wb, mf.data(), k);
+}
+
+static int step_parent(dog_ctx* P, const float* meas, float dt, void* stream)
+{
+    // meas on device_ids[0] (peer-readable by every band); the bands run on the parent's own streams,
+    // forked from and joined back into the caller's stream
+    if (P->poisoned) return DOG_E_CUDA;
+    DevGuard guard;
+    const int w = (int)P->shards.size();
+    cudaSetDevice(P->device);
+    CK2(P, cudaEventRecord(P->ev_caller, (cudaStream_t)stream));
+    std::vector<const float*> mb(w);
+    for (int s = 0; s < w; ++s) {
+        cudaSetDevice(P->shard_dev[s]);
+        CK2(P, cudaStreamWaitEvent(P->shard_st[s], P->ev_caller, 0));
+        mb[s] = meas + (size_t)P->shard_rows[s] * P->grid.width * 2;
+    }
+    if (int rc = sharded_cycle(P, mb.data(), dt, P->shard_st.data())) return rc;
+    for (int s = 0; s < w; ++s) {
+        cudaSetDevice(P->shard_dev[s]);
+        CK2(P, cudaEventRecord(P->sev_done[s], P->shard_st[s]));
+    }
+    cudaSetDevice(P->device);
+    for (int s = 0; s < w; ++s) CK2(P, cudaStreamWaitEvent((cudaStream_t)stream, P->sev_done[s], 0));
+    return DOG_OK;
+}
+
+static int sync_sharded(dog_ctx* P, void* stream)
+{
+    if (P->poisoned) return DOG_E_CUDA;
+    DevGuard guard;
+    cudaSetDevice(P->device);
+    CK2(P, cudaStreamSynchronize((cudaStream_t)stream));
+    int first = DOG_OK;
+    for (size_t s = 0; s < P->shards.size(); ++s) {
+        cudaSetDevice(P->shard_dev[s]);
+        CK2(P, cudaDeviceSynchronize());
+        const int rc = report_meas(P->shards[s]);
+        if (rc && !first) first = rc;
+        if (P->shards[s]->poisoned) P->poisoned = true;
+    }
+    return first;
+}
+
+static int read_cells_parent(dog_ctx* P, float* occ, float* free_mass, float* vel_mean, float* vel_cov, void* stream)
+{
+    // whole-grid outputs on device_ids[0]: each band's rows copied peer-to-peer at its row offset
+    if (P->poisoned) return DOG_E_CUDA;
+    DevGuard guard;
+    int first = DOG_OK;
+    for (size_t s = 0; s < P->shards.size(); ++s) {   // the bands' cycles must be complete
+        cudaSetDevice(P->shard_dev[s]);
+        CK2(P, cudaDeviceSynchronize());
+    }
+    cudaSetDevice(P->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    for (size_t s = 0; s < P->shards.size(); ++s) {
+        dog_ctx* S = P->shards[s];
+        const size_t off = (size_t)P->shard_rows[s] * P->grid.width, n = S->C;
+        const int d = P->shard_dev[s];
+        if (occ) CK2(P, cudaMemcpyPeerAsync(occ + off, P->device, S->occ, d, 4 * n, st));
+        if (free_mass) CK2(P, cudaMemcpyPeerAsync(free_mass + off, P->device, S->fre, d, 4 * n, st));
+        if (vel_mean) CK2(P, cudaMemcpyPeerAsync(vel_mean + 2 * off, P->device, S->mean, d, 8 * n, st));
+        if (vel_cov) CK2(P, cudaMemcpyPeerAsync(vel_cov + 3 * off, P->device, S->cov, d, 12 * n, st));
+    }
+    CK2(P, cudaStreamSynchronize(st));
+    for (size_t s = 0; s < P->shards.size(); ++s) {
+        cudaSetDevice(P->shard_dev[s]);
+        const int rc = report_meas(P->shards[s]);
+        if (rc && !first) first = rc;
+    }
+    return first;
+}
+
+static int get_state_sharded(dog_ctx* P, float* x, float* y, float* vx, float* vy, float* w_bar, float* m_free,
+                             int64_t* k)
+{
+    // the bands' own particles in band (= global index) order; the empty remainder is sentinel particles
+    // (the whole-grid state's particles outside the grid: they carry no weight and are never resampled)
+    if (P->poisoned) return DOG_E_CUDA;
+    DevGuard guard;
+    const size_t nu = (size_t)P->nu;
+    std::vector<float> rec;
+    size_t n_tot = 0;
+    for (size_t s = 0; s < P->shards.size(); ++s) {
+        dog_ctx* S = P->shards[s];
+        uint32_t n = 0;
+        uint64_t g0 = 0;
+        if (int rc = dog_band_particles(S, nullptr, 0, &n, &g0)) return rc;
+        if (n_tot + n > nu) return DOG_E_STATE;
+        rec.resize((size_t)n * 4);
+        if (n) {
+            if (int rc = dog_band_particles(S, rec.data(), n, &n, &g0)) return rc;
+            if (g0 != n_tot) return DOG_E_STATE;     // bands are contiguous in global index order
+        }
+        for (uint32_t i = 0; i < n; ++i) {
+            if (x) x[n_tot + i] = rec[4 * i];
+            if (y) y[n_tot + i] = rec[4 * i + 1];
+            if (vx) vx[n_tot + i] = rec[4 * i + 2];
+            if (vy) vy[n_tot + i] = rec[4 * i + 3];
+        }
+        n_tot += n;
+        if (m_free) {
+            cudaSetDevice(P->shard_dev[s]);
+            CK2(P, cudaMemcpy(m_free + (size_t)P->shard_rows[s] * P->grid.width, S->m_free, (size_t)S->C * 4,
+                              cudaMemcpyDeviceToHost));
+        }
+    }
+    for (size_t i = n_tot; i < nu; ++i) {
+        if (x) x[i] = kSentinelPos;
+        if (y) y[i] = kSentinelPos;
+        if (vx) vx[i] = 0.0f;
+        if (vy) vy[i] = 0.0f;
+    }
+    if (w_bar) {
+        cudaSetDevice(P->shard_dev[0]);
+        CK2(P, cudaMemcpy(w_bar, &P->shards[0]->sc->w_bar, 4, cudaMemcpyDeviceToHost));
+    }
+    if (k) *k = P->k;
+    return DOG_OK;
+}
+
+static int set_state_sharded(dog_ctx* P, const float* x, const float* y, const float* vx, const float* vy,
+                             float w_bar, const float* m_free, int64_t k)
+{
+    // each band's particles must be one contiguous range of the canonical order, ranges in band order;
+    // particles outside the grid belong to no band (they carry no weight) and may sit anywhere else
+    if (P->poisoned) return DOG_E_CUDA;
+    const int w = (int)P->shards.size();
+    const size_t nu = (size_t)P->nu;
+    const float Wf = (float)P->grid.width, Hf = (float)P->grid.height;
+    std::vector<int64_t> first(w, -1), last(w, -1);
+    int prev_band = -1;
+    for (size_t i = 0; i < nu; ++i) {
+        const bool inside = x[i] >= 0.0f && x[i] < Wf && y[i] >= 0.0f && y[i] < Hf;
+        if (!inside) continue;
+        const int32_t row = (int32_t)y[i];
+        int b = 0;
+        while (row >= P->shard_rows[b + 1]) ++b;
+        if (b < prev_band) return DOG_E_INVAL;
+        if (first[b] < 0) first[b] = (int64_t)i;
+        else if (last[b] != (int64_t)i - 1) return DOG_E_INVAL;   // a particle outside the grid splits the band
+        last[b] = (int64_t)i;
+        prev_band = b;
+    }
+    DevGuard guard;
+    std::vector<float> rec;
+    for (int b = 0; b < w; ++b) {
+        const size_t n = first[b] < 0 ? 0 : (size_t)(last[b] - first[b] + 1);
+        const size_t f0 = first[b] < 0 ? 0 : (size_t)first[b];
+        rec.resize(4 * n + 4);
+        for (size_t i = 0; i < n; ++i) {
+            rec[4 * i] = x[f0 + i]; rec[4 * i + 1] = y[f0 + i]; rec[4 * i + 2] = vx[f0 + i]; rec[4 * i + 3] = vy[f0 + i];
+        }
+        const size_t off = (size_t)P->shard_rows[b] * P->grid.width;
+        if (int rc = dog_band_set_state(P->shards[b], n ? rec.data() : nullptr, (uint32_t)n, f0, m_free + off, w_bar, k))
+            return rc;
+    }
+    P->k = k;
+    return DOG_OK;
 }
 
 #ifdef DOG_TIMING

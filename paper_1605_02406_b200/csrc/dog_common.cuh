@@ -25,8 +25,9 @@ struct DevScalars {
     uint64_t o_base[2];          // global index of the first own particle (Philox counter base), by parity
     uint64_t A_acc;              // this context's born mass (k_cells atomics; shared over shards)
     uint64_t Wtot, Ppre;         // joint weight over all shards, joint prefix of the shards below
-    uint32_t mig_cnt[2];         // migrants leaving down / up this cycle
-    uint32_t far;                // migrants that would need more than one hop (dropped, counted)
+    uint32_t mig_cnt[4];         // migrants leaving this cycle: to the band below, above, further below,
+                                 // further above (k_pack_migrants; read by the receivers)
+    uint32_t mig_over;           // sticky: a receive exceeded the migrant capacity (cycle not exact)
     uint32_t pad2;
 };
 
@@ -50,7 +51,7 @@ struct FilterConst {
     uint32_t row0;       // first grid row of the context
     uint32_t lo_cap;     // particle slots reserved before the own region (migrants from below)
     uint32_t rank, world;
-    uint32_t c_lo, c_hi; // global cells of the neighbour bands [c_lo, c_hi) (one-hop migration reach)
+    uint32_t c_lo, c_hi; // global cells of the neighbour bands [c_lo, c_hi): near / far migrant buckets
     uint32_t nu, nu_b;
     float p_s, p_b, sigma_b, occ_max, v_max;
     uint64_t seed;

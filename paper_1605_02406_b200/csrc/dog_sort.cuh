@@ -308,14 +308,16 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
 
 // ------------------------------------------------------------------------------------------------
 // Row-band contexts: Alg. 1 for the own particles, then the particles whose
-// new cell lies in the band below / above are packed, in input (= global index) order, for the
-// neighbour shards.  Their slots in the local array keep them with a key outside the band, so the
-// local sort leaves them out (like particles outside the grid).
+// new cell lies in another band are packed, in input (= global index) order, into four buckets: for the
+// band below, the band above, and the bands further below / above (owner-bucketed: any displacement
+// reaches its band, nothing is dropped).  Their slots in the local array keep them with a key outside
+// the band, so the local sort leaves them out (like particles outside the grid).
 // ------------------------------------------------------------------------------------------------
+constexpr int kMigDirs = 4;   // 0 below, 1 above, 2 further below, 3 further above
 struct Migrants {
-    float4* scr[2];        // per tile, compacted: [tile * 4096 + k]
-    uint32_t* cnt[2];      // per tile
-    float4* send[2];       // packed for the neighbours (capacity cap)
+    float4* scr[kMigDirs];     // per tile, compacted: [tile * 4096 + k]
+    uint32_t* cnt[kMigDirs];   // per tile
+    float4* send[kMigDirs];    // packed for the receivers (capacity cap each)
     uint32_t cap;
 };
 
@@ -324,7 +326,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __res
                                                              StepArgs a)
 {
     PDL_ENTER();
-    __shared__ uint32_t s_w[2][kPsWarps + 1];
+    __shared__ uint32_t s_w[kMigDirs][kPsWarps + 1];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int par = (int)(a.k & 1);
@@ -337,53 +339,58 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __res
         sc->A_acc = 0ull;
     }
     float4 P[kPsRows];
-    uint32_t dir[kPsRows];                                  // 0 down, 1 up, 2 stays
-    uint32_t wc[2] = {0, 0};
+    uint32_t dir[kPsRows];                                  // kMigDirs: stays (or leaves the grid)
+    uint32_t wc[kMigDirs] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < kPsRows; ++i) {
         const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
-        dir[i] = 2u;
+        dir[i] = kMigDirs;
         if (p < n) {
             const uint32_t q = fc.lo_cap + tb + p;
             P[i] = predict_one(st[q], o_base + tb + p, fc, a);
             pst[q] = P[i];
             const uint32_t kg = global_key(P[i], fc);
-            if (kg < fc.Cg && kg < fc.c_off) dir[i] = 0u;
-            else if (kg < fc.Cg && kg - fc.c_off >= fc.C) dir[i] = 1u;
-            if (dir[i] < 2u && (kg < fc.c_lo || kg >= fc.c_hi)) atomicAdd(&sc->far, 1u);   // beyond the neighbour
+            if (kg < fc.Cg && kg < fc.c_off) dir[i] = kg >= fc.c_lo ? 0u : 2u;
+            else if (kg < fc.Cg && kg - fc.c_off >= fc.C) dir[i] = kg < fc.c_hi ? 1u : 3u;
         }
 #pragma unroll
-        for (int d = 0; d < 2; ++d) wc[d] += __popc(__ballot_sync(0xffffffffu, dir[i] == (uint32_t)d));
+        for (int d = 0; d < kMigDirs; ++d) wc[d] += __popc(__ballot_sync(0xffffffffu, dir[i] == (uint32_t)d));
     }
-    if (lane == 0) { s_w[0][warp] = wc[0]; s_w[1][warp] = wc[1]; }
+    if (lane == 0)
+#pragma unroll
+        for (int d = 0; d < kMigDirs; ++d) s_w[d][warp] = wc[d];
     __syncthreads();
-    uint32_t off[2] = {0, 0}, tot[2] = {0, 0};
+    uint32_t off[kMigDirs] = {0, 0, 0, 0}, tot[kMigDirs] = {0, 0, 0, 0};
 #pragma unroll
     for (int w = 0; w < kPsWarps; ++w)
 #pragma unroll
-        for (int d = 0; d < 2; ++d) { if (w < warp) off[d] += s_w[d][w]; tot[d] += s_w[d][w]; }
+        for (int d = 0; d < kMigDirs; ++d) { if (w < warp) off[d] += s_w[d][w]; tot[d] += s_w[d][w]; }
 #pragma unroll
     for (int i = 0; i < kPsRows; ++i) {
+        if (__ballot_sync(0xffffffffu, dir[i] < (uint32_t)kMigDirs) == 0u) continue;   // ~99 %: nobody leaves
 #pragma unroll
-        for (int d = 0; d < 2; ++d) {
+        for (int d = 0; d < kMigDirs; ++d) {
             const uint32_t b = __ballot_sync(0xffffffffu, dir[i] == (uint32_t)d);
             if (dir[i] == (uint32_t)d) mg.scr[d][tb + off[d] + __popc(b & lt)] = P[i];
             off[d] += __popc(b);
         }
     }
-    if (tid < 2) mg.cnt[tid][blockIdx.x] = tot[tid];
+    if (tid < kMigDirs) mg.cnt[tid][blockIdx.x] = tot[tid];
 }
 
-// One block: exclusive prefix of the per-tile migrant counts, then the packed send buffers (input
-// order); counts go to DevScalars (read by the host to size the exchange).
+// One block: exclusive prefix of the per-tile migrant counts of each bucket, then the packed send
+// buffers (input order, one warp per tile copying lane-strided); totals go to DevScalars (read by the
+// receivers' k_gather_migrants, or by the host to size a transport).  A bucket beyond the capacity is
+// truncated and flagged (mig_over): the cycle then cannot complete exactly and the host reports it.
 __global__ __launch_bounds__(1024) void k_pack_migrants(Migrants mg, uint32_t tiles, DevScalars* __restrict__ sc)
 {
     PDL_ENTER();
-    __shared__ uint32_t s_run[2];
+    __shared__ uint32_t s_run;
     __shared__ uint32_t s_w[33];
+    __shared__ uint32_t s_off[1024], s_cnt[1024];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int d = 0; d < 2; ++d) {
-        if (tid == 0) s_run[d] = 0u;
+    for (int d = 0; d < kMigDirs; ++d) {
+        if (tid == 0) s_run = 0u;
         __syncthreads();
         for (uint32_t t0 = 0; t0 < tiles; t0 += 1024) {
             const uint32_t t = t0 + tid;
@@ -398,14 +405,131 @@ __global__ __launch_bounds__(1024) void k_pack_migrants(Migrants mg, uint32_t ti
                 if (lane == 31) s_w[32] = vi;
             }
             __syncthreads();
-            const uint32_t dst0 = s_run[d] + s_w[warp] + inc - c;
-            for (uint32_t k = 0; k < c; ++k)               // migrants are ~1 %: a short serial copy per tile
-                if (dst0 + k < mg.cap) mg.send[d][dst0 + k] = mg.scr[d][t * kSortTile + k];
+            s_off[tid] = s_run + s_w[warp] + inc - c;
+            s_cnt[tid] = c;
             __syncthreads();
-            if (tid == 0) s_run[d] += s_w[32];
+            const uint32_t nt = min(1024u, tiles - t0);
+            for (uint32_t u = warp; u < nt; u += 32) {     // warp per tile (migrants are ~1 %)
+                const uint32_t cu = s_cnt[u], dst0 = s_off[u];
+                const float4* src = mg.scr[d] + (size_t)(t0 + u) * kSortTile;
+                for (uint32_t k = lane; k < cu; k += 32)
+                    if (dst0 + k < mg.cap) mg.send[d][dst0 + k] = src[k];
+            }
+            __syncthreads();
+            if (tid == 0) s_run += s_w[32];
             __syncthreads();
         }
-        if (tid == 0) sc->mig_cnt[d] = s_run[d];
+        if (tid == 0) {
+            sc->mig_cnt[d] = min(s_run, mg.cap);
+            if (s_run > mg.cap) sc->mig_over = 1u;
+        }
+    }
+}
+
+// Where a band's migrants come from (device pointers readable from the receiver: its own memory, a
+// peer GPU's over NVLink, or a transport's receive buffer), each bucket with its device count.
+constexpr int kMaxBands = 16;
+struct MigSrc {
+    const float4* rec;
+    const uint32_t* cnt;
+};
+struct MigGather {
+    MigSrc lo_near, hi_near;        // bucket 1 of band r-1 / bucket 0 of band r+1 (all of it is for r)
+    MigSrc lo_far[kMaxBands];       // bucket 3 of bands 0 .. r-2, in band order (filtered by row)
+    MigSrc hi_far[kMaxBands];       // bucket 2 of bands r+2 .. world-1, in band order (filtered by row)
+    int n_lo_far, n_hi_far;
+};
+
+// Receiver: builds [from below | own | from above] in global index order around the own particles
+// (pst[lo_cap .. lo_cap + n_own)): from below = the far records of bands 0 .. r-2 that land in this band,
+// then all of band r-1's near bucket, ending at lo_cap; from above = band r+1's near bucket, then the
+// far records of bands r+2 .. that land here.  Blocks 1.. copy the near buckets (contiguous); block 0
+// compacts the far buckets (rare) with block scans and publishes n_lo / n_hi.  A receive beyond the
+// capacity copies nothing and raises mig_over.
+__global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* __restrict__ pst,
+                                                          DevScalars* __restrict__ sc, FilterConst fc,
+                                                          uint32_t own_hi_cap, int par)
+{
+    PDL_ENTER();
+    __shared__ uint32_t s_w[33];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n_own = sc->n_own[par];
+    const uint32_t hi_room = own_hi_cap - n_own;              // slots after the own particles
+    const uint32_t nlo = g.lo_near.rec ? *g.lo_near.cnt : 0u;
+    const uint32_t nhi = g.hi_near.rec ? *g.hi_near.cnt : 0u;
+    float4* const lo_end = pst + fc.lo_cap;
+    float4* const hi_beg = pst + fc.lo_cap + n_own;
+    if (blockIdx.x > 0) {
+        const uint32_t nb = gridDim.x - 1, b = blockIdx.x - 1;
+        if (nlo <= fc.lo_cap)
+            for (uint32_t i = b * 1024 + tid; i < nlo; i += nb * 1024) lo_end[(int64_t)i - nlo] = g.lo_near.rec[i];
+        if (nhi <= hi_room)
+            for (uint32_t i = b * 1024 + tid; i < nhi; i += nb * 1024) hi_beg[i] = g.hi_near.rec[i];
+        return;
+    }
+    // block 0: far records landing in this band, stable compaction in band order
+    auto in_band = [&](const float4& P) {
+        const uint32_t kg = global_key(P, fc);
+        return kg < fc.Cg && kg >= fc.c_off && kg - fc.c_off < fc.C;
+    };
+    auto block_excl = [&](uint32_t f, uint32_t& tot) -> uint32_t {
+        const uint32_t b = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) s_w[warp] = __popc(b);
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = s_w[lane];
+            const uint32_t vi = warp_incl_scan(v, lane);
+            s_w[lane] = vi - v;
+            if (lane == 31) s_w[32] = vi;
+        }
+        __syncthreads();
+        const uint32_t r = s_w[warp] + __popc(b & ((1u << lane) - 1u));
+        tot = s_w[32];
+        __syncthreads();
+        return r;
+    };
+    // pass 1: far records from below (their total places them before the near bucket)
+    uint32_t flo = 0;
+    for (int s = 0; s < g.n_lo_far; ++s) {
+        const uint32_t n = *g.lo_far[s].cnt;
+        for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
+            const uint32_t i = i0 + tid;
+            flo += (uint32_t)__syncthreads_count(i < n && in_band(g.lo_far[s].rec[i]));
+        }
+    }
+    const bool lo_ok = nlo + flo <= fc.lo_cap;
+    uint32_t pos = 0;
+    for (int s = 0; s < g.n_lo_far && lo_ok; ++s) {
+        const uint32_t n = *g.lo_far[s].cnt;
+        for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
+            const uint32_t i = i0 + tid;
+            float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool f = i < n && in_band(P = g.lo_far[s].rec[i]);
+            uint32_t tot;
+            const uint32_t r = block_excl(f, tot);
+            if (f) lo_end[(int64_t)pos + r - (nlo + flo)] = P;
+            pos += tot;
+        }
+    }
+    uint32_t fhi = 0;
+    const bool near_hi_ok = nhi <= hi_room;
+    for (int s = 0; s < g.n_hi_far && near_hi_ok; ++s) {
+        const uint32_t n = *g.hi_far[s].cnt;
+        for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
+            const uint32_t i = i0 + tid;
+            float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
+            const bool f = i < n && in_band(P = g.hi_far[s].rec[i]);
+            uint32_t tot;
+            const uint32_t r = block_excl(f, tot);
+            if (f && nhi + fhi + r < hi_room) hi_beg[nhi + fhi + r] = P;
+            fhi += tot;
+        }
+    }
+    if (tid == 0) {
+        const bool hi_ok = nhi + fhi <= hi_room;
+        sc->n_lo = lo_ok ? nlo + flo : 0u;
+        sc->n_hi = hi_ok ? nhi + fhi : 0u;
+        if (!lo_ok || !hi_ok) sc->mig_over = 1u;
     }
 }
 

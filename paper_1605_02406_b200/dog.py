@@ -54,7 +54,12 @@ _SIGS = {
     "dog_version": ([], C.c_int),
     "dog_error_string": ([C.c_int], C.c_char_p),
     "dog_create": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
-                    C.POINTER(_vp)], C.c_int),
+                    C.c_int, C.POINTER(C.c_int), C.POINTER(_vp)], C.c_int),
+    "dog_step_sharded": ([_vp, _vpp, C.c_float, _vpp], C.c_int),
+    "dog_read_cells_sharded": ([_vp, _vpp, _vpp, _vpp, _vpp, _vpp], C.c_int),
+    "dog_set_bands": ([_vp, C.POINTER(C.c_int32)], C.c_int),
+    "dog_get_bands": ([_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int)], C.c_int),
+    "dog_world": ([_vp], C.c_int),
     "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_doppler": ([_vp, _vp, _vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_exact": ([_vp, _vp, C.c_float, _vp], C.c_int),
@@ -77,8 +82,9 @@ _SIGS = {
     "dog_create_band": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
                          C.POINTER(dog_band), C.POINTER(_vp)], C.c_int),
     "dog_band_predict": ([_vp, C.c_float, _vp], C.c_int),
-    "dog_band_sizes": ([_vp, _u32p, _u32p, _u32p, _u32p, _vp], C.c_int),
-    "dog_band_buffers": ([_vp, C.c_uint32, C.c_uint32, _vpp, _vpp, _vpp, _vpp, _vp], C.c_int),
+    "dog_band_sizes": ([_vp, _u32p, _u32p, _vp], C.c_int),
+    "dog_band_outbox": ([_vp, _vpp, _vpp], C.c_int),
+    "dog_band_gather": ([_vp, _vp, _vp, _vp, _vp, C.c_int, _vpp, _vpp, C.c_int, _vpp, _vpp, _vp], C.c_int),
     "dog_band_assign": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_joint": ([_vp, _vp, _vpp, _vp], C.c_int),
     "dog_band_assign_doppler": ([_vp, _vp, _vp, _vp, _vpp, _vp], C.c_int),
@@ -128,20 +134,62 @@ def _np_ptr(a: np.ndarray) -> int:
 
 
 class Filter:
-    """One DS-PHD/MIB filter (a dog_ctx) on the current CUDA device."""
+    """One DS-PHD/MIB filter (a dog_ctx) on the current CUDA device, or -- devices=[d0, d1, ...] with two
+    or more entries -- a sharded context: one row band per listed device (ids may repeat), driven by
+    the library with device-side exchanges (include/dog.h dog_step_sharded)."""
 
     def __init__(self, width: int, height: int, nu: int, nu_b: int, *, cell_size: float = 0.1,
                  p_s: float = 0.99, p_b: float = 0.02, sigma_pos: float = 0.02, sigma_vel: float = 0.8,
                  sigma_birth_vel: float = 4.0, free_tau: float = 2.0, occ_max: float = 1.0,
-                 v_max: float = 0.0, seed: int = 2406, debug: bool = False):
+                 v_max: float = 0.0, seed: int = 2406, debug: bool = False, devices=None):
         self.width, self.height, self.nu, self.nu_b = width, height, nu, nu_b
         self.C = width * height
         g = dog_grid(width, height, cell_size)
         p = dog_params(p_s, p_b, sigma_pos, sigma_vel, sigma_birth_vel, free_tau, occ_max, v_max)
         h = _vp()
-        _check(dog_create(C.byref(g), nu, nu_b, C.byref(p), seed, DOG_FLAG_DEBUG if debug else 0, C.byref(h)),
-               "dog_create")
+        devs = list(devices) if devices is not None else []
+        ids = (C.c_int * max(1, len(devs)))(*devs)
+        _check(dog_create(C.byref(g), nu, nu_b, C.byref(p), seed, DOG_FLAG_DEBUG if debug else 0, len(devs),
+                          ids if devs else None, C.byref(h)), "dog_create")
         self._h = h
+        self.world = dog_world(h)
+
+    def bands(self) -> tuple[list[tuple[int, int]], list[int]]:
+        """Row ranges [row0, row1) of the bands and their devices (one band for a whole-grid context)."""
+        rows = (C.c_int32 * (self.world + 1))()
+        devs = (C.c_int * self.world)()
+        _check(dog_get_bands(self._h, rows, devs), "dog_get_bands")
+        return [(rows[i], rows[i + 1]) for i in range(self.world)], list(devs)
+
+    def set_bands(self, rows: list[tuple[int, int]]):
+        """include/dog.h dog_set_bands: move the band boundaries (between cycles; the state carries over)."""
+        b = [r[0] for r in rows] + [rows[-1][1]]
+        _check(dog_set_bands(self._h, (C.c_int32 * len(b))(*b)), "dog_set_bands")
+
+    def step_sharded(self, meas_bands: list, dt: float, streams: list):
+        """include/dog.h dog_step_sharded: per-band measurement rows (device tensors on each band's device)
+        and one stream per band."""
+        assert len(meas_bands) == self.world and len(streams) == self.world
+        for t in meas_bands:
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+        mp = (_vp * self.world)(*[t.data_ptr() for t in meas_bands])
+        sp = (_vp * self.world)(*[_stream_ptr(s) for s in streams])
+        _check(dog_step_sharded(self._h, mp, dt, sp), "dog_step_sharded")
+
+    def read_cells_sharded(self, streams: list) -> list[dict]:
+        """include/dog.h dog_read_cells_sharded: each band's readouts (tensors on the band's device)."""
+        rows, devs = self.bands()
+        outs = []
+        for (r0, r1), d in zip(rows, devs):
+            n = (r1 - r0) * self.width
+            dev = torch.device("cuda", d)
+            outs.append(dict(occ=torch.empty(n, device=dev), free=torch.empty(n, device=dev),
+                             mean=torch.empty(n, 2, device=dev), cov=torch.empty(n, 3, device=dev)))
+        arr = lambda k: (_vp * self.world)(*[o[k].data_ptr() for o in outs])
+        sp = (_vp * self.world)(*[_stream_ptr(s) for s in streams])
+        _check(dog_read_cells_sharded(self._h, arr("occ"), arr("free"), arr("mean"), arr("cov"), sp),
+               "dog_read_cells_sharded")
+        return outs
 
     @classmethod
     def from_config(cls, cfg, debug: bool = False, **over) -> "Filter":
@@ -337,19 +385,29 @@ class BandFilter:
     def predict(self, dt: float, stream=None):
         _check(dog_band_predict(self._h, dt, _stream_ptr(stream)), "dog_band_predict")
 
-    def sizes(self, stream=None) -> tuple[int, int, int, int]:
-        a, b, c, d = C.c_uint32(), C.c_uint32(), C.c_uint32(), C.c_uint32()
-        _check(dog_band_sizes(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d), _stream_ptr(stream)),
-               "dog_band_sizes")
-        return a.value, b.value, c.value, d.value
+    def sizes(self, stream=None) -> tuple[list[int], int]:
+        """Synchronising: the four migrant bucket counts (below, above, further below, further above) and
+        the own particles of this cycle."""
+        cnt = (C.c_uint32 * 4)()
+        n = C.c_uint32()
+        _check(dog_band_sizes(self._h, cnt, C.byref(n), _stream_ptr(stream)), "dog_band_sizes")
+        return [int(c) for c in cnt], n.value
 
-    def buffers(self, n_down: int, n_up: int, n_lo: int, n_hi: int, stream=None):
-        """(send_down, send_up, recv_lo, recv_hi) as float32 [n, 4] device tensors (views)."""
-        sd, su, rl, rh = _vp(), _vp(), _vp(), _vp()
-        _check(dog_band_buffers(self._h, n_lo, n_hi, C.byref(sd), C.byref(su), C.byref(rl), C.byref(rh),
-                                _stream_ptr(stream)), "dog_band_buffers")
-        v = lambda ptr, n: DeviceArray.tensor(ptr.value or 0, 4 * n, torch.float32).view(-1, 4)
-        return v(sd, n_down), v(su, n_up), v(rl, n_lo), v(rh, n_hi)
+    def outbox(self) -> tuple[list[int], list[int]]:
+        """Device pointers of the four packed migrant buckets and of their u32 counts (no sync)."""
+        rec, cnt = (_vp * 4)(), (_vp * 4)()
+        _check(dog_band_outbox(self._h, rec, cnt), "dog_band_outbox")
+        return [int(r) for r in rec], [int(c) for c in cnt]
+
+    def gather(self, lo_near, hi_near, lo_far=(), hi_far=(), stream=None):
+        """include/dog.h dog_band_gather: each source is (records device pointer, u32 count device pointer);
+        lo_near / hi_near None at the grid edges."""
+        lf, hf = list(lo_far), list(hi_far)
+        arr = lambda xs, i: (_vp * max(1, len(xs)))(*[x[i] for x in xs])
+        _check(dog_band_gather(self._h, lo_near[0] if lo_near else None, lo_near[1] if lo_near else None,
+                               hi_near[0] if hi_near else None, hi_near[1] if hi_near else None,
+                               len(lf), arr(lf, 0), arr(lf, 1), len(hf), arr(hf, 0), arr(hf, 1),
+                               _stream_ptr(stream)), "dog_band_gather")
 
     def assign(self, meas_band: torch.Tensor, stream=None) -> torch.Tensor:
         assert meas_band.is_cuda and meas_band.dtype == torch.float32 and meas_band.is_contiguous()

@@ -1,19 +1,22 @@
-"""Row-band multi-GPU driver: one band context per rank.
+"""Row-band multi-GPU drivers for callers that move the band
+data themselves -- one process per GPU (``ShardedFilter`` over torch.distributed) or several bands in
+one process on one device (``LocalBands``).  The library's own sharded context (``dog.Filter(...,
+devices=[...])``, include/dog.h dog_step_sharded) runs the same phases with device-side exchanges and
+needs neither.
 
 The grid is cut into horizontal bands of rows, one per GPU.  Per cycle the bands exchange exactly what
 the method couples (include/dog.h, "row-band contexts"):
 
-1. after predict, the particles that moved into the band below / above (16-byte records, in global
-   index order) -- point-to-point with the two neighbours;
+1. after predict, the particles that moved into another band (16-byte records in global index order,
+   packed into four owner buckets: to the band below, above, further below, further above -- so no
+   displacement is too large and nothing is dropped);
 2. after the cell update, every band's fixed-point born mass (one u64 each) -- all-gather; each band
    allocates its birth slots on the global born-mass CDF (Alg. 5, A-15);
 3. after the joint-CDF scan, every band's joint weight (one u64 each) -- all-gather; each band then
    produces its contiguous share [F(P'), F(P' + W_band)) of the global systematic resampling (A-24).
 
 Philox counters use global particle / slot indices, so the bands together reproduce the whole-grid
-filter bit for bit (tests/test_band_gpu.py).  The transport is torch.distributed (NCCL between GPUs,
-gloo on CPU for the protocol tests); ``LocalBands`` drives several bands in one process on one device
-(sequential phases, host-mediated copies: no kernel waits on another).
+filter bit for bit (tests/test_band_gpu.py, tests/test_sharded_gpu.py).
 """
 from __future__ import annotations
 
@@ -36,17 +39,19 @@ def band_rows(height: int, world: int) -> list[tuple[int, int]]:
     return rows
 
 
-def plan_bands(row_particles, width: int, world: int, min_rows: int = 8, particle_bytes: float = 64.0,
+def plan_bands(row_particles, width: int, world: int, min_rows: int = 1, particle_bytes: float = 64.0,
                cell_bytes: float = 56.0) -> list[tuple[int, int]]:
     """Band rebalancing: contiguous row bands of near-equal work, from the
     particles per row.  A row costs particle_bytes per particle plus cell_bytes per cell (the
     algorithmic bytes of one cycle: 64 per particle, 56 per cell).  Boundary b is the
     first row whose cost prefix reaches b/world of the total, clamped so every band keeps at least
-    min_rows rows (one-hop migration needs bands at least as tall as a cycle's motion).  Deterministic:
-    every rank computes the same plan from the same counts."""
+    min_rows rows.  Correctness does not depend on the band height (migration is owner-bucketed: a
+    particle reaches its band however far it moved); min_rows only bounds how thin a band may get.
+    Deterministic: every rank computes the same plan from the same counts."""
     import numpy as np
     cnt = np.asarray(row_particles, dtype=np.float64).reshape(-1)
     H = cnt.size
+    min_rows = max(1, int(min_rows))
     if world < 1 or world * min_rows > H:
         raise ValueError(f"cannot split {H} rows into {world} bands of >= {min_rows} rows")
     cost = cnt * particle_bytes + cell_bytes * width
@@ -62,62 +67,130 @@ def plan_bands(row_particles, width: int, world: int, min_rows: int = 8, particl
     return [(bounds[i], bounds[i + 1]) for i in range(world)]
 
 
-def neighbour_counts(counts: list[tuple[int, int]], rank: int) -> tuple[int, int]:
-    """Given every band's (n_down, n_up) migrant counts, the records band `rank` receives from below
-    (the lower band's n_up) and from above (the upper band's n_down)."""
-    world = len(counts)
-    n_lo = counts[rank - 1][1] if rank > 0 else 0
-    n_hi = counts[rank + 1][0] if rank < world - 1 else 0
-    return n_lo, n_hi
+def sources_for(rank: int, world: int):
+    """Which bucket of which band feeds band `rank` (include/dog.h dog_band_gather): (lo_near, hi_near,
+    lo_far, hi_far) as (band, bucket) pairs; buckets 0 below, 1 above, 2 further below, 3 further above."""
+    lo_near = (rank - 1, 1) if rank > 0 else None
+    hi_near = (rank + 1, 0) if rank < world - 1 else None
+    lo_far = [(s, 3) for s in range(0, rank - 1)]
+    hi_far = [(s, 2) for s in range(rank + 2, world)]
+    return lo_near, hi_near, lo_far, hi_far
+
+
+def _band_view(ptr: int, n: int) -> torch.Tensor:
+    return dog.DeviceArray.tensor(ptr, 4 * n, torch.float32).view(-1, 4)
 
 
 class DistTransport:
-    """Exchanges of one band over torch.distributed (rank = band index)."""
+    """Exchanges of one band over torch.distributed (rank = band index).  stage_cpu=True routes every
+    collective through host memory (gloo backend: protocol tests, or several processes sharing one GPU,
+    where NCCL refuses duplicate devices)."""
 
-    def __init__(self, rank: int, world: int, device: torch.device, group=None):
+    def __init__(self, rank: int, world: int, device: torch.device, group=None, stage_cpu: bool = False):
         self.rank, self.world, self.device, self.group = rank, world, device, group
+        self.stage_cpu = stage_cpu
+        self._keep = []
 
-    def counts(self, n_down: int, n_up: int) -> tuple[int, int]:
-        mine = torch.tensor([n_down, n_up], dtype=torch.int64, device=self.device)
-        allc = torch.empty(2 * self.world, dtype=torch.int64, device=self.device)
+    @property
+    def _cdev(self):
+        return torch.device("cpu") if self.stage_cpu else self.device
+
+    def all_counts(self, counts: list[int]) -> list[list[int]]:
+        mine = torch.tensor(counts, dtype=torch.int64, device=self._cdev)
+        allc = torch.empty(len(counts) * self.world, dtype=torch.int64, device=self._cdev)
         dist.all_gather(list(allc.chunk(self.world)), mine, group=self.group)
-        c = allc.view(self.world, 2).tolist()
-        return neighbour_counts([(int(a), int(b)) for a, b in c], self.rank)
+        return allc.view(self.world, len(counts)).tolist()
 
-    def migrate(self, send_down: torch.Tensor, send_up: torch.Tensor, recv_lo: torch.Tensor, recv_hi: torch.Tensor):
-        ops = []
-        if self.rank > 0:
-            if send_down.numel():
-                ops.append(dist.P2POp(dist.isend, send_down, self.rank - 1, group=self.group))
-            if recv_lo.numel():
-                ops.append(dist.P2POp(dist.irecv, recv_lo, self.rank - 1, group=self.group))
-        if self.rank < self.world - 1:
-            if send_up.numel():
-                ops.append(dist.P2POp(dist.isend, send_up, self.rank + 1, group=self.group))
-            if recv_hi.numel():
-                ops.append(dist.P2POp(dist.irecv, recv_hi, self.rank + 1, group=self.group))
+    def _p2p(self, sends, recvs):
+        ops = [dist.P2POp(dist.isend, t, peer, group=self.group) for t, peer in sends if t.numel()]
+        ops += [dist.P2POp(dist.irecv, t, peer, group=self.group) for t, peer in recvs if t.numel()]
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
 
+    def exchange_buckets(self, out: list, counts: list[int], ok: int = 1):
+        """The communication of the migrant exchange: `out` are this band's four buckets ([n_d, 4] f32
+        tensors on the transport's collective device; 0 below, 1 above, 2 further below, 3 further above).
+        Returns the sources of this band in dog_band_gather's order as (kind, records [n, 4], n): "lo" /
+        "hi" near buckets of the neighbours (point to point), then "lof" / "hif" far buckets of the other
+        bands in band order (padded all-gathers, only when some band has any).  Raises on every rank if
+        any rank reports ok = 0."""
+        r, w = self.rank, self.world
+        allc = self.all_counts(list(counts) + [ok])
+        if any(c[4] == 0 for c in allc):
+            raise dog.DogError(dog.DOG_E_NOMEM, "migrant exchange (a band exceeded its migrant capacity)")
+        cdev = self._cdev
+        recv_lo = torch.empty(allc[r - 1][1] if r > 0 else 0, 4, device=cdev)
+        recv_hi = torch.empty(allc[r + 1][0] if r < w - 1 else 0, 4, device=cdev)
+        sends = ([(out[0], r - 1)] if r > 0 else []) + ([(out[1], r + 1)] if r < w - 1 else [])
+        recvs = ([(recv_lo, r - 1)] if r > 0 else []) + ([(recv_hi, r + 1)] if r < w - 1 else [])
+        self._p2p(sends, recvs)
+        far = {}
+        for d in (2, 3):
+            m = max(c[d] for c in allc)
+            if m == 0:
+                continue
+            pad = torch.zeros(m, 4, device=cdev)
+            pad[:counts[d]] = out[d]
+            gathered = [torch.empty(m, 4, device=cdev) for _ in range(w)]
+            dist.all_gather(gathered, pad, group=self.group)
+            far[d] = gathered
+        lo_near, hi_near, lo_far, hi_far = sources_for(r, w)
+        srcs = [("lo", recv_lo, recv_lo.shape[0])] if lo_near else []
+        srcs += [("hi", recv_hi, recv_hi.shape[0])] if hi_near else []
+        for kind, lst in (("lof", lo_far), ("hif", hi_far)):
+            for b, d in lst:
+                n = allc[b][d]
+                srcs.append((kind, far[d][b][:n] if d in far else torch.empty(0, 4, device=cdev), n))
+        return srcs
+
+    def migrate(self, f, stream=None):
+        """Move this band's migrant buckets to their owners and assemble the band's local array
+        (dog_band_gather).  One host synchronisation: the bucket counts size the messages."""
+        try:
+            counts, _ = f.sizes(stream)
+            ok = 1
+        except dog.DogError:                         # overflow: every rank must fail together
+            counts, ok = [0, 0, 0, 0], 0
+        rec, _ = f.outbox()
+        out = [_band_view(rec[d], counts[d]) for d in range(4)]
+        if self.stage_cpu:
+            out = [t.cpu() for t in out]
+        srcs = self.exchange_buckets(out, counts, ok)
+        dev = self.device
+        recs = [t.to(dev).contiguous() if t.numel() else torch.empty(1, 4, device=dev) for _, t, _ in srcs]
+        cnt = torch.tensor([n for _, _, n in srcs] or [0], dtype=torch.int32, device=dev)
+        ptr = [(recs[i].data_ptr(), cnt.data_ptr() + 4 * i) for i in range(len(srcs))]
+        pick = lambda k: [p for p, (kk, _, _) in zip(ptr, srcs) if kk == k]
+        lo, hi = pick("lo"), pick("hi")
+        f.gather(lo[0] if lo else None, hi[0] if hi else None, pick("lof"), pick("hif"), stream)
+        self._keep = [recs, cnt]                     # alive until the gather kernel has run (stream order)
+
     def allgather_u64(self, x: torch.Tensor, out: torch.Tensor):
+        if self.stage_cpu:
+            xs = x.reshape(1).cpu()
+            outs = [torch.empty(1, dtype=x.dtype) for _ in range(self.world)]
+            dist.all_gather(outs, xs, group=self.group)
+            out.copy_(torch.cat(outs).to(out.device))
+            return
         dist.all_gather(list(out.chunk(self.world)), x.reshape(1), group=self.group)
 
     def allgather_var(self, x: torch.Tensor) -> list[torch.Tensor]:
         """Every rank's tensor [n_r, ...] (n_r may differ; same trailing shape and dtype), in rank order."""
-        n = torch.tensor([x.shape[0]], dtype=torch.int64, device=self.device)
-        ns = torch.zeros(self.world, dtype=torch.int64, device=self.device)
+        dev = self._cdev
+        n = torch.tensor([x.shape[0]], dtype=torch.int64, device=dev)
+        ns = torch.zeros(self.world, dtype=torch.int64, device=dev)
         dist.all_gather(list(ns.chunk(self.world)), n, group=self.group)
         ns = [int(v) for v in ns.tolist()]
         m = max(ns)
-        pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=self.device)
-        pad[:x.shape[0]] = x.to(self.device)
+        pad = torch.zeros((m,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+        pad[:x.shape[0]] = x.to(dev)
         outs = [torch.zeros_like(pad) for _ in range(self.world)]
         dist.all_gather(outs, pad, group=self.group)
         return [o[:k] for o, k in zip(outs, ns)]
 
     def allreduce_sum(self, x: torch.Tensor) -> torch.Tensor:
-        y = x.to(self.device).clone()
+        y = x.to(self._cdev).clone()
         dist.all_reduce(y, group=self.group)
         return y
 
@@ -127,7 +200,8 @@ class ShardedFilter:
 
     def __init__(self, width: int, height: int, nu: int, nu_b: int, rank: int, world: int,
                  transport: DistTransport, migrant_cap: int | None = None, **params):
-        self._args = (width, height, nu, nu_b, migrant_cap or max(4096, nu // 8), params)
+        # migrant_cap = nu (default): a band can receive every particle, so no exchange can overflow
+        self._args = (width, height, nu, nu_b, min(migrant_cap or nu, (1 << 26) - 1), params)
         self.rank = rank
         self._make(band_rows(height, world), world)
         self.t = transport
@@ -135,7 +209,6 @@ class ShardedFilter:
         dev = transport.device
         self.mass_all = torch.zeros(world, dtype=torch.int64, device=dev)
         self.weight_all = torch.zeros(world, dtype=torch.int64, device=dev)
-        self.n_far = 0
 
     def _make(self, rows, world):
         width, height, nu, nu_b, cap, params = self._args
@@ -147,9 +220,9 @@ class ShardedFilter:
         self.f = dog.BandFilter(width, height, nu, nu_b, self.row0, self.row1, rank, world, lo_row0, hi_row1, cap,
                                 **params)
 
-    def rebalance(self, min_rows: int = 8) -> bool:
+    def rebalance(self, min_rows: int = 1, rows=None) -> bool:
         """Move the band boundaries to equalise the per-band work (plan_bands over the all-reduced
-        particles per row), between cycles.  The bands' states are exchanged (all-gather of particles and
+        particles per row; `rows` forces a partition instead), between cycles.  The bands' states are exchanged (all-gather of particles and
         m_F rows) and each rank re-creates its band context with its new rows; the global particle order
         is unchanged, so the filter continues bit-exactly.  Returns False (nothing moved) if the plan
         keeps the current bands or the state holds particles outside the grid (an empty world)."""
@@ -166,7 +239,7 @@ class ShardedFilter:
         if int(flags.item()) != self.world:
             return False
         counts = self.t.allreduce_sum(torch.from_numpy(local.astype(np.int64))).cpu().numpy()
-        new_rows = plan_bands(counts, width, self.world, min_rows)
+        new_rows = list(rows) if rows is not None else plan_bands(counts, width, self.world, min_rows)
         if new_rows == self.rows:
             return False
         wb, k = self.f.w_bar_k()
@@ -194,24 +267,23 @@ class ShardedFilter:
 
     def step(self, meas_band: torch.Tensor, dt: float, stream=None, doppler=None, obs=None):
         """One cycle; doppler = (doppler_band [C_band, 4], p_assoc_band [C_band]) for the Doppler branch;
-        obs = obs_band [C_band, 4] for the exact PHD/MIB cycle (meas_band is then ignored)."""
-        f = self.f
-        f.predict(dt, stream)
-        n_down, n_up, n_own, n_far = f.sizes(stream)
-        self.n_far = n_far
-        n_lo, n_hi = self.t.counts(n_down, n_up)
-        sd, su, rl, rh = f.buffers(n_down, n_up, n_lo, n_hi, stream)
-        self.t.migrate(sd, su, rl, rh)
-        if obs is not None:
-            mass = f.assign_exact(obs, stream)
-        elif doppler is not None:
-            mass = f.assign_doppler(meas_band, *doppler, stream)
-        else:
-            mass = f.assign(meas_band, stream)
-        self.t.allgather_u64(mass, self.mass_all)
-        weight = f.joint(self.mass_all, stream)
-        self.t.allgather_u64(weight, self.weight_all)
-        f.resample(self.weight_all, stream)
+        obs = obs_band [C_band, 4] for the exact PHD/MIB cycle (meas_band is then ignored).  Every kernel
+        and every exchange runs on `stream` (default: the current stream)."""
+        st = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            f = self.f
+            f.predict(dt, st)
+            self.t.migrate(f, st)
+            if obs is not None:
+                mass = f.assign_exact(obs, st)
+            elif doppler is not None:
+                mass = f.assign_doppler(meas_band, *doppler, st)
+            else:
+                mass = f.assign(meas_band, st)
+            self.t.allgather_u64(mass, self.mass_all)
+            weight = f.joint(self.mass_all, st)
+            self.t.allgather_u64(weight, self.weight_all)
+            f.resample(self.weight_all, st)
 
 
 class LocalBands:
@@ -220,12 +292,11 @@ class LocalBands:
 
     def __init__(self, width: int, height: int, nu: int, nu_b: int, world: int, migrant_cap: int | None = None,
                  **params):
-        self._args = (width, height, nu, nu_b, migrant_cap or max(4096, nu // 8), params)
+        self._args = (width, height, nu, nu_b, min(migrant_cap or nu, (1 << 26) - 1), params)
         self.world = world
         self._make(band_rows(height, world))
         self.mass_all = torch.zeros(world, dtype=torch.int64, device="cuda")
         self.weight_all = torch.zeros(world, dtype=torch.int64, device="cuda")
-        self.n_far = 0
 
     def _make(self, rows):
         width, height, nu, nu_b, cap, params = self._args
@@ -237,7 +308,7 @@ class LocalBands:
             hi = rows[b + 1][1] if b < world - 1 else r1
             self.bands.append(dog.BandFilter(width, height, nu, nu_b, r0, r1, b, world, lo, hi, cap, **params))
 
-    def rebalance(self, min_rows: int = 8, rows=None) -> bool:
+    def rebalance(self, min_rows: int = 1, rows=None) -> bool:
         """Band rebalancing (see ShardedFilter.rebalance) for the bands of this process; `rows` forces a
         given partition instead of plan_bands'."""
         import numpy as np
@@ -274,18 +345,12 @@ class LocalBands:
         B = self.bands
         for f in B:
             f.predict(dt)
-        sizes = [f.sizes() for f in B]
-        self.n_far = max(s[3] for s in sizes)
-        counts = [(s[0], s[1]) for s in sizes]
-        bufs = []
+        box = [f.outbox() for f in B]                 # (records, counts) device pointers of each bucket
+        src = lambda t, d: (box[t][0][d], box[t][1][d])
         for b, f in enumerate(B):
-            n_lo, n_hi = neighbour_counts(counts, b)
-            bufs.append(f.buffers(counts[b][0], counts[b][1], n_lo, n_hi))
-        for b in range(self.world):                   # band b's down-migrants become band b-1's "from above"
-            if b > 0:
-                bufs[b - 1][3].copy_(bufs[b][0])
-            if b < self.world - 1:
-                bufs[b + 1][2].copy_(bufs[b][1])
+            lo_near, hi_near, lo_far, hi_far = sources_for(b, self.world)
+            f.gather(src(*lo_near) if lo_near else None, src(*hi_near) if hi_near else None,
+                     [src(*x) for x in lo_far], [src(*x) for x in hi_far])
         width = self._args[0]
         for b, f in enumerate(B):
             r0, r1 = self.rows[b]

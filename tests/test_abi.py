@@ -57,14 +57,22 @@ def test_argument_validation_without_device(lib):
     g = dog.dog_grid(0, 10, 0.1)
     p = dog.dog_params(0.99, 0.02, 0.02, 0.8, 4.0, 2.0, 1.0, 0.0)
     h = C.c_void_p()
-    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
     g = dog.dog_grid(16, 16, 0.1)
     bad = dog.dog_params(1.5, 0.02, 0.02, 0.8, 4.0, 2.0, 1.0, 0.0)
-    assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
     bad = dog.dog_params(0.99, 0.02, 0.02, 0.8, 4.0, -2.0, 1.0, 0.0)
-    assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
     g = dog.dog_grid(8192, 4096, 0.1)   # C >= 2^24
-    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
+    ids = (C.c_int * 2)(0, 0)
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, 2, None, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, -1, ids, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, dog.DOG_FLAG_DEBUG, 2, ids, C.byref(h)) == dog.DOG_E_INVAL
+    assert dog.dog_step_sharded(None, None, 0.1, None) == dog.DOG_E_INVAL
+    assert dog.dog_read_cells_sharded(None, None, None, None, None, None) == dog.DOG_E_INVAL
+    assert dog.dog_set_bands(None, None) == dog.DOG_E_INVAL
+    assert dog.dog_band_gather(None, None, None, None, None, 0, None, None, 0, None, None, None) == dog.DOG_E_INVAL
     assert dog.dog_step(None, None, 0.1, None) == dog.DOG_E_INVAL
     assert dog.dog_step_doppler(None, None, None, None, 0.1, None) == dog.DOG_E_INVAL
     assert dog.dog_step_exact(None, None, 0.1, None) == dog.DOG_E_INVAL

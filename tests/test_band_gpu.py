@@ -43,7 +43,6 @@ def run_bands_vs_whole(cfg, world, cycles, frames=None, migrant_cap=None, rebala
         g.step(meas.contiguous(), cfg.dt)
         lb.step(meas.contiguous(), cfg.dt)
         torch.cuda.synchronize()
-        assert lb.n_far == 0
         st = g.get_state()
         whole = np.stack([st["x"], st["y"], st["vx"], st["vy"]], 1)
         parts, spans = lb.particles()
@@ -115,7 +114,6 @@ def test_doppler_bands_bit_exact():
             g.step_doppler(meas, dop, pA, cfg.dt)
             lb.step(meas, cfg.dt, doppler=(dop, pA))
         torch.cuda.synchronize()
-        assert lb.n_far == 0
         st = g.get_state()
         whole = np.stack([st["x"], st["y"], st["vx"], st["vy"]], 1)
         parts, _ = lb.particles()
@@ -149,7 +147,6 @@ def test_exact_bands_bit_exact():
             g.step_exact(obs, cfg.dt)
             lb.step(meas, cfg.dt, obs=obs)
         torch.cuda.synchronize()
-        assert lb.n_far == 0
         st = g.get_state()
         whole = np.stack([st["x"], st["y"], st["vx"], st["vy"]], 1)
         parts, _ = lb.particles()

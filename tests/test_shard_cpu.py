@@ -1,6 +1,7 @@
 """Host logic of the row-band multi-GPU path (paper_1605_02406_b200/shard.py) on CPU: band partition,
-neighbour pairing, and the torch.distributed exchange protocol with the gloo backend at world sizes 2
-and 3 (127.0.0.1 rendezvous).  The device side of the same path is tests/test_band_gpu.py."""
+which bucket of which band feeds each band, and the torch.distributed exchange protocol (near buckets
+point to point, far buckets by all-gather, all-rank failure on overflow) with the gloo backend at world
+sizes 2, 3 and 4 (127.0.0.1 rendezvous).  The device side of the same path is tests/test_band_gpu.py."""
 import os
 import socket
 
@@ -9,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1605_02406_b200.shard import DistTransport, band_rows, neighbour_counts, plan_bands
+from paper_1605_02406_b200.shard import DistTransport, band_rows, plan_bands, sources_for
 
 
 def test_band_rows_partition():
@@ -23,11 +24,12 @@ def test_band_rows_partition():
         band_rows(4, 5)
 
 
-def test_neighbour_counts():
-    counts = [(0, 5), (3, 7), (2, 0)]         # (down, up) per band, bottom-up
-    assert neighbour_counts(counts, 0) == (0, 3)
-    assert neighbour_counts(counts, 1) == (5, 2)
-    assert neighbour_counts(counts, 2) == (7, 0)
+def test_sources_for():
+    # band r is fed by r-1's "above" bucket, r+1's "below" bucket and the far buckets of everyone else
+    assert sources_for(0, 1) == (None, None, [], [])
+    assert sources_for(0, 3) == (None, (1, 0), [], [(2, 2)])
+    assert sources_for(2, 5) == ((1, 1), (3, 0), [(0, 3)], [(4, 2)])
+    assert sources_for(4, 5) == ((3, 1), None, [(0, 3), (1, 3), (2, 3)], [])
 
 
 def test_plan_bands_balances_work():
@@ -66,19 +68,24 @@ def _worker(rank, world, port):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     try:
         t = DistTransport(rank, world, torch.device("cpu"))
-        # every band sends (rank+1) records down and (rank+2) up; edge bands send nothing off the grid
-        n_down = rank + 1 if rank > 0 else 0
-        n_up = rank + 2 if rank < world - 1 else 0
-        n_lo, n_hi = t.counts(n_down, n_up)
-        assert n_lo == (rank + 1 if rank > 0 else 0) and n_hi == (rank + 2 if rank < world - 1 else 0)
-        rec = lambda src, n, tag: torch.arange(4 * n, dtype=torch.float32).view(n, 4) + 1000 * src + tag
-        send_down, send_up = rec(rank, n_down, 1), rec(rank, n_up, 2)
-        recv_lo, recv_hi = torch.zeros(n_lo, 4), torch.zeros(n_hi, 4)
-        t.migrate(send_down, send_up, recv_lo, recv_hi)
-        if rank > 0:                               # what the band below sent up
-            assert torch.equal(recv_lo, rec(rank - 1, n_lo, 2))
-        if rank < world - 1:                       # what the band above sent down
-            assert torch.equal(recv_hi, rec(rank + 1, n_hi, 1))
+        # band b sends (b+1) records to the band below, (b+2) above, 1 further below / above where one exists
+        cnt = lambda b: [b + 1 if b > 0 else 0, b + 2 if b < world - 1 else 0, 1 if b > 1 else 0,
+                         1 if b < world - 2 else 0]
+        rec = lambda src, d, n: torch.arange(4 * n, dtype=torch.float32).view(n, 4) + 1000 * src + 100 * d
+        counts = cnt(rank)
+        out = [rec(rank, d, counts[d]) for d in range(4)]
+        srcs = t.exchange_buckets(out, counts)
+        lo_near, hi_near, lo_far, hi_far = sources_for(rank, world)
+        expect = ([("lo", lo_near)] if lo_near else []) + ([("hi", hi_near)] if hi_near else [])
+        expect += [("lof", x) for x in lo_far] + [("hif", x) for x in hi_far]
+        assert [k for k, _, _ in srcs] == [k for k, _ in expect]
+        for (kind, got, n), (_, (b, d)) in zip(srcs, expect):
+            assert n == cnt(b)[d] and got.shape[0] == n
+            assert torch.equal(got, rec(b, d, n)), (rank, kind, b, d)
+        # a band reporting an overflow makes every rank raise (nobody waits in a collective)
+        from paper_1605_02406_b200 import dog
+        with pytest.raises(dog.DogError):
+            t.exchange_buckets([rec(rank, d, 0) for d in range(4)], [0, 0, 0, 0], ok=0 if rank == world - 1 else 1)
         out = torch.zeros(world, dtype=torch.int64)
         t.allgather_u64(torch.tensor([10 ** 12 + rank], dtype=torch.int64), out)
         assert out.tolist() == [10 ** 12 + r for r in range(world)]
@@ -94,6 +101,6 @@ def _worker(rank, world, port):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_exchange_protocol_gloo(world):
     mp.spawn(_worker, args=(world, _free_port()), nprocs=world, join=True)
