@@ -565,13 +565,13 @@ def bench_sharded(args, cfg):
                                    f"birth particles, urban ray-cast scene", "grid": f"{cfg.width}x{cfg.height}",
                        "nu": cfg.nu, "nu_b": cfg.nu_b, "dt_s": cfg.dt, "settle_cycles": settle,
                        "l2": "flushed between timed cycles (256 MiB write outside the cycle events)",
-                       "parallelism": f"row bands x{world} (migrants: NCCL send/recv; prefixes: NCCL all-gather)",
+                       "parallelism": f"row bands x{world} (migrants: owner buckets, NCCL send/recv + all-gather; "
+                                      f"prefixes: NCCL all-gather)",
                        "rows": shard.band_rows(cfg.height, world), "own_particles": own_all.tolist(),
                        "p10_p90_ms": [step_ms[int(0.1 * (K - 1))], step_ms[int(0.9 * (K - 1))]]},
             "roofline": {"bound": "hbm", "kernel": "cycle per GPU (A_alg / N)", "achieved": per_gpu, "peak": hbm,
                          "unit": "GB/s", "frac": per_gpu / hbm, "traffic": None, "peak_source": peak_src},
-            "cpu_baseline": None, "e2e": e2e, "gpu_launches": 10 * K * world, "clocks": clk,
-            "far_migrants": f.n_far,
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": 11 * K * world, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
