@@ -54,12 +54,14 @@ struct dog_ctx {
 
     // state S_k and predicted state (SoA, f32)
     float4* st = nullptr;                         // (x, y, vx, vy) per particle
-    float4* pst = nullptr;                        // predicted state, same layout
-    RunF* rfg = nullptr;                          // k_resample_tiles per-run parameters beyond its smem
+    float4* pst = nullptr;                        // band contexts: predicted state of the local array (input
+                                                  // order, AoS); whole-grid debug builds: the PRED dumps
+    float2 *pxy = nullptr, *pv = nullptr;         // predicted state in sorted order, (x, y) and (vx, vy) halves
     // assignment (dog_sort.cuh)
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
     TilePairs tp{};                               // runs of equal keys per tile
+    RunF* rfg = nullptr;                          // k_resample_tiles: F parameters of runs beyond its smem cache
     uint32_t *plist = nullptr, *ptmp = nullptr;   // per-cell run lists
     uint32_t *counts = nullptr, *npairs = nullptr;   // n_c and runs per cell, zeroed by k_cells
     // cells
@@ -386,7 +388,8 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->st, N); AL(ctx->pst, N); AL(ctx->rfg, N);
+    AL(ctx->st, N); AL(ctx->pxy, N); AL(ctx->pv, N); AL(ctx->rfg, N);
+    if (dbg || (band && band->world > 1)) AL(ctx->pst, N);
     AL(ctx->lperm, N); AL(ctx->kscr, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
     AL(ctx->plist, N); AL(ctx->ptmp, N); AL(ctx->ppart, N);
@@ -531,11 +534,13 @@ static int L_predict_sort(dog_ctx* ctx, bool fused, const StepArgs& a, const Fil
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     if (fused)
-        CK(launch(k_predict_sort<true>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
-                  dbg ? ctx->keys : nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a, ctx->kscr));
+        CK(launch(k_predict_sort<true>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st,
+                  dbg ? ctx->pst : nullptr, ctx->pxy, ctx->pv, dbg ? ctx->keys : nullptr, dbg ? ctx->lperm : nullptr,
+                  ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a, ctx->kscr));
     else
         CK(launch(k_predict_sort<false>, ctx->tiles, kPsThreads, kPsSmemBytes, st, 0, (const float4*)ctx->st, ctx->pst,
-                  (uint32_t*)nullptr, ctx->lperm, ctx->tp, ctx->counts, ctx->npairs, ctx->sc, fc, a, ctx->kscr));
+                  ctx->pxy, ctx->pv, (uint32_t*)nullptr, (uint16_t*)nullptr, ctx->tp, ctx->counts, ctx->npairs, ctx->sc,
+                  fc, a, ctx->kscr));
     return DOG_OK;
 }
 
@@ -592,13 +597,14 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
     const int par = (int)(a.k & 1);
+    static const bool rs_pdl = getenv("DOG_RS_NOPDL") == nullptr;   // diagnostics
     if (dbg)
-        CK(launch_ex(false, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
-                  ctx->tp, (const float4*)ctx->pst, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
+        CK(launch_ex(rs_pdl, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
+                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
                   (const DevScalars*)ctx->sc, fc, par, tskip));
     else
-        CK(launch_ex(false, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
-                  ctx->tp, (const float4*)ctx->pst, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
+        CK(launch_ex(rs_pdl, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)nullptr,
+                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
                   (const DevScalars*)ctx->sc, fc, par, tskip));
     return DOG_OK;
 }
@@ -734,7 +740,7 @@ static int alloc_doppler(dog_ctx* ctx)
 static int L_dopp_runs(dog_ctx* ctx, const DopIn& din, const FilterConst& fc, int par, cudaStream_t st)
 {
     CK(cudaMemsetAsync(ctx->d_gmax, 0, (size_t)ctx->C * 4, st));
-    CK(launch(k_dopp_g, ctx->tiles, 256, 0, st, 0, (const uint16_t*)ctx->lperm, ctx->tp, (const float4*)ctx->pst, din,
+    CK(launch(k_dopp_g, ctx->tiles, 256, 0, st, 0, ctx->tp, (const float2*)ctx->pv, din,
               ctx->d_gmax, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
     CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, ctx->tp, din, (const uint32_t*)ctx->d_gmax, ctx->d_rg,
               ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
@@ -782,8 +788,8 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     // tiles without a Doppler cell's members: the closed-form kernel; the others: per-member weights
     if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
     NextState ns{ctx->st, nullptr};
-    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                 (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
+    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, ctx->tp,
+                 (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
                  (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const uint32_t*)ctx->d_gfx,
                  (const DevScalars*)ctx->sc, fc, par));
     if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
@@ -957,8 +963,8 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
             return r;
         if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
         NextState ns{ctx->st, nullptr};
-        CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, (const uint16_t*)ctx->lperm, ctx->tp,
-                     (const float4*)ctx->pst, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
+        CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, ctx->tp,
+                     (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
                      (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const uint32_t*)ctx->d_gfx,
                      (const DevScalars*)ctx->sc, fc, par));
         if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
@@ -1330,6 +1336,7 @@ int64_t dog_get_debug(dog_ctx* ctx, int what, void* host_dst, size_t bytes)
         n = nu * 4;
         if (bytes < n) return DOG_E_INVAL;
         const int c = what - DOG_DBG_PRED_X;
+        if (!dbg) return DOG_E_STATE;              // input-order predicted state: debug builds only
         CK(cudaMemcpy2D(host_dst, 4, (const float*)ctx->pst + c, 16, 4, nu, cudaMemcpyDeviceToHost));
         return (int64_t)n;
     }

@@ -175,7 +175,7 @@ template <bool kExact>
 __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
-    uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* __restrict__ sc, FilterConst fc, float alpha,
+    uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* sc, FilterConst fc, float alpha,
     const float4* __restrict__ obs)
 {
     PDL_ENTER();
@@ -409,7 +409,7 @@ __device__ __forceinline__ ulonglong2 cluster_offsets(ulonglong2 t, ulonglong2* 
 __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList L, BlockTotals bt, uint32_t nblk,
                                                           uint32_t chunk, uint32_t* __restrict__ cell2list,
                                                           const uint64_t* __restrict__ A_all,
-                                                          DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+                                                          DevScalars* sc, FilterConst fc, int64_t k)
 {
     PDL_ENTER();
     namespace cg = cooperative_groups;
@@ -569,7 +569,7 @@ struct WideScan {
 // A_all: born mass of every shard (band contexts) or nullptr: the born-mass CDF then starts at the
 // prefix of the shards below and A is the global total (as in k_list_scan).
 __global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nblk, WideScan ws,
-                                                     DevScalars* __restrict__ sc, const uint64_t* __restrict__ A_all,
+                                                     DevScalars* sc, const uint64_t* __restrict__ A_all,
                                                      FilterConst fc)
 {
     PDL_ENTER();
@@ -606,7 +606,7 @@ __global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nb
 
 __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, BlockTotals bt, uint32_t chunk,
                                                     uint32_t* __restrict__ cell2list, WideScan ws,
-                                                    const DevScalars* __restrict__ sc, FilterConst fc)
+                                                    const DevScalars* sc, FilterConst fc)
 {
     PDL_ENTER();
     __shared__ uint64_t s_w[9];
@@ -680,7 +680,7 @@ __global__ __launch_bounds__(1024) void k_ls_prefix2(uint32_t nblk, WideScan ws)
 }
 
 __global__ __launch_bounds__(256) void k_ls_chunks2(CellList L, BlockTotals bt, WideScan ws,
-                                                    DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+                                                    DevScalars* sc, FilterConst fc, int64_t k)
 {
     PDL_ENTER();
     __shared__ uint64_t s_w[9];

@@ -29,6 +29,7 @@ struct DevScalars {
                                  // further above (k_pack_migrants; read by the receivers)
     uint32_t mig_over;           // sticky: a receive exceeded the migrant capacity (cycle not exact)
     uint32_t pad2;
+    double nu_over_W;            // nu / Wtot in fp64 (k_pair_sort), for the resampling kernels
 };
 
 constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
@@ -89,7 +90,15 @@ __device__ __forceinline__ unsigned long long gtimer_ns()
 // Programmatic dependent launch (every kernel of a cycle is launched with the PDL attribute): a kernel
 // lets the next one launch as soon as all its CTAs are running, and waits for its predecessor's results
 // (full completion and memory flush) before touching them.  Hides the launch gap between kernels.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The wait is followed by a gpu-scope acquire fence: an early-launched CTA shares its SM's L1 with CTAs
+// of the predecessor, which may have cached a line (e.g. of DevScalars) before another predecessor CTA
+// wrote it; griddepcontrol.wait alone does not invalidate the L1, the acquire fence does (measured: without
+// it, k_resample_tiles read a stale nu / W and placed copies one cycle off).
+__device__ __forceinline__ void pdl_wait()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 #define PDL_ENTER() do { pdl_trigger(); pdl_wait(); } while (0)
 

@@ -101,10 +101,9 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
 // ---- k_dopp_g: the likelihood g of every member of a Doppler cell (f32 bits per sorted position, in
 //      gfx_out) and the cell's largest g (gmax[cell], integer atomicMax on the bits of a nonnegative float:
 //      order-free).  gmax must be zero on entry (the caller clears it).
-__global__ __launch_bounds__(256) void k_dopp_g(const uint16_t* __restrict__ lperm, TilePairs tp,
-                                                const float4* __restrict__ pred, DopIn din,
+__global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __restrict__ pv, DopIn din,
                                                 uint32_t* __restrict__ gmax, uint32_t* __restrict__ gfx_out,
-                                                const DevScalars* __restrict__ sc, FilterConst fc, int par)
+                                                const DevScalars* sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
@@ -135,8 +134,8 @@ __global__ __launch_bounds__(256) void k_dopp_g(const uint16_t* __restrict__ lpe
         }
         uint32_t gb = 0u;
         if (pa > 0.0f) {
-            const float4 X = pred[pbase + lperm[base + p]];
-            const float g = doppler_g(X.z, X.w, d);
+            const float2 V = pv[pbase + p];                 // the tile's predicted state is in sorted order
+            const float g = doppler_g(V.x, V.y, d);
             gb = g > 0.0f ? __float_as_uint(g) : 0u;            // NaN / 0 -> no weight
             mx = max(mx, gb);
         }
@@ -151,7 +150,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(const uint16_t* __restrict__ lpe
 //      (k_dopp_g) on entry and gfx on exit.
 __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, const uint32_t* __restrict__ gmax,
                                                    uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
-                                                   uint32_t* __restrict__ gfx_io, const DevScalars* __restrict__ sc,
+                                                   uint32_t* __restrict__ gfx_io, const DevScalars* sc,
                                                    FilterConst fc, int par)
 {
     PDL_ENTER();
@@ -198,17 +197,16 @@ struct RdSmem {
     MomPartial pa[256], pb[256];   // first / last run segment of each thread (spanning runs)
     uint64_t scan[9];
     uint16_t first[kSortTile + 1];
-    uint16_t lp[kSortTile];
 };
 constexpr size_t kRdSmemBytes = sizeof(RdSmem);
 
-__global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __restrict__ lperm, TilePairs tp,
-                                                       const float4* __restrict__ pred, CellList L, NextState out,
+__global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const float2* __restrict__ pxy,
+                                                       const float2* __restrict__ pv, CellList L, NextState out,
                                                        MomPartial* __restrict__ ppart, DopIn din,
                                                        const uint64_t* __restrict__ rg, uint64_t* __restrict__ rs,
                                                        const uint64_t* __restrict__ GS, const uint8_t* __restrict__ tflag,
                                                        const uint32_t* __restrict__ gfx_in,
-                                                       const DevScalars* __restrict__ sc, FilterConst fc, int par)
+                                                       const DevScalars* sc, FilterConst fc, int par)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -226,7 +224,6 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
     const RunInfo* __restrict__ runs = tp.run + base;
-    for (uint32_t p = tid; p < n; p += 256) S.lp[p] = lperm[base + p];
     for (uint32_t r = tid; r < nd; r += 256) S.first[r] = tp.first[base + r];
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
@@ -319,7 +316,8 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(const uint16_t* __rest
                 Q0 = (uint64_t)mr * q.bp + min(mr, q.rpm);
                 Q1 = (uint64_t)(mr + 1) * q.bp + min(mr + 1, q.rpm);
             }
-            const float4 X = pred[pbase + S.lp[p]];
+            const float2 XY = pxy[pbase + p], VV = pv[pbase + p];   // sorted order
+            const float4 X = make_float4(XY.x, XY.y, VV.x, VV.y);
             if (rc.W) {
                 const uint32_t F0 = have ? Fc : fcount(q.P + Q0, rc), F1 = fcount(q.P + Q1, rc);
                 DOG_ASSERT(F0 <= F1 && F1 <= fc.nu);

@@ -119,42 +119,36 @@ __device__ __forceinline__ void write_copies(bool valid, uint32_t F0, uint32_t F
 #define RT_MINB (1024 / RT_THREADS)
 #endif
 constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // sorted positions per thread
-static_assert(kRtItems % 8 == 0, "phase B works in batches of 8 positions");
-constexpr int kRtRunCache = 96;                                       // runs whose RunF sits in smem (rest: global)
+static_assert(kRtItems % 8 == 0, "16-byte vector loads of the tile arrays");
 constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
-constexpr int kRtWin = 8192;                                          // compact outputs per phase-C window
-constexpr int kRtWinItems = kRtWin / kRtThreads;                      // 32 window entries per thread
 
-// Per run, everything the owner marks need: F(Q_r) of member r = pre + k (k = position - first) is
-// ceil(y) with y = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
-// pieces, steps bp + 1 and bp); D = F(Q_pre) - the run's offset in the tile's compact output space.
+constexpr int kRtRunCache = 256;                                      // runs whose RunF sits in smem (rest: global)
+
+// Per run, what the copy pass needs to place member r = pre + k (k = position - first): F(Q_r) =
+// ceil(y(r)) with y(r) = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
+// pieces, steps bp + 1 and bp; yR = y0 + rpm d1, d2 = d1 - nu/W).
 struct RunF {
-    double y0, d1;          // the second piece (members beyond rpm) is derived: yR = y0 + rpm d1, d2 = d1 - nu/W
-    uint32_t pre, rpm, D, pad;
+    double y0, d1;
+    uint32_t pre, rpm, first, pad;
 };
 static_assert(sizeof(RunF) == 32, "RunF: two per 64-byte line");
 
-struct RtSmem {   // dynamic shared memory of k_resample_tiles (~47 KB: three blocks per SM with a large L1)
-    uint16_t lp[kSortTile];            // local sorted position -> local index
-    uint16_t first[kSortTile + 8];     // run starts (first[nd] = n)
-    uint16_t runof[kSortTile];         // sorted position -> run
-    alignas(16) RunF rf[kRtRunCache];
-    union alignas(16) {
-        struct { MomPartial pa[kRtThreads], pb[kRtThreads]; } m;   // phase B -> phase R
-        uint16_t osrc[kRtWin];         // phase C: compact output -> owner position + 1
-    } u;
-    uint32_t scan[kRtThreads / 32 + 1];
+struct RtSmem {   // dynamic shared memory of k_resample_tiles (~8.6 KB)
+    RunF rf[kRtRunCache];
+    uint32_t starts[kSortTile / 32];   // bitmap of run starts over the tile's sorted positions
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
-    uint32_t nlong;                    // runs spanning more than kRtShortSpan threads (phase R)
-    uint16_t longr[32];
-    uint32_t slow;                     // an estimate was too close to an integer: exact marks needed
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
-static_assert(offsetof(RtSmem, u) % 16 == 0 && offsetof(RtSmem, runof) % 16 == 0, "vector smem access");
+
+// Q of member mr of a run's cell: P + mr bp + min(mr, rpm) (even split of the cell's R_p, A-23).
+__device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
+{
+    return q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
+}
 
 // ceil(y) clamped to [0, nu] when y is further than `margin` from an integer; otherwise *amb is set (the
-// caller redoes the work with exact products).  The per-run linear estimates are within ~nu 2^-50 of
-// the exact value, so margin = max(2^-22, nu 2^-48) keeps every accepted ceil exact.
+// caller settles it with exact products).  The per-run linear estimates are within ~nu 2^-50 of the exact
+// value, so margin = max(2^-22, nu 2^-48) keeps every accepted ceiling exact.
 __device__ __forceinline__ double fast_ceil_margin(uint32_t nu) { return fmax(0x1p-22, (double)nu * 0x1p-48); }
 __device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, double margin, bool& amb)
 {
@@ -166,53 +160,70 @@ __device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, double marg
     return (uint32_t)cy;
 }
 
-// Block-wide exclusive max-scan of one value per thread (values >= 0).
-__device__ __forceinline__ uint32_t block_excl_max(uint32_t v, uint32_t* s_warp)
+// Warp-cooperative write of the copies of 32 members (lanes) whose output ranges [F0_l, F0_l + c_l) are
+// arbitrary (members of different runs own ranges far apart): the copies are numbered compactly over
+// the lanes (exclusive prefix of c), and 32 consecutive copy numbers are written per round; the owner of
+// copy o is the last lane whose prefix is <= o (a 5-step shuffle search).  Consecutive copies of a run
+// are consecutive outputs, so the stores coalesce within runs; the rounds are balanced whatever the copy
+// counts (a member can own hundreds of outputs).
+__device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const float4& X, uint32_t J, NextState& out,
+                                              uint32_t nu)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t inc = v;
+    const int lane = threadIdx.x & 31;
+    if (__reduce_max_sync(0xffffffffu, c) <= 2u) {         // the common case: each lane writes its own
+        for (uint32_t k = 0; k < c; ++k) {                 // (consecutive members of a run own
+            DOG_ASSERT(F0 + k < nu);                       //  consecutive outputs: coalesced)
+            out.s[F0 + k] = X;
+            if (out.jidx) out.jidx[F0 + k] = J;
+        }
+        return;
+    }
+    uint32_t incl = c;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc = max(inc, o);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
     }
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    uint32_t pre = 0;
-    for (int w = 0; w < warp; ++w) pre = max(pre, s_warp[w]);
-    const uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    __syncthreads();
-    return max(pre, lane ? ex : 0u);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t ex = incl - c;
+    for (uint32_t o0 = 0; o0 < total; o0 += 32) {
+        const uint32_t o = o0 + lane;
+        int own = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const uint32_t e = __shfl_sync(0xffffffffu, ex, own + step);
+            if (e <= o) own += step;
+        }
+        const uint32_t dst = __shfl_sync(0xffffffffu, F0, own) + (o - __shfl_sync(0xffffffffu, ex, own));
+        const float4 V = make_float4(__shfl_sync(0xffffffffu, X.x, own), __shfl_sync(0xffffffffu, X.y, own),
+                                     __shfl_sync(0xffffffffu, X.z, own), __shfl_sync(0xffffffffu, X.w, own));
+        const uint32_t jj = out.jidx ? __shfl_sync(0xffffffffu, J, own) : 0u;
+        if (o < total) {
+            DOG_ASSERT(dst < nu);
+            out.s[dst] = V;
+            if (out.jidx) out.jidx[dst] = jj;
+        }
+    }
+    (void)nu;
 }
 
-// Q of member mr of a run's cell: P + mr bp + min(mr, rpm) (even split of the cell's R_p, A-23).
-__device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
-{
-    return q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
-}
-
-// Persistent particles, one block per sort tile (4096 particles in input order; lperm gives their
-// stable cell order).
-//   phase B (thread t owns sorted positions [16t, 16t+16)): run of every position, batched gathers of
-//     the predicted velocities, velocity sums per run segment (runs inside a thread -> ppart directly).
-//   phase R (thread per run): run segments spanning threads combined in thread order (deterministic)
-//     -> ppart; the run's output range [F(Q_first), F(Q_end)) and its offset in the tile's compact
-//     output space (the runs' ranges concatenated).
-//   phase C, per window of 4096 compact outputs: lanes take consecutive positions, compute F(Q_r) of
-//     their member (the next member's from the neighbour lane) and mark the member's first output; a
-//     block max-scan spreads the owner over its outputs; threads write consecutive outputs (coalesced,
-//     balanced whatever the copy counts).
+// Persistent particles, one block per sort tile: the tile's predicted state arrives in sorted (cell)
+// order (k_predict_sort), so warp w walks sorted positions [512 w, 512 w + 512) 32 at a time, lanes on
+// consecutive positions -- every read is coalesced.  Member r of its cell owns the outputs
+// [F(Q_r), F(Q_{r+1})) (A-24): F from the run's linear estimate, exact whenever the estimate is clear of an
+// integer, else from exact 128-bit products (dog_fcount.cuh); the warp writes its 32 members' copies
+// with write_compact.  The run of a position comes from a bitmap of run starts (popcount), the run's F
+// parameters from shared memory.  (The velocity moments are summed per cell by k_moments.)
 template <bool kDbg>
-__global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
-    const uint16_t* __restrict__ lperm, TilePairs tp, const float4* __restrict__ pred, CellList L, NextState out,
-    uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
-    const DevScalars* __restrict__ sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip)
+__global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
+    const uint16_t* __restrict__ lperm, TilePairs tp, const float2* __restrict__ pxy, const float2* __restrict__ pv,
+    CellList L, NextState out, uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
+    const DevScalars* sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip)
 {
     PDL_ENTER();
-    const double fmargin = fast_ceil_margin(fc.nu);
     extern __shared__ __align__(16) uint8_t smem_raw[];
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x, base = t * kSortTile;     // this tile's slot in the per-tile arrays
     const RsConst rc = make_rsconst(sc, fc.nu);
     const uint32_t n_lo = sc->n_lo, n_loc = n_lo + sc->n_own[par] + sc->n_hi;
@@ -229,291 +240,109 @@ __global__ __launch_bounds__(kRtThreads, RT_MINB) void k_resample_tiles(
     if (n == 0) return;
     if (tskip && tskip[t]) return;                                 // a Doppler tile (k_resample_dopp)
     const uint32_t nd = tp.nd[t];
-    const uint32_t p0 = tid * kRtItems;
     const RunInfo* __restrict__ runs = tp.run + base;
-    PHASE_BEGIN();
-    // ---- phase A: local permutation, run starts
-    const float2* __restrict__ pv = reinterpret_cast<const float2*>(pred);   // (x, y), (vx, vy) halves
-    {
-        uint4 a = make_uint4(0, 0, 0, 0), b = a, c = a, d = a;
-#pragma unroll
-        for (int h = 0; h < kRtItems / 8; ++h) {
-            if (p0 < n) { a = reinterpret_cast<const uint4*>(lperm + base + p0)[h]; reinterpret_cast<uint4*>(S.lp + p0)[h] = a; }
-            if (p0 < nd) { c = reinterpret_cast<const uint4*>(tp.first + base + p0)[h]; reinterpret_cast<uint4*>(S.first + p0)[h] = c; }
-        }
-        (void)b; (void)d;
-        if (tid == 0) { S.slow = 0u; S.nlong = 0u; }
-        if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
-    }
+    // ---- run starts (bitmap) and the runs' F parameters
+    for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) S.starts[w] = 0u;
+    if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     __syncthreads();
-    if (tid == 0) S.first[nd] = (uint16_t)n;
-    __syncthreads();
-    const uint32_t srun = S.sentinel_run;
-    auto runf = [&](uint32_t j) -> const RunF& { return j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j]; };
-
-    PHASE_MARK(0);
-    // ---- phase B: run of every position, velocity sums per run segment
-    if (p0 < n) {
-        uint32_t lo = 0, hi = nd;                           // run containing p0
-        while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (S.first[m] <= p0) lo = m; else hi = m; }
-        uint32_t j = lo, first = S.first[j], end = S.first[j + 1];
-        double acc[5] = {0, 0, 0, 0, 0};
-        bool first_seg = true;
-        auto flush = [&]() {
-            MomPartial mp;
-#pragma unroll
-            for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
-            if (j != srun) {
-                if (first >= p0 && end <= p0 + kRtItems) ppart[base + j] = mp;    // run inside this thread
-                else if (first_seg) S.u.m.pa[tid] = mp;
-                else S.u.m.pb[tid] = mp;
-            }
-            first_seg = false;
-        };
-#pragma unroll 1
-        for (int h = 0; h < kRtItems / 8; ++h) {            // batches of 8 positions
-            uint32_t src[8], rpk[4];
-            {
-                const uint4 a = reinterpret_cast<const uint4*>(S.lp + p0)[h];
-                const uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u) { src[2 * u] = pbase + (w[u] & 0xFFFFu); src[2 * u + 1] = pbase + (w[u] >> 16); }
-            }
-            float2 V[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                V[u] = (p0 + 8 * h + u < n) ? pv[2 * (size_t)src[u] + 1] : make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t p = p0 + 8 * h + u;
-                if (p < n) {
-                    if (p >= end) {                         // next run
-                        flush();
-                        ++j; first = end; end = S.first[j + 1];
-                    }
-                    if (j != srun) {
-                        const double a = (double)V[u].x, bq = (double)V[u].y;
-                        acc[0] += a; acc[1] += bq; acc[2] += a * a; acc[3] += bq * bq; acc[4] += a * bq;
-                        if (kDbg) {
-                            const RunInfo q = runs[j];
-                            perm_dbg[q.jbase - L.sb[q.li] + q.pre + (p - first)] = src[u];
-                        }
-                    }
-                }
-                if (u & 1) rpk[u >> 1] |= j << 16; else rpk[u >> 1] = j;
-            }
-            reinterpret_cast<uint4*>(S.runof + p0)[h] = make_uint4(rpk[0], rpk[1], rpk[2], rpk[3]);
-        }
-        flush();
-    }
-    __syncthreads();
-    PHASE_MARK(1);
-    // ---- phase R: spanning run segments -> ppart; output range and compact offset of every run
-    uint32_t carry = 0;
-    for (uint32_t r0 = 0; r0 < nd; r0 += kRtThreads) {
-        const uint32_t r = r0 + tid;
-        const bool live = r < nd && r != srun;
-        uint32_t Flo = 0, c = 0;
-        RunF x{};
-        if (live) {
-            const uint32_t f = S.first[r], e = S.first[r + 1];
-            const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
-            bool by_warp = false;
-            if (tl - tf > kRtShortSpan) {                   // long run: combined by a warp after this loop
-                const uint32_t k = atomicAdd(&S.nlong, 1u);
-                if (k < 32u) { S.longr[k] = (uint16_t)r; by_warp = true; }
-            }
-            if (tf != tl && !by_warp) {                     // segments over threads tf..tl, in thread order
-                const MomPartial& m0 = (f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf];
-                double s5[5];
-#pragma unroll
-                for (int i = 0; i < 5; ++i) s5[i] = m0.s[i];
-                for (uint32_t u = tf + 1; u <= tl; ++u)
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) s5[i] += S.u.m.pa[u].s[i];
-                MomPartial mp;
-#pragma unroll
-                for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
-                ppart[base + r] = mp;
-            }
-            if (rc.W) {   // F at the run's ends from the same linear estimate phase C uses (exact unless
-                          // ambiguous, then the exact 128-bit count)
-                const RunInfo q = runs[r];
-                x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
-                x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
-                x.pre = q.pre; x.rpm = q.rpm;
-                x.pad = 0u;
-                const double yR = __fma_rn((double)x.rpm, x.d1, x.y0), d2 = x.d1 - rc.nu_over_W;
-                auto yof = [&](uint32_t mr) {
-                    return mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
-                };
-                bool amb = false;
-                Flo = fast_ceil(yof(q.pre), rc.nu, fmargin, amb);
-                uint32_t Fhi = fast_ceil(yof(q.pre + (e - f)), rc.nu, fmargin, amb);
-                if (amb) {
-                    Flo = fcount(member_Q(q, q.pre), rc);
-                    Fhi = fcount(member_Q(q, q.pre + (e - f)), rc);
-                }
-                c = Fhi - Flo;
-            }
-        }
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan<uint32_t, kRtThreads / 32>(c, S.scan, tot);
-        if (live && rc.W) {
-            x.D = Flo - (carry + ex);
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        const uint32_t f = tp.first[base + r];
+        atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
+        if (rc.W) {
+            const RunInfo q = runs[r];
+            RunF x;
+            x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
+            x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
+            x.pre = q.pre; x.rpm = q.rpm; x.first = f; x.pad = 0u;
             if (r < (uint32_t)kRtRunCache) S.rf[r] = x; else rf_g[base + r] = x;
         }
-        carry += tot;
     }
     __syncthreads();
-    {   // long runs: their thread partials summed by one warp each (fixed lane tree: deterministic)
-        const uint32_t nlong = min(S.nlong, 32u);
-        if (nlong > 0u) {
-            const int warp = tid >> 5, lane = tid & 31;
-            for (uint32_t k = warp; k < nlong; k += kRtThreads / 32) {
-                const uint32_t r = S.longr[k];
-                const uint32_t f = S.first[r], e = S.first[r + 1];
-                const uint32_t tf = f / kRtItems, tl = (e - 1) / kRtItems;
-                double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-                for (uint32_t u = tf + 1 + lane; u <= tl; u += 32)
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) s5[i] += S.u.m.pa[u].s[i];
-#pragma unroll
-                for (int d = 16; d; d >>= 1)
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], d);
-                if (lane == 0) {
-                    const MomPartial& m0 = (f > tf * kRtItems) ? S.u.m.pb[tf] : S.u.m.pa[tf];
-                    MomPartial mp;
-#pragma unroll
-                    for (int i = 0; i < 5; ++i) mp.s[i] = m0.s[i] + s5[i];
-                    ppart[base + r] = mp;
-                }
+    const uint32_t srun = S.sentinel_run;
+    const double margin = fast_ceil_margin(fc.nu);
+    // ---- copies: warp w, sorted positions [512 w, 512 w + 512), 32 per round
+    constexpr uint32_t kSpan = kSortTile / (kRtThreads / 32);
+    const uint32_t w0 = warp * kSpan;                      // (warps beyond n skip the loop, not the barrier)
+    int jprev = -1;                                         // run of position w0 - 1
+    {
+        uint32_t c = 0;
+        for (uint32_t k = lane; k < w0 / 32; k += 32) c += __popc(S.starts[k]);
+        jprev += (int)__reduce_add_sync(0xffffffffu, c);
+    }
+    const uint32_t wend = w0 < n ? min(w0 + kSpan, n) : w0;
+    for (uint32_t p0 = w0; p0 < wend; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const uint32_t word = S.starts[p0 >> 5];
+        const uint32_t j = (uint32_t)(jprev + (int)__popc(lane == 31 ? word : (word & ((2u << lane) - 1u))));
+        jprev += (int)__popc(word);
+        const bool mem = p < wend && j != srun;
+        float2 XY = make_float2(0.f, 0.f), V = XY;
+        if (mem) { XY = pxy[pbase + p]; V = pv[pbase + p]; }   // coalesced, issued early
+        uint32_t c = 0, F0 = 0, Jd = 0;
+        if (mem) {
+            const RunF x = j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j];
+            const uint32_t mr = x.pre + (p - x.first);
+            const double yR = __fma_rn((double)x.rpm, x.d1, x.y0), d2 = x.d1 - rc.nu_over_W;
+            const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
+            const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0)
+                                         : __fma_rn((double)(mr + 1u - x.rpm), d2, yR);
+            bool amb = false;
+            uint32_t a0 = fast_ceil(y0, rc.nu, margin, amb), a1 = fast_ceil(y1, rc.nu, margin, amb);
+            if (amb) {                                      // rare: settle with exact products
+                const RunInfo q = runs[j];
+                const uint64_t Q0 = member_Q(q, mr);
+                a0 = fcount(Q0, rc);
+                a1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
             }
-            __syncthreads();                                // phase C reuses the partials' memory
+            DOG_ASSERT(a0 <= a1 && a1 <= fc.nu);
+            F0 = a0; c = a1 - a0;
+            if (kDbg) {
+                const RunInfo q = runs[j];
+                Jd = q.jbase + mr;
+                perm_dbg[q.jbase - L.sb[q.li] + mr] = pbase + lperm[base + p];
+            }
+        }
+        write_compact(c, F0, make_float4(XY.x, XY.y, V.x, V.y), Jd, out, fc.nu);
+    }
+    // ---- velocity sums per run (Eqs. 81-84; k_moments combines a cell's runs in tile order), from the
+    //      sorted predicted velocities just read (L1 / L2): runs of >= 16 members by a warp each (lanes
+    //      strided, fixed butterfly), shorter runs by one lane each in member order -- deterministic
+    const uint32_t nw = kRtThreads / 32;
+    for (uint32_t r = warp; r < nd; r += nw) {            // long runs: warp per run
+        if (r == srun) continue;
+        const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
+        if (e - f < 16u) continue;
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (uint32_t q = f + lane; q < e; q += 32) {
+            const float2 V = pv[pbase + q];
+            const double a = (double)V.x, b = (double)V.y;
+            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], d);
+        if (lane == 0) {
+            MomPartial mp;
+#pragma unroll
+            for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+            ppart[base + r] = mp;
         }
     }
-    const uint32_t Ot = carry;
-    PHASE_MARK(2);
-    // ---- phase C: windows of the compact output space
-    uint16_t* os = S.u.osrc;
-    const uint32_t q0 = tid * kRtWinItems;                  // this thread's window entries in the max-scan
-    for (uint32_t w0 = 0; w0 < Ot; w0 += kRtWin) {
-#pragma unroll
-        for (int i = 0; i < kRtWinItems / 8; ++i) reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(0, 0, 0, 0);
-        __syncthreads();
-        bool amb = false;
-        if (p0 < n) {   // members with copies mark their first output in the window: thread-contiguous
-                        // positions, the run's F parameters held in registers, F(Q_{r+1}) reused as the next
-                        // member's F(Q_r)
-            const uint32_t pend = min(p0 + (uint32_t)kRtItems, n);
-            uint32_t j = S.runof[p0], end = S.first[j + 1];
-            RunF x{};
-            double yR = 0.0, d2 = 0.0;                      // the run's second piece (see RunF)
-            uint32_t xfirst = S.first[j];
-            auto load = [&]() { x = runf(j); yR = __fma_rn((double)x.rpm, x.d1, x.y0); d2 = x.d1 - rc.nu_over_W; };
-            if (j != srun) load();
-            bool have = false;
-            uint32_t Fc = 0;
-            for (uint32_t p = p0; p < pend; ++p) {
-                if (p >= end) {
-                    j = S.runof[p]; xfirst = end; end = S.first[j + 1];
-                    if (j != srun) load();
-                    have = false;
-                }
-                if (j == srun) continue;
-                const uint32_t mr = x.pre + (p - xfirst);
-                uint32_t F0 = Fc;
-                if (!have) {
-                    const double y = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
-                    F0 = fast_ceil(y, rc.nu, fmargin, amb);
-                }
-                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0) : __fma_rn((double)(mr + 1u - x.rpm), d2, yR);
-                const uint32_t F1 = fast_ceil(y1, rc.nu, fmargin, amb);
-                Fc = F1;
-                have = true;
-                const uint32_t C0 = F0 - x.D, C1 = F1 - x.D;
-                if (C1 > C0 && C1 > w0 && C0 < w0 + kRtWin) os[max(C0, w0) - w0] = (uint16_t)(p + 1u);
-            }
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {     // short runs: lane per run
+        if (r == srun) continue;
+        const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
+        if (e - f >= 16u) continue;
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (uint32_t q = f; q < e; ++q) {
+            const float2 V = pv[pbase + q];
+            const double a = (double)V.x, b = (double)V.y;
+            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
         }
-        if (amb) S.slow = 1u;
-        __syncthreads();
-#ifdef DOG_TIMING
-        if (S.slow && tid == 0) atomicAdd(&g_phase_ns[20], 1ull);
-        if (tid == 0) atomicAdd(&g_phase_ns[21], 1ull);
-#endif
-        if (S.slow) {   // rare: some estimate was ambiguous -- redo the marks with exact products
+        MomPartial mp;
 #pragma unroll
-            for (int i = 0; i < kRtWinItems / 8; ++i) reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(0, 0, 0, 0);
-            __syncthreads();
-            for (int it = 0; it < kRtItems; ++it) {
-                const uint32_t p = it * kRtThreads + tid;
-                if (p >= n) break;
-                const uint32_t j = S.runof[p];
-                if (j == srun) continue;
-                const RunInfo q = runs[j];
-                const RunF& x = runf(j);
-                const uint32_t mr = q.pre + (p - S.first[j]);
-                const uint64_t Q0 = member_Q(q, mr);
-                const uint32_t C0 = fcount(Q0, rc) - x.D;
-                const uint32_t C1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc) - x.D;
-                if (C1 > C0 && C1 > w0 && C0 < w0 + kRtWin) os[max(C0, w0) - w0] = (uint16_t)(p + 1u);
-            }
-            __syncthreads();
-        }
-        PHASE_MARK(3);
-        {   // inclusive max-scan over the window: thread-contiguous 32 entries (u16 pairs)
-            uint32_t v[kRtWinItems / 2];
-#pragma unroll
-            for (int i = 0; i < kRtWinItems / 8; ++i) {
-                const uint4 x = reinterpret_cast<const uint4*>(os + q0)[i];
-                v[4 * i] = x.x; v[4 * i + 1] = x.y; v[4 * i + 2] = x.z; v[4 * i + 3] = x.w;
-            }
-            uint32_t run = 0;
-#pragma unroll
-            for (int i = 0; i < kRtWinItems / 2; ++i) {
-                const uint32_t lo = max(v[i] & 0xFFFFu, run), hi = max(v[i] >> 16, lo);
-                v[i] = lo | (hi << 16);
-                run = hi;
-            }
-            const uint32_t pre = block_excl_max(run, S.scan);
-            const uint32_t pre2 = pre | (pre << 16);
-#pragma unroll
-            for (int i = 0; i < kRtWinItems / 8; ++i)
-                reinterpret_cast<uint4*>(os + q0)[i] = make_uint4(__vmaxu2(v[4 * i], pre2), __vmaxu2(v[4 * i + 1], pre2),
-                                                                  __vmaxu2(v[4 * i + 2], pre2), __vmaxu2(v[4 * i + 3], pre2));
-        }
-        __syncthreads();
-        PHASE_MARK(4);
-        const uint32_t wn = min((uint32_t)kRtWin, Ot - w0);
-#pragma unroll 1
-        for (uint32_t i0 = 0; i0 < wn; i0 += 4 * kRtThreads) {
-            uint32_t o[4], src[4], J[4];
-            bool ok[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                const uint32_t i = i0 + h * kRtThreads + tid;
-                ok[h] = i < wn;
-                const uint32_t p = (uint32_t)os[ok[h] ? i : 0u] - 1u;
-                const uint32_t j = S.runof[p];
-                o[h] = w0 + i + runf(j).D;
-                src[h] = pbase + S.lp[p];
-                J[h] = 0;
-                if (kDbg) { const RunInfo q = runs[j]; J[h] = q.jbase + q.pre + (p - S.first[j]); }
-            }
-            float4 X[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) X[h] = pred[src[h]];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                if (!ok[h]) continue;
-                DOG_ASSERT(o[h] < fc.nu);
-                out.s[o[h]] = X[h];
-                if (kDbg) out.jidx[o[h]] = J[h];
-            }
-        }
-        __syncthreads();
-        PHASE_MARK(5);
+        for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+        ppart[base + r] = mp;
     }
 }
 
@@ -525,7 +354,7 @@ constexpr int kMoSmall = 4;   // kBatch (exact filter): cells with <= 4 runs sum
 template <bool kBatch>
 __global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
                                                  const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
-                                                 float* __restrict__ cov, const DevScalars* __restrict__ sc,
+                                                 float* __restrict__ cov, const DevScalars* sc,
                                                  const uint64_t* __restrict__ GSd)
 {
     PDL_ENTER();
@@ -586,7 +415,7 @@ __device__ __forceinline__ void birth_assoc_split(uint64_t Rb, uint32_t nb, floa
 // dpA / ddop: the Doppler grid of the cycle (NEXT-1) or nullptr: slots r < nu_A of a cell with p_A > 0
 // form the associated set (velocity from p(x | z)), sharing R_bA; the rest share R_b - R_bA (A-36).
 __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, BirthDebug bdbg,
-                                                const DevScalars* __restrict__ sc, FilterConst fc, int64_t k,
+                                                const DevScalars* sc, FilterConst fc, int64_t k,
                                                 const float* __restrict__ dpA, const float4* __restrict__ ddop)
 {
     PDL_ENTER();
@@ -682,7 +511,7 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
 // idle).  Slot s belongs to the last list entry with sb <= s; same draws, state and joint CDF as
 // k_births (no Doppler split); copies written by the slot's own thread.
 __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out, BirthDebug bdbg,
-                                                      const DevScalars* __restrict__ sc, FilterConst fc, int64_t k)
+                                                      const DevScalars* sc, FilterConst fc, int64_t k)
 {
     PDL_ENTER();
     const RsConst rc = make_rsconst(sc, fc.nu);

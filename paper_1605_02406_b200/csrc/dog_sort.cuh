@@ -97,11 +97,17 @@ __device__ __forceinline__ uint32_t local_key(uint32_t kg, const FilterConst& fc
 // whole-grid context, predict + sort fused (own particles only).  !kPredict: band context, the tile's
 // particles were predicted by k_predict_band (own) or by the neighbour shard (migrants): keys only.
 // Warp w owns positions [512 w, 512 w + 512) as 16 rows of 32 lanes (position = 512 w + 32 i + lane).
+//
+// The predicted state leaves the kernel IN SORTED ORDER, as two halves: pxy[s0 + tb + p] = (x, y) and
+// pv[s0 + tb + p] = (vx, vy) of the particle at sorted position p of the tile (staged through shared
+// memory after the sort: every later pass reads it coalesced, in cell order).  kPredict writes the
+// predicted halves in input order first and permutes them in place; !kPredict reads the band's records
+// (pst, input order) and writes the halves.  pst (kPredict) and lperm are debug outputs (may be null).
 template <bool kPredict>
 __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
-    const float4* __restrict__ st, float4* __restrict__ pst, uint32_t* __restrict__ keys_dbg,
-    uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs,
-    DevScalars* __restrict__ sc, FilterConst fc, StepArgs a, uint32_t* __restrict__ kscr)
+    const float4* __restrict__ st, float4* __restrict__ pst, float2* __restrict__ pxy, float2* __restrict__ pv,
+    uint32_t* __restrict__ keys_dbg, uint16_t* __restrict__ lperm, TilePairs tp, uint32_t* __restrict__ counts,
+    uint32_t* __restrict__ npairs, DevScalars* sc, FilterConst fc, StepArgs a, uint32_t* __restrict__ kscr)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -137,7 +143,9 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
             float4 P;
             if (kPredict) {
                 P = predict_one(st[g], o_base + (g - fc.lo_cap), fc, a);
-                pst[g] = P;
+                pxy[g] = make_float2(P.x, P.y);
+                pv[g] = make_float2(P.z, P.w);
+                if (pst) pst[g] = P;                        // debug: the predicted state in input order
             } else {
                 P = pst[g];
             }
@@ -297,11 +305,47 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     }
     if (tid == 0) tp.nd[blockIdx.x] = nd;
     PHASE_MARK(10);
-    // ---- local permutation (sorted position -> local input index), two per thread-step
-    for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
-        const uint32_t p = 2 * q;
-        const uint32_t v0 = sw[p] & ((1u << kPkIdx) - 1u), v1 = sw[p + 1] & ((1u << kPkIdx) - 1u);
-        reinterpret_cast<uint32_t*>(lperm + tb)[q] = v0 | (v1 << 16);
+    // ---- local permutation (sorted position -> local input index): debug dumps only
+    if (lperm)
+        for (uint32_t q = tid; 2 * q < n; q += kPsThreads) {
+            const uint32_t p = 2 * q;
+            const uint32_t v0 = sw[p] & ((1u << kPkIdx) - 1u), v1 = sw[p + 1] & ((1u << kPkIdx) - 1u);
+            reinterpret_cast<uint32_t*>(lperm + tb)[q] = v0 | (v1 << 16);
+        }
+    __syncthreads();                                        // s_start (S.rank) is free again
+    // ---- the predicted state in sorted order: inverse permutation, then each half staged through
+    //      shared memory (one 16 KB buffer per component) and written back coalesced
+    uint16_t* inv = S.rank;
+    for (uint32_t p = tid; p < n; p += kPsThreads) inv[sw[p] & ((1u << kPkIdx) - 1u)] = (uint16_t)p;
+    __syncthreads();
+    float* st0 = reinterpret_cast<float*>(S.k[0]);          // the records are dead now: both 16 KB
+    float* st1 = reinterpret_cast<float*>(S.k[1]);          // buffers stage one component each
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+        float2* dst = h ? pv : pxy;
+#pragma unroll 4
+        for (int i = 0; i < kPsRows; ++i) {
+            const uint32_t q = warp * (kPsRows * 32) + i * 32 + lane;
+            if (q < n) {
+                float2 v;
+                if (kPredict) {
+                    v = dst[base + q];
+                } else {
+                    const float4 P = pst[base + q];
+                    v = h ? make_float2(P.z, P.w) : make_float2(P.x, P.y);
+                }
+                const uint32_t p = inv[q];
+                st0[p] = v.x;
+                st1[p] = v.y;
+            }
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int i = 0; i < kPsRows; ++i) {
+            const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
+            if (p < n) dst[base + p] = make_float2(st0[p], st1[p]);
+        }
+        __syncthreads();
     }
     PHASE_MARK(11);
 }
@@ -322,7 +366,7 @@ struct Migrants {
 };
 
 __global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __restrict__ st, float4* __restrict__ pst,
-                                                             Migrants mg, DevScalars* __restrict__ sc, FilterConst fc,
+                                                             Migrants mg, DevScalars* sc, FilterConst fc,
                                                              StepArgs a)
 {
     PDL_ENTER();
@@ -382,7 +426,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __res
 // buffers (input order, one warp per tile copying lane-strided); totals go to DevScalars (read by the
 // receivers' k_gather_migrants, or by the host to size a transport).  A bucket beyond the capacity is
 // truncated and flagged (mig_over): the cycle then cannot complete exactly and the host reports it.
-__global__ __launch_bounds__(1024) void k_pack_migrants(Migrants mg, uint32_t tiles, DevScalars* __restrict__ sc)
+__global__ __launch_bounds__(1024) void k_pack_migrants(Migrants mg, uint32_t tiles, DevScalars* sc)
 {
     PDL_ENTER();
     __shared__ uint32_t s_run;
@@ -447,7 +491,7 @@ struct MigGather {
 // compacts the far buckets (rare) with block scans and publishes n_lo / n_hi.  A receive beyond the
 // capacity copies nothing and raises mig_over.
 __global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* __restrict__ pst,
-                                                          DevScalars* __restrict__ sc, FilterConst fc,
+                                                          DevScalars* sc, FilterConst fc,
                                                           uint32_t own_hi_cap, int par)
 {
     PDL_ENTER();
@@ -575,7 +619,7 @@ static_assert(kPsSmall == 4, "the sorting network below is for 4 entries");
 template <bool kBatch>
 __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uint32_t* __restrict__ plist,
                                                    uint32_t* __restrict__ ptmp, const uint64_t* __restrict__ W_all,
-                                                   DevScalars* __restrict__ sc, FilterConst fc, int par, DopPS dp)
+                                                   DevScalars* sc, FilterConst fc, int par, DopPS dp)
 {
     PDL_ENTER();
     __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
@@ -591,6 +635,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         sc->Wtot = Wtot;
         sc->Ppre = Ppre;
         sc->w_bar = Wtot ? __double2float_rn(__ddiv_rn(__dmul_rn((double)Wtot, 0x1p-40), (double)fc.nu)) : 0.0f;
+        sc->nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
         if (W_all) {
             RsConst r;
             r.W = Wtot; r.U = sc->U; r.nu = fc.nu;

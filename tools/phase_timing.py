@@ -12,8 +12,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_1605_02406_b200 import dog, inputs as I
 
-NAMES = {0: "rs A (loads)", 1: "rs B (moments, runof)", 2: "rs R (spanning, prefix)", 3: "rs C scatter (F)",
-         4: "rs C max-scan", 5: "rs C outputs", 8: "ps predict", 9: "ps radix passes", 10: "ps runs", 11: "ps lperm"}
+NAMES = {0: "rs A (loads)", 1: "rs B (moments, runof)", 2: "rs R (spanning segments)", 3: "rs C (F, copies)",
+         4: "rs long runs", 8: "ps predict", 9: "ps radix passes", 10: "ps runs", 11: "ps lperm"}
 cfg = I.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfgT"]
 sc = I.scene(cfg)
 f = dog.Filter.from_config(cfg)
