@@ -166,6 +166,7 @@ __device__ __forceinline__ uint32_t fast_ceil(double y, uint32_t nu, double marg
 // copy o is the last lane whose prefix is <= o (a 5-step shuffle search).  Consecutive copies of a run
 // are consecutive outputs, so the stores coalesce within runs; the rounds are balanced whatever the copy
 // counts (a member can own hundreds of outputs).
+template <bool kDbg>
 __device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const float4& X, uint32_t J, NextState& out,
                                               uint32_t nu)
 {
@@ -174,7 +175,7 @@ __device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const flo
         for (uint32_t k = 0; k < c; ++k) {                 // (consecutive members of a run own
             DOG_ASSERT(F0 + k < nu);                       //  consecutive outputs: coalesced)
             out.s[F0 + k] = X;
-            if (out.jidx) out.jidx[F0 + k] = J;
+            if (kDbg) out.jidx[F0 + k] = J;
         }
         return;
     }
@@ -197,11 +198,11 @@ __device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const flo
         const uint32_t dst = __shfl_sync(0xffffffffu, F0, own) + (o - __shfl_sync(0xffffffffu, ex, own));
         const float4 V = make_float4(__shfl_sync(0xffffffffu, X.x, own), __shfl_sync(0xffffffffu, X.y, own),
                                      __shfl_sync(0xffffffffu, X.z, own), __shfl_sync(0xffffffffu, X.w, own));
-        const uint32_t jj = out.jidx ? __shfl_sync(0xffffffffu, J, own) : 0u;
+        const uint32_t jj = kDbg ? __shfl_sync(0xffffffffu, J, own) : 0u;
         if (o < total) {
             DOG_ASSERT(dst < nu);
             out.s[dst] = V;
-            if (out.jidx) out.jidx[dst] = jj;
+            if (kDbg) out.jidx[dst] = jj;
         }
     }
     (void)nu;
@@ -278,31 +279,44 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         const bool mem = p < wend && j != srun;
         float2 XY = make_float2(0.f, 0.f), V = XY;
         if (mem) { XY = pxy[pbase + p]; V = pv[pbase + p]; }   // coalesced, issued early
-        uint32_t c = 0, F0 = 0, Jd = 0;
+        // member mr owns [F(Q_mr), F(Q_mr+1)): each lane settles F(Q_mr) (linear estimate, exact fallback);
+        // F(Q_mr+1) is the next lane's value when it holds the run's next member
+        uint32_t F0 = 0, Jd = 0, mr = 0;
+        RunF x{};
         if (mem) {
-            const RunF x = j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j];
-            const uint32_t mr = x.pre + (p - x.first);
-            const double yR = __fma_rn((double)x.rpm, x.d1, x.y0), d2 = x.d1 - rc.nu_over_W;
-            const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0) : __fma_rn((double)(mr - x.rpm), d2, yR);
-            const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0)
-                                         : __fma_rn((double)(mr + 1u - x.rpm), d2, yR);
+            x = j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j];
+            mr = x.pre + (p - x.first);
+            const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0)
+                                          : __fma_rn((double)(mr - x.rpm), x.d1 - rc.nu_over_W, __fma_rn((double)x.rpm, x.d1, x.y0));
             bool amb = false;
-            uint32_t a0 = fast_ceil(y0, rc.nu, margin, amb), a1 = fast_ceil(y1, rc.nu, margin, amb);
-            if (amb) {                                      // rare: settle with exact products
-                const RunInfo q = runs[j];
-                const uint64_t Q0 = member_Q(q, mr);
-                a0 = fcount(Q0, rc);
-                a1 = fcount(Q0 + q.bp + (mr < q.rpm ? 1u : 0u), rc);
-            }
-            DOG_ASSERT(a0 <= a1 && a1 <= fc.nu);
-            F0 = a0; c = a1 - a0;
+            F0 = fast_ceil(y0, rc.nu, margin, amb);
+            if (amb) F0 = fcount(member_Q(runs[j], mr), rc);   // rare: exact products
             if (kDbg) {
                 const RunInfo q = runs[j];
                 Jd = q.jbase + mr;
                 perm_dbg[q.jbase - L.sb[q.li] + mr] = pbase + lperm[base + p];
             }
         }
-        write_compact(c, F0, make_float4(XY.x, XY.y, V.x, V.y), Jd, out, fc.nu);
+        const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);
+        const uint32_t jn = __shfl_down_sync(0xffffffffu, mem ? j : 0xFFFFFFFFu, 1);
+        uint32_t c = 0;
+        if (mem) {
+            uint32_t F1 = Fn;
+            if (lane == 31 || jn != j) {                    // the run's last member in this round
+                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0)
+                                             : __fma_rn((double)(mr + 1u - x.rpm), x.d1 - rc.nu_over_W,
+                                                        __fma_rn((double)x.rpm, x.d1, x.y0));
+                bool amb = false;
+                F1 = fast_ceil(y1, rc.nu, margin, amb);
+                if (amb) {
+                    const RunInfo q = runs[j];
+                    F1 = fcount(member_Q(q, mr) + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                }
+            }
+            DOG_ASSERT(F0 <= F1 && F1 <= fc.nu);
+            c = F1 - F0;
+        }
+        write_compact<kDbg>(c, F0, make_float4(XY.x, XY.y, V.x, V.y), Jd, out, fc.nu);
     }
     // ---- velocity sums per run (Eqs. 81-84; k_moments combines a cell's runs in tile order), from the
     //      sorted predicted velocities just read (L1 / L2): runs of >= 16 members by a warp each (lanes

@@ -16,6 +16,7 @@
 // The global order (cell, input index) of the paper's sort is thereby fully determined without moving
 // any particle: a particle's cell-sorted slot is start_c + pre(tile, run) + (position within the run).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include "dog_cells.cuh"
 #include "dog_common.cuh"
@@ -66,6 +67,8 @@ struct PsSmem {
     uint32_t mn[kPsWarps], mx[kPsWarps];
 };
 constexpr size_t kPsSmemBytes = sizeof(PsSmem);
+static_assert(offsetof(PsSmem, hist) == offsetof(PsSmem, rank) + kSortTile * 2 && sizeof(PsSmem::hist) == kSortTile * 2,
+              "rank + hist form one 16 KB staging buffer");
 
 // One particle of Alg. 1: p' = p + T v + xi_p with the OLD velocity (Eq. 14, A-2); v' = v + xi_v.  The
 // four normals come from one Philox4x32-10 draw keyed by the particle's GLOBAL index (A-20), so a band
@@ -313,13 +316,11 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
             reinterpret_cast<uint32_t*>(lperm + tb)[q] = v0 | (v1 << 16);
         }
     __syncthreads();                                        // s_start (S.rank) is free again
-    // ---- the predicted state in sorted order: inverse permutation, then each half staged through
-    //      shared memory (one 16 KB buffer per component) and written back coalesced
-    uint16_t* inv = S.rank;
-    for (uint32_t p = tid; p < n; p += kPsThreads) inv[sw[p] & ((1u << kPkIdx) - 1u)] = (uint16_t)p;
-    __syncthreads();
-    float* st0 = reinterpret_cast<float*>(S.k[0]);          // the records are dead now: both 16 KB
-    float* st1 = reinterpret_cast<float*>(S.k[1]);          // buffers stage one component each
+    // ---- the predicted state in sorted order: each half staged through shared memory in input order
+    //      (coalesced reads, conflict-free stores), then gathered by sorted position through the
+    //      sorted records (sorted position -> local index) and written back coalesced
+    float* st0 = reinterpret_cast<float*>(S.k[cur ^ 1]);                // 16 KB
+    float* st1 = reinterpret_cast<float*>(S.rank);                      // rank + hist: 16 KB
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
         float2* dst = h ? pv : pxy;
@@ -334,16 +335,18 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
                     const float4 P = pst[base + q];
                     v = h ? make_float2(P.z, P.w) : make_float2(P.x, P.y);
                 }
-                const uint32_t p = inv[q];
-                st0[p] = v.x;
-                st1[p] = v.y;
+                st0[q] = v.x;
+                st1[q] = v.y;
             }
         }
         __syncthreads();
 #pragma unroll 4
         for (int i = 0; i < kPsRows; ++i) {
             const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
-            if (p < n) dst[base + p] = make_float2(st0[p], st1[p]);
+            if (p < n) {
+                const uint32_t q = sw[p] & ((1u << kPkIdx) - 1u);
+                dst[base + p] = make_float2(st0[q], st1[q]);
+            }
         }
         __syncthreads();
     }

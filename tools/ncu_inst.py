@@ -1,0 +1,29 @@
+"""Source lines of one kernel in an ncu report ranked by instructions executed (`--page source`)."""
+import csv
+import io
+import subprocess
+import sys
+
+
+def main(path, kernel, top=30):
+    out = subprocess.run(['ncu', '-i', path, '--page', 'source', '--csv', '-k', f'regex:{kernel}',
+                          '--print-source', 'cuda,sass'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, lines = None, []
+    for r in rows:
+        if r and r[0] == 'Line No':
+            hdr = r
+            continue
+        if len(r) == 2 or hdr is None or len(r) < 5 or not r[0].isdigit():
+            continue
+        ei = hdr.index('Instructions Executed')
+        e = int(r[ei]) if r[ei].isdigit() else 0
+        lines.append((e, int(r[0]), r[1].strip()[:110]))
+    tot = sum(x[0] for x in lines) or 1
+    print(f'total instructions {tot}')
+    for e, ln, src in sorted(lines, reverse=True)[:top]:
+        print(f'{100 * e / tot:5.1f}% {e:9d} {ln}: {src}')
+
+
+if __name__ == '__main__':
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
