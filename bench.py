@@ -208,7 +208,8 @@ def bench_reference(args, cfg):
     def frame(k):
         return sc.frame(k).numpy()[r0:r0 + args.ref_rows].copy()
 
-    ts = run_oracle_steps(band, sc, frame, args.steps, args.warmup)
+    with pinned_core() as core:
+        ts = run_oracle_steps(band, sc, frame, args.steps, args.warmup)
     t = sum(ts) / len(ts)
     value = band.nu / t
     sample = (f"{args.ref_rows}-row band of {cfg.name} through the sensor ({band.width}x{band.height} cells, "
@@ -219,7 +220,8 @@ def bench_reference(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "grid": f"{cfg.width}x{cfg.height}", "nu": cfg.nu, "nu_b": cfg.nu_b,
                    "sample": sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "pinned_core": core, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -263,6 +265,10 @@ def bench_ours(args, cfg):
         ev1[i].record(stream)
     torch.cuda.synchronize()
     m1 = clocks.mark()
+    # the timed workload as it stands right after the timed cycles (before anything else runs on this
+    # filter): the state the CPU oracle is timed from, and the particle / mass counts of the roofline
+    snapshot = f.get_state()
+    sc_dev = dog_scalars(f)
     # continuous operation (the filter at frame rate with nothing in between): K cycles back to back, no
     # flush (the per-cycle working set, ~0.6 GB at cfg T, exceeds the 126 MB L2)
     c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
@@ -322,15 +328,31 @@ def bench_ours(args, cfg):
         torch.cuda.synchronize()
         h2d_ms = (time.perf_counter() - t1) * 1e3 / args.e2e_steps
         del dev_buf
-        e2e = {"value": cfg.nu / (e2e_ms * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 4 * cfg.C,
-               "ms_per_step": e2e_ms, "steps": args.e2e_steps,
-               "entry": "dog_step_host_async (pinned host meas -> device on a copy stream, cycle, occupancy -> "
-                        "pinned host on a second copy stream; overlapped across cycles; wall clock incl. final sync)",
+        # the full readout (occupied / free mass, velocity mean and covariance: 28 B per cell) every cycle
+        outs = [{"occ": torch.empty(cfg.C, dtype=torch.float32).pin_memory(),
+                 "free": torch.empty(cfg.C, dtype=torch.float32).pin_memory(),
+                 "mean": torch.empty(cfg.C, 2, dtype=torch.float32).pin_memory(),
+                 "cov": torch.empty(cfg.C, 3, dtype=torch.float32).pin_memory()} for _ in range(2)]
+        f.step_host_readout(host_frames[0], cfg.dt, outs[0], stream)
+        f.sync(stream)
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            f.step_host_readout(host_frames[i % len(host_frames)], cfg.dt, outs[i % 2], stream)
+        f.sync(stream)
+        full_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        e2e = {"value": cfg.nu / (full_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 28 * cfg.C,
+               "ms_per_step": full_ms, "steps": args.e2e_steps,
+               "entry": "dog_step_host_readout (pinned host meas -> device on a copy stream, cycle, the full readout "
+                        "occ + free + mean + cov -> pinned host on a second copy stream; overlapped across cycles; "
+                        "wall clock incl. final sync)",
+               "h2d_floor_ms": h2d_ms,
+               "occupancy_only": {"value": cfg.nu / (e2e_ms * 1e-3), "ms_per_step": e2e_ms,
+                                  "h2d_bytes_per_step": 8 * cfg.C, "d2h_bytes_per_step": 4 * cfg.C,
+                                  "entry": "dog_step_host_async"},
                "sync_entry_ms_per_step": sync_ms,
-               "h2d_floor_ms": h2d_ms, "h2d_floor_frac": h2d_ms / e2e_ms,
-               "note": "pipelined e2e is bound by the PCIe upload of the measurement grid (h2d_floor_ms: the "
-                       "same bytes as a bare pinned copy); the cycle itself is ms_per_step"}
+               "note": "pipelined e2e is bound by PCIe: 32 MB up and 117 MB down per cycle at cfg T (h2d_floor_ms: "
+                       "the upload alone as a bare pinned copy); the cycle itself is ms_per_step"}
 
     # NEXT-1 (Doppler / association branch): cycles with a radar overlay on half the occupied cells,
     # device-timed like the main line (L2 flushed between cycles); continues the same filter
@@ -442,7 +464,6 @@ def bench_ours(args, cfg):
     kern = {k: v for k, v in st_avg.items() if k != "memset"}
     dom = max(kern, key=kern.get)
     hbm, peak_src = peaks()
-    sc_dev = dog_scalars(f)
     bytes_dom = stage_bytes(dom, cfg, sc_dev["n_in"])
     achieved = bytes_dom / (kern[dom] * 1e-3) / 1e9
     traffic = ncu_traffic(dom)
@@ -453,14 +474,20 @@ def bench_ours(args, cfg):
                  "frac": a_alg(cfg) / (ms_mean * 1e-3) / 1e9 / hbm, "unit": "GB/s",
                  "formula": "64 nu + 32 nu_b + 56 C (SURVEY.md 8(d))"}
 
+    # the other BASELINE configurations on this GPU (cfg2, cfg3, cfg5, and cfg4's 32M particles on one
+    # GPU): ms per cycle, particles/s and the step roofline, timed like the main line (shorter)
+    configs = run_config_lines(args, dev, stream, flush) if args.config_lines else None
+
     cpu = None
     if args.cpu_baseline_steps > 0:
-        st = f.get_state()
-        ts = run_oracle_steps(cfg, sc, lambda k: sc.frame(k).numpy(), args.cpu_baseline_steps, 0, state=st)
+        with pinned_core() as core:
+            ts = run_oracle_steps(cfg, sc, lambda k: sc.frame(k).numpy(), args.cpu_baseline_steps, 0, state=snapshot)
         t = sum(ts) / len(ts)
         cpu = {"value": cfg.nu / t, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{len(ts)} full {cfg.name} cycles ({cfg.width}x{cfg.height}, {cfg.nu} + {cfg.nu_b}) from "
-                         f"the GPU's warmed state, single-threaded C oracle", "ms_per_step": t * 1e3}
+                         f"the state the GPU reached right after its timed cycles, single-threaded C oracle "
+                         f"(gcc -O2 -ffp-contract=off) pinned to one core", "ms_per_step": t * 1e3,
+               "pinned_core": core, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
     value = cfg.nu / (ms_max * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
@@ -479,6 +506,7 @@ def bench_ours(args, cfg):
                        "note": "K cycles back to back, no flush between them (working set > L2)"},
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
         "next_rows": {"doppler": doppler, "exact_phd_mib": exact, "ego_scroll": ego, "evaluate": evaluation},
+        "configs": configs,
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",
     }
@@ -577,6 +605,79 @@ def bench_sharded(args, cfg):
     dist.destroy_process_group()
 
 
+class pinned_core:
+    """Context manager: run on one host core (the first this process may use), as `taskset -c` would."""
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            core = min(self.prev)
+            os.sched_setaffinity(0, {core})
+            return core
+        except Exception:   # noqa: BLE001 -- not Linux: unpinned
+            return None
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+        return False
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:   # noqa: BLE001
+        pass
+    return "unknown"
+
+
+def run_config_lines(args, dev, stream, flush):
+    """ms per cycle, particles/s and the step roofline of the other BASELINE configurations on one GPU."""
+    import numpy as np
+    import torch
+    from paper_1605_02406_b200 import dog
+    from paper_1605_02406_b200 import inputs as I
+    hbm, _ = peaks()
+    out = {}
+    for name in args.config_lines.split(","):
+        if name == args.config:
+            continue
+        try:
+            cfg = I.CONFIGS[name]
+            sc = I.scene(cfg)
+            settle, K = 30, 8
+            frames = [sc.frame(k, device=dev).contiguous() for k in range(settle + K)]
+            f = dog.Filter.from_config(cfg)
+            for k in range(settle):
+                f.step(frames[k], cfg.dt, stream)
+            torch.cuda.synchronize()
+            e0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+            e1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+            for i in range(K):
+                flush.zero_()
+                e0[i].record(stream)
+                f.step(frames[settle + i], cfg.dt, stream)
+                e1[i].record(stream)
+            torch.cuda.synchronize()
+            ms = float(np.mean([e0[i].elapsed_time(e1[i]) for i in range(K)]))
+            A = a_alg(cfg)
+            out[name] = {"workload": f"{cfg.width}x{cfg.height} grid, {cfg.nu} + {cfg.nu_b} particles",
+                         "ms_per_step": ms, "value": cfg.nu / (ms * 1e-3), "unit": UNIT,
+                         "particles_incl_births_per_s": (cfg.nu + cfg.nu_b) / (ms * 1e-3),
+                         "step_roofline": {"A_alg_bytes": A, "achieved": A / (ms * 1e-3) / 1e9,
+                                           "frac": A / (ms * 1e-3) / 1e9 / hbm},
+                         "steps": K, "settle_cycles": settle}
+            f.close()
+            del frames, f
+            torch.cuda.empty_cache()
+        except Exception as exc:   # noqa: BLE001
+            out[name] = {"error": str(exc)}
+    return out
+
+
 def dog_scalars(f):
     import numpy as np
     from paper_1605_02406_b200 import dog
@@ -609,6 +710,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--cpu-baseline-steps", type=int, default=2)
     ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--config-lines", default="cfg2,cfg3,cfg5,cfg4",
+                    help="other configurations timed on this GPU (comma-separated; empty: none)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     from paper_1605_02406_b200 import inputs as I

@@ -88,6 +88,13 @@ typedef struct {
 int dog_create(const dog_grid* grid, int64_t n_particles, int64_t n_birth, const dog_params* params,
                uint64_t seed, uint32_t flags, int n_devices, const int* device_ids, dog_ctx** out);
 
+/* dog_step_host_readout -- dog_step_host_async returning the FULL readout of each cycle (Alg. 3 / Alg. 6
+ * stores): occ_host[C], free_host[C], mean_host[C][2], cov_host[C][3] (pinned HOST
+ * buffers, any may be NULL), snapshot on the device and copied to the host on the copy stream while the
+ * next cycle runs; complete after dog_sync(ctx, stream).  28 B per cell down, 8 B per cell up. */
+int dog_step_host_readout(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, float* free_host,
+                          float* mean_host, float* cov_host, void* stream);
+
 /* ---- sharded contexts (multi-GPU) ----
  * dog_step_sharded -- one filter cycle on every band.  meas_band[s]: DEVICE pointer on device_ids[s] (or
  * peer-readable from it), float[rows of band s][width][2]; streams[s]: a cudaStream_t on device_ids[s].

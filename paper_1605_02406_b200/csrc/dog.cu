@@ -1088,7 +1088,8 @@ int dog_step_host(dog_ctx* ctx, const float* meas_host, float dt, float* occ_hos
     return DOG_OK;
 }
 
-int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream)
+static int step_host_pipelined(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, float* free_host,
+                               float* mean_host, float* cov_host, void* stream)
 {
     if (!ctx || !meas_host) return DOG_E_INVAL;
     if (ctx->poisoned) return DOG_E_CUDA;
@@ -1096,10 +1097,10 @@ int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* o
     if (int r = set_device(ctx)) return r;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t C = ctx->C;
-    if (!ctx->h2d) {   // first use: staging buffers, copy streams and events
+    if (!ctx->h2d) {   // first use: staging buffers (meas; the 7 readout floats per cell), copy streams, events
         for (int b = 0; b < 2; ++b) {
             if (int rc = dalloc(ctx, &ctx->hmeas[b], 2 * C)) return rc;
-            if (int rc = dalloc(ctx, &ctx->hocc[b], C)) return rc;
+            if (int rc = dalloc(ctx, &ctx->hocc[b], 7 * C)) return rc;
             CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ctx->ev_used[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
@@ -1120,15 +1121,34 @@ int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* o
     CK(cudaStreamWaitEvent(st, ctx->ev_in[b], 0));
     if (int rc = dog_step(ctx, ctx->hmeas[b], dt, stream)) return rc;
     CK(cudaEventRecord(ctx->ev_used[b], st));
-    if (occ_host) {   // out: snapshot the occupancy on the device, copy it to the host meanwhile
+    if (occ_host || free_host || mean_host || cov_host) {
+        // out: snapshot the readouts on the device, copy them to the host while the next cycle runs
+        float* snap = ctx->hocc[b];
         CK(cudaStreamWaitEvent(st, ctx->ev_read[b], 0));
-        CK(cudaMemcpyAsync(ctx->hocc[b], ctx->occ, 4 * C, cudaMemcpyDeviceToDevice, st));
+        if (occ_host) CK(cudaMemcpyAsync(snap, ctx->occ, 4 * C, cudaMemcpyDeviceToDevice, st));
+        if (free_host) CK(cudaMemcpyAsync(snap + C, ctx->fre, 4 * C, cudaMemcpyDeviceToDevice, st));
+        if (mean_host) CK(cudaMemcpyAsync(snap + 2 * C, ctx->mean, 8 * C, cudaMemcpyDeviceToDevice, st));
+        if (cov_host) CK(cudaMemcpyAsync(snap + 4 * C, ctx->cov, 12 * C, cudaMemcpyDeviceToDevice, st));
         CK(cudaEventRecord(ctx->ev_out[b], st));
         CK(cudaStreamWaitEvent(ctx->d2h, ctx->ev_out[b], 0));
-        CK(cudaMemcpyAsync(occ_host, ctx->hocc[b], 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (occ_host) CK(cudaMemcpyAsync(occ_host, snap, 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (free_host) CK(cudaMemcpyAsync(free_host, snap + C, 4 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (mean_host) CK(cudaMemcpyAsync(mean_host, snap + 2 * C, 8 * C, cudaMemcpyDeviceToHost, ctx->d2h));
+        if (cov_host) CK(cudaMemcpyAsync(cov_host, snap + 4 * C, 12 * C, cudaMemcpyDeviceToHost, ctx->d2h));
         CK(cudaEventRecord(ctx->ev_read[b], ctx->d2h));
     }
     return DOG_OK;
+}
+
+int dog_step_host_async(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, void* stream)
+{
+    return step_host_pipelined(ctx, meas_host, dt, occ_host, nullptr, nullptr, nullptr, stream);
+}
+
+int dog_step_host_readout(dog_ctx* ctx, const float* meas_host, float dt, float* occ_host, float* free_host,
+                          float* mean_host, float* cov_host, void* stream)
+{
+    return step_host_pipelined(ctx, meas_host, dt, occ_host, free_host, mean_host, cov_host, stream);
 }
 
 int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t* shift_y, void* stream)

@@ -65,6 +65,7 @@ _SIGS = {
     "dog_step_exact": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_step_host_async": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
+    "dog_step_host_readout": ([_vp, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "dog_read_cells": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "dog_sync": ([_vp, _vp], C.c_int),
     "dog_destroy": ([_vp], C.c_int),
@@ -252,6 +253,15 @@ class Filter:
         occ_ptr = occ_host.data_ptr() if occ_host is not None else None
         _check(dog_step_host_async(self._h, meas_host.data_ptr(), dt, occ_ptr, _stream_ptr(stream)),
                "dog_step_host_async")
+
+    def step_host_readout(self, meas_host: torch.Tensor, dt: float, out: dict | None = None, stream=None):
+        """Pipelined host entry with the full readout (include/dog.h dog_step_host_readout): out holds pinned
+        host tensors occ [C], free [C], mean [C, 2], cov [C, 3] (any subset); complete after sync()."""
+        assert not meas_host.is_cuda and meas_host.dtype == torch.float32 and meas_host.is_contiguous()
+        out = out or {}
+        ptr = lambda k: out[k].data_ptr() if k in out and out[k] is not None else None
+        _check(dog_step_host_readout(self._h, meas_host.data_ptr(), dt, ptr("occ"), ptr("free"), ptr("mean"),
+                                     ptr("cov"), _stream_ptr(stream)), "dog_step_host_readout")
 
     def ego_scroll(self, dx: float, dy: float, stream=None) -> tuple[int, int]:
         """Ego-motion compensation between cycles (include/dog.h); the applied shift in cells."""
