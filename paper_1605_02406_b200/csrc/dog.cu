@@ -125,6 +125,10 @@ struct dog_ctx {
     std::vector<cudaEvent_t> sev_pred, sev_asg, sev_jnt, sev_done;
     std::vector<uint64_t*> sh_mass, sh_weight;    // per band, on its device: the all-gathered u64 totals
     cudaEvent_t ev_caller = nullptr;              // on device_ids[0]: the caller's stream -> band streams
+    // the active-list length of a recent cycle, copied to pinned host memory at the end of each cycle (no
+    // sync; read lagged): long lists (dense scenes, cfg 5) take the grid-wide list scan and the lane-per-cell
+    // variants, which produce the same lists / sums as the one-cluster variants
+    uint32_t* lc_host = nullptr;
 
     std::vector<void*> allocs;
 };
@@ -453,6 +457,8 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     if (e == cudaSuccess) e = cudaMemset(ctx->ev_acc, 0, sizeof(EvalAcc));
 
     if (e == cudaSuccess && ctx->world == 1 && ctx->nu_b > 0 && !getenv("DOG_NO_FORK")) {
+        if (cudaHostAlloc((void**)&ctx->lc_host, 16, cudaHostAllocDefault) == cudaSuccess) *ctx->lc_host = 0u;
+        else { ctx->lc_host = nullptr; cudaGetLastError(); }
         e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
@@ -513,6 +519,7 @@ int dog_destroy(dog_ctx* ctx)
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->lc_host) cudaFreeHost(ctx->lc_host);
     free_doppler(ctx);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -679,10 +686,14 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (int r = L_cells(ctx, meas, a, fc, st, obs)) return r;
     CK(mark("cells"));
     // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
-    if (int r = L_list_scan(ctx, nullptr, a, fc, st, obs != nullptr)) return r;
+    const bool heavy = obs != nullptr || (ctx->lc_host && *(volatile uint32_t*)ctx->lc_host > ctx->C / 16);
+    static const int hv = getenv("DOG_HEAVY") ? atoi(getenv("DOG_HEAVY")) : 15;   // diagnostics: which parts
+    const bool h_scan = obs != nullptr || (heavy && (hv & 1)), h_pairs = obs != nullptr || (heavy && (hv & 2));
+    const bool h_mom = obs != nullptr || (heavy && (hv & 4)), h_births = obs != nullptr || (heavy && (hv & 8));
+    if (int r = L_list_scan(ctx, nullptr, a, fc, st, h_scan)) return r;
     CK(mark("list_scan"));
     // 5. each cell's runs in tile order -> stable within-cell ranks; global totals (w_bar)
-    if (int r = L_pairs(ctx, nullptr, a, fc, st, obs != nullptr)) return r;
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, h_pairs)) return r;
     CK(mark("pairs"));
     // 6. persistent particles: moments + resampling copies; births.  Births depend only on the list and
     // the totals (both final here) and write disjoint output slots, so outside profiling they run on the
@@ -691,17 +702,18 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (fork) {
         CK(cudaEventRecord(ctx->ev_fork, st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
-        if (int r = L_births(ctx, a, fc, ctx->side, nullptr, obs != nullptr)) return r;
+        if (ctx->lc_host) CK(cudaMemcpyAsync(ctx->lc_host, &ctx->sc->Lc, 4, cudaMemcpyDeviceToHost, ctx->side));
+        if (int r = L_births(ctx, a, fc, ctx->side, nullptr, h_births)) return r;
         CK(cudaEventRecord(ctx->ev_join, ctx->side));
     }
     if (int r = L_resample(ctx, a, fc, st)) return r;
     CK(mark("resample"));
-    if (int r = L_moments(ctx, st, nullptr, obs != nullptr)) return r;
+    if (int r = L_moments(ctx, st, nullptr, h_mom)) return r;
     CK(mark("moments"));
     if (fork) {
         CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     } else {
-        if (int r = L_births(ctx, a, fc, st, nullptr, obs != nullptr)) return r;
+        if (int r = L_births(ctx, a, fc, st, nullptr, h_births)) return r;
         CK(mark("births"));
     }
     if (prof) {

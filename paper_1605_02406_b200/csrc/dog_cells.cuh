@@ -271,7 +271,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
                 L.np[li] = npc;
                 A_loc += o.Rb;
                 N_loc += o.n;
-                if (kExact) P_loc += npc;                   // (the grid-wide list scan's chunk totals)
+                P_loc += npc;                               // (the grid-wide list scan's chunk totals)
             }
         }
         __syncthreads();
@@ -279,7 +279,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     // block totals (integers: order-independent)
     A_loc = warp_sum(A_loc);
     N_loc = warp_sum(N_loc);
-    if (kExact) P_loc = warp_sum(P_loc);
+    P_loc = warp_sum(P_loc);
     bad_loc = warp_sum(bad_loc);
     __shared__ uint32_t s_P[8];
     if (lane == 0) { s_A[warp] = A_loc; s_N[warp] = N_loc; s_bad[warp] = bad_loc; s_P[warp] = P_loc; }

@@ -115,6 +115,16 @@ def test_ego_motion_compensation():
     run_lockstep(I.CONFIGS["cfg1"], 8, ego=ego)
 
 
+def test_dense_scene_long_list_paths():
+    """A cfg-5-like dense scene (i.i.d. measured cells, 4x process noise, p_B 0.1) on 96x96 cells: from
+    the third cycle the active list exceeds C/16, so the library switches to the grid-wide list scan and
+    the lane-per-cell pair sort, moments and per-slot births -- every stage stays bit-exact with the
+    oracle (the switch must not change a result)."""
+    cfg = I.config("cfg5", width=96, height=96, nu=120_000, nu_b=30_000)
+    o, g = run_lockstep(cfg, 7)
+    assert o.scalars()["n_in"] > 0
+
+
 def test_ragged_sizes():
     """nu not a multiple of 4 / of the 4096-element sort tile, odd nu_b, non-square grid."""
     cfg = I.config("cfg1", width=37, height=23, nu=10_007, nu_b=999)
