@@ -244,6 +244,7 @@ FilterConst filter_const(const dog_ctx* ctx)
     f.occ_max = ctx->params.occ_max;
     f.v_max = ctx->params.v_max;
     f.seed = ctx->seed;
+    f.force_exact = getenv("DOG_FORCE_EXACT_F") ? 1u : 0u;     // diagnostics / tests only
     return f;
 }
 

@@ -56,6 +56,7 @@ struct FilterConst {
     uint32_t nu, nu_b;
     float p_s, p_b, sigma_b, occ_max, v_max;
     uint64_t seed;
+    uint32_t force_exact;  // diagnostics (DOG_FORCE_EXACT_F): every F(X) through exact 128-bit products
 };
 
 // Diagnostics build only (DOG_NVCC_EXTRA=-DDOG_TIMING, tools/phase_timing.py): per-phase block time,

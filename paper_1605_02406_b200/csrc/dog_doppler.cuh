@@ -213,7 +213,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     RdSmem& S = *reinterpret_cast<RdSmem*>(smem_raw);
     const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
-    const RsConst rc = make_rsconst(sc, fc.nu);
+    const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     out.s += fc.lo_cap - sc->o_base[par ^ 1];
     if (rc.W == 0 && fc.world == 1) {   // empty world (A-26)
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x)

@@ -11,11 +11,13 @@ struct RsConst {
     double nu_over_W;  // nu / W  (fp64)
     double U_frac;     // U 2^-32  (exact)
     u128 UW;           // U * W
+    bool exact;        // skip the fp64 estimate (diagnostics: FilterConst::force_exact)
 };
 
-__device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t nu)
+__device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t nu, bool exact = false)
 {
     RsConst r;
+    r.exact = exact;
     r.W = sc->Wtot;            // joint weight over all shards (k_pair_sort)
     r.U = sc->U;
     r.nu = nu;
@@ -36,7 +38,7 @@ __device__ __forceinline__ uint32_t fcount(uint64_t X, const RsConst& r)
     if (y >= (double)r.nu) return r.nu;
     const double cy = ceil(y);
     const double d = cy - y;                       // in [0, 1)
-    if (d > 0x1p-16 && d < 1.0 - 0x1p-16) return (uint32_t)cy;
+    if (d > 0x1p-16 && d < 1.0 - 0x1p-16 && !r.exact) return (uint32_t)cy;
     const u128 num0 = ((u128)X * (u128)r.nu) << 32;
     if (num0 <= r.UW) return 0u;
     const u128 num = num0 - r.UW;

@@ -226,7 +226,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     RtSmem& S = *reinterpret_cast<RtSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x, base = t * kSortTile;     // this tile's slot in the per-tile arrays
-    const RsConst rc = make_rsconst(sc, fc.nu);
+    const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     const uint32_t n_lo = sc->n_lo, n_loc = n_lo + sc->n_own[par] + sc->n_hi;
     const uint32_t pbase = fc.lo_cap - n_lo + base;                // its first particle
     // next-cycle own particles start at lo_cap: global output o -> slot lo_cap + o - F(P'_shard)
@@ -260,7 +260,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     }
     __syncthreads();
     const uint32_t srun = S.sentinel_run;
-    const double margin = fast_ceil_margin(fc.nu);
+    const double margin = fc.force_exact ? 1.0 : fast_ceil_margin(fc.nu);   // 1.0: every estimate ambiguous
     // ---- copies: warp w, sorted positions [512 w, 512 w + 512), 32 per round
     constexpr uint32_t kSpan = kSortTile / (kRtThreads / 32);
     const uint32_t w0 = warp * kSpan;                      // (warps beyond n skip the loop, not the barrier)
@@ -434,7 +434,7 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
 {
     PDL_ENTER();
     const int tid = threadIdx.x, lane = tid & 31;
-    const RsConst rc = make_rsconst(sc, fc.nu);
+    const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     const int par = (int)(k & 1);
     out.s += fc.lo_cap - sc->o_base[par ^ 1];                     // global output -> local slot
     const uint64_t Ppre = sc->Ppre;                                // joint prefix of the shards below
@@ -528,7 +528,7 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
                                                       const DevScalars* sc, FilterConst fc, int64_t k)
 {
     PDL_ENTER();
-    const RsConst rc = make_rsconst(sc, fc.nu);
+    const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     const int par = (int)(k & 1);
     out.s += fc.lo_cap - sc->o_base[par ^ 1];
     const uint64_t Ppre = sc->Ppre;

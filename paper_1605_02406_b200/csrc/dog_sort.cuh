@@ -641,6 +641,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         sc->nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
         if (W_all) {
             RsConst r;
+            r.exact = fc.force_exact != 0;
             r.W = Wtot; r.U = sc->U; r.nu = fc.nu;
             r.nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
             r.U_frac = (double)r.U * 0x1p-32;

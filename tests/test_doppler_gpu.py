@@ -50,6 +50,8 @@ def compare(o, g, nu_b):
     bits(co["occ"], cg["occ"], "occ")
     close(co["mean"], cg["mean"], 1e-4, 1e-6, "vel_mean")
     close(co["cov"][:, :2], cg["cov"][:, :2], 1e-4, 1e-7, "vel_var")
+    scale = np.sqrt(np.abs(co["cov"][:, 0] * co["cov"][:, 1])).astype(np.float64)
+    assert np.all(np.abs(co["cov"][:, 2].astype(np.float64) - cg["cov"][:, 2]) <= 1e-4 * scale + 1e-7), "vel_cov"
     sto, stg = o.get_state(), g.get_state()
     for k in ("x", "y", "vx", "vy", "m_free"):
         bits(sto[k], stg[k], "state." + k)

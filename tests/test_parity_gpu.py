@@ -125,6 +125,15 @@ def test_dense_scene_long_list_paths():
     assert o.scalars()["n_in"] > 0
 
 
+def test_exact_resampling_fallback_forced(monkeypatch):
+    """The exact 128-bit path of F(X) (dog_fcount.cuh), which the fp64 estimates hand over to when they
+    land within the margin of an integer (a few members per cycle at cfg T), forced for every member and
+    output boundary (DOG_FORCE_EXACT_F): the cycles stay bit-exact with the oracle's binary search."""
+    monkeypatch.setenv("DOG_FORCE_EXACT_F", "1")
+    run_lockstep(I.config("cfg2", width=128, height=128, nu=120_000, nu_b=12_000, beams=300, movers=3, peds=2,
+                          boxes=6), 4)
+
+
 def test_ragged_sizes():
     """nu not a multiple of 4 / of the 4096-element sort tile, odd nu_b, non-square grid."""
     cfg = I.config("cfg1", width=37, height=23, nu=10_007, nu_b=999)
@@ -278,6 +287,10 @@ def test_full_size_one_cycle(name):
     assert_bits(co["occ"], cr["occ"], "release occ")
     assert_bits(co["free"], cr["free"], "release free")
     rel_close(co["mean"].reshape(-1), cr["mean"].reshape(-1), 1e-4, 1e-6, "release vel_mean")
+    vo, vr = co["cov"].reshape(-1, 3), cr["cov"].reshape(-1, 3)
+    rel_close(vo[:, :2].reshape(-1), vr[:, :2].reshape(-1), 1e-4, 1e-8, "release vel_var")
+    scale = np.sqrt(np.abs(vo[:, 0] * vo[:, 1])).astype(np.float64)
+    assert np.all(np.abs(vo[:, 2].astype(np.float64) - vr[:, 2]) <= 1e-4 * scale + 1e-8), "release vel_cov"
     r.close()
 
 
