@@ -61,7 +61,6 @@ struct dog_ctx {
     uint32_t* keys = nullptr;                     // cell key per predicted particle
     uint16_t* lperm = nullptr;                    // tile-local sorted position -> local index
     TilePairs tp{};                               // runs of equal keys per tile
-    RunF* rfg = nullptr;                          // k_resample_tiles: F parameters of runs beyond its smem cache
     uint32_t *plist = nullptr, *ptmp = nullptr;   // per-cell run lists
     uint32_t *counts = nullptr, *npairs = nullptr;   // n_c and runs per cell, zeroed by k_cells
     // cells
@@ -393,7 +392,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     int rc = DOG_OK;
 #define AL(ptr, n) \
     if (rc == DOG_OK) rc = dalloc(ctx, &ptr, (n))
-    AL(ctx->st, N); AL(ctx->pxy, N); AL(ctx->pv, N); AL(ctx->rfg, N);
+    AL(ctx->st, N); AL(ctx->pxy, N); AL(ctx->pv, N);
     if (dbg || (band && band->world > 1)) AL(ctx->pst, N);
     AL(ctx->lperm, N); AL(ctx->kscr, N);
     AL(ctx->tp.key, N); AL(ctx->tp.first, N); AL(ctx->tp.cnt, N); AL(ctx->tp.run, N); AL(ctx->tp.nd, ctx->tiles);
@@ -600,7 +599,7 @@ static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const
 }
 
 static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                      const uint8_t* tskip = nullptr)
+                      const uint8_t* tskip = nullptr, bool long_list = false)
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
@@ -608,23 +607,26 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     static const bool rs_pdl = getenv("DOG_RS_NOPDL") == nullptr;   // diagnostics
     if (dbg)
         CK(launch_ex(rs_pdl, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
-                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->perm, ctx->ppart, ctx->rfg,
-                  (const DevScalars*)ctx->sc, fc, par, tskip));
+                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->perm, ctx->ppart,
+                  (const DevScalars*)ctx->sc, fc, par, tskip, long_list ? kMoDirect : 0u));
     else
         CK(launch_ex(rs_pdl, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)nullptr,
-                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart, ctx->rfg,
-                  (const DevScalars*)ctx->sc, fc, par, tskip));
+                  ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart,
+                  (const DevScalars*)ctx->sc, fc, par, tskip, long_list ? kMoDirect : 0u));
     return DOG_OK;
 }
 
 static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullptr, bool long_list = false)
 {
+    const FilterConst fc = filter_const(ctx);
     if (long_list)
-        CK(launch(k_moments<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
-                  (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
+        CK(launch(k_moments<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, ctx->tp, (const uint32_t*)ctx->plist,
+                  (const float2*)ctx->pv, (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc,
+                  fc, GSd));
     else
-        CK(launch(k_moments<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, (const uint32_t*)ctx->plist,
-                  (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc, GSd));
+        CK(launch(k_moments<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, ctx->tp, (const uint32_t*)ctx->plist,
+                  (const float2*)ctx->pv, (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc,
+                  fc, GSd));
     return DOG_OK;
 }
 
@@ -707,7 +709,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
         if (int r = L_births(ctx, a, fc, ctx->side, nullptr, h_births)) return r;
         CK(cudaEventRecord(ctx->ev_join, ctx->side));
     }
-    if (int r = L_resample(ctx, a, fc, st)) return r;
+    if (int r = L_resample(ctx, a, fc, st, nullptr, h_mom)) return r;
     CK(mark("resample"));
     if (int r = L_moments(ctx, st, nullptr, h_mom)) return r;
     CK(mark("moments"));
@@ -987,7 +989,7 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
     } else {
         const bool ex = ctx->band_exact;          // exact filter: long lists, births in every cell
         if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, ex)) return r;
-        if (int r = L_resample(ctx, a, fc, st)) return r;
+        if (int r = L_resample(ctx, a, fc, st, nullptr, ex)) return r;
         if (int r = L_moments(ctx, st, nullptr, ex)) return r;
         if (int r = L_births(ctx, a, fc, st, nullptr, ex)) return r;
         ctx->band_exact = false;

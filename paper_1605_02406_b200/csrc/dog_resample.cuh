@@ -122,7 +122,9 @@ constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // s
 static_assert(kRtItems % 8 == 0, "16-byte vector loads of the tile arrays");
 constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
 
-constexpr int kRtRunCache = 256;                                      // runs whose RunF sits in smem (rest: global)
+constexpr int kRtRunCache = 256;                                      // runs whose RunF sits in smem
+constexpr uint32_t kMoDirect = 32;   // long-list (run-heavy) cycles: cells with at most this many particles are
+                                     // summed directly by k_moments<true> (resample skips their run sums)
 
 // Per run, what the copy pass needs to place member r = pre + k (k = position - first): F(Q_r) =
 // ceil(y(r)) with y(r) = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
@@ -218,8 +220,8 @@ __device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const flo
 template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float2* __restrict__ pxy, const float2* __restrict__ pv,
-    CellList L, NextState out, uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart, RunF* __restrict__ rf_g,
-    const DevScalars* sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip)
+    CellList L, NextState out, uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart,
+    const DevScalars* sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip, uint32_t mo_direct)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -249,13 +251,13 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
         const uint32_t f = tp.first[base + r];
         atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
-        if (rc.W) {
+        if (rc.W && r < (uint32_t)kRtRunCache) {
             const RunInfo q = runs[r];
             RunF x;
             x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
             x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
             x.pre = q.pre; x.rpm = q.rpm; x.first = f; x.pad = 0u;
-            if (r < (uint32_t)kRtRunCache) S.rf[r] = x; else rf_g[base + r] = x;
+            if (r < (uint32_t)kRtRunCache) S.rf[r] = x;
         }
     }
     __syncthreads();
@@ -283,14 +285,22 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         // F(Q_mr+1) is the next lane's value when it holds the run's next member
         uint32_t F0 = 0, Jd = 0, mr = 0;
         RunF x{};
+        RunInfo qf{};
+        const bool cached = j < (uint32_t)kRtRunCache;       // else (run-heavy tiles): F from the RunInfo
         if (mem) {
-            x = j < (uint32_t)kRtRunCache ? S.rf[j] : rf_g[base + j];
-            mr = x.pre + (p - x.first);
-            const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0)
-                                          : __fma_rn((double)(mr - x.rpm), x.d1 - rc.nu_over_W, __fma_rn((double)x.rpm, x.d1, x.y0));
-            bool amb = false;
-            F0 = fast_ceil(y0, rc.nu, margin, amb);
-            if (amb) F0 = fcount(member_Q(runs[j], mr), rc);   // rare: exact products
+            if (cached) {
+                x = S.rf[j];
+                mr = x.pre + (p - x.first);
+                const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0)
+                                              : __fma_rn((double)(mr - x.rpm), x.d1 - rc.nu_over_W, __fma_rn((double)x.rpm, x.d1, x.y0));
+                bool amb = false;
+                F0 = fast_ceil(y0, rc.nu, margin, amb);
+                if (amb) F0 = fcount(member_Q(runs[j], mr), rc);   // rare: exact products
+            } else {
+                qf = runs[j];
+                mr = qf.pre + (p - tp.first[base + j]);
+                F0 = fcount(member_Q(qf, mr), rc);
+            }
             if (kDbg) {
                 const RunInfo q = runs[j];
                 Jd = q.jbase + mr;
@@ -303,14 +313,18 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         if (mem) {
             uint32_t F1 = Fn;
             if (lane == 31 || jn != j) {                    // the run's last member in this round
-                const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0)
-                                             : __fma_rn((double)(mr + 1u - x.rpm), x.d1 - rc.nu_over_W,
-                                                        __fma_rn((double)x.rpm, x.d1, x.y0));
-                bool amb = false;
-                F1 = fast_ceil(y1, rc.nu, margin, amb);
-                if (amb) {
-                    const RunInfo q = runs[j];
-                    F1 = fcount(member_Q(q, mr) + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                if (cached) {
+                    const double y1 = mr < x.rpm ? __fma_rn((double)(mr + 1u), x.d1, x.y0)
+                                                 : __fma_rn((double)(mr + 1u - x.rpm), x.d1 - rc.nu_over_W,
+                                                            __fma_rn((double)x.rpm, x.d1, x.y0));
+                    bool amb = false;
+                    F1 = fast_ceil(y1, rc.nu, margin, amb);
+                    if (amb) {
+                        const RunInfo q = runs[j];
+                        F1 = fcount(member_Q(q, mr) + q.bp + (mr < q.rpm ? 1u : 0u), rc);
+                    }
+                } else {
+                    F1 = fcount(member_Q(qf, mr) + qf.bp + (mr < qf.rpm ? 1u : 0u), rc);
                 }
             }
             DOG_ASSERT(F0 <= F1 && F1 <= fc.nu);
@@ -322,10 +336,11 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     //      sorted predicted velocities just read (L1 / L2): runs of >= 16 members by a warp each (lanes
     //      strided, fixed butterfly), shorter runs by one lane each in member order -- deterministic
     const uint32_t nw = kRtThreads / 32;
+    auto small_cell = [&](uint32_t r) { return mo_direct && L.n[runs[r].li] <= mo_direct; };   // k_moments sums those
     for (uint32_t r = warp; r < nd; r += nw) {            // long runs: warp per run
         if (r == srun) continue;
         const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
-        if (e - f < 16u) continue;
+        if (e - f < 16u || small_cell(r)) continue;
         double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (uint32_t q = f + lane; q < e; q += 32) {
             const float2 V = pv[pbase + q];
@@ -346,7 +361,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     for (uint32_t r = tid; r < nd; r += kRtThreads) {     // short runs: lane per run
         if (r == srun) continue;
         const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
-        if (e - f >= 16u) continue;
+        if (e - f >= 16u || small_cell(r)) continue;
         double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (uint32_t q = f; q < e; ++q) {
             const float2 V = pv[pbase + q];
@@ -365,41 +380,66 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
 constexpr int kMoGroup = 8;
 constexpr int kMoSmall = 4;   // kBatch (exact filter): cells with <= 4 runs summed by one lane each
 
+// Velocity sums of the members of run v (tile << 12 | run) from the sorted predicted velocities (member
+// order); used for cells of at most kMoDirect particles, whose runs' sums k_resample_tiles skips.
+__device__ __forceinline__ void run_vsums(const float2* __restrict__ v0, TilePairs tp, uint32_t v, double (&s5)[5])
+{
+    const uint32_t cnt = (uint32_t)tp.cnt[v] + 1u;
+    const float2* __restrict__ r = v0 + (v & ~0xFFFu) + tp.first[v];
+    for (uint32_t k = 0; k < cnt; ++k) {
+        const float2 V = r[k];
+        const double a = (double)V.x, b = (double)V.y;
+        s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
+    }
+}
+
 template <bool kBatch>
-__global__ __launch_bounds__(256) void k_moments(CellList L, const uint32_t* __restrict__ plist,
-                                                 const MomPartial* __restrict__ ppart, float2* __restrict__ mean,
-                                                 float* __restrict__ cov, const DevScalars* sc,
-                                                 const uint64_t* __restrict__ GSd)
+__global__ __launch_bounds__(256) void k_moments(CellList L, TilePairs tp, const uint32_t* __restrict__ plist,
+                                                 const float2* __restrict__ pv, const MomPartial* __restrict__ ppart,
+                                                 float2* __restrict__ mean, float* __restrict__ cov, const DevScalars* sc,
+                                                 FilterConst fc, const uint64_t* __restrict__ GSd)
 {
     PDL_ENTER();
     const int lane = threadIdx.x & 31, gl = lane & (kMoGroup - 1);
     const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
     const uint32_t Lc = sc->Lc;
     const float w_pred = sc->w_pred;
+    const float2* __restrict__ v0 = pv + (fc.lo_cap - sc->n_lo);   // sorted position p of tile t: v0[t 4096 + p]
+    auto dop = [&](uint32_t li) { return GSd && GSd[li] > 0; };
+    auto direct = [&](uint32_t li) { return kBatch && !dop(li) && L.n[li] <= kMoDirect; };
     auto finalize = [&](uint32_t li, const double (&s5)[5]) {
-        if (GSd && GSd[li] > 0)    // Doppler cell (NEXT-1): weighted sums
+        if (dop(li))               // Doppler cell (NEXT-1): weighted sums
             finalize_cell_dop(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.Rp[li], mean, cov);
         else
             finalize_cell(L.c[li], s5[0], s5[1], s5[2], s5[3], s5[4], L.n[li], L.rho_p[li], w_pred, mean, cov);
     };
     auto single = [&](uint32_t li, uint32_t m = 1u) {      // few runs: one lane sums them in list order
         const uint32_t* pl = plist + L.ps[li];
-        const double* ps = ppart[pl[0]].s;
-        double s5[5] = {ps[0], ps[1], ps[2], ps[3], ps[4]};
-        for (uint32_t q = 1; q < m; ++q) {
-            const double* pq = ppart[pl[q]].s;
+        double s5[5] = {0, 0, 0, 0, 0};
+        const bool dir = direct(li);
+        for (uint32_t q = 0; q < m; ++q) {
+            if (dir) {
+                run_vsums(v0, tp, pl[q], s5);
+            } else {
+                const double* pq = ppart[pl[q]].s;
 #pragma unroll
-            for (int i = 0; i < 5; ++i) s5[i] += pq[i];
+                for (int i = 0; i < 5; ++i) s5[i] += pq[i];
+            }
         }
         finalize(li, s5);
     };
     for_run_entries<kBatch, kMoGroup, kBatch ? kMoSmall : 1>(L.np, Lc, [&](uint32_t li, uint32_t m) {
         const uint32_t* pl = plist + L.ps[li];
         double s5[5] = {0, 0, 0, 0, 0};
+        const bool dir = direct(li);
         for (uint32_t q = gl; q < m; q += kMoGroup) {
-            const double* ps = ppart[pl[q]].s;
+            if (dir) {
+                run_vsums(v0, tp, pl[q], s5);
+            } else {
+                const double* ps = ppart[pl[q]].s;
 #pragma unroll
-            for (int i = 0; i < 5; ++i) s5[i] += ps[i];
+                for (int i = 0; i < 5; ++i) s5[i] += ps[i];
+            }
         }
         if (m > 1) {
 #pragma unroll
