@@ -590,7 +590,7 @@ static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const
     CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist,
               ctx->C));
     if (long_list)   // every cell listed, most without runs (the exact filter)
-        CK(launch(k_pair_sort<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
+        CK(launch(k_pair_sort<true>, 2 * ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
                   ctx->sc, fc, (int)(a.k & 1), dp));
     else
         CK(launch(k_pair_sort<false>, ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
@@ -620,7 +620,7 @@ static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullpt
 {
     const FilterConst fc = filter_const(ctx);
     if (long_list)
-        CK(launch(k_moments<true>, ctx->flat_blocks, 256, 0, st, 0, ctx->list, ctx->tp, (const uint32_t*)ctx->plist,
+        CK(launch(k_moments<true>, 2 * ctx->flat_blocks, 256, 0, st, 0, ctx->list, ctx->tp, (const uint32_t*)ctx->plist,
                   (const float2*)ctx->pv, (const MomPartial*)ctx->ppart, ctx->mean, ctx->cov, (const DevScalars*)ctx->sc,
                   fc, GSd));
     else
