@@ -476,7 +476,7 @@ def bench_ours(args, cfg):
 
     # the other BASELINE configurations on this GPU (cfg2, cfg3, cfg5, and cfg4's 32M particles on one
     # GPU): ms per cycle, particles/s and the step roofline, timed like the main line (shorter)
-    configs = run_config_lines(args, dev, stream, flush) if args.config_lines else None
+    configs = run_config_lines(args, dev, stream, flush) if args.config_lines not in ("", "none") else None
 
     cpu = None
     if args.cpu_baseline_steps > 0:
@@ -643,7 +643,7 @@ def run_config_lines(args, dev, stream, flush):
     hbm, _ = peaks()
     out = {}
     for name in args.config_lines.split(","):
-        if name == args.config:
+        if name == args.config or name not in I.CONFIGS:
             continue
         try:
             cfg = I.CONFIGS[name]
