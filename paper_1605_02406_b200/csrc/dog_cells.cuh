@@ -185,7 +185,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     __shared__ uint32_t s_bad[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
-    const float w_pred = sc->w_pred;
+    const float w_pred = scrd(sc->w_pred);
     const uint32_t c0 = blockIdx.x * chunk;
     const uint32_t c1 = min(c0 + chunk, fc.C);
     const uint32_t lbase = blockIdx.x * chunk;
@@ -611,7 +611,7 @@ __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, Bl
     PDL_ENTER();
     __shared__ uint64_t s_w[9];
     const uint32_t b = blockIdx.x, m = bt.cnt[b];
-    const uint64_t A = sc->A, nu_b = fc.nu_b;
+    const uint64_t A = scrd(sc->A), nu_b = fc.nu_b;
     const double rcpA = A ? 1.0 / (double)A : 0.0;
     uint64_t carryX = ((uint64_t)ws.pnp[b] << 32) | ws.pn[b], carryB = ws.prb[b], sJ = 0, sI = 0;
     for (uint32_t j0 = 0; j0 < m; j0 += 256) {             // block-uniform trip count
@@ -685,8 +685,8 @@ __global__ __launch_bounds__(256) void k_ls_chunks2(CellList L, BlockTotals bt, 
     PDL_ENTER();
     __shared__ uint64_t s_w[9];
     const uint32_t b = blockIdx.x, m = bt.cnt[b];
-    const uint32_t Lc = sc->Lc;
-    const uint64_t A = sc->A;
+    const uint32_t Lc = scrd(sc->Lc);
+    const uint64_t A = scrd(sc->A);
     uint64_t carryJ = ws.pJ[b], carryI = ws.pit[b];
     for (uint32_t j0 = 0; j0 < m; j0 += 256) {
         const uint32_t j = j0 + threadIdx.x;

@@ -7,29 +7,37 @@ namespace dog {
 typedef unsigned __int128 u128;
 
 // Device-resident scalars of the filter (written and read by kernels, so a cycle needs no host sync).
+// Every field sits in its own 128-byte line (DS_F): kernels are launched early (PDL) beside their
+// predecessor, and an SM's L1 may keep a line a predecessor CTA loaded before another predecessor CTA
+// wrote it (griddepcontrol.wait does not invalidate the L1).  No kernel reads a field that another CTA of
+// the same kernel writes, so with one field per line no CTA ever caches a line that is written while the
+// next kernel can run -- plain L1-cached loads stay coherent without a fence (measured: a gpu-scope fence
+// after every wait costs ~7 us per cycle; L2-only loads of the scalars more).
+#define DS_F alignas(128)
 struct DevScalars {
-    float    w_bar;      // uniform particle weight of the current state S_k (Eq. 57)
-    float    w_pred;     // p_S * w_bar of the cycle in flight (Eq. 39)
-    uint32_t U;          // systematic-resampling offset of the cycle (A-24)
-    uint32_t meas_bad;   // invalid measurement cells seen (sticky until reported)
-    uint64_t W;          // total fixed-point joint weight (A-23)
-    uint64_t A;          // total fixed-point born mass
-    uint64_t n_in;       // particles inside the grid after predict
-    uint64_t s_total;    // birth slots allocated (nu_b or 0)
-    uint32_t n_items;    // birth work items of the cycle
-    uint32_t Lc;         // entries of the active-cell list
+    DS_F float    w_bar;      // uniform particle weight of the current state S_k (Eq. 57)
+    DS_F float    w_pred;     // p_S * w_bar of the cycle in flight (Eq. 39)
+    DS_F uint32_t U;          // systematic-resampling offset of the cycle (A-24)
+    DS_F uint32_t meas_bad;   // invalid measurement cells seen (sticky until reported)
+    DS_F uint64_t W;          // total fixed-point joint weight (A-23)
+    DS_F uint64_t A;          // total fixed-point born mass
+    DS_F uint64_t n_in;       // particles inside the grid after predict
+    DS_F uint64_t s_total;    // birth slots allocated (nu_b or 0)
+    DS_F uint32_t n_items;    // birth work items of the cycle
+    DS_F uint32_t Lc;         // entries of the active-cell list
     // Local particle array = [migrants from the shard below | own particles | migrants from above]
     // (row-band contexts; a whole-grid context has only own particles).
-    uint32_t n_lo, n_hi;         // migrants received this cycle
-    uint32_t n_own[2];           // own particles, indexed by cycle parity
-    uint64_t o_base[2];          // global index of the first own particle (Philox counter base), by parity
-    uint64_t A_acc;              // this context's born mass (k_cells atomics; shared over shards)
-    uint64_t Wtot, Ppre;         // joint weight over all shards, joint prefix of the shards below
-    uint32_t mig_cnt[4];         // migrants leaving this cycle: to the band below, above, further below,
-                                 // further above (k_pack_migrants; read by the receivers)
-    uint32_t mig_over;           // sticky: a receive exceeded the migrant capacity (cycle not exact)
-    uint32_t pad2;
-    double nu_over_W;            // nu / Wtot in fp64 (k_pair_sort), for the resampling kernels
+    DS_F uint32_t n_lo;       // migrants received this cycle from below
+    DS_F uint32_t n_hi;       //                          and from above
+    DS_F uint32_t n_own[2];   // own particles, indexed by cycle parity
+    DS_F uint64_t o_base[2];  // global index of the first own particle (Philox counter base), by parity
+    DS_F uint64_t A_acc;      // this context's born mass (k_cells atomics; shared over shards)
+    DS_F uint64_t Wtot;       // joint weight over all shards
+    DS_F uint64_t Ppre;       // joint prefix of the shards below
+    DS_F uint32_t mig_cnt[4]; // migrants leaving this cycle: to the band below, above, further below,
+                              // further above (k_pack_migrants; read by the receivers)
+    DS_F uint32_t mig_over;   // sticky: a receive exceeded the migrant capacity (cycle not exact)
+    DS_F double nu_over_W;    // nu / Wtot in fp64 (k_pair_sort), for the resampling kernels
 };
 
 constexpr float kSentinelPos = -1073741824.0f;  // -2^30 cells: empty-world particle (A-19)
@@ -91,16 +99,11 @@ __device__ __forceinline__ unsigned long long gtimer_ns()
 // Programmatic dependent launch (every kernel of a cycle is launched with the PDL attribute): a kernel
 // lets the next one launch as soon as all its CTAs are running, and waits for its predecessor's results
 // (full completion and memory flush) before touching them.  Hides the launch gap between kernels.
-// The wait is followed by a gpu-scope acquire fence: an early-launched CTA shares its SM's L1 with CTAs
-// of the predecessor, which may have cached a line (e.g. of DevScalars) before another predecessor CTA
-// wrote it; griddepcontrol.wait alone does not invalidate the L1, the acquire fence does (measured: without
-// it, k_resample_tiles read a stale nu / W and placed copies one cycle off).
-__device__ __forceinline__ void pdl_wait()
-{
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// A read of a DevScalars field (see DevScalars: one field per L1 line keeps plain loads coherent).
+template <typename T>
+__device__ __forceinline__ T scrd(const T& v) { return v; }
 #define PDL_ENTER() do { pdl_trigger(); pdl_wait(); } while (0)
 
 // 1-D bulk copy global -> shared (TMA engine, cp.async.bulk), completion counted on an mbarrier as

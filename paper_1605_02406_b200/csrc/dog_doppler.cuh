@@ -86,7 +86,7 @@ __device__ __forceinline__ uint64_t doppler_Q(uint64_t Rp, float pA, uint64_t GS
 // particles of tile t (input order) and its slot base in the local array, as in k_resample_tiles
 __device__ __forceinline__ uint32_t tile_count(const DevScalars* sc, int par, uint32_t base)
 {
-    const uint32_t n_loc = sc->n_lo + sc->n_own[par] + sc->n_hi;
+    const uint32_t n_loc = scrd(sc->n_lo) + scrd(sc->n_own[par]) + scrd(sc->n_hi);
     return n_loc > base ? min((uint32_t)kSortTile, n_loc - base) : 0u;
 }
 
@@ -111,7 +111,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __re
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
-    const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
+    const uint32_t pbase = fc.lo_cap - scrd(sc->n_lo) + base;
     for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) s_first[r] = tp.first[base + r];
     if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
     __syncthreads();
@@ -214,7 +214,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
-    out.s += fc.lo_cap - sc->o_base[par ^ 1];
+    out.s += fc.lo_cap - scrd(sc->o_base[par ^ 1]);
     if (rc.W == 0 && fc.world == 1) {   // empty world (A-26)
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x)
             out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
@@ -222,7 +222,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0 || !tflag[t]) return;                          // tiles without Doppler runs: k_resample_tiles
     const uint32_t nd = tp.nd[t];
-    const uint32_t pbase = fc.lo_cap - sc->n_lo + base;
+    const uint32_t pbase = fc.lo_cap - scrd(sc->n_lo) + base;
     const RunInfo* __restrict__ runs = tp.run + base;
     for (uint32_t r = tid; r < nd; r += 256) S.first[r] = tp.first[base + r];
     if (tid == 0) S.first[nd] = (uint16_t)n;

@@ -18,10 +18,10 @@ __device__ __forceinline__ RsConst make_rsconst(const DevScalars* sc, uint32_t n
 {
     RsConst r;
     r.exact = exact;
-    r.W = sc->Wtot;            // joint weight over all shards (k_pair_sort)
-    r.U = sc->U;
+    r.W = scrd(sc->Wtot);            // joint weight over all shards (k_pair_sort)
+    r.U = scrd(sc->U);
     r.nu = nu;
-    r.nu_over_W = sc->nu_over_W;  // (double)nu / (double)W, divided once in k_pair_sort
+    r.nu_over_W = scrd(sc->nu_over_W);  // (double)nu / (double)W, divided once in k_pair_sort
     r.U_frac = (double)r.U * 0x1p-32;
     r.UW = (u128)r.U * (u128)r.W;
     return r;

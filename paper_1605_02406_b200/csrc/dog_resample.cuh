@@ -229,10 +229,10 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x, base = t * kSortTile;     // this tile's slot in the per-tile arrays
     const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
-    const uint32_t n_lo = sc->n_lo, n_loc = n_lo + sc->n_own[par] + sc->n_hi;
+    const uint32_t n_lo = scrd(sc->n_lo), n_loc = n_lo + scrd(sc->n_own[par]) + scrd(sc->n_hi);
     const uint32_t pbase = fc.lo_cap - n_lo + base;                // its first particle
     // next-cycle own particles start at lo_cap: global output o -> slot lo_cap + o - F(P'_shard)
-    out.s += fc.lo_cap - sc->o_base[par ^ 1];
+    out.s += fc.lo_cap - scrd(sc->o_base[par ^ 1]);
     if (rc.W == 0 && fc.world == 1) {   // empty world (A-26): every next particle goes to the sentinel
         for (uint32_t i = blockIdx.x * blockDim.x + tid; i < fc.nu; i += gridDim.x * blockDim.x) {
             out.s[i] = make_float4(kSentinelPos, kSentinelPos, 0.0f, 0.0f);
@@ -402,9 +402,9 @@ __global__ __launch_bounds__(256) void k_moments(CellList L, TilePairs tp, const
     PDL_ENTER();
     const int lane = threadIdx.x & 31, gl = lane & (kMoGroup - 1);
     const uint32_t gmask = 0xFFu << (lane & ~(kMoGroup - 1));
-    const uint32_t Lc = sc->Lc;
-    const float w_pred = sc->w_pred;
-    const float2* __restrict__ v0 = pv + (fc.lo_cap - sc->n_lo);   // sorted position p of tile t: v0[t 4096 + p]
+    const uint32_t Lc = scrd(sc->Lc);
+    const float w_pred = scrd(sc->w_pred);
+    const float2* __restrict__ v0 = pv + (fc.lo_cap - scrd(sc->n_lo));   // sorted position p of tile t: v0[t 4096 + p]
     auto dop = [&](uint32_t li) { return GSd && GSd[li] > 0; };
     auto direct = [&](uint32_t li) { return kBatch && !dop(li) && L.n[li] <= kMoDirect; };
     auto finalize = [&](uint32_t li, const double (&s5)[5]) {
@@ -476,9 +476,9 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
     const int tid = threadIdx.x, lane = tid & 31;
     const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     const int par = (int)(k & 1);
-    out.s += fc.lo_cap - sc->o_base[par ^ 1];                     // global output -> local slot
-    const uint64_t Ppre = sc->Ppre;                                // joint prefix of the shards below
-    const uint32_t n_items = sc->n_items, Lc = sc->Lc;
+    out.s += fc.lo_cap - scrd(sc->o_base[par ^ 1]);                     // global output -> local slot
+    const uint64_t Ppre = scrd(sc->Ppre);                                // joint prefix of the shards below
+    const uint32_t n_items = scrd(sc->n_items), Lc = scrd(sc->Lc);
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
     const uint32_t per = (n_items + nwarps - 1) / nwarps;
@@ -570,10 +570,10 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
     PDL_ENTER();
     const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
     const int par = (int)(k & 1);
-    out.s += fc.lo_cap - sc->o_base[par ^ 1];
-    const uint64_t Ppre = sc->Ppre;
-    const uint32_t Lc = sc->Lc;
-    const uint32_t ns = (uint32_t)sc->s_total;
+    out.s += fc.lo_cap - scrd(sc->o_base[par ^ 1]);
+    const uint64_t Ppre = scrd(sc->Ppre);
+    const uint32_t Lc = scrd(sc->Lc);
+    const uint32_t ns = (uint32_t)scrd(sc->s_total);
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
         uint32_t lo = 0, hi = Lc;                                   // last entry with sb <= s
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (L.sb[m] <= s) lo = m; else hi = m; }

@@ -118,14 +118,14 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int par = (int)(a.k & 1);
-    const uint32_t n_lo = sc->n_lo, n_own = sc->n_own[par], n_loc = n_lo + n_own + sc->n_hi;
-    const uint64_t o_base = sc->o_base[par];
+    const uint32_t n_lo = scrd(sc->n_lo), n_own = scrd(sc->n_own[par]), n_loc = n_lo + n_own + scrd(sc->n_hi);
+    const uint64_t o_base = scrd(sc->o_base[par]);
     const uint32_t s0 = fc.lo_cap - n_lo;
     const uint32_t tb = blockIdx.x * kSortTile;                // this tile's slot in the per-tile arrays
     const uint32_t base = s0 + tb;                             // its first particle
     const uint32_t n = n_loc > tb ? min((uint32_t)kSortTile, n_loc - tb) : 0u;
     if (kPredict) {
-        const float w_bar = sc->w_bar;
+        const float w_bar = scrd(sc->w_bar);
         const float w_pred = __fmul_rn(fc.p_s, w_bar);      // Eq. 39 (A-3): one scalar
         if (blockIdx.x == 0 && tid == 0) { sc->w_pred = w_pred; sc->A_acc = 0ull; }
     }
@@ -377,12 +377,12 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_band(const float4* __res
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const int par = (int)(a.k & 1);
-    const uint32_t n_own = sc->n_own[par];
-    const uint64_t o_base = sc->o_base[par];
+    const uint32_t n_own = scrd(sc->n_own[par]);
+    const uint64_t o_base = scrd(sc->o_base[par]);
     const uint32_t tb = blockIdx.x * kSortTile;
     const uint32_t n = n_own > tb ? min((uint32_t)kSortTile, n_own - tb) : 0u;
     if (blockIdx.x == 0 && tid == 0) {
-        sc->w_pred = __fmul_rn(fc.p_s, sc->w_bar);         // Eq. 39 (A-3)
+        sc->w_pred = __fmul_rn(fc.p_s, scrd(sc->w_bar));         // Eq. 39 (A-3)
         sc->A_acc = 0ull;
     }
     float4 P[kPsRows];
@@ -500,10 +500,10 @@ __global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* _
     PDL_ENTER();
     __shared__ uint32_t s_w[33];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n_own = sc->n_own[par];
+    const uint32_t n_own = scrd(sc->n_own[par]);
     const uint32_t hi_room = own_hi_cap - n_own;              // slots after the own particles
-    const uint32_t nlo = g.lo_near.rec ? *g.lo_near.cnt : 0u;
-    const uint32_t nhi = g.hi_near.rec ? *g.hi_near.cnt : 0u;
+    const uint32_t nlo = g.lo_near.rec ? __ldcg(g.lo_near.cnt) : 0u;   // the senders' counts: from L2
+    const uint32_t nhi = g.hi_near.rec ? __ldcg(g.hi_near.cnt) : 0u;
     float4* const lo_end = pst + fc.lo_cap;
     float4* const hi_beg = pst + fc.lo_cap + n_own;
     if (blockIdx.x > 0) {
@@ -538,7 +538,7 @@ __global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* _
     // pass 1: far records from below (their total places them before the near bucket)
     uint32_t flo = 0;
     for (int s = 0; s < g.n_lo_far; ++s) {
-        const uint32_t n = *g.lo_far[s].cnt;
+        const uint32_t n = __ldcg(g.lo_far[s].cnt);
         for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
             const uint32_t i = i0 + tid;
             flo += (uint32_t)__syncthreads_count(i < n && in_band(g.lo_far[s].rec[i]));
@@ -547,7 +547,7 @@ __global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* _
     const bool lo_ok = nlo + flo <= fc.lo_cap;
     uint32_t pos = 0;
     for (int s = 0; s < g.n_lo_far && lo_ok; ++s) {
-        const uint32_t n = *g.lo_far[s].cnt;
+        const uint32_t n = __ldcg(g.lo_far[s].cnt);
         for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
             const uint32_t i = i0 + tid;
             float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -561,7 +561,7 @@ __global__ __launch_bounds__(1024) void k_gather_migrants(MigGather g, float4* _
     uint32_t fhi = 0;
     const bool near_hi_ok = nhi <= hi_room;
     for (int s = 0; s < g.n_hi_far && near_hi_ok; ++s) {
-        const uint32_t n = *g.hi_far[s].cnt;
+        const uint32_t n = __ldcg(g.hi_far[s].cnt);
         for (uint32_t i0 = 0; i0 < n; i0 += 1024) {
             const uint32_t i = i0 + tid;
             float4 P = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -628,8 +628,8 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     __shared__ uint32_t s_buf[256 / kPsGroup][2][kPsBuf];
     const int lane = threadIdx.x & 31, gl = lane & (kPsGroup - 1), grp = threadIdx.x / kPsGroup;
     const uint32_t gmask = 0xFFu << (lane & ~(kPsGroup - 1));
-    const uint32_t Lc = sc->Lc;
-    uint64_t Ppre = 0, Wtot = sc->W;
+    const uint32_t Lc = scrd(sc->Lc);
+    uint64_t Ppre = 0, Wtot = scrd(sc->W);
     if (W_all) {
         Wtot = 0;
         for (uint32_t r = 0; r < fc.world; ++r) { if (r < fc.rank) Ppre += W_all[r]; Wtot += W_all[r]; }
@@ -642,12 +642,12 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         if (W_all) {
             RsConst r;
             r.exact = fc.force_exact != 0;
-            r.W = Wtot; r.U = sc->U; r.nu = fc.nu;
+            r.W = Wtot; r.U = scrd(sc->U); r.nu = fc.nu;
             r.nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
             r.U_frac = (double)r.U * 0x1p-32;
             r.UW = (u128)r.U * (u128)Wtot;
             const uint32_t f0 = Wtot ? fcount(Ppre, r) : 0u;
-            const uint32_t f1 = Wtot ? fcount(Ppre + sc->W, r) : 0u;
+            const uint32_t f1 = Wtot ? fcount(Ppre + scrd(sc->W), r) : 0u;
             sc->o_base[par ^ 1] = f0;
             sc->n_own[par ^ 1] = f1 - f0;
         }
