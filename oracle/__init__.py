@@ -91,6 +91,11 @@ def _declare(L):
     L.orc_step_doppler.restype = C.c_int
     L.orc_exp_spec.argtypes = [C.c_float]; L.orc_exp_spec.restype = C.c_float
     L.orc_step_exact.argtypes = [C.c_void_p, f32p, C.c_float]; L.orc_step_exact.restype = C.c_int
+    L.orc_step_exact_lik.argtypes = [C.c_void_p, f32p, f32p, f32p, C.c_float]; L.orc_step_exact_lik.restype = C.c_int
+    L.orc_birth_mean_lik.argtypes = [C.c_float] * 3; L.orc_birth_mean_lik.restype = C.c_float
+    L.orc_exact_lik_cell.argtypes = [C.c_float] * 7 + [C.c_uint64, C.c_float, C.c_uint32, C.c_float, C.c_float,
+                                                        C.c_float, f32p, f32p, f32p, f32p]
+    L.orc_birth_assoc_exact.argtypes = [C.c_uint64, C.c_uint32, C.c_float, u32p, u64p]
     L.orc_exact_cell.argtypes = [C.c_float] * 6 + [f32p, f32p]
     L.orc_doppler_g.argtypes = [C.c_float] * 6; L.orc_doppler_g.restype = C.c_float
     L.orc_doppler_gfx.argtypes = [C.c_float, C.c_float]; L.orc_doppler_gfx.restype = C.c_uint32
@@ -182,6 +187,24 @@ def doppler_gfx(g: float, gmax: float) -> int:
 
 def doppler_Q(Rp: int, pA: float, GSj: int, GS: int, j: int, n: int) -> int:
     return lib().orc_doppler_Q(Rp, pA, GSj, GS, j, n)
+
+
+def birth_mean_lik(vr, sd, sigma_b) -> float:
+    return lib().orc_birth_mean_lik(vr, sd, sigma_b)
+
+
+def exact_lik_cell(S, occ_max, p_b, pTP, pFP, pcl, pA, GS, gmax, n, vr, sd, sigma_b):
+    """A-38 cell update: (rho_p, rho_b, pAe, pi)."""
+    out = [C.c_float() for _ in range(4)]
+    lib().orc_exact_lik_cell(S, occ_max, p_b, pTP, pFP, pcl, pA, GS, gmax, n, vr, sd, sigma_b,
+                             *[C.byref(o) for o in out])
+    return tuple(o.value for o in out)
+
+
+def birth_assoc_exact(Rb: int, nb: int, pi: float):
+    na, ra = C.c_uint32(), C.c_uint64()
+    lib().orc_birth_assoc_exact(Rb, nb, pi, C.byref(na), C.byref(ra))
+    return na.value, ra.value
 
 
 def birth_assoc(Rb: int, nb: int, pA: float):
@@ -301,6 +324,16 @@ class Oracle:
         o = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1)
         assert o.size == 4 * self.C
         return lib().orc_step_exact(self._h, _ptr(o, C.c_float), C.c_float(dt))
+
+    def step_exact_lik(self, obs, lik, pA, dt: float) -> int:
+        """NEXT-3 exact PHD/MIB cycle with a single-object likelihood (A-38): obs [C, 4] = (occurred, p_TP,
+        p_FP, p_cl), lik [C, 4] = (u_x, u_y, v_r, sd), pA [C] association probability."""
+        o = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1)
+        d = np.ascontiguousarray(lik, dtype=np.float32).reshape(-1)
+        a = np.ascontiguousarray(pA, dtype=np.float32).reshape(-1)
+        assert o.size == 4 * self.C and d.size == 4 * self.C and a.size == self.C
+        return lib().orc_step_exact_lik(self._h, _ptr(o, C.c_float), _ptr(d, C.c_float), _ptr(a, C.c_float),
+                                        C.c_float(dt))
 
     def ego_scroll(self, dx: float, dy: float):
         """Ego-motion compensation (NEXT-2): (shift_x, shift_y) in cells, or None if refused."""

@@ -308,6 +308,10 @@ struct orc_ctx {
     uint64_t* GS;            /* [C] its sum over the cell's members                            */
     uint32_t* nA;            /* [C] associated birth slots (NEXT-1)                            */
     uint64_t* RbA;           /* [C] born mass of the associated set                            */
+    float* gmaxc;            /* [C] the cell's largest member likelihood (A-34)                */
+    float* pe;               /* [C] association weight of the members' split: p_A (NEXT-1) or
+                                    the effective pAe of the exact filter with a likelihood (A-38) */
+    float* pic;              /* [C] associated share of the births (A-38)                      */
     uint64_t scal[8];
     double res_x, res_y;     /* ego-motion residual, metres (NEXT-2) */
 };
@@ -342,6 +346,7 @@ int orc_create(const orc_params* p, orc_ctx** out)
     h->mean = xcalloc(2 * C, 4); h->cov = xcalloc(3 * C, 4);
     h->jidx = xcalloc(nu, 4);
     h->gfx = xcalloc(nu, 4); h->GS = xcalloc(C, 8); h->nA = xcalloc(C, 4); h->RbA = xcalloc(C, 8);
+    h->gmaxc = xcalloc(C, 4); h->pe = xcalloc(C, 4); h->pic = xcalloc(C, 4);
     *out = h;
     return 0;
 }
@@ -352,7 +357,7 @@ void orc_destroy(orc_ctx* h)
     void* ptrs[] = { h->x, h->y, h->vx, h->vy, h->m_free, h->px, h->py, h->pvx, h->pvy, h->key,
                      h->perm, h->offsets, h->S, h->mp, h->mfp, h->occ, h->fre, h->rho_p, h->rho_b,
                      h->Rp, h->Rb, h->nb, h->bx, h->by, h->bvx, h->bvy, h->bcell, h->mean, h->cov,
-                     h->jidx, h->gfx, h->GS, h->nA, h->RbA };
+                     h->jidx, h->gfx, h->GS, h->nA, h->RbA, h->gmaxc, h->pe, h->pic };
     for (size_t i = 0; i < sizeof(ptrs) / sizeof(ptrs[0]); ++i) free(ptrs[i]);
     free(h);
 }
@@ -416,6 +421,16 @@ int orc_step_exact(orc_ctx* h, const float* obs, float dt)
     return step_impl(h, NULL, obs, NULL, NULL, dt);
 }
 
+/* The exact PHD/MIB filter with a single-object likelihood (NEXT-3 general form; Eqs. 38, 49-52; A-38):
+ * obs[C][4] = (occurred, p_TP, p_FP, p_cl) -- the 4th value is the clutter density at the measurement;
+ * lik[C][4] = (u_x, u_y, v_r, sd): the measurement's radial-velocity likelihood g(z|x) = N(v.u - v_r;
+ * 0, sd^2) (the spatial likelihood of NEXT-1, Eq. 69); pA[C] = association probability.  Cells with
+ * p_A = 0 or no measurement take the uniform-likelihood update of orc_step_exact. */
+int orc_step_exact_lik(orc_ctx* h, const float* obs, const float* lik, const float* pA, float dt)
+{
+    return step_impl(h, NULL, obs, lik, pA, dt);
+}
+
 /* Cell update of the exact filter (A-37): r_p+ = min(S, occ_max) (Eq. 31 with the truncation of
  * P:938-939), r_b+ = p_B (1 - r_p+) (Eq. 32); r+ = r_p+ + r_b+; the common weight factor
  * f = p_TP / (p_FP (1 - r+) + p_TP r+) if a measurement occurred (Eqs. 38-40; the uniform likelihood
@@ -434,6 +449,65 @@ void orc_exact_cell(float S, float occ_max, float p_b, float occurred, float pTP
     float f = den > 0.0f ? num / den : 0.0f;
     *rho_p = rpp * f;
     *rho_b = rbp * f;
+}
+
+/* Expected single-object likelihood of a new-born object under the birth prior v ~ N(0, sigma_B^2 I)
+ * (A-38): the radial component v.u is N(0, sigma_B^2), so E[N(v.u - v_r; 0, sd^2)] = N(v_r; 0, s^2) with
+ * s^2 = sd^2 + sigma_B^2 -- evaluated like orc_doppler_g (exp spec, f32, this order). */
+float orc_birth_mean_lik(float vr, float sd, float sigma_b)
+{
+    float s = sqrtf(sd * sd + sigma_b * sigma_b);
+    float t = vr / s;
+    float q = (t * t) * -0.5f;
+    return orc_exp_spec(q) / (s * 2.50662827463100050f);
+}
+
+/* Cell update of the exact filter with a single-object likelihood (NEXT-3; Eqs. 49-52, P:973-1004;
+ * multi-object likelihood Eq. 38; A-38), for a cell where a measurement occurred:
+ *   g_A(z|x) = p_A g(z|x) + (1 - p_A) p_cl                               (the bracket of Eq. 38)
+ *   persistent: sum_i w~_i = p_TP r_p+ gbar_p, gbar_p = (p_A Sg + n (1 - p_A) p_cl) / n, Sg = sum_i g_i
+ *               = GS 2^-31 g_max (the members' likelihoods in the fixed point of A-34)
+ *   new-born:   sum_i w~_i = p_TP r_b+ gbar_b, gbar_b = p_A E_b[g] + (1 - p_A) p_cl (orc_birth_mean_lik)
+ *   mu = p_FP p_cl (1 - r+) + p_TP r_p+ gbar_p + p_TP r_b+ gbar_b        (Eq. 51)
+ *   rho_p = p_TP r_p+ gbar_p / mu, rho_b = p_TP r_b+ gbar_b / mu (f32)   (Eqs. 50, 52)
+ * r_p+, r_b+, r+ as orc_exact_cell (f32); the sums in fp64 in the written order.  Also returned: the
+ * effective association weight of the members' split pAe = p_A Sg / (p_A Sg + n (1 - p_A) p_cl), so
+ * that member j's share of rho_p is the Doppler Q_j form (orc_doppler_Q with pAe, A-35) of
+ * g_A(z|x_j) / sum_i g_A(z|x_i); and the associated share of the births pi = p_A E_b[g] / gbar_b. */
+void orc_exact_lik_cell(float S, float occ_max, float p_b, float pTP, float pFP, float pcl, float pA, uint64_t GS,
+                        float gmax, uint32_t n, float vr, float sd, float sigma_b, float* rho_p, float* rho_b,
+                        float* pAe, float* pi)
+{
+    float rpp = fminf(S, occ_max);
+    float rbp = p_b * (1.0f - rpp);
+    float rplus = rpp + rbp;
+    float rbar = 1.0f - rplus;
+    double pa = (double)pA, cl = (double)pcl;
+    double Sg = ((double)GS * 0x1p-31) * (double)gmax;
+    double gA_sum = pa * Sg + ((double)n * (1.0 - pa)) * cl;          /* sum over the members of g_A */
+    double gp = n ? gA_sum / (double)n : 0.0;
+    double Eb = (double)orc_birth_mean_lik(vr, sd, sigma_b);
+    double gb = pa * Eb + (1.0 - pa) * cl;
+    double num_p = ((double)pTP * (double)rpp) * gp;
+    double num_b = ((double)pTP * (double)rbp) * gb;
+    double mu = (((double)pFP * cl) * (double)rbar + num_p) + num_b;
+    *rho_p = mu > 0.0 ? (float)(num_p / mu) : 0.0f;
+    *rho_b = mu > 0.0 ? (float)(num_b / mu) : 0.0f;
+    *pAe = gA_sum > 0.0 ? (float)((pa * Sg) / gA_sum) : 0.0f;
+    *pi = gb > 0.0 ? (float)((pa * Eb) / gb) : 0.0f;
+}
+
+/* Associated births of the exact filter with a likelihood (A-38): nu_A = floor(pi nb + 1/2) of the nb
+ * slots draw the radial component from the posterior given the measurement, the rest from the prior;
+ * all slots share R_b evenly (one weight for the whole birth set), i.e. R_bA = nu_A floor(R_b / nb) +
+ * min(nu_A, R_b mod nb) -- the first nu_A slots' part of the single even split. */
+void orc_birth_assoc_exact(uint64_t Rb, uint32_t nb, float pi, uint32_t* nA, uint64_t* RbA)
+{
+    uint32_t na = (uint32_t)floor((double)pi * (double)nb + 0.5);
+    if (na > nb) na = nb;
+    uint64_t bb = nb ? Rb / nb : 0, rb = nb ? Rb % nb : 0;
+    *nA = na;
+    *RbA = (uint64_t)na * bb + (na < rb ? na : rb);
 }
 
 static int step_impl(orc_ctx* h, const float* meas, const float* obs, const float* dop, const float* pA, float dt)
@@ -477,6 +551,33 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
     for (int64_t c = 0; c < C; ++c) h->offsets[c + 1] = h->offsets[c] + count[c];
     free(kv);
 
+    /* ---- the members' likelihoods in cells with one (NEXT-1 Doppler; NEXT-3 with a likelihood: only
+     *      where a measurement occurred): g from orc_doppler_g, the cell's largest g_max, the fixed point
+     *      gfx relative to it (A-34) and its sum GS -- before the cell update, which needs GS (A-38) ---- */
+#define LIK_CELL(c) (dop && pA && pA[c] > 0.0f && (!obs || obs[4 * (c)] > 0.0f))
+    for (int64_t i = 0; i < nu; ++i) h->gfx[i] = 0u;
+    for (int64_t c = 0; c < C; ++c) {
+        uint32_t a = h->offsets[c], b = h->offsets[c + 1];
+        h->GS[c] = 0; h->gmaxc[c] = 0.0f; h->pe[c] = 0.0f; h->pic[c] = 0.0f;
+        if (!LIK_CELL(c)) continue;
+        h->pe[c] = pA[c];
+        const float* d = dop + 4 * c;
+        float gmax = 0.0f;                                     /* the cell's largest likelihood (A-34) */
+        for (uint32_t j = a; j < b; ++j) {
+            uint32_t i = h->perm[j];
+            float g = orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]);
+            if (g > gmax) gmax = g;
+        }
+        uint64_t gs = 0;
+        for (uint32_t j = a; j < b; ++j) {
+            uint32_t i = h->perm[j];
+            h->gfx[i] = orc_doppler_gfx(orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]), gmax);
+            gs += h->gfx[i];
+        }
+        h->GS[c] = gs;
+        h->gmaxc[c] = gmax;
+    }
+
     /* ---- O3 Cells (Alg. 3; Eqs. 61-63, 67-68; A-7..A-13, A-22, A-23, A-27) ---- */
     uint64_t bad = 0;
     for (int64_t c = 0; c < C && obs; ++c) {                  /* exact PHD/MIB (NEXT-3, A-37) */
@@ -486,7 +587,13 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
         float S = (float)sum;
         const float* ob = obs + 4 * c;
         float rp, rb;
-        orc_exact_cell(S, P->occ_max, P->p_b, ob[0], ob[1], ob[2], &rp, &rb);
+        if (LIK_CELL(c)) {                                     /* a measurement with a likelihood (A-38) */
+            const float* d = dop + 4 * c;
+            orc_exact_lik_cell(S, P->occ_max, P->p_b, ob[1], ob[2], ob[3], pA[c], h->GS[c], h->gmaxc[c], b - a,
+                               d[2], d[3], P->sigma_birth_vel, &rp, &rb, &h->pe[c], &h->pic[c]);
+        } else {
+            orc_exact_cell(S, P->occ_max, P->p_b, ob[0], ob[1], ob[2], &rp, &rb);
+        }
         h->S[c] = S; h->mp[c] = fminf(S, P->occ_max); h->mfp[c] = 0.0f;
         h->occ[c] = rp + rb; h->fre[c] = 1.0f - (rp + rb); h->rho_p[c] = rp; h->rho_b[c] = rb;
         h->Rp[c] = (b > a) ? fx40(rp) : 0;                     /* A-23 */
@@ -519,27 +626,8 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
      * gfx relative to the cell's largest g (orc_doppler_gfx, A-34); the members' fixed-point weights
      * are the differences of Q_j (orc_doppler_Q, A-35), and the moments weight each member by
      * q_j / R_p.  Sum of gfx = 0 (no member compatible with the
-     * measurement): the mu_A term is dropped -- the cell is treated as p_A = 0. */
-    for (int64_t i = 0; i < nu; ++i) h->gfx[i] = 0u;
-    for (int64_t c = 0; c < C; ++c) {
-        uint32_t a = h->offsets[c], b = h->offsets[c + 1];
-        h->GS[c] = 0;
-        if (!(dop && pA && pA[c] > 0.0f)) continue;
-        const float* d = dop + 4 * c;
-        float gmax = 0.0f;                                     /* the cell's largest likelihood (A-34) */
-        for (uint32_t j = a; j < b; ++j) {
-            uint32_t i = h->perm[j];
-            float g = orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]);
-            if (g > gmax) gmax = g;
-        }
-        uint64_t gs = 0;
-        for (uint32_t j = a; j < b; ++j) {
-            uint32_t i = h->perm[j];
-            h->gfx[i] = orc_doppler_gfx(orc_doppler_g(h->pvx[i], h->pvy[i], d[0], d[1], d[2], d[3]), gmax);
-            gs += h->gfx[i];
-        }
-        h->GS[c] = gs;
-    }
+     * measurement): the mu_A term is dropped -- the cell is treated as p_A = 0.
+     * (gfx and GS were computed before the cell update; h->pe holds the split's association weight.) */
     for (int64_t c = 0; c < C; ++c) {
         uint32_t a = h->offsets[c], b = h->offsets[c + 1];
         float* mean = h->mean + 2 * c; float* cov = h->cov + 3 * c;
@@ -555,7 +643,7 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
             for (uint32_t j = 0; j < n; ++j) {
                 uint32_t i = h->perm[a + j];
                 gsj += h->gfx[i];
-                uint64_t Qn = orc_doppler_Q(Rp, pA[c], gsj, GS, j + 1, n);
+                uint64_t Qn = orc_doppler_Q(Rp, h->pe[c], gsj, GS, j + 1, n);
                 double wd = (double)(Qn - Qj) * 0x1p-40, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
                 Mx += wd * vx; My += wd * vy;
                 Mxx += wd * vx * vx; Myy += wd * vy * vy; Mxy += wd * vx * vy;
@@ -589,7 +677,10 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
     }
     for (int64_t c = 0; c < C; ++c) {
         h->nA[c] = 0; h->RbA[c] = 0;
-        if (dop && pA && pA[c] > 0.0f && h->nb[c] > 0) orc_birth_assoc(h->Rb[c], h->nb[c], pA[c], &h->nA[c], &h->RbA[c]);
+        if (LIK_CELL(c) && h->nb[c] > 0) {
+            if (obs) orc_birth_assoc_exact(h->Rb[c], h->nb[c], h->pic[c], &h->nA[c], &h->RbA[c]);   /* A-38 */
+            else orc_birth_assoc(h->Rb[c], h->nb[c], pA[c], &h->nA[c], &h->RbA[c]);               /* A-36 */
+        }
     }
     {
         int64_t j = 0;
@@ -606,7 +697,16 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
                 float n0, n1;
                 orc_box_muller(R[2], R[3], &n0, &n1);
                 float bvx, bvy;
-                if (r < h->nA[c]) {                            /* associated: p(x | z), Eq. 74 */
+                if (r < h->nA[c] && obs) {                     /* exact filter: the posterior given z (A-38) */
+                    const float* d = dop + 4 * c;
+                    const float sb2 = P->sigma_birth_vel * P->sigma_birth_vel, sd2 = d[3] * d[3];
+                    const float mu_r = (d[2] * sb2) / (sb2 + sd2);
+                    const float s_r = (P->sigma_birth_vel * d[3]) / sqrtf(sb2 + sd2);
+                    float sr = fmaf(s_r, n0, mu_r);            /* radial speed */
+                    float st = P->sigma_birth_vel * n1;        /* tangential speed */
+                    bvx = fmaf(sr, d[0], -(st * d[1]));
+                    bvy = fmaf(sr, d[1], st * d[0]);
+                } else if (r < h->nA[c]) {                     /* associated: p(x | z), Eq. 74 */
                     const float* d = dop + 4 * c;
                     float sr = fmaf(d[3], n0, d[2]);           /* radial speed */
                     float st = P->sigma_birth_vel * n1;        /* tangential speed */
@@ -641,7 +741,7 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
                 uint64_t gsj = 0, Qj = 0;
                 for (uint32_t r = 0; r < n; ++r, ++jj) {
                     gsj += h->gfx[h->perm[a + r]];
-                    uint64_t Qn = orc_doppler_Q(h->Rp[c], pA[c], gsj, h->GS[c], r + 1, n);
+                    uint64_t Qn = orc_doppler_Q(h->Rp[c], h->pe[c], gsj, h->GS[c], r + 1, n);
                     q[jj] = Qn - Qj;
                     Qj = Qn;
                     src[jj] = h->perm[a + r];

@@ -97,6 +97,12 @@ int  orc_step_doppler(orc_ctx* h, const float* meas, const float* dop, const flo
  * clutter density (section IV-F setting): obs[C][4] = (occurred 0/1, p_TP, p_FP, unused) (A-37).
  * m_F is not used (left unchanged); occupancy readout = rho_p + rho_b, free = 1 - occupancy. */
 int  orc_step_exact(orc_ctx* h, const float* obs, float dt);
+int  orc_step_exact_lik(orc_ctx* h, const float* obs, const float* lik, const float* pA, float dt);
+float orc_birth_mean_lik(float vr, float sd, float sigma_b);
+void orc_exact_lik_cell(float S, float occ_max, float p_b, float pTP, float pFP, float pcl, float pA, uint64_t GS,
+                        float gmax, uint32_t n, float vr, float sd, float sigma_b, float* rho_p, float* rho_b,
+                        float* pAe, float* pi);
+void orc_birth_assoc_exact(uint64_t Rb, uint32_t nb, float pi, uint32_t* nA, uint64_t* RbA);
 void orc_exact_cell(float S, float occ_max, float p_b, float occurred, float pTP, float pFP, float* rho_p,
                     float* rho_b);
 /* NEXT-1 primitives (exported for the pins) */
