@@ -389,8 +389,8 @@ def bench_ours(args, cfg):
     try:
         ne = min(K, 6)
         obs = [I.Scene.exact_obs(frames[settle + W + i]) for i in range(ne)]
-        for i in range(2):
-            f.step_exact(obs[i], cfg.dt, stream)
+        for i in range(12):                                # to the exact filter's steady state (spread births)
+            f.step_exact(obs[i % ne], cfg.dt, stream)
         torch.cuda.synchronize()
         x0 = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
         x1 = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
@@ -408,6 +408,36 @@ def bench_ours(args, cfg):
                  "input": "inputs.Scene.exact_obs of the same frames (DESIGN.md A-37 recipe)"}
     except Exception as exc:   # noqa: BLE001
         exact = {"error": str(exc)}
+
+    # NEXT-3 general form: the exact filter with a single-object likelihood (A-38), continuing from there
+    exact_lik = None
+    try:
+        nl = min(K, 6)
+        kk = [settle + W + i for i in range(nl)]
+        ins = [sc.exact_lik(k, frames[k].cpu()) for k in kk]
+        ins = [tuple(t.to(dev).contiguous() for t in x) for x in ins]
+        for i in range(4):
+            f.step_exact_lik(*ins[i % nl], cfg.dt, stream)
+        torch.cuda.synchronize()
+        l0 = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
+        l1 = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
+        for i in range(nl):
+            flush.zero_()
+            l0[i].record(stream)
+            f.step_exact_lik(*ins[i], cfg.dt, stream)
+            l1[i].record(stream)
+        torch.cuda.synchronize()
+        lms = float(np.mean([l0[i].elapsed_time(l1[i]) for i in range(nl)]))
+        n_lik = int(sum(((x[2] > 0) & (x[0][..., 0] > 0)).sum().item() for x in ins) / nl)
+        # + lik grid 16 B and p_A 4 B per cell; members' g / gfx written and read (16 B) per particle
+        lk_bytes = a_alg(cfg) + 36.0 * cfg.C + 16.0 * cfg.nu
+        exact_lik = {"ms_per_step": lms, "value": cfg.nu / (lms * 1e-3), "unit": UNIT,
+                     "algorithmic_bytes": lk_bytes, "achieved_GBps": lk_bytes / (lms * 1e-3) / 1e9,
+                     "frac": lk_bytes / (lms * 1e-3) / 1e9 / peaks()[0], "likelihood_cells": n_lik,
+                     "input": "inputs.Scene.exact_lik of the same frames (DESIGN.md A-38 recipe: radar overlay on 50 % "
+                              "of the cells with a return, p_A 0.8, sd 0.25 m/s, p_cl 0.02)"}
+    except Exception as exc:   # noqa: BLE001
+        exact_lik = {"error": str(exc)}
 
     # NEXT-2 (ego-motion compensation): one scroll of grid and particles at this size, device-timed
     ego = None
@@ -505,7 +535,7 @@ def bench_ours(args, cfg):
         "continuous": {"ms_per_step": cont_ms, "value": cfg.nu / (cont_ms * 1e-3), "unit": UNIT,
                        "note": "K cycles back to back, no flush between them (working set > L2)"},
         "gpu_launches": f.launches_per_step() * K, "clocks": clk,
-        "next_rows": {"doppler": doppler, "exact_phd_mib": exact, "ego_scroll": ego, "evaluate": evaluation},
+        "next_rows": {"doppler": doppler, "exact_phd_mib": exact, "exact_lik": exact_lik, "ego_scroll": ego, "evaluate": evaluation},
         "configs": configs,
         "n_in": sc_dev["n_in"], "W_total_mass": sc_dev["W"] * 2.0 ** -40,
         "paper_context": "GTX980: 2e6 particles, 1.44e6 cells -> 31.055 ms (PAPER.md:1832), not this workload",

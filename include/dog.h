@@ -262,6 +262,22 @@ int dog_eval_cells(dog_ctx* ctx, const float* mean_dev, const float* cov_dev, co
  * existence probability r (Eq. 42), free = 1 - r, moments as dog_step.  DOG_E_STATE for bands. */
 int dog_step_exact(dog_ctx* ctx, const float* obs, float dt, void* stream);
 
+/* dog_step_exact_lik -- one cycle of the exact PHD/MIB filter with a single-object likelihood (NEXT-3
+ * general form; Eqs. 38, 49-52; A-38).  obs as dog_step_exact with
+ * the 4th value the clutter density p_cl at the cell's measurement; plus two DEVICE arrays:
+ *   lik[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) -- the measurement's radial-velocity likelihood
+ *             g(z|x) = N(v.u - v_r; 0, sd^2) (Eq. 69), read only where p_assoc > 0 and occurred;
+ *   p_assoc[C] f32: association probability p_A in [0, 1].
+ * In a cell where a measurement occurred and p_A > 0: g_A(z|x) = p_A g(z|x) + (1 - p_A) p_cl, rho_p
+ * and rho_b from the members' likelihood sum and the birth prior's expected likelihood (Eqs. 50-52),
+ * the members' weights proportional to g_A (the Doppler Q_j split with the effective association
+ * weight), and the associated births' radial velocity drawn from the posterior given z.  Every other
+ * cell takes dog_step_exact's update; p_assoc all 0 gives exactly dog_step_exact.  Whole-grid contexts
+ * only (DOG_E_STATE for bands); working buffers (16 B per particle slot + 28 B per cell) are allocated
+ * on first use (DOG_E_NOMEM).  DOG_E_INVAL for a NULL or misaligned argument or an invalid dt. */
+int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const float* p_assoc, float dt,
+                       void* stream);
+
 /* dog_step_doppler -- one cycle with the Doppler / association branch (Eqs. 69-80,
  * P:1157-1232; A-34..A-36).  As dog_step, plus two DEVICE arrays:
  *   doppler[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) per cell -- unit radial direction, measured

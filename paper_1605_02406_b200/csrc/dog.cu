@@ -103,6 +103,10 @@ struct dog_ctx {
     uint8_t* d_tflag = nullptr;                   // per sort tile: holds members of a Doppler cell
     uint32_t* d_gfx = nullptr;                    // per sorted position: g (f32 bits), then fixed-point gfx
     uint32_t* d_gmax = nullptr;                   // per cell: the largest member likelihood (f32 bits, A-34)
+    // exact filter with a likelihood (NEXT-3, A-38), allocated on the first dog_step_exact_lik
+    uint64_t* d_GSc = nullptr;                    // per cell: sum of the members' gfx (zero between cycles)
+    float* d_pAe = nullptr;                       // per cell: effective association weight of the members' split
+    float* d_pic = nullptr;                       // per cell: associated share of the births
     const float* band_dop = nullptr;              // band contexts: the cycle's Doppler grid (assign -> resample)
     const float* band_pA = nullptr;
     bool band_exact = false;                      // band contexts: this cycle runs the exact PHD/MIB update
@@ -552,18 +556,18 @@ static int L_predict_sort(dog_ctx* ctx, bool fused, const StepArgs& a, const Fil
 }
 
 static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                   const float* obs = nullptr)
+                   const float* obs = nullptr, const ExactLik& xl = ExactLik{})
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
     if (obs)
         CK(launch(k_cells<true>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
                   (const float2*)nullptr, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)obs));
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)obs, xl));
     else
         CK(launch(k_cells<false>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
                   (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)nullptr));
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)nullptr, xl));
     return DOG_OK;
 }
 
@@ -631,7 +635,7 @@ static int L_moments(dog_ctx* ctx, cudaStream_t st, const uint64_t* GSd = nullpt
 }
 
 static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                    const DopIn* din = nullptr, bool per_slot = false)
+                    const DopIn* din = nullptr, bool per_slot = false, const BirthLik& bl = BirthLik{})
 {
     if (ctx->nu_b == 0) return DOG_OK;
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
@@ -639,7 +643,7 @@ static int L_births(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cuda
     BirthDebug bd{dbg ? ctx->bx : nullptr, ctx->by, ctx->bvx, ctx->bvy};
     if (per_slot)
         CK(launch(k_births_slots, (uint32_t)std::max<int64_t>(1, std::min<int64_t>((ctx->nu_b + 255) / 256, 8 * 148)), 256, 0,
-                  st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc, (int64_t)a.k));
+                  st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc, (int64_t)a.k, bl));
     else
         CK(launch(k_births, ctx->birth_blocks, 256, 0, st, 0, ctx->list, ns, bd, (const DevScalars*)ctx->sc, fc,
                   (int64_t)a.k, din ? din->pA : (const float*)nullptr, din ? din->dop : (const float4*)nullptr));
@@ -731,7 +735,8 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
 static void free_doppler(dog_ctx* ctx)
 {
     for (void** p : {(void**)&ctx->d_rg, (void**)&ctx->d_rs, (void**)&ctx->d_GS, (void**)&ctx->d_tflag,
-                     (void**)&ctx->d_gfx, (void**)&ctx->d_gmax}) {
+                     (void**)&ctx->d_gfx, (void**)&ctx->d_gmax, (void**)&ctx->d_GSc, (void**)&ctx->d_pAe,
+                     (void**)&ctx->d_pic}) {
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
@@ -752,13 +757,14 @@ static int alloc_doppler(dog_ctx* ctx)
 }
 
 // the members' likelihoods g, the cell maxima g_max, then gfx relative to g_max summed per run (A-34)
-static int L_dopp_runs(dog_ctx* ctx, const DopIn& din, const FilterConst& fc, int par, cudaStream_t st)
+static int L_dopp_runs(dog_ctx* ctx, const DopIn& din, const FilterConst& fc, int par, cudaStream_t st,
+                       uint64_t* gsc = nullptr)
 {
     CK(cudaMemsetAsync(ctx->d_gmax, 0, (size_t)ctx->C * 4, st));
     CK(launch(k_dopp_g, ctx->tiles, 256, 0, st, 0, ctx->tp, (const float2*)ctx->pv, din,
               ctx->d_gmax, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
     CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, ctx->tp, din, (const uint32_t*)ctx->d_gmax, ctx->d_rg,
-              ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
+              ctx->d_tflag, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par, gsc));
     return DOG_OK;
 }
 
@@ -810,6 +816,72 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     if (int r = L_moments(ctx, st, ctx->d_GS)) return r;
     if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     else if (int r = L_births(ctx, a, fc, st, &din)) return r;
+    ctx->k += 1;
+    return DOG_OK;
+}
+
+// ---- exact filter with a single-object likelihood (NEXT-3 general form, A-38): the members'
+// likelihoods and their per-cell sums come first (the cell update needs them), then the exact cycle
+// with the Doppler split in the likelihood cells.
+static int alloc_lik(dog_ctx* ctx)
+{
+    if (int r = alloc_doppler(ctx)) return r;
+    if (ctx->d_GSc && ctx->d_pAe && ctx->d_pic) return DOG_OK;
+    for (void** p : {(void**)&ctx->d_GSc, (void**)&ctx->d_pAe, (void**)&ctx->d_pic}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    if (cudaMalloc(&ctx->d_GSc, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_pAe, (size_t)ctx->C * 4) != cudaSuccess ||
+        cudaMalloc(&ctx->d_pic, (size_t)ctx->C * 4) != cudaSuccess ||
+        cudaMemset(ctx->d_GSc, 0, (size_t)ctx->C * 8) != cudaSuccess) {   // k_cells clears what it reads
+        free_doppler(ctx);
+        cudaGetLastError();
+        return DOG_E_NOMEM;
+    }
+    return DOG_OK;
+}
+
+int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const float* p_assoc, float dt, void* stream)
+{
+    if (!ctx || !obs || !lik || !p_assoc) return DOG_E_INVAL;
+    if (((uintptr_t)obs & 15u) != 0 || ((uintptr_t)lik & 15u) != 0) return DOG_E_INVAL;
+    if (ctx->poisoned) return DOG_E_CUDA;
+    if (ctx->world > 1) return DOG_E_STATE;                 // whole-grid contexts only
+    if (!(dt > 0.0f) || !finite(dt)) return DOG_E_INVAL;
+    if (int r = set_device(ctx)) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int r = alloc_lik(ctx)) return r;
+    const StepArgs a = step_args(ctx, dt);
+    const FilterConst fc = filter_const(ctx);
+    const int par = (int)(a.k & 1);
+    // gated: only cells where a measurement occurred carry the likelihood
+    const DopIn dg{(const float4*)lik, p_assoc, (const float4*)obs};
+    if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
+    if (int r = L_dopp_runs(ctx, dg, fc, par, st, ctx->d_GSc)) return r;
+    const ExactLik xl{p_assoc, (const float4*)lik, ctx->d_GSc, (const uint32_t*)ctx->d_gmax, ctx->d_pAe, ctx->d_pic};
+    if (int r = L_cells(ctx, nullptr, a, fc, st, obs, xl)) return r;
+    if (int r = L_list_scan(ctx, nullptr, a, fc, st, true)) return r;
+    // run sums are nonzero only in the gated cells, so the ungated p_A marks the same Doppler cells
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, true, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag})) return r;
+    const BirthLik bl{p_assoc, (const float4*)obs, (const float4*)lik, ctx->d_pic};
+    const bool fork = ctx->side != nullptr;
+    if (fork) {   // births beside the resampling (disjoint output slots), as in dog_step
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        if (int r = L_births(ctx, a, fc, ctx->side, nullptr, true, bl)) return r;
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+    }
+    if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag, true)) return r;
+    // the members' split weight in the likelihood cells is the effective pAe (A-38)
+    const DopIn de{(const float4*)lik, ctx->d_pAe, nullptr};
+    NextState ns{ctx->st, nullptr};
+    CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, ctx->tp,
+                 (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->ppart, de, (const uint64_t*)ctx->d_rg, ctx->d_rs,
+                 (const uint64_t*)ctx->d_GS, (const uint8_t*)ctx->d_tflag, (const uint32_t*)ctx->d_gfx,
+                 (const DevScalars*)ctx->sc, fc, par));
+    if (int r = L_moments(ctx, st, ctx->d_GS, true)) return r;
+    if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
+    else if (int r = L_births(ctx, a, fc, st, nullptr, true, bl)) return r;
     ctx->k += 1;
     return DOG_OK;
 }

@@ -64,6 +64,27 @@ __device__ __forceinline__ uint64_t fx40(float m)
     return (m > 0.0f) ? __double2ull_rz(__dmul_rn((double)m, 1099511627776.0)) : 0ull;
 }
 
+// e^q for q <= 0 (A-34 "exp spec")
+__device__ __forceinline__ float exp_spec(float q)
+{
+    if (!(q >= -87.0f)) return 0.0f;
+    if (q > 0.0f) q = 0.0f;
+    const float kf = rintf(__fmul_rn(q, 1.44269504088896341f));
+    float r = __fmaf_rn(-kf, 0.693359375f, q);
+    r = __fmaf_rn(-kf, -2.12194440e-4f, r);
+    const float z = __fmul_rn(r, r);
+    float y = 1.9875691500e-4f;
+    y = __fmaf_rn(y, r, 1.3981999507e-3f);
+    y = __fmaf_rn(y, r, 8.3334519073e-3f);
+    y = __fmaf_rn(y, r, 4.1665795894e-2f);
+    y = __fmaf_rn(y, r, 1.6666665459e-1f);
+    y = __fmaf_rn(y, r, 5.0000001201e-1f);
+    y = __fmaf_rn(y, z, r);
+    y = __fadd_rn(y, 1.0f);
+    const int k = (int)kf;                                   // -126 <= k <= 0
+    return __fmul_rn(y, __int_as_float((127 + k) << 23));
+}
+
 struct CellOut {
     uint32_t n;
     float S, mO, mF, rp, rb;
@@ -141,6 +162,82 @@ __device__ __forceinline__ CellOut cell_math_exact(uint32_t n, float4 obs, float
     return o;
 }
 
+// The exact filter with a single-object likelihood (NEXT-3 general form, A-38): cells where
+// a measurement occurred and p_A > 0 take the g_A update of cell_math_exact_lik.  pA == nullptr: off.
+struct ExactLik {
+    const float* pA;          // [C] association probability
+    const float4* lik;        // [C] (u_x, u_y, v_r, sd)
+    uint64_t* GSc;            // [C] sum of the members' gfx (k_dopp_runs); cleared here after reading
+    const uint32_t* gmax;     // [C] largest member likelihood (f32 bits, A-34)
+    float* pAe;               // [C] out: effective association weight of the members' split
+    float* pic;               // [C] out: associated share of the births
+};
+
+__device__ __forceinline__ bool lik_cell(const ExactLik& xl, float4 ob, uint32_t c)
+{
+    return xl.pA && ob.x > 0.0f && xl.pA[c] > 0.0f;
+}
+
+// E[g] of a new-born object under the birth prior v ~ N(0, sigma_B^2 I): N(v_r; 0, sd^2 + sigma_B^2)
+// (A-38), f32 in the order of the oracle's orc_birth_mean_lik
+__device__ __forceinline__ float birth_mean_lik(float vr, float sd, float sigma_b)
+{
+    const float s = __fsqrt_rn(__fadd_rn(__fmul_rn(sd, sd), __fmul_rn(sigma_b, sigma_b)));
+    const float t = __fdiv_rn(vr, s);
+    const float q = __fmul_rn(__fmul_rn(t, t), -0.5f);
+    return __fdiv_rn(exp_spec(q), __fmul_rn(s, 2.50662827463100050f));
+}
+
+// Eqs. 49-52 with g_A = p_A g + (1 - p_A) p_cl for a cell with a measurement (A-38): the fp64 sums in
+// the oracle's written order (orc_exact_lik_cell), r_p+, r_b+ as cell_math_exact.  pAe / pi returned.
+__device__ __forceinline__ CellOut cell_math_exact_lik(uint32_t n, float4 ob, float w_pred, const FilterConst& fc,
+                                                       float pA, float4 d, uint64_t GS, float gmax, float& pAe,
+                                                       float& pi)
+{
+    CellOut o;
+    o.n = n;
+    o.S = __double2float_rn(__dmul_rn((double)n, (double)w_pred));
+    const float rpp = fminf(o.S, fc.occ_max);
+    const float rbp = __fmul_rn(fc.p_b, __fsub_rn(1.0f, rpp));
+    const float rplus = __fadd_rn(rpp, rbp), rbar = __fsub_rn(1.0f, rplus);
+    const double pa = (double)pA, cl = (double)ob.w;
+    const double Sg = __dmul_rn(__dmul_rn(__ull2double_rn(GS), 0x1p-31), (double)gmax);
+    const double gA_sum = __dadd_rn(__dmul_rn(pa, Sg), __dmul_rn(__dmul_rn((double)n, __dsub_rn(1.0, pa)), cl));
+    const double gp = n ? __ddiv_rn(gA_sum, (double)n) : 0.0;
+    const double Eb = (double)birth_mean_lik(d.z, d.w, fc.sigma_b);
+    const double gb = __dadd_rn(__dmul_rn(pa, Eb), __dmul_rn(__dsub_rn(1.0, pa), cl));
+    const double num_p = __dmul_rn(__dmul_rn((double)ob.y, (double)rpp), gp);
+    const double num_b = __dmul_rn(__dmul_rn((double)ob.y, (double)rbp), gb);
+    const double mu = __dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn((double)ob.z, cl), (double)rbar), num_p), num_b);
+    o.rp = mu > 0.0 ? __double2float_rn(__ddiv_rn(num_p, mu)) : 0.0f;
+    o.rb = mu > 0.0 ? __double2float_rn(__ddiv_rn(num_b, mu)) : 0.0f;
+    pAe = gA_sum > 0.0 ? __double2float_rn(__ddiv_rn(__dmul_rn(pa, Sg), gA_sum)) : 0.0f;
+    pi = gb > 0.0 ? __double2float_rn(__ddiv_rn(__dmul_rn(pa, Eb), gb)) : 0.0f;
+    o.mO = __fadd_rn(o.rp, o.rb);
+    o.mF = __fsub_rn(1.0f, o.mO);
+    o.Rp = n > 0 ? fx40(o.rp) : 0ull;
+    o.Rb = fx40(o.rb);
+    o.bad = false;
+    return o;
+}
+
+// the exact update of cell c: with the likelihood where lik_cell, else cell_math_exact.  commit: the
+// final evaluation of an active cell -- writes pAe / pi and clears the cell's GS accumulator.
+__device__ __forceinline__ CellOut cell_exact_any(uint32_t n, float4 ob, uint32_t c, float w_pred, const FilterConst& fc,
+                                                  const ExactLik& xl, bool commit)
+{
+    if (!lik_cell(xl, ob, c)) return cell_math_exact(n, ob, w_pred, fc);
+    const uint64_t GS = xl.GSc[c];
+    float pAe, pi;
+    const CellOut o = cell_math_exact_lik(n, ob, w_pred, fc, xl.pA[c], xl.lik[c], GS, __uint_as_float(xl.gmax[c]), pAe, pi);
+    if (commit) {
+        xl.pAe[c] = pAe;
+        xl.pic[c] = pi;
+        if (GS) xl.GSc[c] = 0ull;
+    }
+    return o;
+}
+
 constexpr int kCellThreads = 256, kCellItems = 8, kCellIter = kCellThreads * kCellItems;   // 2048 cells
 constexpr int kMaxCellBlocks = 4096;
 
@@ -176,7 +273,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* sc, FilterConst fc, float alpha,
-    const float4* __restrict__ obs)
+    const float4* __restrict__ obs, ExactLik xl)
 {
     PDL_ENTER();
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
@@ -219,7 +316,8 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
-            const CellOut o = kExact ? cell_math_exact(n[i], ob[i], w_pred, fc) : cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
+            const CellOut o = kExact ? cell_exact_any(n[i], ob[i], c, w_pred, fc, xl, false)
+                                     : cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
             const bool vnow = valid && o.n > 0 && o.rp > 0.0f && o.S > 0.0f;
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
             const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
@@ -259,7 +357,7 @@ __global__ __launch_bounds__(kCellThreads, 4) void k_cells(
             if ((abal[i] >> lane) & 1u) {               // active cell: same inputs (untouched), same arithmetic
                 const uint32_t c = base + i * kCellThreads + tid;
                 // exact filter: the inputs are still in registers (no reload: every cell comes here)
-                const CellOut o = kExact ? cell_math_exact(n[i], ob[i], w_pred, fc)
+                const CellOut o = kExact ? cell_exact_any(n[i], ob[i], c, w_pred, fc, xl, true)
                                          : cell_math(__ldcg(counts + c), __ldcg(m_free + c), meas[c], w_pred, alpha, fc);
                 if (!kExact) m_free[c] = o.mF;
                 if (o.n) counts[c] = 0u;                // ready for the next cycle's k_predict_sort

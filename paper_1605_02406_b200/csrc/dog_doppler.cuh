@@ -33,27 +33,15 @@ namespace dog {
 struct DopIn {
     const float4* dop;    // [C] (u_x, u_y, v_r, sd)
     const float* pA;      // [C] association probability (0: no Doppler in the cell)
+    const float4* gate;   // [C] obs of the exact filter (A-38): only cells where a measurement occurred; or nullptr
 };
 
-// e^q for q <= 0 (A-34 "exp spec")
-__device__ __forceinline__ float exp_spec(float q)
+// the association probability a member of cell `key` is weighted with (0: no likelihood)
+__device__ __forceinline__ float din_pa(const DopIn& din, uint32_t key, uint32_t C)
 {
-    if (!(q >= -87.0f)) return 0.0f;
-    if (q > 0.0f) q = 0.0f;
-    const float kf = rintf(__fmul_rn(q, 1.44269504088896341f));
-    float r = __fmaf_rn(-kf, 0.693359375f, q);
-    r = __fmaf_rn(-kf, -2.12194440e-4f, r);
-    const float z = __fmul_rn(r, r);
-    float y = 1.9875691500e-4f;
-    y = __fmaf_rn(y, r, 1.3981999507e-3f);
-    y = __fmaf_rn(y, r, 8.3334519073e-3f);
-    y = __fmaf_rn(y, r, 4.1665795894e-2f);
-    y = __fmaf_rn(y, r, 1.6666665459e-1f);
-    y = __fmaf_rn(y, r, 5.0000001201e-1f);
-    y = __fmaf_rn(y, z, r);
-    y = __fadd_rn(y, 1.0f);
-    const int k = (int)kf;                                   // -126 <= k <= 0
-    return __fmul_rn(y, __int_as_float((127 + k) << 23));
+    if (key >= C) return 0.0f;
+    const float pa = din.pA[key];
+    return (pa > 0.0f && din.gate && !(din.gate[key].x > 0.0f)) ? 0.0f : pa;
 }
 
 // Doppler likelihood g(z | x) of a predicted velocity (Eq. 69; A-34), f32
@@ -120,7 +108,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __re
     uint32_t j = run_of(s_first, nd, p0);
     uint32_t end = s_first[j + 1];
     uint32_t key = tp.key[base + j];
-    float pa = key < fc.C ? din.pA[key] : 0.0f;
+    float pa = din_pa(din, key, fc.C);
     float4 d = pa > 0.0f ? din.dop[key] : make_float4(0.f, 0.f, 0.f, 1.f);
     uint32_t mx = 0u;
     for (uint32_t p = p0; p < p1; ++p) {
@@ -129,7 +117,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __re
             mx = 0u;
             ++j; end = s_first[j + 1];
             key = tp.key[base + j];
-            pa = key < fc.C ? din.pA[key] : 0.0f;
+            pa = din_pa(din, key, fc.C);
             if (pa > 0.0f) d = din.dop[key];
         }
         uint32_t gb = 0u;
@@ -151,7 +139,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __re
 __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, const uint32_t* __restrict__ gmax,
                                                    uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
                                                    uint32_t* __restrict__ gfx_io, const DevScalars* sc,
-                                                   FilterConst fc, int par)
+                                                   FilterConst fc, int par, uint64_t* __restrict__ gsc)
 {
     PDL_ENTER();
     __shared__ uint16_t s_first[kSortTile + 1];
@@ -168,16 +156,19 @@ __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, cons
     uint32_t j = run_of(s_first, nd, p0);
     uint32_t end = s_first[j + 1];
     uint32_t key = tp.key[base + j];
-    float pa = key < fc.C ? din.pA[key] : 0.0f;
+    float pa = din_pa(din, key, fc.C);
     float gm = pa > 0.0f ? __uint_as_float(gmax[key]) : 0.0f;
     uint64_t acc = 0;
     for (uint32_t p = p0; p < p1; ++p) {
         if (p >= end) {
-            if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+            if (acc) {
+                atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+                if (gsc) atomicAdd((unsigned long long*)&gsc[key], (unsigned long long)acc);
+            }
             acc = 0;
             ++j; end = s_first[j + 1];
             key = tp.key[base + j];
-            pa = key < fc.C ? din.pA[key] : 0.0f;
+            pa = din_pa(din, key, fc.C);
             if (pa > 0.0f) gm = __uint_as_float(gmax[key]);
         }
         uint32_t gf = 0u;
@@ -187,7 +178,10 @@ __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, cons
         }
         gfx_io[base + p] = gf;                               // per sorted position, for k_resample_dopp
     }
-    if (acc) atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+    if (acc) {
+        atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+        if (gsc) atomicAdd((unsigned long long*)&gsc[key], (unsigned long long)acc);
+    }
 }
 
 // ---- k_resample_dopp: persistent members with per-member weights ---------------------------------------

@@ -564,8 +564,18 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
 // exact filter spreads nu_b over the whole grid, so k_births' per-cell work items would leave most lanes
 // idle).  Slot s belongs to the last list entry with sb <= s; same draws, state and joint CDF as
 // k_births (no Doppler split); copies written by the slot's own thread.
+// The exact filter with a likelihood (A-38): in a cell where a measurement occurred and p_A > 0, the
+// first nu_A = floor(pi nb + 1/2) slots draw the radial velocity from the posterior given z; the weights
+// stay the single even split of R_b (the associated set's part of it is R_bA).  pA == nullptr: off.
+struct BirthLik {
+    const float* pA;
+    const float4* obs;
+    const float4* lik;
+    const float* pic;
+};
+
 __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out, BirthDebug bdbg,
-                                                      const DevScalars* sc, FilterConst fc, int64_t k)
+                                                      const DevScalars* sc, FilterConst fc, int64_t k, BirthLik bl)
 {
     PDL_ENTER();
     const RsConst rc = make_rsconst(sc, fc.nu, fc.force_exact != 0);
@@ -596,6 +606,19 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
         float n0, n1;
         box_muller(d.r2, d.r3, n0, n1);
         float bvx = __fmul_rn(fc.sigma_b, n0), bvy = __fmul_rn(fc.sigma_b, n1);
+        if (bl.pA && bl.obs[c].x > 0.0f && bl.pA[c] > 0.0f) {
+            uint32_t nA = (uint32_t)floor(__dadd_rn(__dmul_rn((double)bl.pic[c], (double)nb), 0.5));
+            if (r < min(nA, nb)) {                                  // posterior radial velocity given z (A-38)
+                const float4 z = bl.lik[c];
+                const float sb2 = __fmul_rn(fc.sigma_b, fc.sigma_b), sd2 = __fmul_rn(z.w, z.w);
+                const float mu_r = __fdiv_rn(__fmul_rn(z.z, sb2), __fadd_rn(sb2, sd2));
+                const float s_r = __fdiv_rn(__fmul_rn(fc.sigma_b, z.w), __fsqrt_rn(__fadd_rn(sb2, sd2)));
+                const float sr = __fmaf_rn(s_r, n0, mu_r);
+                const float st = __fmul_rn(fc.sigma_b, n1);
+                bvx = __fmaf_rn(sr, z.x, -__fmul_rn(st, z.y));
+                bvy = __fmaf_rn(sr, z.y, __fmul_rn(st, z.x));
+            }
+        }
         if (fc.v_max > 0.0f) {
             bvx = fminf(fmaxf(bvx, -fc.v_max), fc.v_max);
             bvy = fminf(fmaxf(bvy, -fc.v_max), fc.v_max);

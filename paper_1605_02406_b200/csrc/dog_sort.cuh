@@ -681,8 +681,9 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             dop_single(li, pl[0]);
             return;
         }
-        // kBatch (exact filter, no Doppler): 2..kPsSmall runs sorted by one lane in registers (a
-        // 4-element sorting network; entries are distinct), then the exclusive prefix of their counts
+        // kBatch (exact filter): 2..kPsSmall runs sorted by one lane in registers (a 4-element sorting
+        // network; entries are distinct), then the exclusive prefix of their counts (and, likelihood
+        // cells of the exact filter with a likelihood, of the runs' likelihood sums)
         uint32_t v[kPsSmall];
 #pragma unroll
         for (int q = 0; q < kPsSmall; ++q) v[q] = (uint32_t)q < m ? pl[q] : 0xFFFFFFFFu;
@@ -690,6 +691,8 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         cs(v[0], v[1]); cs(v[2], v[3]); cs(v[0], v[2]); cs(v[1], v[3]); cs(v[1], v[2]);
         RunInfo r2 = run_info(li);
         uint32_t carry = 0;
+        const bool dcell = dp.pA && dp.pA[L.c[li]] > 0.0f;
+        uint64_t gcarry = 0;
 #pragma unroll
         for (int q = 0; q < kPsSmall; ++q) {
             if ((uint32_t)q < m) {
@@ -697,7 +700,19 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
                 tp.run[v[q]] = r2;
                 pl[q] = v[q];                                 // the cell's list, now in tile order
                 carry += (uint32_t)tp.cnt[v[q]] + 1u;
+                if (dcell) {
+                    const uint64_t g = dp.rg[v[q]];
+                    dp.rg[v[q]] = gcarry;
+                    gcarry += g;
+                }
             }
+        }
+        if (dp.pA) {
+            dp.GS[li] = gcarry;
+            if (gcarry)
+#pragma unroll
+                for (int q = 0; q < kPsSmall; ++q)
+                    if ((uint32_t)q < m) dp.tflag[v[q] >> 12] = 1;
         }
     };
     for_run_entries<kBatch, kPsGroup, kBatch ? kPsSmall : 1>(L.np, Lc, [&](uint32_t li, uint32_t m) {

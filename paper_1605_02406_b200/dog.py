@@ -63,6 +63,7 @@ _SIGS = {
     "dog_step": ([_vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_doppler": ([_vp, _vp, _vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_exact": ([_vp, _vp, C.c_float, _vp], C.c_int),
+    "dog_step_exact_lik": ([_vp, _vp, _vp, _vp, C.c_float, _vp], C.c_int),
     "dog_step_host": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_step_host_async": ([_vp, _vp, C.c_float, _vp, _vp], C.c_int),
     "dog_step_host_readout": ([_vp, _vp, C.c_float, _vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -233,6 +234,14 @@ class Filter:
         """include/dog.h dog_step_exact (NEXT-3): obs [C, 4] = (occurred, p_TP, p_FP, 0) on the device."""
         assert obs.is_cuda and obs.dtype == torch.float32 and obs.is_contiguous() and obs.numel() == 4 * self.C
         _check(dog_step_exact(self._h, obs.data_ptr(), dt, _stream_ptr(stream)), "dog_step_exact")
+
+    def step_exact_lik(self, obs: torch.Tensor, lik: torch.Tensor, p_assoc: torch.Tensor, dt: float, stream=None):
+        """include/dog.h dog_step_exact_lik (NEXT-3 with a likelihood, A-38): obs [C, 4] = (occurred, p_TP, p_FP,
+        p_cl), lik [C, 4] = (u_x, u_y, v_r, sd), p_assoc [C], all on the device."""
+        for t, n in ((obs, 4), (lik, 4), (p_assoc, 1)):
+            assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.numel() == n * self.C
+        _check(dog_step_exact_lik(self._h, obs.data_ptr(), lik.data_ptr(), p_assoc.data_ptr(), dt,
+                                  _stream_ptr(stream)), "dog_step_exact_lik")
 
     def step_doppler(self, meas: torch.Tensor, doppler: torch.Tensor, p_assoc: torch.Tensor, dt: float, stream=None):
         """include/dog.h dog_step_doppler (NEXT-1): doppler [C, 4] = (u_x, u_y, v_r, sd), p_assoc [C]."""

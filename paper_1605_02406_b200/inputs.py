@@ -296,6 +296,18 @@ class Scene:
         out[..., 2] = torch.where(hit, pfp_hit, torch.where(seen, torch.full_like(mO, 0.01), torch.full_like(mO, 0.05)))
         return out.contiguous()
 
+    def exact_lik(self, k: int, meas: torch.Tensor, p_cl: float = 0.02, frac: float = 0.5, p_assoc: float = 0.8,
+                  sd: float = 0.25):
+        """Inputs of the exact filter with a single-object likelihood (NEXT-3 general form; A-38
+        input recipe): the observation grid of exact_obs with the clutter density p_cl in its 4th column --
+        a clutter return's radial speed uniform over +-25 m/s, 0.02 per m/s -- and the Doppler overlay of
+        `doppler` (same seeded fraction of the cells with a return) as the measurement's likelihood.
+        Returns (obs [H, W, 4], lik [H, W, 4] = (u_x, u_y, v_r, sd), p_A [H, W]), f32 on the CPU."""
+        obs = Scene.exact_obs(meas.detach().cpu())
+        obs[..., 3] = p_cl
+        lik, pA = self.doppler(k, meas, frac=frac, p_assoc=p_assoc, sd=sd)
+        return obs.contiguous(), lik, pA
+
     def frames(self, k0: int, n: int, device="cpu") -> torch.Tensor:
         return torch.stack([self.frame(k0 + i, device) for i in range(n)])
 

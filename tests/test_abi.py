@@ -76,6 +76,7 @@ def test_argument_validation_without_device(lib):
     assert dog.dog_step(None, None, 0.1, None) == dog.DOG_E_INVAL
     assert dog.dog_step_doppler(None, None, None, None, 0.1, None) == dog.DOG_E_INVAL
     assert dog.dog_step_exact(None, None, 0.1, None) == dog.DOG_E_INVAL
+    assert dog.dog_step_exact_lik(None, None, None, None, 0.1, None) == dog.DOG_E_INVAL
     assert dog.dog_band_set_state(None, None, 0, 0, None, 0.0, 0) == dog.DOG_E_INVAL
     assert dog.dog_check_transforms(None) == dog.DOG_E_INVAL
     assert dog.dog_eval_cells(None, None, None, None, 0, None, None, None, 0, None, None, None, None) == dog.DOG_E_INVAL
