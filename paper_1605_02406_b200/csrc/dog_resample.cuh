@@ -31,12 +31,12 @@ __device__ __forceinline__ void finalize_cell(uint32_t c, double s0, double s1, 
     const float S = __double2float_rn(__dmul_rn((double)n, (double)w_pred));
     if (!(rp > 0.0f) || !(S > 0.0f)) return;
     const float w = __fmul_rn(__fdiv_rn(rp, S), w_pred);       // Eq. 71 with p_A = 0, Eq. 73
-    const double wd = (double)w, rd = (double)rp;
-    const double mx = wd * s0 / rd, my = wd * s1 / rd;
+    const double f = (double)w / (double)rp;                   // one fp64 division per cell
+    const double mx = s0 * f, my = s1 * f;
     mean[c] = make_float2((float)mx, (float)my);
-    cov[3 * (size_t)c] = (float)(wd * s2 / rd - mx * mx);
-    cov[3 * (size_t)c + 1] = (float)(wd * s3 / rd - my * my);
-    cov[3 * (size_t)c + 2] = (float)(wd * s4 / rd - mx * my);
+    cov[3 * (size_t)c] = (float)(s2 * f - mx * mx);
+    cov[3 * (size_t)c + 1] = (float)(s3 * f - my * my);
+    cov[3 * (size_t)c + 2] = (float)(s4 * f - mx * my);
 }
 
 // Moments of a Doppler cell (NEXT-1, A-35): sums weighted by the members' fixed-point weights q_j,
@@ -49,12 +49,12 @@ __device__ __forceinline__ void finalize_cell_dop(uint32_t c, double s0, double 
         cov[3 * (size_t)c] = 0.0f; cov[3 * (size_t)c + 1] = 0.0f; cov[3 * (size_t)c + 2] = 0.0f;
         return;
     }
-    const double rd = (double)Rp;
-    const double mx = s0 / rd, my = s1 / rd;
+    const double f = 1.0 / (double)Rp;
+    const double mx = s0 * f, my = s1 * f;
     mean[c] = make_float2((float)mx, (float)my);
-    cov[3 * (size_t)c] = (float)(s2 / rd - mx * mx);
-    cov[3 * (size_t)c + 1] = (float)(s3 / rd - my * my);
-    cov[3 * (size_t)c + 2] = (float)(s4 / rd - mx * my);
+    cov[3 * (size_t)c] = (float)(s2 * f - mx * mx);
+    cov[3 * (size_t)c + 1] = (float)(s3 * f - my * my);
+    cov[3 * (size_t)c + 2] = (float)(s4 * f - mx * my);
 }
 
 struct NextState { float4* s; uint32_t* jidx; };   // (x, y, vx, vy) per particle; joint index (debug)
@@ -123,8 +123,6 @@ static_assert(kRtItems % 8 == 0, "16-byte vector loads of the tile arrays");
 constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
 
 constexpr int kRtRunCache = 256;                                      // runs whose RunF sits in smem
-constexpr uint32_t kMoDirect = 32;   // long-list (run-heavy) cycles: cells with at most this many particles are
-                                     // summed directly by k_moments<true> (resample skips their run sums)
 
 // Per run, what the copy pass needs to place member r = pre + k (k = position - first): F(Q_r) =
 // ceil(y(r)) with y(r) = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
@@ -138,6 +136,7 @@ static_assert(sizeof(RunF) == 32, "RunF: two per 64-byte line");
 struct RtSmem {   // dynamic shared memory of k_resample_tiles (~8.6 KB)
     RunF rf[kRtRunCache];
     uint32_t starts[kSortTile / 32];   // bitmap of run starts over the tile's sorted positions
+    uint32_t dir[kSortTile / 32];      // bitmap over the tile's runs: RunInfo::direct (no run sums needed)
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
@@ -245,14 +244,15 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint32_t nd = tp.nd[t];
     const RunInfo* __restrict__ runs = tp.run + base;
     // ---- run starts (bitmap) and the runs' F parameters
-    for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) S.starts[w] = 0u;
+    for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) { S.starts[w] = 0u; S.dir[w] = 0u; }
     if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     __syncthreads();
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
         const uint32_t f = tp.first[base + r];
         atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
-        if (rc.W && r < (uint32_t)kRtRunCache) {
+        if (r < (uint32_t)kRtRunCache) {
             const RunInfo q = runs[r];
+            if (q.direct) atomicOr(&S.dir[r >> 5], 1u << (r & 31u));
             RunF x;
             x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
             x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
@@ -298,13 +298,14 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
                 if (amb) F0 = fcount(member_Q(runs[j], mr), rc);   // rare: exact products
             } else {
                 qf = runs[j];
+                if (qf.direct) atomicOr(&S.dir[j >> 5], 1u << (j & 31u));
                 mr = qf.pre + (p - tp.first[base + j]);
                 F0 = fcount(member_Q(qf, mr), rc);
             }
             if (kDbg) {
                 const RunInfo q = runs[j];
-                Jd = q.jbase + mr;
-                perm_dbg[q.jbase - L.sb[q.li] + mr] = pbase + lperm[base + p];
+                Jd = L.start[q.li] + L.sb[q.li] + mr;
+                perm_dbg[L.start[q.li] + mr] = pbase + lperm[base + p];
             }
         }
         const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);
@@ -333,45 +334,53 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         write_compact<kDbg>(c, F0, make_float4(XY.x, XY.y, V.x, V.y), Jd, out, fc.nu);
     }
     // ---- velocity sums per run (Eqs. 81-84; k_moments combines a cell's runs in tile order), from the
-    //      sorted predicted velocities just read (L1 / L2): runs of >= 16 members by a warp each (lanes
-    //      strided, fixed butterfly), shorter runs by one lane each in member order -- deterministic
-    const uint32_t nw = kRtThreads / 32;
-    auto small_cell = [&](uint32_t r) { return mo_direct && L.n[runs[r].li] <= mo_direct; };   // k_moments sums those
-    for (uint32_t r = warp; r < nd; r += nw) {            // long runs: warp per run
-        if (r == srun) continue;
-        const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
-        if (e - f < 16u || small_cell(r)) continue;
-        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (uint32_t q = f + lane; q < e; q += 32) {
-            const float2 V = pv[pbase + q];
-            const double a = (double)V.x, b = (double)V.y;
-            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
+    //      sorted predicted velocities just read (L1 / L2).  Each warp takes 32 consecutive runs, one per
+    //      lane: runs shorter than 16 members are summed by their lane in member order; longer ones are
+    //      collected (ballot) and summed by the whole warp (lanes strided, fixed butterfly) -- deterministic.
+    //      Runs of cells k_moments sums directly (at most mo_direct members) are skipped.
+    __syncthreads();                                        // S.dir complete (every run has a member here)
+    for (uint32_t r0 = (uint32_t)warp * 32u; r0 < nd; r0 += kRtThreads) {
+        const uint32_t r = r0 + lane;
+        const bool need = r < nd && r != srun && !(mo_direct && ((S.dir[r >> 5] >> (r & 31u)) & 1u));
+        uint32_t f = 0, e = 0;
+        if (need) {
+            f = tp.first[base + r];
+            e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
         }
-#pragma unroll
-        for (int d = 16; d; d >>= 1)
-#pragma unroll
-            for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], d);
-        if (lane == 0) {
+        if (need && e - f < 16u) {
+            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (uint32_t q = f; q < e; ++q) {
+                const float2 V = pv[pbase + q];
+                const double a = (double)V.x, b = (double)V.y;
+                s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
+            }
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
             ppart[base + r] = mp;
         }
-    }
-    for (uint32_t r = tid; r < nd; r += kRtThreads) {     // short runs: lane per run
-        if (r == srun) continue;
-        const uint32_t f = tp.first[base + r], e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
-        if (e - f >= 16u || small_cell(r)) continue;
-        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (uint32_t q = f; q < e; ++q) {
-            const float2 V = pv[pbase + q];
-            const double a = (double)V.x, b = (double)V.y;
-            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
-        }
-        MomPartial mp;
+        uint32_t lm = __ballot_sync(0xffffffffu, need && e - f >= 16u);
+        while (lm) {
+            const int src = __ffs(lm) - 1;
+            lm &= lm - 1u;
+            const uint32_t fr = __shfl_sync(0xffffffffu, f, src), er = __shfl_sync(0xffffffffu, e, src);
+            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+            for (uint32_t q = fr + lane; q < er; q += 32) {
+                const float2 V = pv[pbase + q];
+                const double a = (double)V.x, b = (double)V.y;
+                s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
+            }
 #pragma unroll
-        for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
-        ppart[base + r] = mp;
+            for (int dd = 16; dd; dd >>= 1)
+#pragma unroll
+                for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], dd);
+            if (lane == 0) {
+                MomPartial mp;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+                ppart[base + r0 + (uint32_t)src] = mp;
+            }
+        }
     }
 }
 
@@ -584,8 +593,15 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
     const uint64_t Ppre = scrd(sc->Ppre);
     const uint32_t Lc = scrd(sc->Lc);
     const uint32_t ns = (uint32_t)scrd(sc->s_total);
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
-        uint32_t lo = 0, hi = Lc;                                   // last entry with sb <= s
+    const uint32_t lane = threadIdx.x & 31u;
+    for (uint32_t s0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); s0 < ns; s0 += gridDim.x * blockDim.x) {
+        // last entry with sb <= s: the warp brackets its 32 slots with two 32-ary searches, then each lane
+        // bisects the (short) bracket
+        const uint32_t s = s0 + lane;
+        const uint32_t l0 = warp_last_le(0u, Lc, s0, [&](uint32_t i) { return L.sb[i]; });
+        const uint32_t l1 = warp_last_le(l0, Lc, min(s0 + 31u, ns - 1u), [&](uint32_t i) { return L.sb[i]; });
+        if (s >= ns) continue;
+        uint32_t lo = l0, hi = l1 + 1u;
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (L.sb[m] <= s) lo = m; else hi = m; }
         const uint32_t li = lo;
         const uint32_t c = L.c[li], nb = L.nb[li], sb = L.sb[li];

@@ -26,13 +26,16 @@
 
 namespace dog {
 
+constexpr uint32_t kMoDirect = 32;   // long-list (run-heavy) cycles: cells with at most this many particles are
+                                     // summed directly by k_moments<true> (resample skips their run sums)
+
 // What k_resample_tiles needs of a run (written by k_pair_sort, one coalesced 32-byte load per run).
 struct RunInfo {
     uint64_t P;             // joint-CDF prefix of the run's cell (A-25)
     uint64_t bp;            // R_p / n_c of the cell (even split, A-23)
     uint32_t rpm;           // R_p mod n_c
     uint32_t pre;           // rank of the run's first particle among the cell's particles
-    uint32_t jbase;         // joint index of the cell's first member (debug)
+    uint32_t direct;        // 1: k_moments<true> sums the cell's velocities itself (at most kMoDirect members)
     uint32_t li;            // the cell's active-list entry
 };
 
@@ -658,7 +661,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         ri.bp = L.bp[li];
         ri.rpm = L.rp[li];
         ri.pre = 0u;
-        ri.jbase = L.start[li] + L.sb[li];
+        ri.direct = kBatch && L.n[li] <= kMoDirect ? 1u : 0u;
         ri.li = li;
         return ri;
     };

@@ -22,7 +22,12 @@ for k in range(settle, settle + n):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    last = k == settle + n - 1
+    if last:
+        torch.cuda.nvtx.range_push("capture")   # ncu --nvtx --nvtx-include "capture/": the last cycle only
     f.step_exact(obs, cfg.dt)
+    if last:
+        torch.cuda.nvtx.range_pop()
     e1.record()
     torch.cuda.synchronize()
     ms.append(round(e0.elapsed_time(e1), 3))
