@@ -133,10 +133,12 @@ struct RunF {
 };
 static_assert(sizeof(RunF) == 32, "RunF: two per 64-byte line");
 
-struct RtSmem {   // dynamic shared memory of k_resample_tiles (~8.6 KB)
+struct RtSmem {   // dynamic shared memory of k_resample_tiles (~9.7 KB)
     RunF rf[kRtRunCache];
     uint32_t starts[kSortTile / 32];   // bitmap of run starts over the tile's sorted positions
     uint32_t dir[kSortTile / 32];      // bitmap over the tile's runs: RunInfo::direct (no run sums needed)
+    uint16_t long_run[kSortTile / 16]; // runs of >= 16 members (summed warp-wide)
+    uint32_t n_long;
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
 };
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
@@ -334,53 +336,73 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         write_compact<kDbg>(c, F0, make_float4(XY.x, XY.y, V.x, V.y), Jd, out, fc.nu);
     }
     // ---- velocity sums per run (Eqs. 81-84; k_moments combines a cell's runs in tile order), from the
-    //      sorted predicted velocities just read (L1 / L2).  Each warp takes 32 consecutive runs, one per
-    //      lane: runs shorter than 16 members are summed by their lane in member order; longer ones are
-    //      collected (ballot) and summed by the whole warp (lanes strided, fixed butterfly) -- deterministic.
-    //      Runs of cells k_moments sums directly (at most mo_direct members) are skipped.
-    __syncthreads();                                        // S.dir complete (every run has a member here)
-    for (uint32_t r0 = (uint32_t)warp * 32u; r0 < nd; r0 += kRtThreads) {
-        const uint32_t r = r0 + lane;
-        const bool need = r < nd && r != srun && !(mo_direct && ((S.dir[r >> 5] >> (r & 31u)) & 1u));
-        uint32_t f = 0, e = 0;
-        if (need) {
-            f = tp.first[base + r];
-            e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
+    //      sorted predicted velocities just read (L1 / L2): runs of >= 16 members by a warp each (lanes
+    //      strided, fixed butterfly), shorter runs by one thread each in member order -- deterministic.
+    auto run_bounds = [&](uint32_t r, uint32_t& f, uint32_t& e) {
+        f = tp.first[base + r];
+        e = r + 1 < nd ? (uint32_t)tp.first[base + r + 1] : n;
+    };
+    auto warp_run = [&](uint32_t r, uint32_t f, uint32_t e) {
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (uint32_t q = f + lane; q < e; q += 32) {
+            const float2 V = pv[pbase + q];
+            const double a = (double)V.x, b = (double)V.y;
+            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
         }
-        if (need && e - f < 16u) {
-            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (uint32_t q = f; q < e; ++q) {
-                const float2 V = pv[pbase + q];
-                const double a = (double)V.x, b = (double)V.y;
-                s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
-            }
+#pragma unroll
+        for (int dd = 16; dd; dd >>= 1)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], dd);
+        if (lane == 0) {
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
             ppart[base + r] = mp;
         }
-        uint32_t lm = __ballot_sync(0xffffffffu, need && e - f >= 16u);
-        while (lm) {
-            const int src = __ffs(lm) - 1;
-            lm &= lm - 1u;
-            const uint32_t fr = __shfl_sync(0xffffffffu, f, src), er = __shfl_sync(0xffffffffu, e, src);
-            double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-            for (uint32_t q = fr + lane; q < er; q += 32) {
-                const float2 V = pv[pbase + q];
-                const double a = (double)V.x, b = (double)V.y;
-                s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
-            }
-#pragma unroll
-            for (int dd = 16; dd; dd >>= 1)
-#pragma unroll
-                for (int i = 0; i < 5; ++i) s5[i] += __shfl_xor_sync(0xffffffffu, s5[i], dd);
-            if (lane == 0) {
-                MomPartial mp;
-#pragma unroll
-                for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
-                ppart[base + r0 + (uint32_t)src] = mp;
-            }
+    };
+    auto thread_run = [&](uint32_t r, uint32_t f, uint32_t e) {
+        double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (uint32_t q = f; q < e; ++q) {
+            const float2 V = pv[pbase + q];
+            const double a = (double)V.x, b = (double)V.y;
+            s5[0] += a; s5[1] += b; s5[2] += a * a; s5[3] += b * b; s5[4] += a * b;
         }
+        MomPartial mp;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) mp.s[i] = s5[i];
+        ppart[base + r] = mp;
+    };
+    constexpr uint32_t nw = kRtThreads / 32;
+    if (!mo_direct) {   // few, long runs: warps walk the runs directly (no barrier)
+        for (uint32_t r = warp; r < nd; r += nw) {
+            uint32_t f, e;
+            run_bounds(r, f, e);
+            if (r != srun && e - f >= 16u) warp_run(r, f, e);
+        }
+        for (uint32_t r = tid; r < nd; r += kRtThreads) {
+            uint32_t f, e;
+            run_bounds(r, f, e);
+            if (r != srun && e - f < 16u) thread_run(r, f, e);
+        }
+        return;
+    }
+    // long-list cycles (thousands of short runs per tile): thread per run; the runs of cells k_moments sums
+    // directly (RunInfo::direct) are skipped, the (at most 256) long ones listed, then summed warp-wide
+    if (tid == 0) S.n_long = 0u;
+    __syncthreads();                                        // S.dir complete (every run has a member here)
+    for (uint32_t r = tid; r < nd; r += kRtThreads) {
+        if (r == srun || ((S.dir[r >> 5] >> (r & 31u)) & 1u)) continue;
+        uint32_t f, e;
+        run_bounds(r, f, e);
+        if (e - f >= 16u) S.long_run[atomicAdd(&S.n_long, 1u)] = (uint16_t)r;
+        else thread_run(r, f, e);
+    }
+    __syncthreads();
+    for (uint32_t w = (uint32_t)warp; w < S.n_long; w += nw) {
+        const uint32_t r = S.long_run[w];
+        uint32_t f, e;
+        run_bounds(r, f, e);
+        warp_run(r, f, e);
     }
 }
 

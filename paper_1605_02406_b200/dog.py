@@ -97,6 +97,8 @@ _SIGS = {
 }
 DOG_MAX_STAGES = 16
 for _name, (_args, _res) in _SIGS.items():
+    if os.environ.get("DOG_LIB") and not hasattr(_lib, _name):   # A/B against an older build (tools/ab.sh)
+        continue
     _f = getattr(_lib, _name)
     _f.argtypes = _args
     _f.restype = _res

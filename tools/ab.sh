@@ -6,7 +6,7 @@ python -m paper_1605_02406_b200.build > /dev/null 2>&1 || echo build_B_failed
 for r in 1 2; do
   for v in A B; do
     if [ $v = A ]; then L=$PWD/paper_1605_02406_b200/csrc_ab/libdog.so; E="${AB_ENV_A:-}"; else L=$PWD/paper_1605_02406_b200/libdog.so; E="${AB_ENV_B:-}"; fi
-    env $E DOG_LIB=$L python bench.py --steps 20 --warmup 5 --cpu-baseline-steps 0 --e2e-steps 0 2>/dev/null | tail -1 | \
+    env $E DOG_LIB=$L python bench.py --steps 20 --warmup 5 --cpu-baseline-steps 0 --e2e-steps 0 --config-lines '' 2>/dev/null | tail -1 | \
       python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), {k: round(v*1000,1) for k,v in d['stages_ms'].items()})"
   done
 done
