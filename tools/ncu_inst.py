@@ -9,8 +9,11 @@ def main(path, kernel, top=30):
     out = subprocess.run(['ncu', '-i', path, '--page', 'source', '--csv', '-k', f'regex:{kernel}',
                           '--print-source', 'cuda,sass'], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, lines = None, []
+    hdr, lines, fname, per_file = None, [], "?", {}
     for r in rows:
+        if len(r) == 2 and r[0] in ('File Name', 'File Path'):
+            fname = r[1].split('/')[-1]
+            continue
         if r and r[0] == 'Line No':
             hdr = r
             continue
@@ -18,9 +21,10 @@ def main(path, kernel, top=30):
             continue
         ei = hdr.index('Instructions Executed')
         e = int(r[ei]) if r[ei].isdigit() else 0
-        lines.append((e, int(r[0]), r[1].strip()[:110]))
+        lines.append((e, int(r[0]), fname + ': ' + r[1].strip()[:100]))
+        per_file[fname] = per_file.get(fname, 0) + e
     tot = sum(x[0] for x in lines) or 1
-    print(f'total instructions {tot}')
+    print(f'total instructions {tot}; per file:', {k: f'{100 * v / tot:.1f}%' for k, v in per_file.items()})
     for e, ln, src in sorted(lines, reverse=True)[:top]:
         print(f'{100 * e / tot:5.1f}% {e:9d} {ln}: {src}')
 
