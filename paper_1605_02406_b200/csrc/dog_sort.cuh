@@ -148,23 +148,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
             const uint32_t g = base + p;
             float4 P;
             if (kPredict) {
-#ifdef DOG_DIAG_NORNG   // diagnostics: the draws replaced by a 16-byte load from elsewhere (cost model only)
-                {
-                    const float4 X = st[g], R = st[(g + 3000000u) % (fc.lo_cap + n_loc)];
-                    float nn[4];
-                    uint32_t h = (g + 0x9E3779B9u * (uint32_t)a.k) * 0x85EBCA6Bu;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {   // ~N(0,1): sum of four 8-bit uniforms, + 0 x the load
-                        h = h * 0xC2B2AE35u + 0x27D4EB2Fu;
-                        const float s = (float)(h & 255u) + (float)((h >> 8) & 255u) + (float)((h >> 16) & 255u) + (float)(h >> 24);
-                        nn[q] = __fmaf_rn(s, 0.0135f, -3.44f) + 0.0f * (&R.x)[q];
-                    }
-                    P = make_float4(__fmaf_rn(a.s_p, nn[0], __fmaf_rn(X.z, a.Tc, X.x)), __fmaf_rn(a.s_p, nn[1], __fmaf_rn(X.w, a.Tc, X.y)),
-                                    __fmaf_rn(a.s_v, nn[2], X.z), __fmaf_rn(a.s_v, nn[3], X.w));
-                }
-#else
                 P = predict_one(st[g], o_base + (g - fc.lo_cap), fc, a);
-#endif
                 pxy[g] = make_float2(P.x, P.y);
                 pv[g] = make_float2(P.z, P.w);
                 if (pst) pst[g] = P;                        // debug: the predicted state in input order
