@@ -35,7 +35,7 @@ extern "C" {
 #endif
 
 #define DOG_OK        0
-#define DOG_E_INVAL  (-1) /* invalid argument: sizes <= 0, C >= 2^24, probabilities out of range,
+#define DOG_E_INVAL  (-1) /* invalid argument: sizes <= 0, C >= 2^31-1, probabilities out of range,
                              non-positive dt, NaN parameters, null pointers                        */
 #define DOG_E_NOMEM  (-2) /* device or pinned-host allocation failed                             */
 #define DOG_E_CUDA   (-3) /* a CUDA call failed; the context is poisoned (only dog_destroy)     */
@@ -49,8 +49,12 @@ extern "C" {
 typedef struct dog_ctx dog_ctx;   /* opaque; created and owned by the library */
 
 typedef struct {
-    int32_t width, height;        /* cells; C = width*height, 1 <= C < 2^24 (see dog_create)   */
+    int32_t width, height;        /* cells; C = width*height, 1 <= C < 2^31-1 (see dog_create) */
     float   cell_size;            /* metres per cell, > 0 (Table I: 0.1 m)             */
+    float   origin_x, origin_y;   /* world metres of the lower-left corner of cell (0, 0): the
+                                     map between world and cell coordinates x = (X - origin_x) /
+                                     cell_size; bookkeeping only (no kernel reads it), moved by
+                                     dog_ego_scroll, read back with dog_get_origin               */
 } dog_grid;
 
 typedef struct {
@@ -66,8 +70,10 @@ typedef struct {
 
 /* dog_create -- allocate a filter in the empty initial state (A-19): all nu particles at the sentinel
  * position (-2^30 cells) with weight 0, m_F = 0, k = 0.
- *   grid, params : validated copies are kept (DOG_E_INVAL on violation; width, height <= 65535 and
- *                  width * height < 2^24, which keeps every fixed-point total below 2^64, A-23).
+ *   grid, params : validated copies are kept (DOG_E_INVAL on violation; width, height <= 65535 (16-bit
+ *                  rows / columns in the sort keys), width * height < 2^31 - 1 (u32 cell keys); the
+ *                  masses' fixed point has 40 fractional bits below 2^24 cells and 63 - bitlen(C)
+ *                  beyond, so every total stays below 2^64, A-23).
  *   n_particles  : nu, 1 <= nu < 2^30, persistent particles per cycle.
  *   n_birth      : nu_b, 0 <= nu_b < 2^30, new-born particles per cycle ("remains constant").
  *   seed         : Philox key (low 32 bits, high 32 bits).
@@ -235,6 +241,10 @@ int dog_band_set_state(dog_ctx* ctx, const float* xyvv_host, uint32_t n_own, uin
  * readouts of the last cycle are not moved (they describe the cycle that produced them). */
 int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t* shift_y, void* stream);
 int dog_ego_residual(dog_ctx* ctx, double* rx, double* ry);
+/* dog_get_origin -- world metres of the lower-left corner of cell (0, 0) now: dog_grid's origin moved by
+ * every applied ego shift (content moves by +shift cells, so the grid moves by -shift cell_size in the
+ * world; fp64).  For band contexts the grid origin of the creating call (bands do not scroll). */
+int dog_get_origin(dog_ctx* ctx, double* origin_x, double* origin_y);
 
 /* ---- evaluation workload (PAPER section VIII, Eqs. 85-88) ----
  * dog_eval_cells -- per cell c of the context: the Mahalanobis distance m = v P^-1 v^T of the velocity

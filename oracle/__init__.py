@@ -79,6 +79,7 @@ def _declare(L):
     L.orc_dempster.argtypes = [C.c_float] * 4 + [f32p, f32p]
     L.orc_birth_split.argtypes = [C.c_float] * 3 + [f32p, f32p]
     L.orc_birth_slots.argtypes = [u64p, C.c_int64, C.c_int64, u32p]; L.orc_birth_slots.restype = C.c_uint64
+    L.orc_fx_bits.argtypes = [C.c_int64]; L.orc_fx_bits.restype = C.c_int
     L.orc_systematic_resample.argtypes = [u64p, C.c_int64, C.c_int64, C.c_uint32, u32p]
     L.orc_systematic_resample.restype = C.c_uint64
     L.orc_step_scalars.argtypes = [_p(OrcParams), C.c_float, f32p]
@@ -158,6 +159,11 @@ def birth_split(m_p, m_O, p_b):
     rb, rp = C.c_float(), C.c_float()
     lib().orc_birth_split(m_p, m_O, p_b, C.byref(rb), C.byref(rp))
     return rb.value, rp.value
+
+
+def fx_bits(C_cells: int) -> int:
+    """Fixed-point exponent FX of the masses for a grid of C cells (A-23)."""
+    return int(lib().orc_fx_bits(int(C_cells)))
 
 
 def birth_slots(Rb, nu_b: int) -> np.ndarray:

@@ -219,11 +219,21 @@ void orc_birth_split(float m_p, float m_O, float p_b, float* rho_b, float* rho_p
     *rho_p = m_O - rb;
 }
 
-/* Fixed point fx(m) = floor(max(m,0) 2^40) (A-23): exact in fp64. */
-static uint64_t fx40(float m)
+/* Fixed-point exponent of the masses (A-23): 40 bits per unit of mass while C < 2^24; beyond, 63 minus
+ * the bit length of C, so that a total over all cells (each holding at most 1 + 2^-24 units of mass after
+ * rounding) stays below 2^64. */
+int orc_fx_bits(int64_t C)
+{
+    int bits = 0;                                  /* bit length of C */
+    while (bits < 62 && ((int64_t)1 << bits) <= C) ++bits;
+    return bits <= 24 ? 40 : 63 - bits;
+}
+
+/* Fixed point fx(m) = floor(max(m,0) 2^FX) (A-23): exact in fp64 (a power-of-two scale). */
+static uint64_t fxq(double scale, float m)
 {
     if (!(m > 0.0f)) return 0;
-    return (uint64_t)((double)m * 1099511627776.0);
+    return (uint64_t)((double)m * scale);
 }
 
 /* Birth slot allocation (Alg. 5 lines 2-3; A-14, A-15): cumulative nearest rounding
@@ -312,6 +322,7 @@ struct orc_ctx {
     float* pe;               /* [C] association weight of the members' split: p_A (NEXT-1) or
                                     the effective pAe of the exact filter with a likelihood (A-38) */
     float* pic;              /* [C] associated share of the births (A-38)                      */
+    double fx, fx_inv;       /* 2^FX and 2^-FX: fixed-point scale of the masses (orc_fx_bits)  */
     uint64_t scal[8];
     double res_x, res_y;     /* ego-motion residual, metres (NEXT-2) */
 };
@@ -332,6 +343,8 @@ int orc_create(const orc_params* p, orc_ctx** out)
     h->p = *p;
     int64_t C = (int64_t)p->width * p->height, nu = p->nu, nb = p->nu_b;
     h->C = C;
+    h->fx = ldexp(1.0, orc_fx_bits(C));
+    h->fx_inv = ldexp(1.0, -orc_fx_bits(C));
     h->x = xcalloc(nu, 4); h->y = xcalloc(nu, 4); h->vx = xcalloc(nu, 4); h->vy = xcalloc(nu, 4);
     for (int64_t i = 0; i < nu; ++i) { h->x[i] = SENTINEL_POS; h->y[i] = SENTINEL_POS; }
     h->m_free = xcalloc(C, 4);
@@ -596,8 +609,8 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
         }
         h->S[c] = S; h->mp[c] = fminf(S, P->occ_max); h->mfp[c] = 0.0f;
         h->occ[c] = rp + rb; h->fre[c] = 1.0f - (rp + rb); h->rho_p[c] = rp; h->rho_b[c] = rb;
-        h->Rp[c] = (b > a) ? fx40(rp) : 0;                     /* A-23 */
-        h->Rb[c] = fx40(rb);                                   /* births wherever r_b > 0 */
+        h->Rp[c] = (b > a) ? fxq(h->fx, rp) : 0;                     /* A-23 */
+        h->Rb[c] = fxq(h->fx, rb);                                   /* births wherever r_b > 0 */
     }
     for (int64_t c = 0; c < C && !obs; ++c) {
         uint32_t a = h->offsets[c], b = h->offsets[c + 1];
@@ -615,8 +628,8 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
         h->S[c] = S; h->mp[c] = m_p; h->mfp[c] = m_fp;
         h->occ[c] = mO; h->fre[c] = mF; h->rho_p[c] = rp; h->rho_b[c] = rb;
         h->m_free[c] = mF;                                     /* Alg. 3 store_values */
-        h->Rp[c] = (b > a) ? fx40(rp) : 0;                     /* A-23 */
-        h->Rb[c] = (zO > 0.0f) ? fx40(rb) : 0;                 /* P:1197 gate (A-13) */
+        h->Rp[c] = (b > a) ? fxq(h->fx, rp) : 0;                     /* A-23 */
+        h->Rb[c] = (zO > 0.0f) ? fxq(h->fx, rb) : 0;                 /* P:1197 gate (A-13) */
     }
 
     /* ---- O4 Persistent update (Alg. 4; Eqs. 69-73) and
@@ -644,12 +657,12 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
                 uint32_t i = h->perm[a + j];
                 gsj += h->gfx[i];
                 uint64_t Qn = orc_doppler_Q(Rp, h->pe[c], gsj, GS, j + 1, n);
-                double wd = (double)(Qn - Qj) * 0x1p-40, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
+                double wd = (double)(Qn - Qj) * h->fx_inv, vx = (double)h->pvx[i], vy = (double)h->pvy[i];
                 Mx += wd * vx; My += wd * vy;
                 Mxx += wd * vx * vx; Myy += wd * vy * vy; Mxy += wd * vx * vy;
                 Qj = Qn;
             }
-            rd = (double)Rp * 0x1p-40;
+            rd = (double)Rp * h->fx_inv;
         } else {
             for (uint32_t j = a; j < b; ++j) {
                 uint32_t i = h->perm[j];
@@ -783,7 +796,7 @@ static int step_impl(orc_ctx* h, const float* meas, const float* obs, const floa
                 h->x[i] = h->bx[b]; h->y[i] = h->by[b]; h->vx[i] = h->bvx[b]; h->vy[i] = h->bvy[b];
             }
         }
-        h->w_bar = (float)((double)Wt * 0x1p-40 / (double)nu);   /* Eq. 57 */
+        h->w_bar = (float)((double)Wt * h->fx_inv / (double)nu);   /* Eq. 57 */
     }
     free(q); free(src); free(count);
 

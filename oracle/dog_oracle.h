@@ -76,6 +76,8 @@ void  orc_dempster(float aO, float aF, float bO, float bF, float* mO, float* mF)
 void  orc_birth_split(float m_p, float m_O, float p_b, float* rho_b, float* rho_p);
 /* slots: Rb[C] (u64) -> nb[C] (u32); returns total A's low 64 bits */
 uint64_t orc_birth_slots(const uint64_t* Rb, int64_t C, int64_t nu_b, uint32_t* nb);
+/* fixed-point exponent FX of the masses for a grid of C cells (A-23): 40 while C < 2^24 */
+int orc_fx_bits(int64_t C);
 /* systematic resampling on a plain weight list q[n] (u64): idx[nu] (Alg. 7, A-24) */
 uint64_t orc_systematic_resample(const uint64_t* q, int64_t n, int64_t nu, uint32_t U, uint32_t* idx);
 void  orc_step_scalars(const orc_params* p, float dt, float out[4]); /* Tc, s_p, s_v, alpha */

@@ -86,6 +86,7 @@ struct dog_ctx {
     float* meas_dev = nullptr;
     // ego-motion compensation (dog_ego_scroll)
     double res_x = 0.0, res_y = 0.0;
+    double org_x = 0.0, org_y = 0.0;              // world metres of cell (0, 0)'s lower-left corner
     unsigned long long* ev_counts = nullptr;      // dog_eval_cells results
     EvalAcc* ev_acc = nullptr;                    // dog_eval_cells accumulator (self-resetting)
     double* ev_sums = nullptr;
@@ -248,6 +249,13 @@ FilterConst filter_const(const dog_ctx* ctx)
     f.v_max = ctx->params.v_max;
     f.seed = ctx->seed;
     f.force_exact = getenv("DOG_FORCE_EXACT_F") ? 1u : 0u;     // diagnostics / tests only
+    // fixed-point exponent of the masses (A-23): 40 while the GRID has fewer than 2^24 cells, else 63 minus
+    // the bit length of its cell count, so totals over every cell of every band stay below 2^64
+    int bits = 0;
+    while (bits < 62 && (1ll << bits) <= (int64_t)ctx->grid.width * ctx->grid.height) ++bits;
+    const int fxb = bits <= 24 ? 40 : 63 - bits;
+    f.fx = std::ldexp(1.0, fxb);
+    f.fx_inv = std::ldexp(1.0, -fxb);
     return f;
 }
 
@@ -305,9 +313,9 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     *out = nullptr;
     const dog_params& p = *params;
     const int64_t C = (int64_t)grid->width * grid->height;
-    if (grid->width <= 0 || grid->height <= 0 || C >= (1ll << 24) || !(grid->cell_size > 0.0f) ||
+    if (grid->width <= 0 || grid->height <= 0 || C >= (1ll << 31) - 1 || !(grid->cell_size > 0.0f) ||
         !finite(grid->cell_size) || grid->width > 65535 || grid->height > 65535)
-        return DOG_E_INVAL;   // C < 2^24 keeps every fixed-point total below 2^64 (A-23); 16-bit rows/cols
+        return DOG_E_INVAL;   // C < 2^31 - 1 (u32 cell keys, sentinel C); 16-bit rows/cols in the sort keys
     if (n_particles < 1 || n_particles >= (1ll << 30) || n_birth < 0 || n_birth >= (1ll << 30))
         return DOG_E_INVAL;
     if (!(p.p_s > 0.0f && p.p_s <= 1.0f) || !(p.p_b >= 0.0f && p.p_b < 1.0f) ||
@@ -326,6 +334,8 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     if (!ctx) return DOG_E_NOMEM;
     cudaGetDevice(&ctx->device);
     ctx->grid = *grid;
+    ctx->org_x = (double)grid->origin_x;
+    ctx->org_y = (double)grid->origin_y;
     ctx->params = p;
     ctx->seed = seed;
     ctx->flags = flags;
@@ -1254,6 +1264,8 @@ int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t
     const int32_t sx = (int32_t)qx, sy = (int32_t)qy;
     ctx->res_x = tx - qx * cs;
     ctx->res_y = ty - qy * cs;
+    ctx->org_x -= qx * cs;                                  // the grid moves by -shift in the world
+    ctx->org_y -= qy * cs;
     if (shift_x) *shift_x = sx;
     if (shift_y) *shift_y = sy;
     if (sx == 0 && sy == 0) return DOG_OK;
@@ -1262,6 +1274,14 @@ int dog_ego_scroll(dog_ctx* ctx, double dx, double dy, int32_t* shift_x, int32_t
                  sx, sy, W, H));
     CK(launch_ex(false, k_ego_particles, 8u * (uint32_t)sms, 256, 0, st, 0, ctx->st, (uint32_t)ctx->nu, sx, sy, W, H));
     std::swap(ctx->m_free, ctx->m_free_tmp);
+    return DOG_OK;
+}
+
+int dog_get_origin(dog_ctx* ctx, double* origin_x, double* origin_y)
+{
+    if (!ctx) return DOG_E_INVAL;
+    if (origin_x) *origin_x = ctx->org_x;
+    if (origin_y) *origin_y = ctx->org_y;
     return DOG_OK;
 }
 

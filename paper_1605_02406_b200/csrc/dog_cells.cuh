@@ -27,8 +27,8 @@ constexpr uint32_t kItem = 256;   // members per k_resample work item
 struct StageList {          // k_cells staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
     uint32_t* c;            // cell index
     uint32_t* n;            // persistent particles n_c
-    uint64_t* Rp;           // floor(rho_p 2^40) (0 if n_c = 0)
-    uint64_t* Rb;           // floor(rho_b 2^40) if m_zO > 0 else 0
+    uint64_t* Rp;           // floor(rho_p 2^FX) (0 if n_c = 0)
+    uint64_t* Rb;           // floor(rho_b 2^FX) if m_zO > 0 else 0
     float* rho_p;           // f32 rho_p (moments denominator)
     uint32_t* np;           // runs ("pairs") of the cell over the sort tiles
 };
@@ -36,7 +36,7 @@ struct StageList {          // k_cells staging, capacity nblk * chunk (>= C); en
 struct CellList {           // the flat active list in cell order (SoA, capacity C)   (k_list_scan)
     uint32_t* c;            // cell index
     uint32_t* n;            // persistent particles n_c
-    uint64_t* Rp;           // floor(rho_p 2^40)
+    uint64_t* Rp;           // floor(rho_p 2^FX)
     float* rho_p;           // f32 rho_p
     uint32_t* start;        // first cell-sorted slot of the cell
     uint32_t* sb;           // first birth slot of the cell (global)
@@ -59,9 +59,10 @@ struct BlockTotals {        // one entry per cell chunk (k_cells); prefixes / to
     uint32_t* np0;          // sum of their run counts
 };
 
-__device__ __forceinline__ uint64_t fx40(float m)
+// floor(max(m, 0) 2^FX) (A-23): exact (a power-of-two scale)
+__device__ __forceinline__ uint64_t fxq(float m, const FilterConst& fc)
 {
-    return (m > 0.0f) ? __double2ull_rz(__dmul_rn((double)m, 1099511627776.0)) : 0ull;
+    return (m > 0.0f) ? __double2ull_rz(__dmul_rn((double)m, fc.fx)) : 0ull;
 }
 
 // e^q for q <= 0 (A-34 "exp spec")
@@ -127,8 +128,8 @@ __device__ __forceinline__ CellOut cell_math(uint32_t n, float m_free, float2 z,
     const float mq = __fmul_rn(o.mO, q);
     o.rb = den > 0.0f ? (mq == 0.0f ? mq : __fdiv_rn(mq, den)) : 0.0f;     // (+-0)/den = +-0
     o.rp = __fsub_rn(o.mO, o.rb);
-    o.Rp = n > 0 ? fx40(o.rp) : 0ull;                                      // A-23
-    o.Rb = z.x > 0.0f ? fx40(o.rb) : 0ull;                                 // P:1197 gate (A-13)
+    o.Rp = n > 0 ? fxq(o.rp, fc) : 0ull;                                      // A-23
+    o.Rb = z.x > 0.0f ? fxq(o.rb, fc) : 0ull;                                 // P:1197 gate (A-13)
     return o;
 }
 
@@ -156,8 +157,8 @@ __device__ __forceinline__ CellOut cell_math_exact(uint32_t n, float4 obs, float
     o.rb = __fmul_rn(rbp, f);
     o.mO = __fadd_rn(o.rp, o.rb);                                          // Eq. 42
     o.mF = __fsub_rn(1.0f, o.mO);
-    o.Rp = n > 0 ? fx40(o.rp) : 0ull;
-    o.Rb = fx40(o.rb);
+    o.Rp = n > 0 ? fxq(o.rp, fc) : 0ull;
+    o.Rb = fxq(o.rb, fc);
     o.bad = false;
     return o;
 }
@@ -215,8 +216,8 @@ __device__ __forceinline__ CellOut cell_math_exact_lik(uint32_t n, float4 ob, fl
     pi = gb > 0.0 ? __double2float_rn(__ddiv_rn(__dmul_rn(pa, Eb), gb)) : 0.0f;
     o.mO = __fadd_rn(o.rp, o.rb);
     o.mF = __fsub_rn(1.0f, o.mO);
-    o.Rp = n > 0 ? fx40(o.rp) : 0ull;
-    o.Rb = fx40(o.rb);
+    o.Rp = n > 0 ? fxq(o.rp, fc) : 0ull;
+    o.Rb = fxq(o.rb, fc);
     o.bad = false;
     return o;
 }

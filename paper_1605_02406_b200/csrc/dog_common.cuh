@@ -65,6 +65,7 @@ struct FilterConst {
     float p_s, p_b, sigma_b, occ_max, v_max;
     uint64_t seed;
     uint32_t force_exact;  // diagnostics (DOG_FORCE_EXACT_F): every F(X) through exact 128-bit products
+    double fx, fx_inv;     // 2^FX, 2^-FX: fixed-point scale of the masses (A-23; FX = 40 below 2^24 cells)
 };
 
 // Diagnostics build only (DOG_NVCC_EXTRA=-DDOG_TIMING, tools/phase_timing.py): per-phase block time,

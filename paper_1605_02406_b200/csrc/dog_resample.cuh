@@ -619,10 +619,14 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
     for (uint32_t s0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); s0 < ns; s0 += gridDim.x * blockDim.x) {
         // last entry with sb <= s: the warp brackets its 32 slots with two 32-ary searches, then each lane
         // bisects the (short) bracket
+        // (band contexts: slots are global, so those below the band's first entry belong to other bands)
         const uint32_t s = s0 + lane;
-        const uint32_t l0 = warp_last_le(0u, Lc, s0, [&](uint32_t i) { return L.sb[i]; });
-        const uint32_t l1 = warp_last_le(l0, Lc, min(s0 + 31u, ns - 1u), [&](uint32_t i) { return L.sb[i]; });
-        if (s >= ns) continue;
+        if (Lc == 0u) continue;
+        const uint32_t sb0 = L.sb[0], s_last = min(s0 + 31u, ns - 1u);
+        if (s_last < sb0) continue;                                 // warp-uniform
+        const uint32_t l0 = warp_last_le(0u, Lc, max(s0, sb0), [&](uint32_t i) { return L.sb[i]; });
+        const uint32_t l1 = warp_last_le(l0, Lc, s_last, [&](uint32_t i) { return L.sb[i]; });
+        if (s >= ns || s < sb0) continue;
         uint32_t lo = l0, hi = l1 + 1u;
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (L.sb[m] <= s) lo = m; else hi = m; }
         const uint32_t li = lo;

@@ -640,7 +640,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         sc->Wtot = Wtot;
         sc->Ppre = Ppre;
-        sc->w_bar = Wtot ? __double2float_rn(__ddiv_rn(__dmul_rn((double)Wtot, 0x1p-40), (double)fc.nu)) : 0.0f;
+        sc->w_bar = Wtot ? __double2float_rn(__ddiv_rn(__dmul_rn((double)Wtot, fc.fx_inv), (double)fc.nu)) : 0.0f;
         sc->nu_over_W = Wtot ? (double)fc.nu / (double)Wtot : 0.0;
         if (W_all) {
             RsConst r;

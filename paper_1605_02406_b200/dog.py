@@ -34,7 +34,8 @@ DEBUG_IDS = {n: i + 1 for i, n in enumerate([
 
 
 class dog_grid(C.Structure):
-    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("cell_size", C.c_float)]
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("cell_size", C.c_float), ("origin_x", C.c_float),
+                ("origin_y", C.c_float)]
 
 
 class dog_params(C.Structure):
@@ -79,6 +80,7 @@ _SIGS = {
     "dog_profile_end": ([_vp, _vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
     "dog_profile_stage_name": ([_vp, C.c_int], C.c_char_p),
     "dog_ego_scroll": ([_vp, C.c_double, C.c_double, C.POINTER(C.c_int32), C.POINTER(C.c_int32), _vp], C.c_int),
+    "dog_get_origin": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "dog_ego_residual": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "dog_eval_cells": ([_vp, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp, _vp, _vp], C.c_int),
     "dog_create_band": ([C.POINTER(dog_grid), C.c_int64, C.c_int64, C.POINTER(dog_params), C.c_uint64, C.c_uint32,
@@ -145,10 +147,10 @@ class Filter:
     def __init__(self, width: int, height: int, nu: int, nu_b: int, *, cell_size: float = 0.1,
                  p_s: float = 0.99, p_b: float = 0.02, sigma_pos: float = 0.02, sigma_vel: float = 0.8,
                  sigma_birth_vel: float = 4.0, free_tau: float = 2.0, occ_max: float = 1.0,
-                 v_max: float = 0.0, seed: int = 2406, debug: bool = False, devices=None):
+                 v_max: float = 0.0, seed: int = 2406, debug: bool = False, devices=None, origin=(0.0, 0.0)):
         self.width, self.height, self.nu, self.nu_b = width, height, nu, nu_b
         self.C = width * height
-        g = dog_grid(width, height, cell_size)
+        g = dog_grid(width, height, cell_size, float(origin[0]), float(origin[1]))
         p = dog_params(p_s, p_b, sigma_pos, sigma_vel, sigma_birth_vel, free_tau, occ_max, v_max)
         h = _vp()
         devs = list(devices) if devices is not None else []
@@ -280,6 +282,12 @@ class Filter:
         _check(dog_ego_scroll(self._h, float(dx), float(dy), C.byref(sx), C.byref(sy), _stream_ptr(stream)),
                "dog_ego_scroll")
         return sx.value, sy.value
+
+    def origin(self) -> tuple[float, float]:
+        """include/dog.h dog_get_origin: world metres of cell (0, 0)'s lower-left corner, moved by ego scrolls."""
+        ox, oy = C.c_double(), C.c_double()
+        _check(dog_get_origin(self._h, C.byref(ox), C.byref(oy)), "dog_get_origin")
+        return ox.value, oy.value
 
     def ego_residual(self) -> tuple[float, float]:
         rx, ry = C.c_double(), C.c_double()

@@ -63,7 +63,7 @@ def test_argument_validation_without_device(lib):
     assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
     bad = dog.dog_params(0.99, 0.02, 0.02, 0.8, 4.0, -2.0, 1.0, 0.0)
     assert dog.dog_create(C.byref(g), 100, 10, C.byref(bad), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
-    g = dog.dog_grid(8192, 4096, 0.1)   # C >= 2^24
+    g = dog.dog_grid(65535, 32769, 0.1)   # C >= 2^31 - 1
     assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, 0, None, C.byref(h)) == dog.DOG_E_INVAL
     ids = (C.c_int * 2)(0, 0)
     assert dog.dog_create(C.byref(g), 100, 10, C.byref(p), 1, 0, 2, None, C.byref(h)) == dog.DOG_E_INVAL

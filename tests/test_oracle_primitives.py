@@ -259,3 +259,20 @@ def test_step_scalars(orc):
     assert abs(al - math.exp(-0.05)) <= ulp32(al)
     p.free_tau = float("inf")
     assert orc.step_scalars(p, 0.1)[3] == 1.0
+
+
+def test_fixed_point_exponent_keeps_totals_below_2_64():
+    """A-23: a cell contributes R_p + R_b <= (rho_p + rho_b) 2^FX, and rho_p + rho_b <= 1 + 2^-24 (DS:
+    rho_p = fl(m_O - rho_b), off by at most half an ulp below 1; exact filter: two quotients of a sum <= 1,
+    each within a relative 2^-24), so a total over C cells is at most C 2^FX (1 + 2^-24); FX = 40 for every
+    grid below 2^24 cells (the pinned examples), 63 - bitlen(C) beyond, never more than one bit given away."""
+    import oracle
+    for C in [1, 2, 1000, (1 << 24) - 1, 1 << 24, (1 << 24) + 1, (1 << 25) - 1, 4096 * 4096, 8192 * 8192,
+              (1 << 31) - 2]:
+        fx = oracle.fx_bits(C)
+        if C < (1 << 24):
+            assert fx == 40
+        bound = Fraction(C) * 2 ** fx * (1 + Fraction(1, 2 ** 24))
+        assert bound < 2 ** 64, (C, fx)
+        if fx < 40:                                      # the next larger exponent would not be safe
+            assert Fraction(C) * 2 ** (fx + 2) >= 2 ** 64, (C, fx)

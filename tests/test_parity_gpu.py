@@ -115,6 +115,22 @@ def test_ego_motion_compensation():
     run_lockstep(I.CONFIGS["cfg1"], 8, ego=ego)
 
 
+def test_grid_origin_follows_the_ego_shifts():
+    """dog_grid's origin (world metres of cell (0, 0)) is kept by the context and moved by -shift * cell_size
+    for every applied ego shift (content moves by +shift cells), so world <-> cell stays consistent."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    f = dog.Filter(cfg.width, cfg.height, cfg.nu, cfg.nu_b, cell_size=cfg.cell_size, origin=(12.5, -3.25))
+    assert f.origin() == (12.5, -3.25)
+    cs = float(np.float32(cfg.cell_size))
+    ox, oy = 12.5, -3.25
+    for dx, dy in [(0.35, -0.12), (-0.71, 0.0), (0.04, 0.33), (0.0, 0.0)]:
+        sx, sy = f.ego_scroll(dx, dy)
+        ox -= sx * cs
+        oy -= sy * cs
+        assert f.origin() == (ox, oy), (dx, dy, f.origin(), (ox, oy))
+
+
 def test_dense_scene_long_list_paths():
     """A cfg-5-like dense scene (i.i.d. measured cells, 4x process noise, p_B 0.1) on 96x96 cells: from
     the third cycle the active list exceeds C/16, so the library switches to the grid-wide list scan and
@@ -337,6 +353,28 @@ def test_maximum_width_grid():
         hit = rng.random(cfg.C) < 0.05
         f[hit, 0] = 0.95
         f[~hit, 1] = 0.3
+        frames.append(f)
+    run_lockstep(cfg, 2, st=st, frames=frames)
+
+
+def test_grid_of_2_24_cells():
+    """4096 x 4096 cells (C = 2^24, the first size past the 40-bit mass fixed point: FX = 38, A-23): a random
+    injected state over the whole grid, every cell with a return or a free observation (every cell active),
+    two cycles -- keys, masses (R_p, R_b at 2^38), slots, W, the next state bit-exact vs the oracle."""
+    import oracle
+    assert oracle.fx_bits(4096 * 4096) == 38
+    cfg = I.config("cfg1", width=4096, height=4096, nu=2_000_000, nu_b=200_000)
+    rng = np.random.default_rng(7)
+    st = dict(x=rng.uniform(0, cfg.width, cfg.nu).astype(np.float32),
+              y=rng.uniform(0, cfg.height, cfg.nu).astype(np.float32),
+              vx=rng.normal(0, 3, cfg.nu).astype(np.float32), vy=rng.normal(0, 3, cfg.nu).astype(np.float32),
+              w_bar=np.float32(0.9 * cfg.C / cfg.nu), m_free=np.zeros(cfg.C, np.float32), k=1)
+    frames = []
+    for k in range(2):
+        f = np.zeros((cfg.C, 2), np.float32)
+        hit = rng.random(cfg.C) < 0.5
+        f[hit, 0] = 0.9
+        f[~hit, 1] = 0.4
         frames.append(f)
     run_lockstep(cfg, 2, st=st, frames=frames)
 
