@@ -178,11 +178,18 @@ void free_all(dog_ctx* ctx)
 
 bool finite(float v) { return std::isfinite(v); }
 
-// Every kernel of a cycle is launched with programmatic stream serialization (PDL, dog_common.cuh):
+// Every kernel of a plain cycle is launched with programmatic stream serialization (PDL, dog_common.cuh):
 // its CTAs may start while the previous kernel drains and wait in griddepcontrol.wait for its results.
-// Measured exception: k_resample_tiles is launched WITHOUT the attribute -- its CTAs resident early
-// beside k_pair_sort's cost ~50 us at cfg T (smem/L1 carveout of the co-resident kernels).
 bool g_pdl = getenv("DOG_NO_PDL") == nullptr;
+// Per cycle: run-heavy cycles (the exact filter, dense scenes) launch without PDL -- measured at cfg T:
+// their multi-wave kernels ran up to 1.7x slower with the next kernel's CTAs launched early (exact
+// cycle 1.39 ms with PDL, 1.21 ms without), while the plain cycle gains ~6 us from it.
+thread_local bool t_pdl_cycle = true;
+struct PdlScope {
+    bool prev;
+    explicit PdlScope(bool on) : prev(t_pdl_cycle) { t_pdl_cycle = on; }
+    ~PdlScope() { t_pdl_cycle = prev; }
+};
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -191,7 +198,7 @@ cudaError_t launch_ex(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, s
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (g_pdl && pdl) {
+    if (g_pdl && t_pdl_cycle && pdl) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -688,6 +695,9 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     const StepArgs a = step_args(ctx, dt);
     const FilterConst fc = filter_const(ctx);
 
+    // run-heavy cycle: the exact filter, or a dense scene by the lagged list length
+    const bool heavy = obs != nullptr || (ctx->lc_host && *(volatile uint32_t*)ctx->lc_host > ctx->C / 16);
+    const PdlScope pdl_scope(!heavy);
     const bool prof = ctx->prof_steps < ctx->prof_max;
     int mark_i = 0;
     auto mark = [&](const char* name) -> cudaError_t {
@@ -703,7 +713,6 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     if (int r = L_cells(ctx, meas, a, fc, st, obs)) return r;
     CK(mark("cells"));
     // 4. flat active list: slots, joint CDF, run-list offsets (Alg. 5 / Alg. 7 prefix sums), one cluster
-    const bool heavy = obs != nullptr || (ctx->lc_host && *(volatile uint32_t*)ctx->lc_host > ctx->C / 16);
     static const int hv = getenv("DOG_HEAVY") ? atoi(getenv("DOG_HEAVY")) : 15;   // diagnostics: which parts
     const bool h_scan = obs != nullptr || (heavy && (hv & 1)), h_pairs = obs != nullptr || (heavy && (hv & 2));
     const bool h_mom = obs != nullptr || (heavy && (hv & 4)), h_births = obs != nullptr || (heavy && (hv & 8));
@@ -864,6 +873,7 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
     const StepArgs a = step_args(ctx, dt);
     const FilterConst fc = filter_const(ctx);
     const int par = (int)(a.k & 1);
+    const PdlScope pdl_scope(false);                        // a run-heavy cycle (see t_pdl_cycle)
     // gated: only cells where a measurement occurred carry the likelihood
     const DopIn dg{(const float4*)lik, p_assoc, (const float4*)obs};
     if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;

@@ -218,6 +218,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - scrd(sc->n_lo) + base;
     const RunInfo* __restrict__ runs = tp.run + base;
+    const uint64_t Ppre = scrd(sc->Ppre);
     for (uint32_t r = tid; r < nd; r += 256) S.first[r] = tp.first[base + r];
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
@@ -261,15 +262,15 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
         double acc[5] = {0, 0, 0, 0, 0};
         bool first_seg = true;
         uint64_t x = tb;
-        auto load_run = [&](RunInfo& q, uint32_t& key, uint64_t& Rp, uint32_t& nm, uint64_t& gsc, float& pa) {
+        auto load_run = [&](RunQ& q, uint32_t& key, uint64_t& Rp, uint32_t& nm, uint64_t& gsc, float& pa) {
             key = tp.key[base + j];
             if (key < fc.C) {
-                q = runs[j];
+                q = run_q(runs[j], L, Ppre);
                 Rp = L.Rp[q.li]; nm = L.n[q.li]; gsc = GS[q.li];
                 pa = din.pA[key];
             }
         };
-        RunInfo q{};
+        RunQ q{};
         uint32_t key = 0, nm = 0;
         uint64_t Rp = 0, gsc = 0;
         float pa = 0.0f;

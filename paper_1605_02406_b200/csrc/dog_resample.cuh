@@ -136,7 +136,7 @@ static_assert(sizeof(RunF) == 32, "RunF: two per 64-byte line");
 struct RtSmem {   // dynamic shared memory of k_resample_tiles (~9.7 KB)
     RunF rf[kRtRunCache];
     uint32_t starts[kSortTile / 32];   // bitmap of run starts over the tile's sorted positions
-    uint32_t dir[kSortTile / 32];      // bitmap over the tile's runs: RunInfo::direct (no run sums needed)
+    uint32_t dir[kSortTile / 32];      // bitmap over the tile's runs: kRunDirect (no run sums needed)
     uint16_t long_run[kSortTile / 16]; // runs of >= 16 members (summed warp-wide)
     uint32_t n_long;
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
@@ -144,7 +144,7 @@ struct RtSmem {   // dynamic shared memory of k_resample_tiles (~9.7 KB)
 constexpr size_t kRtSmemBytes = sizeof(RtSmem);
 
 // Q of member mr of a run's cell: P + mr bp + min(mr, rpm) (even split of the cell's R_p, A-23).
-__device__ __forceinline__ uint64_t member_Q(const RunInfo& q, uint32_t mr)
+__device__ __forceinline__ uint64_t member_Q(const RunQ& q, uint32_t mr)
 {
     return q.P + (uint64_t)mr * q.bp + min(mr, q.rpm);
 }
@@ -245,6 +245,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     if (tskip && tskip[t]) return;                                 // a Doppler tile (k_resample_dopp)
     const uint32_t nd = tp.nd[t];
     const RunInfo* __restrict__ runs = tp.run + base;
+    const uint64_t Ppre = scrd(sc->Ppre);                          // joint prefix of the shards below
     // ---- run starts (bitmap) and the runs' F parameters
     for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) { S.starts[w] = 0u; S.dir[w] = 0u; }
     if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
@@ -253,7 +254,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         const uint32_t f = tp.first[base + r];
         atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
         if (r < (uint32_t)kRtRunCache) {
-            const RunInfo q = runs[r];
+            const RunQ q = run_q(runs[r], L, Ppre);
             if (q.direct) atomicOr(&S.dir[r >> 5], 1u << (r & 31u));
             RunF x;
             x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
@@ -287,8 +288,8 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         // F(Q_mr+1) is the next lane's value when it holds the run's next member
         uint32_t F0 = 0, Jd = 0, mr = 0;
         RunF x{};
-        RunInfo qf{};
-        const bool cached = j < (uint32_t)kRtRunCache;       // else (run-heavy tiles): F from the RunInfo
+        RunQ qf{};
+        const bool cached = j < (uint32_t)kRtRunCache;       // else (run-heavy tiles): F from the cell parameters
         if (mem) {
             if (cached) {
                 x = S.rf[j];
@@ -297,15 +298,15 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
                                               : __fma_rn((double)(mr - x.rpm), x.d1 - rc.nu_over_W, __fma_rn((double)x.rpm, x.d1, x.y0));
                 bool amb = false;
                 F0 = fast_ceil(y0, rc.nu, margin, amb);
-                if (amb) F0 = fcount(member_Q(runs[j], mr), rc);   // rare: exact products
+                if (amb) F0 = fcount(member_Q(run_q(runs[j], L, Ppre), mr), rc);   // rare: exact products
             } else {
-                qf = runs[j];
+                qf = run_q(runs[j], L, Ppre);
                 if (qf.direct) atomicOr(&S.dir[j >> 5], 1u << (j & 31u));
                 mr = qf.pre + (p - tp.first[base + j]);
                 F0 = fcount(member_Q(qf, mr), rc);
             }
             if (kDbg) {
-                const RunInfo q = runs[j];
+                const RunQ q = run_q(runs[j], L, Ppre);
                 Jd = L.start[q.li] + L.sb[q.li] + mr;
                 perm_dbg[L.start[q.li] + mr] = pbase + lperm[base + p];
             }
@@ -323,7 +324,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
                     bool amb = false;
                     F1 = fast_ceil(y1, rc.nu, margin, amb);
                     if (amb) {
-                        const RunInfo q = runs[j];
+                        const RunQ q = run_q(runs[j], L, Ppre);
                         F1 = fcount(member_Q(q, mr) + q.bp + (mr < q.rpm ? 1u : 0u), rc);
                     }
                 } else {
@@ -387,7 +388,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         return;
     }
     // long-list cycles (thousands of short runs per tile): thread per run; the runs of cells k_moments sums
-    // directly (RunInfo::direct) are skipped, the (at most 256) long ones listed, then summed warp-wide
+    // directly (kRunDirect) are skipped, the (at most 256) long ones listed, then summed warp-wide
     if (tid == 0) S.n_long = 0u;
     __syncthreads();                                        // S.dir complete (every run has a member here)
     for (uint32_t r = tid; r < nd; r += kRtThreads) {

@@ -29,15 +29,37 @@ namespace dog {
 constexpr uint32_t kMoDirect = 32;   // long-list (run-heavy) cycles: cells with at most this many particles are
                                      // summed directly by k_moments<true> (resample skips their run sums)
 
-// What k_resample_tiles needs of a run (written by k_pair_sort, one coalesced 32-byte load per run).
+// What the resampling kernels need of a run beyond its cell (written by k_pair_sort): 8 bytes per run --
+// in the run-heavy regime of the exact filter (~1 member per run) the per-run record is a particle-sized
+// stream, so the cell's own parameters are gathered from the list (consecutive runs of a tile belong to
+// consecutive list entries: coalesced) instead of being copied into every run.
 struct RunInfo {
-    uint64_t P;             // joint-CDF prefix of the run's cell (A-25)
+    uint32_t pre;           // rank of the run's first particle among the cell's particles
+    uint32_t li;            // the cell's active-list entry | kRunDirect
+};
+constexpr uint32_t kRunDirect = 0x80000000u;   // k_moments<true> sums the cell's velocities itself (<= kMoDirect
+                                               // members): no run sums needed (list entries are < 2^31)
+
+// A run with its cell's resampling parameters
+struct RunQ {
+    uint64_t P;             // joint-CDF prefix of the cell (A-25), including the shards below
     uint64_t bp;            // R_p / n_c of the cell (even split, A-23)
     uint32_t rpm;           // R_p mod n_c
     uint32_t pre;           // rank of the run's first particle among the cell's particles
-    uint32_t direct;        // 1: k_moments<true> sums the cell's velocities itself (at most kMoDirect members)
     uint32_t li;            // the cell's active-list entry
+    bool direct;
 };
+__device__ __forceinline__ RunQ run_q(RunInfo r, const CellList& L, uint64_t Ppre)
+{
+    RunQ q;
+    q.li = r.li & ~kRunDirect;
+    q.direct = (r.li & kRunDirect) != 0u;
+    q.pre = r.pre;
+    q.P = Ppre + L.P[q.li];
+    q.bp = L.bp[q.li];
+    q.rpm = L.rp[q.li];
+    return q;
+}
 
 struct TilePairs {          // per tile t: entries [t*4096, t*4096 + nd[t])
     uint32_t* key;          // cell key of the run (C = outside the grid)
@@ -657,12 +679,8 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     }
     auto run_info = [&](uint32_t li) {
         RunInfo ri;
-        ri.P = Ppre + L.P[li];
-        ri.bp = L.bp[li];
-        ri.rpm = L.rp[li];
         ri.pre = 0u;
-        ri.direct = kBatch && L.n[li] <= kMoDirect ? 1u : 0u;
-        ri.li = li;
+        ri.li = li | (kBatch && L.n[li] <= kMoDirect ? kRunDirect : 0u);
         return ri;
     };
     auto dop_single = [&](uint32_t li, uint32_t v) {     // a one-run cell: its prefix is 0, its total the run's

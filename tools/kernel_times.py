@@ -41,6 +41,14 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     for x in ins[3:]:
         step(*x, cfg.dt)
     torch.cuda.synchronize()
+if len(sys.argv) > 4 and sys.argv[4] == "timeline":   # start / end of every kernel of the last cycle
+    ev = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA],
+                key=lambda e: e.time_range.start)
+    last = ev[-(len(ev) // n):]
+    t0 = last[0].time_range.start
+    for e in last:
+        print(f"{e.time_range.start - t0:8.1f} {e.time_range.end - t0:8.1f} {e.time_range.end - e.time_range.start:7.1f}  "
+              f"{e.name.split('(')[0].replace('void dog::', '')[:50]}")
 tot = defaultdict(float)
 cnt = defaultdict(int)
 for e in prof.events():
