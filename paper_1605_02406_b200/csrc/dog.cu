@@ -433,7 +433,7 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     AL(ctx->stage.c, LC); AL(ctx->stage.n, LC); AL(ctx->stage.Rp, LC); AL(ctx->stage.Rb, LC);
     AL(ctx->stage.rho_p, LC); AL(ctx->stage.np, LC);
     AL(ctx->list.c, Cs); AL(ctx->list.n, Cs); AL(ctx->list.Rp, Cs); AL(ctx->list.rho_p, Cs);
-    AL(ctx->list.start, Cs); AL(ctx->list.sb, Cs); AL(ctx->list.nb, Cs); AL(ctx->list.P, Cs);
+    AL(ctx->list.start, Cs); AL(ctx->list.sb, Cs); AL(ctx->list.nb, Cs); AL(ctx->list.P, Cs); AL(ctx->list.brec, Cs);
     AL(ctx->list.it, Cs); AL(ctx->list.bp, Cs); AL(ctx->list.rp, Cs); AL(ctx->list.bb, Cs);
     AL(ctx->list.rb, Cs); AL(ctx->list.np, Cs); AL(ctx->list.ps, Cs); AL(ctx->list.pfill, Cs);
     AL(ctx->cell2list, Cs);

@@ -33,6 +33,12 @@ struct StageList {          // k_cells staging, capacity nblk * chunk (>= C); en
     uint32_t* np;           // runs ("pairs") of the cell over the sort tiles
 };
 
+struct BirthRec {           // what the birth kernels need of an entry with birth slots: one 32-byte load
+    uint64_t PB;            // P_c + R_p: joint-CDF position of the cell's first birth (this context)
+    uint64_t bb;            // R_b / n_b
+    uint32_t c, nb, sb, rb; // cell, birth slots, first slot (global), R_b mod n_b
+};
+
 struct CellList {           // the flat active list in cell order (SoA, capacity C)   (k_list_scan)
     uint32_t* c;            // cell index
     uint32_t* n;            // persistent particles n_c
@@ -50,6 +56,7 @@ struct CellList {           // the flat active list in cell order (SoA, capacity
     uint32_t* np;           // runs of the cell
     uint32_t* ps;           // exclusive prefix of np (offset of the cell's run list)
     uint32_t* pfill;        // run-list fill counter (reset here, k_pair_fill)
+    BirthRec* brec;         // entries with n_b > 0 only (written with P; the others hold stale records)
 };
 
 struct BlockTotals {        // one entry per cell chunk (k_cells); prefixes / totals are formed in k_list_scan
@@ -588,8 +595,8 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
         ulonglong2 tot1;
         const ulonglong2 off1 = cluster_offsets(make_ulonglong2(wX, wB), s_w, &s_tot[0], s_base, tot1);
         const ulonglong2 base1 = make_ulonglong2(carry1.x + off1.x, carry1.y + off1.y);
-        uint64_t J[kLsItems], its[kLsItems], sp[kLsItems];
-        uint32_t nbv[kLsItems];
+        uint64_t J[kLsItems], its[kLsItems], sp[kLsItems], bbv[kLsItems];
+        uint32_t nbv[kLsItems], rbv[kLsItems];
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
             const bool ok = gw + 32 * i < Lc;
@@ -614,7 +621,9 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
             L.bp[g] = n[i] ? divmod53(Rp[i], n[i], rem) : 0ull;
             L.rp[g] = rem;
             rem = 0;
-            L.bb[g] = nbv[i] ? divmod53(Rb[i], nbv[i], rem) : 0ull;
+            bbv[i] = nbv[i] ? divmod53(Rb[i], nbv[i], rem) : 0ull;
+            rbv[i] = rem;
+            L.bb[g] = bbv[i];
             L.rb[g] = rem;
             cell2list[c[i]] = g;
         }
@@ -632,6 +641,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
             const uint32_t it0 = (uint32_t)(base2.y + exI[i]);
             L.P[g] = P;
             L.it[g] = it0;
+            if (nbv[i]) L.brec[g] = BirthRec{P + Rp[i], bbv[i], c[i], nbv[i], (uint32_t)sp[i], rbv[i]};
             if (g == Lc - 1) {   // the list's last entry publishes the totals (this context's W)
                 sc->W = P + J[i];
                 sc->n_items = it0 + (uint32_t)its[i];
@@ -791,10 +801,13 @@ __global__ __launch_bounds__(256) void k_ls_chunks2(CellList L, BlockTotals bt, 
         const uint32_t j = j0 + threadIdx.x;
         const bool ok = j < m;
         const uint32_t g = ws.pcnt[b] + j;
-        uint64_t J = 0, I = 0;
+        uint64_t J = 0, I = 0, Rpg = 0, bbg = 0;
+        uint32_t nbv = 0, rbg = 0;
         if (ok) {
-            const uint32_t nbv = L.nb[g];
-            J = L.Rp[g] + (nbv ? L.bb[g] * nbv + L.rb[g] : 0ull);   // R_p + gated R_b = bb nb + rb
+            nbv = L.nb[g];
+            Rpg = L.Rp[g];
+            if (nbv) { bbg = L.bb[g]; rbg = L.rb[g]; }
+            J = Rpg + (nbv ? bbg * nbv + rbg : 0ull);                // R_p + gated R_b = bb nb + rb
             I = (nbv + kItem - 1) / kItem;
         }
         uint64_t tJ, tI;
@@ -805,6 +818,7 @@ __global__ __launch_bounds__(256) void k_ls_chunks2(CellList L, BlockTotals bt, 
             const uint32_t it0 = (uint32_t)(carryI + eI);
             L.P[g] = P;
             L.it[g] = it0;
+            if (nbv) L.brec[g] = BirthRec{P + Rpg, bbg, L.c[g], nbv, L.sb[g], rbg};
             if (g == Lc - 1) {
                 sc->W = P + J;
                 sc->n_items = it0 + (uint32_t)I;

@@ -520,13 +520,13 @@ __global__ __launch_bounds__(256) void k_births(CellList L, NextState out, Birth
     uint32_t li = warp_last_le(0u, Lc, q, [&](uint32_t i) { return L.it[i]; });
     uint32_t sub = q - L.it[li];
     while (true) {
-        const uint32_t c = L.c[li], n = L.n[li], start = L.start[li], nb = L.nb[li];
-        const uint64_t P = Ppre + L.P[li];
+        const BirthRec R = L.brec[li];                                // an entry with items has n_b > 0
+        const uint32_t c = R.c, nb = R.nb;
         const uint32_t r0 = sub * kItem, m = min(kItem, nb - r0);
-        const uint64_t bb = L.bb[li];
-        const uint32_t rbm = L.rb[li], sb = L.sb[li];
-        const uint64_t PB = P + L.Rp[li];
-        const uint32_t jbase = start + sb + n;
+        const uint64_t bb = R.bb;
+        const uint32_t rbm = R.rb, sb = R.sb;
+        const uint64_t PB = Ppre + R.PB;
+        const uint32_t jbase = out.jidx ? L.start[li] + sb + L.n[li] : 0u;   // joint index (debug dump)
         uint32_t nA = 0;                                              // associated slots (NEXT-1)
         uint64_t RbA = 0, bbA = 0, bbB = bb;
         uint32_t rbA = 0, rbB = rbm;
@@ -631,12 +631,13 @@ __global__ __launch_bounds__(256) void k_births_slots(CellList L, NextState out,
         uint32_t lo = l0, hi = l1 + 1u;
         while (hi - lo > 1) { const uint32_t m = (lo + hi) >> 1; if (L.sb[m] <= s) lo = m; else hi = m; }
         const uint32_t li = lo;
-        const uint32_t c = L.c[li], nb = L.nb[li], sb = L.sb[li];
-        if (s - sb >= nb) continue;                                 // (not reached: slots are dense)
+        if (s - L.sb[li] >= L.nb[li]) continue;                     // slots of another band's cells
+        const BirthRec R = L.brec[li];
+        const uint32_t c = R.c, nb = R.nb, sb = R.sb;
         const uint32_t r = s - sb;
-        const uint64_t bb = L.bb[li];
-        const uint32_t rbm = L.rb[li];
-        const uint64_t PB = Ppre + L.P[li] + L.Rp[li];
+        const uint64_t bb = R.bb;
+        const uint32_t rbm = R.rb;
+        const uint64_t PB = Ppre + R.PB;
         const uint32_t cg = c + fc.c_off;
         const uint32_t col = cg % (uint32_t)fc.W, row = cg / (uint32_t)fc.W;
         const float colf = (float)col, rowf = (float)row;
