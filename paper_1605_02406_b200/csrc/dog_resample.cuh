@@ -175,10 +175,15 @@ __device__ __forceinline__ void write_compact(uint32_t c, uint32_t F0, const flo
 {
     const int lane = threadIdx.x & 31;
     if (__reduce_max_sync(0xffffffffu, c) <= 2u) {         // the common case: each lane writes its own
-        for (uint32_t k = 0; k < c; ++k) {                 // (consecutive members of a run own
-            DOG_ASSERT(F0 + k < nu);                       //  consecutive outputs: coalesced)
-            out.s[F0 + k] = X;
-            if (kDbg) out.jidx[F0 + k] = J;
+        if (c > 0u) {                                      // (consecutive members of a run own
+            DOG_ASSERT(F0 < nu);                           //  consecutive outputs: coalesced)
+            out.s[F0] = X;
+            if (kDbg) out.jidx[F0] = J;
+        }
+        if (c > 1u) {
+            DOG_ASSERT(F0 + 1u < nu);
+            out.s[F0 + 1u] = X;
+            if (kDbg) out.jidx[F0 + 1u] = J;
         }
         return;
     }
