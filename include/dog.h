@@ -283,7 +283,7 @@ int dog_step_exact(dog_ctx* ctx, const float* obs, float dt, void* stream);
  * the members' weights proportional to g_A (the Doppler Q_j split with the effective association
  * weight), and the associated births' radial velocity drawn from the posterior given z.  Every other
  * cell takes dog_step_exact's update; p_assoc all 0 gives exactly dog_step_exact.  Whole-grid contexts
- * only (DOG_E_STATE for bands); working buffers (16 B per particle slot + 28 B per cell) are allocated
+ * only (DOG_E_STATE for bands); working buffers (20 B per particle slot + 28 B per cell) are allocated
  * on first use (DOG_E_NOMEM).  DOG_E_INVAL for a NULL or misaligned argument or an invalid dt. */
 int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const float* p_assoc, float dt,
                        void* stream);
@@ -297,7 +297,7 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
  * predicted velocity (Eq. 71: w = p_A mu_A g w + (1 - p_A) mu_Abar w; A-35) and its birth slots split
  * into associated (velocity drawn around the measured radial speed) and unassociated ones (A-36).
  * p_assoc all 0 gives exactly dog_step's cycle.  Whole-grid contexts only (DOG_E_STATE for bands);
- * the three working buffers (16 B per particle slot + 8 B per cell) are allocated on first use
+ * the working buffers (20 B per particle slot + 12 B per cell) are allocated on first use
  * (DOG_E_NOMEM).  DOG_E_INVAL for a NULL or misaligned argument or an invalid dt. */
 int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, const float* p_assoc, float dt,
                      void* stream);

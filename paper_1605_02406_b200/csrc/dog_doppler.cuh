@@ -86,102 +86,133 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
     return lo;
 }
 
-// ---- k_dopp_g: the likelihood g of every member of a Doppler cell (f32 bits per sorted position, in
-//      gfx_out) and the cell's largest g (gmax[cell], integer atomicMax on the bits of a nonnegative float:
-//      order-free).  gmax must be zero on entry (the caller clears it).
+// Warp walk over a tile's sorted positions (as k_resample_tiles): warp w takes [512 w, 512 w + 512), 32
+// consecutive positions per round, lane-contiguous (coalesced); the run of a position from a bitmap of
+// run starts (popcount).  Per round, values of the same run are combined by a segmented reduction
+// (shuffle doubling; runs are contiguous), whose result sits in the run's first lane of the round.
+struct DopWalkSmem {
+    uint32_t starts[kSortTile / 32];   // run starts over the tile's sorted positions
+    uint32_t key[kSortTile];           // cell of each run (C: outside)
+};
+
+// loads the run starts and keys; returns false (block-uniform) if no run of the tile has a likelihood
+__device__ __forceinline__ bool dop_walk_setup(DopWalkSmem& S, TilePairs tp, uint32_t base, uint32_t nd,
+                                               const DopIn& din, uint32_t C)
+{
+    for (uint32_t w = threadIdx.x; w < kSortTile / 32; w += blockDim.x) S.starts[w] = 0u;
+    __syncthreads();
+    bool any = false;
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
+        const uint32_t f = tp.first[base + r], key = tp.key[base + r];
+        atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
+        S.key[r] = key;
+        any |= din_pa(din, key, C) > 0.0f;
+    }
+    return __syncthreads_or(any);
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ T seg_reduce(T v, uint32_t j, Op op)   // lane l: op over [l, end of its run)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const T o = __shfl_down_sync(0xffffffffu, v, dd);
+        const uint32_t oj = __shfl_down_sync(0xffffffffu, j, dd);
+        if (lane + dd < 32 && oj == j) v = op(v, o);
+    }
+    return v;
+}
+
+// calls body(p, j, lane_valid) for the positions of this warp, 32 per round (warp-uniform calls)
+template <typename F>
+__device__ __forceinline__ void dop_walk(const DopWalkSmem& S, uint32_t n, F&& body)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr uint32_t kSpan = kSortTile / 8;
+    const uint32_t w0 = (uint32_t)warp * kSpan;
+    int jprev = -1;
+    {
+        uint32_t c = 0;
+        for (uint32_t k = lane; k < w0 / 32; k += 32) c += __popc(S.starts[k]);
+        jprev += (int)__reduce_add_sync(0xffffffffu, c);
+    }
+    const uint32_t wend = w0 < n ? min(w0 + kSpan, n) : w0;
+    for (uint32_t p0 = w0; p0 < wend; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        const uint32_t word = S.starts[p0 >> 5];
+        const uint32_t j = (uint32_t)(jprev + (int)__popc(lane == 31 ? word : (word & ((2u << lane) - 1u))));
+        jprev += (int)__popc(word);
+        body(p, j, p < wend);
+    }
+}
+
+// ---- k_dopp_g: the likelihood g of every member of a cell with a likelihood (f32 bits per sorted position,
+//      in gfx_out; 0 elsewhere in such tiles) and the cell's largest g (gmax[cell], integer atomicMax on
+//      the bits of a nonnegative float: order-free; one per run and round).  gmax must be zero on entry.
 __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __restrict__ pv, DopIn din,
                                                 uint32_t* __restrict__ gmax, uint32_t* __restrict__ gfx_out,
                                                 const DevScalars* sc, FilterConst fc, int par)
 {
     PDL_ENTER();
-    __shared__ uint16_t s_first[kSortTile + 1];
+    __shared__ DopWalkSmem S;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
     const uint32_t pbase = fc.lo_cap - scrd(sc->n_lo) + base;
-    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) s_first[r] = tp.first[base + r];
-    if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
-    __syncthreads();
-    const uint32_t p0 = threadIdx.x * 16u, p1 = min(p0 + 16u, n);
-    if (p0 >= n) return;
-    uint32_t j = run_of(s_first, nd, p0);
-    uint32_t end = s_first[j + 1];
-    uint32_t key = tp.key[base + j];
-    float pa = din_pa(din, key, fc.C);
-    float4 d = pa > 0.0f ? din.dop[key] : make_float4(0.f, 0.f, 0.f, 1.f);
-    uint32_t mx = 0u;
-    for (uint32_t p = p0; p < p1; ++p) {
-        if (p >= end) {
-            if (mx) atomicMax(&gmax[key], mx);
-            mx = 0u;
-            ++j; end = s_first[j + 1];
-            key = tp.key[base + j];
-            pa = din_pa(din, key, fc.C);
-            if (pa > 0.0f) d = din.dop[key];
+    if (!dop_walk_setup(S, tp, base, nd, din, fc.C)) return;   // (tiles without one: nothing of them is read)
+    const int lane = threadIdx.x & 31;
+    dop_walk(S, n, [&](uint32_t p, uint32_t j, bool valid) {
+        uint32_t gb = 0u, key = fc.C;
+        if (valid) {
+            key = S.key[j];
+            const float pa = din_pa(din, key, fc.C);
+            if (pa > 0.0f) {
+                const float2 V = pv[pbase + p];              // the tile's predicted state is in sorted order
+                const float g = doppler_g(V.x, V.y, din.dop[key]);
+                gb = g > 0.0f ? __float_as_uint(g) : 0u;        // NaN / 0 -> no weight
+            }
+            gfx_out[base + p] = gb;
         }
-        uint32_t gb = 0u;
-        if (pa > 0.0f) {
-            const float2 V = pv[pbase + p];                 // the tile's predicted state is in sorted order
-            const float g = doppler_g(V.x, V.y, d);
-            gb = g > 0.0f ? __float_as_uint(g) : 0u;            // NaN / 0 -> no weight
-            mx = max(mx, gb);
-        }
-        gfx_out[base + p] = gb;
-    }
-    if (mx) atomicMax(&gmax[key], mx);
+        const uint32_t mx = seg_reduce(gb, j, [](uint32_t a, uint32_t b) { return max(a, b); });
+        const uint32_t jl = __shfl_up_sync(0xffffffffu, j, 1);
+        if (valid && (lane == 0 || jl != j) && mx) atomicMax(&gmax[key], mx);
+    });
 }
 
-// ---- k_dopp_runs: gfx = floor((g / g_max) 2^31) of every member of a Doppler cell, summed per run
-//      (rg[run slot]).  Thread t takes sorted positions [16t, 16t+16) (one run search, then sequential),
-//      sums its run segments and adds each segment once (integer atomics: order-free).  gfx_io holds g
-//      (k_dopp_g) on entry and gfx on exit.
+// ---- k_dopp_runs: gfx = floor((g / g_max) 2^31) of every member of a cell with a likelihood, summed per run
+//      (rg[run slot]; and per cell into gsc when given) by integer atomics (order-free, one per run and
+//      round).  gfx_io holds g (k_dopp_g) on entry and gfx on exit.
 __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, const uint32_t* __restrict__ gmax,
                                                    uint64_t* __restrict__ rg, uint8_t* __restrict__ tflag,
                                                    uint32_t* __restrict__ gfx_io, const DevScalars* sc,
                                                    FilterConst fc, int par, uint64_t* __restrict__ gsc)
 {
     PDL_ENTER();
-    __shared__ uint16_t s_first[kSortTile + 1];
+    __shared__ DopWalkSmem S;
     const uint32_t t = blockIdx.x, base = t * kSortTile;
     if (threadIdx.x == 0) tflag[t] = 0;                      // set by k_pair_sort for Doppler tiles
     const uint32_t n = tile_count(sc, par, base);
     if (n == 0) return;
     const uint32_t nd = tp.nd[t];
-    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) { s_first[r] = tp.first[base + r]; rg[base + r] = 0ull; }
-    if (threadIdx.x == 0) s_first[nd] = (uint16_t)n;
-    __syncthreads();
-    const uint32_t p0 = threadIdx.x * 16u, p1 = min(p0 + 16u, n);
-    if (p0 >= n) return;
-    uint32_t j = run_of(s_first, nd, p0);
-    uint32_t end = s_first[j + 1];
-    uint32_t key = tp.key[base + j];
-    float pa = din_pa(din, key, fc.C);
-    float gm = pa > 0.0f ? __uint_as_float(gmax[key]) : 0.0f;
-    uint64_t acc = 0;
-    for (uint32_t p = p0; p < p1; ++p) {
-        if (p >= end) {
-            if (acc) {
-                atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
-                if (gsc) atomicAdd((unsigned long long*)&gsc[key], (unsigned long long)acc);
-            }
-            acc = 0;
-            ++j; end = s_first[j + 1];
-            key = tp.key[base + j];
-            pa = din_pa(din, key, fc.C);
-            if (pa > 0.0f) gm = __uint_as_float(gmax[key]);
+    for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) rg[base + r] = 0ull;
+    if (!dop_walk_setup(S, tp, base, nd, din, fc.C)) return;   // no likelihood cell: gfx / rg of this tile unused
+    const int lane = threadIdx.x & 31;
+    dop_walk(S, n, [&](uint32_t p, uint32_t j, bool valid) {
+        uint32_t gf = 0u, key = fc.C;
+        if (valid) {
+            key = S.key[j];
+            if (din_pa(din, key, fc.C) > 0.0f) gf = doppler_gfx(__uint_as_float(gfx_io[base + p]), __uint_as_float(gmax[key]));
+            gfx_io[base + p] = gf;                           // per sorted position, for k_resample_dopp
         }
-        uint32_t gf = 0u;
-        if (pa > 0.0f) {
-            gf = doppler_gfx(__uint_as_float(gfx_io[base + p]), gm);
-            acc += gf;
+        const uint64_t acc = seg_reduce((uint64_t)gf, j, [](uint64_t a, uint64_t b) { return a + b; });
+        const uint32_t jl = __shfl_up_sync(0xffffffffu, j, 1);
+        if (valid && (lane == 0 || jl != j) && acc) {
+            atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
+            if (gsc) atomicAdd((unsigned long long*)&gsc[key], (unsigned long long)acc);
         }
-        gfx_io[base + p] = gf;                               // per sorted position, for k_resample_dopp
-    }
-    if (acc) {
-        atomicAdd((unsigned long long*)&rg[base + j], (unsigned long long)acc);
-        if (gsc) atomicAdd((unsigned long long*)&gsc[key], (unsigned long long)acc);
-    }
+    });
 }
 
 // ---- k_resample_dopp: persistent members with per-member weights ---------------------------------------

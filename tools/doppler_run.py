@@ -17,6 +17,11 @@ for k in range(30, 30 + n):
     m = sc.frame(k, device="cuda").contiguous()
     dop, pA = sc.doppler(k, m, frac=0.5, p_assoc=0.8, sd=0.25, device="cuda")
     torch.cuda.synchronize()
+    last = k == 30 + n - 1
+    if last:
+        torch.cuda.nvtx.range_push("capture")   # ncu --nvtx --nvtx-include "capture/": the last cycle only
     f.step_doppler(m, dop.contiguous(), pA.contiguous(), cfg.dt)
+    if last:
+        torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 print("ok", int((pA > 0).sum()))
