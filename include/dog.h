@@ -276,7 +276,8 @@ int dog_step_exact(dog_ctx* ctx, const float* obs, float dt, void* stream);
  * general form; Eqs. 38, 49-52; A-38).  obs as dog_step_exact with
  * the 4th value the clutter density p_cl at the cell's measurement; plus two DEVICE arrays:
  *   lik[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) -- the measurement's radial-velocity likelihood
- *             g(z|x) = N(v.u - v_r; 0, sd^2) (Eq. 69), read only where p_assoc > 0 and occurred;
+ *             g(z|x) = N(v.u - v_r; 0, sd^2) (Eq. 69), read only where p_assoc > 0 and occurred; finite,
+ *             sd a normal positive f32 (as dog_step_doppler);
  *   p_assoc[C] f32: association probability p_A in [0, 1].
  * In a cell where a measurement occurred and p_A > 0: g_A(z|x) = p_A g(z|x) + (1 - p_A) p_cl, rho_p
  * and rho_b from the members' likelihood sum and the birth prior's expected likelihood (Eqs. 50-52),
@@ -291,7 +292,8 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
 /* dog_step_doppler -- one cycle with the Doppler / association branch (Eqs. 69-80,
  * P:1157-1232; A-34..A-36).  As dog_step, plus two DEVICE arrays:
  *   doppler[C][4] f32, 16-byte aligned: (u_x, u_y, v_r, sd) per cell -- unit radial direction, measured
- *                 radial speed (m/s) and its SD (> 0), read only where p_assoc > 0;
+ *                 radial speed (m/s) and its SD (a normal positive f32), read only where p_assoc > 0;
+ *                 finite values required (results for NaN / infinite entries are unspecified);
  *   p_assoc[C]    f32: association probability p_A in [0, 1]; 0 = the cell has no Doppler measurement.
  * In a cell with p_A > 0 the persistent members are weighted by the Doppler likelihood g of their
  * predicted velocity (Eq. 71: w = p_A mu_A g w + (1 - p_A) mu_Abar w; A-35) and its birth slots split

@@ -51,7 +51,7 @@ __device__ __forceinline__ float doppler_g(float vx, float vy, float4 d)
     const float t = __fdiv_rn(e, d.w);
     const float q = __fmul_rn(__fmul_rn(t, t), -0.5f);
     const float g = __fdiv_rn(exp_spec(q), __fmul_rn(d.w, 2.50662827463100050f));
-    return g < 0x1.fffffep+127f ? g : 0x1.fffffep+127f;      // inf -> FLT_MAX; NaN stays NaN
+    return g < 0x1.fffffep+127f ? g : 0x1.fffffep+127f;      // inf (and NaN) -> FLT_MAX: finite inputs only, see dog.h
 }
 
 // fixed point relative to the cell's largest likelihood: floor((g / g_max) 2^31) (A-34)
