@@ -620,7 +620,7 @@ static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const
 }
 
 static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                      const uint8_t* tskip = nullptr, bool long_list = false)
+                      const uint64_t* dopGS = nullptr, bool long_list = false)
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     NextState ns{ctx->st, dbg ? ctx->jidx : nullptr};
@@ -629,11 +629,11 @@ static int L_resample(dog_ctx* ctx, const StepArgs& a, const FilterConst& fc, cu
     if (dbg)
         CK(launch_ex(rs_pdl, k_resample_tiles<true>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)ctx->lperm,
                   ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->perm, ctx->ppart,
-                  (const DevScalars*)ctx->sc, fc, par, tskip, long_list ? kMoDirect : 0u));
+                  (const DevScalars*)ctx->sc, fc, par, dopGS, long_list ? kMoDirect : 0u));
     else
         CK(launch_ex(rs_pdl, k_resample_tiles<false>, ctx->tiles, kRtThreads, kRtSmemBytes, st, 0, (const uint16_t*)nullptr,
                   ctx->tp, (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, (uint32_t*)nullptr, ctx->ppart,
-                  (const DevScalars*)ctx->sc, fc, par, tskip, long_list ? kMoDirect : 0u));
+                  (const DevScalars*)ctx->sc, fc, par, dopGS, long_list ? kMoDirect : 0u));
     return DOG_OK;
 }
 
@@ -826,7 +826,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
         CK(cudaEventRecord(ctx->ev_join, ctx->side));
     }
     // tiles without a Doppler cell's members: the closed-form kernel; the others: per-member weights
-    if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
+    if (int r = L_resample(ctx, a, fc, st, ctx->d_GS)) return r;
     NextState ns{ctx->st, nullptr};
     CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, ctx->tp,
                  (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,
@@ -891,7 +891,7 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
         if (int r = L_births(ctx, a, fc, ctx->side, nullptr, true, bl)) return r;
         CK(cudaEventRecord(ctx->ev_join, ctx->side));
     }
-    if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag, true)) return r;
+    if (int r = L_resample(ctx, a, fc, st, ctx->d_GS, true)) return r;
     // the members' split weight in the likelihood cells is the effective pAe (A-38)
     const DopIn de{(const float4*)lik, ctx->d_pAe, nullptr};
     NextState ns{ctx->st, nullptr};
@@ -1068,7 +1068,7 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
         const int par = (int)(a.k & 1);
         if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, false, DopPS{ctx->band_pA, ctx->d_rg, ctx->d_GS, ctx->d_tflag}))
             return r;
-        if (int r = L_resample(ctx, a, fc, st, ctx->d_tflag)) return r;
+        if (int r = L_resample(ctx, a, fc, st, ctx->d_GS)) return r;
         NextState ns{ctx->st, nullptr};
         CK(launch_ex(false, k_resample_dopp, ctx->tiles, 256, kRdSmemBytes, st, 0, ctx->tp,
                      (const float2*)ctx->pxy, (const float2*)ctx->pv, ctx->list, ns, ctx->ppart, din, (const uint64_t*)ctx->d_rg, ctx->d_rs,

@@ -277,7 +277,10 @@ __device__ __forceinline__ T block_prefix_inplace(T* v, uint32_t m, T* s_scan)
 // (identical arithmetic) and staged, and only then is m_F updated and n_c cleared.
 // kExact: the exact PHD/MIB update from obs[C] (NEXT-3) instead of Dempster's rule from meas; m_F untouched.
 template <bool kExact>
-__global__ __launch_bounds__(kCellThreads, 4) void k_cells(
+#ifndef CELL_MINB
+#define CELL_MINB 4
+#endif
+__global__ __launch_bounds__(kCellThreads, CELL_MINB) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* sc, FilterConst fc, float alpha,

@@ -222,6 +222,7 @@ struct RdSmem {
     MomPartial pa[256], pb[256];   // first / last run segment of each thread (spanning runs)
     uint64_t scan[9];
     uint16_t first[kSortTile + 1];
+    uint32_t wrun[kSortTile / 32]; // bitmap over the tile's runs: a likelihood-weighted cell (GS > 0)
 };
 constexpr size_t kRdSmemBytes = sizeof(RdSmem);
 
@@ -250,9 +251,15 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     const uint32_t pbase = fc.lo_cap - scrd(sc->n_lo) + base;
     const RunInfo* __restrict__ runs = tp.run + base;
     const uint64_t Ppre = scrd(sc->Ppre);
-    for (uint32_t r = tid; r < nd; r += 256) S.first[r] = tp.first[base + r];
+    for (uint32_t w = tid; w < kSortTile / 32; w += 256) S.wrun[w] = 0u;
+    __syncthreads();
+    for (uint32_t r = tid; r < nd; r += 256) {             // run starts; weighted runs (parallel gathers)
+        S.first[r] = tp.first[base + r];
+        if (tp.key[base + r] < fc.C && GS[runs[r].li & ~kRunDirect] > 0) atomicOr(&S.wrun[r >> 5], 1u << (r & 31u));
+    }
     if (tid == 0) S.first[nd] = (uint16_t)n;
     __syncthreads();
+    auto weighted = [&](uint32_t r) { return ((S.wrun[r >> 5] >> (r & 31u)) & 1u) != 0u; };
     const uint32_t p0 = tid * kRdItems;
     const uint32_t p1 = min(p0 + kRdItems, n);
 
@@ -294,8 +301,10 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
         bool first_seg = true;
         uint64_t x = tb;
         auto load_run = [&](RunQ& q, uint32_t& key, uint64_t& Rp, uint32_t& nm, uint64_t& gsc, float& pa) {
-            key = tp.key[base + j];
-            if (key < fc.C) {
+            gsc = 0;
+            key = fc.C;
+            if (weighted(j)) {                                // (other runs: k_resample_tiles)
+                key = tp.key[base + j];
                 q = run_q(runs[j], L, Ppre);
                 Rp = L.Rp[q.li]; nm = L.n[q.li]; gsc = GS[q.li];
                 pa = din.pA[key];
@@ -310,7 +319,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
             MomPartial mp;
 #pragma unroll
             for (int i = 0; i < 5; ++i) { mp.s[i] = acc[i]; acc[i] = 0.0; }
-            if (key < fc.C) {
+            if (key < fc.C && gsc > 0) {
                 if (first >= p0 && end <= p0 + kRdItems) ppart[base + j] = mp;   // run inside this thread
                 else if (first_seg) S.pa[tid] = mp;
                 else S.pb[tid] = mp;
@@ -331,7 +340,7 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
             }
             const uint64_t xp = x;
             x += gf[u];
-            if (key >= fc.C) continue;                        // outside the grid: no weight
+            if (key >= fc.C || gsc == 0) continue;            // outside the grid / no weights: k_resample_tiles
             const uint32_t mr = q.pre + (p - first);
             uint64_t Q0, Q1;
             if (gsc > 0) {
@@ -364,9 +373,8 @@ __global__ __launch_bounds__(256, 4) void k_resample_dopp(TilePairs tp, const fl
     const int warp = tid >> 5, lane = tid & 31;
     for (uint32_t r = warp; r < nd; r += 8) {
         const uint32_t f = S.first[r], e = S.first[r + 1];
-        if (tp.key[base + r] >= fc.C) continue;
         const uint32_t tf = f / kRdItems, tl = (e - 1) / kRdItems;
-        if (tf == tl) continue;
+        if (tf == tl || !weighted(r)) continue;             // weighted runs over several threads only
         double s5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         for (uint32_t u = tf + 1 + lane; u <= tl; u += 32)
 #pragma unroll

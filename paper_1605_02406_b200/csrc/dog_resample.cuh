@@ -137,6 +137,7 @@ struct RtSmem {   // dynamic shared memory of k_resample_tiles (~9.7 KB)
     RunF rf[kRtRunCache];
     uint32_t starts[kSortTile / 32];   // bitmap of run starts over the tile's sorted positions
     uint32_t dir[kSortTile / 32];      // bitmap over the tile's runs: kRunDirect (no run sums needed)
+    uint32_t dop[kSortTile / 32];      // bitmap over the tile's runs: likelihood-weighted cell (k_resample_dopp)
     uint16_t long_run[kSortTile / 16]; // runs of >= 16 members (summed warp-wide)
     uint32_t n_long;
     uint32_t sentinel_run;             // index of the run outside the grid, or 0xFFFFFFFF
@@ -227,7 +228,7 @@ template <bool kDbg>
 __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     const uint16_t* __restrict__ lperm, TilePairs tp, const float2* __restrict__ pxy, const float2* __restrict__ pv,
     CellList L, NextState out, uint32_t* __restrict__ perm_dbg, MomPartial* __restrict__ ppart,
-    const DevScalars* sc, FilterConst fc, int par, const uint8_t* __restrict__ tskip, uint32_t mo_direct)
+    const DevScalars* sc, FilterConst fc, int par, const uint64_t* __restrict__ dopGS, uint32_t mo_direct)
 {
     PDL_ENTER();
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -247,12 +248,11 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     }
     const uint32_t n = n_loc > base ? min((uint32_t)kSortTile, n_loc - base) : 0u;
     if (n == 0) return;
-    if (tskip && tskip[t]) return;                                 // a Doppler tile (k_resample_dopp)
     const uint32_t nd = tp.nd[t];
     const RunInfo* __restrict__ runs = tp.run + base;
     const uint64_t Ppre = scrd(sc->Ppre);                          // joint prefix of the shards below
     // ---- run starts (bitmap) and the runs' F parameters
-    for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) { S.starts[w] = 0u; S.dir[w] = 0u; }
+    for (uint32_t w = tid; w < kSortTile / 32; w += kRtThreads) { S.starts[w] = 0u; S.dir[w] = 0u; S.dop[w] = 0u; }
     if (tid == 0) S.sentinel_run = tp.key[base + nd - 1] >= fc.C ? nd - 1 : 0xFFFFFFFFu;
     __syncthreads();
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
@@ -261,6 +261,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         if (r < (uint32_t)kRtRunCache) {
             const RunQ q = run_q(runs[r], L, Ppre);
             if (q.direct) atomicOr(&S.dir[r >> 5], 1u << (r & 31u));
+            if (dopGS && dopGS[q.li] > 0) atomicOr(&S.dop[r >> 5], 1u << (r & 31u));
             RunF x;
             x.y0 = __fma_rn((double)q.P, rc.nu_over_W, -rc.U_frac);
             x.d1 = __dmul_rn((double)(q.bp + 1u), rc.nu_over_W);
@@ -295,8 +296,11 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         RunF x{};
         RunQ qf{};
         const bool cached = j < (uint32_t)kRtRunCache;       // else (run-heavy tiles): F from the cell parameters
+        bool memb = mem;                                    // members of likelihood-weighted cells: k_resample_dopp
         if (mem) {
-            if (cached) {
+            if (cached && dopGS && ((S.dop[j >> 5] >> (j & 31u)) & 1u)) {
+                memb = false;
+            } else if (cached) {
                 x = S.rf[j];
                 mr = x.pre + (p - x.first);
                 const double y0 = mr <= x.rpm ? __fma_rn((double)mr, x.d1, x.y0)
@@ -307,19 +311,24 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
             } else {
                 qf = run_q(runs[j], L, Ppre);
                 if (qf.direct) atomicOr(&S.dir[j >> 5], 1u << (j & 31u));
-                mr = qf.pre + (p - tp.first[base + j]);
-                F0 = fcount(member_Q(qf, mr), rc);
+                if (dopGS && dopGS[qf.li] > 0) {
+                    memb = false;
+                    atomicOr(&S.dop[j >> 5], 1u << (j & 31u));
+                } else {
+                    mr = qf.pre + (p - tp.first[base + j]);
+                    F0 = fcount(member_Q(qf, mr), rc);
+                }
             }
-            if (kDbg) {
+            if (kDbg && memb) {
                 const RunQ q = run_q(runs[j], L, Ppre);
                 Jd = L.start[q.li] + L.sb[q.li] + mr;
                 perm_dbg[L.start[q.li] + mr] = pbase + lperm[base + p];
             }
         }
         const uint32_t Fn = __shfl_down_sync(0xffffffffu, F0, 1);
-        const uint32_t jn = __shfl_down_sync(0xffffffffu, mem ? j : 0xFFFFFFFFu, 1);
+        const uint32_t jn = __shfl_down_sync(0xffffffffu, memb ? j : 0xFFFFFFFFu, 1);
         uint32_t c = 0;
-        if (mem) {
+        if (memb) {
             uint32_t F1 = Fn;
             if (lane == 31 || jn != j) {                    // the run's last member in this round
                 if (cached) {
@@ -379,16 +388,21 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
         ppart[base + r] = mp;
     };
     constexpr uint32_t nw = kRtThreads / 32;
+    auto dop_run = [&](uint32_t r) -> bool {                // weighted runs: k_resample_dopp sums them
+        if (!dopGS) return false;
+        if (r < (uint32_t)kRtRunCache) return ((S.dop[r >> 5] >> (r & 31u)) & 1u) != 0u;
+        return dopGS[runs[r].li & ~kRunDirect] > 0;
+    };
     if (!mo_direct) {   // few, long runs: warps walk the runs directly (no barrier)
         for (uint32_t r = warp; r < nd; r += nw) {
             uint32_t f, e;
             run_bounds(r, f, e);
-            if (r != srun && e - f >= 16u) warp_run(r, f, e);
+            if (r != srun && e - f >= 16u && !dop_run(r)) warp_run(r, f, e);
         }
         for (uint32_t r = tid; r < nd; r += kRtThreads) {
             uint32_t f, e;
             run_bounds(r, f, e);
-            if (r != srun && e - f < 16u) thread_run(r, f, e);
+            if (r != srun && e - f < 16u && !dop_run(r)) thread_run(r, f, e);
         }
         return;
     }
@@ -397,7 +411,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     if (tid == 0) S.n_long = 0u;
     __syncthreads();                                        // S.dir complete (every run has a member here)
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
-        if (r == srun || ((S.dir[r >> 5] >> (r & 31u)) & 1u)) continue;
+        if (r == srun || ((S.dir[r >> 5] >> (r & 31u)) & 1u) || ((S.dop[r >> 5] >> (r & 31u)) & 1u)) continue;
         uint32_t f, e;
         run_bounds(r, f, e);
         if (e - f >= 16u) S.long_run[atomicAdd(&S.n_long, 1u)] = (uint16_t)r;
