@@ -365,6 +365,8 @@ static int create_impl(const dog_grid* grid, int64_t n_particles, int64_t n_birt
     ctx->own_tiles = ctx->own_cap / kSortTile;
     {   // cell chunks of 2048 cells (at most kMaxCellBlocks chunks)
         uint32_t chunk = kCellIter;
+        if (const char* e = getenv("DOG_CELL_CHUNK"))       // diagnostics: a multiple of 2048 cells
+            chunk = std::max<uint32_t>(kCellIter, (uint32_t)atoi(e) / kCellIter * kCellIter);
         uint32_t nblk = cdiv(ctx->C, chunk);
         while (nblk > (uint32_t)kMaxCellBlocks) { chunk *= 2; nblk = cdiv(ctx->C, chunk); }
         ctx->cell_chunk = chunk;
@@ -1740,6 +1742,8 @@ static int create_sharded(const dog_grid* grid, int64_t n_particles, int64_t n_b
     if (!P) return DOG_E_NOMEM;
     P->device = device_ids[0];
     P->grid = *grid;
+    P->org_x = (double)grid->origin_x;
+    P->org_y = (double)grid->origin_y;
     P->params = *params;
     P->seed = seed;
     P->nu = n_particles;
