@@ -74,6 +74,7 @@ struct dog_ctx {
     WideScan ws{};                                // grid-wide list scan (large active lists)
     uint32_t ls_cluster = 0, flat_blocks = 0;     // k_list_scan cluster size; lane-per-cell grids
     uint32_t* cell2list = nullptr;
+    bool dense = false;                           // this cycle lists every cell at its own index (exact filter)
     MomPartial* ppart = nullptr;                  // velocity sums per run
     // debug-only arrays
     uint32_t* perm = nullptr;
@@ -579,14 +580,19 @@ static int L_cells(dog_ctx* ctx, const float* meas, const StepArgs& a, const Fil
 {
     const bool dbg = (ctx->flags & DOG_FLAG_DEBUG) != 0;
     CellDebug cdbg{dbg ? ctx->dbg_rho_p : nullptr, ctx->dbg_rho_b, ctx->dbg_Rp, ctx->dbg_Rb};
+    // dense cycles stage every cell at its own index directly into the list arrays (~all cells are active
+    // in the exact filter: no compaction, no copy to the list, cell -> entry is the identity)
+    const StageList sl = ctx->dense ? StageList{ctx->list.c, ctx->list.n, ctx->list.Rp, ctx->stage.Rb, ctx->list.rho_p,
+                                                ctx->list.np}
+                                    : ctx->stage;
     if (obs)
         CK(launch(k_cells<true>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
-                  (const float2*)nullptr, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)obs, xl));
+                  (const float2*)nullptr, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, sl, ctx->bt,
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)obs, xl, (uint32_t)ctx->dense));
     else
         CK(launch(k_cells<false>, ctx->cell_blocks, kCellThreads, 0, st, 0, ctx->counts, ctx->npairs, ctx->m_free,
-                  (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, ctx->stage, ctx->bt,
-                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)nullptr, xl));
+                  (const float2*)meas, ctx->occ, ctx->fre, ctx->mean, ctx->cov, ctx->mvalid, cdbg, sl, ctx->bt,
+                  ctx->cell_chunk, ctx->sc, fc, a.alpha, (const float4*)nullptr, xl, (uint32_t)ctx->dense));
     return DOG_OK;
 }
 
@@ -595,8 +601,11 @@ static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, c
 {
     if (wide) {   // every cell may be active (exact filter): grid-wide scan over k_cells' chunks
         CK(launch(k_ls_prefix1, 1, 1024, 0, st, 0, ctx->bt, ctx->cell_blocks, ctx->ws, ctx->sc, A_all, fc));
-        CK(launch(k_ls_chunks1, ctx->cell_blocks, 256, 0, st, 0, ctx->stage, ctx->list, ctx->bt, ctx->cell_chunk,
-                  ctx->cell2list, ctx->ws, (const DevScalars*)ctx->sc, fc));
+        const StageList sl = ctx->dense ? StageList{ctx->list.c, ctx->list.n, ctx->list.Rp, ctx->stage.Rb, ctx->list.rho_p,
+                                                    ctx->list.np}
+                                        : ctx->stage;
+        CK(launch(k_ls_chunks1, ctx->cell_blocks, 256, 0, st, 0, sl, ctx->list, ctx->bt, ctx->cell_chunk,
+                  ctx->cell2list, ctx->ws, (const DevScalars*)ctx->sc, fc, (uint32_t)ctx->dense));
         CK(launch(k_ls_prefix2, 1, 1024, 0, st, 0, ctx->cell_blocks, ctx->ws));
         CK(launch(k_ls_chunks2, ctx->cell_blocks, 256, 0, st, 0, ctx->list, ctx->bt, ctx->ws, ctx->sc, fc,
                   (int64_t)a.k));
@@ -610,8 +619,8 @@ static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, c
 static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
                    bool long_list = false, DopPS dp = DopPS{nullptr, nullptr, nullptr, nullptr})
 {
-    CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list, (const uint32_t*)ctx->cell2list, ctx->plist,
-              ctx->C));
+    CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list,
+              ctx->dense ? (const uint32_t*)nullptr : (const uint32_t*)ctx->cell2list, ctx->plist, ctx->C));
     if (long_list)   // every cell listed, most without runs (the exact filter)
         CK(launch(k_pair_sort<true>, 2 * ctx->flat_blocks, 256, 0, st, 0, ctx->tp, ctx->list, ctx->plist, ctx->ptmp, W_all,
                   ctx->sc, fc, (int)(a.k & 1), dp));
@@ -700,6 +709,7 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     // run-heavy cycle: the exact filter, or a dense scene by the lagged list length
     const bool heavy = obs != nullptr || (ctx->lc_host && *(volatile uint32_t*)ctx->lc_host > ctx->C / 16);
     const PdlScope pdl_scope(!heavy);
+    ctx->dense = obs != nullptr;                            // the exact filter: every cell is active
     const bool prof = ctx->prof_steps < ctx->prof_max;
     int mark_i = 0;
     auto mark = [&](const char* name) -> cudaError_t {
@@ -805,6 +815,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     const FilterConst fc = filter_const(ctx);
     const DopIn din{(const float4*)doppler, p_assoc};
     const int par = (int)(a.k & 1);
+    ctx->dense = false;
     if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;
     // the per-run likelihood sums need only the tile sort: on the side stream beside k_cells and the
     // list scan (they touch nothing it reads or writes), joined before the pair sort consumes them
@@ -876,6 +887,7 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
     const FilterConst fc = filter_const(ctx);
     const int par = (int)(a.k & 1);
     const PdlScope pdl_scope(false);                        // a run-heavy cycle (see t_pdl_cycle)
+    ctx->dense = true;                                      // every cell listed at its own index
     // gated: only cells where a measurement occurred carry the likelihood
     const DopIn dg{(const float4*)lik, p_assoc, (const float4*)obs};
     if (int r = L_predict_sort(ctx, true, a, fc, st)) return r;

@@ -284,7 +284,7 @@ __global__ __launch_bounds__(kCellThreads, CELL_MINB) void k_cells(
     uint32_t* __restrict__ counts, uint32_t* __restrict__ npairs, float* __restrict__ m_free, const float2* __restrict__ meas,
     float* __restrict__ occ, float* __restrict__ free_out, float2* __restrict__ mean, float* __restrict__ cov,
     uint32_t* __restrict__ mvalid, CellDebug dbg, StageList L, BlockTotals bt, uint32_t chunk, DevScalars* sc, FilterConst fc, float alpha,
-    const float4* __restrict__ obs, ExactLik xl)
+    const float4* __restrict__ obs, ExactLik xl, uint32_t dense)
 {
     PDL_ENTER();
     __shared__ uint32_t s_cnt[kCellItems][kCellThreads / 32];
@@ -333,7 +333,7 @@ __global__ __launch_bounds__(kCellThreads, CELL_MINB) void k_cells(
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
             const uint32_t pw = __shfl_sync(0xffffffffu, prev[i], 0);
             const uint32_t word = (base + i * kCellThreads + warp * 32) >> 5;
-            const bool act = valid && (o.n > 0 || o.Rb > 0);
+            const bool act = valid && (dense || o.n > 0 || o.Rb > 0);   // dense: every cell is an entry (li = c)
             if (valid) {
                 occ[c] = o.mO;
                 free_out[c] = o.mF;
@@ -718,7 +718,7 @@ __global__ __launch_bounds__(1024) void k_ls_prefix1(BlockTotals bt, uint32_t nb
 
 __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, BlockTotals bt, uint32_t chunk,
                                                     uint32_t* __restrict__ cell2list, WideScan ws,
-                                                    const DevScalars* sc, FilterConst fc)
+                                                    const DevScalars* sc, FilterConst fc, uint32_t dense)
 {
     PDL_ENTER();
     __shared__ uint64_t s_w[9];
@@ -744,8 +744,12 @@ __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, Bl
             const uint64_t sp = slot_of(Ax, A, nu_b, rcpA);
             const uint64_t s_next = Rb ? slot_of(Ax + Rb, A, nu_b, rcpA) : sp;
             const uint32_t nbv = (uint32_t)(s_next - sp);
-            L.c[g] = c; L.n[g] = n; L.Rp[g] = Rp; L.rho_p[g] = rho;
-            L.np[g] = npv; L.ps[g] = (uint32_t)(x0 >> 32); L.pfill[g] = 0u;
+            if (!dense) {   // (dense cycles: k_cells staged every cell in place, entry g = cell c = si)
+                L.c[g] = c; L.n[g] = n; L.Rp[g] = Rp; L.rho_p[g] = rho; L.np[g] = npv;
+                cell2list[c] = g;
+            }
+            DOG_ASSERT(!dense || g == si);
+            L.ps[g] = (uint32_t)(x0 >> 32); L.pfill[g] = 0u;
             L.start[g] = (uint32_t)x0;
             L.sb[g] = (uint32_t)sp;
             L.nb[g] = nbv;
@@ -755,7 +759,6 @@ __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, Bl
             rem = 0;
             L.bb[g] = nbv ? divmod53(Rb, nbv, rem) : 0ull;
             L.rb[g] = rem;
-            cell2list[c] = g;
             sJ += Rp + (nbv ? Rb : 0ull);
             sI += (nbv + kItem - 1) / kItem;
         }

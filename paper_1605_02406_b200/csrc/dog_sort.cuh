@@ -615,7 +615,7 @@ __global__ __launch_bounds__(256) void k_pair_fill(TilePairs tp, CellList L, con
     for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
         const uint32_t key = tp.key[base + r];
         if (key >= C) continue;
-        const uint32_t li = cell2list[key];
+        const uint32_t li = cell2list ? cell2list[key] : key;    // (dense cycles: entry = cell)
         const uint32_t slot = atomicAdd(&L.pfill[li], 1u);
         DOG_ASSERT(slot < L.np[li]);
         plist[L.ps[li] + slot] = (t << 12) | r;
