@@ -258,7 +258,7 @@ __global__ __launch_bounds__(kRtThreads) void k_resample_tiles(
     for (uint32_t r = tid; r < nd; r += kRtThreads) {
         const uint32_t f = tp.first[base + r];
         atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
-        if (r < (uint32_t)kRtRunCache) {
+        if (r < (uint32_t)kRtRunCache && r != S.sentinel_run) {   // (the run outside the grid has no RunInfo)
             const RunQ q = run_q(runs[r], L, Ppre);
             if (q.direct) atomicOr(&S.dir[r >> 5], 1u << (r & 31u));
             if (dopGS && dopGS[q.li] > 0) atomicOr(&S.dop[r >> 5], 1u << (r & 31u));
