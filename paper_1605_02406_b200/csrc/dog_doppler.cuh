@@ -92,6 +92,7 @@ __device__ __forceinline__ uint32_t run_of(const uint16_t* first, uint32_t nd, u
 // (shuffle doubling; runs are contiguous), whose result sits in the run's first lane of the round.
 struct DopWalkSmem {
     uint32_t starts[kSortTile / 32];   // run starts over the tile's sorted positions
+    uint32_t lik[kSortTile / 32];      // runs of a cell with a likelihood (din_pa > 0)
     uint32_t key[kSortTile];           // cell of each run (C: outside)
 };
 
@@ -99,14 +100,17 @@ struct DopWalkSmem {
 __device__ __forceinline__ bool dop_walk_setup(DopWalkSmem& S, TilePairs tp, uint32_t base, uint32_t nd,
                                                const DopIn& din, uint32_t C)
 {
-    for (uint32_t w = threadIdx.x; w < kSortTile / 32; w += blockDim.x) S.starts[w] = 0u;
+    for (uint32_t w = threadIdx.x; w < kSortTile / 32; w += blockDim.x) { S.starts[w] = 0u; S.lik[w] = 0u; }
     __syncthreads();
     bool any = false;
     for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
         const uint32_t f = tp.first[base + r], key = tp.key[base + r];
         atomicOr(&S.starts[f >> 5], 1u << (f & 31u));
         S.key[r] = key;
-        any |= din_pa(din, key, C) > 0.0f;
+        if (din.pA && din_pa(din, key, C) > 0.0f) {
+            atomicOr(&S.lik[r >> 5], 1u << (r & 31u));
+            any = true;
+        }
     }
     return __syncthreads_or(any);
 }
@@ -167,8 +171,7 @@ __global__ __launch_bounds__(256) void k_dopp_g(TilePairs tp, const float2* __re
         uint32_t gb = 0u, key = fc.C;
         if (valid) {
             key = S.key[j];
-            const float pa = din_pa(din, key, fc.C);
-            if (pa > 0.0f) {
+            if ((S.lik[j >> 5] >> (j & 31u)) & 1u) {         // a run of a cell with a likelihood
                 const float2 V = pv[pbase + p];              // the tile's predicted state is in sorted order
                 const float g = doppler_g(V.x, V.y, din.dop[key]);
                 gb = g > 0.0f ? __float_as_uint(g) : 0u;        // NaN / 0 -> no weight
@@ -203,7 +206,8 @@ __global__ __launch_bounds__(256) void k_dopp_runs(TilePairs tp, DopIn din, cons
         uint32_t gf = 0u, key = fc.C;
         if (valid) {
             key = S.key[j];
-            if (din_pa(din, key, fc.C) > 0.0f) gf = doppler_gfx(__uint_as_float(gfx_io[base + p]), __uint_as_float(gmax[key]));
+            if ((S.lik[j >> 5] >> (j & 31u)) & 1u)
+                gf = doppler_gfx(__uint_as_float(gfx_io[base + p]), __uint_as_float(gmax[key]));
             gfx_io[base + p] = gf;                           // per sorted position, for k_resample_dopp
         }
         const uint64_t acc = seg_reduce((uint64_t)gf, j, [](uint64_t a, uint64_t b) { return a + b; });
