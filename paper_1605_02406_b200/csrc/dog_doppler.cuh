@@ -9,15 +9,16 @@
 //   * the cell's nu_b birth slots split into nu_A associated slots (velocity from p(x | z)) and
 //     nu_b - nu_A unassociated ones, sharing R_bA and R_b - R_bA (A-36).
 // Weights are no longer uniform within a cell, so the closed-form per-run resampling of
-// k_resample_tiles does not apply; this path uses
+// k_resample_tiles does not apply to its runs; this path uses
 //   k_dopp_g       per tile: g of every member, the cell maxima g_max (integer atomicMax: order-free)
 //   k_dopp_runs    per tile: gfx of every member, summed per run (integer atomics: order-free)
 //   k_pair_sort    (its Doppler branch) per active cell: the runs' gfx sums in tile order -> exclusive
 //                  prefixes, cell total GS, tile flags
-//   k_resample_dopp per tile holding a Doppler cell's members: block prefix of gfx -> GS_j of every
-//                  member -> Q_j, Q_{j+1} -> F(.) -> copies; weighted velocity sums per run for the
-//                  moments.  Every other tile goes through k_resample_tiles (closed form, even split).
-//   k_moments<true>, k_births<true>.
+//   k_resample_dopp per tile holding a Doppler cell's members, for the runs of such cells only: block
+//                  prefix of gfx -> GS_j of every member -> Q_j, Q_{j+1} -> F(.) -> copies; weighted
+//                  velocity sums per run for the moments.  k_resample_tiles takes every tile and skips
+//                  those runs (closed form, even split for the others).
+//   k_moments (its Doppler branch), k_births (the associated slots).
 // Every floating-point step uses explicit round-to-nearest intrinsics in the oracle's operation order,
 // so the next state is bit-identical to orc_step_doppler.
 #pragma once
