@@ -162,7 +162,7 @@ __global__ __launch_bounds__(kPsThreads) void k_predict_sort(
     //      (one or two radix passes instead of the 13+ bits of the cell index itself).
     constexpr uint32_t kOut = 0xFFFFFFFEu;                  // outside the context's band (or the grid)
     uint32_t rmin = 0xFFFFu, rmax = 0u, cmin = 0xFFFFu, cmax = 0u, anyout = 0u;
-#pragma unroll 2
+#pragma unroll 4
     for (int i = 0; i < kPsRows; ++i) {
         const uint32_t p = warp * (kPsRows * 32) + i * 32 + lane;
         uint32_t key = 0xFFFFFFFFu;
