@@ -327,7 +327,8 @@ __global__ __launch_bounds__(kCellThreads, CELL_MINB) void k_cells(
         for (int i = 0; i < kCellItems; ++i) {
             const uint32_t c = base + i * kCellThreads + tid;
             const bool valid = c < c1;
-            const CellOut o = kExact ? cell_exact_any(n[i], ob[i], c, w_pred, fc, xl, false)
+            const bool inl = kExact && dense;                // dense exact cycles: the entry is written here
+            const CellOut o = kExact ? cell_exact_any(n[i], ob[i], c, w_pred, fc, xl, inl && valid)
                                      : cell_math(n[i], mf[i], z[i], w_pred, alpha, fc);
             const bool vnow = valid && o.n > 0 && o.rp > 0.0f && o.S > 0.0f;
             const uint32_t bal = __ballot_sync(0xffffffffu, vnow);
@@ -348,8 +349,26 @@ __global__ __launch_bounds__(kCellThreads, CELL_MINB) void k_cells(
                 bad_loc += o.bad ? 1u : 0u;
             }
             if (lane == 0 && (word << 5) < c1 && bal != pw) mvalid[word] = bal;
+            if (inl) {                                      // entry li = c (the list is the grid, no staging)
+                if (valid) {
+                    if (o.n) counts[c] = 0u;
+                    L.c[c] = c; L.n[c] = o.n; L.Rp[c] = o.Rp; L.Rb[c] = o.Rb; L.rho_p[c] = o.rp;
+                    uint32_t npc = 0;
+                    if (o.n) { npc = npf[i]; npairs[c] = 0u; }
+                    L.np[c] = npc;
+                    A_loc += o.Rb;
+                    N_loc += o.n;
+                    P_loc += npc;
+                }
+                continue;
+            }
             abal[i] = __ballot_sync(0xffffffffu, act);
             if (lane == 0) s_cnt[i][warp] = __popc(abal[i]);
+        }
+        if (kExact && dense) {                              // block-uniform
+            if (tid == 0) s_run += min(c1 - base, (uint32_t)kCellIter);
+            __syncthreads();
+            continue;
         }
         __syncthreads();
         if (warp == 0) {   // exclusive offsets in cell order (item-major, then warp) + running total
