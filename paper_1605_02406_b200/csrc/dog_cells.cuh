@@ -752,7 +752,11 @@ __global__ __launch_bounds__(256) void k_ls_chunks1(StageList Ls, CellList L, Bl
         uint32_t c = 0, n = 0, npv = 0;
         uint64_t Rp = 0, Rb = 0;
         float rho = 0.0f;
-        if (ok) { c = Ls.c[si]; n = Ls.n[si]; npv = Ls.np[si]; Rp = Ls.Rp[si]; Rb = Ls.Rb[si]; rho = Ls.rho_p[si]; }
+        if (ok) {
+            n = Ls.n[si]; npv = Ls.np[si]; Rp = Ls.Rp[si]; Rb = Ls.Rb[si];
+            if (dense) c = si;                               // (entry = cell; c and rho_p are in place already)
+            else { c = Ls.c[si]; rho = Ls.rho_p[si]; }
+        }
         const uint64_t X = (uint64_t)n | ((uint64_t)npv << 32);
         uint64_t tX, tB;
         const uint64_t exX = block_excl_scan<uint64_t, 8>(X, s_w, tX);
