@@ -97,3 +97,29 @@ def test_exact_full_size_cfgT_one_cycle():
     co = o.read_cells()
     cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
     bits(co["occ"], cg["occ"], "occ")
+
+
+def test_exact_then_plain_cycles_alternate():
+    """Mode switches on one filter: exact cycles (dense list, no PDL), plain Dempster-Shafer cycles
+    (compacted list, cluster scan), exact again -- every cycle bit-exact with the oracle."""
+    cfg = I.config("cfg2", width=128, height=96, nu=40_000, nu_b=4_000, beams=300, movers=3, peds=2, boxes=6)
+    o, g = pair(cfg)
+    sc = I.scene(cfg)
+    for k, mode in enumerate(["plain", "exact", "exact", "plain", "plain", "exact", "plain"]):
+        meas = sc.frame(k)
+        if mode == "exact":
+            obs = I.Scene.exact_obs(meas)
+            o.step_exact(obs.numpy(), cfg.dt)
+            g.step_exact(obs.cuda().contiguous(), cfg.dt)
+        else:
+            o.step(meas.numpy(), cfg.dt)
+            g.step(meas.cuda().contiguous(), cfg.dt)
+        for n in ("KEY", "OFFSETS", "RHO_P", "RHO_B", "RP", "RB", "NB", "JOINT_IDX"):
+            bits(o.dump(n), g.debug(n), f"cycle {k} ({mode}): {n}")
+        sto, stg = o.get_state(), g.get_state()
+        for key in ("x", "y", "vx", "vy", "m_free"):
+            bits(sto[key], stg[key], f"cycle {k} ({mode}): state.{key}")
+        co = o.read_cells()
+        cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
+        bits(co["occ"], cg["occ"], f"cycle {k} ({mode}): occ")
+        close(co["mean"], cg["mean"], 1e-4, 1e-6, f"cycle {k} ({mode}): mean")
