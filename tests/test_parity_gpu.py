@@ -133,12 +133,15 @@ def test_grid_origin_follows_the_ego_shifts():
 
 def test_dense_scene_long_list_paths():
     """A cfg-5-like dense scene (i.i.d. measured cells, 4x process noise, p_B 0.1) on 96x96 cells: from
-    the third cycle the active list exceeds C/16, so the library switches to the grid-wide list scan and
+    the third cycle the active list exceeds C/4, so the library switches to the grid-wide list scan and
     the lane-per-cell pair sort, moments and per-slot births -- every stage stays bit-exact with the
     oracle (the switch must not change a result)."""
     cfg = I.config("cfg5", width=96, height=96, nu=120_000, nu_b=30_000)
     o, g = run_lockstep(cfg, 7)
     assert o.scalars()["n_in"] > 0
+    n_c = np.diff(o.dump("OFFSETS").astype(np.int64))
+    active = int(np.count_nonzero((n_c > 0) | (o.dump("RB") > 0)))
+    assert active > cfg.C // 4, (active, cfg.C)              # the run-heavy paths were taken
 
 
 def test_exact_resampling_fallback_forced(monkeypatch):
