@@ -122,7 +122,10 @@ constexpr int kRtThreads = RT_THREADS, kRtItems = kSortTile / kRtThreads;   // s
 static_assert(kRtItems % 8 == 0, "16-byte vector loads of the tile arrays");
 constexpr uint32_t kRtShortSpan = 8;                                  // phase R: longer runs combined by a warp
 
-constexpr int kRtRunCache = 256;                                      // runs whose RunF sits in smem
+#ifndef RT_RUNCACHE
+#define RT_RUNCACHE 256
+#endif
+constexpr int kRtRunCache = RT_RUNCACHE;                                      // runs whose RunF sits in smem
 
 // Per run, what the copy pass needs to place member r = pre + k (k = position - first): F(Q_r) =
 // ceil(y(r)) with y(r) = y0 + r d1 for r <= rpm and yR + (r - rpm) d2 beyond (Q is linear in r on both
