@@ -709,7 +709,8 @@ static int step_impl(dog_ctx* ctx, const float* meas, const float* obs, float dt
     // run-heavy cycle: the exact filter, or a dense scene by the lagged list length
     static const uint32_t heavy_div = getenv("DOG_HEAVY_DIV") ? (uint32_t)atoi(getenv("DOG_HEAVY_DIV")) : 4u;
     const bool heavy = obs != nullptr || (ctx->lc_host && *(volatile uint32_t*)ctx->lc_host > ctx->C / heavy_div);
-    const PdlScope pdl_scope(!heavy);
+    static const bool heavy_pdl = getenv("DOG_HEAVY_PDL") != nullptr;   // diagnostics
+    const PdlScope pdl_scope(!heavy || heavy_pdl);
     ctx->dense = obs != nullptr;                            // the exact filter: every cell is active
     const bool prof = ctx->prof_steps < ctx->prof_max;
     int mark_i = 0;

@@ -26,7 +26,10 @@
 
 namespace dog {
 
-constexpr uint32_t kMoDirect = 32;   // long-list (run-heavy) cycles: cells with at most this many particles are
+#ifndef MO_DIRECT
+#define MO_DIRECT 32
+#endif
+constexpr uint32_t kMoDirect = MO_DIRECT;   // long-list (run-heavy) cycles: cells with at most this many particles are
                                      // summed directly by k_moments<true> (resample skips their run sums)
 
 // What the resampling kernels need of a run beyond its cell (written by k_pair_sort): 8 bytes per run --
