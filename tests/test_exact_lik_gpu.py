@@ -171,3 +171,24 @@ def test_exact_lik_full_size_cfgT_one_cycle():
     cg = {key: v.cpu().numpy() for key, v in g.read_cells(check=False).items() if key != "status"}
     bits(co["occ"], cg["occ"], "occ")
     close(co["mean"], cg["mean"], 1e-4, 1e-6, "mean")
+
+
+def test_no_measurement_gate_and_no_births():
+    """p_A > 0 everywhere but no measurement anywhere: dog_step_exact_lik is dog_step_exact bit for bit (the
+    gate); and a filter without birth slots (nu_b = 0) runs the likelihood cycle bit-exact vs the oracle."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    kw = dict(cell_size=cfg.cell_size, seed=cfg.seed, **cfg.filter_params())
+    a = dog.Filter(cfg.width, cfg.height, cfg.nu, cfg.nu_b, **kw)
+    b = dog.Filter(cfg.width, cfg.height, cfg.nu, cfg.nu_b, **kw)
+    sc = I.scene(cfg)
+    for k in range(4):
+        meas = sc.frame(k)
+        obs, lik, pA = sc.exact_lik(k, meas, frac=1.0)
+        obs[..., 0] = 0.0
+        a.step_exact(dev(obs), cfg.dt)
+        b.step_exact_lik(dev(obs), dev(lik), torch.full_like(dev(pA), 0.9), cfg.dt)
+    sa, sb = a.get_state(), b.get_state()
+    for key in ("x", "y", "vx", "vy"):
+        bits(sa[key], sb[key], key)
+    run(I.config("cfg1", nu_b=0), 4)

@@ -223,3 +223,18 @@ def test_associated_births_follow_the_posterior():
     z = np.array(z)
     assert z.size > 500
     assert abs(z.mean()) < 4 / math.sqrt(z.size) + 0.02 and abs(z.std() - 1) < 0.05
+
+
+def test_no_measurement_no_likelihood():
+    """The likelihood enters only where a measurement occurred (Eq. 38 applies to the measured cell): with
+    p_A > 0 everywhere but no cell holding a measurement, the cycle is orc_step_exact bit for bit."""
+    p, state, obs, lik, pA = scene(seed=17)
+    obs[:, 0] = 0.0
+    pA[:] = 0.9
+    a, b = fresh(p, state), fresh(p, state)
+    a.step_exact(obs, 0.1)
+    b.step_exact_lik(obs, lik, pA, 0.1)
+    sa, sb = a.get_state(), b.get_state()
+    for k in ("x", "y", "vx", "vy"):
+        assert np.array_equal(sa[k].view(np.uint32), sb[k].view(np.uint32)), k
+    assert np.array_equal(a.read_cells()["occ"], b.read_cells()["occ"])
