@@ -131,6 +131,16 @@ def test_grid_origin_follows_the_ego_shifts():
         assert f.origin() == (ox, oy), (dx, dy, f.origin(), (ox, oy))
 
 
+def test_sharded_context_keeps_the_origin():
+    """A sharded context (two bands on cuda:0) reports the dog_grid origin it was created with."""
+    from paper_1605_02406_b200 import dog
+    cfg = I.CONFIGS["cfg1"]
+    f = dog.Filter(cfg.width, cfg.height, cfg.nu, cfg.nu_b, cell_size=cfg.cell_size, devices=[0, 0],
+                   origin=(-7.5, 102.25))
+    assert f.origin() == (-7.5, 102.25)
+    f.close()
+
+
 def test_dense_scene_long_list_paths():
     """A cfg-5-like dense scene (i.i.d. measured cells, 4x process noise, p_B 0.1) on 96x96 cells: from
     the third cycle the active list exceeds C/4, so the library switches to the grid-wide list scan and
