@@ -617,7 +617,7 @@ static int L_list_scan(dog_ctx* ctx, const uint64_t* A_all, const StepArgs& a, c
 }
 
 static int L_pairs(dog_ctx* ctx, const uint64_t* W_all, const StepArgs& a, const FilterConst& fc, cudaStream_t st,
-                   bool long_list = false, DopPS dp = DopPS{nullptr, nullptr, nullptr, nullptr})
+                   bool long_list = false, DopPS dp = DopPS{nullptr, nullptr, nullptr, nullptr, nullptr})
 {
     CK(launch(k_pair_fill, ctx->tiles, 256, 0, st, 0, ctx->tp, ctx->list,
               ctx->dense ? (const uint32_t*)nullptr : (const uint32_t*)ctx->cell2list, ctx->plist, ctx->C));
@@ -781,7 +781,8 @@ static int alloc_doppler(dog_ctx* ctx)
     free_doppler(ctx);
     if (cudaMalloc(&ctx->d_rg, ctx->nu_cap * 8) != cudaSuccess || cudaMalloc(&ctx->d_rs, ctx->nu_cap * 8) != cudaSuccess ||
         cudaMalloc(&ctx->d_GS, (size_t)ctx->C * 8) != cudaSuccess || cudaMalloc(&ctx->d_tflag, ctx->tiles) != cudaSuccess ||
-        cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess || cudaMalloc(&ctx->d_gmax, (size_t)ctx->C * 4) != cudaSuccess) {
+        cudaMalloc(&ctx->d_gfx, ctx->nu_cap * 4) != cudaSuccess || cudaMalloc(&ctx->d_gmax, (size_t)ctx->C * 4) != cudaSuccess ||
+        cudaMemset(ctx->d_gmax, 0, (size_t)ctx->C * 4) != cudaSuccess) {
         free_doppler(ctx);
         cudaGetLastError();
         return DOG_E_NOMEM;
@@ -793,7 +794,7 @@ static int alloc_doppler(dog_ctx* ctx)
 static int L_dopp_runs(dog_ctx* ctx, const DopIn& din, const FilterConst& fc, int par, cudaStream_t st,
                        uint64_t* gsc = nullptr)
 {
-    CK(cudaMemsetAsync(ctx->d_gmax, 0, (size_t)ctx->C * 4, st));
+    // (d_gmax is zero here: zeroed at allocation, and k_pair_sort clears every cell it set)
     CK(launch(k_dopp_g, ctx->tiles, 256, 0, st, 0, ctx->tp, (const float2*)ctx->pv, din,
               ctx->d_gmax, ctx->d_gfx, (const DevScalars*)ctx->sc, fc, par));
     CK(launch(k_dopp_runs, ctx->tiles, 256, 0, st, 0, ctx->tp, din, (const uint32_t*)ctx->d_gmax, ctx->d_rg,
@@ -833,7 +834,7 @@ int dog_step_doppler(dog_ctx* ctx, const float* meas, const float* doppler, cons
     if (int r = L_list_scan(ctx, nullptr, a, fc, st)) return r;
     if (fork) CK(cudaStreamWaitEvent(st, ctx->ev_join, 0));
     // the pair sort also turns the run sums into in-cell prefixes, the cell totals GS and the tile flags
-    if (int r = L_pairs(ctx, nullptr, a, fc, st, false, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag})) return r;
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, false, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag, ctx->d_gmax})) return r;
     if (fork) {   // births beside the resampling (disjoint output slots), as in dog_step
         CK(cudaEventRecord(ctx->ev_fork, st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
@@ -898,7 +899,7 @@ int dog_step_exact_lik(dog_ctx* ctx, const float* obs, const float* lik, const f
     if (int r = L_cells(ctx, nullptr, a, fc, st, obs, xl)) return r;
     if (int r = L_list_scan(ctx, nullptr, a, fc, st, true)) return r;
     // run sums are nonzero only in the gated cells, so the ungated p_A marks the same Doppler cells
-    if (int r = L_pairs(ctx, nullptr, a, fc, st, true, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag})) return r;
+    if (int r = L_pairs(ctx, nullptr, a, fc, st, true, DopPS{p_assoc, ctx->d_rg, ctx->d_GS, ctx->d_tflag, ctx->d_gmax})) return r;
     const BirthLik bl{p_assoc, (const float4*)obs, (const float4*)lik, ctx->d_pic};
     const bool fork = ctx->side != nullptr;
     if (fork) {   // births beside the resampling (disjoint output slots), as in dog_step
@@ -1082,7 +1083,7 @@ int dog_band_resample(dog_ctx* ctx, const uint64_t* weight_all_dev, void* stream
     if (ctx->band_pA) {   // Doppler cycle (dog_band_assign_doppler): as dog_step_doppler, on the band
         const DopIn din{(const float4*)ctx->band_dop, ctx->band_pA};
         const int par = (int)(a.k & 1);
-        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, false, DopPS{ctx->band_pA, ctx->d_rg, ctx->d_GS, ctx->d_tflag}))
+        if (int r = L_pairs(ctx, weight_all_dev, a, fc, st, false, DopPS{ctx->band_pA, ctx->d_rg, ctx->d_GS, ctx->d_tflag, ctx->d_gmax}))
             return r;
         if (int r = L_resample(ctx, a, fc, st, ctx->d_GS)) return r;
         NextState ns{ctx->st, nullptr};

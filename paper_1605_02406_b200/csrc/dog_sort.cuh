@@ -643,6 +643,7 @@ struct DopPS {
     uint64_t* rg;
     uint64_t* GS;
     uint8_t* tflag;
+    uint32_t* gmax;   // the cells' likelihood maxima (k_dopp_g): cleared here for the next cycle (or nullptr)
 };
 
 constexpr int kPsSmall = 4;   // kBatch: cells with <= 4 runs handled by one lane (sorting network)
@@ -688,7 +689,10 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
     };
     auto dop_single = [&](uint32_t li, uint32_t v) {     // a one-run cell: its prefix is 0, its total the run's
         if (!dp.pA) return;
-        const uint64_t gs = dp.pA[L.c[li]] > 0.0f ? dp.rg[v] : 0ull;
+        const uint32_t c = L.c[li];
+        const bool dc = dp.pA[c] > 0.0f;
+        if (dc && dp.gmax) dp.gmax[c] = 0u;
+        const uint64_t gs = dc ? dp.rg[v] : 0ull;
         dp.rg[v] = 0ull;
         dp.GS[li] = gs;
         if (gs) dp.tflag[v >> 12] = 1;
@@ -716,6 +720,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
         RunInfo r2 = run_info(li);
         uint32_t carry = 0;
         const bool dcell = dp.pA && dp.pA[L.c[li]] > 0.0f;
+        if (dcell && dp.gmax) dp.gmax[L.c[li]] = 0u;
         uint64_t gcarry = 0;
 #pragma unroll
         for (int q = 0; q < kPsSmall; ++q) {
@@ -747,6 +752,7 @@ __global__ __launch_bounds__(256) void k_pair_sort(TilePairs tp, CellList L, uin
             return;
         }
         const bool dcell = dp.pA && dp.pA[L.c[li]] > 0.0f;
+        if (dcell && dp.gmax && gl == 0) dp.gmax[L.c[li]] = 0u;
         const bool sm = m <= (uint32_t)kPsBuf;
         uint32_t* src = sm ? s_buf[grp][0] : pl;
         uint32_t* tmp = sm ? s_buf[grp][1] : ptmp + L.ps[li];
