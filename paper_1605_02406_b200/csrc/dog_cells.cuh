@@ -488,15 +488,18 @@ __device__ __forceinline__ ulonglong2 cta_excl_scan2(ulonglong2 v, ulonglong2* s
     const uint64_t ix = warp_incl_scan(v.x, lane), iy = warp_incl_scan(v.y, lane);
     if (lane == 31) s_w[warp] = make_ulonglong2(ix, iy);
     __syncthreads();
-    uint64_t ox = 0, oy = 0, tx = 0, ty = 0;
-    for (int w = 0; w < kLsWarps; ++w) {
-        const ulonglong2 x = s_w[w];
-        if (w < warp) { ox += x.x; oy += x.y; }
-        tx += x.x; ty += x.y;
+    if (warp == 0) {   // exclusive prefix of the 32 warp totals by one warp; the total in s_w[32]
+        const ulonglong2 x = s_w[lane];
+        const uint64_t px = warp_incl_scan(x.x, lane), py = warp_incl_scan(x.y, lane);
+        __syncwarp();
+        s_w[lane] = make_ulonglong2(px - x.x, py - x.y);
+        if (lane == 31) s_w[kLsWarps] = make_ulonglong2(px, py);
     }
     __syncthreads();
-    off = make_ulonglong2(ox + ix - v.x, oy + iy - v.y);
-    return make_ulonglong2(tx, ty);
+    const ulonglong2 o = s_w[warp], t = s_w[kLsWarps];
+    __syncthreads();
+    off = make_ulonglong2(o.x + ix - v.x, o.y + iy - v.y);
+    return t;
 }
 
 // Two-value exclusive prefix over the CTA's warps (warp totals t) and over the cluster's CTAs.
@@ -543,7 +546,7 @@ __global__ __launch_bounds__(kLsThreads) void k_list_scan(StageList Ls, CellList
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     __shared__ uint32_t s_cnt0[kMaxCellBlocks + 1];
-    __shared__ ulonglong2 s_w[kLsWarps];
+    __shared__ ulonglong2 s_w[kLsWarps + 1];
     __shared__ ulonglong2 s_tot[2];
     __shared__ ulonglong2 s_base[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
