@@ -22,7 +22,10 @@
 
 namespace dog {
 
-constexpr uint32_t kItem = 256;   // members per k_resample work item
+#ifndef BIRTH_ITEM
+#define BIRTH_ITEM 256
+#endif
+constexpr uint32_t kItem = BIRTH_ITEM;   // birth slots per k_births work item
 
 struct StageList {          // k_cells staging, capacity nblk * chunk (>= C); entry li belongs to block li / chunk
     uint32_t* c;            // cell index
